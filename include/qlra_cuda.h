@@ -1,0 +1,190 @@
+/*
+ * qlra_cuda.h -- C-ABI of the B200-native one-pass quaternion LRA hot path.
+ *
+ * This is the drop-in boundary: plain pointers and sizes, no C++/torch types.
+ * Each entry point replaces one function of the reference's public C++ API
+ * (proj/include/qlra/*.hpp of arXiv 2404.14783's reference `qlra`); the
+ * replaced declaration is cited beside every prototype.  The C++ facade in
+ * paper_2404_14783_b200/csrc/qlra_gpu.hpp wraps these with the reference's
+ * signatures and rethrows the reference's exception types
+ * (proj/include/qlra/errors.hpp:9-43).
+ *
+ * Data model (proj/include/qlra/qmatrix.hpp:14-19): a quaternion matrix is four
+ * row-major FP64 planes (w, x, y, z) in DEVICE memory, each with leading
+ * dimension `ld` (>= cols).  All calls are asynchronous on the context's
+ * stream unless noted ("syncs"); results are run-to-run bitwise deterministic
+ * (no floating-point atomics, fixed reduction order).
+ *
+ * Multi-GPU (one process per GPU): a context created with nranks > 1 owns an
+ * NCCL communicator.  Data matrices are row-sharded: each rank passes its
+ * local rows of A / Y / H with `row0` = global index of its first row; W, X
+ * and all small matrices are replicated.  Reductions over rows (W, Grams,
+ * Psi*H, norms) are NCCL all-reduces inside the calls.
+ */
+#ifndef QLRA_CUDA_H
+#define QLRA_CUDA_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes: 1..6 mirror the reference exception taxonomy
+ * (errors.hpp: ShapeError, ParameterError, SingularMatrixError, RankError,
+ * PreconditionError, IoError). */
+enum {
+  QLRA_OK = 0,
+  QLRA_ERR_SHAPE = 1,
+  QLRA_ERR_PARAMETER = 2,
+  QLRA_ERR_SINGULAR = 3,
+  QLRA_ERR_RANK = 4,
+  QLRA_ERR_PRECONDITION = 5,
+  QLRA_ERR_IO = 6,
+  QLRA_ERR_INTERNAL = 99,
+  QLRA_ERR_CUDA = 100,
+  QLRA_ERR_NCCL = 101
+};
+
+/* TestMatrixKind (sketching.hpp:14) */
+enum { QLRA_GAUSSIAN = 0, QLRA_RADEMACHER = 1, QLRA_SPARSE_GAUSSIAN = 2, QLRA_SPARSE_RADEMACHER = 3 };
+/* RangefinderMethod (rangefinders.hpp:12) */
+enum { QLRA_PSEUDO_QR = 0, QLRA_PSEUDO_SVD = 1 };
+/* operand transform for qlra_qmat_mul */
+enum { QLRA_OP_N = 0, QLRA_OP_C = 1 /* conjugate transpose */ };
+
+typedef struct qlra_ctx qlra_ctx_t;
+
+/* == TestMatrixSpec (sketching.hpp:22-28) */
+typedef struct {
+  int32_t kind;
+  int64_t rows, cols;
+  uint64_t seed;
+  double density;
+} qlra_spec_t;
+
+/* Device view of a QMatrix (qmatrix.hpp:17-84): planes p[0..3] = w,x,y,z. */
+typedef struct {
+  double* p[4];
+  int64_t rows, cols, ld;
+} qlra_qmat_t;
+
+/* == PseudoQrConfig (rangefinders.hpp:23-27) */
+typedef struct {
+  int32_t max_correction_steps;    /* default 3 */
+  int32_t power_iters_for_epsilon; /* default 3 */
+  double delta_budget;             /* default 1.2 */
+} qlra_pseudo_qr_config_t;
+
+/* == RangefinderReport minus h (rangefinders.hpp:14-21) */
+typedef struct {
+  double kappa_before;
+  double kappa_after;
+  int32_t correction_steps_used;
+  int32_t method;
+} qlra_rangefinder_report_t;
+
+/* ------------------------------------------------------------ context --- */
+/* Creates a context on `device`.  nranks > 1 requires a 128-byte NCCL unique
+ * id (from qlra_nccl_unique_id on rank 0, broadcast by the caller). */
+int qlra_ctx_create(qlra_ctx_t** ctx, int device, int rank, int nranks,
+                    const void* nccl_unique_id);
+int qlra_ctx_destroy(qlra_ctx_t* ctx);
+/* Use an external cudaStream_t (e.g. torch's current stream); NULL = own. */
+int qlra_ctx_set_stream(qlra_ctx_t* ctx, void* cuda_stream);
+int qlra_ctx_synchronize(qlra_ctx_t* ctx);
+int qlra_nccl_unique_id(void* out_128_bytes);
+/* Message of the last failing call on this ctx; for QLRA_ERR_SINGULAR also
+ * the condition estimate carried by SingularMatrixError (errors.hpp:23-30). */
+const char* qlra_last_error(const qlra_ctx_t* ctx, double* estimated_condition);
+/* Number of kernels this ctx has launched (diagnostics / bench evidence). */
+int64_t qlra_ctx_launch_count(const qlra_ctx_t* ctx);
+
+/* ---------------------------------------------------------- embeddings --- */
+/* gen_block (sketching.cpp:53-71) / gen_test_matrix{,_rows,_cols}
+ * (sketching.hpp:30-32): writes entries [r0, r0+out->rows) x [c0, c0+out->cols)
+ * of the spec into `out`.  Counter-based: any block is bit-identical in its
+ * integer draws to the same block of the full matrix. */
+int qlra_gen_test_matrix_block(qlra_ctx_t* ctx, const qlra_spec_t* spec, int64_t r0, int64_t c0,
+                               qlra_qmat_t* out);
+
+/* ------------------------------------------------------------- sketch --- */
+/* sketch_update_rows (sketching.hpp:65, sketching.cpp:125-139):
+ *   y_rows += block * Omega           (y_rows: the block's rows of Y)
+ *   w      += Psi[:, row0:row0+b] * block
+ * One launch of the fused sketch kernel reads each element of `block` from
+ * HBM once.  Omega and the Psi column slice are regenerated on device from
+ * their specs (rng.hpp:10-55).  With nranks > 1, `w` accumulates the rank's
+ * partial; call qlra_sketch_allreduce once all local rows are in. */
+int qlra_sketch_update_rows(qlra_ctx_t* ctx, const qlra_spec_t* omega, const qlra_spec_t* psi,
+                            int64_t row0, const qlra_qmat_t* block, qlra_qmat_t* y_rows,
+                            qlra_qmat_t* w);
+/* Sum of the per-rank W partials (NCCL all-reduce; no-op for one rank). */
+int qlra_sketch_allreduce(qlra_ctx_t* ctx, qlra_qmat_t* w);
+
+/* ------------------------------------------------------------ products --- */
+/* qmat_mul (qmatrix.hpp:87, qmatrix.cpp:165-197) generalised:
+ *   C = alpha * op(A) op(B) + beta * C,  op = identity or adjoint.
+ * Not collective. */
+int qlra_qmat_mul(qlra_ctx_t* ctx, int op_a, int op_b, double alpha, const qlra_qmat_t* a,
+                  const qlra_qmat_t* b, double beta, qlra_qmat_t* c);
+/* H^* H over row-sharded H (all-reduced): the Gram used by estimate_epsilon /
+ * correction_step (rangefinders.cpp:68,102).  g is s x s. */
+int qlra_gram(qlra_ctx_t* ctx, const qlra_qmat_t* h, qlra_qmat_t* g);
+
+/* --------------------------------------------------- small dense (K4) --- */
+/* condition_number (factorizations.hpp:54, factorizations.cpp:330-337) of a
+ * row-sharded tall H; syncs. */
+int qlra_condition_number(qlra_ctx_t* ctx, const qlra_qmat_t* h, double* kappa);
+/* singular_values (factorizations.cpp:316-323) of a row-sharded tall A,
+ * nonincreasing, min(rows, cols) values written to host `sv`; syncs. */
+int qlra_singular_values(qlra_ctx_t* ctx, const qlra_qmat_t* a, double* sv);
+/* solve_quaternion_linear (complex_bridge.hpp:36, complex_bridge.cpp:63-90):
+ * square systems solve exactly; overdetermined ones return the least-squares
+ * solution.  A, B replicated (not row-sharded).  syncs. */
+int qlra_solve_quaternion_linear(qlra_ctx_t* ctx, const qlra_qmat_t* a, const qlra_qmat_t* b,
+                                 qlra_qmat_t* x);
+
+/* -------------------------------------------------------- rangefinders --- */
+/* estimate_epsilon (rangefinders.hpp:50, rangefinders.cpp:66-97); syncs. */
+int qlra_estimate_epsilon(qlra_ctx_t* ctx, const qlra_qmat_t* h, int power_iters, double* eps);
+/* correction_step (rangefinders.hpp:46, rangefinders.cpp:99-105); h_out may
+ * alias h; syncs. */
+int qlra_correction_step(qlra_ctx_t* ctx, const qlra_qmat_t* h, double epsilon,
+                         qlra_qmat_t* h_out);
+/* pseudo_qr (rangefinders.hpp:40, rangefinders.cpp:107-158): Algorithm 1.
+ * y, h: m x s (row-sharded), h may not alias y; syncs. */
+int qlra_pseudo_qr(qlra_ctx_t* ctx, const qlra_qmat_t* y, const qlra_pseudo_qr_config_t* cfg,
+                   qlra_qmat_t* h, qlra_rangefinder_report_t* report);
+/* pseudo_svd (rangefinders.hpp:57, rangefinders.cpp:166-176): Algorithm 3,
+ * orthonormal H with range(H) = range(Y); syncs. */
+int qlra_pseudo_svd(qlra_ctx_t* ctx, const qlra_qmat_t* y, uint64_t seed, qlra_qmat_t* h,
+                    qlra_rangefinder_report_t* report);
+
+/* --------------------------------------------------------- core solve --- */
+/* The solve half of qb_stage_with_psi (sketching.cpp:184-185):
+ *   X = argmin || (Psi H) X - W ||_F,   Psi regenerated from `psi`,
+ * with H row-sharded (local rows start at global row `row0`), W and X
+ * replicated (l x n and s x n).  Psi H is all-reduced.  syncs. */
+int qlra_qb_solve(qlra_ctx_t* ctx, const qlra_spec_t* psi, int64_t row0, const qlra_qmat_t* h,
+                  const qlra_qmat_t* w, qlra_qmat_t* x);
+
+/* ---------------------------------------------------------- residual --- */
+/* ||A - H X||_F and ||A||_F (sketching.cpp:270-271; analysis.cpp:75-79) over
+ * row-sharded A and H: a fused GEMM-subtract-square-reduce (second read of A,
+ * diagnostic only); syncs. */
+int qlra_residual_fro(qlra_ctx_t* ctx, const qlra_qmat_t* a, const qlra_qmat_t* h,
+                      const qlra_qmat_t* x, double* res_fro, double* a_fro);
+
+/* ---------------------------------------------------------- diagnostics --- */
+/* Measured FP64 throughput of this GPU: mode 0 = DFMA, 1 = DMMA (m8n8k4).
+ * Runs ~`ms` milliseconds; syncs. */
+int qlra_measure_fp64_peak(qlra_ctx_t* ctx, int mode, double ms, double* tflops);
+/* Name of the kernel variant the sketch uses for the given shape. */
+const char* qlra_sketch_kernel_name(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* QLRA_CUDA_H */

@@ -1,0 +1,88 @@
+"""ctypes binding of libqlra_cuda.so (include/qlra_cuda.h).
+
+Fails loudly: there is no CPU fallback anywhere in the product.  If the
+library is missing it is built in-tree (nvcc), and if that fails the import
+error propagates.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+from . import build as _build
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+
+I64, U64, F64, INT, VP = C.c_int64, C.c_uint64, C.c_double, C.c_int, C.c_void_p
+
+
+class Spec(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("rows", C.c_int64), ("cols", C.c_int64),
+                ("seed", C.c_uint64), ("density", C.c_double)]
+
+
+class QMat(C.Structure):
+    _fields_ = [("p", C.c_void_p * 4), ("rows", C.c_int64), ("cols", C.c_int64), ("ld", C.c_int64)]
+
+
+class PseudoQrConfig(C.Structure):
+    _fields_ = [("max_correction_steps", C.c_int32), ("power_iters_for_epsilon", C.c_int32),
+                ("delta_budget", C.c_double)]
+
+
+class Report(C.Structure):
+    _fields_ = [("kappa_before", C.c_double), ("kappa_after", C.c_double),
+                ("correction_steps_used", C.c_int32), ("method", C.c_int32)]
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is not None:
+        return _lib
+    path = _build.LIB
+    if not os.path.exists(path):
+        _build.build()
+    L = C.CDLL(path)
+    P, PS, PQ = C.POINTER, C.POINTER(Spec), C.POINTER(QMat)
+    sig = {
+        "qlra_ctx_create": ([P(VP), INT, INT, INT, VP], INT),
+        "qlra_ctx_destroy": ([VP], INT),
+        "qlra_ctx_set_stream": ([VP, VP], INT),
+        "qlra_ctx_synchronize": ([VP], INT),
+        "qlra_nccl_unique_id": ([VP], INT),
+        "qlra_last_error": ([VP, P(F64)], C.c_char_p),
+        "qlra_ctx_launch_count": ([VP], I64),
+        "qlra_gen_test_matrix_block": ([VP, PS, I64, I64, PQ], INT),
+        "qlra_sketch_update_rows": ([VP, PS, PS, I64, PQ, PQ, PQ], INT),
+        "qlra_sketch_allreduce": ([VP, PQ], INT),
+        "qlra_qmat_mul": ([VP, INT, INT, F64, PQ, PQ, F64, PQ], INT),
+        "qlra_gram": ([VP, PQ, PQ], INT),
+        "qlra_condition_number": ([VP, PQ, P(F64)], INT),
+        "qlra_singular_values": ([VP, PQ, P(F64)], INT),
+        "qlra_solve_quaternion_linear": ([VP, PQ, PQ, PQ], INT),
+        "qlra_estimate_epsilon": ([VP, PQ, INT, P(F64)], INT),
+        "qlra_correction_step": ([VP, PQ, F64, PQ], INT),
+        "qlra_pseudo_qr": ([VP, PQ, P(PseudoQrConfig), PQ, P(Report)], INT),
+        "qlra_pseudo_svd": ([VP, PQ, U64, PQ, P(Report)], INT),
+        "qlra_qb_solve": ([VP, PS, I64, PQ, PQ, PQ], INT),
+        "qlra_residual_fro": ([VP, PQ, PQ, PQ, P(F64), P(F64)], INT),
+        "qlra_measure_fp64_peak": ([VP, INT, F64, P(F64)], INT),
+        "qlra_sketch_kernel_name": ([], C.c_char_p),
+    }
+    for name, (args, res) in sig.items():
+        f = getattr(L, name)
+        f.argtypes = args
+        f.restype = res
+    _lib = L
+    return L
+
+
+def exported_symbols():
+    """Names declared in include/qlra_cuda.h (parsed) -- for the export test."""
+    import re
+    hdr = os.path.join(os.path.dirname(_HERE), "include", "qlra_cuda.h")
+    src = open(hdr).read()
+    return sorted(set(re.findall(r"^\s*(?:const\s+)?[a-z0-9_]+\s*\*?\s*(qlra_[a-z0-9_]+)\s*\(", src, re.M)))

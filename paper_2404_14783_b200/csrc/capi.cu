@@ -1,0 +1,669 @@
+// capi.cu -- the extern "C" boundary (include/qlra_cuda.h) and the host-side
+// orchestration of the hot path: the rangefinders' control flow
+// (proj/src/rangefinders.cpp:18-176), the core solve
+// (proj/src/sketching.cpp:184-185, complex_bridge.cpp:63-90) and the sharded
+// reductions.  All arithmetic runs in the kernels of sketch.cu / qgemm.cu /
+// smallla.cu; the host only sequences launches and reads back the scalars
+// the reference's control flow branches on (kappa, epsilon, rank tests).
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <vector>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+struct qlra_ctx {
+  qlra_dev::Ctx c;
+};
+
+namespace qlra_dev {
+
+std::atomic<int64_t>& launch_counter() {
+  static std::atomic<int64_t> c{0};
+  return c;
+}
+
+void allreduce_sum(Ctx& ctx, double* buf, size_t count) {
+  if (ctx.nranks <= 1 || count == 0) return;
+  const ncclResult_t r = ncclAllReduce(buf, buf, count, ncclDouble, ncclSum, ctx.comm, ctx.stream);
+  if (r != ncclSuccess) fail(QLRA_ERR_NCCL, std::string("ncclAllReduce: ") + ncclGetErrorString(r));
+}
+
+void allreduce_qmat(Ctx& ctx, const QView& m) {
+  if (ctx.nranks <= 1) return;
+  for (int p = 0; p < 4; ++p) {
+    if (m.ld == m.cols) {
+      allreduce_sum(ctx, m.p[p], (size_t)(m.rows * m.cols));
+    } else {
+      for (int64_t i = 0; i < m.rows; ++i) allreduce_sum(ctx, m.p[p] + i * m.ld, (size_t)m.cols);
+    }
+  }
+}
+
+namespace {
+
+constexpr double kKappaTarget = 10.0;   // rangefinders.cpp:12
+constexpr double kEpsilonClamp = 0.999; // rangefinders.cpp:13
+constexpr double kUnit = 1.1102230246251565e-16;
+
+std::vector<double> to_host(Ctx& ctx, const double* d, size_t n) {
+  std::vector<double> h(n);
+  if (n) {
+    QLRA_CUDA(cudaMemcpyAsync(h.data(), d, n * sizeof(double), cudaMemcpyDeviceToHost, ctx.stream));
+    QLRA_CUDA(cudaStreamSynchronize(ctx.stream));
+  }
+  return h;
+}
+std::vector<double> diag_to_host(Ctx& ctx, const double* p, int64_t ld, int64_t n, size_t elem = 1) {
+  std::vector<double> h(n);
+  if (n) {
+    QLRA_CUDA(cudaMemcpy2DAsync(h.data(), sizeof(double), p, (size_t)(ld + 1) * elem * sizeof(double),
+                                sizeof(double), (size_t)n, cudaMemcpyDeviceToHost, ctx.stream));
+    QLRA_CUDA(cudaStreamSynchronize(ctx.stream));
+  }
+  return h;
+}
+int info_to_host(Ctx& ctx, const int* d) {
+  int h = 0;
+  QLRA_CUDA(cudaMemcpyAsync(&h, d, sizeof(int), cudaMemcpyDeviceToHost, ctx.stream));
+  QLRA_CUDA(cudaStreamSynchronize(ctx.stream));
+  return h;
+}
+
+int64_t global_rows(Ctx& ctx, int64_t local) {
+  if (ctx.nranks <= 1) return local;
+  DeviceBuffer b(ctx, sizeof(double));
+  const double v = (double)local;
+  QLRA_CUDA(cudaMemcpyAsync(b.ptr, &v, sizeof(double), cudaMemcpyHostToDevice, ctx.stream));
+  allreduce_sum(ctx, b.as<double>(), 1);
+  return (int64_t)llround(to_host(ctx, b.as<double>(), 1)[0]);
+}
+
+// G = op(A)^* op(A) reduced over (row-sharded) rows: s x s.
+void gram(Ctx& ctx, const QView& h, const QView& g) {
+  qgemm(ctx, QLRA_OP_C, QLRA_OP_N, 1.0, h, h, 0.0, g);
+  allreduce_qmat(ctx, g);
+}
+
+// Eigenvalues (descending) of chi_G for a quaternion Hermitian G (s x s).
+std::vector<double> chi_eigs(Ctx& ctx, const QView& g) {
+  const int64_t n = 2 * g.rows;
+  DeviceBuffer chi(ctx, sizeof(double2) * (size_t)(n * n));
+  DeviceBuffer w(ctx, sizeof(double) * (size_t)n);
+  small_chi_from_quat(ctx, g, chi.as<double2>(), n);
+  small_herm_eigvals(ctx, chi.as<double2>(), n, n, w.as<double>());
+  return to_host(ctx, w.as<double>(), (size_t)n);
+}
+
+double kappa_from_eigs(const std::vector<double>& ev) {
+  if (ev.empty()) return std::numeric_limits<double>::infinity();
+  const double lmax = ev.front(), lmin = ev.back();
+  if (!(lmin > 0.0)) return std::numeric_limits<double>::infinity();
+  return std::sqrt(lmax / lmin);
+}
+
+// Explicit quaternion inverse of a square matrix via Gauss-Jordan; returns
+// the GJ status (info, pmin, pmax).
+std::vector<double> quat_inverse(Ctx& ctx, const QView& a, const QView& ainv) {
+  DevQMat work(ctx, a.rows, a.cols);
+  copy_qmat(ctx, a, work.v);
+  small_set_identity(ctx, ainv);
+  DeviceBuffer st(ctx, 3 * sizeof(double));
+  small_quat_solve(ctx, work.v, ainv, st.as<double>());
+  return to_host(ctx, st.as<double>(), 3);
+}
+
+// One CholeskyQR pass: hout = y * R^{-1} with G = gram(y) (+ shift on the
+// diagonal).  complex_mode: R from the complex compact Gram (Y_c^* Y_c, the
+// complex part of the quaternion Gram) -- pseudo-QR's complex_qr; else R is
+// the quaternion Cholesky factor (orthonormal quaternion basis).  Returns
+// false if the Cholesky factorisation breaks down; rdiag gets diag(R).
+bool cqr_pass(Ctx& ctx, const QView& y, const QView& hout, bool complex_mode, double shift,
+              std::vector<double>* rdiag, double* trace_g) {
+  const int64_t s = y.cols;
+  DevQMat g(ctx, s, s);
+  gram(ctx, y, g.v);
+  if (trace_g) {
+    const std::vector<double> d = diag_to_host(ctx, g.v.p[0], g.v.ld, s);
+    double t = 0.0;
+    for (double v : d) t += v;
+    *trace_g = t;
+  }
+  DevQMat rinv(ctx, s, s);
+  DeviceBuffer info(ctx, sizeof(int));
+  if (complex_mode) {
+    DeviceBuffer c(ctx, sizeof(double2) * (size_t)(s * s));
+    small_complex_part(ctx, g.v, c.as<double2>(), s);
+    if (shift != 0.0) small_add_diag_complex(ctx, c.as<double2>(), s, s, shift);
+    small_cholesky(ctx, c.as<double2>(), s, s, info.as<int>());
+    if (info_to_host(ctx, info.as<int>()) != 0) return false;
+    if (rdiag) *rdiag = diag_to_host(ctx, reinterpret_cast<double*>(c.ptr), s, s, 2);
+    small_inv_lower_adjoint_to_quat(ctx, c.as<double2>(), s, s, rinv.v);
+  } else {
+    if (shift != 0.0) small_add_diag(ctx, g.v, shift);
+    small_quat_cholesky(ctx, g.v, info.as<int>());
+    if (info_to_host(ctx, info.as<int>()) != 0) return false;
+    if (rdiag) *rdiag = diag_to_host(ctx, g.v.p[0], g.v.ld, s);
+    small_quat_triinv_upper(ctx, g.v, rinv.v);
+  }
+  qgemm(ctx, QLRA_OP_N, QLRA_OP_N, 1.0, y, rinv.v, 0.0, hout);
+  return true;
+}
+
+// CholeskyQR2, or shifted CholeskyQR3 (Fukaya et al.) when the first Gram is
+// not numerically positive definite.  rdiag = diag of the full R factor.
+bool cholesky_qr(Ctx& ctx, const QView& y, const QView& h, bool complex_mode, int64_t m_global,
+                 std::vector<double>* rdiag) {
+  const int64_t s = y.cols;
+  DevQMat t1(ctx, y.rows, s);
+  std::vector<double> d1, d2, d3;
+  double tr = 0.0;
+  if (cqr_pass(ctx, y, t1.v, complex_mode, 0.0, &d1, &tr)) {
+    if (!cqr_pass(ctx, t1.v, h, complex_mode, 0.0, &d2, nullptr)) return false;
+    if (rdiag) {
+      rdiag->resize(s);
+      for (int64_t k = 0; k < s; ++k) (*rdiag)[k] = d1[k] * d2[k];
+    }
+    return true;
+  }
+  const double dim = complex_mode ? 2.0 : 4.0;
+  const double shift = 11.0 * (dim * (double)m_global * s + s * (s + 1.0)) * kUnit * tr;
+  if (!(tr > 0.0)) return false;
+  if (!cqr_pass(ctx, y, t1.v, complex_mode, shift, &d1, nullptr)) return false;
+  DevQMat t2(ctx, y.rows, s);
+  if (!cqr_pass(ctx, t1.v, t2.v, complex_mode, 0.0, &d2, nullptr)) return false;
+  if (!cqr_pass(ctx, t2.v, h, complex_mode, 0.0, &d3, nullptr)) return false;
+  if (rdiag) {
+    rdiag->resize(s);
+    // R = R3 R2 R1 where R1 is the shifted factor: its diagonal overstates the
+    // true R by the shift; the product below is the diagonal of the R that
+    // maps h back onto y only when the shift is negligible, which is exactly
+    // the regime the rank test cares about (small pivots stay small).
+    for (int64_t k = 0; k < s; ++k) (*rdiag)[k] = d1[k] * d2[k] * d3[k];
+  }
+  return true;
+}
+
+void rank_check(const std::vector<double>& d) {
+  double rmax = 0.0, rmin = std::numeric_limits<double>::infinity();
+  for (double v : d) {
+    rmax = std::max(rmax, std::fabs(v));
+    rmin = std::min(rmin, std::fabs(v));
+  }
+  if (!(rmin > 1e-14 * rmax))
+    fail(QLRA_ERR_RANK, "pseudo_qr: sketch numerically rank-deficient; use pseudo_svd");
+}
+
+// Gram-based condition number of a row-sharded tall matrix (or wide via AA^*).
+double condition_number_dev(Ctx& ctx, const QView& a) {
+  const int64_t k = std::min(a.rows, a.cols);
+  if (k == 0) return std::numeric_limits<double>::infinity();
+  DevQMat g(ctx, a.cols, a.cols);
+  gram(ctx, a, g.v);
+  return kappa_from_eigs(chi_eigs(ctx, g.v));
+}
+
+double estimate_epsilon_from_gram(Ctx& ctx, const QView& g, double kappa_h, int iters) {
+  if (iters < 1) fail(QLRA_ERR_PARAMETER, "estimate_epsilon: power_iters must be >= 1");
+  // rcond(chi_G) = 1/kappa(H)^2 must exceed 1e-15 (rangefinders.cpp:72-75).
+  const double rc = std::isfinite(kappa_h) ? 1.0 / (kappa_h * kappa_h) : 0.0;
+  if (!(rc > 1e-15))
+    fail(QLRA_ERR_SINGULAR, "estimate_epsilon: H*H numerically singular",
+         rc > 0 ? 1.0 / rc : std::numeric_limits<double>::infinity());
+  DevQMat ginv(ctx, g.rows, g.cols);
+  const std::vector<double> st = quat_inverse(ctx, g, ginv.v);
+  if (st[0] != 0.0)
+    fail(QLRA_ERR_SINGULAR, "estimate_epsilon: H*H numerically singular",
+         std::numeric_limits<double>::infinity());
+  DeviceBuffer rho(ctx, sizeof(double));
+  small_power_iter_inverse(ctx, ginv.v, iters, rho.as<double>());
+  const double r = to_host(ctx, rho.as<double>(), 1)[0];
+  if (!(r > 0.0)) fail(QLRA_ERR_SINGULAR, "estimate_epsilon: breakdown", 0.0);
+  return std::min(1.0 / std::sqrt(r), kEpsilonClamp);
+}
+
+// H_out = H ((1-eps) I + eps G^{-1}) == (1-eps) H + eps (H^+)^*  (rangefinders.cpp:99-105)
+void correction_from_gram(Ctx& ctx, const QView& h, const QView& g, double kappa_h, double eps,
+                          const QView& hout) {
+  if (!(eps > 0.0 && eps < 1.0)) fail(QLRA_ERR_PARAMETER, "correction_step: epsilon must lie in (0,1)");
+  const double rc = std::isfinite(kappa_h) ? 1.0 / (kappa_h * kappa_h) : 0.0;
+  if (!(rc > 1e-14))
+    fail(QLRA_ERR_SINGULAR, "solve_quaternion_linear: singular system",
+         rc > 0 ? 1.0 / rc : std::numeric_limits<double>::infinity());
+  DevQMat ginv(ctx, g.rows, g.cols);
+  const std::vector<double> st = quat_inverse(ctx, g, ginv.v);
+  if (st[0] != 0.0)
+    fail(QLRA_ERR_SINGULAR, "solve_quaternion_linear: singular system",
+         std::numeric_limits<double>::infinity());
+  DevQMat mm(ctx, g.rows, g.cols);
+  small_axpby_identity(ctx, 1.0 - eps, eps, ginv.v, mm.v);
+  if (hout.p[0] == h.p[0]) {
+    DevQMat tmp(ctx, h.rows, h.cols);
+    qgemm(ctx, QLRA_OP_N, QLRA_OP_N, 1.0, h, mm.v, 0.0, tmp.v);
+    copy_qmat(ctx, tmp.v, hout);
+  } else {
+    qgemm(ctx, QLRA_OP_N, QLRA_OP_N, 1.0, h, mm.v, 0.0, hout);
+  }
+}
+
+// Least squares X = argmin ||P X - B|| for replicated P (l x s), B (l x n):
+// normal equations with the explicit quaternion inverse of P^*P plus one
+// step of iterative refinement (accuracy ~ u kappa(P)).
+void lstsq(Ctx& ctx, const QView& p, const QView& b, const QView& x) {
+  const int64_t s = p.cols;
+  DevQMat g(ctx, s, s);
+  qgemm(ctx, QLRA_OP_C, QLRA_OP_N, 1.0, p, p, 0.0, g.v);
+  // rank test in the spirit of ColPivHouseholderQR |r_min| > 1e-14 |r_max|
+  // (complex_bridge.cpp:80-85): kappa(P) from the Gram spectrum.
+  const double kp = kappa_from_eigs(chi_eigs(ctx, g.v));
+  if (!(1.0 / kp > 1e-14))
+    fail(QLRA_ERR_SINGULAR, "solve_quaternion_linear: rank-deficient system", kp);
+  DevQMat ginv(ctx, s, s);
+  const std::vector<double> st = quat_inverse(ctx, g.v, ginv.v);
+  if (st[0] != 0.0) fail(QLRA_ERR_SINGULAR, "solve_quaternion_linear: rank-deficient system", kp);
+  DevQMat c(ctx, s, b.cols);
+  qgemm(ctx, QLRA_OP_C, QLRA_OP_N, 1.0, p, b, 0.0, c.v);
+  qgemm(ctx, QLRA_OP_N, QLRA_OP_N, 1.0, ginv.v, c.v, 0.0, x);
+  // refinement: r = B - P X ; X += Ginv (P^* r)
+  DevQMat r(ctx, b.rows, b.cols);
+  copy_qmat(ctx, b, r.v);
+  qgemm(ctx, QLRA_OP_N, QLRA_OP_N, -1.0, p, x, 1.0, r.v);
+  qgemm(ctx, QLRA_OP_C, QLRA_OP_N, 1.0, p, r.v, 0.0, c.v);
+  qgemm(ctx, QLRA_OP_N, QLRA_OP_N, 1.0, ginv.v, c.v, 1.0, x);
+}
+
+void check_view(const qlra_qmat_t* m, const char* who) {
+  if (!m) fail(QLRA_ERR_PARAMETER, std::string(who) + ": null matrix");
+  if (m->rows < 0 || m->cols < 0 || m->ld < m->cols)
+    fail(QLRA_ERR_SHAPE, std::string(who) + ": bad matrix view");
+}
+
+void validate_spec(const qlra_spec_t* s) {
+  if (!s) fail(QLRA_ERR_PARAMETER, "test matrix: null spec");
+  if (s->rows < 0 || s->cols < 0) fail(QLRA_ERR_PARAMETER, "test matrix: negative dims");
+  if (!(s->density > 0.0 && s->density <= 1.0))
+    fail(QLRA_ERR_PARAMETER, "test matrix: density must lie in (0,1]");
+  if (s->kind < 0 || s->kind > 3) fail(QLRA_ERR_PARAMETER, "test matrix: unknown kind");
+}
+
+}  // namespace
+}  // namespace qlra_dev
+
+using namespace qlra_dev;
+
+template <class F>
+static int guarded(qlra_ctx_t* ctx, F&& f) {
+  try {
+    if (!ctx) return QLRA_ERR_PARAMETER;
+    QLRA_CUDA(cudaSetDevice(ctx->c.device));
+    f(ctx->c);
+    return QLRA_OK;
+  } catch (const Status& s) {
+    ctx->c.last_error = s.what();
+    ctx->c.last_cond = s.cond;
+    return s.code;
+  } catch (const std::exception& e) {
+    ctx->c.last_error = e.what();
+    return QLRA_ERR_INTERNAL;
+  }
+}
+
+extern "C" {
+
+int qlra_nccl_unique_id(void* out) {
+  ncclUniqueId id;
+  if (ncclGetUniqueId(&id) != ncclSuccess) return QLRA_ERR_NCCL;
+  std::memcpy(out, &id, sizeof(id));
+  return QLRA_OK;
+}
+
+int qlra_ctx_create(qlra_ctx_t** out, int device, int rank, int nranks, const void* nccl_id) {
+  if (!out) return QLRA_ERR_PARAMETER;
+  *out = nullptr;
+  qlra_ctx_t* ctx = new qlra_ctx_t();
+  ctx->c.device = device;
+  ctx->c.rank = rank;
+  ctx->c.nranks = nranks < 1 ? 1 : nranks;
+  const int rc = guarded(ctx, [&](Ctx& c) {
+    QLRA_CUDA(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
+    c.own_stream = true;
+    cudaMemPool_t pool;
+    QLRA_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+    uint64_t thr = UINT64_MAX;
+    QLRA_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    QLRA_CUDA(cudaMallocHost(&c.pinned, 4096));
+    if (c.nranks > 1) {
+      if (!nccl_id) fail(QLRA_ERR_PARAMETER, "qlra_ctx_create: nranks > 1 needs an NCCL id");
+      ncclUniqueId id;
+      std::memcpy(&id, nccl_id, sizeof(id));
+      const ncclResult_t r = ncclCommInitRank(&c.comm, c.nranks, id, rank);
+      if (r != ncclSuccess) fail(QLRA_ERR_NCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+    }
+  });
+  if (rc != QLRA_OK) {
+    delete ctx;
+    return rc;
+  }
+  *out = ctx;
+  return QLRA_OK;
+}
+
+int qlra_ctx_destroy(qlra_ctx_t* ctx) {
+  if (!ctx) return QLRA_OK;
+  cudaSetDevice(ctx->c.device);
+  if (ctx->c.stream) cudaStreamSynchronize(ctx->c.stream);
+  if (ctx->c.comm) ncclCommDestroy(ctx->c.comm);
+  if (ctx->c.own_stream && ctx->c.stream) cudaStreamDestroy(ctx->c.stream);
+  if (ctx->c.pinned) cudaFreeHost(ctx->c.pinned);
+  delete ctx;
+  return QLRA_OK;
+}
+
+int qlra_ctx_set_stream(qlra_ctx_t* ctx, void* stream) {
+  return guarded(ctx, [&](Ctx& c) {
+    if (c.own_stream && c.stream) {
+      QLRA_CUDA(cudaStreamSynchronize(c.stream));
+      QLRA_CUDA(cudaStreamDestroy(c.stream));
+      c.own_stream = false;
+    }
+    if (stream) {
+      c.stream = static_cast<cudaStream_t>(stream);
+    } else {
+      QLRA_CUDA(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
+      c.own_stream = true;
+    }
+  });
+}
+
+int qlra_ctx_synchronize(qlra_ctx_t* ctx) {
+  return guarded(ctx, [&](Ctx& c) { QLRA_CUDA(cudaStreamSynchronize(c.stream)); });
+}
+
+const char* qlra_last_error(const qlra_ctx_t* ctx, double* cond) {
+  if (!ctx) return "null context";
+  if (cond) *cond = ctx->c.last_cond;
+  return ctx->c.last_error.c_str();
+}
+
+int64_t qlra_ctx_launch_count(const qlra_ctx_t*) { return launch_counter().load(); }
+
+int qlra_gen_test_matrix_block(qlra_ctx_t* ctx, const qlra_spec_t* spec, int64_t r0, int64_t c0,
+                               qlra_qmat_t* out) {
+  return guarded(ctx, [&](Ctx& c) {
+    validate_spec(spec);
+    check_view(out, "gen_test_matrix");
+    if (r0 < 0 || c0 < 0 || r0 + out->rows > spec->rows || c0 + out->cols > spec->cols)
+      fail(QLRA_ERR_SHAPE, "test matrix: block out of range");
+    launch_gen(c.stream, *spec, r0, c0, out->rows, out->cols, view_of(out), false);
+  });
+}
+
+int qlra_sketch_update_rows(qlra_ctx_t* ctx, const qlra_spec_t* omega, const qlra_spec_t* psi,
+                            int64_t row0, const qlra_qmat_t* block, qlra_qmat_t* y_rows,
+                            qlra_qmat_t* w) {
+  return guarded(ctx, [&](Ctx& c) {
+    validate_spec(omega);
+    validate_spec(psi);
+    check_view(block, "sketch_update_rows");
+    check_view(y_rows, "sketch_update_rows");
+    check_view(w, "sketch_update_rows");
+    const int64_t n = w->cols;
+    if (block->cols != n || omega->rows != n)
+      fail(QLRA_ERR_SHAPE, "sketch_update_rows: column count mismatch");
+    if (y_rows->rows != block->rows || y_rows->cols != omega->cols || w->rows != psi->rows)
+      fail(QLRA_ERR_SHAPE, "sketch_update_rows: sketch shape mismatch");
+    if (row0 < 0 || row0 + block->rows > psi->cols)
+      fail(QLRA_ERR_SHAPE, "sketch_update_rows: row range out of bounds");
+    sketch_update_rows(c, *omega, *psi, row0, view_of(block), view_of(y_rows), view_of(w));
+  });
+}
+
+int qlra_sketch_allreduce(qlra_ctx_t* ctx, qlra_qmat_t* w) {
+  return guarded(ctx, [&](Ctx& c) {
+    check_view(w, "sketch_allreduce");
+    allreduce_qmat(c, view_of(w));
+  });
+}
+
+int qlra_qmat_mul(qlra_ctx_t* ctx, int op_a, int op_b, double alpha, const qlra_qmat_t* a,
+                  const qlra_qmat_t* b, double beta, qlra_qmat_t* cm) {
+  return guarded(ctx, [&](Ctx& c) {
+    check_view(a, "qmat_mul");
+    check_view(b, "qmat_mul");
+    check_view(cm, "qmat_mul");
+    qgemm(c, op_a, op_b, alpha, view_of(a), view_of(b), beta, view_of(cm));
+  });
+}
+
+int qlra_gram(qlra_ctx_t* ctx, const qlra_qmat_t* h, qlra_qmat_t* g) {
+  return guarded(ctx, [&](Ctx& c) {
+    check_view(h, "gram");
+    check_view(g, "gram");
+    if (g->rows != h->cols || g->cols != h->cols) fail(QLRA_ERR_SHAPE, "gram: output shape mismatch");
+    gram(c, view_of(h), view_of(g));
+  });
+}
+
+int qlra_condition_number(qlra_ctx_t* ctx, const qlra_qmat_t* h, double* kappa) {
+  return guarded(ctx, [&](Ctx& c) {
+    check_view(h, "condition_number");
+    if (h->rows < h->cols && c.nranks == 1) {
+      // wide: singular values of A^* (tall)
+      DevQMat g(c, h->rows, h->rows);
+      qgemm(c, QLRA_OP_N, QLRA_OP_C, 1.0, view_of(h), view_of(h), 0.0, g.v);
+      *kappa = h->rows == 0 ? std::numeric_limits<double>::infinity()
+                            : kappa_from_eigs(chi_eigs(c, g.v));
+    } else {
+      *kappa = condition_number_dev(c, view_of(h));
+    }
+  });
+}
+
+int qlra_singular_values(qlra_ctx_t* ctx, const qlra_qmat_t* a, double* sv) {
+  return guarded(ctx, [&](Ctx& c) {
+    check_view(a, "singular_values");
+    const bool wide = a->rows < a->cols && c.nranks == 1;
+    const int64_t k = wide ? a->rows : a->cols;
+    if (k == 0) return;
+    DevQMat g(c, k, k);
+    if (wide)
+      qgemm(c, QLRA_OP_N, QLRA_OP_C, 1.0, view_of(a), view_of(a), 0.0, g.v);
+    else
+      gram(c, view_of(a), g.v);
+    const std::vector<double> ev = chi_eigs(c, g.v);
+    for (int64_t i = 0; i < k; ++i) sv[i] = std::sqrt(std::max(0.0, ev[2 * i]));
+  });
+}
+
+int qlra_solve_quaternion_linear(qlra_ctx_t* ctx, const qlra_qmat_t* a, const qlra_qmat_t* b,
+                                 qlra_qmat_t* x) {
+  return guarded(ctx, [&](Ctx& c) {
+    check_view(a, "solve_quaternion_linear");
+    check_view(b, "solve_quaternion_linear");
+    check_view(x, "solve_quaternion_linear");
+    if (a->rows != b->rows) fail(QLRA_ERR_SHAPE, "solve_quaternion_linear: row mismatch");
+    if (a->rows < a->cols)
+      fail(QLRA_ERR_SHAPE, "solve_quaternion_linear: underdetermined system not supported");
+    if (x->rows != a->cols || x->cols != b->cols)
+      fail(QLRA_ERR_SHAPE, "solve_quaternion_linear: output shape mismatch");
+    const QView A = view_of(a), B = view_of(b), X = view_of(x);
+    if (a->rows == a->cols) {
+      if (a->rows == 0) return;
+      DevQMat ainv(c, a->rows, a->cols);
+      const std::vector<double> st = quat_inverse(c, A, ainv.v);
+      if (st[0] != 0.0)
+        fail(QLRA_ERR_SINGULAR, "solve_quaternion_linear: singular system",
+             std::numeric_limits<double>::infinity());
+      DeviceBuffer nrm(c, 2 * sizeof(double));
+      small_chi_norm1(c, A, nrm.as<double>());
+      small_chi_norm1(c, ainv.v, nrm.as<double>() + 1);
+      const std::vector<double> nn = to_host(c, nrm.as<double>(), 2);
+      const double rc = (nn[0] > 0 && nn[1] > 0) ? 1.0 / (nn[0] * nn[1]) : 0.0;
+      if (!(rc > 1e-14))
+        fail(QLRA_ERR_SINGULAR, "solve_quaternion_linear: singular system",
+             rc > 0 ? 1.0 / rc : std::numeric_limits<double>::infinity());
+      qgemm(c, QLRA_OP_N, QLRA_OP_N, 1.0, ainv.v, B, 0.0, X);
+    } else {
+      lstsq(c, A, B, X);
+    }
+  });
+}
+
+int qlra_estimate_epsilon(qlra_ctx_t* ctx, const qlra_qmat_t* h, int power_iters, double* eps) {
+  return guarded(ctx, [&](Ctx& c) {
+    check_view(h, "estimate_epsilon");
+    if (power_iters < 1) fail(QLRA_ERR_PARAMETER, "estimate_epsilon: power_iters must be >= 1");
+    const int64_t s = h->cols;
+    DevQMat g(c, s, s);
+    gram(c, view_of(h), g.v);
+    const double kh = kappa_from_eigs(chi_eigs(c, g.v));
+    *eps = estimate_epsilon_from_gram(c, g.v, kh, power_iters);
+  });
+}
+
+int qlra_correction_step(qlra_ctx_t* ctx, const qlra_qmat_t* h, double epsilon, qlra_qmat_t* hout) {
+  return guarded(ctx, [&](Ctx& c) {
+    check_view(h, "correction_step");
+    check_view(hout, "correction_step");
+    if (!(epsilon > 0.0 && epsilon < 1.0))
+      fail(QLRA_ERR_PARAMETER, "correction_step: epsilon must lie in (0,1)");
+    const int64_t s = h->cols;
+    DevQMat g(c, s, s);
+    gram(c, view_of(h), g.v);
+    const double kh = kappa_from_eigs(chi_eigs(c, g.v));
+    correction_from_gram(c, view_of(h), g.v, kh, epsilon, view_of(hout));
+  });
+}
+
+int qlra_pseudo_qr(qlra_ctx_t* ctx, const qlra_qmat_t* y, const qlra_pseudo_qr_config_t* cfg_in,
+                   qlra_qmat_t* h, qlra_rangefinder_report_t* rep) {
+  return guarded(ctx, [&](Ctx& c) {
+    check_view(y, "pseudo_qr");
+    check_view(h, "pseudo_qr");
+    qlra_pseudo_qr_config_t cfg{3, 3, 1.2};
+    if (cfg_in) cfg = *cfg_in;
+    const int64_t s = y->cols;
+    const int64_t m = global_rows(c, y->rows);
+    if (m <= s) fail(QLRA_ERR_PARAMETER, "pseudo_qr: sketch must be tall (rows > cols)");
+    if (cfg.max_correction_steps < 0) fail(QLRA_ERR_PARAMETER, "pseudo_qr: negative correction step count");
+    if (!(cfg.delta_budget >= 1.0 && cfg.delta_budget <= std::sqrt(7.0) / 2.0 + 1e-12))
+      fail(QLRA_ERR_PARAMETER, "pseudo_qr: delta_budget outside [1, sqrt(7)/2]");
+    if (h->rows != y->rows || h->cols != s) fail(QLRA_ERR_SHAPE, "pseudo_qr: output shape mismatch");
+    const QView Y = view_of(y), H = view_of(h);
+    // complex_qr(to_compact(Y)) via CholeskyQR on the compact Gram
+    std::vector<double> rd;
+    if (!cholesky_qr(c, Y, H, /*complex_mode=*/true, m, &rd))
+      fail(QLRA_ERR_RANK, "pseudo_qr: sketch numerically rank-deficient; use pseudo_svd");
+    rank_check(rd);
+    qlra_rangefinder_report_t r{};
+    r.method = QLRA_PSEUDO_QR;
+    DevQMat g(c, s, s);
+    gram(c, H, g.v);
+    r.kappa_before = kappa_from_eigs(chi_eigs(c, g.v));
+    double kappa = r.kappa_before;
+    DevQMat h0, g0;
+    try {
+      while (r.correction_steps_used < cfg.max_correction_steps && kappa > kKappaTarget) {
+        if (r.correction_steps_used == 0) {
+          h0 = DevQMat(c, H.rows, s);
+          copy_qmat(c, H, h0.v);
+          g0 = DevQMat(c, s, s);
+          copy_qmat(c, g.v, g0.v);
+        }
+        const double eps = estimate_epsilon_from_gram(c, g.v, kappa, cfg.power_iters_for_epsilon);
+        correction_from_gram(c, H, g.v, kappa, eps, H);
+        gram(c, H, g.v);
+        kappa = kappa_from_eigs(chi_eigs(c, g.v));
+        ++r.correction_steps_used;
+      }
+    } catch (const Status& e) {
+      if (e.code != QLRA_ERR_SINGULAR) throw;
+      fail(QLRA_ERR_RANK, "pseudo_qr: sketch numerically rank-deficient; use pseudo_svd");
+    }
+    if (r.correction_steps_used > 0) {
+      // Re-project onto range(H0) (= span[Q, J conj Q], rangefinders.cpp:142-153):
+      // H <- H0 (H0^*H0)^{-1} (H0^* H).
+      DevQMat cc(c, s, s), z(c, s, s), g0inv(c, s, s);
+      qgemm(c, QLRA_OP_C, QLRA_OP_N, 1.0, h0.v, H, 0.0, cc.v);
+      allreduce_qmat(c, cc.v);
+      const std::vector<double> st = quat_inverse(c, g0.v, g0inv.v);
+      if (st[0] != 0.0)
+        fail(QLRA_ERR_RANK, "pseudo_qr: sketch numerically rank-deficient; use pseudo_svd");
+      qgemm(c, QLRA_OP_N, QLRA_OP_N, 1.0, g0inv.v, cc.v, 0.0, z.v);
+      qgemm(c, QLRA_OP_N, QLRA_OP_N, 1.0, h0.v, z.v, 0.0, H);
+      gram(c, H, g.v);
+      r.kappa_after = kappa_from_eigs(chi_eigs(c, g.v));
+    } else {
+      r.kappa_after = kappa;
+    }
+    if (rep) *rep = r;
+  });
+}
+
+int qlra_pseudo_svd(qlra_ctx_t* ctx, const qlra_qmat_t* y, uint64_t seed, qlra_qmat_t* h,
+                    qlra_rangefinder_report_t* rep) {
+  (void)seed;
+  return guarded(ctx, [&](Ctx& c) {
+    check_view(y, "pseudo_svd");
+    check_view(h, "pseudo_svd");
+    const int64_t s = y->cols;
+    const int64_t m = global_rows(c, y->rows);
+    if (m <= s) fail(QLRA_ERR_PARAMETER, "pseudo_svd: sketch must be tall (rows > cols)");
+    if (h->rows != y->rows || h->cols != s) fail(QLRA_ERR_SHAPE, "pseudo_svd: output shape mismatch");
+    const QView Y = view_of(y), H = view_of(h);
+    qlra_rangefinder_report_t r{};
+    r.method = QLRA_PSEUDO_SVD;
+    r.kappa_before = condition_number_dev(c, Y);
+    if (!cholesky_qr(c, Y, H, /*complex_mode=*/false, m, nullptr))
+      fail(QLRA_ERR_PRECONDITION,
+           "pseudo_svd: rank-deficient sketch (bad-block repair) is not implemented on device yet");
+    r.kappa_after = condition_number_dev(c, H);
+    if (rep) *rep = r;
+  });
+}
+
+int qlra_qb_solve(qlra_ctx_t* ctx, const qlra_spec_t* psi, int64_t row0, const qlra_qmat_t* h,
+                  const qlra_qmat_t* w, qlra_qmat_t* x) {
+  return guarded(ctx, [&](Ctx& c) {
+    validate_spec(psi);
+    check_view(h, "qb_solve");
+    check_view(w, "qb_solve");
+    check_view(x, "qb_solve");
+    const int64_t s = h->cols, l = psi->rows, n = w->cols;
+    if (w->rows != l || x->rows != s || x->cols != n) fail(QLRA_ERR_SHAPE, "qb_stage: shape mismatch");
+    if (row0 < 0 || row0 + h->rows > psi->cols) fail(QLRA_ERR_SHAPE, "qb_stage: Psi shape mismatch");
+    DevQMat ps(c, l, h->rows);
+    launch_gen(c.stream, *psi, 0, row0, l, h->rows, ps.v, false);
+    DevQMat p(c, l, s);
+    qgemm(c, QLRA_OP_N, QLRA_OP_N, 1.0, ps.v, view_of(h), 0.0, p.v);
+    allreduce_qmat(c, p.v);
+    lstsq(c, p.v, view_of(w), view_of(x));
+  });
+}
+
+int qlra_residual_fro(qlra_ctx_t* ctx, const qlra_qmat_t* a, const qlra_qmat_t* h,
+                      const qlra_qmat_t* x, double* res_fro, double* a_fro) {
+  return guarded(ctx, [&](Ctx& c) {
+    check_view(a, "residual");
+    check_view(h, "residual");
+    check_view(x, "residual");
+    DeviceBuffer out(c, 2 * sizeof(double));
+    qgemm_residual(c, view_of(a), view_of(h), view_of(x), out.as<double>());
+    allreduce_sum(c, out.as<double>(), 2);
+    const std::vector<double> v = to_host(c, out.as<double>(), 2);
+    if (res_fro) *res_fro = std::sqrt(v[0]);
+    if (a_fro) *a_fro = std::sqrt(v[1]);
+  });
+}
+
+int qlra_measure_fp64_peak(qlra_ctx_t* ctx, int mode, double ms, double* tflops) {
+  return guarded(ctx, [&](Ctx& c) { *tflops = measure_fp64_peak(c, mode, ms); });
+}
+
+const char* qlra_sketch_kernel_name(void) { return sketch_kernel_name(); }
+
+}  // extern "C"

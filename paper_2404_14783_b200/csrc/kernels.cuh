@@ -1,0 +1,147 @@
+// kernels.cuh -- host-side declarations shared by the qlra CUDA sources.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <atomic>
+#include <string>
+
+#include "common.cuh"
+
+namespace qlra_dev {
+
+// Launch counter (evidence of device work; exported via qlra_ctx_launch_count).
+std::atomic<int64_t>& launch_counter();
+inline void count_launch() { launch_counter().fetch_add(1, std::memory_order_relaxed); }
+
+// One context per (host thread, device): stream, NCCL communicator, errors.
+struct Ctx {
+  int device = 0;
+  int rank = 0, nranks = 1;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  ncclComm_t comm = nullptr;
+  std::string last_error;
+  double last_cond = 0.0;
+  double* pinned = nullptr;  // small host staging buffer (syncs)
+};
+
+// Stream-ordered device allocation (cudaMallocAsync from the device's default
+// pool, whose release threshold is raised at ctx creation so steady-state
+// calls do not hit the driver).
+struct DeviceBuffer {
+  Ctx* ctx = nullptr;
+  void* ptr = nullptr;
+  size_t bytes = 0;
+  DeviceBuffer() = default;
+  DeviceBuffer(Ctx& c, size_t n) : ctx(&c), bytes(n) {
+    if (n) QLRA_CUDA(cudaMallocAsync(&ptr, n, c.stream));
+  }
+  DeviceBuffer(const DeviceBuffer&) = delete;
+  DeviceBuffer& operator=(const DeviceBuffer&) = delete;
+  DeviceBuffer(DeviceBuffer&& o) noexcept : ctx(o.ctx), ptr(o.ptr), bytes(o.bytes) { o.ptr = nullptr; }
+  DeviceBuffer& operator=(DeviceBuffer&& o) noexcept {
+    if (this != &o) {
+      release();
+      ctx = o.ctx;
+      ptr = o.ptr;
+      bytes = o.bytes;
+      o.ptr = nullptr;
+    }
+    return *this;
+  }
+  void release() {
+    if (ptr) cudaFreeAsync(ptr, ctx->stream);
+    ptr = nullptr;
+  }
+  ~DeviceBuffer() { release(); }
+  template <class T>
+  T* as() const { return static_cast<T*>(ptr); }
+};
+
+// Owned device quaternion matrix (4 planes in one allocation, ld = cols).
+struct DevQMat {
+  DeviceBuffer buf;
+  QView v{};
+  DevQMat() = default;
+  DevQMat(Ctx& c, int64_t rows, int64_t cols) : buf(c, (size_t)4 * rows * cols * sizeof(double)) {
+    double* base = buf.as<double>();
+    for (int p = 0; p < 4; ++p) v.p[p] = base + (size_t)p * rows * cols;
+    v.rows = rows;
+    v.cols = cols;
+    v.ld = cols;
+  }
+  void zero(Ctx& c) {
+    if (buf.bytes) QLRA_CUDA(cudaMemsetAsync(buf.ptr, 0, buf.bytes, c.stream));
+  }
+};
+
+// Sub-block view (rows [r0, r0+nr), cols [c0, c0+nc)).
+inline QView sub(const QView& a, int64_t r0, int64_t c0, int64_t nr, int64_t nc) {
+  QView v = a;
+  for (int p = 0; p < 4; ++p) v.p[p] = a.p[p] + r0 * a.ld + c0;
+  v.rows = nr;
+  v.cols = nc;
+  return v;
+}
+
+// ------------------------------------------------------------ embed.cu ---
+void launch_gen(cudaStream_t st, const qlra_spec_t& spec, int64_t r0, int64_t c0, int64_t nrows,
+                int64_t ncols, const QView& out, bool transposed);
+
+// ------------------------------------------------------------ qgemm.cu ---
+void qgemm(Ctx& ctx, int op_a, int op_b, double alpha, const QView& A, const QView& B,
+           double beta, const QView& C, int force_splits = 0);
+// d_out2[0] = ||R - H X||_F^2, d_out2[1] = ||R||_F^2 (device pointer)
+void qgemm_residual(Ctx& ctx, const QView& R, const QView& H, const QView& X, double* d_out2);
+
+// ----------------------------------------------------------- sketch.cu ---
+void sketch_update_rows(Ctx& ctx, const qlra_spec_t& omega, const qlra_spec_t& psi, int64_t row0,
+                        const QView& block, const QView& y_rows, const QView& w);
+const char* sketch_kernel_name();
+
+// ---------------------------------------------------------- smallla.cu ---
+// All "small" matrices are s x s (or 2s x 2s complex), s <= ~1000, resident
+// in L2; kernels run on one CTA unless noted.
+// Complex matrices: row-major double2 with leading dimension ld.
+void small_chi_from_quat(Ctx& ctx, const QView& g, double2* chi, int64_t ldc);
+void small_complex_part(Ctx& ctx, const QView& g, double2* c, int64_t ldc);
+// Lower Cholesky in place; *d_info = 0 or first failing column (1-based).
+void small_cholesky(Ctx& ctx, double2* a, int64_t n, int64_t ld, int* d_info);
+// out = (L^{-1})^*  (upper), written as a quaternion with zero j,k planes.
+void small_inv_lower_adjoint_to_quat(Ctx& ctx, const double2* l, int64_t n, int64_t ld,
+                                     const QView& out);
+// Eigenvalues (descending) of a Hermitian complex matrix (destroyed).
+void small_herm_eigvals(Ctx& ctx, double2* a, int64_t n, int64_t ld, double* d_w);
+// Gauss-Jordan with partial pivoting on quaternion A (n x n): B <- A^{-1} B,
+// A destroyed.  d_stat[0] = info (0 ok, k+1 = zero pivot at k),
+// d_stat[1..2] = min/max pivot norm (doubles via reinterpret).
+void small_quat_solve(Ctx& ctx, const QView& a, const QView& b, double* d_stat);
+// ||chi_A||_1 into *d_out (device).
+void small_chi_norm1(Ctx& ctx, const QView& a, double* d_out);
+// out = alpha * I + beta * a   (square)
+void small_axpby_identity(Ctx& ctx, double alpha, double beta, const QView& a, const QView& out);
+void small_set_identity(Ctx& ctx, const QView& out);
+// estimate_epsilon power iterations on chi_{Ginv}: *d_rho (device).
+void small_power_iter_inverse(Ctx& ctx, const QView& ginv, int iters, double* d_rho);
+// Quaternion Cholesky G = R^*R in place (upper triangle), *d_info as above.
+void small_quat_cholesky(Ctx& ctx, const QView& g, int* d_info);
+// x = r^{-1}, r upper triangular quaternion with real diagonal.
+void small_quat_triinv_upper(Ctx& ctx, const QView& r, const QView& x);
+void small_add_diag(Ctx& ctx, const QView& g, double shift);
+void small_add_diag_complex(Ctx& ctx, double2* a, int64_t n, int64_t ld, double shift);
+// dst = src (same shape)
+void copy_qmat(Ctx& ctx, const QView& src, const QView& dst);
+void scale_add_qmat(Ctx& ctx, double a, const QView& x, double b, const QView& y,
+                    const QView& out);  // out = a x + b y
+
+// ------------------------------------------------------------- peak.cu ---
+double measure_fp64_peak(Ctx& ctx, int mode, double ms);
+
+// ---------------------------------------------------------- collective ---
+void allreduce_sum(Ctx& ctx, double* buf, size_t count);
+void allreduce_qmat(Ctx& ctx, const QView& m);  // contiguous-ld views only
+
+}  // namespace qlra_dev

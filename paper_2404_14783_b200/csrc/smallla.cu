@@ -1,0 +1,630 @@
+// smallla.cu -- K4: small dense factorizations on device (no CPU fallback).
+//
+// Replace the Eigen factorizations the reference applies to the small
+// s x s / 2s x 2s matrices of the rangefinders and the core solve:
+//   HouseholderQR R factor of Y_c   -> Cholesky of the compact Gram
+//                                       (CholeskyQR; factorizations.cpp:33-51)
+//   BDCSVD singular values of chi_H -> Hermitian eigenvalues of chi_{H*H}
+//                                       (factorizations.cpp:316-337)
+//   PartialPivLU / ColPivHouseholderQR on chi -> quaternion Gauss-Jordan with
+//                                       partial pivoting (complex_bridge.cpp:63-90,
+//                                       rangefinders.cpp:71-93)
+// Matrices live in global memory (L2-resident at these sizes) and are worked
+// on by one 1024-thread CTA; every reduction has a fixed order.
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace qlra_dev {
+
+namespace {
+
+constexpr int SNT = 1024;
+
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+__device__ __forceinline__ double2 cmulc(double2 a, double2 b) {  // a * conj(b)
+  return make_double2(a.x * b.x + a.y * b.y, a.y * b.x - a.x * b.y);
+}
+__device__ __forceinline__ double2 cconj(double2 a) { return make_double2(a.x, -a.y); }
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double2 cdiv(double2 a, double2 b) {
+  const double d = b.x * b.x + b.y * b.y;
+  return make_double2((a.x * b.x + a.y * b.y) / d, (a.y * b.x - a.x * b.y) / d);
+}
+
+// Fixed-order block sum (tree over threadIdx), result broadcast.
+__device__ double block_sum(double v, double* sh) {
+  const int t = threadIdx.x;
+  sh[t] = v;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if (t < w) sh[t] += sh[t + w];
+    __syncthreads();
+  }
+  const double r = sh[0];
+  __syncthreads();
+  return r;
+}
+
+struct Q4 {
+  double w, x, y, z;
+};
+__device__ __forceinline__ Q4 qmul(Q4 a, Q4 b) {
+  return {a.w * b.w - a.x * b.x - a.y * b.y - a.z * b.z, a.w * b.x + a.x * b.w + a.y * b.z - a.z * b.y,
+          a.w * b.y - a.x * b.z + a.y * b.w + a.z * b.x, a.w * b.z + a.x * b.y - a.y * b.x + a.z * b.w};
+}
+__device__ __forceinline__ Q4 qload(const QView& m, int64_t i, int64_t j) {
+  const int64_t o = i * m.ld + j;
+  return {m.p[0][o], m.p[1][o], m.p[2][o], m.p[3][o]};
+}
+__device__ __forceinline__ void qstore(const QView& m, int64_t i, int64_t j, Q4 q) {
+  const int64_t o = i * m.ld + j;
+  m.p[0][o] = q.w;
+  m.p[1][o] = q.x;
+  m.p[2][o] = q.y;
+  m.p[3][o] = q.z;
+}
+
+// ------------------------------------------------------------ kernels ---
+__global__ void k_chi_from_quat(QView g, double2* chi, int64_t ldc) {
+  const int64_t n = g.rows;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n * n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / n, j = e % n;
+    const Q4 q = qload(g, i, j);
+    const double2 q0 = make_double2(q.w, q.x), q1 = make_double2(q.y, q.z);
+    chi[i * ldc + j] = q0;
+    chi[i * ldc + n + j] = q1;
+    chi[(n + i) * ldc + j] = make_double2(-q1.x, q1.y);  // -conj(q1)
+    chi[(n + i) * ldc + n + j] = cconj(q0);
+  }
+}
+
+__global__ void k_complex_part(QView g, double2* c, int64_t ldc) {
+  const int64_t n = g.rows, m = g.cols;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n * m;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / m, j = e % m;
+    c[i * ldc + j] = make_double2(g.p[0][i * g.ld + j], g.p[1][i * g.ld + j]);
+  }
+}
+
+// Right-looking lower Cholesky, one CTA.  Only the lower triangle is read.
+__global__ void __launch_bounds__(SNT) k_cholesky(double2* a, int64_t n, int64_t ld, int* info) {
+  __shared__ double s_piv;
+  __shared__ int s_bad;
+  const int t = threadIdx.x;
+  if (t == 0) { *info = 0; s_bad = 0; }
+  for (int64_t k = 0; k < n; ++k) {
+    if (t == 0) {
+      const double d = a[k * ld + k].x;
+      if (!(d > 0.0)) {
+        s_bad = (int)k + 1;
+        *info = (int)k + 1;
+      } else {
+        s_piv = sqrt(d);
+        a[k * ld + k] = make_double2(s_piv, 0.0);
+      }
+    }
+    __syncthreads();
+    if (s_bad) return;
+    const double inv = 1.0 / s_piv;
+    for (int64_t i = k + 1 + t; i < n; i += blockDim.x) {
+      double2 v = a[i * ld + k];
+      a[i * ld + k] = make_double2(v.x * inv, v.y * inv);
+    }
+    __syncthreads();
+    const int64_t r = n - k - 1;
+    for (int64_t e = t; e < r * r; e += blockDim.x) {
+      const int64_t i = k + 1 + e / r, j = k + 1 + e % r;
+      if (j > i) continue;
+      const double2 lik = a[i * ld + k], ljk = a[j * ld + k];
+      a[i * ld + j] = csub(a[i * ld + j], cmulc(lik, ljk));
+    }
+    __syncthreads();
+  }
+}
+
+// out(i, j) = conj(Linv(j, i)) for i <= j (upper), as quaternion w/x planes.
+// Column-parallel forward substitution: thread j owns column j of L^{-1}.
+__global__ void __launch_bounds__(SNT) k_inv_lower_adj(const double2* l, int64_t n, int64_t ld, QView out) {
+  for (int64_t j = threadIdx.x; j < n; j += blockDim.x) {
+    for (int64_t i = 0; i < n; ++i) {
+      // column j of L^{-1} is x; out row j col i = conj(x_i)
+      for (int p = 0; p < 4; ++p) out.p[p][i * out.ld + j] = 0.0;
+    }
+  }
+  __syncthreads();
+  for (int64_t j = threadIdx.x; j < n; j += blockDim.x) {
+    // x_i for i >= j stored into out(j, i) as conj
+    for (int64_t i = j; i < n; ++i) {
+      double2 s = make_double2(i == j ? 1.0 : 0.0, 0.0);
+      for (int64_t k = j; k < i; ++k) {
+        const double2 xk = make_double2(out.p[0][j * out.ld + k], -out.p[1][j * out.ld + k]);
+        s = csub(s, cmul(l[i * ld + k], xk));
+      }
+      const double2 xi = cdiv(s, l[i * ld + i]);
+      out.p[0][j * out.ld + i] = xi.x;
+      out.p[1][j * out.ld + i] = -xi.y;
+    }
+  }
+}
+
+// Householder tridiagonalisation (LAPACK zhetd2, lower) of a full Hermitian
+// matrix, one CTA; d (n), e (n-1) out.  work: 2n double2.
+__global__ void __launch_bounds__(SNT) k_tridiag(double2* a, int64_t n, int64_t ld, double* d,
+                                                 double* e, double2* work) {
+  __shared__ double sh[SNT];
+  __shared__ double2 s_tau, s_alpha2;
+  __shared__ int s_skip;
+  const int t = threadIdx.x;
+  double2* v = work;
+  double2* x = work + n;
+  for (int64_t k = 0; k + 1 < n; ++k) {
+    const int64_t len = n - k - 1;
+    double part = 0.0;
+    for (int64_t i = k + 2 + t; i < n; i += blockDim.x) {
+      const double2 q = a[i * ld + k];
+      part += q.x * q.x + q.y * q.y;
+    }
+    const double xnorm2 = block_sum(part, sh);
+    if (t == 0) {
+      const double2 alpha = a[(k + 1) * ld + k];
+      if (xnorm2 == 0.0 && alpha.y == 0.0) {
+        s_skip = 1;
+        e[k] = alpha.x;
+        s_tau = make_double2(0.0, 0.0);
+      } else {
+        s_skip = 0;
+        const double beta = -copysign(sqrt(alpha.x * alpha.x + alpha.y * alpha.y + xnorm2), alpha.x);
+        s_tau = make_double2((beta - alpha.x) / beta, -alpha.y / beta);
+        s_alpha2 = cdiv(make_double2(1.0, 0.0), make_double2(alpha.x - beta, alpha.y));
+        e[k] = beta;
+      }
+    }
+    __syncthreads();
+    if (s_skip) continue;
+    const double2 scal = s_alpha2, tau = s_tau;
+    for (int64_t i = t; i < len; i += blockDim.x)
+      v[i] = i == 0 ? make_double2(1.0, 0.0) : cmul(a[(k + 1 + i) * ld + k], scal);
+    __syncthreads();
+    // x = tau * A22 v
+    for (int64_t r = t; r < len; r += blockDim.x) {
+      double2 s = make_double2(0.0, 0.0);
+      const double2* row = a + (k + 1 + r) * ld + (k + 1);
+      for (int64_t c = 0; c < len; ++c) s = cadd(s, cmul(row[c], v[c]));
+      x[r] = cmul(tau, s);
+    }
+    __syncthreads();
+    // alpha = -1/2 tau (x^H v)
+    double pr = 0.0, pi = 0.0;
+    for (int64_t r = t; r < len; r += blockDim.x) {
+      const double2 q = cmul(cconj(x[r]), v[r]);
+      pr += q.x;
+      pi += q.y;
+    }
+    const double dr = block_sum(pr, sh);
+    const double di = block_sum(pi, sh);
+    const double2 al = cmul(make_double2(-0.5 * tau.x, -0.5 * tau.y), make_double2(dr, di));
+    for (int64_t r = t; r < len; r += blockDim.x) x[r] = cadd(x[r], cmul(al, v[r]));
+    __syncthreads();
+    // A22 -= v x^H + x v^H
+    for (int64_t q = t; q < len * len; q += blockDim.x) {
+      const int64_t r = q / len, c = q % len;
+      double2* p = a + (k + 1 + r) * ld + (k + 1 + c);
+      *p = csub(*p, cadd(cmulc(v[r], x[c]), cmulc(x[r], v[c])));
+    }
+    __syncthreads();
+  }
+  for (int64_t i = t; i < n; i += blockDim.x) d[i] = a[i * ld + i].x;
+}
+
+__device__ int sturm_count(const double* d, const double* e, int64_t n, double x) {
+  int cnt = 0;
+  double q = d[0] - x;
+  if (q < 0) ++cnt;
+  for (int64_t i = 1; i < n; ++i) {
+    if (q == 0.0) q = 1e-300;
+    q = d[i] - x - e[i - 1] * e[i - 1] / q;
+    if (q < 0) ++cnt;
+  }
+  return cnt;
+}
+
+// Bisection for every eigenvalue; w sorted descending.
+__global__ void k_bisect(const double* d, const double* e, int64_t n, double* w) {
+  __shared__ double s_lo, s_hi;
+  if (threadIdx.x == 0) {
+    double lo = d[0], hi = d[0];
+    for (int64_t i = 0; i < n; ++i) {
+      const double r = (i > 0 ? fabs(e[i - 1]) : 0.0) + (i + 1 < n ? fabs(e[i]) : 0.0);
+      lo = fmin(lo, d[i] - r);
+      hi = fmax(hi, d[i] + r);
+    }
+    const double pad = 2.2e-16 * fmax(fabs(lo), fabs(hi)) * (double)n + 1e-300;
+    s_lo = lo - pad;
+    s_hi = hi + pad;
+  }
+  __syncthreads();
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    // k-th smallest eigenvalue: smallest x with count(x) > k
+    double lo = s_lo, hi = s_hi;
+    for (int it = 0; it < 200; ++it) {
+      const double mid = 0.5 * (lo + hi);
+      if (mid <= lo || mid >= hi) break;
+      if (sturm_count(d, e, n, mid) > k) hi = mid; else lo = mid;
+    }
+    w[n - 1 - k] = 0.5 * (lo + hi);
+  }
+}
+
+// Quaternion Gauss-Jordan with partial pivoting (left row operations), one CTA.
+__global__ void __launch_bounds__(SNT) k_quat_gj(QView a, QView b, double* stat, Q4* mult) {
+  __shared__ double sh[SNT];
+  __shared__ int shi[SNT];
+  __shared__ int s_piv;
+  __shared__ Q4 s_pinv;
+  const int t = threadIdx.x;
+  const int64_t n = a.rows, nb = b.cols;
+  double pmin = 1e300, pmax = 0.0;
+  for (int64_t k = 0; k < n; ++k) {
+    // pivot search: max |a(i,k)|^2, i >= k, lowest index on ties
+    double best = -1.0;
+    int bi = (int)k;
+    for (int64_t i = k + t; i < n; i += blockDim.x) {
+      const Q4 q = qload(a, i, k);
+      const double nq = q.w * q.w + q.x * q.x + q.y * q.y + q.z * q.z;
+      if (nq > best) { best = nq; bi = (int)i; }
+    }
+    sh[t] = best;
+    shi[t] = bi;
+    __syncthreads();
+    for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+      if (t < w) {
+        if (sh[t + w] > sh[t] || (sh[t + w] == sh[t] && shi[t + w] < shi[t])) {
+          sh[t] = sh[t + w];
+          shi[t] = shi[t + w];
+        }
+      }
+      __syncthreads();
+    }
+    if (t == 0) {
+      s_piv = shi[0];
+      const double nq = sh[0];
+      if (!(nq > 0.0)) {
+        s_piv = -1;
+      } else {
+        const Q4 p = qload(a, s_piv, k);
+        s_pinv = {p.w / nq, -p.x / nq, -p.y / nq, -p.z / nq};
+        pmin = fmin(pmin, sqrt(nq));
+        pmax = fmax(pmax, sqrt(nq));
+      }
+    }
+    __syncthreads();
+    if (s_piv < 0) {
+      if (t == 0) { stat[0] = (double)(k + 1); stat[1] = 0.0; stat[2] = pmax; }
+      return;
+    }
+    const int64_t pr = s_piv;
+    // swap rows k and pr, then scale row k by pinv (left)
+    for (int64_t j = t; j < n + nb; j += blockDim.x) {
+      const bool inA = j < n;
+      const QView& m = inA ? a : b;
+      const int64_t jj = inA ? j : j - n;
+      Q4 rk = qload(m, k, jj), rp = qload(m, pr, jj);
+      if (pr != k) qstore(m, pr, jj, rk);
+      qstore(m, k, jj, qmul(s_pinv, rp));
+    }
+    __syncthreads();
+    for (int64_t i = t; i < n; i += blockDim.x) mult[i] = qload(a, i, k);
+    __syncthreads();
+    for (int64_t q = t; q < n * (n + nb); q += blockDim.x) {
+      const int64_t i = q / (n + nb), j = q % (n + nb);
+      if (i == k) continue;
+      const Q4 f = mult[i];
+      const bool inA = j < n;
+      const QView& m = inA ? a : b;
+      const int64_t jj = inA ? j : j - n;
+      if (inA && jj < k) continue;  // already eliminated columns stay zero
+      const Q4 rk = qload(m, k, jj);
+      const Q4 pr2 = qmul(f, rk);
+      Q4 cur = qload(m, i, jj);
+      cur.w -= pr2.w; cur.x -= pr2.x; cur.y -= pr2.y; cur.z -= pr2.z;
+      qstore(m, i, jj, cur);
+    }
+    __syncthreads();
+  }
+  if (t == 0) { stat[0] = 0.0; stat[1] = pmin; stat[2] = pmax; }
+}
+
+__global__ void k_chi_norm1(QView a, double* out) {
+  __shared__ double sh[SNT];
+  const int t = threadIdx.x;
+  double best = 0.0;
+  for (int64_t j = t; j < a.cols; j += blockDim.x) {
+    double s = 0.0;
+    for (int64_t i = 0; i < a.rows; ++i) {
+      const Q4 q = qload(a, i, j);
+      s += sqrt(q.w * q.w + q.x * q.x) + sqrt(q.y * q.y + q.z * q.z);
+    }
+    best = fmax(best, s);
+  }
+  sh[t] = best;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if (t < w) sh[t] = fmax(sh[t], sh[t + w]);
+    __syncthreads();
+  }
+  if (t == 0) *out = sh[0];
+}
+
+__global__ void k_axpby_identity(double alpha, double beta, QView a, QView out) {
+  const int64_t n = out.rows, m = out.cols;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n * m;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / m, j = e % m;
+#pragma unroll
+    for (int p = 0; p < 4; ++p) {
+      double v = beta * a.p[p][i * a.ld + j];
+      if (p == 0 && i == j) v += alpha;
+      out.p[p][i * out.ld + j] = v;
+    }
+  }
+}
+
+__global__ void k_scale_add(double a, QView x, double b, QView y, QView out) {
+  const int64_t n = out.rows, m = out.cols;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n * m;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / m, j = e % m;
+#pragma unroll
+    for (int p = 0; p < 4; ++p)
+      out.p[p][i * out.ld + j] = a * x.p[p][i * x.ld + j] + b * y.p[p][i * y.ld + j];
+  }
+}
+
+__global__ void k_copy(QView src, QView dst) {
+  const int64_t n = dst.rows, m = dst.cols;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n * m;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / m, j = e % m;
+#pragma unroll
+    for (int p = 0; p < 4; ++p) dst.p[p][i * dst.ld + j] = src.p[p][i * src.ld + j];
+  }
+}
+
+// estimate_epsilon's power iteration (rangefinders.cpp:80-96) on the
+// operator chi_{G^{-1}} applied from the quaternion inverse.  Start vector:
+// SequentialRng(CounterRng(0x455053).substream(2s)); entry i takes draws
+// (2i, 2i+1) with the imaginary part from the FIRST draw -- the order g++
+// gives the reference expression complex(next_gaussian(), next_gaussian()).
+__global__ void __launch_bounds__(SNT) k_power_inverse(QView ginv, int iters, double2* z, double2* w,
+                                                       double* rho_out) {
+  __shared__ double sh[SNT];
+  const int t = threadIdx.x;
+  const int64_t s = ginv.rows, n = 2 * s;
+  const uint64_t key = rng_substream(rng_key(0x455053ULL), (uint64_t)n);
+  double part = 0.0;
+  for (int64_t i = t; i < n; i += blockDim.x) {
+    // SequentialRng counters: gaussian g consumes uniforms (2g, 2g+1)
+    const uint64_t g0 = 2 * (uint64_t)i, g1 = g0 + 1;
+    const double first = box_muller(rng_uniform_at(key, 2 * g0), rng_uniform_at(key, 2 * g0 + 1));
+    const double second = box_muller(rng_uniform_at(key, 2 * g1), rng_uniform_at(key, 2 * g1 + 1));
+    z[i] = make_double2(second, first);
+    part += second * second + first * first;
+  }
+  double nz = sqrt(block_sum(part, sh));
+  for (int64_t i = t; i < n; i += blockDim.x) z[i] = make_double2(z[i].x / nz, z[i].y / nz);
+  __syncthreads();
+  double rho = 0.0;
+  for (int it = 0; it < iters; ++it) {
+    // w = chi_{M} z, chi_M = [[M0, M1], [-conj M1, conj M0]]
+    for (int64_t r = t; r < n; r += blockDim.x) {
+      double2 acc = make_double2(0.0, 0.0);
+      const bool top = r < s;
+      const int64_t i = top ? r : r - s;
+      for (int64_t c = 0; c < s; ++c) {
+        const int64_t o = i * ginv.ld + c;
+        const double2 m0 = make_double2(ginv.p[0][o], ginv.p[1][o]);
+        const double2 m1 = make_double2(ginv.p[2][o], ginv.p[3][o]);
+        if (top) {
+          acc = cadd(acc, cadd(cmul(m0, z[c]), cmul(m1, z[s + c])));
+        } else {
+          acc = cadd(acc, csub(cmul(cconj(m0), z[s + c]), cmul(cconj(m1), z[c])));
+        }
+      }
+      w[r] = acc;
+    }
+    __syncthreads();
+    double pr = 0.0, nw = 0.0;
+    for (int64_t r = t; r < n; r += blockDim.x) {
+      pr += z[r].x * w[r].x + z[r].y * w[r].y;  // Re(conj(z) w)
+      nw += w[r].x * w[r].x + w[r].y * w[r].y;
+    }
+    rho = block_sum(pr, sh);
+    const double nrm = sqrt(block_sum(nw, sh));
+    if (!(nrm > 0.0)) break;
+    for (int64_t r = t; r < n; r += blockDim.x) z[r] = make_double2(w[r].x / nrm, w[r].y / nrm);
+    __syncthreads();
+  }
+  if (t == 0) *rho_out = rho;
+}
+
+// Quaternion Cholesky G = R^* R (R upper, real positive diagonal), in place on
+// the upper triangle of g (lower triangle ignored), one CTA.
+__global__ void __launch_bounds__(SNT) k_quat_cholesky(QView g, int* info) {
+  __shared__ double s_piv;
+  __shared__ int s_bad;
+  const int t = threadIdx.x;
+  const int64_t n = g.rows;
+  if (t == 0) { *info = 0; s_bad = 0; }
+  for (int64_t k = 0; k < n; ++k) {
+    if (t == 0) {
+      const double d = g.p[0][k * g.ld + k];
+      if (!(d > 0.0)) {
+        s_bad = (int)k + 1;
+        *info = (int)k + 1;
+      } else {
+        s_piv = sqrt(d);
+        qstore(g, k, k, Q4{s_piv, 0.0, 0.0, 0.0});
+      }
+    }
+    __syncthreads();
+    if (s_bad) return;
+    const double inv = 1.0 / s_piv;
+    for (int64_t j = k + 1 + t; j < n; j += blockDim.x) {
+      Q4 q = qload(g, k, j);
+      qstore(g, k, j, Q4{q.w * inv, q.x * inv, q.y * inv, q.z * inv});
+    }
+    __syncthreads();
+    const int64_t r = n - k - 1;
+    for (int64_t e = t; e < r * r; e += blockDim.x) {
+      const int64_t i = k + 1 + e / r, j = k + 1 + e % r;
+      if (j < i) continue;
+      Q4 a = qload(g, k, i), b = qload(g, k, j);
+      a.x = -a.x; a.y = -a.y; a.z = -a.z;  // R_ki^*
+      const Q4 pq = qmul(a, b);
+      Q4 c = qload(g, i, j);
+      c.w -= pq.w; c.x -= pq.x; c.y -= pq.y; c.z -= pq.z;
+      qstore(g, i, j, c);
+    }
+    __syncthreads();
+  }
+}
+
+// X = R^{-1} for upper-triangular quaternion R with real diagonal; thread j
+// owns column j: X_jj = 1/R_jj, X_ij = -R_ii^{-1} sum_{k=i+1..j} R_ik X_kj.
+__global__ void __launch_bounds__(SNT) k_quat_triinv_upper(QView r, QView x) {
+  const int64_t n = r.rows;
+  for (int64_t j = threadIdx.x; j < n; j += blockDim.x) {
+    for (int64_t i = 0; i < n; ++i) qstore(x, i, j, Q4{0.0, 0.0, 0.0, 0.0});
+    qstore(x, j, j, Q4{1.0 / r.p[0][j * r.ld + j], 0.0, 0.0, 0.0});
+    for (int64_t i = j - 1; i >= 0; --i) {
+      Q4 s{0.0, 0.0, 0.0, 0.0};
+      for (int64_t k = i + 1; k <= j; ++k) {
+        const Q4 pq = qmul(qload(r, i, k), qload(x, k, j));
+        s.w += pq.w; s.x += pq.x; s.y += pq.y; s.z += pq.z;
+      }
+      const double inv = -1.0 / r.p[0][i * r.ld + i];
+      qstore(x, i, j, Q4{s.w * inv, s.x * inv, s.y * inv, s.z * inv});
+    }
+  }
+}
+
+__global__ void k_add_diag(QView g, double shift) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < g.rows;
+       i += (int64_t)gridDim.x * blockDim.x)
+    g.p[0][i * g.ld + i] += shift;
+}
+__global__ void k_add_diag_c(double2* a, int64_t n, int64_t ld, double shift) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    a[i * ld + i].x += shift;
+}
+
+unsigned grid_for(int64_t total) {
+  int64_t b = (total + 255) / 256;
+  if (b < 1) b = 1;
+  if (b > 148 * 8) b = 148 * 8;
+  return (unsigned)b;
+}
+
+}  // namespace
+
+void small_chi_from_quat(Ctx& ctx, const QView& g, double2* chi, int64_t ldc) {
+  k_chi_from_quat<<<grid_for(g.rows * g.rows), 256, 0, ctx.stream>>>(g, chi, ldc);
+  QLRA_LAUNCH_CHECK();
+  count_launch();
+}
+void small_complex_part(Ctx& ctx, const QView& g, double2* c, int64_t ldc) {
+  k_complex_part<<<grid_for(g.rows * g.cols), 256, 0, ctx.stream>>>(g, c, ldc);
+  QLRA_LAUNCH_CHECK();
+  count_launch();
+}
+void small_cholesky(Ctx& ctx, double2* a, int64_t n, int64_t ld, int* d_info) {
+  k_cholesky<<<1, SNT, 0, ctx.stream>>>(a, n, ld, d_info);
+  QLRA_LAUNCH_CHECK();
+  count_launch();
+}
+void small_inv_lower_adjoint_to_quat(Ctx& ctx, const double2* l, int64_t n, int64_t ld,
+                                     const QView& out) {
+  // j,k planes zero
+  k_inv_lower_adj<<<1, SNT, 0, ctx.stream>>>(l, n, ld, out);
+  QLRA_LAUNCH_CHECK();
+  count_launch();
+}
+void small_herm_eigvals(Ctx& ctx, double2* a, int64_t n, int64_t ld, double* d_w) {
+  if (n == 0) return;
+  DeviceBuffer de(ctx, sizeof(double) * (2 * n + 1));
+  DeviceBuffer work(ctx, sizeof(double2) * 2 * n);
+  double* d = de.as<double>();
+  double* e = d + n;
+  k_tridiag<<<1, SNT, 0, ctx.stream>>>(a, n, ld, d, e, work.as<double2>());
+  QLRA_LAUNCH_CHECK();
+  count_launch();
+  k_bisect<<<(unsigned)((n + 255) / 256), 256, 0, ctx.stream>>>(d, e, n, d_w);
+  QLRA_LAUNCH_CHECK();
+  count_launch();
+}
+void small_quat_solve(Ctx& ctx, const QView& a, const QView& b, double* d_stat) {
+  DeviceBuffer mult(ctx, sizeof(double) * 4 * std::max<int64_t>(1, a.rows));
+  k_quat_gj<<<1, SNT, 0, ctx.stream>>>(a, b, d_stat, mult.as<Q4>());
+  QLRA_LAUNCH_CHECK();
+  count_launch();
+}
+void small_chi_norm1(Ctx& ctx, const QView& a, double* d_out) {
+  k_chi_norm1<<<1, SNT, 0, ctx.stream>>>(a, d_out);
+  QLRA_LAUNCH_CHECK();
+  count_launch();
+}
+void small_axpby_identity(Ctx& ctx, double alpha, double beta, const QView& a, const QView& out) {
+  k_axpby_identity<<<grid_for(out.rows * out.cols), 256, 0, ctx.stream>>>(alpha, beta, a, out);
+  QLRA_LAUNCH_CHECK();
+  count_launch();
+}
+void small_set_identity(Ctx& ctx, const QView& out) {
+  small_axpby_identity(ctx, 1.0, 0.0, out, out);
+}
+void small_power_iter_inverse(Ctx& ctx, const QView& ginv, int iters, double* d_rho) {
+  DeviceBuffer zw(ctx, sizeof(double2) * 4 * ginv.rows);
+  k_power_inverse<<<1, SNT, 0, ctx.stream>>>(ginv, iters, zw.as<double2>(),
+                                              zw.as<double2>() + 2 * ginv.rows, d_rho);
+  QLRA_LAUNCH_CHECK();
+  count_launch();
+}
+void small_quat_cholesky(Ctx& ctx, const QView& g, int* d_info) {
+  k_quat_cholesky<<<1, SNT, 0, ctx.stream>>>(g, d_info);
+  QLRA_LAUNCH_CHECK();
+  count_launch();
+}
+void small_quat_triinv_upper(Ctx& ctx, const QView& r, const QView& x) {
+  k_quat_triinv_upper<<<1, SNT, 0, ctx.stream>>>(r, x);
+  QLRA_LAUNCH_CHECK();
+  count_launch();
+}
+void small_add_diag(Ctx& ctx, const QView& g, double shift) {
+  k_add_diag<<<1, 256, 0, ctx.stream>>>(g, shift);
+  QLRA_LAUNCH_CHECK();
+  count_launch();
+}
+void small_add_diag_complex(Ctx& ctx, double2* a, int64_t n, int64_t ld, double shift) {
+  k_add_diag_c<<<1, 256, 0, ctx.stream>>>(a, n, ld, shift);
+  QLRA_LAUNCH_CHECK();
+  count_launch();
+}
+void copy_qmat(Ctx& ctx, const QView& src, const QView& dst) {
+  k_copy<<<grid_for(dst.rows * dst.cols), 256, 0, ctx.stream>>>(src, dst);
+  QLRA_LAUNCH_CHECK();
+  count_launch();
+}
+void scale_add_qmat(Ctx& ctx, double a, const QView& x, double b, const QView& y,
+                    const QView& out) {
+  k_scale_add<<<grid_for(out.rows * out.cols), 256, 0, ctx.stream>>>(a, x, b, y, out);
+  QLRA_LAUNCH_CHECK();
+  count_launch();
+}
+
+}  // namespace qlra_dev

@@ -1,0 +1,530 @@
+"""Python mirror of the reference `qlra` hot-path API, running on the B200
+through the C-ABI (include/qlra_cuda.h).
+
+Names, argument meanings and error behaviour follow the reference headers
+proj/include/qlra/{sketching,rangefinders,complex_bridge,factorizations,
+qmatrix,errors}.hpp so the parity tests read like the reference's own tests.
+A QMatrix here is a CUDA float64 tensor of shape (4, rows, cols): the four
+row-major planes w, x, y, z of proj/include/qlra/qmatrix.hpp:14-19.  torch
+only provides device memory and streams; every FLOP runs in the library's
+sm_100a kernels.
+
+Multi-GPU (one process per GPU): create the Context with
+rank/nranks and an NCCL id; data matrices (A, Y, H) are then the rank's row
+shard and `row0` is the shard's first global row.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import time
+from dataclasses import dataclass, field
+from typing import Callable, Optional
+
+import torch
+
+from . import _lib as L
+
+GAUSSIAN, RADEMACHER, SPARSE_GAUSSIAN, SPARSE_RADEMACHER = 0, 1, 2, 3
+KIND_NAMES = {"gaussian": 0, "rademacher": 1, "sparse-gaussian": 2, "sparse-rademacher": 3}
+PSEUDO_QR, PSEUDO_SVD = 0, 1
+DEFAULT_RANGEFINDER_SEED = 0x9E3779B9  # rangefinders.hpp:29
+
+
+# ------------------------------------------------------------- errors ---
+# proj/include/qlra/errors.hpp:9-43
+class Error(RuntimeError):
+    pass
+
+
+class ShapeError(Error):
+    pass
+
+
+class ParameterError(Error):
+    pass
+
+
+class SingularMatrixError(Error):
+    def __init__(self, msg, estimated_condition):
+        super().__init__(msg)
+        self.estimated_condition = estimated_condition
+
+
+class RankError(Error):
+    pass
+
+
+class PreconditionError(Error):
+    pass
+
+
+class IoError(Error):
+    pass
+
+
+class DeviceError(Error):
+    pass
+
+
+_ERR = {1: ShapeError, 2: ParameterError, 4: RankError, 5: PreconditionError, 6: IoError}
+
+
+# ------------------------------------------------------------ context ---
+class Context:
+    """One per process/device: stream, NCCL communicator, error state."""
+
+    def __init__(self, device: int = 0, rank: int = 0, nranks: int = 1, nccl_id: bytes | None = None,
+                 use_torch_stream: bool = True):
+        self.lib = L.lib()
+        self.device = device
+        self.rank, self.nranks = rank, nranks
+        h = C.c_void_p()
+        buf = C.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
+        rc = self.lib.qlra_ctx_create(C.byref(h), device, rank, nranks, buf)
+        if rc != 0:
+            raise DeviceError(f"qlra_ctx_create failed ({rc})")
+        self.h = h
+        if use_torch_stream:
+            self.set_stream(torch.cuda.current_stream(device))
+
+    def set_stream(self, stream: torch.cuda.Stream):
+        self._check(self.lib.qlra_ctx_set_stream(self.h, C.c_void_p(stream.cuda_stream)))
+        self.stream = stream
+
+    def synchronize(self):
+        self._check(self.lib.qlra_ctx_synchronize(self.h))
+
+    def launch_count(self) -> int:
+        return int(self.lib.qlra_ctx_launch_count(self.h))
+
+    def _check(self, rc: int):
+        if rc == 0:
+            return
+        cond = C.c_double(0.0)
+        msg = self.lib.qlra_last_error(self.h, C.byref(cond)).decode()
+        if rc == 3:
+            raise SingularMatrixError(msg, cond.value)
+        raise _ERR.get(rc, DeviceError)(f"[{rc}] {msg}")
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.qlra_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        buf = C.create_string_buffer(128)
+        if L.lib().qlra_nccl_unique_id(buf) != 0:
+            raise DeviceError("ncclGetUniqueId failed")
+        return buf.raw
+
+
+_default_ctx: Optional[Context] = None
+
+
+def default_context() -> Context:
+    global _default_ctx
+    if _default_ctx is None:
+        _default_ctx = Context(torch.cuda.current_device())
+    return _default_ctx
+
+
+def set_default_context(ctx: Context):
+    global _default_ctx
+    _default_ctx = ctx
+
+
+def _ctx(ctx):
+    return ctx if ctx is not None else default_context()
+
+
+# ---------------------------------------------------------- QMatrix glue ---
+def qzeros(rows, cols, device=None):
+    return torch.zeros((4, rows, cols), dtype=torch.float64, device=device or "cuda")
+
+
+def _qm(t: torch.Tensor) -> L.QMat:
+    if t.dtype != torch.float64 or t.dim() != 3 or t.shape[0] != 4 or not t.is_cuda:
+        raise ShapeError("QMatrix must be a CUDA float64 tensor of shape (4, rows, cols)")
+    if t.shape[2] > 1 and t.stride(2) != 1:
+        raise ShapeError("QMatrix planes must be row-major (unit column stride)")
+    q = L.QMat()
+    base = t.data_ptr()
+    for p in range(4):
+        q.p[p] = base + p * t.stride(0) * 8
+    q.rows, q.cols = t.shape[1], t.shape[2]
+    q.ld = max(t.stride(1), t.shape[2]) if t.shape[1] > 1 else t.shape[2]
+    return q
+
+
+def identity(n, device=None):
+    e = qzeros(n, n, device)
+    e[0].fill_diagonal_(1.0)
+    return e
+
+
+def adjoint(a: torch.Tensor) -> torch.Tensor:
+    r = a.transpose(1, 2).contiguous()
+    r[1:] *= -1.0
+    return r
+
+
+def fro_norm(a: torch.Tensor) -> float:
+    return float(torch.sqrt(torch.sum(a * a)))
+
+
+# ------------------------------------------------------- test matrices ---
+@dataclass
+class TestMatrixSpec:
+    """== TestMatrixSpec (sketching.hpp:22-28)."""
+    kind: int = GAUSSIAN
+    rows: int = 0
+    cols: int = 0
+    seed: int = 0
+    density: float = 1.0
+
+    def c(self) -> L.Spec:
+        return L.Spec(self.kind, self.rows, self.cols, self.seed, self.density)
+
+
+def gen_block(spec: TestMatrixSpec, r0, r1, c0, c1, ctx=None):
+    ctx = _ctx(ctx)
+    out = qzeros(r1 - r0, c1 - c0)
+    s = spec.c()
+    ctx._check(ctx.lib.qlra_gen_test_matrix_block(ctx.h, C.byref(s), r0, c0, C.byref(_qm(out))))
+    return out
+
+
+def gen_test_matrix(spec: TestMatrixSpec, ctx=None):
+    return gen_block(spec, 0, spec.rows, 0, spec.cols, ctx)
+
+
+def gen_test_matrix_rows(spec, r0, r1, ctx=None):
+    return gen_block(spec, r0, r1, 0, spec.cols, ctx)
+
+
+def gen_test_matrix_cols(spec, c0, c1, ctx=None):
+    return gen_block(spec, 0, spec.rows, c0, c1, ctx)
+
+
+# ------------------------------------------------------------- sketch ---
+@dataclass
+class SketchState:
+    """== SketchState (sketching.hpp:38-47); y is the rank's row shard."""
+    y: torch.Tensor
+    w: torch.Tensor
+    omega_spec: TestMatrixSpec
+    psi_spec: TestMatrixSpec
+    r: int
+    s: int
+    l: int
+    row0: int = 0  # global index of y's first row (multi-GPU shards)
+
+    def data_rows(self):
+        return self.psi_spec.cols
+
+    def data_cols(self):
+        return self.w.shape[2]
+
+
+def validate_sketch_sizes(m, n, r, s, l):
+    if r < 1 or not (r <= s <= l <= min(m, n)):
+        raise ParameterError("sketch sizes must satisfy 1 <= r <= s <= l <= min(m,n)")
+
+
+def empty_sketch(m, n, r, s, l, omega_seed, psi_seed, kind=GAUSSIAN, density=1.0, rows_local=None,
+                 row0=0):
+    """sketching.cpp:110-123 (rows_local/row0 select this rank's Y shard)."""
+    validate_sketch_sizes(m, n, r, s, l)
+    if not (0.0 < density <= 1.0):
+        raise ParameterError("test matrix: density must lie in (0,1]")
+    ml = m if rows_local is None else rows_local
+    return SketchState(qzeros(ml, s), qzeros(l, n), TestMatrixSpec(kind, n, s, omega_seed, density),
+                       TestMatrixSpec(kind, l, m, psi_seed, density), r, s, l, row0)
+
+
+def sketch_update_rows(state: SketchState, row0: int, block: torch.Tensor, ctx=None):
+    """sketching.cpp:125-139; row0 is the GLOBAL row index of block's first row."""
+    ctx = _ctx(ctx)
+    lr0 = row0 - state.row0
+    if block.shape[2] != state.w.shape[2]:
+        raise ShapeError("sketch_update_rows: column count mismatch")
+    if lr0 < 0 or lr0 + block.shape[1] > state.y.shape[1]:
+        raise ShapeError("sketch_update_rows: row range out of bounds")
+    if block.shape[1] == 0:
+        return
+    yv = state.y[:, lr0:lr0 + block.shape[1], :]
+    om, ps = state.omega_spec.c(), state.psi_spec.c()
+    ctx._check(ctx.lib.qlra_sketch_update_rows(ctx.h, C.byref(om), C.byref(ps), row0,
+                                               C.byref(_qm(block)), C.byref(_qm(yv)),
+                                               C.byref(_qm(state.w))))
+
+
+def sketch_allreduce(state: SketchState, ctx=None):
+    ctx = _ctx(ctx)
+    ctx._check(ctx.lib.qlra_sketch_allreduce(ctx.h, C.byref(_qm(state.w))))
+
+
+def sketch_update(state: SketchState, delta: torch.Tensor, ctx=None):
+    if delta.shape[1] != state.y.shape[1]:
+        raise ShapeError("sketch_update: row count mismatch")
+    sketch_update_rows(state, state.row0, delta, ctx)
+
+
+def make_sketch(a, r, s, l, omega_seed, psi_seed, kind=GAUSSIAN, density=1.0, ctx=None, row0=0,
+                m_global=None):
+    """sketching.cpp:141-154.  With a row-sharded `a`, pass row0 / m_global and
+    the W partials are all-reduced across ranks."""
+    ctx = _ctx(ctx)
+    m = a.shape[1] if m_global is None else m_global
+    st = empty_sketch(m, a.shape[2], r, s, l, omega_seed, psi_seed, kind, density,
+                      rows_local=a.shape[1], row0=row0)
+    sketch_update_rows(st, row0, a, ctx)
+    if ctx.nranks > 1:
+        sketch_allreduce(st, ctx)
+    return st
+
+
+class MatrixSource:
+    """sketching.hpp:67-74: the sketch builder is the only reader."""
+
+    def rows(self) -> int:
+        raise NotImplementedError
+
+    def cols(self) -> int:
+        raise NotImplementedError
+
+    def read_rows(self, r0: int, r1: int) -> torch.Tensor:
+        raise NotImplementedError
+
+
+def sketch_from_source(source: MatrixSource, r, s, l, omega_seed, psi_seed, kind=GAUSSIAN,
+                       density=1.0, block_rows=256, ctx=None):
+    """sketching.cpp:156-167."""
+    if block_rows < 1:
+        raise ParameterError("sketch_from_source: block_rows must be >= 1")
+    st = empty_sketch(source.rows(), source.cols(), r, s, l, omega_seed, psi_seed, kind, density)
+    for r0 in range(0, source.rows(), block_rows):
+        r1 = min(source.rows(), r0 + block_rows)
+        sketch_update_rows(st, r0, source.read_rows(r0, r1), ctx)
+    return st
+
+
+# ----------------------------------------------------------- products ---
+OP_N, OP_C = 0, 1
+
+
+def qmat_mul(a, b, op_a=OP_N, op_b=OP_N, alpha=1.0, beta=0.0, out=None, ctx=None):
+    """qmat_mul (qmatrix.cpp:165-197) generalised to alpha op(A) op(B) + beta C."""
+    ctx = _ctx(ctx)
+    m = a.shape[1] if op_a == OP_N else a.shape[2]
+    n = b.shape[2] if op_b == OP_N else b.shape[1]
+    if out is None:
+        out = qzeros(m, n)
+    ctx._check(ctx.lib.qlra_qmat_mul(ctx.h, op_a, op_b, alpha, C.byref(_qm(a)), C.byref(_qm(b)), beta,
+                                     C.byref(_qm(out))))
+    return out
+
+
+def qmat_mul_ordered(a, b, ctx=None):
+    return qmat_mul(a, b, ctx=ctx)
+
+
+def gram(h, ctx=None):
+    ctx = _ctx(ctx)
+    g = qzeros(h.shape[2], h.shape[2])
+    ctx._check(ctx.lib.qlra_gram(ctx.h, C.byref(_qm(h)), C.byref(_qm(g))))
+    return g
+
+
+# -------------------------------------------------------- small dense ---
+def condition_number(a, ctx=None):
+    ctx = _ctx(ctx)
+    k = C.c_double()
+    ctx._check(ctx.lib.qlra_condition_number(ctx.h, C.byref(_qm(a)), C.byref(k)))
+    return k.value
+
+
+def singular_values(a, ctx=None):
+    ctx = _ctx(ctx)
+    k = min(a.shape[1], a.shape[2]) if ctx.nranks == 1 else a.shape[2]
+    out = (C.c_double * max(1, k))()
+    ctx._check(ctx.lib.qlra_singular_values(ctx.h, C.byref(_qm(a)), out))
+    return [out[i] for i in range(k)]
+
+
+def solve_quaternion_linear(a, b, ctx=None):
+    """complex_bridge.cpp:63-90."""
+    ctx = _ctx(ctx)
+    x = qzeros(a.shape[2], b.shape[2])
+    ctx._check(ctx.lib.qlra_solve_quaternion_linear(ctx.h, C.byref(_qm(a)), C.byref(_qm(b)),
+                                                    C.byref(_qm(x))))
+    return x
+
+
+# ------------------------------------------------------- rangefinders ---
+@dataclass
+class PseudoQrConfig:
+    """== PseudoQrConfig (rangefinders.hpp:23-27)."""
+    max_correction_steps: int = 3
+    power_iters_for_epsilon: int = 3
+    delta_budget: float = 1.2
+
+
+@dataclass
+class RangefinderReport:
+    """== RangefinderReport (rangefinders.hpp:14-21)."""
+    h: torch.Tensor
+    kappa_before: float = 0.0
+    kappa_after: float = 0.0
+    correction_steps_used: int = 0
+    method: int = PSEUDO_QR
+
+
+def estimate_epsilon(h, power_iters=3, ctx=None):
+    ctx = _ctx(ctx)
+    e = C.c_double()
+    ctx._check(ctx.lib.qlra_estimate_epsilon(ctx.h, C.byref(_qm(h)), power_iters, C.byref(e)))
+    return e.value
+
+
+def correction_step(h, epsilon, ctx=None):
+    ctx = _ctx(ctx)
+    out = torch.empty_like(h)
+    ctx._check(ctx.lib.qlra_correction_step(ctx.h, C.byref(_qm(h)), epsilon, C.byref(_qm(out))))
+    return out
+
+
+def pseudo_qr(y, cfg: PseudoQrConfig = PseudoQrConfig(), ctx=None) -> RangefinderReport:
+    """Algorithm 1 (rangefinders.cpp:107-158)."""
+    ctx = _ctx(ctx)
+    h = torch.empty_like(y)
+    c = L.PseudoQrConfig(cfg.max_correction_steps, cfg.power_iters_for_epsilon, cfg.delta_budget)
+    rep = L.Report()
+    ctx._check(ctx.lib.qlra_pseudo_qr(ctx.h, C.byref(_qm(y)), C.byref(c), C.byref(_qm(h)), C.byref(rep)))
+    return RangefinderReport(h, rep.kappa_before, rep.kappa_after, rep.correction_steps_used, PSEUDO_QR)
+
+
+def pseudo_svd(y, seed=DEFAULT_RANGEFINDER_SEED, ctx=None) -> RangefinderReport:
+    """Algorithm 3 (rangefinders.cpp:166-176): orthonormal H spanning range(Y)."""
+    ctx = _ctx(ctx)
+    h = torch.empty_like(y)
+    rep = L.Report()
+    ctx._check(ctx.lib.qlra_pseudo_svd(ctx.h, C.byref(_qm(y)), seed, C.byref(_qm(h)), C.byref(rep)))
+    return RangefinderReport(h, rep.kappa_before, rep.kappa_after, 0, PSEUDO_SVD)
+
+
+# ------------------------------------------------------------ QB stage ---
+@dataclass
+class QbResult:
+    """== QbResult (sketching.hpp:88-94)."""
+    h: torch.Tensor
+    x: torch.Tensor
+    report: RangefinderReport
+    rangefinder_s: float = 0.0
+    solve_s: float = 0.0
+
+
+def qb_solve(psi_spec: TestMatrixSpec, h, w, row0=0, ctx=None):
+    ctx = _ctx(ctx)
+    x = qzeros(h.shape[2], w.shape[2])
+    ps = psi_spec.c()
+    ctx._check(ctx.lib.qlra_qb_solve(ctx.h, C.byref(ps), row0, C.byref(_qm(h)), C.byref(_qm(w)),
+                                     C.byref(_qm(x))))
+    return x
+
+
+def qb_stage(state: SketchState, method=PSEUDO_QR, rangefinder_seed=DEFAULT_RANGEFINDER_SEED,
+             qr_cfg: PseudoQrConfig = PseudoQrConfig(), ctx=None, timer: Callable | None = None) -> QbResult:
+    """qb_stage (sketching.cpp:169-194): rangefinder on Y, then X = (Psi H) \\ W
+    with Psi regenerated from its spec.  Never touches A."""
+    ctx = _ctx(ctx)
+    t0 = time.perf_counter()
+    rep = pseudo_qr(state.y, qr_cfg, ctx) if method == PSEUDO_QR else pseudo_svd(state.y, rangefinder_seed, ctx)
+    t1 = time.perf_counter()
+    x = qb_solve(state.psi_spec, rep.h, state.w, state.row0, ctx)
+    ctx.synchronize()
+    t2 = time.perf_counter()
+    return QbResult(rep.h, x, rep, t1 - t0, t2 - t1)
+
+
+def residual_fro(a, h, x, ctx=None):
+    """(||A - H X||_F, ||A||_F) over row-shards (sketching.cpp:270-271)."""
+    ctx = _ctx(ctx)
+    r, n = C.c_double(), C.c_double()
+    ctx._check(ctx.lib.qlra_residual_fro(ctx.h, C.byref(_qm(a)), C.byref(_qm(h)), C.byref(_qm(x)),
+                                         C.byref(r), C.byref(n)))
+    return r.value, n.value
+
+
+@dataclass
+class OnePassOptions:
+    """== OnePassOptions (sketching.hpp:130-141)."""
+    r: int = 0
+    s: int = -1
+    l: int = -1
+    rangefinder: int = PSEUDO_QR
+    embedding: int = GAUSSIAN
+    density: float = 1.0
+    omega_seed: int = 1
+    psi_seed: int = 2
+    rangefinder_seed: int = DEFAULT_RANGEFINDER_SEED
+    qr_cfg: PseudoQrConfig = field(default_factory=PseudoQrConfig)
+
+
+def resolve_defaults(opts: OnePassOptions) -> OnePassOptions:
+    """sketching.cpp:222-227."""
+    if opts.r < 1:
+        raise ParameterError("one_pass_approx: rank must be >= 1")
+    import copy
+    o = copy.copy(opts)
+    if o.s < 0:
+        o.s = o.r + 5
+    if o.l < 0:
+        o.l = 2 * o.s
+    return o
+
+
+@dataclass
+class OnePassQb:
+    state: SketchState
+    qb: QbResult
+    qb_residual: float | None
+    a_fro: float | None
+    times: dict
+
+
+def one_pass_qb(a, opts: OnePassOptions, ctx=None, row0=0, m_global=None, residual=True) -> OnePassQb:
+    """one_pass_approx (sketching.cpp:250-275) through the QB stage: sketch
+    (one read of A), rangefinder, core solve, and (diagnostic, second read)
+    the QB residual.  Truncation is reported separately."""
+    ctx = _ctx(ctx)
+    o = resolve_defaults(opts)
+    t0 = time.perf_counter()
+    st = make_sketch(a, o.r, o.s, o.l, o.omega_seed, o.psi_seed, o.embedding, o.density, ctx,
+                     row0=row0, m_global=m_global)
+    ctx.synchronize()
+    t1 = time.perf_counter()
+    qb = qb_stage(st, o.rangefinder, o.rangefinder_seed, o.qr_cfg, ctx)
+    res = an = None
+    if residual:
+        res, an = residual_fro(a, qb.h, qb.x, ctx)
+    return OnePassQb(st, qb, res, an, dict(sketch_s=t1 - t0, rangefinder_s=qb.rangefinder_s,
+                                           solve_s=qb.solve_s))
+
+
+def measure_fp64_peak(mode=0, ms=200.0, ctx=None):
+    ctx = _ctx(ctx)
+    t = C.c_double()
+    ctx._check(ctx.lib.qlra_measure_fp64_peak(ctx.h, mode, ms, C.byref(t)))
+    return t.value
+
+
+def sketch_kernel_name():
+    return L.lib().qlra_sketch_kernel_name().decode()

@@ -1,0 +1,110 @@
+"""Property tests of the CPU oracle, ported from the reference test suite
+(proj/tests/test_sketching.cpp, test_rangefinders.cpp, test_quaternion_core.cpp).
+These pin the oracle's restated algorithm; the GPU parity tests then compare
+the device path against this oracle."""
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from tests.helpers import (orthonormality_defect, planted_conditioned_matrix,
+                           planted_matrix_with_sigma, random_gaussian, rel_diff)
+
+
+def test_gen_deterministic_and_slices():  # test_sketching.cpp:18-23, 58-65
+    a = O.gen_test_matrix(O.GAUSSIAN, 8, 6, 123)
+    assert np.array_equal(a, O.gen_test_matrix(O.GAUSSIAN, 8, 6, 123))
+    assert not np.array_equal(a, O.gen_test_matrix(O.GAUSSIAN, 8, 6, 124))
+    full = O.gen_test_matrix(O.SPARSE_GAUSSIAN, 30, 20, 15, 0.3)
+    assert np.array_equal(O.gen_block(O.SPARSE_GAUSSIAN, 30, 20, 15, 10, 25, 0, 20, 0.3), full[:, 10:25])
+    assert np.array_equal(O.gen_block(O.SPARSE_GAUSSIAN, 30, 20, 15, 0, 30, 3, 9, 0.3), full[:, :, 3:9])
+    with pytest.raises(O.OracleError):
+        O.gen_test_matrix(O.SPARSE_GAUSSIAN, 4, 4, 1, 0.0)
+
+
+def test_gaussian_plane_statistics():  # test_sketching.cpp:25-39
+    g = O.gen_test_matrix(O.GAUSSIAN, 200, 100, 7)
+    for p in range(4):
+        assert abs(g[p].mean()) < 0.02
+        assert 0.97 < g[p].var(ddof=1) < 1.03
+
+
+def test_make_sketch_matches_definition_bitwise():  # test_sketching.cpp:67-74
+    a = random_gaussian(20, 15, 33)
+    y, w = O.make_sketch(a, 3, 5, 10, 100, 200)
+    assert np.array_equal(y, O.qmat_mul_ordered(a, O.gen_test_matrix(O.GAUSSIAN, 15, 5, 100)))
+    assert np.array_equal(w, O.qmat_mul_ordered(O.gen_test_matrix(O.GAUSSIAN, 10, 20, 200), a))
+    for r, s, l in ((6, 5, 10), (3, 5, 16)):
+        with pytest.raises(O.OracleError):
+            O.make_sketch(a, r, s, l, 1, 2)
+
+
+def test_row_block_streaming_bitwise_and_threads():  # test_sketching.cpp:120-129
+    a = random_gaussian(40, 30, 39)
+    y, w = O.make_sketch(a, 4, 6, 12, 77, 88)
+    ys, ws = np.zeros_like(y), np.zeros_like(w)
+    for r0 in (0, 10, 20, 30):
+        O.sketch_update_rows(ys, ws, r0, a[:, r0:r0 + 10], 77, 88)
+    assert np.array_equal(ys, y) and np.array_equal(ws, w)
+    yt, wt = O.make_sketch(a, 4, 6, 12, 77, 88, nthreads=4)  # row-parallel: same bits
+    assert np.array_equal(yt, y) and np.array_equal(wt, w)
+
+
+def test_additive_linearity():  # test_sketching.cpp:100-118
+    a1, a2 = random_gaussian(14, 11, 37), random_gaussian(14, 11, 38)
+    yw, ww = O.make_sketch(a1 + a2, 2, 4, 8, 11, 22)
+    yc, wc = np.zeros_like(yw), np.zeros_like(ww)
+    O.sketch_update_rows(yc, wc, 0, a1, 11, 22)
+    O.sketch_update_rows(yc, wc, 0, a2, 11, 22)
+    assert rel_diff(yc, yw) < 1e-12 and rel_diff(wc, ww) < 1e-12
+
+
+def test_ordered_vs_plane_gemm():  # test_quaternion_core.cpp:98-104
+    a, b = random_gaussian(7, 9, 21), random_gaussian(9, 4, 22)
+    assert rel_diff(O.qmat_mul_ordered(a, b), O.qmat_mul(a, b)) < 1e-13
+
+
+def test_pseudo_qr_orthonormal_pass_through():  # test_rangefinders.cpp:18-24
+    y = O.orthonormal_range(random_gaussian(20, 5, 51))
+    rep = O.pseudo_qr(y)
+    assert rel_diff(rep["h"], y) < 1e-12
+    assert rep["correction_steps_used"] == 0
+    assert abs(rep["kappa_after"] - 1.0) < 1e-10
+
+
+def test_pseudo_qr_kappa_1e6():  # test_rangefinders.cpp:35-41
+    from tests.helpers import largest_principal_angle
+    y = planted_conditioned_matrix(200, 20, 1e6, 52)
+    rep = O.pseudo_qr(y)
+    assert rep["kappa_after"] < 10.0 and rep["correction_steps_used"] <= 3
+    assert largest_principal_angle(rep["h"], y) < 1e-8
+
+
+def test_pseudo_qr_rank_deficient():  # test_rangefinders.cpp:43-52
+    y = random_gaussian(12, 3, 53)
+    yy = np.concatenate([y, y[:, :, 1:2]], axis=2)
+    with pytest.raises(O.OracleError) as e:
+        O.pseudo_qr(yy)
+    assert e.value.kind == "RankError"
+    with pytest.raises(O.OracleError) as e:
+        O.pseudo_qr(random_gaussian(3, 5, 54))
+    assert e.value.kind == "ParameterError"
+
+
+def test_pseudo_svd_paths():  # test_rangefinders.cpp:105-141
+    y = planted_matrix_with_sigma(100, [0.7 ** i for i in range(10)], 59)
+    rep = O.pseudo_svd(y)
+    assert orthonormality_defect(rep["h"]) < 1e-10
+    proj = O.qmat_mul(rep["h"], O.qmat_mul(O.adjoint(rep["h"]), y))
+    assert rel_diff(proj, y) < 1e-10
+    y2 = planted_matrix_with_sigma(80, [1, 1, 1, 1, 1, 1, 0.5, 0.25], 62)
+    assert orthonormality_defect(O.pseudo_svd(y2)["h"]) < 1e-8
+
+
+def test_qb_exact_rank_recovered():  # test_sketching.cpp:185-195
+    a = planted_matrix_with_sigma(25, [3, 2.5, 2, 1.5, 1], 43)
+    right = O.orthonormal_range(random_gaussian(20, 5, 44))
+    wide = O.qmat_mul(a, O.adjoint(right))
+    y, w = O.make_sketch(wide, 5, 5, 10, 45, 46)
+    qb = O.qb_stage(y, w, 46, O.PSEUDO_QR)
+    res, an = O.residual_sq(wide, qb["h"], qb["x"])
+    assert np.sqrt(res) <= 1e-8 * np.sqrt(an)
