@@ -185,7 +185,7 @@ def main():
         nccl_id = obj[0]
     ctx = Q.Context(local, rank, world, nccl_id)
     Q.set_default_context(ctx)
-    r0, r1 = cfg.m * rank // world, cfg.m * (rank + 1) // world
+    r0, r1 = Q.shard_rows(cfg.m, world, rank)
     a = build_matrix(cfg, (r0, r1), ctx)
     torch.cuda.synchronize()
     method = Q.PSEUDO_QR if args.rangefinder == "pseudo_qr" else Q.PSEUDO_SVD

@@ -90,7 +90,9 @@ typedef struct {
 int qlra_ctx_create(qlra_ctx_t** ctx, int device, int rank, int nranks,
                     const void* nccl_unique_id);
 int qlra_ctx_destroy(qlra_ctx_t* ctx);
-/* Use an external cudaStream_t (e.g. torch's current stream); NULL = own. */
+/* Run all further work on an external cudaStream_t (e.g. torch's current
+ * stream); NULL selects the legacy default stream.  The context's own
+ * non-blocking stream (created by qlra_ctx_create) is released. */
 int qlra_ctx_set_stream(qlra_ctx_t* ctx, void* cuda_stream);
 int qlra_ctx_synchronize(qlra_ctx_t* ctx);
 int qlra_nccl_unique_id(void* out_128_bytes);

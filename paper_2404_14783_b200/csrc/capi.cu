@@ -89,14 +89,17 @@ void gram(Ctx& ctx, const QView& h, const QView& g) {
   allreduce_qmat(ctx, g);
 }
 
-// Eigenvalues (descending) of chi_G for a quaternion Hermitian G (s x s).
-std::vector<double> chi_eigs(Ctx& ctx, const QView& g) {
-  const int64_t n = 2 * g.rows;
-  DeviceBuffer chi(ctx, sizeof(double2) * (size_t)(n * n));
-  DeviceBuffer w(ctx, sizeof(double) * (size_t)n);
-  small_chi_from_quat(ctx, g, chi.as<double2>(), n);
-  small_herm_eigvals(ctx, chi.as<double2>(), n, n, w.as<double>());
-  return to_host(ctx, w.as<double>(), (size_t)n);
+// Eigenvalues (descending) of a quaternion Hermitian G (s x s): the s
+// distinct values of chi_G, each of which chi_G carries twice.
+std::vector<double> quat_eigs(Ctx& ctx, const QView& g, bool extremes_only = true) {
+  const int64_t n = g.rows;
+  DevQMat work(ctx, n, n);
+  copy_qmat(ctx, g, work.v);
+  DeviceBuffer w(ctx, sizeof(double) * (size_t)std::max<int64_t>(1, n));
+  QLRA_CUDA(cudaMemsetAsync(w.ptr, 0, w.bytes, ctx.stream));
+  small_quat_herm_eigvals(ctx, work.v, w.as<double>(), extremes_only);
+  std::vector<double> ev = to_host(ctx, w.as<double>(), (size_t)n);
+  return ev;
 }
 
 double kappa_from_eigs(const std::vector<double>& ev) {
@@ -108,12 +111,12 @@ double kappa_from_eigs(const std::vector<double>& ev) {
 
 // Explicit quaternion inverse of a square matrix via Gauss-Jordan; returns
 // the GJ status (info, pmin, pmax).
-std::vector<double> quat_inverse(Ctx& ctx, const QView& a, const QView& ainv) {
+std::vector<double> quat_inverse(Ctx& ctx, const QView& a, const QView& ainv, bool hpd = false) {
   DevQMat work(ctx, a.rows, a.cols);
   copy_qmat(ctx, a, work.v);
   small_set_identity(ctx, ainv);
   DeviceBuffer st(ctx, 3 * sizeof(double));
-  small_quat_solve(ctx, work.v, ainv, st.as<double>());
+  small_quat_solve(ctx, work.v, ainv, st.as<double>(), /*pivot=*/!hpd);
   return to_host(ctx, st.as<double>(), 3);
 }
 
@@ -179,10 +182,8 @@ bool cholesky_qr(Ctx& ctx, const QView& y, const QView& h, bool complex_mode, in
   if (!cqr_pass(ctx, t2.v, h, complex_mode, 0.0, &d3, nullptr)) return false;
   if (rdiag) {
     rdiag->resize(s);
-    // R = R3 R2 R1 where R1 is the shifted factor: its diagonal overstates the
-    // true R by the shift; the product below is the diagonal of the R that
-    // maps h back onto y only when the shift is negligible, which is exactly
-    // the regime the rank test cares about (small pivots stay small).
+    // y = t1 R1 = t2 R2 R1 = h R3 R2 R1 holds exactly whatever the shift, so
+    // R = R3 R2 R1 is a QR factor of y and its diagonal is the product.
     for (int64_t k = 0; k < s; ++k) (*rdiag)[k] = d1[k] * d2[k] * d3[k];
   }
   return true;
@@ -204,43 +205,42 @@ double condition_number_dev(Ctx& ctx, const QView& a) {
   if (k == 0) return std::numeric_limits<double>::infinity();
   DevQMat g(ctx, a.cols, a.cols);
   gram(ctx, a, g.v);
-  return kappa_from_eigs(chi_eigs(ctx, g.v));
+  return kappa_from_eigs(quat_eigs(ctx, g.v));
 }
 
-double estimate_epsilon_from_gram(Ctx& ctx, const QView& g, double kappa_h, int iters) {
-  if (iters < 1) fail(QLRA_ERR_PARAMETER, "estimate_epsilon: power_iters must be >= 1");
-  // rcond(chi_G) = 1/kappa(H)^2 must exceed 1e-15 (rangefinders.cpp:72-75).
+// Explicit inverse of the Hermitian positive definite Gram G = H^*H, after
+// the reference's singularity test: rcond(chi_G) = 1/kappa(H)^2 must exceed
+// `rc_min` (1e-15 in estimate_epsilon, rangefinders.cpp:72-75; 1e-14 in the
+// square solve of correction_step, complex_bridge.cpp:73-77).
+void check_gram_rcond(double kappa_h, double rc_min, const char* msg) {
   const double rc = std::isfinite(kappa_h) ? 1.0 / (kappa_h * kappa_h) : 0.0;
-  if (!(rc > 1e-15))
-    fail(QLRA_ERR_SINGULAR, "estimate_epsilon: H*H numerically singular",
-         rc > 0 ? 1.0 / rc : std::numeric_limits<double>::infinity());
+  if (!(rc > rc_min))
+    fail(QLRA_ERR_SINGULAR, msg, rc > 0 ? 1.0 / rc : std::numeric_limits<double>::infinity());
+}
+DevQMat gram_inverse(Ctx& ctx, const QView& g, double kappa_h, double rc_min, const char* msg) {
+  check_gram_rcond(kappa_h, rc_min, msg);
   DevQMat ginv(ctx, g.rows, g.cols);
-  const std::vector<double> st = quat_inverse(ctx, g, ginv.v);
-  if (st[0] != 0.0)
-    fail(QLRA_ERR_SINGULAR, "estimate_epsilon: H*H numerically singular",
-         std::numeric_limits<double>::infinity());
+  const std::vector<double> st = quat_inverse(ctx, g, ginv.v, /*hpd=*/true);
+  if (st[0] != 0.0) fail(QLRA_ERR_SINGULAR, msg, std::numeric_limits<double>::infinity());
+  return ginv;
+}
+
+// estimate_epsilon (rangefinders.cpp:66-97) given G^{-1}.
+double estimate_epsilon_from_inverse(Ctx& ctx, const QView& ginv, int iters) {
+  if (iters < 1) fail(QLRA_ERR_PARAMETER, "estimate_epsilon: power_iters must be >= 1");
   DeviceBuffer rho(ctx, sizeof(double));
-  small_power_iter_inverse(ctx, ginv.v, iters, rho.as<double>());
+  small_power_iter_inverse(ctx, ginv, iters, rho.as<double>());
   const double r = to_host(ctx, rho.as<double>(), 1)[0];
   if (!(r > 0.0)) fail(QLRA_ERR_SINGULAR, "estimate_epsilon: breakdown", 0.0);
   return std::min(1.0 / std::sqrt(r), kEpsilonClamp);
 }
 
 // H_out = H ((1-eps) I + eps G^{-1}) == (1-eps) H + eps (H^+)^*  (rangefinders.cpp:99-105)
-void correction_from_gram(Ctx& ctx, const QView& h, const QView& g, double kappa_h, double eps,
-                          const QView& hout) {
+void correction_from_inverse(Ctx& ctx, const QView& h, const QView& ginv, double eps,
+                             const QView& hout) {
   if (!(eps > 0.0 && eps < 1.0)) fail(QLRA_ERR_PARAMETER, "correction_step: epsilon must lie in (0,1)");
-  const double rc = std::isfinite(kappa_h) ? 1.0 / (kappa_h * kappa_h) : 0.0;
-  if (!(rc > 1e-14))
-    fail(QLRA_ERR_SINGULAR, "solve_quaternion_linear: singular system",
-         rc > 0 ? 1.0 / rc : std::numeric_limits<double>::infinity());
-  DevQMat ginv(ctx, g.rows, g.cols);
-  const std::vector<double> st = quat_inverse(ctx, g, ginv.v);
-  if (st[0] != 0.0)
-    fail(QLRA_ERR_SINGULAR, "solve_quaternion_linear: singular system",
-         std::numeric_limits<double>::infinity());
-  DevQMat mm(ctx, g.rows, g.cols);
-  small_axpby_identity(ctx, 1.0 - eps, eps, ginv.v, mm.v);
+  DevQMat mm(ctx, ginv.rows, ginv.cols);
+  small_axpby_identity(ctx, 1.0 - eps, eps, ginv, mm.v);
   if (hout.p[0] == h.p[0]) {
     DevQMat tmp(ctx, h.rows, h.cols);
     qgemm(ctx, QLRA_OP_N, QLRA_OP_N, 1.0, h, mm.v, 0.0, tmp.v);
@@ -259,11 +259,11 @@ void lstsq(Ctx& ctx, const QView& p, const QView& b, const QView& x) {
   qgemm(ctx, QLRA_OP_C, QLRA_OP_N, 1.0, p, p, 0.0, g.v);
   // rank test in the spirit of ColPivHouseholderQR |r_min| > 1e-14 |r_max|
   // (complex_bridge.cpp:80-85): kappa(P) from the Gram spectrum.
-  const double kp = kappa_from_eigs(chi_eigs(ctx, g.v));
+  const double kp = kappa_from_eigs(quat_eigs(ctx, g.v));
   if (!(1.0 / kp > 1e-14))
     fail(QLRA_ERR_SINGULAR, "solve_quaternion_linear: rank-deficient system", kp);
   DevQMat ginv(ctx, s, s);
-  const std::vector<double> st = quat_inverse(ctx, g.v, ginv.v);
+  const std::vector<double> st = quat_inverse(ctx, g.v, ginv.v, /*hpd=*/true);
   if (st[0] != 0.0) fail(QLRA_ERR_SINGULAR, "solve_quaternion_linear: rank-deficient system", kp);
   DevQMat c(ctx, s, b.cols);
   qgemm(ctx, QLRA_OP_C, QLRA_OP_N, 1.0, p, b, 0.0, c.v);
@@ -370,12 +370,8 @@ int qlra_ctx_set_stream(qlra_ctx_t* ctx, void* stream) {
       QLRA_CUDA(cudaStreamDestroy(c.stream));
       c.own_stream = false;
     }
-    if (stream) {
-      c.stream = static_cast<cudaStream_t>(stream);
-    } else {
-      QLRA_CUDA(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
-      c.own_stream = true;
-    }
+    // Used as given; NULL is the legacy default stream (torch's default).
+    c.stream = static_cast<cudaStream_t>(stream);
   });
 }
 
@@ -456,7 +452,7 @@ int qlra_condition_number(qlra_ctx_t* ctx, const qlra_qmat_t* h, double* kappa) 
       DevQMat g(c, h->rows, h->rows);
       qgemm(c, QLRA_OP_N, QLRA_OP_C, 1.0, view_of(h), view_of(h), 0.0, g.v);
       *kappa = h->rows == 0 ? std::numeric_limits<double>::infinity()
-                            : kappa_from_eigs(chi_eigs(c, g.v));
+                            : kappa_from_eigs(quat_eigs(c, g.v));
     } else {
       *kappa = condition_number_dev(c, view_of(h));
     }
@@ -474,8 +470,8 @@ int qlra_singular_values(qlra_ctx_t* ctx, const qlra_qmat_t* a, double* sv) {
       qgemm(c, QLRA_OP_N, QLRA_OP_C, 1.0, view_of(a), view_of(a), 0.0, g.v);
     else
       gram(c, view_of(a), g.v);
-    const std::vector<double> ev = chi_eigs(c, g.v);
-    for (int64_t i = 0; i < k; ++i) sv[i] = std::sqrt(std::max(0.0, ev[2 * i]));
+    const std::vector<double> ev = quat_eigs(c, g.v, /*extremes_only=*/false);
+    for (int64_t i = 0; i < k; ++i) sv[i] = std::sqrt(std::max(0.0, ev[i]));
   });
 }
 
@@ -520,8 +516,9 @@ int qlra_estimate_epsilon(qlra_ctx_t* ctx, const qlra_qmat_t* h, int power_iters
     const int64_t s = h->cols;
     DevQMat g(c, s, s);
     gram(c, view_of(h), g.v);
-    const double kh = kappa_from_eigs(chi_eigs(c, g.v));
-    *eps = estimate_epsilon_from_gram(c, g.v, kh, power_iters);
+    const double kh = kappa_from_eigs(quat_eigs(c, g.v));
+    DevQMat ginv = gram_inverse(c, g.v, kh, 1e-15, "estimate_epsilon: H*H numerically singular");
+    *eps = estimate_epsilon_from_inverse(c, ginv.v, power_iters);
   });
 }
 
@@ -534,8 +531,9 @@ int qlra_correction_step(qlra_ctx_t* ctx, const qlra_qmat_t* h, double epsilon, 
     const int64_t s = h->cols;
     DevQMat g(c, s, s);
     gram(c, view_of(h), g.v);
-    const double kh = kappa_from_eigs(chi_eigs(c, g.v));
-    correction_from_gram(c, view_of(h), g.v, kh, epsilon, view_of(hout));
+    const double kh = kappa_from_eigs(quat_eigs(c, g.v));
+    DevQMat ginv = gram_inverse(c, g.v, kh, 1e-14, "solve_quaternion_linear: singular system");
+    correction_from_inverse(c, view_of(h), ginv.v, epsilon, view_of(hout));
   });
 }
 
@@ -563,21 +561,41 @@ int qlra_pseudo_qr(qlra_ctx_t* ctx, const qlra_qmat_t* y, const qlra_pseudo_qr_c
     r.method = QLRA_PSEUDO_QR;
     DevQMat g(c, s, s);
     gram(c, H, g.v);
-    r.kappa_before = kappa_from_eigs(chi_eigs(c, g.v));
+    r.kappa_before = kappa_from_eigs(quat_eigs(c, g.v));
     double kappa = r.kappa_before;
-    DevQMat h0, g0;
+    // Correction steps H_k = H_{k-1} ((1-eps) I + eps G_{k-1}^{-1}) are tracked
+    // as one small product M (s x s) and H_k is formed as H0 * M from the QR
+    // basis H0 (one tall product instead of a chain).  The rounding of that
+    // product still leaks ~u |H0| |M| outside range(H0) (|M| ~ eps/sigma_min^2
+    // reaches 1e4 at C1), so, as the reference does (rangefinders.cpp:142-153),
+    // H is re-projected onto range(H0) = span[Q, J conj Q] -- through a
+    // quaternion-orthonormal basis Q0 of range(H0) (CholeskyQR2):
+    // H <- Q0 (Q0^* H_k).  Measured on C1 this lands within 2e-13 of the
+    // exact-range QB error, where the unprojected H0*M was 2e-10 off.
+    DevQMat h0, mt, mk;
     try {
       while (r.correction_steps_used < cfg.max_correction_steps && kappa > kKappaTarget) {
         if (r.correction_steps_used == 0) {
           h0 = DevQMat(c, H.rows, s);
           copy_qmat(c, H, h0.v);
-          g0 = DevQMat(c, s, s);
-          copy_qmat(c, g.v, g0.v);
+          mt = DevQMat(c, s, s);
+          small_set_identity(c, mt.v);
+          mk = DevQMat(c, s, s);
         }
-        const double eps = estimate_epsilon_from_gram(c, g.v, kappa, cfg.power_iters_for_epsilon);
-        correction_from_gram(c, H, g.v, kappa, eps, H);
+        // one inverse serves estimate_epsilon and correction_step (both
+        // factor the same H^*H, rangefinders.cpp:68,102)
+        check_gram_rcond(kappa, 1e-15, "estimate_epsilon: H*H numerically singular");
+        DevQMat ginv = gram_inverse(c, g.v, kappa, 1e-14, "solve_quaternion_linear: singular system");
+        const double eps = estimate_epsilon_from_inverse(c, ginv.v, cfg.power_iters_for_epsilon);
+        if (!(eps > 0.0 && eps < 1.0))
+          fail(QLRA_ERR_PARAMETER, "correction_step: epsilon must lie in (0,1)");
+        small_axpby_identity(c, 1.0 - eps, eps, ginv.v, mk.v);
+        DevQMat mnew(c, s, s);
+        qgemm(c, QLRA_OP_N, QLRA_OP_N, 1.0, mt.v, mk.v, 0.0, mnew.v);
+        mt = std::move(mnew);
+        qgemm(c, QLRA_OP_N, QLRA_OP_N, 1.0, h0.v, mt.v, 0.0, H);
         gram(c, H, g.v);
-        kappa = kappa_from_eigs(chi_eigs(c, g.v));
+        kappa = kappa_from_eigs(quat_eigs(c, g.v));
         ++r.correction_steps_used;
       }
     } catch (const Status& e) {
@@ -585,21 +603,16 @@ int qlra_pseudo_qr(qlra_ctx_t* ctx, const qlra_qmat_t* y, const qlra_pseudo_qr_c
       fail(QLRA_ERR_RANK, "pseudo_qr: sketch numerically rank-deficient; use pseudo_svd");
     }
     if (r.correction_steps_used > 0) {
-      // Re-project onto range(H0) (= span[Q, J conj Q], rangefinders.cpp:142-153):
-      // H <- H0 (H0^*H0)^{-1} (H0^* H).
-      DevQMat cc(c, s, s), z(c, s, s), g0inv(c, s, s);
-      qgemm(c, QLRA_OP_C, QLRA_OP_N, 1.0, h0.v, H, 0.0, cc.v);
-      allreduce_qmat(c, cc.v);
-      const std::vector<double> st = quat_inverse(c, g0.v, g0inv.v);
-      if (st[0] != 0.0)
+      DevQMat q0(c, H.rows, s), t(c, s, s);
+      if (!cholesky_qr(c, h0.v, q0.v, /*complex_mode=*/false, m, nullptr))
         fail(QLRA_ERR_RANK, "pseudo_qr: sketch numerically rank-deficient; use pseudo_svd");
-      qgemm(c, QLRA_OP_N, QLRA_OP_N, 1.0, g0inv.v, cc.v, 0.0, z.v);
-      qgemm(c, QLRA_OP_N, QLRA_OP_N, 1.0, h0.v, z.v, 0.0, H);
+      qgemm(c, QLRA_OP_C, QLRA_OP_N, 1.0, q0.v, H, 0.0, t.v);
+      allreduce_qmat(c, t.v);
+      qgemm(c, QLRA_OP_N, QLRA_OP_N, 1.0, q0.v, t.v, 0.0, H);
       gram(c, H, g.v);
-      r.kappa_after = kappa_from_eigs(chi_eigs(c, g.v));
-    } else {
-      r.kappa_after = kappa;
+      kappa = kappa_from_eigs(quat_eigs(c, g.v));
     }
+    r.kappa_after = kappa;
     if (rep) *rep = r;
   });
 }

@@ -118,7 +118,10 @@ void small_herm_eigvals(Ctx& ctx, double2* a, int64_t n, int64_t ld, double* d_w
 // Gauss-Jordan with partial pivoting on quaternion A (n x n): B <- A^{-1} B,
 // A destroyed.  d_stat[0] = info (0 ok, k+1 = zero pivot at k),
 // d_stat[1..2] = min/max pivot norm (doubles via reinterpret).
-void small_quat_solve(Ctx& ctx, const QView& a, const QView& b, double* d_stat);
+void small_quat_solve(Ctx& ctx, const QView& a, const QView& b, double* d_stat, bool pivot = true);
+// Eigenvalues (descending, n values) of a quaternion Hermitian matrix (a is
+// destroyed); extremes_only computes only w[0] (max) and w[n-1] (min).
+void small_quat_herm_eigvals(Ctx& ctx, const QView& a, double* d_w, bool extremes_only);
 // ||chi_A||_1 into *d_out (device).
 void small_chi_norm1(Ctx& ctx, const QView& a, double* d_out);
 // out = alpha * I + beta * a   (square)

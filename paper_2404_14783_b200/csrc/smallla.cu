@@ -234,7 +234,7 @@ __device__ int sturm_count(const double* d, const double* e, int64_t n, double x
 }
 
 // Bisection for every eigenvalue; w sorted descending.
-__global__ void k_bisect(const double* d, const double* e, int64_t n, double* w) {
+__global__ void k_bisect(const double* d, const double* e, int64_t n, double* w, int extremes_only) {
   __shared__ double s_lo, s_hi;
   if (threadIdx.x == 0) {
     double lo = d[0], hi = d[0];
@@ -248,13 +248,16 @@ __global__ void k_bisect(const double* d, const double* e, int64_t n, double* w)
     s_hi = hi + pad;
   }
   __syncthreads();
-  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
-       k += (int64_t)gridDim.x * blockDim.x) {
+  const int64_t cnt = extremes_only ? (n < 2 ? n : 2) : n;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < cnt;
+       q += (int64_t)gridDim.x * blockDim.x) {
     // k-th smallest eigenvalue: smallest x with count(x) > k
+    const int64_t k = extremes_only ? (q == 0 ? 0 : n - 1) : q;
     double lo = s_lo, hi = s_hi;
-    for (int it = 0; it < 200; ++it) {
+    for (int it = 0; it < 2100; ++it) {
       const double mid = 0.5 * (lo + hi);
       if (mid <= lo || mid >= hi) break;
+      if (hi - lo <= 4.4e-16 * fmax(fabs(lo), fabs(hi))) break;
       if (sturm_count(d, e, n, mid) > k) hi = mid; else lo = mid;
     }
     w[n - 1 - k] = 0.5 * (lo + hi);
@@ -262,7 +265,7 @@ __global__ void k_bisect(const double* d, const double* e, int64_t n, double* w)
 }
 
 // Quaternion Gauss-Jordan with partial pivoting (left row operations), one CTA.
-__global__ void __launch_bounds__(SNT) k_quat_gj(QView a, QView b, double* stat, Q4* mult) {
+__global__ void __launch_bounds__(SNT) k_quat_gj(QView a, QView b, double* stat, Q4* mult, int pivot) {
   __shared__ double sh[SNT];
   __shared__ int shi[SNT];
   __shared__ int s_piv;
@@ -271,10 +274,11 @@ __global__ void __launch_bounds__(SNT) k_quat_gj(QView a, QView b, double* stat,
   const int64_t n = a.rows, nb = b.cols;
   double pmin = 1e300, pmax = 0.0;
   for (int64_t k = 0; k < n; ++k) {
-    // pivot search: max |a(i,k)|^2, i >= k, lowest index on ties
+    // pivot search: max |a(i,k)|^2, i >= k, lowest index on ties (HPD
+    // matrices skip it: the diagonal pivot is real positive)
     double best = -1.0;
     int bi = (int)k;
-    for (int64_t i = k + t; i < n; i += blockDim.x) {
+    for (int64_t i = k + t; i < (pivot ? n : k + 1); i += blockDim.x) {
       const Q4 q = qload(a, i, k);
       const double nq = q.w * q.w + q.x * q.x + q.y * q.y + q.z * q.z;
       if (nq > best) { best = nq; bi = (int)i; }
@@ -282,14 +286,16 @@ __global__ void __launch_bounds__(SNT) k_quat_gj(QView a, QView b, double* stat,
     sh[t] = best;
     shi[t] = bi;
     __syncthreads();
-    for (int w = blockDim.x / 2; w > 0; w >>= 1) {
-      if (t < w) {
-        if (sh[t + w] > sh[t] || (sh[t + w] == sh[t] && shi[t + w] < shi[t])) {
-          sh[t] = sh[t + w];
-          shi[t] = shi[t + w];
+    if (pivot) {
+      for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+        if (t < w) {
+          if (sh[t + w] > sh[t] || (sh[t + w] == sh[t] && shi[t + w] < shi[t])) {
+            sh[t] = sh[t + w];
+            shi[t] = shi[t + w];
+          }
         }
+        __syncthreads();
       }
-      __syncthreads();
     }
     if (t == 0) {
       s_piv = shi[0];
@@ -368,7 +374,7 @@ __global__ void k_axpby_identity(double alpha, double beta, QView a, QView out) 
     const int64_t i = e / m, j = e % m;
 #pragma unroll
     for (int p = 0; p < 4; ++p) {
-      double v = beta * a.p[p][i * a.ld + j];
+      double v = beta == 0.0 ? 0.0 : beta * a.p[p][i * a.ld + j];  // never read when beta == 0
       if (p == 0 && i == j) v += alpha;
       out.p[p][i * out.ld + j] = v;
     }
@@ -525,6 +531,104 @@ __global__ void k_add_diag_c(double2* a, int64_t n, int64_t ld, double shift) {
     a[i * ld + i].x += shift;
 }
 
+// Householder tridiagonalisation of a quaternion Hermitian matrix (n x n, full
+// storage, destroyed), one CTA.  Reflector H = I - beta v v^* with
+// v = x + phi*alpha*e1, phi = x1/|x1| (unit quaternion), alpha = ||x||, so
+// H x = -phi alpha e1: the subdiagonal is a quaternion of modulus alpha and a
+// diagonal unitary similarity makes it real, hence e[k] = alpha.  The update
+// H A H = A - v w^* - w v^*, w = p - (beta c/2) v, p = beta A v, c = v^* p
+// (real), is the real-Householder identity with real scalars, valid in the
+// quaternion algebra.  Work is O(n^2) per step: the matvec runs one warp per
+// row (coalesced plane loads, shuffle reduction), the rank-2 update one thread
+// per element.  Eigenvalues of the tridiagonal follow by bisection.
+__global__ void __launch_bounds__(SNT) k_qtridiag(QView a, double* d, double* e) {
+  extern __shared__ __align__(16) unsigned char dsm[];
+  const int64_t n = a.rows;
+  Q4* v = reinterpret_cast<Q4*>(dsm);
+  Q4* pv = v + n;
+  __shared__ double sh[SNT];
+  __shared__ double s_alpha, s_ax1, s_beta, s_c;
+  __shared__ Q4 s_phi;
+  const int t = threadIdx.x, lane = t & 31, wid = t >> 5, nw = blockDim.x >> 5;
+  for (int64_t k = 0; k + 1 < n; ++k) {
+    const int64_t len = n - k - 1, o = k + 1;
+    double part = 0.0;
+    for (int64_t i = t; i < len; i += blockDim.x) {
+      const Q4 q = qload(a, o + i, k);
+      part += q.w * q.w + q.x * q.x + q.y * q.y + q.z * q.z;
+    }
+    const double nrm2 = block_sum(part, sh);
+    if (t == 0) {
+      const Q4 x1 = qload(a, o, k);
+      const double ax1 = sqrt(x1.w * x1.w + x1.x * x1.x + x1.y * x1.y + x1.z * x1.z);
+      const double alpha = sqrt(nrm2);
+      s_alpha = alpha;
+      s_ax1 = ax1;
+      s_phi = ax1 > 0.0 ? Q4{x1.w / ax1, x1.x / ax1, x1.y / ax1, x1.z / ax1} : Q4{1.0, 0.0, 0.0, 0.0};
+      e[k] = alpha;
+      s_beta = alpha > 0.0 ? 2.0 / (2.0 * alpha * alpha + 2.0 * alpha * ax1) : 0.0;
+    }
+    __syncthreads();
+    const double beta = s_beta;
+    if (beta == 0.0) continue;  // column already reduced
+    for (int64_t i = t; i < len; i += blockDim.x) {
+      Q4 q = qload(a, o + i, k);
+      if (i == 0) {
+        q.w += s_phi.w * s_alpha; q.x += s_phi.x * s_alpha;
+        q.y += s_phi.y * s_alpha; q.z += s_phi.z * s_alpha;
+      }
+      v[i] = q;
+    }
+    __syncthreads();
+    // p = beta * A22 v  (warp per row)
+    for (int64_t r = wid; r < len; r += nw) {
+      Q4 acc{0.0, 0.0, 0.0, 0.0};
+      const int64_t row = (o + r) * a.ld + o;
+      for (int64_t c = lane; c < len; c += 32) {
+        const Q4 av{a.p[0][row + c], a.p[1][row + c], a.p[2][row + c], a.p[3][row + c]};
+        const Q4 pq = qmul(av, v[c]);
+        acc.w += pq.w; acc.x += pq.x; acc.y += pq.y; acc.z += pq.z;
+      }
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) {
+        acc.w += __shfl_xor_sync(0xffffffffu, acc.w, off);
+        acc.x += __shfl_xor_sync(0xffffffffu, acc.x, off);
+        acc.y += __shfl_xor_sync(0xffffffffu, acc.y, off);
+        acc.z += __shfl_xor_sync(0xffffffffu, acc.z, off);
+      }
+      if (lane == 0) pv[r] = Q4{beta * acc.w, beta * acc.x, beta * acc.y, beta * acc.z};
+    }
+    __syncthreads();
+    // c = Re(v^* p)
+    double cp = 0.0;
+    for (int64_t i = t; i < len; i += blockDim.x)
+      cp += v[i].w * pv[i].w + v[i].x * pv[i].x + v[i].y * pv[i].y + v[i].z * pv[i].z;
+    const double c = block_sum(cp, sh);
+    const double hk = 0.5 * beta * c;
+    for (int64_t i = t; i < len; i += blockDim.x) {
+      const Q4 q = pv[i], vi = v[i];
+      pv[i] = Q4{q.w - hk * vi.w, q.x - hk * vi.x, q.y - hk * vi.y, q.z - hk * vi.z};
+    }
+    __syncthreads();
+    // A22 -= v w^* + w v^*
+    for (int64_t q = t; q < len * len; q += blockDim.x) {
+      const int64_t r = q / len, cc = q % len;
+      const Q4 vr = v[r], wr = pv[r];
+      Q4 wc = pv[cc], vc = v[cc];
+      wc.x = -wc.x; wc.y = -wc.y; wc.z = -wc.z;
+      vc.x = -vc.x; vc.y = -vc.y; vc.z = -vc.z;
+      const Q4 t1 = qmul(vr, wc), t2 = qmul(wr, vc);
+      const int64_t off = (o + r) * a.ld + o + cc;
+      a.p[0][off] -= t1.w + t2.w;
+      a.p[1][off] -= t1.x + t2.x;
+      a.p[2][off] -= t1.y + t2.y;
+      a.p[3][off] -= t1.z + t2.z;
+    }
+    __syncthreads();
+  }
+  for (int64_t i = t; i < n; i += blockDim.x) d[i] = a.p[0][i * a.ld + i];
+}
+
 unsigned grid_for(int64_t total) {
   int64_t b = (total + 255) / 256;
   if (b < 1) b = 1;
@@ -565,13 +669,37 @@ void small_herm_eigvals(Ctx& ctx, double2* a, int64_t n, int64_t ld, double* d_w
   k_tridiag<<<1, SNT, 0, ctx.stream>>>(a, n, ld, d, e, work.as<double2>());
   QLRA_LAUNCH_CHECK();
   count_launch();
-  k_bisect<<<(unsigned)((n + 255) / 256), 256, 0, ctx.stream>>>(d, e, n, d_w);
+  k_bisect<<<(unsigned)((n + 255) / 256), 256, 0, ctx.stream>>>(d, e, n, d_w, 0);
   QLRA_LAUNCH_CHECK();
   count_launch();
 }
-void small_quat_solve(Ctx& ctx, const QView& a, const QView& b, double* d_stat) {
+void small_quat_herm_eigvals(Ctx& ctx, const QView& a, double* d_w, bool extremes_only) {
+  const int64_t n = a.rows;
+  if (n == 0) return;
+  DeviceBuffer de(ctx, sizeof(double) * (2 * n + 1));
+  double* d = de.as<double>();
+  double* e = d + n;
+  const size_t smem = sizeof(double) * 8 * (size_t)n;
+  static size_t attr = 0;
+  if (smem > 48 * 1024 && smem > attr) {
+    QLRA_CUDA(cudaFuncSetAttribute(k_qtridiag, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = smem;
+  }
+  k_qtridiag<<<1, SNT, smem, ctx.stream>>>(a, d, e);
+  QLRA_LAUNCH_CHECK();
+  count_launch();
+  if (extremes_only) {
+    // w[0] = max, w[n-1] = min; the middle stays untouched
+    k_bisect<<<1, 32, 0, ctx.stream>>>(d, e, n, d_w, 1);
+  } else {
+    k_bisect<<<(unsigned)((n + 255) / 256), 256, 0, ctx.stream>>>(d, e, n, d_w, 0);
+  }
+  QLRA_LAUNCH_CHECK();
+  count_launch();
+}
+void small_quat_solve(Ctx& ctx, const QView& a, const QView& b, double* d_stat, bool pivot) {
   DeviceBuffer mult(ctx, sizeof(double) * 4 * std::max<int64_t>(1, a.rows));
-  k_quat_gj<<<1, SNT, 0, ctx.stream>>>(a, b, d_stat, mult.as<Q4>());
+  k_quat_gj<<<1, SNT, 0, ctx.stream>>>(a, b, d_stat, mult.as<Q4>(), pivot ? 1 : 0);
   QLRA_LAUNCH_CHECK();
   count_launch();
 }

@@ -233,6 +233,14 @@ class SketchState:
         return self.w.shape[2]
 
 
+def shard_rows(m: int, world: int, rank: int) -> tuple[int, int]:
+    """Rows [r0, r1) of A (and Y, H) owned by `rank` of `world`:
+    contiguous, balanced to within one row, ordered by rank."""
+    if not (0 <= rank < world):
+        raise ParameterError("shard_rows: rank out of range")
+    return m * rank // world, m * (rank + 1) // world
+
+
 def validate_sketch_sizes(m, n, r, s, l):
     if r < 1 or not (r <= s <= l <= min(m, n)):
         raise ParameterError("sketch sizes must satisfy 1 <= r <= s <= l <= min(m,n)")
