@@ -94,6 +94,11 @@ void launch_gen(cudaStream_t st, const qlra_spec_t& spec, int64_t r0, int64_t c0
 // ------------------------------------------------------------ qgemm.cu ---
 void qgemm(Ctx& ctx, int op_a, int op_b, double alpha, const QView& A, const QView& B,
            double beta, const QView& C, int force_splits = 0);
+// Split count filling whole waves for `tiles` 64x64 tiles over K (plus
+// `other_ctas` CTAs sharing the launch).
+int64_t choose_splits(int64_t tiles, int64_t K, int64_t other_ctas);
+// C = alpha * sum_{z<nz} ws[z] + beta * C  (ws: [nz][4][rows][cols], fixed order)
+void splitk_reduce(Ctx& ctx, const double* ws, int nz, const QView& C, double alpha, double beta);
 // d_out2[0] = ||R - H X||_F^2, d_out2[1] = ||R||_F^2 (device pointer)
 void qgemm_residual(Ctx& ctx, const QView& R, const QView& H, const QView& X, double* d_out2);
 

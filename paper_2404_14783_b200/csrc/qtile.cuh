@@ -1,0 +1,202 @@
+// qtile.cuh -- the quaternion tile engine on the FP64 tensor pipe (DMMA).
+//
+// One CTA (512 threads, 16 warps) computes a 64x64 quaternion tile
+//   acc += op(A)[i0:i0+64, kbeg:kend] * op(B)[kbeg:kend, j0:j0+64]
+// with `mma.sync.aligned.m8n8k4.row.col.f64` (SASS DMMA.8x8x4; tcgen05 has
+// no f64 kind).  A quaternion MAC is 16 real products
+// (proj/include/qlra/quaternion.hpp:33-38); output plane p is
+// sum_q sign(p,q) * A_q * B_perm(p,q).  Each warp keeps + and - copies of the
+// B fragments it needs, so every one of the 16 products is a plain DMMA and
+// conjugation of either operand (op = adjoint) only changes which copy is
+// selected -- no extra instructions.
+//
+// Warp layout: 4 (rows) x 4 (cols) warps, each owning a 16x16 quaternion
+// sub-tile = 2x2 blocks of 8x8 per plane: 32 FP64 accumulators per thread
+// (16 warps per SM keep the DMMA pipe fed).
+// Operands are staged by cp.async into a 3-stage shared-memory ring in the
+// layout of their contiguous global dimension (k-fast rows padded to 10
+// doubles, i/j-fast rows to 72), which makes every fragment read a
+// 2-wavefront (conflict-free-optimal) LDS.64.
+#pragma once
+
+#include "common.cuh"
+
+namespace qlra_dev {
+namespace qt {
+
+constexpr int BM = 64, BN = 64, BK = 8, NT = 512, STAGES = 3;
+constexpr int WRB = 2, WCB = 2;  // 8x8 blocks per warp (warp tile 16x16, 4x4 warps)
+constexpr int LDK = BK + 2;    // k-fast rows: [x][k]
+constexpr int LDX = BM + 8;    // i/j-fast rows: [k][x]
+constexpr int OP_STAGE = 4 * BM * LDK > 4 * BK * LDX ? 4 * BM * LDK : 4 * BK * LDX;  // doubles
+constexpr int STAGE = 2 * OP_STAGE;
+constexpr size_t SMEM_BYTES = (size_t)STAGES * STAGE * sizeof(double);
+
+// op(A)(i, k) = a[q][i * a_si + k * a_sk];  op(B)(k, j) = b[q][k * b_sk + j * b_sj]
+struct Operands {
+  const double* a[4];
+  const double* b[4];
+  int64_t a_si, a_sk, b_sk, b_sj;
+  int64_t M, N;
+};
+
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool pred) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  const int n = pred ? 8 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(n) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+__device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+
+// AK: op(A) is k-fast in memory (a_sk == 1), smem [q][i][k]; else [q][k][i].
+// BJ: op(B) is j-fast (b_sj == 1), smem [q][k][j]; else [q][j][k].
+template <bool AK, bool BJ>
+__device__ __forceinline__ void load_stage(const Operands& g, double* As, double* Bs, int64_t i0,
+                                           int64_t j0, int64_t k0, int64_t kend, int tid) {
+#pragma unroll
+  for (int r = 0; r < 2048 / NT; ++r) {
+    const int e = tid + NT * r;  // 0..2047 = 4 planes x 64 x 8
+    const int q = e >> 9, idx = e & 511;
+    int x, k;
+    if (AK) { x = idx >> 3; k = idx & 7; } else { x = idx & 63; k = idx >> 6; }
+    const int64_t gi = i0 + x, gk = k0 + k;
+    const bool ok = gi < g.M && gk < kend;
+    const double* src = ok ? g.a[q] + gi * g.a_si + gk * g.a_sk : g.a[q];
+    double* dst = AK ? As + (q * BM + x) * LDK + k : As + (q * BK + k) * LDX + x;
+    cp_async8(dst, src, ok);
+  }
+#pragma unroll
+  for (int r = 0; r < 2048 / NT; ++r) {
+    const int e = tid + NT * r;
+    const int q = e >> 9, idx = e & 511;
+    int x, k;
+    if (BJ) { x = idx & 63; k = idx >> 6; } else { x = idx >> 3; k = idx & 7; }
+    const int64_t gj = j0 + x, gk = k0 + k;
+    const bool ok = gj < g.N && gk < kend;
+    const double* src = ok ? g.b[q] + gk * g.b_sk + gj * g.b_sj : g.b[q];
+    double* dst = BJ ? Bs + (q * BK + k) * LDX + x : Bs + (q * BN + x) * LDK + k;
+    cp_async8(dst, src, ok);
+  }
+}
+
+// Accumulator fragment: acc[rb][cb][p][0..1] = C_p[row][col..col+1] with
+// row = i0 + 16*wr + 8*rb + lane/4, col = j0 + 16*wc + 8*cb + 2*(lane%4).
+using Acc = double[WRB][WCB][4][2];
+
+__device__ __forceinline__ void zero_acc(Acc& acc) {
+#pragma unroll
+  for (int rb = 0; rb < WRB; ++rb)
+#pragma unroll
+    for (int cb = 0; cb < WCB; ++cb)
+#pragma unroll
+      for (int p = 0; p < 4; ++p) acc[rb][cb][p][0] = acc[rb][cb][p][1] = 0.0;
+}
+
+__device__ __forceinline__ int acc_row(int rb) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  return 16 * (w >> 2) + 8 * rb + (lane >> 2);
+}
+__device__ __forceinline__ int acc_col(int cb) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  return 16 * (w & 3) + 8 * cb + 2 * (lane & 3);
+}
+
+// Hamilton table in (term q, output plane p) -> (B plane, sign):
+//   q=0 (a_w): +bw +bx +by +bz      q=1 (a_x): -bx +bw -bz +by
+//   q=2 (a_y): -by +bz +bw -bx      q=3 (a_z): -bz -by +bx +bw
+__device__ __forceinline__ constexpr int hplane(int q, int p) {
+  return q == 0 ? p : q == 1 ? (p == 0 ? 1 : p == 1 ? 0 : p == 2 ? 3 : 2)
+                    : q == 2 ? (p == 0 ? 2 : p == 1 ? 3 : p == 2 ? 0 : 1)
+                             : (p == 0 ? 3 : p == 1 ? 2 : p == 2 ? 1 : 0);
+}
+__device__ __forceinline__ constexpr int hsign(int q, int p) {
+  return q == 0 ? 1 : q == 1 ? (p == 0 || p == 2 ? -1 : 1)
+                    : q == 2 ? (p == 0 || p == 3 ? -1 : 1)
+                             : (p == 0 || p == 1 ? -1 : 1);
+}
+
+// acc += op(A) op(B) over k in [kbeg, kend).  CA/CB: op = adjoint, which
+// requires the i-fast / k-fast layouts (AK = !CA, BJ = !CB).  The caller must
+// __syncthreads() between successive calls that reuse `smem`.
+template <bool CA, bool CB>
+__device__ __forceinline__ void mma_tile(const Operands& g, double* smem, int64_t i0, int64_t j0,
+                                         int64_t kbeg, int64_t kend, Acc& acc) {
+  constexpr bool AK = !CA, BJ = !CB;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int wr = w >> 2, wc = w & 3;
+  const int gid = lane >> 2, tig = lane & 3;
+  const int nk = kend > kbeg ? (int)((kend - kbeg + BK - 1) / BK) : 0;
+
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < nk)
+      load_stage<AK, BJ>(g, smem + s * STAGE, smem + s * STAGE + OP_STAGE, i0, j0, kbeg + s * BK, kend, tid);
+    cp_async_commit();
+  }
+  for (int kt = 0; kt < nk; ++kt) {
+    cp_async_wait<STAGES - 2>();
+    __syncthreads();
+    {
+      const int nxt = kt + STAGES - 1;
+      if (nxt < nk) {
+        const int s = nxt % STAGES;
+        load_stage<AK, BJ>(g, smem + s * STAGE, smem + s * STAGE + OP_STAGE, i0, j0,
+                           kbeg + (int64_t)nxt * BK, kend, tid);
+      }
+      cp_async_commit();
+    }
+    const double* As = smem + (kt % STAGES) * STAGE;
+    const double* Bs = As + OP_STAGE;
+#pragma unroll
+    for (int kk = 0; kk < BK / 4; ++kk) {
+      const int k = 4 * kk + tig;
+      double a[WRB][4];  // [rb][q]
+#pragma unroll
+      for (int rb = 0; rb < WRB; ++rb) {
+        const int x = 16 * wr + 8 * rb + gid;
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          a[rb][q] = AK ? As[(q * BM + x) * LDK + k] : As[(q * BK + k) * LDX + x];
+      }
+      double bp[WCB][4], bn[WCB][4];  // + and - copies, [cb][plane]
+#pragma unroll
+      for (int cb = 0; cb < WCB; ++cb) {
+        const int x = 16 * wc + 8 * cb + gid;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          bp[cb][q] = BJ ? Bs[(q * BK + k) * LDX + x] : Bs[(q * BN + x) * LDK + k];
+          bn[cb][q] = -bp[cb][q];
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int rb = 0; rb < WRB; ++rb)
+#pragma unroll
+          for (int cb = 0; cb < WCB; ++cb)
+#pragma unroll
+            for (int p = 0; p < 4; ++p) {
+              const int bq = hplane(q, p);
+              // conj(A): a_x,y,z negated -> flip terms q >= 1;
+              // conj(B): b_x,y,z negated -> flip when the B plane is not w.
+              int sg = hsign(q, p);
+              if (CA && q > 0) sg = -sg;
+              if (CB && bq > 0) sg = -sg;
+              dmma(acc[rb][cb][p], a[rb][q], sg > 0 ? bp[cb][bq] : bn[cb][bq]);
+            }
+    }
+  }
+  cp_async_wait<0>();
+}
+
+}  // namespace qt
+}  // namespace qlra_dev

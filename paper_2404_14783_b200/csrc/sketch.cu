@@ -1,28 +1,196 @@
-// sketch.cu -- K1+K2: the dual sketch Y += A Omega, W += Psi A.
+// sketch.cu -- K1+K2: the fused dual sketch  Y += A Omega,  W += Psi A.
 //
-// Replaces sketch_update_rows (proj/src/sketching.cpp:125-139), i.e.
+// Replaces sketch_update_rows (proj/src/sketching.cpp:125-139):
 // gen_test_matrix(Omega) + qmat_mul_accumulate_ordered(Y, A, Omega) +
 // gen_test_matrix_cols(Psi, rows) + qmat_mul_accumulate_ordered(W, Psi, A).
 //
-// v1 layout: Omega (n x s) and the Psi column slice (l x b) are generated into
-// HBM by K1 and both products run on the DFMA quaternion GEMM.
+// The block of A is walked in row panels sized to stay resident in the 126 MB
+// L2.  Each panel is ONE launch of sketch_fused_kernel whose CTAs are either
+// Y-tasks (64x64 tile of Y_panel = A_panel * Omega over a K-chunk of the n
+// columns) or W-tasks (64x64 tile of W += Psi[:, panel] * A_panel over a
+// chunk of the panel rows), both on the DMMA tile core (qtile.cuh).  The
+// panel is read from HBM once and re-served from L2 to every task that
+// stages it, so HBM traffic for A is 32*m*n bytes -- the "A is read once"
+// contract of the one-pass method.  Split-K partials
+// go to workspaces reduced in fixed order afterwards: deterministic, no
+// atomics.  Omega (n x s) and the Psi column slice (l x b) are generated on
+// device by K1 (embed.cu) from the reference's counter RNG.
 #include "common.cuh"
 #include "kernels.cuh"
+#include "qtile.cuh"
 
 namespace qlra_dev {
 
-const char* sketch_kernel_name() { return "qgemm_dfma_64x64x8_v1"; }
+namespace {
+
+using qt::BK;
+using qt::BM;
+using qt::BN;
+using qt::NT;
+
+struct FusedArgs {
+  qt::Operands yop;  // A_panel (k-fast) x Omega (j-fast): M = panel rows, N = s, K = n
+  qt::Operands wop;  // Psi_panel (k-fast) x A_panel (j-fast): M = l, N = n, K = panel rows
+  int64_t ky, kw;    // K extents
+  int y_tm, y_tn, zy;
+  int64_t ky_chunk;
+  int w_tm, w_tn, zw;
+  int64_t kw_chunk;
+  double* y[4];
+  int64_t ldy;
+  double* yp;  // [zy][4][My][Ny] partials when zy > 1
+  double* w[4];
+  int64_t ldw;
+  double* wp;  // [zw][4][l][n] partials when zw > 1
+};
+
+__device__ __forceinline__ void store_tile(const qt::Acc& acc, int64_t i0, int64_t j0, int64_t M,
+                                           int64_t N, double* const* c, int64_t ldc,
+                                           double* part, bool rmw) {
+#pragma unroll
+  for (int rb = 0; rb < qt::WRB; ++rb) {
+    const int64_t gi = i0 + qt::acc_row(rb);
+    if (gi >= M) continue;
+#pragma unroll
+    for (int cb = 0; cb < qt::WCB; ++cb)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int64_t gj = j0 + qt::acc_col(cb) + h;
+        if (gj >= N) continue;
+        if (part) {
+#pragma unroll
+          for (int p = 0; p < 4; ++p) part[(int64_t)p * M * N + gi * N + gj] = acc[rb][cb][p][h];
+        } else {
+#pragma unroll
+          for (int p = 0; p < 4; ++p) {
+            double* dst = c[p] + gi * ldc + gj;
+            *dst = rmw ? *dst + acc[rb][cb][p][h] : acc[rb][cb][p][h];
+          }
+        }
+      }
+  }
+}
+
+__global__ void __launch_bounds__(NT, 1) sketch_fused_kernel(FusedArgs f) {
+  extern __shared__ __align__(16) double smem[];
+  qt::Acc acc;
+  qt::zero_acc(acc);
+  const int ny = f.y_tm * f.y_tn * f.zy;
+  int t = blockIdx.x;
+  if (t < ny) {
+    const int z = t % f.zy;
+    t /= f.zy;
+    const int tn = t % f.y_tn, tm = t / f.y_tn;
+    const int64_t kb = (int64_t)z * f.ky_chunk, ke = min(f.ky, kb + f.ky_chunk);
+    qt::mma_tile<false, false>(f.yop, smem, (int64_t)tm * BM, (int64_t)tn * BN, kb, ke, acc);
+    double* part = f.zy > 1 ? f.yp + (int64_t)z * 4 * f.yop.M * f.yop.N : nullptr;
+    store_tile(acc, (int64_t)tm * BM, (int64_t)tn * BN, f.yop.M, f.yop.N, f.y, f.ldy, part, true);
+  } else {
+    t -= ny;
+    const int z = t % f.zw;
+    t /= f.zw;
+    const int tm = t % f.w_tm, tn = t / f.w_tm;  // a-tiles fastest: neighbours share A columns
+    const int64_t kb = (int64_t)z * f.kw_chunk, ke = min(f.kw, kb + f.kw_chunk);
+    qt::mma_tile<false, false>(f.wop, smem, (int64_t)tm * BM, (int64_t)tn * BN, kb, ke, acc);
+    double* part = f.zw > 1 ? f.wp + (int64_t)z * 4 * f.wop.M * f.wop.N : nullptr;
+    store_tile(acc, (int64_t)tm * BM, (int64_t)tn * BN, f.wop.M, f.wop.N, f.w, f.ldw, part, true);
+  }
+}
+
+constexpr double kL2Budget = 48e6;  // bytes of A panel kept L2-resident
+
+}  // namespace
+
+const char* sketch_kernel_name() { return "sketch_fused_kernel(dmma_64x64x8,L2-panel)"; }
 
 void sketch_update_rows(Ctx& ctx, const qlra_spec_t& omega, const qlra_spec_t& psi, int64_t row0,
                         const QView& block, const QView& y_rows, const QView& w) {
   const int64_t b = block.rows, n = block.cols, s = omega.cols, l = psi.rows;
-  if (b == 0) return;
+  if (b == 0 || n == 0) return;
+  static bool attr = false;
+  if (!attr) {
+    QLRA_CUDA(cudaFuncSetAttribute(sketch_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)qt::SMEM_BYTES));
+    attr = true;
+  }
   DevQMat om(ctx, n, s);
   launch_gen(ctx.stream, omega, 0, 0, n, s, om.v, false);
-  qgemm(ctx, QLRA_OP_N, QLRA_OP_N, 1.0, block, om.v, 1.0, y_rows);
   DevQMat ps(ctx, l, b);
   launch_gen(ctx.stream, psi, 0, row0, l, b, ps.v, false);
-  qgemm(ctx, QLRA_OP_N, QLRA_OP_N, 1.0, ps.v, block, 1.0, w);
+
+  // Panel rows: L2 budget, multiple of 64, at least 64.
+  int64_t R = (int64_t)(kL2Budget / (32.0 * (double)n));
+  R = std::max<int64_t>(256, (R / 64) * 64);  // >= 256 rows keeps W tasks compute-dense
+  R = std::min<int64_t>(R, ((b + 63) / 64) * 64);
+  const int w_tm = (int)((l + BM - 1) / BM), w_tn = (int)((n + BN - 1) / BN);
+  // Shared partial workspaces sized for the largest panel.
+  DeviceBuffer yp, wp;
+  for (int64_t r0 = 0; r0 < b; r0 += R) {
+    const int64_t rp = std::min(R, b - r0);
+    FusedArgs f{};
+    const QView ap = sub(block, r0, 0, rp, n);
+    const QView yv = sub(y_rows, r0, 0, rp, s);
+    for (int p = 0; p < 4; ++p) {
+      f.yop.a[p] = ap.p[p];
+      f.yop.b[p] = om.v.p[p];
+      f.wop.a[p] = ps.v.p[p] + r0;  // Psi[:, r0:r0+rp]
+      f.wop.b[p] = ap.p[p];
+      f.y[p] = yv.p[p];
+      f.w[p] = w.p[p];
+    }
+    f.yop.a_si = ap.ld; f.yop.a_sk = 1; f.yop.b_sk = om.v.ld; f.yop.b_sj = 1;
+    f.yop.M = rp; f.yop.N = s;
+    f.wop.a_si = ps.v.ld; f.wop.a_sk = 1; f.wop.b_sk = ap.ld; f.wop.b_sj = 1;
+    f.wop.M = l; f.wop.N = n;
+    f.ky = n;
+    f.kw = rp;
+    f.ldy = yv.ld;
+    f.ldw = w.ld;
+    f.y_tm = (int)((rp + BM - 1) / BM);
+    f.y_tn = (int)((s + BN - 1) / BN);
+    f.w_tm = w_tm;
+    f.w_tn = w_tn;
+    // Task lengths (in k-steps) are balanced with a makespan model: every
+    // CTA runs one task, the launch takes ~waves * (longest task), and we
+    // maximise useful work / (148 * waves * longest).  W is split over the
+    // panel rows only when its tiles cannot fill the GPU (C5-like shapes).
+    const int64_t wt = (int64_t)w_tm * w_tn, yt = (int64_t)f.y_tm * f.y_tn;
+    const double work = (double)yt * n + (double)wt * rp;
+    double best = -1.0;
+    int best_zw = 1, best_zy = 1;
+    const int zw_max = wt >= 148 ? 1 : (int)std::max<int64_t>(1, std::min<int64_t>(64, rp / 64));
+    for (int zw = 1; zw <= zw_max; ++zw) {
+      const int64_t kwc = ((rp + zw - 1) / zw + BK - 1) / BK * BK;
+      const int zy_max = (int)std::max<int64_t>(1, std::min<int64_t>(512, n / 32));
+      for (int zy = 1; zy <= zy_max; ++zy) {
+        const int64_t kyc = ((n + zy - 1) / zy + BK - 1) / BK * BK;
+        const int64_t ctas = yt * ((n + kyc - 1) / kyc) + wt * ((rp + kwc - 1) / kwc);
+        const int64_t waves = (ctas + 147) / 148;
+        const double score = work / (148.0 * (double)waves * (double)std::max(kyc, kwc) + 16.0 * ctas);
+        if (score > best) { best = score; best_zw = zw; best_zy = zy; }
+      }
+    }
+    f.kw_chunk = ((rp + best_zw - 1) / best_zw + BK - 1) / BK * BK;
+    f.zw = (int)((rp + f.kw_chunk - 1) / f.kw_chunk);
+    f.ky_chunk = ((n + best_zy - 1) / best_zy + BK - 1) / BK * BK;
+    f.zy = (int)((n + f.ky_chunk - 1) / f.ky_chunk);
+    if (f.zy > 1) {
+      const size_t need = (size_t)f.zy * 4 * rp * s * sizeof(double);
+      if (yp.bytes < need) yp = DeviceBuffer(ctx, need);
+      f.yp = yp.as<double>();
+    }
+    if (f.zw > 1) {
+      const size_t need = (size_t)f.zw * 4 * l * n * sizeof(double);
+      if (wp.bytes < need) wp = DeviceBuffer(ctx, need);
+      f.wp = wp.as<double>();
+    }
+    const int64_t ctas = yt * f.zy + wt * f.zw;
+    sketch_fused_kernel<<<(unsigned)ctas, NT, qt::SMEM_BYTES, ctx.stream>>>(f);
+    QLRA_LAUNCH_CHECK();
+    count_launch();
+    if (f.zy > 1) splitk_reduce(ctx, f.yp, f.zy, yv, 1.0, 1.0);
+    if (f.zw > 1) splitk_reduce(ctx, f.wp, f.zw, w, 1.0, 1.0);
+  }
 }
 
 }  // namespace qlra_dev
