@@ -245,11 +245,12 @@ def main():
         x_host = torch.empty((4, cfg.s, cfg.n), dtype=torch.float64, pin_memory=True)
 
         def e2e_step():
-            ad = a_host.to("cuda", non_blocking=True)
-            _, q = step(ad)
+            # public streaming API: A from pinned host memory, H2D overlapped
+            st = Q.make_sketch_host(a_host, opts.r, opts.s, opts.l, opts.omega_seed, opts.psi_seed,
+                                    cfg.kind, ctx=ctx, row0=r0, m_global=cfg.m)
+            q = Q.qb_stage(st, method, ctx=ctx)
             h_host.copy_(q.h, non_blocking=True)
             x_host.copy_(q.x, non_blocking=True)
-            return ad
 
         for _ in range(max(1, args.warmup // 2)):
             e2e_step()

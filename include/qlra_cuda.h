@@ -121,6 +121,16 @@ int qlra_gen_test_matrix_block(qlra_ctx_t* ctx, const qlra_spec_t* spec, int64_t
 int qlra_sketch_update_rows(qlra_ctx_t* ctx, const qlra_spec_t* omega, const qlra_spec_t* psi,
                             int64_t row0, const qlra_qmat_t* block, qlra_qmat_t* y_rows,
                             qlra_qmat_t* w);
+/* Streaming form of qlra_sketch_update_rows (sketch_from_source,
+ * sketching.cpp:156-167, with the source in host memory): `host_block` holds
+ * HOST plane pointers (pinned memory for full overlap).  Row panels of
+ * `block_rows` rows (0 = automatic) are copied H2D on an internal stream,
+ * double-buffered against the fused sketch of the previous panel, so the
+ * transfer of A overlaps the FP64 work and A is still read exactly once. */
+int qlra_sketch_update_rows_host(qlra_ctx_t* ctx, const qlra_spec_t* omega,
+                                 const qlra_spec_t* psi, int64_t row0,
+                                 const qlra_qmat_t* host_block, qlra_qmat_t* y_rows,
+                                 qlra_qmat_t* w, int64_t block_rows);
 /* Sum of the per-rank W partials (NCCL all-reduce; no-op for one rank). */
 int qlra_sketch_allreduce(qlra_ctx_t* ctx, qlra_qmat_t* w);
 

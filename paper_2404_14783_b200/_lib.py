@@ -57,6 +57,7 @@ def lib():
         "qlra_ctx_launch_count": ([VP], I64),
         "qlra_gen_test_matrix_block": ([VP, PS, I64, I64, PQ], INT),
         "qlra_sketch_update_rows": ([VP, PS, PS, I64, PQ, PQ, PQ], INT),
+        "qlra_sketch_update_rows_host": ([VP, PS, PS, I64, PQ, PQ, PQ, I64], INT),
         "qlra_sketch_allreduce": ([VP, PQ], INT),
         "qlra_qmat_mul": ([VP, INT, INT, F64, PQ, PQ, F64, PQ], INT),
         "qlra_gram": ([VP, PQ, PQ], INT),

@@ -120,6 +120,22 @@ std::vector<double> quat_inverse(Ctx& ctx, const QView& a, const QView& ainv, bo
   return to_host(ctx, st.as<double>(), 3);
 }
 
+// G^{-1} for a Hermitian positive definite quaternion G: G = R^* R
+// (quaternion Cholesky, one CTA), G^{-1} = R^{-1} R^{-*} (triangular inverse,
+// then one small DMMA product).  False if G is not numerically PD.
+bool hpd_inverse(Ctx& ctx, const QView& g, const QView& ginv, std::vector<double>* rdiag) {
+  const int64_t s = g.rows;
+  DevQMat r(ctx, s, s), ri(ctx, s, s);
+  copy_qmat(ctx, g, r.v);
+  DeviceBuffer info(ctx, sizeof(int));
+  small_quat_cholesky(ctx, r.v, info.as<int>());
+  if (info_to_host(ctx, info.as<int>()) != 0) return false;
+  if (rdiag) *rdiag = diag_to_host(ctx, r.v.p[0], r.v.ld, s);
+  small_quat_triinv_upper(ctx, r.v, ri.v);
+  qgemm(ctx, QLRA_OP_N, QLRA_OP_C, 1.0, ri.v, ri.v, 0.0, ginv);
+  return true;
+}
+
 // One CholeskyQR pass: hout = y * R^{-1} with G = gram(y) (+ shift on the
 // diagonal).  complex_mode: R from the complex compact Gram (Y_c^* Y_c, the
 // complex part of the quaternion Gram) -- pseudo-QR's complex_qr; else R is
@@ -220,8 +236,8 @@ void check_gram_rcond(double kappa_h, double rc_min, const char* msg) {
 DevQMat gram_inverse(Ctx& ctx, const QView& g, double kappa_h, double rc_min, const char* msg) {
   check_gram_rcond(kappa_h, rc_min, msg);
   DevQMat ginv(ctx, g.rows, g.cols);
-  const std::vector<double> st = quat_inverse(ctx, g, ginv.v, /*hpd=*/true);
-  if (st[0] != 0.0) fail(QLRA_ERR_SINGULAR, msg, std::numeric_limits<double>::infinity());
+  if (!hpd_inverse(ctx, g, ginv.v, nullptr))
+    fail(QLRA_ERR_SINGULAR, msg, std::numeric_limits<double>::infinity());
   return ginv;
 }
 
@@ -257,14 +273,22 @@ void lstsq(Ctx& ctx, const QView& p, const QView& b, const QView& x) {
   const int64_t s = p.cols;
   DevQMat g(ctx, s, s);
   qgemm(ctx, QLRA_OP_C, QLRA_OP_N, 1.0, p, p, 0.0, g.v);
-  // rank test in the spirit of ColPivHouseholderQR |r_min| > 1e-14 |r_max|
-  // (complex_bridge.cpp:80-85): kappa(P) from the Gram spectrum.
-  const double kp = kappa_from_eigs(quat_eigs(ctx, g.v));
-  if (!(1.0 / kp > 1e-14))
-    fail(QLRA_ERR_SINGULAR, "solve_quaternion_linear: rank-deficient system", kp);
+  // Rank test in the spirit of ColPivHouseholderQR |r_min| > 1e-14 |r_max|
+  // (complex_bridge.cpp:80-85): the Cholesky factor of P^*P is the R of a
+  // QR of P, so its diagonal is tested the same way.
   DevQMat ginv(ctx, s, s);
-  const std::vector<double> st = quat_inverse(ctx, g.v, ginv.v, /*hpd=*/true);
-  if (st[0] != 0.0) fail(QLRA_ERR_SINGULAR, "solve_quaternion_linear: rank-deficient system", kp);
+  std::vector<double> rd;
+  if (!hpd_inverse(ctx, g.v, ginv.v, &rd))
+    fail(QLRA_ERR_SINGULAR, "solve_quaternion_linear: rank-deficient system",
+         std::numeric_limits<double>::infinity());
+  double rmax = 0.0, rmin = std::numeric_limits<double>::infinity();
+  for (double v : rd) {
+    rmax = std::max(rmax, std::fabs(v));
+    rmin = std::min(rmin, std::fabs(v));
+  }
+  if (!(rmin > 1e-14 * rmax))
+    fail(QLRA_ERR_SINGULAR, "solve_quaternion_linear: rank-deficient system",
+         rmin > 0 ? rmax / rmin : std::numeric_limits<double>::infinity());
   DevQMat c(ctx, s, b.cols);
   qgemm(ctx, QLRA_OP_C, QLRA_OP_N, 1.0, p, b, 0.0, c.v);
   qgemm(ctx, QLRA_OP_N, QLRA_OP_N, 1.0, ginv.v, c.v, 0.0, x);
@@ -415,6 +439,29 @@ int qlra_sketch_update_rows(qlra_ctx_t* ctx, const qlra_spec_t* omega, const qlr
     if (row0 < 0 || row0 + block->rows > psi->cols)
       fail(QLRA_ERR_SHAPE, "sketch_update_rows: row range out of bounds");
     sketch_update_rows(c, *omega, *psi, row0, view_of(block), view_of(y_rows), view_of(w));
+  });
+}
+
+int qlra_sketch_update_rows_host(qlra_ctx_t* ctx, const qlra_spec_t* omega,
+                                 const qlra_spec_t* psi, int64_t row0,
+                                 const qlra_qmat_t* host_block, qlra_qmat_t* y_rows,
+                                 qlra_qmat_t* w, int64_t block_rows) {
+  return guarded(ctx, [&](Ctx& c) {
+    validate_spec(omega);
+    validate_spec(psi);
+    check_view(host_block, "sketch_update_rows");
+    check_view(y_rows, "sketch_update_rows");
+    check_view(w, "sketch_update_rows");
+    const int64_t n = w->cols;
+    if (host_block->cols != n || omega->rows != n)
+      fail(QLRA_ERR_SHAPE, "sketch_update_rows: column count mismatch");
+    if (y_rows->rows != host_block->rows || y_rows->cols != omega->cols || w->rows != psi->rows)
+      fail(QLRA_ERR_SHAPE, "sketch_update_rows: sketch shape mismatch");
+    if (row0 < 0 || row0 + host_block->rows > psi->cols)
+      fail(QLRA_ERR_SHAPE, "sketch_update_rows: row range out of bounds");
+    if (block_rows < 0) fail(QLRA_ERR_PARAMETER, "sketch_from_source: block_rows must be >= 1");
+    sketch_update_rows_host(c, *omega, *psi, row0, view_of(host_block), view_of(y_rows),
+                            view_of(w), block_rows);
   });
 }
 
@@ -609,8 +656,9 @@ int qlra_pseudo_qr(qlra_ctx_t* ctx, const qlra_qmat_t* y, const qlra_pseudo_qr_c
       qgemm(c, QLRA_OP_C, QLRA_OP_N, 1.0, q0.v, H, 0.0, t.v);
       allreduce_qmat(c, t.v);
       qgemm(c, QLRA_OP_N, QLRA_OP_N, 1.0, q0.v, t.v, 0.0, H);
-      gram(c, H, g.v);
-      kappa = kappa_from_eigs(quat_eigs(c, g.v));
+      // kappa_after (rangefinders.cpp:153): the projection moves H only by
+      // the rounding it removes (H_k already lies in range(H0)), so the
+      // condition number of the last iterate is kept.
     }
     r.kappa_after = kappa;
     if (rep) *rep = r;

@@ -105,6 +105,11 @@ void qgemm_residual(Ctx& ctx, const QView& R, const QView& H, const QView& X, do
 // ----------------------------------------------------------- sketch.cu ---
 void sketch_update_rows(Ctx& ctx, const qlra_spec_t& omega, const qlra_spec_t& psi, int64_t row0,
                         const QView& block, const QView& y_rows, const QView& w);
+// Same with the block in HOST memory (pinned for full overlap): row panels
+// are streamed H2D on a copy stream, double-buffered against the sketch.
+void sketch_update_rows_host(Ctx& ctx, const qlra_spec_t& omega, const qlra_spec_t& psi,
+                             int64_t row0, const QView& host_block, const QView& y_rows,
+                             const QView& w, int64_t block_rows);
 const char* sketch_kernel_name();
 
 // ---------------------------------------------------------- smallla.cu ---

@@ -103,44 +103,33 @@ constexpr double kL2Budget = 48e6;  // bytes of A panel kept L2-resident
 
 const char* sketch_kernel_name() { return "sketch_fused_kernel(dmma_64x64x8,L2-panel)"; }
 
-void sketch_update_rows(Ctx& ctx, const qlra_spec_t& omega, const qlra_spec_t& psi, int64_t row0,
-                        const QView& block, const QView& y_rows, const QView& w) {
-  const int64_t b = block.rows, n = block.cols, s = omega.cols, l = psi.rows;
-  if (b == 0 || n == 0) return;
-  static bool attr = false;
-  if (!attr) {
-    QLRA_CUDA(cudaFuncSetAttribute(sketch_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)qt::SMEM_BYTES));
-    attr = true;
-  }
-  DevQMat om(ctx, n, s);
-  launch_gen(ctx.stream, omega, 0, 0, n, s, om.v, false);
-  DevQMat ps(ctx, l, b);
-  launch_gen(ctx.stream, psi, 0, row0, l, b, ps.v, false);
+namespace {
 
-  // Panel rows: L2 budget, multiple of 64, at least 64.
-  int64_t R = (int64_t)(kL2Budget / (32.0 * (double)n));
-  R = std::max<int64_t>(256, (R / 64) * 64);  // >= 256 rows keeps W tasks compute-dense
-  R = std::min<int64_t>(R, ((b + 63) / 64) * 64);
+struct SketchWork {
+  DeviceBuffer yp, wp;  // split-K partial workspaces, grown on demand
+};
+
+// One fused launch (+ ordered partial reductions) for a row panel `ap` of A
+// whose Psi columns are ps[:, pc0 : pc0 + ap.rows].
+void sketch_panel(Ctx& ctx, const QView& om, const QView& ps, int64_t pc0, const QView& ap,
+                  const QView& yv, const QView& w, SketchWork& ws) {
+  const int64_t rp = ap.rows, n = ap.cols, s = om.cols, l = ps.rows;
   const int w_tm = (int)((l + BM - 1) / BM), w_tn = (int)((n + BN - 1) / BN);
-  // Shared partial workspaces sized for the largest panel.
-  DeviceBuffer yp, wp;
-  for (int64_t r0 = 0; r0 < b; r0 += R) {
-    const int64_t rp = std::min(R, b - r0);
+  DeviceBuffer& yp = ws.yp;
+  DeviceBuffer& wp = ws.wp;
+  {
     FusedArgs f{};
-    const QView ap = sub(block, r0, 0, rp, n);
-    const QView yv = sub(y_rows, r0, 0, rp, s);
     for (int p = 0; p < 4; ++p) {
       f.yop.a[p] = ap.p[p];
-      f.yop.b[p] = om.v.p[p];
-      f.wop.a[p] = ps.v.p[p] + r0;  // Psi[:, r0:r0+rp]
+      f.yop.b[p] = om.p[p];
+      f.wop.a[p] = ps.p[p] + pc0;  // Psi[:, pc0:pc0+rp]
       f.wop.b[p] = ap.p[p];
       f.y[p] = yv.p[p];
       f.w[p] = w.p[p];
     }
-    f.yop.a_si = ap.ld; f.yop.a_sk = 1; f.yop.b_sk = om.v.ld; f.yop.b_sj = 1;
+    f.yop.a_si = ap.ld; f.yop.a_sk = 1; f.yop.b_sk = om.ld; f.yop.b_sj = 1;
     f.yop.M = rp; f.yop.N = s;
-    f.wop.a_si = ps.v.ld; f.wop.a_sk = 1; f.wop.b_sk = ap.ld; f.wop.b_sj = 1;
+    f.wop.a_si = ps.ld; f.wop.a_sk = 1; f.wop.b_sk = ap.ld; f.wop.b_sj = 1;
     f.wop.M = l; f.wop.N = n;
     f.ky = n;
     f.kw = rp;
@@ -191,6 +180,92 @@ void sketch_update_rows(Ctx& ctx, const qlra_spec_t& omega, const qlra_spec_t& p
     if (f.zy > 1) splitk_reduce(ctx, f.yp, f.zy, yv, 1.0, 1.0);
     if (f.zw > 1) splitk_reduce(ctx, f.wp, f.zw, w, 1.0, 1.0);
   }
+}
+
+void set_kernel_attrs() {
+  static bool attr = false;
+  if (!attr) {
+    QLRA_CUDA(cudaFuncSetAttribute(sketch_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)qt::SMEM_BYTES));
+    attr = true;
+  }
+}
+
+// Panel rows: L2 budget, multiple of 64, at least 256 (keeps W tasks dense).
+int64_t panel_rows(int64_t n, int64_t b) {
+  int64_t R = (int64_t)(kL2Budget / (32.0 * (double)n));
+  R = std::max<int64_t>(256, (R / 64) * 64);
+  return std::min<int64_t>(R, ((b + 63) / 64) * 64);
+}
+
+}  // namespace
+
+void sketch_update_rows(Ctx& ctx, const qlra_spec_t& omega, const qlra_spec_t& psi, int64_t row0,
+                        const QView& block, const QView& y_rows, const QView& w) {
+  const int64_t b = block.rows, n = block.cols, s = omega.cols, l = psi.rows;
+  if (b == 0 || n == 0) return;
+  set_kernel_attrs();
+  DevQMat om(ctx, n, s);
+  launch_gen(ctx.stream, omega, 0, 0, n, s, om.v, false);
+  DevQMat ps(ctx, l, b);
+  launch_gen(ctx.stream, psi, 0, row0, l, b, ps.v, false);
+  const int64_t R = panel_rows(n, b);
+  SketchWork ws;
+  for (int64_t r0 = 0; r0 < b; r0 += R) {
+    const int64_t rp = std::min(R, b - r0);
+    sketch_panel(ctx, om.v, ps.v, r0, sub(block, r0, 0, rp, n), sub(y_rows, r0, 0, rp, s), w, ws);
+  }
+}
+
+// Streaming ingestion (sketch_from_source, sketching.cpp:156-167, with the
+// source in host memory): row panels are copied H2D on a dedicated stream into
+// a double buffer while the previous panel is sketched, so the PCIe transfer
+// of A overlaps the FP64 work.  A is still read exactly once.
+void sketch_update_rows_host(Ctx& ctx, const qlra_spec_t& omega, const qlra_spec_t& psi,
+                             int64_t row0, const QView& host_block, const QView& y_rows,
+                             const QView& w, int64_t block_rows) {
+  const int64_t b = host_block.rows, n = host_block.cols, s = omega.cols, l = psi.rows;
+  if (b == 0 || n == 0) return;
+  set_kernel_attrs();
+  DevQMat om(ctx, n, s);
+  launch_gen(ctx.stream, omega, 0, 0, n, s, om.v, false);
+  DevQMat ps(ctx, l, b);
+  launch_gen(ctx.stream, psi, 0, row0, l, b, ps.v, false);
+  int64_t R = block_rows > 0 ? block_rows : panel_rows(n, b);
+  R = std::min(R, b);
+  DevQMat buf[2] = {DevQMat(ctx, R, n), DevQMat(ctx, R, n)};
+  cudaStream_t cs;
+  QLRA_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+  cudaEvent_t copied[2], freed[2];
+  for (int i = 0; i < 2; ++i) {
+    QLRA_CUDA(cudaEventCreateWithFlags(&copied[i], cudaEventDisableTiming));
+    QLRA_CUDA(cudaEventCreateWithFlags(&freed[i], cudaEventDisableTiming));
+  }
+  // buffers were allocated on ctx.stream: make the copy stream wait for that
+  QLRA_CUDA(cudaEventRecord(freed[0], ctx.stream));
+  QLRA_CUDA(cudaEventRecord(freed[1], ctx.stream));
+  SketchWork ws;
+  int idx = 0;
+  for (int64_t r0 = 0; r0 < b; r0 += R, idx ^= 1) {
+    const int64_t rp = std::min(R, b - r0);
+    const QView dst = sub(buf[idx].v, 0, 0, rp, n);
+    QLRA_CUDA(cudaStreamWaitEvent(cs, freed[idx], 0));
+    for (int p = 0; p < 4; ++p)
+      QLRA_CUDA(cudaMemcpy2DAsync(dst.p[p], (size_t)dst.ld * sizeof(double),
+                                  host_block.p[p] + r0 * host_block.ld,
+                                  (size_t)host_block.ld * sizeof(double),
+                                  (size_t)n * sizeof(double), (size_t)rp, cudaMemcpyHostToDevice, cs));
+    QLRA_CUDA(cudaEventRecord(copied[idx], cs));
+    QLRA_CUDA(cudaStreamWaitEvent(ctx.stream, copied[idx], 0));
+    sketch_panel(ctx, om.v, ps.v, r0, dst, sub(y_rows, r0, 0, rp, s), w, ws);
+    QLRA_CUDA(cudaEventRecord(freed[idx], ctx.stream));
+  }
+  QLRA_CUDA(cudaStreamSynchronize(cs));
+  for (int i = 0; i < 2; ++i) {
+    cudaEventDestroy(copied[i]);
+    cudaEventDestroy(freed[i]);
+  }
+  cudaStreamDestroy(cs);
 }
 
 }  // namespace qlra_dev

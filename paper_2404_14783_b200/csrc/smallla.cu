@@ -34,16 +34,20 @@ __device__ __forceinline__ double2 cdiv(double2 a, double2 b) {
   return make_double2((a.x * b.x + a.y * b.y) / d, (a.y * b.x - a.x * b.y) / d);
 }
 
-// Fixed-order block sum (tree over threadIdx), result broadcast.
+// Fixed-order block sum (shuffle trees within and across warps), result
+// broadcast; deterministic for a given blockDim.  sh needs 32 doubles.
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+  return v;
+}
 __device__ double block_sum(double v, double* sh) {
-  const int t = threadIdx.x;
-  sh[t] = v;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  v = warp_sum(v);
+  if (lane == 0) sh[wid] = v;
   __syncthreads();
-  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
-    if (t < w) sh[t] += sh[t + w];
-    __syncthreads();
-  }
-  const double r = sh[0];
+  double r = lane < nw ? sh[lane] : 0.0;
+  r = warp_sum(r);
   __syncthreads();
   return r;
 }
@@ -261,6 +265,53 @@ __global__ void k_bisect(const double* d, const double* e, int64_t n, double* w,
       if (sturm_count(d, e, n, mid) > k) hi = mid; else lo = mid;
     }
     w[n - 1 - k] = 0.5 * (lo + hi);
+  }
+}
+
+// Extreme eigenvalues of the symmetric tridiagonal (d, e) by parallel
+// multisection: half the CTA brackets the largest, half the smallest; each
+// round evaluates 511 Sturm counts and shrinks the bracket 512-fold.
+__global__ void __launch_bounds__(1024) k_multisect_extremes(const double* d, const double* e,
+                                                             int64_t n, double* w) {
+  __shared__ double s_lo[2], s_hi[2];
+  __shared__ int s_first[2];
+  const int t = threadIdx.x, half = t >> 9, j = t & 511;
+  if (t == 0) {
+    double lo = d[0], hi = d[0];
+    for (int64_t i = 0; i < n; ++i) {
+      const double r = (i > 0 ? fabs(e[i - 1]) : 0.0) + (i + 1 < n ? fabs(e[i]) : 0.0);
+      lo = fmin(lo, d[i] - r);
+      hi = fmax(hi, d[i] + r);
+    }
+    const double pad = 2.2e-16 * fmax(fabs(lo), fabs(hi)) * (double)n + 1e-300;
+    s_lo[0] = s_lo[1] = lo - pad;
+    s_hi[0] = s_hi[1] = hi + pad;
+  }
+  __syncthreads();
+  // half 0: k = n-1 (largest), half 1: k = 0 (smallest); want smallest x with count(x) > k
+  const int64_t k = half == 0 ? n - 1 : 0;
+  for (int round = 0; round < 9; ++round) {
+    const double lo = s_lo[half], hi = s_hi[half];
+    const bool done = !(hi - lo > 4.4e-16 * fmax(fabs(lo), fabs(hi)));
+    if (j == 0) s_first[half] = 512;
+    __syncthreads();
+    if (!done && j < 511) {
+      const double x = lo + (hi - lo) * (double)(j + 1) / 512.0;
+      if (x > lo && x < hi && sturm_count(d, e, n, x) > k) atomicMin(&s_first[half], j);
+    }
+    __syncthreads();
+    if (!done && j == 0) {
+      const int f = s_first[half];  // first point with count > k (512: none)
+      const double nlo = f == 0 ? lo : lo + (hi - lo) * (double)f / 512.0;
+      const double nhi = f == 512 ? hi : lo + (hi - lo) * (double)(f + 1) / 512.0;
+      s_lo[half] = nlo;
+      s_hi[half] = nhi;
+    }
+    __syncthreads();
+  }
+  if (t == 0) {
+    w[0] = 0.5 * (s_lo[0] + s_hi[0]);
+    w[n - 1] = 0.5 * (s_lo[1] + s_hi[1]);
   }
 }
 
@@ -501,21 +552,33 @@ __global__ void __launch_bounds__(SNT) k_quat_cholesky(QView g, int* info) {
   }
 }
 
-// X = R^{-1} for upper-triangular quaternion R with real diagonal; thread j
-// owns column j: X_jj = 1/R_jj, X_ij = -R_ii^{-1} sum_{k=i+1..j} R_ik X_kj.
+// X = R^{-1} for upper-triangular quaternion R with real diagonal.  One warp
+// per column j: X_jj = 1/R_jj, then for i = j-1 .. 0,
+// X_ij = -R_ii^{-1} sum_{k=i+1..j} R_ik X_kj with the sum split across the
+// 32 lanes (fixed-order shuffle reduction).  X must not alias R.
 __global__ void __launch_bounds__(SNT) k_quat_triinv_upper(QView r, QView x) {
   const int64_t n = r.rows;
-  for (int64_t j = threadIdx.x; j < n; j += blockDim.x) {
-    for (int64_t i = 0; i < n; ++i) qstore(x, i, j, Q4{0.0, 0.0, 0.0, 0.0});
-    qstore(x, j, j, Q4{1.0 / r.p[0][j * r.ld + j], 0.0, 0.0, 0.0});
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int64_t j = wid; j < n; j += nw) {
+    for (int64_t i = lane; i < n; i += 32) qstore(x, i, j, Q4{0.0, 0.0, 0.0, 0.0});
+    __syncwarp();
+    if (lane == 0) qstore(x, j, j, Q4{1.0 / r.p[0][j * r.ld + j], 0.0, 0.0, 0.0});
+    __syncwarp();
     for (int64_t i = j - 1; i >= 0; --i) {
-      Q4 s{0.0, 0.0, 0.0, 0.0};
-      for (int64_t k = i + 1; k <= j; ++k) {
+      Q4 acc{0.0, 0.0, 0.0, 0.0};
+      for (int64_t k = i + 1 + lane; k <= j; k += 32) {
         const Q4 pq = qmul(qload(r, i, k), qload(x, k, j));
-        s.w += pq.w; s.x += pq.x; s.y += pq.y; s.z += pq.z;
+        acc.w += pq.w; acc.x += pq.x; acc.y += pq.y; acc.z += pq.z;
       }
-      const double inv = -1.0 / r.p[0][i * r.ld + i];
-      qstore(x, i, j, Q4{s.w * inv, s.x * inv, s.y * inv, s.z * inv});
+      acc.w = warp_sum(acc.w);
+      acc.x = warp_sum(acc.x);
+      acc.y = warp_sum(acc.y);
+      acc.z = warp_sum(acc.z);
+      if (lane == 0) {
+        const double inv = -1.0 / r.p[0][i * r.ld + i];
+        qstore(x, i, j, Q4{acc.w * inv, acc.x * inv, acc.y * inv, acc.z * inv});
+      }
+      __syncwarp();
     }
   }
 }
@@ -690,7 +753,7 @@ void small_quat_herm_eigvals(Ctx& ctx, const QView& a, double* d_w, bool extreme
   count_launch();
   if (extremes_only) {
     // w[0] = max, w[n-1] = min; the middle stays untouched
-    k_bisect<<<1, 32, 0, ctx.stream>>>(d, e, n, d_w, 1);
+    k_multisect_extremes<<<1, 1024, 0, ctx.stream>>>(d, e, n, d_w);
   } else {
     k_bisect<<<(unsigned)((n + 255) / 256), 256, 0, ctx.stream>>>(d, e, n, d_w, 0);
   }

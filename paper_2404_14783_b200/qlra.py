@@ -149,9 +149,10 @@ def qzeros(rows, cols, device=None):
     return torch.zeros((4, rows, cols), dtype=torch.float64, device=device or "cuda")
 
 
-def _qm(t: torch.Tensor) -> L.QMat:
-    if t.dtype != torch.float64 or t.dim() != 3 or t.shape[0] != 4 or not t.is_cuda:
-        raise ShapeError("QMatrix must be a CUDA float64 tensor of shape (4, rows, cols)")
+def _qm(t: torch.Tensor, host: bool = False) -> L.QMat:
+    if t.dtype != torch.float64 or t.dim() != 3 or t.shape[0] != 4 or t.is_cuda == host:
+        where = "CPU (pinned)" if host else "CUDA"
+        raise ShapeError(f"QMatrix must be a {where} float64 tensor of shape (4, rows, cols)")
     if t.shape[2] > 1 and t.stride(2) != 1:
         raise ShapeError("QMatrix planes must be row-major (unit column stride)")
     q = L.QMat()
@@ -272,6 +273,38 @@ def sketch_update_rows(state: SketchState, row0: int, block: torch.Tensor, ctx=N
     ctx._check(ctx.lib.qlra_sketch_update_rows(ctx.h, C.byref(om), C.byref(ps), row0,
                                                C.byref(_qm(block)), C.byref(_qm(yv)),
                                                C.byref(_qm(state.w))))
+
+
+def sketch_update_rows_host(state: SketchState, row0: int, block_host: torch.Tensor, block_rows: int = 0,
+                            ctx=None):
+    """sketch_update_rows with the block in host memory (pinned for overlap):
+    H2D row panels are streamed and double-buffered against the sketch."""
+    ctx = _ctx(ctx)
+    lr0 = row0 - state.row0
+    if block_host.shape[2] != state.w.shape[2]:
+        raise ShapeError("sketch_update_rows: column count mismatch")
+    if lr0 < 0 or lr0 + block_host.shape[1] > state.y.shape[1]:
+        raise ShapeError("sketch_update_rows: row range out of bounds")
+    if block_host.shape[1] == 0:
+        return
+    yv = state.y[:, lr0:lr0 + block_host.shape[1], :]
+    om, ps = state.omega_spec.c(), state.psi_spec.c()
+    ctx._check(ctx.lib.qlra_sketch_update_rows_host(ctx.h, C.byref(om), C.byref(ps), row0,
+                                                    C.byref(_qm(block_host, host=True)),
+                                                    C.byref(_qm(yv)), C.byref(_qm(state.w)), block_rows))
+
+
+def make_sketch_host(a_host, r, s, l, omega_seed, psi_seed, kind=GAUSSIAN, density=1.0, ctx=None, row0=0,
+                     m_global=None, block_rows=0):
+    """make_sketch from a host-resident (pinned) A: the public streaming entry."""
+    ctx = _ctx(ctx)
+    m = a_host.shape[1] if m_global is None else m_global
+    st = empty_sketch(m, a_host.shape[2], r, s, l, omega_seed, psi_seed, kind, density,
+                      rows_local=a_host.shape[1], row0=row0)
+    sketch_update_rows_host(st, row0, a_host, block_rows, ctx)
+    if ctx.nranks > 1:
+        sketch_allreduce(st, ctx)
+    return st
 
 
 def sketch_allreduce(state: SketchState, ctx=None):

@@ -249,3 +249,14 @@ def test_residual_kernel(ctx):
 def test_fp64_peak_positive(ctx):
     from paper_2404_14783_b200 import qlra as Q
     assert Q.measure_fp64_peak(0, 20.0, ctx) > 1.0
+
+
+def test_host_streaming_sketch_matches_device(ctx):  # sketching.cpp:156-167 streaming form
+    from paper_2404_14783_b200 import qlra as Q
+    a = random_gaussian(1000, 300, 71)
+    whole = Q.make_sketch(dev(a), 8, 10, 20, 3, 4, ctx=ctx)
+    ah = torch.from_numpy(a).pin_memory()
+    for br in (0, 64, 333):
+        st = Q.make_sketch_host(ah, 8, 10, 20, 3, 4, ctx=ctx, block_rows=br)
+        assert rel_diff(host(st.y), host(whole.y)) < 1e-14
+        assert rel_diff(host(st.w), host(whole.w)) < 1e-13
