@@ -44,6 +44,8 @@ def parse():
 
 # ------------------------------------------------------------ clocks ---
 class ClockSampler:
+    """SM clock and throttle reasons sampled DURING the timed region (NVML,
+    every 20 ms; nvidia-smi fallback)."""
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
@@ -55,6 +57,21 @@ class ClockSampler:
         self._t = threading.Thread(target=self._run, daemon=True)
 
     def _run(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.device)
+            mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            bits = [("hw_slowdown", 0x8), ("hw_thermal_slowdown", 0x40), ("sw_thermal_slowdown", 0x20),
+                    ("sw_power_cap", 0x4)]
+            while not self._stop.is_set():
+                sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.samples.append([str(sm), str(mx)] + ["Active" if r & b else "Not Active" for _, b in bits])
+                self._stop.wait(0.02)
+            return
+        except Exception:
+            pass
         while not self._stop.is_set():
             try:
                 out = subprocess.run(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
@@ -104,9 +121,9 @@ def cpu_leg(cfg, y_h, w_h, a_rows_h, nthreads, method):
 
 
 def sample_rows(cfg, nthreads):
-    # ~4 s of serial sketch work per thread at ~2 GFLOP/s, at least 32 rows
+    # ~2 s of serial sketch work per thread at ~2 GFLOP/s, at least 32 rows
     per_row = 32.0 * cfg.n * (cfg.s + cfg.l)
-    return int(max(32, min(cfg.m, 4.0 * 2e9 * nthreads / per_row)))
+    return int(max(32, min(cfg.m, 2.0 * 2e9 * nthreads / per_row)))
 
 
 def run_reference(args):
@@ -214,6 +231,7 @@ def main():
         step(a)
     barrier()
     sk_events.clear()
+    ctx.kernel_timing(True)
     launches0 = ctx.launch_count()
     with ClockSampler(local) as clk:
         t0 = torch.cuda.Event(enable_timing=True)
@@ -224,12 +242,15 @@ def main():
         t1.record(stream)
         barrier()
     launches = ctx.launch_count() - launches0
+    kst = ctx.kernel_stats()
+    ctx.kernel_timing(False)
     ms = t0.elapsed_time(t1) / args.steps
     sk_ms = float(np.mean([e0.elapsed_time(e1) for e0, e1 in sk_events]))
-    tt = torch.tensor([ms, sk_ms], dtype=torch.float64, device="cuda")
+    k_ms = kst["ms"] / max(1, kst["launches"])  # fused sketch kernel, per launch
+    tt = torch.tensor([ms, sk_ms, k_ms], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-    ms, sk_ms = float(tt[0]), float(tt[1])
+    ms, sk_ms, k_ms = float(tt[0]), float(tt[1]), float(tt[2])
 
     # parity sanity on the measured result (second read of A, not timed)
     res, an = Q.residual_fro(a, qb.h, qb.x, ctx)
@@ -272,8 +293,16 @@ def main():
 
     peaks = {"dfma_tflops": Q.measure_fp64_peak(0, 300.0, ctx), "dmma_tflops": Q.measure_fp64_peak(1, 300.0, ctx)}
     peak = max(peaks.values())
-    flops_local = 32.0 * (r1 - r0) * cfg.n * (cfg.s + cfg.l)
-    achieved = flops_local / (sk_ms * 1e-3) / 1e12
+    # achieved: algorithmic flops of one fused-kernel launch / its mean
+    # CUDA-event duration, measured on the launching stream in the timed region
+    flops_launch = kst["flops"] / max(1, kst["launches"])
+    achieved = flops_launch / (k_ms * 1e-3) / 1e12
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "sketch_traffic.json")
+    if os.path.exists(prof):
+        pt = json.load(open(prof))
+        if pt.get("config") == cfg.name and world == 1:
+            traffic = pt["dram_bytes_per_launch"]
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -294,14 +323,19 @@ def main():
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"{cfg.name} {cfg.m}x{cfg.n} fp64 quaternion, s={cfg.s}, l={cfg.l}, "
                                    f"{args.rangefinder}",
-                       "model": None, "parallelism": f"row-shard x{world}",
+                       "parallelism": f"row-shard x{world}",
                        "l2": "A (%.2f GB) larger than the 126 MB L2; no flush needed" % (cfg.a_bytes() / 1e9)},
-            "sketch_ms": sk_ms, "sketch_tflops": cfg.flops() / (sk_ms * 1e-3) / 1e12,
+            "sketch_ms": sk_ms, "sketch_tflops": 32.0 * (r1 - r0) * cfg.n * (cfg.s + cfg.l) / (sk_ms * 1e-3) / 1e12,
             "sketch_kernel": Q.sketch_kernel_name(),
-            "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                         "frac": achieved / peak, "traffic": None,
-                         "peak_source": "measured in this run: " + json.dumps(peaks),
-                         "note": "sketch stage (Omega/Psi generation + both products) per rank"},
+            "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "kernel_ms_per_launch": k_ms, "launches": kst["launches"],
+                         "algorithmic_per_launch": {"flops": flops_launch,
+                                                    "a_bytes": kst["a_bytes"] / max(1, kst["launches"])},
+                         "peak_source": "FP64 measured in this run (DMMA m8n8k4 / DFMA microbenchmarks; "
+                                        "MEASURED_PEAKS.json has no FP64 entry): " + json.dumps(peaks),
+                         "note": "FP64 tensor pipe (DMMA); per-unit = 32 flop per quaternion MAC, "
+                                 "a launch covers one L2-resident row panel: 32*rows*n*(s+l) flop"},
             "rel_error": res / an, "e2e": e2e, "gpu_launches": int(launches), "clocks": clk.summary(),
             "cpu_baseline": cpu,
         }

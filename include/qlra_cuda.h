@@ -101,6 +101,12 @@ int qlra_nccl_unique_id(void* out_128_bytes);
 const char* qlra_last_error(const qlra_ctx_t* ctx, double* estimated_condition);
 /* Number of kernels this ctx has launched (diagnostics / bench evidence). */
 int64_t qlra_ctx_launch_count(const qlra_ctx_t* ctx);
+/* Start (enable=1, resetting) or stop per-launch CUDA-event timing of the
+ * fused sketch kernel, and read it back: total device ms, launches, and the
+ * algorithmic flops / bytes of A those launches processed; stats syncs. */
+int qlra_ctx_kernel_timing(qlra_ctx_t* ctx, int enable);
+int qlra_ctx_kernel_stats(qlra_ctx_t* ctx, double* ms, int64_t* launches, double* flops,
+                          double* a_bytes);
 
 /* ---------------------------------------------------------- embeddings --- */
 /* gen_block (sketching.cpp:53-71) / gen_test_matrix{,_rows,_cols}

@@ -55,6 +55,8 @@ def lib():
         "qlra_nccl_unique_id": ([VP], INT),
         "qlra_last_error": ([VP, P(F64)], C.c_char_p),
         "qlra_ctx_launch_count": ([VP], I64),
+        "qlra_ctx_kernel_timing": ([VP, INT], INT),
+        "qlra_ctx_kernel_stats": ([VP, P(F64), P(I64), P(F64), P(F64)], INT),
         "qlra_gen_test_matrix_block": ([VP, PS, I64, I64, PQ], INT),
         "qlra_sketch_update_rows": ([VP, PS, PS, I64, PQ, PQ, PQ], INT),
         "qlra_sketch_update_rows_host": ([VP, PS, PS, I64, PQ, PQ, PQ, I64], INT),

@@ -411,6 +411,40 @@ const char* qlra_last_error(const qlra_ctx_t* ctx, double* cond) {
 
 int64_t qlra_ctx_launch_count(const qlra_ctx_t*) { return launch_counter().load(); }
 
+static void drop_events(Ctx& c) {
+  for (auto& e : c.ktimer.ev) {
+    cudaEventDestroy(e.first);
+    cudaEventDestroy(e.second);
+  }
+  c.ktimer.ev.clear();
+  c.ktimer.flops = c.ktimer.a_bytes = 0.0;
+  c.ktimer.launches = 0;
+}
+
+int qlra_ctx_kernel_timing(qlra_ctx_t* ctx, int enable) {
+  return guarded(ctx, [&](Ctx& c) {
+    drop_events(c);
+    c.ktimer.on = enable != 0;
+  });
+}
+
+int qlra_ctx_kernel_stats(qlra_ctx_t* ctx, double* ms, int64_t* launches, double* flops,
+                          double* a_bytes) {
+  return guarded(ctx, [&](Ctx& c) {
+    double total = 0.0;
+    for (auto& e : c.ktimer.ev) {
+      QLRA_CUDA(cudaEventSynchronize(e.second));
+      float t = 0.f;
+      QLRA_CUDA(cudaEventElapsedTime(&t, e.first, e.second));
+      total += t;
+    }
+    if (ms) *ms = total;
+    if (launches) *launches = c.ktimer.launches;
+    if (flops) *flops = c.ktimer.flops;
+    if (a_bytes) *a_bytes = c.ktimer.a_bytes;
+  });
+}
+
 int qlra_gen_test_matrix_block(qlra_ctx_t* ctx, const qlra_spec_t* spec, int64_t r0, int64_t c0,
                                qlra_qmat_t* out) {
   return guarded(ctx, [&](Ctx& c) {

@@ -7,6 +7,8 @@
 #include <algorithm>
 #include <atomic>
 #include <string>
+#include <utility>
+#include <vector>
 
 #include "common.cuh"
 
@@ -26,6 +28,14 @@ struct Ctx {
   std::string last_error;
   double last_cond = 0.0;
   double* pinned = nullptr;  // small host staging buffer (syncs)
+  // Optional per-launch timing of the fused sketch kernel (bench evidence):
+  // CUDA events bracket every launch on the launching stream.
+  struct KernelTimer {
+    bool on = false;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;
+    double flops = 0.0, a_bytes = 0.0;
+    int64_t launches = 0;
+  } ktimer;
 };
 
 // Stream-ordered device allocation (cudaMallocAsync from the device's default

@@ -174,9 +174,22 @@ void sketch_panel(Ctx& ctx, const QView& om, const QView& ps, int64_t pc0, const
       f.wp = wp.as<double>();
     }
     const int64_t ctas = yt * f.zy + wt * f.zw;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (ctx.ktimer.on) {
+      QLRA_CUDA(cudaEventCreate(&e0));
+      QLRA_CUDA(cudaEventCreate(&e1));
+      QLRA_CUDA(cudaEventRecord(e0, ctx.stream));
+    }
     sketch_fused_kernel<<<(unsigned)ctas, NT, qt::SMEM_BYTES, ctx.stream>>>(f);
     QLRA_LAUNCH_CHECK();
     count_launch();
+    if (ctx.ktimer.on) {
+      QLRA_CUDA(cudaEventRecord(e1, ctx.stream));
+      ctx.ktimer.ev.emplace_back(e0, e1);
+      ctx.ktimer.flops += 32.0 * (double)rp * (double)n * (double)(s + l);
+      ctx.ktimer.a_bytes += 32.0 * (double)rp * (double)n;
+      ++ctx.ktimer.launches;
+    }
     if (f.zy > 1) splitk_reduce(ctx, f.yp, f.zy, yv, 1.0, 1.0);
     if (f.zw > 1) splitk_reduce(ctx, f.wp, f.zw, w, 1.0, 1.0);
   }

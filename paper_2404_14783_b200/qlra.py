@@ -97,6 +97,15 @@ class Context:
     def launch_count(self) -> int:
         return int(self.lib.qlra_ctx_launch_count(self.h))
 
+    def kernel_timing(self, enable: bool):
+        """Start/stop CUDA-event timing of every fused sketch launch."""
+        self._check(self.lib.qlra_ctx_kernel_timing(self.h, 1 if enable else 0))
+
+    def kernel_stats(self) -> dict:
+        ms, n, fl, by = C.c_double(), C.c_int64(), C.c_double(), C.c_double()
+        self._check(self.lib.qlra_ctx_kernel_stats(self.h, C.byref(ms), C.byref(n), C.byref(fl), C.byref(by)))
+        return dict(ms=ms.value, launches=n.value, flops=fl.value, a_bytes=by.value)
+
     def _check(self, rc: int):
         if rc == 0:
             return
