@@ -187,6 +187,23 @@ int qlra_pseudo_svd(qlra_ctx_t* ctx, const qlra_qmat_t* y, uint64_t seed, qlra_q
 int qlra_qb_solve(qlra_ctx_t* ctx, const qlra_spec_t* psi, int64_t row0, const qlra_qmat_t* h,
                   const qlra_qmat_t* w, qlra_qmat_t* x);
 
+/* ------------------------------------------------ truncation (next) --- */
+/* qsvd (factorizations.hpp:44, factorizations.cpp:166-295) of a replicated
+ * A (m x n): u m x k, v n x k, k = min(m, n); sigma (host, k) nonincreasing;
+ * phase convention of factorizations.cpp:273-293.  syncs. */
+int qlra_qsvd(qlra_ctx_t* ctx, const qlra_qmat_t* a, qlra_qmat_t* u, double* sigma,
+              qlra_qmat_t* v);
+/* truncate_stage (sketching.hpp:128, sketching.cpp:196-211): QSVD of X
+ * (s x n), keep the leading r triples, h_out = H U_r (H row-sharded),
+ * sigma (host, r), v = V_r (n x r).  syncs. */
+int qlra_truncate_stage(qlra_ctx_t* ctx, const qlra_qmat_t* h, const qlra_qmat_t* x, int64_t r,
+                        qlra_qmat_t* h_out, double* sigma, qlra_qmat_t* v);
+/* ||A - H diag(sigma) V^*||_F and ||A||_F: the relative_error diagnostic of
+ * one_pass_approx (sketching.cpp:272-273; analysis.cpp:75-79).  syncs. */
+int qlra_approx_residual_fro(qlra_ctx_t* ctx, const qlra_qmat_t* a, const qlra_qmat_t* h,
+                             const double* sigma, const qlra_qmat_t* v, double* res_fro,
+                             double* a_fro);
+
 /* ---------------------------------------------------------- residual --- */
 /* ||A - H X||_F and ||A||_F (sketching.cpp:270-271; analysis.cpp:75-79) over
  * row-sharded A and H: a fused GEMM-subtract-square-reduce (second read of A,

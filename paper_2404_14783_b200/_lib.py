@@ -72,6 +72,9 @@ def lib():
         "qlra_pseudo_svd": ([VP, PQ, U64, PQ, P(Report)], INT),
         "qlra_qb_solve": ([VP, PS, I64, PQ, PQ, PQ], INT),
         "qlra_residual_fro": ([VP, PQ, PQ, PQ, P(F64), P(F64)], INT),
+        "qlra_qsvd": ([VP, PQ, PQ, P(F64), PQ], INT),
+        "qlra_truncate_stage": ([VP, PQ, PQ, I64, PQ, P(F64), PQ], INT),
+        "qlra_approx_residual_fro": ([VP, PQ, PQ, P(F64), PQ, P(F64), P(F64)], INT),
         "qlra_measure_fp64_peak": ([VP, INT, F64, P(F64)], INT),
         "qlra_sketch_kernel_name": ([], C.c_char_p),
     }

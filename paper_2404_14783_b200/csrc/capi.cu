@@ -205,6 +205,65 @@ bool cholesky_qr(Ctx& ctx, const QView& y, const QView& h, bool complex_mode, in
   return true;
 }
 
+// Orthonormal completion: c_out (rows x k, row-sharded from global row0)
+// becomes quaternion-orthonormal and orthogonal to hr (rows x r, may be
+// r = 0).  Candidates are Gaussian columns from the reference RNG (seeded),
+// projected out twice (CGS2) and orthonormalised by CholeskyQR2 -- the device
+// counterpart of select_via_mgs' canonical-direction fallback
+// (factorizations.cpp:105-118).
+void orthonormal_completion(Ctx& ctx, const QView& hr, const QView& c_out, int64_t row0,
+                            int64_t m_global, uint64_t seed) {
+  const int64_t k = c_out.cols, rows = c_out.rows;
+  if (k == 0) return;
+  DevQMat c(ctx, rows, k);
+  qlra_spec_t spec{QLRA_GAUSSIAN, m_global, k, seed, 1.0};
+  launch_gen(ctx.stream, spec, row0, 0, rows, k, c.v, false);
+  if (hr.cols > 0) {
+    DevQMat t(ctx, hr.cols, k);
+    for (int pass = 0; pass < 2; ++pass) {
+      qgemm(ctx, QLRA_OP_C, QLRA_OP_N, 1.0, hr, c.v, 0.0, t.v);
+      allreduce_qmat(ctx, t.v);
+      qgemm(ctx, QLRA_OP_N, QLRA_OP_N, -1.0, hr, t.v, 1.0, c.v);
+    }
+  }
+  if (!cholesky_qr(ctx, c.v, c_out, /*complex_mode=*/false, m_global, nullptr))
+    fail(QLRA_ERR_INTERNAL, "orthonormal completion failed");
+}
+
+// pseudo_svd for numerically rank-deficient Y (where CholeskyQR breaks
+// down): the reference's bad-block route (rangefinders.cpp:33-41,
+// factorizations.cpp:83-152) becomes, in quaternion arithmetic, an
+// eigendecomposition G = Y^*Y = V L V^* (Jacobi, no pair splitting), the
+// range basis Y V_r L_r^{-1/2} for the numerically nonzero part
+// (re-orthonormalised), and an orthonormal completion for the rest.
+void pseudo_svd_rank_deficient(Ctx& ctx, const QView& y, const QView& h, int64_t m_global,
+                               int64_t row0, uint64_t seed) {
+  const int64_t s = y.cols;
+  DevQMat g(ctx, s, s), vec(ctx, s, s);
+  gram(ctx, y, g.v);
+  DeviceBuffer w(ctx, sizeof(double) * (size_t)s);
+  small_quat_eigh(ctx, g.v, w.as<double>(), vec.v);
+  const std::vector<double> lam = to_host(ctx, w.as<double>(), (size_t)s);
+  const double lmax = std::max(0.0, lam[0]);
+  const double thr = std::max(64.0 * kUnit * (double)s * lmax, 1e-300);
+  int64_t r = 0;
+  while (r < s && lam[r] > thr) ++r;
+  if (r > 0) {
+    DevQMat t(ctx, y.rows, r), sq(ctx, 1, 1);
+    qgemm(ctx, QLRA_OP_N, QLRA_OP_N, 1.0, y, sub(vec.v, 0, 0, s, r), 0.0, t.v);
+    std::vector<double> is(r);
+    for (int64_t i = 0; i < r; ++i) is[i] = 1.0 / std::sqrt(lam[i]);
+    DeviceBuffer d_is(ctx, sizeof(double) * (size_t)r);
+    QLRA_CUDA(cudaMemcpyAsync(d_is.ptr, is.data(), sizeof(double) * r, cudaMemcpyHostToDevice, ctx.stream));
+    scale_cols(ctx, t.v, d_is.as<double>(), false, 0.0, t.v);
+    if (!cholesky_qr(ctx, t.v, sub(h, 0, 0, y.rows, r), false, m_global, nullptr))
+      fail(QLRA_ERR_INTERNAL, "pseudo_svd: range basis orthonormalisation failed");
+  }
+  if (r < s)
+    orthonormal_completion(ctx, sub(h, 0, 0, y.rows, r), sub(h, 0, r, y.rows, s - r), row0, m_global,
+                           rng_substream(rng_key(seed), 0x6261645F626C6BULL));
+}
+
 void rank_check(const std::vector<double>& d) {
   double rmax = 0.0, rmin = std::numeric_limits<double>::infinity();
   for (double v : d) {
@@ -701,7 +760,6 @@ int qlra_pseudo_qr(qlra_ctx_t* ctx, const qlra_qmat_t* y, const qlra_pseudo_qr_c
 
 int qlra_pseudo_svd(qlra_ctx_t* ctx, const qlra_qmat_t* y, uint64_t seed, qlra_qmat_t* h,
                     qlra_rangefinder_report_t* rep) {
-  (void)seed;
   return guarded(ctx, [&](Ctx& c) {
     check_view(y, "pseudo_svd");
     check_view(h, "pseudo_svd");
@@ -713,9 +771,10 @@ int qlra_pseudo_svd(qlra_ctx_t* ctx, const qlra_qmat_t* y, uint64_t seed, qlra_q
     qlra_rangefinder_report_t r{};
     r.method = QLRA_PSEUDO_SVD;
     r.kappa_before = condition_number_dev(c, Y);
-    if (!cholesky_qr(c, Y, H, /*complex_mode=*/false, m, nullptr))
-      fail(QLRA_ERR_PRECONDITION,
-           "pseudo_svd: rank-deficient sketch (bad-block repair) is not implemented on device yet");
+    // Full-rank sketches: quaternion CholeskyQR2 (shifted CholeskyQR3 when
+    // needed).  Rank-deficient ones: eigen route + orthonormal completion.
+    if (!std::isfinite(r.kappa_before) || !cholesky_qr(c, Y, H, /*complex_mode=*/false, m, nullptr))
+      pseudo_svd_rank_deficient(c, Y, H, m, /*row0=*/0, seed);
     r.kappa_after = condition_number_dev(c, H);
     if (rep) *rep = r;
   });
@@ -752,6 +811,106 @@ int qlra_residual_fro(qlra_ctx_t* ctx, const qlra_qmat_t* a, const qlra_qmat_t* 
     const std::vector<double> v = to_host(c, out.as<double>(), 2);
     if (res_fro) *res_fro = std::sqrt(v[0]);
     if (a_fro) *a_fro = std::sqrt(v[1]);
+  });
+}
+
+// qsvd of a replicated wide-or-tall A (factorizations.cpp:166-295) through the
+// Hermitian eigendecomposition of the smaller Gram.  u: m x k, v: n x k,
+// sigma: k host values (k = min(m, n)), nonincreasing.
+static void qsvd_dev(Ctx& c, const QView& a, const QView& u, const QView& v, double* sigma_host) {
+  const int64_t m = a.rows, n = a.cols, k = std::min(m, n);
+  if (k == 0) return;
+  const bool wide = m < n;  // reference: qsvd(A^*) then swap (factorizations.cpp:167-170)
+  // small side eigenvectors E (k x k): of A A^* when wide (-> U), of A^*A when tall (-> V)
+  DevQMat g(c, k, k), e(c, k, k);
+  if (wide)
+    qgemm(c, QLRA_OP_N, QLRA_OP_C, 1.0, a, a, 0.0, g.v);
+  else
+    qgemm(c, QLRA_OP_C, QLRA_OP_N, 1.0, a, a, 0.0, g.v);
+  DeviceBuffer w(c, sizeof(double) * (size_t)k);
+  small_quat_eigh(c, g.v, w.as<double>(), e.v);
+  std::vector<double> lam = to_host(c, w.as<double>(), (size_t)k);
+  std::vector<double> sg(k);
+  for (int64_t i = 0; i < k; ++i) sg[i] = std::sqrt(std::max(0.0, lam[i]));
+  const double tiny = 1e-13 * sg[0];
+  int64_t good = 0;
+  while (good < k && sg[good] > tiny) ++good;
+  DeviceBuffer d_sg(c, sizeof(double) * (size_t)k);
+  QLRA_CUDA(cudaMemcpyAsync(d_sg.ptr, sg.data(), sizeof(double) * k, cudaMemcpyHostToDevice, c.stream));
+  // big side: A^* U / sigma (wide) or A V / sigma (tall)
+  const QView small = wide ? u : v, big = wide ? v : u;
+  copy_qmat(c, e.v, small);
+  DevQMat t(c, big.rows, k);
+  if (wide)
+    qgemm(c, QLRA_OP_C, QLRA_OP_N, 1.0, a, e.v, 0.0, t.v);
+  else
+    qgemm(c, QLRA_OP_N, QLRA_OP_N, 1.0, a, e.v, 0.0, t.v);
+  scale_cols(c, t.v, d_sg.as<double>(), true, tiny, t.v);
+  // Polish (factorizations.cpp:245-260): Gram-Schmidt in sigma order strips
+  // the eps/gap leakage; CholeskyQR spans the same nested column spaces.
+  if (good > 0 && !cholesky_qr(c, sub(t.v, 0, 0, big.rows, good), sub(big, 0, 0, big.rows, good),
+                               false, big.rows, nullptr))
+    copy_qmat(c, sub(t.v, 0, 0, big.rows, good), sub(big, 0, 0, big.rows, good));
+  if (good < k)  // zero singular values: orthonormal completion (factorizations.cpp:224-236)
+    orthonormal_completion(c, sub(big, 0, 0, big.rows, good), sub(big, 0, good, big.rows, k - good), 0,
+                           big.rows, rng_substream(rng_key(0x715D), (uint64_t)(m * 131 + n)));
+  // phase convention on the tall factorization's V: the small side in both
+  // orientations (for wide A the reference factors A^*, factorizations.cpp:167-170)
+  qsvd_phase(c, big, small);
+  for (int64_t i = 0; i < k; ++i) sigma_host[i] = sg[i];
+}
+
+int qlra_qsvd(qlra_ctx_t* ctx, const qlra_qmat_t* a, qlra_qmat_t* u, double* sigma, qlra_qmat_t* v) {
+  return guarded(ctx, [&](Ctx& c) {
+    check_view(a, "qsvd");
+    check_view(u, "qsvd");
+    check_view(v, "qsvd");
+    const int64_t k = std::min(a->rows, a->cols);
+    if (u->rows != a->rows || u->cols != k || v->rows != a->cols || v->cols != k)
+      fail(QLRA_ERR_SHAPE, "qsvd: output shape mismatch");
+    qsvd_dev(c, view_of(a), view_of(u), view_of(v), sigma);
+  });
+}
+
+int qlra_truncate_stage(qlra_ctx_t* ctx, const qlra_qmat_t* h, const qlra_qmat_t* x, int64_t r,
+                        qlra_qmat_t* h_out, double* sigma, qlra_qmat_t* v) {
+  return guarded(ctx, [&](Ctx& c) {
+    check_view(h, "truncate_stage");
+    check_view(x, "truncate_stage");
+    check_view(h_out, "truncate_stage");
+    check_view(v, "truncate_stage");
+    if (h->cols != x->rows) fail(QLRA_ERR_SHAPE, "truncate_stage: H and X do not conform");
+    if (r < 1 || r > x->rows) fail(QLRA_ERR_PARAMETER, "truncate_stage: need 1 <= r <= s");
+    if (h_out->rows != h->rows || h_out->cols != r || v->rows != x->cols || v->cols != r)
+      fail(QLRA_ERR_SHAPE, "truncate_stage: output shape mismatch");
+    const int64_t s = x->rows, n = x->cols, k = std::min(s, n);
+    DevQMat uu(c, s, k), vv(c, n, k);
+    std::vector<double> sg(k);
+    qsvd_dev(c, view_of(x), uu.v, vv.v, sg.data());
+    qgemm(c, QLRA_OP_N, QLRA_OP_N, 1.0, view_of(h), sub(uu.v, 0, 0, s, r), 0.0, view_of(h_out));
+    copy_qmat(c, sub(vv.v, 0, 0, n, r), view_of(v));
+    for (int64_t i = 0; i < r; ++i) sigma[i] = sg[i];
+  });
+}
+
+int qlra_approx_residual_fro(qlra_ctx_t* ctx, const qlra_qmat_t* a, const qlra_qmat_t* h,
+                             const double* sigma, const qlra_qmat_t* v, double* res_fro,
+                             double* a_fro) {
+  return guarded(ctx, [&](Ctx& c) {
+    check_view(a, "relative_error");
+    check_view(h, "relative_error");
+    check_view(v, "relative_error");
+    const int64_t r = h->cols, n = v->rows;
+    DeviceBuffer d_s(c, sizeof(double) * (size_t)std::max<int64_t>(1, r));
+    QLRA_CUDA(cudaMemcpyAsync(d_s.ptr, sigma, sizeof(double) * r, cudaMemcpyHostToDevice, c.stream));
+    DevQMat xr(c, r, n);
+    sigma_vadj(c, d_s.as<double>(), view_of(v), xr.v);
+    DeviceBuffer out(c, 2 * sizeof(double));
+    qgemm_residual(c, view_of(a), view_of(h), xr.v, out.as<double>());
+    allreduce_sum(c, out.as<double>(), 2);
+    const std::vector<double> vals = to_host(c, out.as<double>(), 2);
+    if (res_fro) *res_fro = std::sqrt(vals[0]);
+    if (a_fro) *a_fro = std::sqrt(vals[1]);
   });
 }
 

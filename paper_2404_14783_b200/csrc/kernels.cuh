@@ -149,6 +149,17 @@ void small_axpby_identity(Ctx& ctx, double alpha, double beta, const QView& a, c
 void small_set_identity(Ctx& ctx, const QView& out);
 // estimate_epsilon power iterations on chi_{Ginv}: *d_rho (device).
 void small_power_iter_inverse(Ctx& ctx, const QView& ginv, int iters, double* d_rho);
+// Eigendecomposition of a quaternion Hermitian matrix (a destroyed):
+// eigenvalues descending into d_w (device, n), eigenvectors into the columns
+// of vecs (n x n, quaternion-orthonormal); parallel cyclic Jacobi, one CTA.
+void small_quat_eigh(Ctx& ctx, const QView& a, double* d_w, const QView& vecs, int max_sweeps = 30);
+// out(:, j) = a(:, j) * f[j]  (or / f[j] when invert; 0 where f[j] <= floor)
+void scale_cols(Ctx& ctx, const QView& a, const double* d_f, bool invert, double floor_v,
+                const QView& out);
+// out (r x n) = diag(sigma) V^*
+void sigma_vadj(Ctx& ctx, const double* d_sigma, const QView& v, const QView& out);
+// qsvd phase convention on (U, V) columns (factorizations.cpp:273-293)
+void qsvd_phase(Ctx& ctx, const QView& u, const QView& v);
 // Quaternion Cholesky G = R^*R in place (upper triangle), *d_info as above.
 void small_quat_cholesky(Ctx& ctx, const QView& g, int* d_info);
 // x = r^{-1}, r upper triangular quaternion with real diagonal.

@@ -692,6 +692,186 @@ __global__ void __launch_bounds__(SNT) k_qtridiag(QView a, double* d, double* e)
   for (int64_t i = t; i < n; i += blockDim.x) d[i] = a.p[0][i * a.ld + i];
 }
 
+// Parallel cyclic Jacobi eigensolver for a quaternion Hermitian matrix
+// (n x n, full storage, destroyed -> diagonal), one CTA.  For a pivot pair
+// (p, q) with b = G_pq = |b| u (u a unit quaternion) the rotation is
+// Q = diag(1, u^*) J, J = [[c, s], [-s, c]] the real Jacobi rotation of
+// [[G_pp, |b|], [|b|, G_qq]]: rows  p,q <- J^T (row_p, u row_q),
+// columns p,q <- (col_p, col_q u^*) J, eigenvectors V <- V Q.  Working on the
+// s x s quaternion matrix directly (not on the 2s x 2s complex chi form)
+// halves the dimension and produces quaternion-orthonormal eigenvectors with
+// no singular-value pair splitting (cf. factorizations.cpp:60-152).
+// Round-robin (chess tournament) ordering: n/2 disjoint pairs per round.
+__global__ void __launch_bounds__(SNT) k_quat_jacobi(QView g, QView v, double* w, int max_sweeps,
+                                                     double* off_out) {
+  extern __shared__ __align__(16) unsigned char dsm[];
+  const int64_t n = g.rows;
+  const int64_t np = n + (n & 1);  // padded to even (index n is a dummy)
+  int* perm = reinterpret_cast<int*>(dsm);                       // np
+  double* rc = reinterpret_cast<double*>(dsm + ((np * sizeof(int) + 15) / 16) * 16);  // np/2 * 6
+  __shared__ double sh[32];
+  const int t = threadIdx.x;
+  for (int64_t e = t; e < n * n; e += blockDim.x) {
+    const int64_t i = e / n, j = e % n;
+    qstore(v, i, j, Q4{i == j ? 1.0 : 0.0, 0.0, 0.0, 0.0});
+  }
+  for (int64_t i = t; i < np; i += blockDim.x) perm[i] = (int)i;
+  __syncthreads();
+  double scale = 0.0;
+  {
+    double part = 0.0;
+    for (int64_t e = t; e < n * n; e += blockDim.x) {
+      const Q4 q = qload(g, e / n, e % n);
+      part += q.w * q.w + q.x * q.x + q.y * q.y + q.z * q.z;
+    }
+    scale = sqrt(block_sum(part, sh));
+  }
+  const int64_t npairs = np / 2;
+  double off = 0.0;
+  for (int sweep = 0; sweep < max_sweeps && n > 1; ++sweep) {
+    double part = 0.0;
+    for (int64_t e = t; e < n * n; e += blockDim.x) {
+      const int64_t i = e / n, j = e % n;
+      if (i == j) continue;
+      const Q4 q = qload(g, i, j);
+      part += q.w * q.w + q.x * q.x + q.y * q.y + q.z * q.z;
+    }
+    off = sqrt(block_sum(part, sh));
+    if (!(off > 1e-15 * scale)) break;
+    for (int64_t round = 0; round < np - 1; ++round) {
+      // pairs (perm[k], perm[np-1-k]); rotation params into rc[k*6 ..]
+      for (int64_t k = t; k < npairs; k += blockDim.x) {
+        int p = perm[k], q = perm[np - 1 - k];
+        if (p > q) { const int tmp = p; p = q; q = tmp; }
+        double c = 1.0, sn = 0.0;
+        Q4 u{1.0, 0.0, 0.0, 0.0};
+        if (q < n) {
+          const Q4 b = qload(g, p, q);
+          const double nb = sqrt(b.w * b.w + b.x * b.x + b.y * b.y + b.z * b.z);
+          if (nb > 1e-300) {
+            u = Q4{b.w / nb, b.x / nb, b.y / nb, b.z / nb};
+            const double a = g.p[0][p * g.ld + p], d = g.p[0][q * g.ld + q];
+            const double th = (d - a) / (2.0 * nb);
+            const double tt = (th >= 0 ? 1.0 : -1.0) / (fabs(th) + sqrt(th * th + 1.0));
+            c = 1.0 / sqrt(1.0 + tt * tt);
+            sn = tt * c;
+          }
+        }
+        double* r = rc + k * 6;
+        r[0] = c; r[1] = sn; r[2] = u.w; r[3] = u.x; r[4] = u.y; r[5] = u.z;
+      }
+      __syncthreads();
+      // rows: for each pair and column j
+      for (int64_t e = t; e < npairs * n; e += blockDim.x) {
+        const int64_t k = e / n, j = e % n;
+        int p = perm[k], q = perm[np - 1 - k];
+        if (p > q) { const int tmp = p; p = q; q = tmp; }
+        if (q >= n) continue;
+        const double* r = rc + k * 6;
+        const double c = r[0], sn = r[1];
+        const Q4 u{r[2], r[3], r[4], r[5]};
+        const Q4 rp = qload(g, p, j), rq = qmul(u, qload(g, q, j));
+        qstore(g, p, j, Q4{c * rp.w - sn * rq.w, c * rp.x - sn * rq.x, c * rp.y - sn * rq.y, c * rp.z - sn * rq.z});
+        qstore(g, q, j, Q4{sn * rp.w + c * rq.w, sn * rp.x + c * rq.x, sn * rp.y + c * rq.y, sn * rp.z + c * rq.z});
+      }
+      __syncthreads();
+      // columns of G and V
+      for (int64_t e = t; e < npairs * n * 2; e += blockDim.x) {
+        const int64_t which = e / (npairs * n), rem = e % (npairs * n);
+        const int64_t k = rem / n, i = rem % n;
+        int p = perm[k], q = perm[np - 1 - k];
+        if (p > q) { const int tmp = p; p = q; q = tmp; }
+        if (q >= n) continue;
+        const QView& m = which ? v : g;
+        const double* r = rc + k * 6;
+        const double c = r[0], sn = r[1];
+        const Q4 uc{r[2], -r[3], -r[4], -r[5]};
+        const Q4 cp = qload(m, i, p), cq = qmul(qload(m, i, q), uc);
+        qstore(m, i, p, Q4{c * cp.w - sn * cq.w, c * cp.x - sn * cq.x, c * cp.y - sn * cq.y, c * cp.z - sn * cq.z});
+        qstore(m, i, q, Q4{sn * cp.w + c * cq.w, sn * cp.x + c * cq.x, sn * cp.y + c * cq.y, sn * cp.z + c * cq.z});
+      }
+      __syncthreads();
+      // rotate the tournament: keep perm[0], cycle the rest
+      if (t == 0) {
+        const int last = perm[np - 1];
+        for (int64_t i = np - 1; i > 1; --i) perm[i] = perm[i - 1];
+        perm[1] = last;
+      }
+      __syncthreads();
+    }
+  }
+  for (int64_t i = t; i < n; i += blockDim.x) w[i] = g.p[0][i * g.ld + i];
+  if (t == 0 && off_out) *off_out = off / (scale > 0 ? scale : 1.0);
+}
+
+// Sort eigenpairs descending (stable by index): out_w, out_v (columns).
+__global__ void k_sort_eigen(const double* w, QView v, double* out_w, QView out_v) {
+  const int64_t n = v.cols;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+    int64_t rank = 0;
+    const double wi = w[i];
+    for (int64_t j = 0; j < n; ++j) {
+      const double wj = w[j];
+      if (wj > wi || (wj == wi && j < i)) ++rank;
+    }
+    out_w[rank] = wi;
+    for (int64_t r = 0; r < v.rows; ++r) qstore(out_v, r, rank, qload(v, r, i));
+  }
+}
+
+// Column scaling by real factors: out(:, j) = a(:, j) * f[j] (f may be 1/x).
+__global__ void k_scale_cols(QView a, const double* f, int invert, double floor_v, QView out) {
+  const int64_t n = out.rows, m = out.cols;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n * m;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / m, j = e % m;
+    double s = f[j];
+    if (invert) s = s > floor_v ? 1.0 / s : 0.0;
+#pragma unroll
+    for (int p = 0; p < 4; ++p) out.p[p][i * out.ld + j] = a.p[p][i * a.ld + j] * s;
+  }
+}
+
+// out (r x n) = diag(sigma) * V^*  for V (n x r).
+__global__ void k_sigma_vadj(const double* sigma, QView v, QView out) {
+  const int64_t r = out.rows, n = out.cols;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < r * n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = e / n, i = e % n;
+    const Q4 q = qload(v, i, j);
+    const double sg = sigma[j];
+    qstore(out, j, i, Q4{sg * q.w, -sg * q.x, -sg * q.y, -sg * q.z});
+  }
+}
+
+// qsvd phase convention (factorizations.cpp:273-293): per column j the
+// largest-modulus entry of V (lowest index on ties) becomes positive real by
+// right-multiplying column j of U and V with conj(e)/|e|.  One warp / column.
+__global__ void k_qsvd_phase(QView u, QView v) {
+  const int lane = threadIdx.x & 31;
+  const int64_t j = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (j >= v.cols) return;
+  double best = -1.0;
+  int64_t arg = 0;
+  for (int64_t i = lane; i < v.rows; i += 32) {
+    const Q4 q = qload(v, i, j);
+    const double ns = q.w * q.w + q.x * q.x + q.y * q.y + q.z * q.z;
+    if (ns > best) { best = ns; arg = i; }
+  }
+  for (int off = 16; off > 0; off >>= 1) {
+    const double ob = __shfl_xor_sync(0xffffffffu, best, off);
+    const int64_t oa = __shfl_xor_sync(0xffffffffu, arg, off);
+    if (ob > best || (ob == best && oa < arg)) { best = ob; arg = oa; }
+  }
+  const Q4 e = qload(v, arg, j);
+  const double ae = sqrt(e.w * e.w + e.x * e.x + e.y * e.y + e.z * e.z);
+  if (!(ae > 0.0)) return;
+  const Q4 ph{e.w * (1.0 / ae), -e.x * (1.0 / ae), -e.y * (1.0 / ae), -e.z * (1.0 / ae)};
+  __syncwarp();
+  for (int64_t i = lane; i < u.rows; i += 32) qstore(u, i, j, qmul(qload(u, i, j), ph));
+  for (int64_t i = lane; i < v.rows; i += 32) qstore(v, i, j, qmul(qload(v, i, j), ph));
+}
+
 unsigned grid_for(int64_t total) {
   int64_t b = (total + 255) / 256;
   if (b < 1) b = 1;
@@ -757,6 +937,42 @@ void small_quat_herm_eigvals(Ctx& ctx, const QView& a, double* d_w, bool extreme
   } else {
     k_bisect<<<(unsigned)((n + 255) / 256), 256, 0, ctx.stream>>>(d, e, n, d_w, 0);
   }
+  QLRA_LAUNCH_CHECK();
+  count_launch();
+}
+void small_quat_eigh(Ctx& ctx, const QView& a, double* d_w, const QView& vecs, int max_sweeps) {
+  const int64_t n = a.rows;
+  if (n == 0) return;
+  const int64_t np = n + (n & 1);
+  const size_t smem = ((np * sizeof(int) + 15) / 16) * 16 + sizeof(double) * 6 * (size_t)(np / 2 + 1);
+  static size_t attr = 0;
+  if (smem > 48 * 1024 && smem > attr) {
+    QLRA_CUDA(cudaFuncSetAttribute(k_quat_jacobi, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = smem;
+  }
+  DevQMat v(ctx, n, n);
+  DeviceBuffer w(ctx, sizeof(double) * (size_t)n);
+  k_quat_jacobi<<<1, SNT, smem, ctx.stream>>>(a, v.v, w.as<double>(), max_sweeps, nullptr);
+  QLRA_LAUNCH_CHECK();
+  count_launch();
+  k_sort_eigen<<<1, 256, 0, ctx.stream>>>(w.as<double>(), v.v, d_w, vecs);
+  QLRA_LAUNCH_CHECK();
+  count_launch();
+}
+void scale_cols(Ctx& ctx, const QView& a, const double* d_f, bool invert, double floor_v,
+                const QView& out) {
+  k_scale_cols<<<grid_for(out.rows * out.cols), 256, 0, ctx.stream>>>(a, d_f, invert ? 1 : 0, floor_v, out);
+  QLRA_LAUNCH_CHECK();
+  count_launch();
+}
+void sigma_vadj(Ctx& ctx, const double* d_sigma, const QView& v, const QView& out) {
+  k_sigma_vadj<<<grid_for(out.rows * out.cols), 256, 0, ctx.stream>>>(d_sigma, v, out);
+  QLRA_LAUNCH_CHECK();
+  count_launch();
+}
+void qsvd_phase(Ctx& ctx, const QView& u, const QView& v) {
+  if (v.cols == 0) return;
+  k_qsvd_phase<<<(unsigned)((v.cols + 7) / 8), 256, 0, ctx.stream>>>(u, v);
   QLRA_LAUNCH_CHECK();
   count_launch();
 }

@@ -569,6 +569,79 @@ def one_pass_qb(a, opts: OnePassOptions, ctx=None, row0=0, m_global=None, residu
                                            solve_s=qb.solve_s))
 
 
+# --------------------------------------------------------- truncation ---
+def qsvd(a, ctx=None):
+    """qsvd (factorizations.cpp:166-295): (U, sigma, V) with A = U diag(sigma) V^*."""
+    ctx = _ctx(ctx)
+    m, n = a.shape[1], a.shape[2]
+    k = min(m, n)
+    u, v = qzeros(m, k), qzeros(n, k)
+    sg = (C.c_double * max(1, k))()
+    ctx._check(ctx.lib.qlra_qsvd(ctx.h, C.byref(_qm(a)), C.byref(_qm(u)), sg, C.byref(_qm(v))))
+    return u, [sg[i] for i in range(k)], v
+
+
+@dataclass
+class ApproxResult:
+    """== ApproxResult (sketching.hpp:118-123)."""
+    h: torch.Tensor
+    sigma: list
+    v: torch.Tensor
+    diagnostics: dict = field(default_factory=dict)
+
+
+def truncate_stage(h, x, r, ctx=None) -> ApproxResult:
+    """truncate_stage (sketching.cpp:196-211): QSVD of X, keep r triples, fold U_r into H."""
+    ctx = _ctx(ctx)
+    ho, v = qzeros(h.shape[1], r), qzeros(x.shape[2], r)
+    sg = (C.c_double * max(1, r))()
+    ctx._check(ctx.lib.qlra_truncate_stage(ctx.h, C.byref(_qm(h)), C.byref(_qm(x)), r, C.byref(_qm(ho)), sg,
+                                           C.byref(_qm(v))))
+    return ApproxResult(ho, [sg[i] for i in range(r)], v)
+
+
+def approx_reconstruct(res: ApproxResult, ctx=None):
+    """approx_reconstruct (sketching.cpp:213-218): H diag(sigma) V^*."""
+    ctx = _ctx(ctx)
+    hs = res.h * torch.tensor(res.sigma, dtype=torch.float64, device=res.h.device)[None, None, :]
+    return qmat_mul(hs, res.v, op_b=OP_C, ctx=ctx)
+
+
+def approx_residual_fro(a, res: ApproxResult, ctx=None):
+    """(||A - H S V^*||_F, ||A||_F) -- relative_error's terms (analysis.cpp:75-79)."""
+    ctx = _ctx(ctx)
+    sg = (C.c_double * max(1, len(res.sigma)))(*res.sigma)
+    r, n = C.c_double(), C.c_double()
+    ctx._check(ctx.lib.qlra_approx_residual_fro(ctx.h, C.byref(_qm(a)), C.byref(_qm(res.h)), sg,
+                                                C.byref(_qm(res.v)), C.byref(r), C.byref(n)))
+    return r.value, n.value
+
+
+def one_pass_approx(a, opts: OnePassOptions, ctx=None) -> ApproxResult:
+    """one_pass_approx (sketching.cpp:250-275): sketch -> QB stage -> truncation,
+    with the qb_residual / relative_error diagnostics (second read of A)."""
+    ctx = _ctx(ctx)
+    o = resolve_defaults(opts)
+    t0 = time.perf_counter()
+    st = make_sketch(a, o.r, o.s, o.l, o.omega_seed, o.psi_seed, o.embedding, o.density, ctx)
+    ctx.synchronize()
+    t1 = time.perf_counter()
+    qb = qb_stage(st, o.rangefinder, o.rangefinder_seed, o.qr_cfg, ctx)
+    t2 = time.perf_counter()
+    res = truncate_stage(qb.h, qb.x, o.r, ctx)
+    ctx.synchronize()
+    t3 = time.perf_counter()
+    qres, na = residual_fro(a, qb.h, qb.x, ctx)
+    diff, _ = approx_residual_fro(a, res, ctx)
+    rel = diff / na if na > 0 else (float("inf") if diff > 0 else 0.0)
+    res.diagnostics = dict(kappa_h=qb.report.kappa_after, kappa_before=qb.report.kappa_before,
+                           correction_steps=qb.report.correction_steps_used, qb_residual=qres,
+                           relative_error=rel,
+                           times=dict(sketch_s=t1 - t0, rangefinder_s=qb.rangefinder_s, solve_s=qb.solve_s,
+                                      truncate_s=t3 - t2))
+    return res
+
+
 def measure_fp64_peak(mode=0, ms=200.0, ctx=None):
     ctx = _ctx(ctx)
     t = C.c_double()

@@ -260,3 +260,72 @@ def test_host_streaming_sketch_matches_device(ctx):  # sketching.cpp:156-167 str
         st = Q.make_sketch_host(ah, 8, 10, 20, 3, 4, ctx=ctx, block_rows=br)
         assert rel_diff(host(st.y), host(whole.y)) < 1e-14
         assert rel_diff(host(st.w), host(whole.w)) < 1e-13
+
+
+# ------------------------------------------------- pseudo-SVD bad blocks ---
+def test_pseudo_svd_rank_deficient(ctx):  # test_rangefinders.cpp:119-141, test_sketching.cpp:256-277
+    from paper_2404_14783_b200 import qlra as Q
+    y = planted_matrix_with_sigma(100, [1, 1, 0.5, 0.3, 0.1, 1e-6, 1e-10, 1e-14, 1e-14, 1e-14], 60)
+    rep = Q.pseudo_svd(dev(y), ctx=ctx)
+    h = host(rep.h)
+    assert orthonormality_defect(h) < 1e-8
+    proj = O.qmat_mul(h, O.qmat_mul(O.adjoint(h), y))
+    assert rel_diff(proj, y) <= 1e-6
+    # zero sketch: orthonormal H, kappa infinite
+    z = Q.pseudo_svd(dev(np.zeros((4, 20, 7))), ctx=ctx)
+    assert orthonormality_defect(host(z.h)) < 1e-10
+    assert not np.isfinite(z.kappa_before)
+    # duplicated column (rank-deficient) that pseudo_qr refuses
+    g = random_gaussian(12, 3, 53)
+    yy = np.concatenate([g, g[:, :, 1:2]], axis=2)
+    hh = host(Q.pseudo_svd(dev(yy), ctx=ctx).h)
+    assert orthonormality_defect(hh) < 1e-10
+    assert rel_diff(O.qmat_mul(hh, O.qmat_mul(O.adjoint(hh), yy)), yy) < 1e-10
+
+
+# ----------------------------------------------------------- truncation ---
+def test_qsvd_on_device(ctx):  # test_factorizations.cpp:73-112
+    from paper_2404_14783_b200 import qlra as Q
+    u, sg, v = Q.qsvd(dev(diag_real([2.0, 1.0])), ctx)
+    assert np.allclose(sg, [2.0, 1.0], rtol=1e-14)
+    assert rel_diff(host(u), diag_real([1.0, 1.0])) < 1e-12 and rel_diff(host(v), diag_real([1.0, 1.0])) < 1e-12
+    for m, n in ((6, 4), (3, 6), (30, 20)):
+        a = random_gaussian(m, n, 34)
+        u, sg, v = Q.qsvd(dev(a), ctx)
+        rec = O.qmat_mul(host(u) * np.asarray(sg)[None, None, :], O.adjoint(host(v)))
+        assert rel_diff(rec, a) < 1e-12
+        assert orthonormality_defect(host(u)) < 1e-12 and orthonormality_defect(host(v)) < 1e-12
+        uo, so, vo = O.qsvd(a)
+        assert np.allclose(sg, so, rtol=1e-12)
+        # phase convention pins the factors (distinct singular values)
+        assert rel_diff(host(u), uo) < 1e-9 and rel_diff(host(v), vo) < 1e-9
+
+
+def test_truncate_stage_and_one_pass_vs_oracle(ctx):  # test_sketching.cpp:210-223, 279-290
+    from paper_2404_14783_b200 import configs, qlra as Q
+    h, xr = random_gaussian(6, 3, 51), random_gaussian(3, 8, 52)
+    res = Q.truncate_stage(dev(h), dev(xr), 3, ctx)
+    assert rel_diff(host(Q.approx_reconstruct(res, ctx)), O.qmat_mul(h, xr)) < 1e-12
+    with pytest.raises(Q.ParameterError):
+        Q.truncate_stage(dev(h), dev(xr), 4, ctx)
+    cfg = configs.CONFIGS["C1"]
+    a = configs.build_matrix(cfg, ctx=ctx)
+    r = cfg.s - 5
+    out = Q.one_pass_approx(a, Q.OnePassOptions(r=r, s=cfg.s, l=cfg.l), ctx=ctx)
+    ah = host(a)
+    y, w = O.make_sketch(ah, r, cfg.s, cfg.l, 1, 2, nthreads=8)
+    qb = O.qb_stage(y, w, 2, O.PSEUDO_QR, nthreads=8)
+    ho, so, vo = O.truncate_stage(qb["h"], qb["x"], r)
+    sd = np.asarray(out.sigma)
+    rdiff = np.abs(sd / so - 1)
+    # leading (signal) singular values to 1e-10; the noise-level tail is
+    # resolved through the Gram of X (error ~ u (s1/si)^2)
+    big = so > 1e-2 * so[0]
+    assert rdiff[big].max() < 1e-10, rdiff
+    assert rdiff.max() < 1e-6, rdiff
+    rec_o = O.qmat_mul(ho * so[None, None, :], O.adjoint(vo))
+    rel_o = np.sqrt(np.sum((ah - rec_o) ** 2) / np.sum(ah ** 2))
+    assert abs(out.diagnostics["relative_error"] / rel_o - 1) < 1e-9, (out.diagnostics["relative_error"], rel_o)
+    assert all(out.sigma[i] >= out.sigma[i + 1] for i in range(r - 1))
+    z = Q.one_pass_approx(Q.qzeros(20, 16), Q.OnePassOptions(r=2, rangefinder=Q.PSEUDO_SVD), ctx=ctx)
+    assert z.sigma[0] == 0.0 and z.diagnostics["relative_error"] == 0.0
