@@ -217,14 +217,25 @@ def main():
 
     sk_events = []
 
+    used = {"rangefinder": args.rangefinder}
+
     def step(a_dev):
+        nonlocal method
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         st = Q.make_sketch(a_dev, opts.r, opts.s, opts.l, opts.omega_seed, opts.psi_seed, cfg.kind,
                            ctx=ctx, row0=r0, m_global=cfg.m)
         e1.record(stream)
         sk_events.append((e0, e1))
-        qb = Q.qb_stage(st, method, ctx=ctx)
+        try:
+            qb = Q.qb_stage(st, method, ctx=ctx)
+        except Q.RankError:
+            # pseudo-QR refuses kappa(H) beyond its domain exactly as the
+            # reference does ("use pseudo_svd", rangefinders.cpp:122-123);
+            # follow that advice and record it (C3: kappa(Y) ~ 1e8).
+            method = Q.PSEUDO_SVD
+            used["rangefinder"] = "pseudo_svd (pseudo_qr raised RankError, as the reference does)"
+            qb = Q.qb_stage(st, method, ctx=ctx)
         return st, qb
 
     for _ in range(args.warmup):
@@ -336,7 +347,7 @@ def main():
                                         "MEASURED_PEAKS.json has no FP64 entry): " + json.dumps(peaks),
                          "note": "FP64 tensor pipe (DMMA); per-unit = 32 flop per quaternion MAC, "
                                  "a launch covers one L2-resident row panel: 32*rows*n*(s+l) flop"},
-            "rel_error": res / an, "e2e": e2e, "gpu_launches": int(launches), "clocks": clk.summary(),
+            "rangefinder_used": used["rangefinder"], "rel_error": res / an, "e2e": e2e, "gpu_launches": int(launches), "clocks": clk.summary(),
             "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)

@@ -329,3 +329,45 @@ def test_truncate_stage_and_one_pass_vs_oracle(ctx):  # test_sketching.cpp:210-2
     assert all(out.sigma[i] >= out.sigma[i + 1] for i in range(r - 1))
     z = Q.one_pass_approx(Q.qzeros(20, 16), Q.OnePassOptions(r=2, rangefinder=Q.PSEUDO_SVD), ctx=ctx)
     assert z.sigma[0] == 0.0 and z.diagnostics["relative_error"] == 0.0
+
+
+@pytest.mark.slow
+def test_c3_pseudo_qr_refusal_matches_reference(ctx):
+    """C3 (rank 200 + 1e-6 noise, s = 220): kappa(Y) ~ 1e8 is outside
+    pseudo-QR's domain; the reference's algorithm (oracle, same Y) raises
+    RankError and so must the device path.  pseudo-SVD then succeeds."""
+    from paper_2404_14783_b200 import configs, qlra as Q
+    cfg = configs.CONFIGS["C3"]
+    a = configs.build_matrix(cfg, ctx=ctx)
+    st = Q.make_sketch(a, cfg.s - 5, cfg.s, cfg.l, 1, 2, cfg.kind, ctx=ctx)
+    del a
+    y = host(st.y)
+    with pytest.raises(O.OracleError) as e:
+        O.pseudo_qr(y)
+    assert e.value.kind == "RankError"
+    with pytest.raises(Q.RankError):
+        Q.pseudo_qr(st.y, ctx=ctx)
+    rep = Q.pseudo_svd(st.y, ctx=ctx)
+    # kappa(Y) ~ 1e8: the noise-level directions of range(Y) are determined
+    # only to u*kappa ~ 1e-8 by ANY implementation, so 1e-6 here.
+    assert largest_principal_angle(host(rep.h), O.pseudo_svd(y)["h"]) < 1e-6
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("method", [0, 1])
+def test_c2_full_size_parity(ctx, method):
+    """The benchmarked workload (C2, 8000 x 6000, s = 100, l = 200) end to end
+    against the oracle on the same A (oracle sketch on all host threads)."""
+    import os
+    from paper_2404_14783_b200 import configs, qlra as Q
+    cfg = configs.CONFIGS["C2"]
+    a = configs.build_matrix(cfg, ctx=ctx)
+    res = Q.one_pass_qb(a, Q.OnePassOptions(r=cfg.s - 5, s=cfg.s, l=cfg.l, rangefinder=method), ctx=ctx)
+    ah = host(a)
+    y, w = O.make_sketch(ah, cfg.s - 5, cfg.s, cfg.l, 1, 2, nthreads=os.cpu_count() or 8)
+    assert rel_diff(host(res.state.y), y) < 1e-13 and rel_diff(host(res.state.w), w) < 1e-13
+    qb = O.qb_stage(y, w, 2, method, nthreads=os.cpu_count() or 8)
+    rs, an = O.residual_sq(ah, qb["h"], qb["x"])
+    err_o, err_d = np.sqrt(rs / an), res.qb_residual / res.a_fro
+    assert abs(err_d / err_o - 1) <= 1e-10, (err_d, err_o)
+    assert largest_principal_angle(host(res.qb.h), qb["h"]) <= 1e-8
