@@ -125,13 +125,8 @@ std::vector<double> quat_inverse(Ctx& ctx, const QView& a, const QView& ainv, bo
 // then one small DMMA product).  False if G is not numerically PD.
 bool hpd_inverse(Ctx& ctx, const QView& g, const QView& ginv, std::vector<double>* rdiag) {
   const int64_t s = g.rows;
-  DevQMat r(ctx, s, s), ri(ctx, s, s);
-  copy_qmat(ctx, g, r.v);
-  DeviceBuffer info(ctx, sizeof(int));
-  small_quat_cholesky(ctx, r.v, info.as<int>());
-  if (info_to_host(ctx, info.as<int>()) != 0) return false;
-  if (rdiag) *rdiag = diag_to_host(ctx, r.v.p[0], r.v.ld, s);
-  small_quat_triinv_upper(ctx, r.v, ri.v);
+  DevQMat ri(ctx, s, s);
+  if (!blocked_chol_inv(ctx, g, ri.v, rdiag)) return false;
   qgemm(ctx, QLRA_OP_N, QLRA_OP_C, 1.0, ri.v, ri.v, 0.0, ginv);
   return true;
 }
@@ -152,23 +147,12 @@ bool cqr_pass(Ctx& ctx, const QView& y, const QView& hout, bool complex_mode, do
     for (double v : d) t += v;
     *trace_g = t;
   }
+  // complex_qr's R: Cholesky of the complex part (j, k planes zeroed; the
+  // quaternion factorisation then stays inside the complex subalgebra).
+  if (complex_mode) zero_jk_planes(ctx, g.v);
+  if (shift != 0.0) small_add_diag(ctx, g.v, shift);
   DevQMat rinv(ctx, s, s);
-  DeviceBuffer info(ctx, sizeof(int));
-  if (complex_mode) {
-    DeviceBuffer c(ctx, sizeof(double2) * (size_t)(s * s));
-    small_complex_part(ctx, g.v, c.as<double2>(), s);
-    if (shift != 0.0) small_add_diag_complex(ctx, c.as<double2>(), s, s, shift);
-    small_cholesky(ctx, c.as<double2>(), s, s, info.as<int>());
-    if (info_to_host(ctx, info.as<int>()) != 0) return false;
-    if (rdiag) *rdiag = diag_to_host(ctx, reinterpret_cast<double*>(c.ptr), s, s, 2);
-    small_inv_lower_adjoint_to_quat(ctx, c.as<double2>(), s, s, rinv.v);
-  } else {
-    if (shift != 0.0) small_add_diag(ctx, g.v, shift);
-    small_quat_cholesky(ctx, g.v, info.as<int>());
-    if (info_to_host(ctx, info.as<int>()) != 0) return false;
-    if (rdiag) *rdiag = diag_to_host(ctx, g.v.p[0], g.v.ld, s);
-    small_quat_triinv_upper(ctx, g.v, rinv.v);
-  }
+  if (!blocked_chol_inv(ctx, g.v, rinv.v, rdiag)) return false;
   qgemm(ctx, QLRA_OP_N, QLRA_OP_N, 1.0, y, rinv.v, 0.0, hout);
   return true;
 }

@@ -160,6 +160,11 @@ void scale_cols(Ctx& ctx, const QView& a, const double* d_f, bool invert, double
 void sigma_vadj(Ctx& ctx, const double* d_sigma, const QView& v, const QView& out);
 // qsvd phase convention on (U, V) columns (factorizations.cpp:273-293)
 void qsvd_phase(Ctx& ctx, const QView& u, const QView& v);
+// Blocked quaternion Cholesky G = R^*R (R upper) returning R^{-1} in rinv
+// (s x s, fully written) and diag(R); false if G is not numerically PD.
+bool blocked_chol_inv(Ctx& ctx, const QView& g, const QView& rinv, std::vector<double>* rdiag);
+// zero the j, k planes (restrict a quaternion matrix to its complex part)
+void zero_jk_planes(Ctx& ctx, const QView& g);
 // Quaternion Cholesky G = R^*R in place (upper triangle), *d_info as above.
 void small_quat_cholesky(Ctx& ctx, const QView& g, int* d_info);
 // x = r^{-1}, r upper triangular quaternion with real diagonal.

@@ -11,6 +11,8 @@
 //                                       rangefinders.cpp:71-93)
 // Matrices live in global memory (L2-resident at these sizes) and are worked
 // on by one 1024-thread CTA; every reduction has a fixed order.
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -872,6 +874,192 @@ __global__ void k_qsvd_phase(QView u, QView v) {
   for (int64_t i = lane; i < v.rows; i += 32) qstore(v, i, j, qmul(qload(v, i, j), ph));
 }
 
+// Cholesky + inverse of one diagonal block (nb <= 64) in shared memory:
+// G = R^* R (R upper, real positive diagonal) and X = R^{-1} by the in-place
+// column recurrence x_{0:j, j} = -X_{0:j,0:j} r_{0:j,j} / r_jj (LAPACK trti2
+// order).  Quaternion arithmetic throughout; complex inputs (j,k planes 0)
+// stay complex.  One CTA; *info = 0 or first failing column (1-based).
+constexpr int CB = 64;
+__global__ void __launch_bounds__(SNT) k_qchol_block(QView g, QView r, QView rinv, int* info,
+                                                     double* rdiag) {
+  extern __shared__ __align__(16) unsigned char dsm[];
+  Q4* a = reinterpret_cast<Q4*>(dsm);  // CB x CB
+  __shared__ Q4 tmp[CB];
+  __shared__ int s_bad;
+  const int n = (int)g.rows, t = threadIdx.x;
+  for (int e = t; e < n * n; e += blockDim.x) {
+    const int i = e / n, j = e % n;
+    a[i * CB + j] = j >= i ? qload(g, i, j) : Q4{0.0, 0.0, 0.0, 0.0};
+  }
+  if (t == 0) s_bad = 0;
+  __syncthreads();
+  for (int k = 0; k < n; ++k) {
+    if (t == 0) {
+      const double d = a[k * CB + k].w;
+      if (!(d > 0.0)) {
+        s_bad = k + 1;
+      } else {
+        a[k * CB + k] = Q4{sqrt(d), 0.0, 0.0, 0.0};
+      }
+    }
+    __syncthreads();
+    if (s_bad) break;
+    const double inv = 1.0 / a[k * CB + k].w;
+    for (int j = k + 1 + t; j < n; j += blockDim.x) {
+      Q4 q = a[k * CB + j];
+      a[k * CB + j] = Q4{q.w * inv, q.x * inv, q.y * inv, q.z * inv};
+    }
+    __syncthreads();
+    const int rr = n - k - 1;
+    for (int e = t; e < rr * rr; e += blockDim.x) {
+      const int i = k + 1 + e / rr, j = k + 1 + e % rr;
+      if (j < i) continue;
+      Q4 ai = a[k * CB + i];
+      ai.x = -ai.x; ai.y = -ai.y; ai.z = -ai.z;
+      const Q4 pq = qmul(ai, a[k * CB + j]);
+      Q4 c = a[i * CB + j];
+      c.w -= pq.w; c.x -= pq.x; c.y -= pq.y; c.z -= pq.z;
+      a[i * CB + j] = c;
+    }
+    __syncthreads();
+  }
+  if (s_bad) {
+    if (t == 0) *info = s_bad;
+    return;
+  }
+  if (t == 0) *info = 0;
+  for (int e = t; e < n * n; e += blockDim.x) {
+    const int i = e / n, j = e % n;
+    qstore(r, i, j, j >= i ? a[i * CB + j] : Q4{0.0, 0.0, 0.0, 0.0});
+  }
+  for (int i = t; i < n; i += blockDim.x) if (rdiag) rdiag[i] = a[i * CB + i].w;
+  __syncthreads();
+  // in-place inverse, column by column
+  for (int j = 0; j < n; ++j) {
+    const double ajj = 1.0 / a[j * CB + j].w;
+    // tmp[i] = sum_{k=i..j-1} X_ik r_kj   for i < j   (X = already inverted block)
+    for (int i = t; i < j; i += blockDim.x) {
+      Q4 acc{0.0, 0.0, 0.0, 0.0};
+      for (int k = i; k < j; ++k) {
+        const Q4 pq = qmul(a[i * CB + k], a[k * CB + j]);
+        acc.w += pq.w; acc.x += pq.x; acc.y += pq.y; acc.z += pq.z;
+      }
+      tmp[i] = acc;
+    }
+    __syncthreads();
+    for (int i = t; i < j; i += blockDim.x)
+      a[i * CB + j] = Q4{-tmp[i].w * ajj, -tmp[i].x * ajj, -tmp[i].y * ajj, -tmp[i].z * ajj};
+    if (t == 0) a[j * CB + j] = Q4{ajj, 0.0, 0.0, 0.0};
+    __syncthreads();
+  }
+  for (int e = t; e < n * n; e += blockDim.x) {
+    const int i = e / n, j = e % n;
+    qstore(rinv, i, j, j >= i ? a[i * CB + j] : Q4{0.0, 0.0, 0.0, 0.0});
+  }
+}
+
+__global__ void k_zero_jk(QView g) {
+  const int64_t n = g.rows, m = g.cols;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n * m;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / m, j = e % m;
+    g.p[2][i * g.ld + j] = 0.0;
+    g.p[3][i * g.ld + j] = 0.0;
+  }
+}
+
+// Cooperative multi-CTA version of k_qtridiag for large n (every CTA is
+// resident; grid.sync() separates the phases of each Householder step).
+// Reductions: per-CTA partial sums in fixed order, then every CTA sums the
+// partials in CTA order, so all CTAs hold bitwise-identical scalars.  The
+// reflector v is never stored: v_0 = x_1 + phi*alpha, v_i = x_i = A(k+1+i, k).
+__global__ void __launch_bounds__(512) k_qtridiag_coop(QView a, double* d, double* e, double* part,
+                                                       Q4* pvec) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double sh[32];
+  const int64_t n = a.rows;
+  const int t = threadIdx.x, lane = t & 31;
+  const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + t, gthreads = (int64_t)gridDim.x * blockDim.x;
+  const int64_t gwarp = gtid >> 5, gwarps = gthreads >> 5;
+  const int nb = gridDim.x;
+  for (int64_t k = 0; k + 1 < n; ++k) {
+    const int64_t len = n - k - 1, o = k + 1;
+    // phase A: ||x||^2 partials
+    double pa = 0.0;
+    for (int64_t i = gtid; i < len; i += gthreads) {
+      const Q4 q = qload(a, o + i, k);
+      pa += q.w * q.w + q.x * q.x + q.y * q.y + q.z * q.z;
+    }
+    pa = block_sum(pa, sh);
+    if (t == 0) part[blockIdx.x] = pa;
+    grid.sync();
+    double nrm2 = 0.0;
+    for (int b = 0; b < nb; ++b) nrm2 += part[b];
+    const Q4 x1 = qload(a, o, k);
+    const double ax1 = sqrt(x1.w * x1.w + x1.x * x1.x + x1.y * x1.y + x1.z * x1.z);
+    const double alpha = sqrt(nrm2);
+    const Q4 phi = ax1 > 0.0 ? Q4{x1.w / ax1, x1.x / ax1, x1.y / ax1, x1.z / ax1} : Q4{1.0, 0.0, 0.0, 0.0};
+    const double beta = alpha > 0.0 ? 2.0 / (2.0 * alpha * alpha + 2.0 * alpha * ax1) : 0.0;
+    if (gtid == 0) e[k] = alpha;
+    if (beta == 0.0) {
+      grid.sync();
+      continue;
+    }
+    const Q4 v0{x1.w + phi.w * alpha, x1.x + phi.x * alpha, x1.y + phi.y * alpha, x1.z + phi.z * alpha};
+    // phase C: p = beta A22 v (warp per row) and partials of Re(v^* p)
+    double pc = 0.0;
+    for (int64_t r = gwarp; r < len; r += gwarps) {
+      Q4 acc{0.0, 0.0, 0.0, 0.0};
+      const int64_t row = (o + r) * a.ld + o;
+      for (int64_t c = lane; c < len; c += 32) {
+        const Q4 av{a.p[0][row + c], a.p[1][row + c], a.p[2][row + c], a.p[3][row + c]};
+        const Q4 vc = c == 0 ? v0 : qload(a, o + c, k);
+        const Q4 pq = qmul(av, vc);
+        acc.w += pq.w; acc.x += pq.x; acc.y += pq.y; acc.z += pq.z;
+      }
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) {
+        acc.w += __shfl_xor_sync(0xffffffffu, acc.w, off);
+        acc.x += __shfl_xor_sync(0xffffffffu, acc.x, off);
+        acc.y += __shfl_xor_sync(0xffffffffu, acc.y, off);
+        acc.z += __shfl_xor_sync(0xffffffffu, acc.z, off);
+      }
+      if (lane == 0) {
+        const Q4 pr{beta * acc.w, beta * acc.x, beta * acc.y, beta * acc.z};
+        pvec[r] = pr;
+        const Q4 vr = r == 0 ? v0 : qload(a, o + r, k);
+        pc += vr.w * pr.w + vr.x * pr.x + vr.y * pr.y + vr.z * pr.z;
+      }
+    }
+    pc = block_sum(pc, sh);
+    if (t == 0) part[nb + blockIdx.x] = pc;
+    grid.sync();
+    double c = 0.0;
+    for (int b = 0; b < nb; ++b) c += part[nb + b];
+    const double hk = 0.5 * beta * c;
+    // phase E: A22 -= v w^* + w v^*,  w = p - hk v.  Column k (x) is still
+    // read as v here, so it is updated by nobody (it is outside A22).
+    for (int64_t q = gtid; q < len * len; q += gthreads) {
+      const int64_t r = q / len, cc = q % len;
+      const Q4 vr = r == 0 ? v0 : qload(a, o + r, k);
+      const Q4 vcc = cc == 0 ? v0 : qload(a, o + cc, k);
+      const Q4 pr = pvec[r], pcc = pvec[cc];
+      const Q4 wr{pr.w - hk * vr.w, pr.x - hk * vr.x, pr.y - hk * vr.y, pr.z - hk * vr.z};
+      Q4 wc{pcc.w - hk * vcc.w, -(pcc.x - hk * vcc.x), -(pcc.y - hk * vcc.y), -(pcc.z - hk * vcc.z)};
+      Q4 vc{vcc.w, -vcc.x, -vcc.y, -vcc.z};
+      const Q4 t1 = qmul(vr, wc), t2 = qmul(wr, vc);
+      const int64_t off = (o + r) * a.ld + o + cc;
+      a.p[0][off] -= t1.w + t2.w;
+      a.p[1][off] -= t1.x + t2.x;
+      a.p[2][off] -= t1.y + t2.y;
+      a.p[3][off] -= t1.z + t2.z;
+    }
+    grid.sync();
+  }
+  for (int64_t i = gtid; i < n; i += gthreads) d[i] = a.p[0][i * a.ld + i];
+}
+
 unsigned grid_for(int64_t total) {
   int64_t b = (total + 255) / 256;
   if (b < 1) b = 1;
@@ -928,9 +1116,27 @@ void small_quat_herm_eigvals(Ctx& ctx, const QView& a, double* d_w, bool extreme
     QLRA_CUDA(cudaFuncSetAttribute(k_qtridiag, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = smem;
   }
-  k_qtridiag<<<1, SNT, smem, ctx.stream>>>(a, d, e);
-  QLRA_LAUNCH_CHECK();
-  count_launch();
+  if (n > 160) {
+    // large n: cooperative grid over all SMs
+    int dev = 0, sms = 148, per_sm = 0;
+    QLRA_CUDA(cudaGetDevice(&dev));
+    QLRA_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    QLRA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_qtridiag_coop, 512, 0));
+    const int blocks = std::max(1, std::min(sms * std::max(per_sm, 1), sms));
+    DeviceBuffer part(ctx, sizeof(double) * 2 * (size_t)blocks);
+    DeviceBuffer pv(ctx, sizeof(Q4) * (size_t)n);
+    QView av = a;
+    double* pp = part.as<double>();
+    Q4* pvp = pv.as<Q4>();
+    void* args[] = {&av, &d, &e, &pp, &pvp};
+    QLRA_CUDA(cudaLaunchCooperativeKernel((const void*)k_qtridiag_coop, dim3(blocks), dim3(512), args, 0,
+                                          ctx.stream));
+    count_launch();
+  } else {
+    k_qtridiag<<<1, SNT, smem, ctx.stream>>>(a, d, e);
+    QLRA_LAUNCH_CHECK();
+    count_launch();
+  }
   if (extremes_only) {
     // w[0] = max, w[n-1] = min; the middle stays untouched
     k_multisect_extremes<<<1, 1024, 0, ctx.stream>>>(d, e, n, d_w);
@@ -976,6 +1182,70 @@ void qsvd_phase(Ctx& ctx, const QView& u, const QView& v) {
   QLRA_LAUNCH_CHECK();
   count_launch();
 }
+// Blocked right-looking quaternion Cholesky G = R^* R and R^{-1}: 64-wide
+// diagonal blocks factor+invert in shared memory (k_qchol_block), panels
+// R_12 = R_11^{-*} G_12 and trailing updates G_22 -= R_12^* R_12 run on the
+// DMMA GEMM, and R^{-1} follows by block back-substitution
+// X_{i, i+1:} = -R_ii^{-1} (R_{i, i+1:} X_{i+1:, i+1:}).
+bool blocked_chol_inv(Ctx& ctx, const QView& g, const QView& rinv, std::vector<double>* rdiag) {
+  const int64_t s = g.rows;
+  if (s == 0) return true;
+  static bool attr = false;
+  const size_t smem = sizeof(Q4) * CB * CB;
+  if (!attr) {
+    QLRA_CUDA(cudaFuncSetAttribute(k_qchol_block, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = true;
+  }
+  DevQMat work(ctx, s, s), r(ctx, s, s);
+  copy_qmat(ctx, g, work.v);
+  r.zero(ctx);
+  for (int p = 0; p < 4; ++p)
+    QLRA_CUDA(cudaMemset2DAsync(rinv.p[p], (size_t)rinv.ld * sizeof(double), 0,
+                                (size_t)s * sizeof(double), (size_t)s, ctx.stream));
+  DeviceBuffer info(ctx, sizeof(int) * (size_t)((s + CB - 1) / CB));
+  DeviceBuffer dg(ctx, sizeof(double) * (size_t)s);
+  const int64_t nb = (s + CB - 1) / CB;
+  for (int64_t b = 0; b < nb; ++b) {
+    const int64_t k0 = b * CB, kb = std::min<int64_t>(CB, s - k0), rest = s - k0 - kb;
+    k_qchol_block<<<1, SNT, smem, ctx.stream>>>(sub(work.v, k0, k0, kb, kb), sub(r.v, k0, k0, kb, kb),
+                                                 sub(rinv, k0, k0, kb, kb), info.as<int>() + b,
+                                                 dg.as<double>() + k0);
+    QLRA_LAUNCH_CHECK();
+    count_launch();
+    if (rest > 0) {
+      qgemm(ctx, QLRA_OP_C, QLRA_OP_N, 1.0, sub(rinv, k0, k0, kb, kb), sub(work.v, k0, k0 + kb, kb, rest),
+            0.0, sub(r.v, k0, k0 + kb, kb, rest));
+      qgemm(ctx, QLRA_OP_C, QLRA_OP_N, -1.0, sub(r.v, k0, k0 + kb, kb, rest),
+            sub(r.v, k0, k0 + kb, kb, rest), 1.0, sub(work.v, k0 + kb, k0 + kb, rest, rest));
+    }
+  }
+  std::vector<int> inf(nb);
+  QLRA_CUDA(cudaMemcpyAsync(inf.data(), info.ptr, sizeof(int) * nb, cudaMemcpyDeviceToHost, ctx.stream));
+  QLRA_CUDA(cudaStreamSynchronize(ctx.stream));
+  for (int64_t b = 0; b < nb; ++b)
+    if (inf[b] != 0) return false;
+  if (rdiag) {
+    rdiag->resize(s);
+    QLRA_CUDA(cudaMemcpy(rdiag->data(), dg.ptr, sizeof(double) * s, cudaMemcpyDeviceToHost));
+  }
+  if (nb > 1) {
+    DevQMat tmp(ctx, CB, s);
+    for (int64_t b = nb - 2; b >= 0; --b) {
+      const int64_t i0 = b * CB, ib = std::min<int64_t>(CB, s - i0), j0 = i0 + ib, rest = s - j0;
+      const QView t = sub(tmp.v, 0, 0, ib, rest);
+      qgemm(ctx, QLRA_OP_N, QLRA_OP_N, 1.0, sub(r.v, i0, j0, ib, rest), sub(rinv, j0, j0, rest, rest), 0.0, t);
+      qgemm(ctx, QLRA_OP_N, QLRA_OP_N, -1.0, sub(rinv, i0, i0, ib, ib), t, 0.0, sub(rinv, i0, j0, ib, rest));
+    }
+  }
+  return true;
+}
+
+void zero_jk_planes(Ctx& ctx, const QView& g) {
+  k_zero_jk<<<grid_for(g.rows * g.cols), 256, 0, ctx.stream>>>(g);
+  QLRA_LAUNCH_CHECK();
+  count_launch();
+}
+
 void small_quat_solve(Ctx& ctx, const QView& a, const QView& b, double* d_stat, bool pivot) {
   DeviceBuffer mult(ctx, sizeof(double) * 4 * std::max<int64_t>(1, a.rows));
   k_quat_gj<<<1, SNT, 0, ctx.stream>>>(a, b, d_stat, mult.as<Q4>(), pivot ? 1 : 0);

@@ -371,3 +371,13 @@ def test_c2_full_size_parity(ctx, method):
     err_o, err_d = np.sqrt(rs / an), res.qb_residual / res.a_fro
     assert abs(err_d / err_o - 1) <= 1e-10, (err_d, err_o)
     assert largest_principal_angle(host(res.qb.h), qb["h"]) <= 1e-8
+
+
+@pytest.mark.parametrize("s", [40, 200])
+def test_singular_values_and_kappa(ctx, s):  # factorizations.cpp:316-337 (both tridiag paths)
+    from paper_2404_14783_b200 import qlra as Q
+    y = planted_conditioned_matrix(3 * s, s, 1e3, 90 + s)
+    sv = np.asarray(Q.singular_values(dev(y), ctx))
+    so = O.singular_values(y)
+    assert np.allclose(sv, so, rtol=1e-9)
+    assert abs(Q.condition_number(dev(y), ctx) / O.condition_number(y) - 1) < 1e-8
