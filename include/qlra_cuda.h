@@ -211,6 +211,25 @@ int qlra_approx_residual_fro(qlra_ctx_t* ctx, const qlra_qmat_t* a, const qlra_q
 int qlra_residual_fro(qlra_ctx_t* ctx, const qlra_qmat_t* a, const qlra_qmat_t* h,
                       const qlra_qmat_t* x, double* res_fro, double* a_fro);
 
+/* ------------------------------------------------ checkpoint I/O (next) --- */
+/* QMAT1 / QSKT1 files byte-compatible with the reference (io.hpp:13-33,
+ * io.cpp:77-145).  Device matrices are dense-packed on write.  All sync. */
+int qlra_write_qmat(qlra_ctx_t* ctx, const char* path, const qlra_qmat_t* m);
+int qlra_qmat_file_shape(const char* path, int64_t* rows, int64_t* cols);
+int qlra_read_qmat(qlra_ctx_t* ctx, const char* path, qlra_qmat_t* m);
+int qlra_write_sketch(qlra_ctx_t* ctx, const char* path, const qlra_spec_t* omega,
+                      const qlra_spec_t* psi, int64_t r, int64_t s, int64_t l,
+                      const qlra_qmat_t* y, const qlra_qmat_t* w);
+/* header of a QSKT1 file: both specs and r, s, l (rsl[3]) */
+int qlra_sketch_file_header(const char* path, qlra_spec_t* omega, qlra_spec_t* psi, int64_t* rsl);
+int qlra_read_sketch(qlra_ctx_t* ctx, const char* path, qlra_qmat_t* y, qlra_qmat_t* w);
+/* sketch_from_source over a QMAT1 file (QmatFileSource, io.cpp:213-239):
+ * blocks of block_rows rows are read into pinned buffers and sketched with
+ * H2D overlap; y (m x s) and w (l x n) accumulate. */
+int qlra_sketch_from_qmat_file(qlra_ctx_t* ctx, const char* path, const qlra_spec_t* omega,
+                               const qlra_spec_t* psi, qlra_qmat_t* y, qlra_qmat_t* w,
+                               int64_t block_rows);
+
 /* ---------------------------------------------------------- diagnostics --- */
 /* Measured FP64 throughput of this GPU: mode 0 = DFMA, 1 = DMMA (m8n8k4).
  * Runs ~`ms` milliseconds; syncs. */

@@ -75,6 +75,13 @@ def lib():
         "qlra_qsvd": ([VP, PQ, PQ, P(F64), PQ], INT),
         "qlra_truncate_stage": ([VP, PQ, PQ, I64, PQ, P(F64), PQ], INT),
         "qlra_approx_residual_fro": ([VP, PQ, PQ, P(F64), PQ, P(F64), P(F64)], INT),
+        "qlra_write_qmat": ([VP, C.c_char_p, PQ], INT),
+        "qlra_qmat_file_shape": ([C.c_char_p, P(I64), P(I64)], INT),
+        "qlra_read_qmat": ([VP, C.c_char_p, PQ], INT),
+        "qlra_write_sketch": ([VP, C.c_char_p, PS, PS, I64, I64, I64, PQ, PQ], INT),
+        "qlra_sketch_file_header": ([C.c_char_p, PS, PS, P(I64)], INT),
+        "qlra_read_sketch": ([VP, C.c_char_p, PQ, PQ], INT),
+        "qlra_sketch_from_qmat_file": ([VP, C.c_char_p, PS, PS, PQ, PQ, I64], INT),
         "qlra_measure_fp64_peak": ([VP, INT, F64, P(F64)], INT),
         "qlra_sketch_kernel_name": ([], C.c_char_p),
     }

@@ -898,6 +898,74 @@ int qlra_approx_residual_fro(qlra_ctx_t* ctx, const qlra_qmat_t* a, const qlra_q
   });
 }
 
+int qlra_write_qmat(qlra_ctx_t* ctx, const char* path, const qlra_qmat_t* m) {
+  return guarded(ctx, [&](Ctx& c) {
+    check_view(m, "write_qmat");
+    write_qmat(c, path, view_of(m));
+  });
+}
+
+int qlra_qmat_file_shape(const char* path, int64_t* rows, int64_t* cols) {
+  try {
+    qmat_header(path, rows, cols);
+    return QLRA_OK;
+  } catch (const Status& s) {
+    return s.code;
+  } catch (...) {
+    return QLRA_ERR_IO;
+  }
+}
+
+int qlra_read_qmat(qlra_ctx_t* ctx, const char* path, qlra_qmat_t* m) {
+  return guarded(ctx, [&](Ctx& c) {
+    check_view(m, "read_qmat");
+    read_qmat(c, path, view_of(m));
+  });
+}
+
+int qlra_write_sketch(qlra_ctx_t* ctx, const char* path, const qlra_spec_t* omega,
+                      const qlra_spec_t* psi, int64_t r, int64_t s, int64_t l,
+                      const qlra_qmat_t* y, const qlra_qmat_t* w) {
+  return guarded(ctx, [&](Ctx& c) {
+    validate_spec(omega);
+    validate_spec(psi);
+    check_view(y, "write_sketch");
+    check_view(w, "write_sketch");
+    write_sketch(c, path, *omega, *psi, r, s, l, view_of(y), view_of(w));
+  });
+}
+
+int qlra_sketch_file_header(const char* path, qlra_spec_t* omega, qlra_spec_t* psi, int64_t* rsl) {
+  try {
+    sketch_header(path, omega, psi, rsl);
+    return QLRA_OK;
+  } catch (const Status& s) {
+    return s.code;
+  } catch (...) {
+    return QLRA_ERR_IO;
+  }
+}
+
+int qlra_read_sketch(qlra_ctx_t* ctx, const char* path, qlra_qmat_t* y, qlra_qmat_t* w) {
+  return guarded(ctx, [&](Ctx& c) {
+    check_view(y, "read_sketch");
+    check_view(w, "read_sketch");
+    read_sketch(c, path, view_of(y), view_of(w));
+  });
+}
+
+int qlra_sketch_from_qmat_file(qlra_ctx_t* ctx, const char* path, const qlra_spec_t* omega,
+                               const qlra_spec_t* psi, qlra_qmat_t* y, qlra_qmat_t* w,
+                               int64_t block_rows) {
+  return guarded(ctx, [&](Ctx& c) {
+    validate_spec(omega);
+    validate_spec(psi);
+    check_view(y, "sketch_from_source");
+    check_view(w, "sketch_from_source");
+    sketch_from_qmat_file(c, path, *omega, *psi, view_of(y), view_of(w), block_rows);
+  });
+}
+
 int qlra_measure_fp64_peak(qlra_ctx_t* ctx, int mode, double ms, double* tflops) {
   return guarded(ctx, [&](Ctx& c) { *tflops = measure_fp64_peak(c, mode, ms); });
 }

@@ -176,6 +176,17 @@ void copy_qmat(Ctx& ctx, const QView& src, const QView& dst);
 void scale_add_qmat(Ctx& ctx, double a, const QView& x, double b, const QView& y,
                     const QView& out);  // out = a x + b y
 
+// --------------------------------------------------------------- io.cu ---
+void write_qmat(Ctx& ctx, const std::string& path, const QView& m);
+void qmat_header(const std::string& path, int64_t* rows, int64_t* cols);
+void read_qmat(Ctx& ctx, const std::string& path, const QView& m);
+void write_sketch(Ctx& ctx, const std::string& path, const qlra_spec_t& om, const qlra_spec_t& ps,
+                  int64_t r, int64_t s, int64_t l, const QView& y, const QView& w);
+void sketch_header(const std::string& path, qlra_spec_t* om, qlra_spec_t* ps, int64_t* rsl);
+void read_sketch(Ctx& ctx, const std::string& path, const QView& y, const QView& w);
+void sketch_from_qmat_file(Ctx& ctx, const std::string& path, const qlra_spec_t& omega,
+                           const qlra_spec_t& psi, const QView& y, const QView& w, int64_t block_rows);
+
 // ------------------------------------------------------------- peak.cu ---
 double measure_fp64_peak(Ctx& ctx, int mode, double ms);
 

@@ -642,6 +642,66 @@ def one_pass_approx(a, opts: OnePassOptions, ctx=None) -> ApproxResult:
     return res
 
 
+# ------------------------------------------------------- checkpoint I/O ---
+def write_qmat(path, m, ctx=None):
+    """write_qmat (io.cpp:77-88): QMAT1 file from a device QMatrix."""
+    ctx = _ctx(ctx)
+    ctx._check(ctx.lib.qlra_write_qmat(ctx.h, str(path).encode(), C.byref(_qm(m))))
+
+
+def read_qmat(path, ctx=None):
+    """read_qmat (io.cpp:89-114) into a new device QMatrix."""
+    ctx = _ctx(ctx)
+    r, c = C.c_int64(), C.c_int64()
+    rc = L.lib().qlra_qmat_file_shape(str(path).encode(), C.byref(r), C.byref(c))
+    if rc != 0:
+        raise IoError(f"not a readable QMAT1 file: {path}")
+    m = qzeros(r.value, c.value)
+    ctx._check(ctx.lib.qlra_read_qmat(ctx.h, str(path).encode(), C.byref(_qm(m))))
+    return m
+
+
+def _spec_from_c(cs) -> TestMatrixSpec:
+    return TestMatrixSpec(cs.kind, cs.rows, cs.cols, cs.seed, cs.density)
+
+
+def write_sketch(path, st: SketchState, ctx=None):
+    """write_sketch (io.cpp:116-128): QSKT1 checkpoint of a sketch state."""
+    ctx = _ctx(ctx)
+    om, ps = st.omega_spec.c(), st.psi_spec.c()
+    ctx._check(ctx.lib.qlra_write_sketch(ctx.h, str(path).encode(), C.byref(om), C.byref(ps), st.r, st.s,
+                                         st.l, C.byref(_qm(st.y)), C.byref(_qm(st.w))))
+
+
+def read_sketch(path, ctx=None) -> SketchState:
+    """read_sketch (io.cpp:130-145)."""
+    ctx = _ctx(ctx)
+    om, ps, rsl = L.Spec(), L.Spec(), (C.c_int64 * 3)()
+    if L.lib().qlra_sketch_file_header(str(path).encode(), C.byref(om), C.byref(ps), rsl) != 0:
+        raise IoError(f"not a readable QSKT1 file: {path}")
+    st = SketchState(qzeros(ps.cols, om.cols), qzeros(ps.rows, om.rows), _spec_from_c(om), _spec_from_c(ps),
+                     rsl[0], rsl[1], rsl[2])
+    ctx._check(ctx.lib.qlra_read_sketch(ctx.h, str(path).encode(), C.byref(_qm(st.y)), C.byref(_qm(st.w))))
+    return st
+
+
+def sketch_from_qmat_file(path, r, s, l, omega_seed, psi_seed, kind=GAUSSIAN, density=1.0, block_rows=256,
+                          ctx=None) -> SketchState:
+    """sketch_from_source over a QMAT1 file (QmatFileSource, io.cpp:213-239):
+    the file is the only reader of A; blocks stream through pinned buffers."""
+    ctx = _ctx(ctx)
+    rr, cc = C.c_int64(), C.c_int64()
+    if L.lib().qlra_qmat_file_shape(str(path).encode(), C.byref(rr), C.byref(cc)) != 0:
+        raise IoError(f"not a readable QMAT1 file: {path}")
+    if block_rows < 1:
+        raise ParameterError("sketch_from_source: block_rows must be >= 1")
+    st = empty_sketch(rr.value, cc.value, r, s, l, omega_seed, psi_seed, kind, density)
+    om, ps = st.omega_spec.c(), st.psi_spec.c()
+    ctx._check(ctx.lib.qlra_sketch_from_qmat_file(ctx.h, str(path).encode(), C.byref(om), C.byref(ps),
+                                                  C.byref(_qm(st.y)), C.byref(_qm(st.w)), block_rows))
+    return st
+
+
 def measure_fp64_peak(mode=0, ms=200.0, ctx=None):
     ctx = _ctx(ctx)
     t = C.c_double()

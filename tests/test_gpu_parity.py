@@ -381,3 +381,48 @@ def test_singular_values_and_kappa(ctx, s):  # factorizations.cpp:316-337 (both 
     so = O.singular_values(y)
     assert np.allclose(sv, so, rtol=1e-9)
     assert abs(Q.condition_number(dev(y), ctx) / O.condition_number(y) - 1) < 1e-8
+
+
+# ------------------------------------------------------- checkpoint I/O ---
+def _np_write_qmat(path, a):  # QMAT1 per proj/include/qlra/io.hpp:15-18
+    import struct
+    with open(path, "wb") as f:
+        f.write(b"QMAT1\0" + struct.pack("<QQ", a.shape[1], a.shape[2]))
+        f.write(np.ascontiguousarray(a, dtype="<f8").tobytes())
+
+
+def _np_read_qmat(path):
+    import struct
+    b = open(path, "rb").read()
+    assert b[:6] == b"QMAT1\0"
+    r, c = struct.unpack("<QQ", b[6:22])
+    return np.frombuffer(b[22:22 + 32 * r * c], dtype="<f8").reshape(4, r, c)
+
+
+def test_qmat_and_sketch_checkpoints(ctx, tmp_path):  # test_sketching.cpp:292-308, io.cpp:77-145
+    from paper_2404_14783_b200 import qlra as Q
+    a = random_gaussian(30, 24, 60)
+    _np_write_qmat(tmp_path / "a.qmat", a)
+    ad = Q.read_qmat(tmp_path / "a.qmat", ctx)
+    assert np.array_equal(host(ad), a)
+    Q.write_qmat(tmp_path / "b.qmat", ad, ctx)
+    assert open(tmp_path / "a.qmat", "rb").read() == open(tmp_path / "b.qmat", "rb").read()
+    st = Q.make_sketch(ad, 4, 8, 16, 61, 62, ctx=ctx)
+    Q.write_sketch(tmp_path / "s.qskt", st, ctx)
+    ld = Q.read_sketch(tmp_path / "s.qskt", ctx)
+    assert torch.equal(ld.y, st.y) and torch.equal(ld.w, st.w)
+    assert (ld.r, ld.s, ld.l) == (4, 8, 16) and ld.psi_spec == st.psi_spec and ld.omega_spec == st.omega_spec
+    q1 = Q.qb_stage(st, ctx=ctx)
+    q2 = Q.qb_stage(ld, ctx=ctx)
+    assert torch.equal(q1.h, q2.h) and torch.equal(q1.x, q2.x)  # pipeline reproduced bitwise
+    with pytest.raises(Q.IoError):
+        Q.read_sketch(tmp_path / "a.qmat", ctx)
+
+
+def test_sketch_from_qmat_file(ctx, tmp_path):  # CS-2: qlra sketch --input A.qmat
+    from paper_2404_14783_b200 import qlra as Q
+    a = random_gaussian(700, 90, 62)
+    _np_write_qmat(tmp_path / "a.qmat", a)
+    st = Q.sketch_from_qmat_file(tmp_path / "a.qmat", 5, 10, 20, 7, 8, block_rows=256, ctx=ctx)
+    y, w = O.make_sketch(a, 5, 10, 20, 7, 8)
+    assert rel_diff(host(st.y), y) < 1e-13 and rel_diff(host(st.w), w) < 1e-13
