@@ -136,11 +136,15 @@ bool hpd_inverse(Ctx& ctx, const QView& g, const QView& ginv, std::vector<double
 // complex part of the quaternion Gram) -- pseudo-QR's complex_qr; else R is
 // the quaternion Cholesky factor (orthonormal quaternion basis).  Returns
 // false if the Cholesky factorisation breaks down; rdiag gets diag(R).
+// distributed: y is row-sharded over the ranks (Gram all-reduced); else y is
+// replicated.  rinv_out (optional) receives R^{-1}.
 bool cqr_pass(Ctx& ctx, const QView& y, const QView& hout, bool complex_mode, double shift,
-              std::vector<double>* rdiag, double* trace_g) {
+              std::vector<double>* rdiag, double* trace_g, bool distributed = true,
+              const QView* rinv_out = nullptr) {
   const int64_t s = y.cols;
   DevQMat g(ctx, s, s);
-  gram(ctx, y, g.v);
+  if (distributed) gram(ctx, y, g.v);
+  else qgemm(ctx, QLRA_OP_C, QLRA_OP_N, 1.0, y, y, 0.0, g.v);
   if (trace_g) {
     const std::vector<double> d = diag_to_host(ctx, g.v.p[0], g.v.ld, s);
     double t = 0.0;
@@ -154,37 +158,65 @@ bool cqr_pass(Ctx& ctx, const QView& y, const QView& hout, bool complex_mode, do
   DevQMat rinv(ctx, s, s);
   if (!blocked_chol_inv(ctx, g.v, rinv.v, rdiag)) return false;
   qgemm(ctx, QLRA_OP_N, QLRA_OP_N, 1.0, y, rinv.v, 0.0, hout);
+  if (rinv_out) copy_qmat(ctx, rinv.v, *rinv_out);
   return true;
 }
 
+// rinv <- rinv * next (s x s, upper triangular factors of R^{-1} = R1^{-1} R2^{-1} ...)
+void chain_rinv(Ctx& ctx, DevQMat& rinv, const QView& next) {
+  DevQMat t(ctx, rinv.v.rows, rinv.v.cols);
+  qgemm(ctx, QLRA_OP_N, QLRA_OP_N, 1.0, rinv.v, next, 0.0, t.v);
+  rinv = std::move(t);
+}
+
 // CholeskyQR2, or shifted CholeskyQR3 (Fukaya et al.) when the first Gram is
-// not numerically positive definite.  rdiag = diag of the full R factor.
+// not numerically positive definite.  rdiag = diag of the full R factor;
+// rinv (optional, s x s) = R^{-1} of y = h R.
 bool cholesky_qr(Ctx& ctx, const QView& y, const QView& h, bool complex_mode, int64_t m_global,
-                 std::vector<double>* rdiag) {
+                 std::vector<double>* rdiag, bool distributed = true, DevQMat* rinv = nullptr) {
   const int64_t s = y.cols;
   DevQMat t1(ctx, y.rows, s);
+  DevQMat r1, r2, r3;
+  if (rinv) {
+    r1 = DevQMat(ctx, s, s);
+    r2 = DevQMat(ctx, s, s);
+  }
   std::vector<double> d1, d2, d3;
   double tr = 0.0;
-  if (cqr_pass(ctx, y, t1.v, complex_mode, 0.0, &d1, &tr)) {
-    if (!cqr_pass(ctx, t1.v, h, complex_mode, 0.0, &d2, nullptr)) return false;
+  if (cqr_pass(ctx, y, t1.v, complex_mode, 0.0, &d1, &tr, distributed, rinv ? &r1.v : nullptr)) {
+    if (!cqr_pass(ctx, t1.v, h, complex_mode, 0.0, &d2, nullptr, distributed, rinv ? &r2.v : nullptr))
+      return false;
     if (rdiag) {
       rdiag->resize(s);
       for (int64_t k = 0; k < s; ++k) (*rdiag)[k] = d1[k] * d2[k];
+    }
+    if (rinv) {
+      *rinv = std::move(r1);
+      chain_rinv(ctx, *rinv, r2.v);
     }
     return true;
   }
   const double dim = complex_mode ? 2.0 : 4.0;
   const double shift = 11.0 * (dim * (double)m_global * s + s * (s + 1.0)) * kUnit * tr;
   if (!(tr > 0.0)) return false;
-  if (!cqr_pass(ctx, y, t1.v, complex_mode, shift, &d1, nullptr)) return false;
+  if (rinv) r3 = DevQMat(ctx, s, s);
+  if (!cqr_pass(ctx, y, t1.v, complex_mode, shift, &d1, nullptr, distributed, rinv ? &r1.v : nullptr))
+    return false;
   DevQMat t2(ctx, y.rows, s);
-  if (!cqr_pass(ctx, t1.v, t2.v, complex_mode, 0.0, &d2, nullptr)) return false;
-  if (!cqr_pass(ctx, t2.v, h, complex_mode, 0.0, &d3, nullptr)) return false;
+  if (!cqr_pass(ctx, t1.v, t2.v, complex_mode, 0.0, &d2, nullptr, distributed, rinv ? &r2.v : nullptr))
+    return false;
+  if (!cqr_pass(ctx, t2.v, h, complex_mode, 0.0, &d3, nullptr, distributed, rinv ? &r3.v : nullptr))
+    return false;
   if (rdiag) {
     rdiag->resize(s);
     // y = t1 R1 = t2 R2 R1 = h R3 R2 R1 holds exactly whatever the shift, so
     // R = R3 R2 R1 is a QR factor of y and its diagonal is the product.
     for (int64_t k = 0; k < s; ++k) (*rdiag)[k] = d1[k] * d2[k] * d3[k];
+  }
+  if (rinv) {
+    *rinv = std::move(r1);
+    chain_rinv(ctx, *rinv, r2.v);
+    chain_rinv(ctx, *rinv, r3.v);
   }
   return true;
 }
@@ -309,19 +341,18 @@ void correction_from_inverse(Ctx& ctx, const QView& h, const QView& ginv, double
   }
 }
 
-// Least squares X = argmin ||P X - B|| for replicated P (l x s), B (l x n):
-// normal equations with the explicit quaternion inverse of P^*P plus one
-// step of iterative refinement (accuracy ~ u kappa(P)).
+// Least squares X = argmin ||P X - B|| for replicated P (l x s, l >= s),
+// B (l x n), through a QR of P as the reference does (ColPivHouseholderQR,
+// complex_bridge.cpp:80-90): P = Q R by CholeskyQR2 (shifted CholeskyQR3 if
+// needed), T = Q R^{-*} (small), X = T^* B = R^{-1} Q^* B -- one wide product.
+// Accuracy ~ u kappa(P) like a Householder solve (no normal equations).
 void lstsq(Ctx& ctx, const QView& p, const QView& b, const QView& x) {
-  const int64_t s = p.cols;
-  DevQMat g(ctx, s, s);
-  qgemm(ctx, QLRA_OP_C, QLRA_OP_N, 1.0, p, p, 0.0, g.v);
-  // Rank test in the spirit of ColPivHouseholderQR |r_min| > 1e-14 |r_max|
-  // (complex_bridge.cpp:80-85): the Cholesky factor of P^*P is the R of a
-  // QR of P, so its diagonal is tested the same way.
-  DevQMat ginv(ctx, s, s);
+  const int64_t s = p.cols, l = p.rows;
+  DevQMat q(ctx, l, s), rinv;
   std::vector<double> rd;
-  if (!hpd_inverse(ctx, g.v, ginv.v, &rd))
+  // Rank test of ColPivHouseholderQR, |r_min| > 1e-14 |r_max|
+  // (complex_bridge.cpp:80-85), on the diagonal of R.
+  if (!cholesky_qr(ctx, p, q.v, /*complex_mode=*/false, l, &rd, /*distributed=*/false, &rinv))
     fail(QLRA_ERR_SINGULAR, "solve_quaternion_linear: rank-deficient system",
          std::numeric_limits<double>::infinity());
   double rmax = 0.0, rmin = std::numeric_limits<double>::infinity();
@@ -332,15 +363,9 @@ void lstsq(Ctx& ctx, const QView& p, const QView& b, const QView& x) {
   if (!(rmin > 1e-14 * rmax))
     fail(QLRA_ERR_SINGULAR, "solve_quaternion_linear: rank-deficient system",
          rmin > 0 ? rmax / rmin : std::numeric_limits<double>::infinity());
-  DevQMat c(ctx, s, b.cols);
-  qgemm(ctx, QLRA_OP_C, QLRA_OP_N, 1.0, p, b, 0.0, c.v);
-  qgemm(ctx, QLRA_OP_N, QLRA_OP_N, 1.0, ginv.v, c.v, 0.0, x);
-  // refinement: r = B - P X ; X += Ginv (P^* r)
-  DevQMat r(ctx, b.rows, b.cols);
-  copy_qmat(ctx, b, r.v);
-  qgemm(ctx, QLRA_OP_N, QLRA_OP_N, -1.0, p, x, 1.0, r.v);
-  qgemm(ctx, QLRA_OP_C, QLRA_OP_N, 1.0, p, r.v, 0.0, c.v);
-  qgemm(ctx, QLRA_OP_N, QLRA_OP_N, 1.0, ginv.v, c.v, 1.0, x);
+  DevQMat t(ctx, l, s);
+  qgemm(ctx, QLRA_OP_N, QLRA_OP_C, 1.0, q.v, rinv.v, 0.0, t.v);
+  qgemm(ctx, QLRA_OP_C, QLRA_OP_N, 1.0, t.v, b, 0.0, x);
 }
 
 void check_view(const qlra_qmat_t* m, const char* who) {

@@ -694,6 +694,210 @@ __global__ void __launch_bounds__(SNT) k_qtridiag(QView a, double* d, double* e)
   for (int64_t i = t; i < n; i += blockDim.x) d[i] = a.p[0][i * a.ld + i];
 }
 
+// Shared-memory variant of k_qtridiag for n <= QT_SMEM_MAX: the Hermitian
+// matrix lives in shared memory as its packed lower triangle (A[r][c], r >= c,
+// at r(r+1)/2 + c; the upper half is the conjugate).  Same reflectors and the
+// same arithmetic as k_qtridiag; three barriers per step: warp 0 forms the
+// reflector, the matvec runs one warp per row, every warp recomputes
+// c = Re(v^* p) itself and the rank-2 update touches only the lower triangle.
+constexpr int QT_SMEM_MAX = 112;
+__device__ __forceinline__ int tri(int r, int c) { return r * (r + 1) / 2 + c; }
+__global__ void __launch_bounds__(512) k_qtridiag_smem(QView a, double* d, double* e) {
+  extern __shared__ __align__(16) unsigned char dsm[];
+  const int n = (int)a.rows;
+  Q4* L = reinterpret_cast<Q4*>(dsm);
+  Q4* v = L + n * (n + 1) / 2;
+  Q4* pv = v + n;
+  __shared__ double s_beta;
+  const int t = threadIdx.x, lane = t & 31, wid = t >> 5, nw = blockDim.x >> 5;
+  for (int r = wid; r < n; r += nw)
+    for (int c = lane; c <= r; c += 32) L[tri(r, c)] = qload(a, r, c);
+  __syncthreads();
+  for (int k = 0; k + 1 < n; ++k) {
+    const int len = n - k - 1, o = k + 1;
+    if (wid == 0) {
+      double part = 0.0;
+      for (int i = lane; i < len; i += 32) {
+        const Q4 q = L[tri(o + i, k)];
+        part += q.w * q.w + q.x * q.x + q.y * q.y + q.z * q.z;
+      }
+      const double nrm2 = warp_sum(part);
+      const Q4 x1 = L[tri(o, k)];
+      const double ax1 = sqrt(x1.w * x1.w + x1.x * x1.x + x1.y * x1.y + x1.z * x1.z);
+      const double alpha = sqrt(nrm2);
+      const Q4 phi = ax1 > 0.0 ? Q4{x1.w / ax1, x1.x / ax1, x1.y / ax1, x1.z / ax1} : Q4{1.0, 0.0, 0.0, 0.0};
+      const double beta = alpha > 0.0 ? 2.0 / (2.0 * alpha * alpha + 2.0 * alpha * ax1) : 0.0;
+      for (int i = lane; i < len; i += 32) {
+        Q4 q = L[tri(o + i, k)];
+        if (i == 0) {
+          q.w += phi.w * alpha; q.x += phi.x * alpha;
+          q.y += phi.y * alpha; q.z += phi.z * alpha;
+        }
+        v[i] = q;
+      }
+      if (lane == 0) {
+        e[k] = alpha;
+        s_beta = beta;
+      }
+    }
+    __syncthreads();
+    const double beta = s_beta;
+    if (beta == 0.0) continue;  // column already reduced (uniform across the CTA)
+    // p = beta * A22 v, warp per row
+    for (int r = wid; r < len; r += nw) {
+      Q4 acc{0.0, 0.0, 0.0, 0.0};
+      for (int c = lane; c < len; c += 32) {
+        Q4 av;
+        if (c <= r) {
+          av = L[tri(o + r, o + c)];
+        } else {
+          av = L[tri(o + c, o + r)];
+          av.x = -av.x; av.y = -av.y; av.z = -av.z;
+        }
+        const Q4 pq = qmul(av, v[c]);
+        acc.w += pq.w; acc.x += pq.x; acc.y += pq.y; acc.z += pq.z;
+      }
+      acc.w = warp_sum(acc.w);
+      acc.x = warp_sum(acc.x);
+      acc.y = warp_sum(acc.y);
+      acc.z = warp_sum(acc.z);
+      if (lane == 0) pv[r] = Q4{beta * acc.w, beta * acc.x, beta * acc.y, beta * acc.z};
+    }
+    __syncthreads();
+    double cp = 0.0;
+    for (int i = lane; i < len; i += 32)
+      cp += v[i].w * pv[i].w + v[i].x * pv[i].x + v[i].y * pv[i].y + v[i].z * pv[i].z;
+    const double hk = 0.5 * beta * warp_sum(cp);
+    // A22 -= v w^* + w v^*, w = p - hk v, lower triangle only
+    for (int r = wid; r < len; r += nw) {
+      const Q4 vr = v[r], pr = pv[r];
+      const Q4 wr{pr.w - hk * vr.w, pr.x - hk * vr.x, pr.y - hk * vr.y, pr.z - hk * vr.z};
+      for (int cc = lane; cc <= r; cc += 32) {
+        const Q4 vc0 = v[cc], pc = pv[cc];
+        Q4 wc{pc.w - hk * vc0.w, -(pc.x - hk * vc0.x), -(pc.y - hk * vc0.y), -(pc.z - hk * vc0.z)};
+        const Q4 vc{vc0.w, -vc0.x, -vc0.y, -vc0.z};
+        const Q4 t1 = qmul(vr, wc), t2 = qmul(wr, vc);
+        Q4& dst = L[tri(o + r, o + cc)];
+        dst.w -= t1.w + t2.w;
+        dst.x -= t1.x + t2.x;
+        dst.y -= t1.y + t2.y;
+        dst.z -= t1.z + t2.z;
+      }
+    }
+    __syncthreads();
+  }
+  for (int i = t; i < n; i += blockDim.x) d[i] = L[tri(i, i)].w;
+}
+
+// Cluster variant of k_qtridiag for QT_SMEM_MAX < n <= QTC_MAX: one cluster
+// of QTC CTAs on QTC SMs (the single-CTA kernel is bound by one SM's FP64
+// pipe).  Row r lives in the shared memory of CTA r % QTC (full rows, both
+// triangles).  Step k: the owner of row k broadcasts x = conj(A[k, k+1:]) (the
+// Hermitian image of column k) into every CTA's v buffer over DSMEM; every CTA
+// forms the identical reflector redundantly; each CTA computes p = beta A v
+// for its rows and scatters it into every CTA's p buffer; then each CTA
+// applies A -= v w^* + w v^* to its rows.  Two cluster barriers per step; v
+// is double-buffered across steps so the next broadcast cannot overwrite a v
+// still being read.  Same reflectors as k_qtridiag.
+constexpr int QTC = 8;
+constexpr int QTC_MAX = 224;
+constexpr int QTC_THREADS = 256;
+__global__ void __cluster_dims__(QTC, 1, 1) __launch_bounds__(QTC_THREADS)
+    k_qtridiag_cluster(QView a, double* d, double* e) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  extern __shared__ __align__(16) unsigned char dsm[];
+  const int n = (int)a.rows, rank = (int)cl.block_rank();
+  const int rmax = (n + QTC - 1) / QTC, nr = (n - rank + QTC - 1) / QTC;
+  Q4* rows = reinterpret_cast<Q4*>(dsm);  // rmax x n: global row rank + QTC*li
+  Q4* vb = rows + (size_t)rmax * n;       // 2 x n
+  Q4* pb = vb + 2 * n;                    // n
+  __shared__ double s_beta;
+  const int t = threadIdx.x, lane = t & 31, wid = t >> 5, nw = blockDim.x >> 5;
+  for (int li = wid; li < nr; li += nw)
+    for (int c = lane; c < n; c += 32) rows[li * n + c] = qload(a, rank + QTC * li, c);
+  cl.sync();
+  for (int k = 0; k + 1 < n; ++k) {
+    const int len = n - k - 1, o = k + 1;
+    Q4* v = vb + (k & 1) * n;
+    if (k % QTC == rank) {
+      const Q4* src = rows + (k / QTC) * n + o;
+      for (int dst = 0; dst < QTC; ++dst) {
+        Q4* rv = cl.map_shared_rank(v, dst);
+        for (int i = t; i < len; i += blockDim.x) {
+          const Q4 q = src[i];
+          rv[i] = Q4{q.w, -q.x, -q.y, -q.z};
+        }
+      }
+    }
+    cl.sync();
+    if (wid == 0) {
+      double part = 0.0;
+      for (int i = lane; i < len; i += 32) {
+        const Q4 q = v[i];
+        part += q.w * q.w + q.x * q.x + q.y * q.y + q.z * q.z;
+      }
+      const double nrm2 = warp_sum(part);
+      const Q4 x1 = v[0];
+      const double ax1 = sqrt(x1.w * x1.w + x1.x * x1.x + x1.y * x1.y + x1.z * x1.z);
+      const double alpha = sqrt(nrm2);
+      const Q4 phi = ax1 > 0.0 ? Q4{x1.w / ax1, x1.x / ax1, x1.y / ax1, x1.z / ax1} : Q4{1.0, 0.0, 0.0, 0.0};
+      const double beta = alpha > 0.0 ? 2.0 / (2.0 * alpha * alpha + 2.0 * alpha * ax1) : 0.0;
+      __syncwarp();
+      if (lane == 0) {
+        v[0] = Q4{x1.w + phi.w * alpha, x1.x + phi.x * alpha, x1.y + phi.y * alpha, x1.z + phi.z * alpha};
+        s_beta = beta;
+        if (rank == 0) e[k] = alpha;
+      }
+    }
+    __syncthreads();
+    const double beta = s_beta;  // bitwise identical in every CTA
+    if (beta == 0.0) continue;
+    for (int li = wid; li < nr; li += nw) {
+      const int r = rank + QTC * li;
+      if (r < o) continue;
+      const Q4* row = rows + li * n + o;
+      Q4 acc{0.0, 0.0, 0.0, 0.0};
+      for (int c = lane; c < len; c += 32) {
+        const Q4 pq = qmul(row[c], v[c]);
+        acc.w += pq.w; acc.x += pq.x; acc.y += pq.y; acc.z += pq.z;
+      }
+      acc.w = warp_sum(acc.w);
+      acc.x = warp_sum(acc.x);
+      acc.y = warp_sum(acc.y);
+      acc.z = warp_sum(acc.z);
+      if (lane < QTC) cl.map_shared_rank(pb, lane)[r - o] = Q4{beta * acc.w, beta * acc.x, beta * acc.y, beta * acc.z};
+    }
+    cl.sync();
+    double cp = 0.0;
+    for (int i = lane; i < len; i += 32)
+      cp += v[i].w * pb[i].w + v[i].x * pb[i].x + v[i].y * pb[i].y + v[i].z * pb[i].z;
+    const double hk = 0.5 * beta * warp_sum(cp);
+    const int first = (o - rank + QTC - 1) / QTC;  // first owned row >= o
+    const int nt = nr - first;
+    for (int q = t; q < nt * len; q += blockDim.x) {
+      const int li = first + q / len, cc = q % len;
+      const int ri = rank + QTC * li - o;
+      const Q4 vr = v[ri], pr = pb[ri], vc0 = v[cc], pc = pb[cc];
+      const Q4 wr{pr.w - hk * vr.w, pr.x - hk * vr.x, pr.y - hk * vr.y, pr.z - hk * vr.z};
+      const Q4 wc{pc.w - hk * vc0.w, -(pc.x - hk * vc0.x), -(pc.y - hk * vc0.y), -(pc.z - hk * vc0.z)};
+      const Q4 vc{vc0.w, -vc0.x, -vc0.y, -vc0.z};
+      const Q4 t1 = qmul(vr, wc), t2 = qmul(wr, vc);
+      Q4& dst = rows[li * n + o + cc];
+      dst.w -= t1.w + t2.w;
+      dst.x -= t1.x + t2.x;
+      dst.y -= t1.y + t2.y;
+      dst.z -= t1.z + t2.z;
+    }
+    __syncthreads();
+  }
+  for (int li = t; li < nr; li += blockDim.x) {
+    const int r = rank + QTC * li;
+    d[r] = rows[li * n + r].w;
+  }
+  cl.sync();  // no CTA exits while a peer may still touch its shared memory
+}
+
 // Parallel cyclic Jacobi eigensolver for a quaternion Hermitian matrix
 // (n x n, full storage, destroyed -> diagonal), one CTA.  For a pivot pair
 // (p, q) with b = G_pq = |b| u (u a unit quaternion) the rotation is
@@ -874,87 +1078,148 @@ __global__ void k_qsvd_phase(QView u, QView v) {
   for (int64_t i = lane; i < v.rows; i += 32) qstore(v, i, j, qmul(qload(v, i, j), ph));
 }
 
-// Cholesky + inverse of one diagonal block (nb <= 64) in shared memory:
-// G = R^* R (R upper, real positive diagonal) and X = R^{-1} by the in-place
-// column recurrence x_{0:j, j} = -X_{0:j,0:j} r_{0:j,j} / r_jj (LAPACK trti2
-// order).  Quaternion arithmetic throughout; complex inputs (j,k planes 0)
-// stay complex.  One CTA; *info = 0 or first failing column (1-based).
+// Cholesky + inverse of one diagonal block (nb <= 64): G = R^* R (R upper,
+// real positive diagonal) and X = R^{-1}, quaternion arithmetic throughout
+// (complex inputs stay complex).  Register-tiled: thread (ti, tj) of a 16x16
+// grid owns the cyclic 4x4 tile {ti + 16a} x {tj + 16b} in registers, so the
+// shrinking trailing matrix stays spread over all threads.  Factorisation:
+// unscaled right-looking updates a_rc -= a_kr^* a_kc / a_kk; step k publishes
+// row k through a double-buffered shared row (one barrier per step) and every
+// thread reads the pivot from it.  Rows are scaled by 1/sqrt(a_rr) at the end.
+// Inverse: right-looking back substitution in the same registers, X = I,
+// for i = n-1..0: X[i,:] /= r_ii, publish, X[r,:] -= R[r,i] X[i,:] (r < i);
+// R is kept in shared memory for its columns.  *info = 0 or the first
+// failing column (1-based).
 constexpr int CB = 64;
-__global__ void __launch_bounds__(SNT) k_qchol_block(QView g, QView r, QView rinv, int* info,
-                                                     double* rdiag) {
+constexpr int QB_THREADS = 256;
+__global__ void __launch_bounds__(QB_THREADS, 1) k_qchol_block(QView g, QView r, QView rinv, int* info,
+                                                               double* rdiag) {
   extern __shared__ __align__(16) unsigned char dsm[];
-  Q4* a = reinterpret_cast<Q4*>(dsm);  // CB x CB
-  __shared__ Q4 tmp[CB];
-  __shared__ int s_bad;
-  const int n = (int)g.rows, t = threadIdx.x;
-  for (int e = t; e < n * n; e += blockDim.x) {
-    const int i = e / n, j = e % n;
-    a[i * CB + j] = j >= i ? qload(g, i, j) : Q4{0.0, 0.0, 0.0, 0.0};
+  Q4* rs = reinterpret_cast<Q4*>(dsm);  // CB x CB, R
+  __shared__ Q4 rowbuf[2][CB];
+  __shared__ double dg[CB];
+  const int n = (int)g.rows, t = threadIdx.x, ti = t >> 4, tj = t & 15;
+  Q4 a[4][4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      const int rr = ti + 16 * u, cc = tj + 16 * v;
+      a[u][v] = (rr < n && cc < n && cc >= rr) ? qload(g, rr, cc) : Q4{0.0, 0.0, 0.0, 0.0};
+    }
+  if (ti == 0) {
+#pragma unroll
+    for (int v = 0; v < 4; ++v) rowbuf[0][tj + 16 * v] = a[0][v];
   }
-  if (t == 0) s_bad = 0;
   __syncthreads();
+  int bad = 0;
   for (int k = 0; k < n; ++k) {
-    if (t == 0) {
-      const double d = a[k * CB + k].w;
-      if (!(d > 0.0)) {
-        s_bad = k + 1;
-      } else {
-        a[k * CB + k] = Q4{sqrt(d), 0.0, 0.0, 0.0};
+    const int buf = k & 1;
+    const double akk = rowbuf[buf][k].w;
+    if (!(akk > 0.0)) { bad = k + 1; break; }  // identical decision in every thread
+    const double inv = 1.0 / akk;
+    Q4 uc[4];
+#pragma unroll
+    for (int v = 0; v < 4; ++v) uc[v] = rowbuf[buf][(tj + 16 * v) & (CB - 1)];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int rr = ti + 16 * u;
+      if (rr > k && rr < n) {
+        const Q4 q = rowbuf[buf][rr];
+        const Q4 ur{q.w * inv, -q.x * inv, -q.y * inv, -q.z * inv};  // a_kr^* / a_kk
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          const int cc = tj + 16 * v;
+          if (cc >= rr && cc < n) {
+            const Q4 pq = qmul(ur, uc[v]);
+            a[u][v].w -= pq.w; a[u][v].x -= pq.x; a[u][v].y -= pq.y; a[u][v].z -= pq.z;
+          }
+        }
       }
     }
-    __syncthreads();
-    if (s_bad) break;
-    const double inv = 1.0 / a[k * CB + k].w;
-    for (int j = k + 1 + t; j < n; j += blockDim.x) {
-      Q4 q = a[k * CB + j];
-      a[k * CB + j] = Q4{q.w * inv, q.x * inv, q.y * inv, q.z * inv};
-    }
-    __syncthreads();
-    const int rr = n - k - 1;
-    for (int e = t; e < rr * rr; e += blockDim.x) {
-      const int i = k + 1 + e / rr, j = k + 1 + e % rr;
-      if (j < i) continue;
-      Q4 ai = a[k * CB + i];
-      ai.x = -ai.x; ai.y = -ai.y; ai.z = -ai.z;
-      const Q4 pq = qmul(ai, a[k * CB + j]);
-      Q4 c = a[i * CB + j];
-      c.w -= pq.w; c.x -= pq.x; c.y -= pq.y; c.z -= pq.z;
-      a[i * CB + j] = c;
+    const int nk = k + 1;
+    if (nk < n && (nk & 15) == ti) {
+      // select, not a[nk >> 4][v]: keeps the tile in registers
+      const int sl = nk >> 4;
+#pragma unroll
+      for (int v = 0; v < 4; ++v)
+        rowbuf[buf ^ 1][tj + 16 * v] = sl == 0 ? a[0][v] : sl == 1 ? a[1][v] : sl == 2 ? a[2][v] : a[3][v];
     }
     __syncthreads();
   }
-  if (s_bad) {
-    if (t == 0) *info = s_bad;
+  if (bad) {
+    if (t == 0) *info = bad;
     return;
   }
   if (t == 0) *info = 0;
-  for (int e = t; e < n * n; e += blockDim.x) {
-    const int i = e / n, j = e % n;
-    qstore(r, i, j, j >= i ? a[i * CB + j] : Q4{0.0, 0.0, 0.0, 0.0});
+  if (ti == tj) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (ti + 16 * u < n) dg[ti + 16 * u] = sqrt(a[u][u].w);
   }
-  for (int i = t; i < n; i += blockDim.x) if (rdiag) rdiag[i] = a[i * CB + i].w;
   __syncthreads();
-  // in-place inverse, column by column
-  for (int j = 0; j < n; ++j) {
-    const double ajj = 1.0 / a[j * CB + j].w;
-    // tmp[i] = sum_{k=i..j-1} X_ik r_kj   for i < j   (X = already inverted block)
-    for (int i = t; i < j; i += blockDim.x) {
-      Q4 acc{0.0, 0.0, 0.0, 0.0};
-      for (int k = i; k < j; ++k) {
-        const Q4 pq = qmul(a[i * CB + k], a[k * CB + j]);
-        acc.w += pq.w; acc.x += pq.x; acc.y += pq.y; acc.z += pq.z;
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int rr = ti + 16 * u;
+    if (rr >= n) continue;
+    const double sc = 1.0 / dg[rr];
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      const int cc = tj + 16 * v;
+      if (cc >= n) continue;
+      Q4 q{0.0, 0.0, 0.0, 0.0};
+      if (cc > rr) q = Q4{a[u][v].w * sc, a[u][v].x * sc, a[u][v].y * sc, a[u][v].z * sc};
+      else if (cc == rr) q = Q4{dg[rr], 0.0, 0.0, 0.0};
+      rs[rr * CB + cc] = q;
+      qstore(r, rr, cc, q);
+      a[u][v] = cc == rr ? Q4{1.0, 0.0, 0.0, 0.0} : Q4{0.0, 0.0, 0.0, 0.0};  // X = I
+    }
+  }
+  if (rdiag)
+    for (int i = t; i < n; i += blockDim.x) rdiag[i] = dg[i];
+  __syncthreads();
+  for (int i = n - 1, it = 0; i >= 0; --i, ++it) {
+    const int buf = it & 1;
+    if ((i & 15) == ti) {
+      const double sc = 1.0 / dg[i];
+      const int sl = i >> 4;
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        Q4 q = sl == 0 ? a[0][v] : sl == 1 ? a[1][v] : sl == 2 ? a[2][v] : a[3][v];
+        q = Q4{q.w * sc, q.x * sc, q.y * sc, q.z * sc};
+        rowbuf[buf][tj + 16 * v] = q;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) a[u][v] = sl == u ? q : a[u][v];
       }
-      tmp[i] = acc;
     }
     __syncthreads();
-    for (int i = t; i < j; i += blockDim.x)
-      a[i * CB + j] = Q4{-tmp[i].w * ajj, -tmp[i].x * ajj, -tmp[i].y * ajj, -tmp[i].z * ajj};
-    if (t == 0) a[j * CB + j] = Q4{ajj, 0.0, 0.0, 0.0};
-    __syncthreads();
+    Q4 xi[4];
+#pragma unroll
+    for (int v = 0; v < 4; ++v) xi[v] = rowbuf[buf][(tj + 16 * v) & (CB - 1)];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int rr = ti + 16 * u;
+      if (rr < i) {
+        const Q4 rri = rs[rr * CB + i];
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          const int cc = tj + 16 * v;
+          if (cc >= i && cc < n) {
+            const Q4 pq = qmul(rri, xi[v]);
+            a[u][v].w -= pq.w; a[u][v].x -= pq.x; a[u][v].y -= pq.y; a[u][v].z -= pq.z;
+          }
+        }
+      }
+    }
   }
-  for (int e = t; e < n * n; e += blockDim.x) {
-    const int i = e / n, j = e % n;
-    qstore(rinv, i, j, j >= i ? a[i * CB + j] : Q4{0.0, 0.0, 0.0, 0.0});
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int rr = ti + 16 * u;
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      const int cc = tj + 16 * v;
+      if (rr < n && cc < n) qstore(rinv, rr, cc, cc >= rr ? a[u][v] : Q4{0.0, 0.0, 0.0, 0.0});
+    }
   }
 }
 
@@ -1116,7 +1381,7 @@ void small_quat_herm_eigvals(Ctx& ctx, const QView& a, double* d_w, bool extreme
     QLRA_CUDA(cudaFuncSetAttribute(k_qtridiag, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = smem;
   }
-  if (n > 160) {
+  if (n > QTC_MAX) {
     // large n: cooperative grid over all SMs
     int dev = 0, sms = 148, per_sm = 0;
     QLRA_CUDA(cudaGetDevice(&dev));
@@ -1131,6 +1396,27 @@ void small_quat_herm_eigvals(Ctx& ctx, const QView& a, double* d_w, bool extreme
     void* args[] = {&av, &d, &e, &pp, &pvp};
     QLRA_CUDA(cudaLaunchCooperativeKernel((const void*)k_qtridiag_coop, dim3(blocks), dim3(512), args, 0,
                                           ctx.stream));
+    count_launch();
+  } else if (n > 48 && n <= QTC_MAX) {
+    const int64_t rmax = (n + QTC - 1) / QTC;
+    const size_t csm = sizeof(Q4) * (size_t)(rmax * n + 3 * n);
+    static size_t cattr = 0;
+    if (csm > 48 * 1024 && csm > cattr) {
+      QLRA_CUDA(cudaFuncSetAttribute(k_qtridiag_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm));
+      cattr = csm;
+    }
+    k_qtridiag_cluster<<<QTC, QTC_THREADS, csm, ctx.stream>>>(a, d, e);
+    QLRA_LAUNCH_CHECK();
+    count_launch();
+  } else if (n <= QT_SMEM_MAX) {
+    const size_t tsm = sizeof(Q4) * (size_t)(n * (n + 1) / 2 + 2 * n);
+    static size_t tattr = 0;
+    if (tsm > 48 * 1024 && tsm > tattr) {
+      QLRA_CUDA(cudaFuncSetAttribute(k_qtridiag_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm));
+      tattr = tsm;
+    }
+    k_qtridiag_smem<<<1, 512, tsm, ctx.stream>>>(a, d, e);
+    QLRA_LAUNCH_CHECK();
     count_launch();
   } else {
     k_qtridiag<<<1, SNT, smem, ctx.stream>>>(a, d, e);
@@ -1207,7 +1493,7 @@ bool blocked_chol_inv(Ctx& ctx, const QView& g, const QView& rinv, std::vector<d
   const int64_t nb = (s + CB - 1) / CB;
   for (int64_t b = 0; b < nb; ++b) {
     const int64_t k0 = b * CB, kb = std::min<int64_t>(CB, s - k0), rest = s - k0 - kb;
-    k_qchol_block<<<1, SNT, smem, ctx.stream>>>(sub(work.v, k0, k0, kb, kb), sub(r.v, k0, k0, kb, kb),
+    k_qchol_block<<<1, QB_THREADS, smem, ctx.stream>>>(sub(work.v, k0, k0, kb, kb), sub(r.v, k0, k0, kb, kb),
                                                  sub(rinv, k0, k0, kb, kb), info.as<int>() + b,
                                                  dg.as<double>() + k0);
     QLRA_LAUNCH_CHECK();

@@ -373,8 +373,10 @@ def test_c2_full_size_parity(ctx, method):
     assert largest_principal_angle(host(res.qb.h), qb["h"]) <= 1e-8
 
 
-@pytest.mark.parametrize("s", [40, 200])
-def test_singular_values_and_kappa(ctx, s):  # factorizations.cpp:316-337 (both tridiag paths)
+@pytest.mark.parametrize("s", [40, 100, 200, 260])
+def test_singular_values_and_kappa(ctx, s):  # factorizations.cpp:316-337
+    # s = 40: single-CTA shared-memory tridiagonalisation; 100, 200: 8-CTA
+    # cluster kernel; 260: cooperative grid kernel
     from paper_2404_14783_b200 import qlra as Q
     y = planted_conditioned_matrix(3 * s, s, 1e3, 90 + s)
     sv = np.asarray(Q.singular_values(dev(y), ctx))
