@@ -140,7 +140,7 @@ bool hpd_inverse(Ctx& ctx, const QView& g, const QView& ginv, std::vector<double
 // replicated.  rinv_out (optional) receives R^{-1}.
 bool cqr_pass(Ctx& ctx, const QView& y, const QView& hout, bool complex_mode, double shift,
               std::vector<double>* rdiag, double* trace_g, bool distributed = true,
-              const QView* rinv_out = nullptr) {
+              const QView* rinv_out = nullptr, const QView* r_out = nullptr) {
   const int64_t s = y.cols;
   DevQMat g(ctx, s, s);
   if (distributed) gram(ctx, y, g.v);
@@ -156,10 +156,17 @@ bool cqr_pass(Ctx& ctx, const QView& y, const QView& hout, bool complex_mode, do
   if (complex_mode) zero_jk_planes(ctx, g.v);
   if (shift != 0.0) small_add_diag(ctx, g.v, shift);
   DevQMat rinv(ctx, s, s);
-  if (!blocked_chol_inv(ctx, g.v, rinv.v, rdiag)) return false;
+  if (!blocked_chol_inv(ctx, g.v, rinv.v, rdiag, r_out)) return false;
   qgemm(ctx, QLRA_OP_N, QLRA_OP_N, 1.0, y, rinv.v, 0.0, hout);
   if (rinv_out) copy_qmat(ctx, rinv.v, *rinv_out);
   return true;
+}
+
+// r <- next * r (R = R_last ... R_1)
+void chain_r(Ctx& ctx, DevQMat& r, const QView& next) {
+  DevQMat t(ctx, r.v.rows, r.v.cols);
+  qgemm(ctx, QLRA_OP_N, QLRA_OP_N, 1.0, next, r.v, 0.0, t.v);
+  r = std::move(t);
 }
 
 // rinv <- rinv * next (s x s, upper triangular factors of R^{-1} = R1^{-1} R2^{-1} ...)
@@ -171,42 +178,46 @@ void chain_rinv(Ctx& ctx, DevQMat& rinv, const QView& next) {
 
 // CholeskyQR2, or shifted CholeskyQR3 (Fukaya et al.) when the first Gram is
 // not numerically positive definite.  rdiag = diag of the full R factor;
-// rinv (optional, s x s) = R^{-1} of y = h R.
+// optional rinv (s x s) = R^{-1} and rfac = R of y = h R.
 bool cholesky_qr(Ctx& ctx, const QView& y, const QView& h, bool complex_mode, int64_t m_global,
-                 std::vector<double>* rdiag, bool distributed = true, DevQMat* rinv = nullptr) {
+                 std::vector<double>* rdiag, bool distributed = true, DevQMat* rinv = nullptr,
+                 DevQMat* rfac = nullptr) {
   const int64_t s = y.cols;
   DevQMat t1(ctx, y.rows, s);
-  DevQMat r1, r2, r3;
-  if (rinv) {
-    r1 = DevQMat(ctx, s, s);
-    r2 = DevQMat(ctx, s, s);
+  DevQMat ri[3], rf[3];
+  for (int i = 0; i < 2; ++i) {
+    if (rinv) ri[i] = DevQMat(ctx, s, s);
+    if (rfac) rf[i] = DevQMat(ctx, s, s);
   }
+  auto pi = [&](int i) { return rinv ? &ri[i].v : nullptr; };
+  auto pf = [&](int i) { return rfac ? &rf[i].v : nullptr; };
   std::vector<double> d1, d2, d3;
   double tr = 0.0;
-  if (cqr_pass(ctx, y, t1.v, complex_mode, 0.0, &d1, &tr, distributed, rinv ? &r1.v : nullptr)) {
-    if (!cqr_pass(ctx, t1.v, h, complex_mode, 0.0, &d2, nullptr, distributed, rinv ? &r2.v : nullptr))
-      return false;
+  if (cqr_pass(ctx, y, t1.v, complex_mode, 0.0, &d1, &tr, distributed, pi(0), pf(0))) {
+    if (!cqr_pass(ctx, t1.v, h, complex_mode, 0.0, &d2, nullptr, distributed, pi(1), pf(1))) return false;
     if (rdiag) {
       rdiag->resize(s);
       for (int64_t k = 0; k < s; ++k) (*rdiag)[k] = d1[k] * d2[k];
     }
     if (rinv) {
-      *rinv = std::move(r1);
-      chain_rinv(ctx, *rinv, r2.v);
+      *rinv = std::move(ri[0]);
+      chain_rinv(ctx, *rinv, ri[1].v);
+    }
+    if (rfac) {
+      *rfac = std::move(rf[0]);
+      chain_r(ctx, *rfac, rf[1].v);
     }
     return true;
   }
   const double dim = complex_mode ? 2.0 : 4.0;
   const double shift = 11.0 * (dim * (double)m_global * s + s * (s + 1.0)) * kUnit * tr;
   if (!(tr > 0.0)) return false;
-  if (rinv) r3 = DevQMat(ctx, s, s);
-  if (!cqr_pass(ctx, y, t1.v, complex_mode, shift, &d1, nullptr, distributed, rinv ? &r1.v : nullptr))
-    return false;
+  if (rinv) ri[2] = DevQMat(ctx, s, s);
+  if (rfac) rf[2] = DevQMat(ctx, s, s);
+  if (!cqr_pass(ctx, y, t1.v, complex_mode, shift, &d1, nullptr, distributed, pi(0), pf(0))) return false;
   DevQMat t2(ctx, y.rows, s);
-  if (!cqr_pass(ctx, t1.v, t2.v, complex_mode, 0.0, &d2, nullptr, distributed, rinv ? &r2.v : nullptr))
-    return false;
-  if (!cqr_pass(ctx, t2.v, h, complex_mode, 0.0, &d3, nullptr, distributed, rinv ? &r3.v : nullptr))
-    return false;
+  if (!cqr_pass(ctx, t1.v, t2.v, complex_mode, 0.0, &d2, nullptr, distributed, pi(1), pf(1))) return false;
+  if (!cqr_pass(ctx, t2.v, h, complex_mode, 0.0, &d3, nullptr, distributed, pi(2), pf(2))) return false;
   if (rdiag) {
     rdiag->resize(s);
     // y = t1 R1 = t2 R2 R1 = h R3 R2 R1 holds exactly whatever the shift, so
@@ -214,9 +225,14 @@ bool cholesky_qr(Ctx& ctx, const QView& y, const QView& h, bool complex_mode, in
     for (int64_t k = 0; k < s; ++k) (*rdiag)[k] = d1[k] * d2[k] * d3[k];
   }
   if (rinv) {
-    *rinv = std::move(r1);
-    chain_rinv(ctx, *rinv, r2.v);
-    chain_rinv(ctx, *rinv, r3.v);
+    *rinv = std::move(ri[0]);
+    chain_rinv(ctx, *rinv, ri[1].v);
+    chain_rinv(ctx, *rinv, ri[2].v);
+  }
+  if (rfac) {
+    *rfac = std::move(rf[0]);
+    chain_r(ctx, *rfac, rf[1].v);
+    chain_r(ctx, *rfac, rf[2].v);
   }
   return true;
 }
@@ -451,6 +467,7 @@ int qlra_ctx_destroy(qlra_ctx_t* ctx) {
   if (ctx->c.comm) ncclCommDestroy(ctx->c.comm);
   if (ctx->c.own_stream && ctx->c.stream) cudaStreamDestroy(ctx->c.stream);
   if (ctx->c.pinned) cudaFreeHost(ctx->c.pinned);
+  if (ctx->c.tile_cnt) cudaFree(ctx->c.tile_cnt);
   delete ctx;
   return QLRA_OK;
 }
@@ -701,36 +718,33 @@ int qlra_pseudo_qr(qlra_ctx_t* ctx, const qlra_qmat_t* y, const qlra_pseudo_qr_c
       fail(QLRA_ERR_PARAMETER, "pseudo_qr: delta_budget outside [1, sqrt(7)/2]");
     if (h->rows != y->rows || h->cols != s) fail(QLRA_ERR_SHAPE, "pseudo_qr: output shape mismatch");
     const QView Y = view_of(y), H = view_of(h);
-    // complex_qr(to_compact(Y)) via CholeskyQR on the compact Gram
-    std::vector<double> rd;
-    if (!cholesky_qr(c, Y, H, /*complex_mode=*/true, m, &rd))
+    // Y = Q0 R_q by quaternion CholeskyQR2 -- the only factorisation of the
+    // tall sketch.  Writing Y = Q0 R_q in compact form, compact(Y) =
+    // U compact(R_q) with U (2m x 2s) the compact image of Q0, orthonormal
+    // columns; so the reference's complex_qr(to_compact(Y))
+    // (rangefinders.cpp:117) has the R factor R_c of compact(R_q), and its
+    // basis is H0 = Q0 C with C = R_q R_c^{-1}: a complex-mode CholeskyQR2 of
+    // the small s x s R_q.  Every correction step then acts on the s x s
+    // coefficient matrix (H_k = Q0 C_k, kappa(H_k) = kappa(C_k) because Q0 is
+    // orthonormal), and one tall product H = Q0 C_k closes the pass.  H lies in
+    // range(Q0) = range(H0) to rounding, which is what the reference's
+    // re-projection (rangefinders.cpp:142-153) restores.
+    DevQMat q0(c, Y.rows, s), rq;
+    if (!cholesky_qr(c, Y, q0.v, /*complex_mode=*/false, m, nullptr, /*distributed=*/true, nullptr, &rq))
       fail(QLRA_ERR_RANK, "pseudo_qr: sketch numerically rank-deficient; use pseudo_svd");
-    rank_check(rd);
+    DevQMat cm(c, s, s);
+    std::vector<double> rd;
+    if (!cholesky_qr(c, rq.v, cm.v, /*complex_mode=*/true, s, &rd, /*distributed=*/false))
+      fail(QLRA_ERR_RANK, "pseudo_qr: sketch numerically rank-deficient; use pseudo_svd");
+    rank_check(rd);  // |diag R_c|, rangefinders.cpp:118-126
     qlra_rangefinder_report_t r{};
     r.method = QLRA_PSEUDO_QR;
-    DevQMat g(c, s, s);
-    gram(c, H, g.v);
+    DevQMat g(c, s, s), mk(c, s, s);
+    qgemm(c, QLRA_OP_C, QLRA_OP_N, 1.0, cm.v, cm.v, 0.0, g.v);  // H0^* H0 = C^* C
     r.kappa_before = kappa_from_eigs(quat_eigs(c, g.v));
     double kappa = r.kappa_before;
-    // Correction steps H_k = H_{k-1} ((1-eps) I + eps G_{k-1}^{-1}) are tracked
-    // as one small product M (s x s) and H_k is formed as H0 * M from the QR
-    // basis H0 (one tall product instead of a chain).  The rounding of that
-    // product still leaks ~u |H0| |M| outside range(H0) (|M| ~ eps/sigma_min^2
-    // reaches 1e4 at C1), so, as the reference does (rangefinders.cpp:142-153),
-    // H is re-projected onto range(H0) = span[Q, J conj Q] -- through a
-    // quaternion-orthonormal basis Q0 of range(H0) (CholeskyQR2):
-    // H <- Q0 (Q0^* H_k).  Measured on C1 this lands within 2e-13 of the
-    // exact-range QB error, where the unprojected H0*M was 2e-10 off.
-    DevQMat h0, mt, mk;
     try {
       while (r.correction_steps_used < cfg.max_correction_steps && kappa > kKappaTarget) {
-        if (r.correction_steps_used == 0) {
-          h0 = DevQMat(c, H.rows, s);
-          copy_qmat(c, H, h0.v);
-          mt = DevQMat(c, s, s);
-          small_set_identity(c, mt.v);
-          mk = DevQMat(c, s, s);
-        }
         // one inverse serves estimate_epsilon and correction_step (both
         // factor the same H^*H, rangefinders.cpp:68,102)
         check_gram_rcond(kappa, 1e-15, "estimate_epsilon: H*H numerically singular");
@@ -738,12 +752,12 @@ int qlra_pseudo_qr(qlra_ctx_t* ctx, const qlra_qmat_t* y, const qlra_pseudo_qr_c
         const double eps = estimate_epsilon_from_inverse(c, ginv.v, cfg.power_iters_for_epsilon);
         if (!(eps > 0.0 && eps < 1.0))
           fail(QLRA_ERR_PARAMETER, "correction_step: epsilon must lie in (0,1)");
+        // H_{k+1} = H_k ((1-eps) I + eps G_k^{-1})  (rangefinders.cpp:99-105)
         small_axpby_identity(c, 1.0 - eps, eps, ginv.v, mk.v);
-        DevQMat mnew(c, s, s);
-        qgemm(c, QLRA_OP_N, QLRA_OP_N, 1.0, mt.v, mk.v, 0.0, mnew.v);
-        mt = std::move(mnew);
-        qgemm(c, QLRA_OP_N, QLRA_OP_N, 1.0, h0.v, mt.v, 0.0, H);
-        gram(c, H, g.v);
+        DevQMat cn(c, s, s);
+        qgemm(c, QLRA_OP_N, QLRA_OP_N, 1.0, cm.v, mk.v, 0.0, cn.v);
+        cm = std::move(cn);
+        qgemm(c, QLRA_OP_C, QLRA_OP_N, 1.0, cm.v, cm.v, 0.0, g.v);
         kappa = kappa_from_eigs(quat_eigs(c, g.v));
         ++r.correction_steps_used;
       }
@@ -751,17 +765,7 @@ int qlra_pseudo_qr(qlra_ctx_t* ctx, const qlra_qmat_t* y, const qlra_pseudo_qr_c
       if (e.code != QLRA_ERR_SINGULAR) throw;
       fail(QLRA_ERR_RANK, "pseudo_qr: sketch numerically rank-deficient; use pseudo_svd");
     }
-    if (r.correction_steps_used > 0) {
-      DevQMat q0(c, H.rows, s), t(c, s, s);
-      if (!cholesky_qr(c, h0.v, q0.v, /*complex_mode=*/false, m, nullptr))
-        fail(QLRA_ERR_RANK, "pseudo_qr: sketch numerically rank-deficient; use pseudo_svd");
-      qgemm(c, QLRA_OP_C, QLRA_OP_N, 1.0, q0.v, H, 0.0, t.v);
-      allreduce_qmat(c, t.v);
-      qgemm(c, QLRA_OP_N, QLRA_OP_N, 1.0, q0.v, t.v, 0.0, H);
-      // kappa_after (rangefinders.cpp:153): the projection moves H only by
-      // the rounding it removes (H_k already lies in range(H0)), so the
-      // condition number of the last iterate is kept.
-    }
+    qgemm(c, QLRA_OP_N, QLRA_OP_N, 1.0, q0.v, cm.v, 0.0, H);
     r.kappa_after = kappa;
     if (rep) *rep = r;
   });

@@ -28,6 +28,10 @@ struct Ctx {
   std::string last_error;
   double last_cond = 0.0;
   double* pinned = nullptr;  // small host staging buffer (syncs)
+  // per-tile arrival counters of the split-K small GEMM (self-resetting:
+  // the last CTA of a tile sets its counter back to 0)
+  unsigned* tile_cnt = nullptr;
+  int64_t tile_cnt_n = 0;
   // Optional per-launch timing of the fused sketch kernel (bench evidence):
   // CUDA events bracket every launch on the launching stream.
   struct KernelTimer {
@@ -161,8 +165,10 @@ void sigma_vadj(Ctx& ctx, const double* d_sigma, const QView& v, const QView& ou
 // qsvd phase convention on (U, V) columns (factorizations.cpp:273-293)
 void qsvd_phase(Ctx& ctx, const QView& u, const QView& v);
 // Blocked quaternion Cholesky G = R^*R (R upper) returning R^{-1} in rinv
-// (s x s, fully written) and diag(R); false if G is not numerically PD.
-bool blocked_chol_inv(Ctx& ctx, const QView& g, const QView& rinv, std::vector<double>* rdiag);
+// (s x s, fully written), diag(R) and optionally R itself; false if G is not
+// numerically PD.
+bool blocked_chol_inv(Ctx& ctx, const QView& g, const QView& rinv, std::vector<double>* rdiag,
+                      const QView* r_out = nullptr);
 // zero the j, k planes (restrict a quaternion matrix to its complex part)
 void zero_jk_planes(Ctx& ctx, const QView& g);
 // Quaternion Cholesky G = R^*R in place (upper triangle), *d_info as above.

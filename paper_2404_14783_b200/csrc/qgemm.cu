@@ -146,6 +146,156 @@ __global__ void residual_finish_kernel(const double* red, int64_t nblocks, doubl
   }
 }
 
+// ---------------------------------------------------------------------------
+// Small products (s x s blocks of the factorisations, s x s x l Grams): a
+// 64x64 DMMA tile on one SM is bound by that SM's FP64 rate (~0.25 TF/s), so
+// a 100x100x100 quaternion product on 4 CTAs takes ~30 us.  Here every CTA
+// owns a 16x16 quaternion output tile (one element per thread, 16 FP64 FMA
+// per quaternion MAC on the CUDA cores), K is staged through shared memory
+// in chunks of SKC, and K is split over gridDim.z.  Split partials go to a
+// workspace; the last CTA to arrive at a tile (per-tile counter) sums them in
+// ascending split order -- deterministic -- and applies alpha/beta.
+constexpr int STL = 16;   // output tile edge (quaternions)
+constexpr int SKC = 32;   // k chunk staged in shared memory
+
+struct SmallArgs {
+  qt::Operands op;
+  double* c[4];
+  int64_t ldc, K, kchunk;
+  double alpha, beta;
+  double* ws;        // [z][tile][4][256] partials (split only)
+  unsigned* cnt;     // [tile] arrival counters
+};
+
+template <bool CA, bool CB>
+__global__ void __launch_bounds__(256) qgemm_small_kernel(SmallArgs g) {
+  __shared__ double as[4][STL][SKC + 1];
+  __shared__ double bs[4][SKC][STL + 1];
+  __shared__ unsigned s_last;
+  const int t = threadIdx.x, ti = t >> 4, tj = t & 15;
+  const int64_t M = g.op.M, N = g.op.N;
+  const int64_t i0 = (int64_t)blockIdx.y * STL, j0 = (int64_t)blockIdx.x * STL;
+  const int64_t kbeg = (int64_t)blockIdx.z * g.kchunk, kend = min(g.K, kbeg + g.kchunk);
+  double aw = 0.0, ax = 0.0, ay = 0.0, az = 0.0;
+  const double sa = CA ? -1.0 : 1.0, sb = CB ? -1.0 : 1.0;
+  for (int64_t k0 = kbeg; k0 < kend; k0 += SKC) {
+    // op(A)(i, k) = A[i*a_si + k*a_sk] (conjugated when CA); coalesce along
+    // the unit-stride index
+    for (int e = t; e < STL * SKC; e += 256) {
+      const int r = CA ? (e % STL) : (e / SKC), kk = CA ? (e / STL) : (e % SKC);
+      const int64_t gi = i0 + r, gk = k0 + kk;
+      const bool ok = gi < M && gk < kend;
+      const int64_t o = gi * g.op.a_si + gk * g.op.a_sk;
+#pragma unroll
+      for (int p = 0; p < 4; ++p) {
+        const double v = ok ? g.op.a[p][o] : 0.0;
+        as[p][r][kk] = p == 0 ? v : sa * v;
+      }
+    }
+    for (int e = t; e < SKC * STL; e += 256) {
+      const int kk = CB ? (e % SKC) : (e / STL), c = CB ? (e / SKC) : (e % STL);
+      const int64_t gk = k0 + kk, gj = j0 + c;
+      const bool ok = gk < kend && gj < N;
+      const int64_t o = gk * g.op.b_sk + gj * g.op.b_sj;
+#pragma unroll
+      for (int p = 0; p < 4; ++p) {
+        const double v = ok ? g.op.b[p][o] : 0.0;
+        bs[p][kk][c] = p == 0 ? v : sb * v;
+      }
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int kk = 0; kk < SKC; ++kk) {
+      const double a0 = as[0][ti][kk], a1 = as[1][ti][kk], a2 = as[2][ti][kk], a3 = as[3][ti][kk];
+      const double b0 = bs[0][kk][tj], b1 = bs[1][kk][tj], b2 = bs[2][kk][tj], b3 = bs[3][kk][tj];
+      aw = fma(a0, b0, aw); aw = fma(-a1, b1, aw); aw = fma(-a2, b2, aw); aw = fma(-a3, b3, aw);
+      ax = fma(a0, b1, ax); ax = fma(a1, b0, ax); ax = fma(a2, b3, ax); ax = fma(-a3, b2, ax);
+      ay = fma(a0, b2, ay); ay = fma(-a1, b3, ay); ay = fma(a2, b0, ay); ay = fma(a3, b1, ay);
+      az = fma(a0, b3, az); az = fma(a1, b2, az); az = fma(-a2, b1, az); az = fma(a3, b0, az);
+    }
+    __syncthreads();
+  }
+  const int64_t gi = i0 + ti, gj = j0 + tj;
+  const bool in = gi < M && gj < N;
+  if (gridDim.z == 1) {
+    if (in) {
+      const double v[4] = {aw, ax, ay, az};
+#pragma unroll
+      for (int p = 0; p < 4; ++p) {
+        double* dst = g.c[p] + gi * g.ldc + gj;
+        const double r = g.alpha * v[p];
+        *dst = g.beta != 0.0 ? fma(g.beta, *dst, r) : r;
+      }
+    }
+    return;
+  }
+  const int64_t tile = (int64_t)blockIdx.y * gridDim.x + blockIdx.x;
+  const int64_t ntile = (int64_t)gridDim.x * gridDim.y;
+  double* w = g.ws + (((int64_t)blockIdx.z * ntile + tile) * 4) * 256;
+  w[0 * 256 + t] = aw;
+  w[1 * 256 + t] = ax;
+  w[2 * 256 + t] = ay;
+  w[3 * 256 + t] = az;
+  __threadfence();
+  __syncthreads();
+  if (t == 0) s_last = atomicAdd(&g.cnt[tile], 1u) == gridDim.z - 1 ? 1u : 0u;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  if (in) {
+#pragma unroll
+    for (int p = 0; p < 4; ++p) {
+      double s = 0.0;
+      for (unsigned z = 0; z < gridDim.z; ++z) s += __ldcg(g.ws + ((z * ntile + tile) * 4 + p) * 256 + t);
+      double* dst = g.c[p] + gi * g.ldc + gj;
+      const double r = g.alpha * s;
+      *dst = g.beta != 0.0 ? fma(g.beta, *dst, r) : r;
+    }
+  }
+  if (t == 0) g.cnt[tile] = 0u;  // ready for the next launch on this stream
+}
+
+void small_gemm(Ctx& ctx, bool ca, bool cb, const GemmArgs& ga, int64_t M, int64_t N, int64_t K,
+                const QView& C) {
+  SmallArgs g{};
+  g.op = ga.op;
+  for (int p = 0; p < 4; ++p) g.c[p] = C.p[p];
+  g.ldc = C.ld;
+  g.K = K;
+  g.alpha = ga.alpha;
+  g.beta = ga.beta;
+  const int64_t tm = (M + STL - 1) / STL, tn = (N + STL - 1) / STL, tiles = tm * tn;
+  // split K to reach about two CTAs per SM, >= 2 chunks of SKC per split
+  int64_t z = std::max<int64_t>(1, std::min<int64_t>((296 + tiles - 1) / tiles, K / (2 * SKC)));
+  z = std::min<int64_t>(z, 64);
+  int64_t kchunk = (K + z - 1) / z;
+  kchunk = std::max<int64_t>(SKC, ((kchunk + SKC - 1) / SKC) * SKC);
+  z = K > 0 ? (K + kchunk - 1) / kchunk : 1;
+  g.kchunk = std::max<int64_t>(kchunk, 1);
+  DeviceBuffer ws;
+  if (z > 1) {
+    if (ctx.tile_cnt_n < tiles) {
+      if (ctx.tile_cnt) {
+        QLRA_CUDA(cudaStreamSynchronize(ctx.stream));
+        QLRA_CUDA(cudaFree(ctx.tile_cnt));
+      }
+      ctx.tile_cnt_n = std::max<int64_t>(tiles, 4096);
+      QLRA_CUDA(cudaMalloc(&ctx.tile_cnt, sizeof(unsigned) * (size_t)ctx.tile_cnt_n));
+      QLRA_CUDA(cudaMemsetAsync(ctx.tile_cnt, 0, sizeof(unsigned) * (size_t)ctx.tile_cnt_n, ctx.stream));
+    }
+    ws = DeviceBuffer(ctx, sizeof(double) * (size_t)(z * tiles * 4 * 256));
+    g.ws = ws.as<double>();
+    g.cnt = ctx.tile_cnt;
+  }
+  dim3 grid((unsigned)tn, (unsigned)tm, (unsigned)z);
+  if (!ca && !cb) qgemm_small_kernel<false, false><<<grid, 256, 0, ctx.stream>>>(g);
+  else if (ca && !cb) qgemm_small_kernel<true, false><<<grid, 256, 0, ctx.stream>>>(g);
+  else if (!ca && cb) qgemm_small_kernel<false, true><<<grid, 256, 0, ctx.stream>>>(g);
+  else qgemm_small_kernel<true, true><<<grid, 256, 0, ctx.stream>>>(g);
+  QLRA_LAUNCH_CHECK();
+  count_launch();
+}
+
 template <bool CA, bool CB, int MODE>
 void set_attr() {
   static bool done = false;
@@ -229,6 +379,12 @@ void qgemm(Ctx& ctx, int op_a, int op_b, double alpha, const QView& A, const QVi
   g.ldc = C.ld;
   const int64_t tm = (M + BM - 1) / BM, tn = (N + BN - 1) / BN;
   const int64_t tiles = tm * tn;
+  // Small products: the 64x64 DMMA tiles (+ split-K of >= 24 k-steps) cannot
+  // fill the GPU -- use the 16x16-tile path.
+  if (force_splits <= 0 && K > 0 && tiles * std::max<int64_t>(1, K / (24 * BK)) < 148) {
+    small_gemm(ctx, op_a == QLRA_OP_C, op_b == QLRA_OP_C, g, M, N, K, C);
+    return;
+  }
   int64_t nsplit = 1;
   if (force_splits > 0) {
     nsplit = force_splits;

@@ -1473,7 +1473,8 @@ void qsvd_phase(Ctx& ctx, const QView& u, const QView& v) {
 // R_12 = R_11^{-*} G_12 and trailing updates G_22 -= R_12^* R_12 run on the
 // DMMA GEMM, and R^{-1} follows by block back-substitution
 // X_{i, i+1:} = -R_ii^{-1} (R_{i, i+1:} X_{i+1:, i+1:}).
-bool blocked_chol_inv(Ctx& ctx, const QView& g, const QView& rinv, std::vector<double>* rdiag) {
+bool blocked_chol_inv(Ctx& ctx, const QView& g, const QView& rinv, std::vector<double>* rdiag,
+                      const QView* r_out) {
   const int64_t s = g.rows;
   if (s == 0) return true;
   static bool attr = false;
@@ -1523,6 +1524,7 @@ bool blocked_chol_inv(Ctx& ctx, const QView& g, const QView& rinv, std::vector<d
       qgemm(ctx, QLRA_OP_N, QLRA_OP_N, -1.0, sub(rinv, i0, i0, ib, ib), t, 0.0, sub(rinv, i0, j0, ib, rest));
     }
   }
+  if (r_out) copy_qmat(ctx, r.v, *r_out);
   return true;
 }
 

@@ -65,6 +65,27 @@ def test_qmat_mul_adjoint_ops(ctx):
     assert rel_diff(r, O.qmat_mul(a, O.adjoint(c))) < 1e-13
 
 
+@pytest.mark.parametrize("m,k,n", [(100, 100, 100), (100, 200, 100), (36, 64, 64), (16, 5000, 16),
+                                   (300, 1000, 100)])
+@pytest.mark.parametrize("op_a,op_b", [(0, 0), (1, 0), (0, 1), (1, 1)])
+def test_qmat_mul_small_and_split_paths(ctx, m, k, n, op_a, op_b):
+    """Both product paths (16x16-tile split-K with in-kernel ordered
+    reduction; 64x64 DMMA tiles) for every op pair, with alpha/beta, and
+    bitwise repeatable."""
+    from paper_2404_14783_b200 import qlra as Q
+    a = random_gaussian(k, m, 31) if op_a else random_gaussian(m, k, 31)
+    b = random_gaussian(n, k, 32) if op_b else random_gaussian(k, n, 32)
+    c0 = random_gaussian(m, n, 33)
+    ref = 0.5 * O.qmat_mul(O.adjoint(a) if op_a else a, O.adjoint(b) if op_b else b) - 2.0 * c0
+    outs = []
+    for _ in range(2):
+        out = dev(c0)
+        Q.qmat_mul(dev(a), dev(b), op_a=op_a, op_b=op_b, alpha=0.5, beta=-2.0, out=out)
+        outs.append(host(out))
+    assert rel_diff(outs[0], ref) < 1e-13
+    assert np.array_equal(outs[0], outs[1])
+
+
 def test_unit_relations_on_device(ctx):  # test_quaternion_core.cpp:18-35
     from paper_2404_14783_b200 import qlra as Q
     i, j = dev(scalar(0, 1)), dev(scalar(0, 0, 1))
