@@ -789,19 +789,60 @@ __global__ void __launch_bounds__(512) k_qtridiag_smem(QView a, double* d, doubl
   for (int i = t; i < n; i += blockDim.x) d[i] = L[tri(i, i)].w;
 }
 
-// Cluster variant of k_qtridiag for QT_SMEM_MAX < n <= QTC_MAX: one cluster
-// of QTC CTAs on QTC SMs (the single-CTA kernel is bound by one SM's FP64
-// pipe).  Row r lives in the shared memory of CTA r % QTC (full rows, both
-// triangles).  Step k: the owner of row k broadcasts x = conj(A[k, k+1:]) (the
-// Hermitian image of column k) into every CTA's v buffer over DSMEM; every CTA
-// forms the identical reflector redundantly; each CTA computes p = beta A v
-// for its rows and scatters it into every CTA's p buffer; then each CTA
-// applies A -= v w^* + w v^* to its rows.  Two cluster barriers per step; v
-// is double-buffered across steps so the next broadcast cannot overwrite a v
-// still being read.  Same reflectors as k_qtridiag.
+// Cluster variant of k_qtridiag for 48 < n <= QTC_MAX: one cluster of QTC
+// CTAs on QTC SMs (the single-CTA kernel is bound by one SM's FP64 pipe).
+// Row r lives in the shared memory of CTA r % QTC (full rows, both
+// triangles).  Step k: every CTA all-gathers x = A[k+1:, k] -- each owner
+// holds the current column-k entries of its own rows -- into every CTA's v
+// buffer; every CTA forms the identical reflector redundantly; each CTA
+// computes p = beta A v for its rows and all-gathers p; then each CTA applies
+// A -= v w^* + w v^* to its rows (warp per row).  The exchanges are
+// point-to-point: st.async into the peer's shared memory completes bytes on
+// the peer's mbarrier (mbarrier::complete_tx), and each CTA waits on its own
+// barrier for len * 32 bytes -- no cluster-wide rendezvous per step.  Buffer
+// reuse is ordered by the data dependencies: a peer sends v(k+2) only after
+// it has this CTA's p(k+1), i.e. after this CTA finished step k with v(k)
+// (v double-buffered), and p(k+1) only after it has this CTA's part of
+// v(k+1), i.e. after this CTA finished reading p(k).
+// Same reflectors as k_qtridiag.
 constexpr int QTC = 8;
 constexpr int QTC_MAX = 224;
 constexpr int QTC_THREADS = 256;
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(smem_addr(bar)),
+      "r"(parity)
+      : "memory");
+}
+// store q into `dst` (an address in this CTA's layout) of CTA `rank`,
+// completing 32 bytes on that CTA's barrier `bar` (same layout)
+__device__ __forceinline__ void st_async_q4(const Q4* dst, const uint64_t* bar, unsigned rank, Q4 q) {
+  uint32_t ra, rb;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(smem_addr(dst)), "r"(rank));
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rb) : "r"(smem_addr(bar)), "r"(rank));
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];" ::"r"(ra),
+               "d"(q.w), "d"(q.x), "r"(rb)
+               : "memory");
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];" ::"r"(ra + 16),
+               "d"(q.y), "d"(q.z), "r"(rb)
+               : "memory");
+}
+
 __global__ void __cluster_dims__(QTC, 1, 1) __launch_bounds__(QTC_THREADS)
     k_qtridiag_cluster(QView a, double* d, double* e) {
   namespace cg = cooperative_groups;
@@ -812,25 +853,31 @@ __global__ void __cluster_dims__(QTC, 1, 1) __launch_bounds__(QTC_THREADS)
   Q4* rows = reinterpret_cast<Q4*>(dsm);  // rmax x n: global row rank + QTC*li
   Q4* vb = rows + (size_t)rmax * n;       // 2 x n
   Q4* pb = vb + 2 * n;                    // n
+  __shared__ __align__(8) uint64_t bar_v[2], bar_p;
   __shared__ double s_beta;
   const int t = threadIdx.x, lane = t & 31, wid = t >> 5, nw = blockDim.x >> 5;
   for (int li = wid; li < nr; li += nw)
     for (int c = lane; c < n; c += 32) rows[li * n + c] = qload(a, rank + QTC * li, c);
-  cl.sync();
+  if (t == 0) {
+    mbar_init(&bar_v[0], 1);
+    mbar_init(&bar_v[1], 1);
+    mbar_init(&bar_p, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  cl.sync();  // barriers initialised everywhere before any peer sends
+  unsigned pphase = 0;
   for (int k = 0; k + 1 < n; ++k) {
     const int len = n - k - 1, o = k + 1;
-    Q4* v = vb + (k & 1) * n;
-    if (k % QTC == rank) {
-      const Q4* src = rows + (k / QTC) * n + o;
-      for (int dst = 0; dst < QTC; ++dst) {
-        Q4* rv = cl.map_shared_rank(v, dst);
-        for (int i = t; i < len; i += blockDim.x) {
-          const Q4 q = src[i];
-          rv[i] = Q4{q.w, -q.x, -q.y, -q.z};
-        }
-      }
+    const int vb_i = k & 1;
+    Q4* v = vb + vb_i * n;
+    const unsigned vphase = (unsigned)(k >> 1) & 1u;
+    if (t == 0) mbar_arrive_expect(&bar_v[vb_i], 32u * (unsigned)len);
+    const int first = (o - rank + QTC - 1) / QTC;  // first owned row >= o
+    for (int q = t; q < (nr - first) * QTC; q += blockDim.x) {
+      const int li = first + q / QTC, dst = q % QTC;
+      st_async_q4(v + (rank + QTC * li - o), &bar_v[vb_i], (unsigned)dst, rows[li * n + k]);
     }
-    cl.sync();
+    mbar_wait(&bar_v[vb_i], vphase);
     if (wid == 0) {
       double part = 0.0;
       for (int i = lane; i < len; i += 32) {
@@ -841,21 +888,22 @@ __global__ void __cluster_dims__(QTC, 1, 1) __launch_bounds__(QTC_THREADS)
       const Q4 x1 = v[0];
       const double ax1 = sqrt(x1.w * x1.w + x1.x * x1.x + x1.y * x1.y + x1.z * x1.z);
       const double alpha = sqrt(nrm2);
-      const Q4 phi = ax1 > 0.0 ? Q4{x1.w / ax1, x1.x / ax1, x1.y / ax1, x1.z / ax1} : Q4{1.0, 0.0, 0.0, 0.0};
-      const double beta = alpha > 0.0 ? 2.0 / (2.0 * alpha * alpha + 2.0 * alpha * ax1) : 0.0;
+      const double ia = ax1 > 0.0 ? 1.0 / ax1 : 0.0;
+      const Q4 phi = ax1 > 0.0 ? Q4{x1.w * ia, x1.x * ia, x1.y * ia, x1.z * ia} : Q4{1.0, 0.0, 0.0, 0.0};
+      const double beta = alpha > 0.0 ? 1.0 / (alpha * alpha + alpha * ax1) : 0.0;
       __syncwarp();
       if (lane == 0) {
         v[0] = Q4{x1.w + phi.w * alpha, x1.x + phi.x * alpha, x1.y + phi.y * alpha, x1.z + phi.z * alpha};
         s_beta = beta;
         if (rank == 0) e[k] = alpha;
+        if (beta != 0.0) mbar_arrive_expect(&bar_p, 32u * (unsigned)len);
       }
     }
     __syncthreads();
     const double beta = s_beta;  // bitwise identical in every CTA
-    if (beta == 0.0) continue;
-    for (int li = wid; li < nr; li += nw) {
+    if (beta == 0.0) continue;   // no p exchange this step, anywhere
+    for (int li = first + wid; li < nr; li += nw) {
       const int r = rank + QTC * li;
-      if (r < o) continue;
       const Q4* row = rows + li * n + o;
       Q4 acc{0.0, 0.0, 0.0, 0.0};
       for (int c = lane; c < len; c += 32) {
@@ -866,28 +914,33 @@ __global__ void __cluster_dims__(QTC, 1, 1) __launch_bounds__(QTC_THREADS)
       acc.x = warp_sum(acc.x);
       acc.y = warp_sum(acc.y);
       acc.z = warp_sum(acc.z);
-      if (lane < QTC) cl.map_shared_rank(pb, lane)[r - o] = Q4{beta * acc.w, beta * acc.x, beta * acc.y, beta * acc.z};
+      if (lane < QTC)
+        st_async_q4(pb + (r - o), &bar_p, (unsigned)lane,
+                    Q4{beta * acc.w, beta * acc.x, beta * acc.y, beta * acc.z});
     }
-    cl.sync();
+    mbar_wait(&bar_p, pphase);
+    pphase ^= 1u;
     double cp = 0.0;
     for (int i = lane; i < len; i += 32)
       cp += v[i].w * pb[i].w + v[i].x * pb[i].x + v[i].y * pb[i].y + v[i].z * pb[i].z;
     const double hk = 0.5 * beta * warp_sum(cp);
-    const int first = (o - rank + QTC - 1) / QTC;  // first owned row >= o
-    const int nt = nr - first;
-    for (int q = t; q < nt * len; q += blockDim.x) {
-      const int li = first + q / len, cc = q % len;
+    for (int li = first + wid; li < nr; li += nw) {
       const int ri = rank + QTC * li - o;
-      const Q4 vr = v[ri], pr = pb[ri], vc0 = v[cc], pc = pb[cc];
+      const Q4 vr = v[ri], pr = pb[ri];
       const Q4 wr{pr.w - hk * vr.w, pr.x - hk * vr.x, pr.y - hk * vr.y, pr.z - hk * vr.z};
-      const Q4 wc{pc.w - hk * vc0.w, -(pc.x - hk * vc0.x), -(pc.y - hk * vc0.y), -(pc.z - hk * vc0.z)};
-      const Q4 vc{vc0.w, -vc0.x, -vc0.y, -vc0.z};
-      const Q4 t1 = qmul(vr, wc), t2 = qmul(wr, vc);
-      Q4& dst = rows[li * n + o + cc];
-      dst.w -= t1.w + t2.w;
-      dst.x -= t1.x + t2.x;
-      dst.y -= t1.y + t2.y;
-      dst.z -= t1.z + t2.z;
+      Q4* row = rows + li * n + o;
+      for (int cc = lane; cc < len; cc += 32) {
+        const Q4 vc0 = v[cc], pc = pb[cc];
+        const Q4 wc{pc.w - hk * vc0.w, -(pc.x - hk * vc0.x), -(pc.y - hk * vc0.y), -(pc.z - hk * vc0.z)};
+        const Q4 vc{vc0.w, -vc0.x, -vc0.y, -vc0.z};
+        const Q4 t1 = qmul(vr, wc), t2 = qmul(wr, vc);
+        Q4 dst = row[cc];
+        dst.w -= t1.w + t2.w;
+        dst.x -= t1.x + t2.x;
+        dst.y -= t1.y + t2.y;
+        dst.z -= t1.z + t2.z;
+        row[cc] = dst;
+      }
     }
     __syncthreads();
   }
@@ -895,7 +948,7 @@ __global__ void __cluster_dims__(QTC, 1, 1) __launch_bounds__(QTC_THREADS)
     const int r = rank + QTC * li;
     d[r] = rows[li * n + r].w;
   }
-  cl.sync();  // no CTA exits while a peer may still touch its shared memory
+  cl.sync();  // no CTA exits while a peer may still write into its shared memory
 }
 
 // Parallel cyclic Jacobi eigensolver for a quaternion Hermitian matrix
@@ -1332,6 +1385,182 @@ unsigned grid_for(int64_t total) {
   return (unsigned)b;
 }
 
+
+// ---------------------------------------------------------------------------
+// Cholesky + triangular inverse of a Hermitian PD quaternion G (s <= CHC_MAX)
+// in ONE launch: a cluster of CHC CTAs (one per SM) on 16x16 quaternion
+// tiles; R and X = R^{-1} live in (L2-resident) global memory, the output
+// arrays.  Left-looking (Crout) block order, one cluster barrier per block
+// step J:
+//   every CTA   A_JJ = G_JJ - sum_{I<J} R_IJ^* R_IJ, factors and inverts it
+//               (redundantly -- bitwise identical in every CTA, so pivot
+//               failure is a uniform decision and needs no broadcast);
+//   owners      R_JK = X_JJ^* (G_JK - sum_{I<J} R_IJ^* R_IK),  K > J;
+//   owners      X_IJ = -(sum_{K=I}^{J-1} X_IK R_KJ) X_JJ,       I < J.
+// Column J of R is loaded into shared memory once per step; streamed operand
+// tiles come in batches of CHB (one L2 round trip per batch).  Tile (I, J)
+// belongs to CTA (linear upper-triangle index) % CHC.  Elements past s act as
+// the identity (padded tiles factor trivially and are never stored).
+constexpr int CHC = 8;
+constexpr int CTB = 16;
+constexpr int CHC_MAX = 256;
+constexpr int CHB = 4;
+using Tile = Q4[CTB][CTB];
+
+struct CholArgs {
+  QView g, r, x;
+  double* rdiag;
+  int* info;
+};
+
+__device__ __forceinline__ int chc_owner(int I, int J, int nb) {
+  return (I <= J ? I * nb - I * (I - 1) / 2 + (J - I) : I * nb + J) % CHC;
+}
+__device__ __forceinline__ Q4 qconj(Q4 q) { return Q4{q.w, -q.x, -q.y, -q.z}; }
+__device__ __forceinline__ void qacc(Q4& a, Q4 b, double sgn) {
+  a.w += sgn * b.w; a.x += sgn * b.x; a.y += sgn * b.y; a.z += sgn * b.z;
+}
+// one element per thread: (i, j) = (t >> 4, t & 15)
+__device__ __forceinline__ Q4 tile_get(const QView& m, int I, int J, int s, int i, int j) {
+  const int gi = I * CTB + i, gj = J * CTB + j;
+  if (gi < s && gj < s) return qload(m, gi, gj);
+  return Q4{gi == gj ? 1.0 : 0.0, 0.0, 0.0, 0.0};
+}
+__device__ __forceinline__ void tile_put(const QView& m, int I, int J, int s, int i, int j, Q4 q) {
+  const int gi = I * CTB + i, gj = J * CTB + j;
+  if (gi < s && gj < s) qstore(m, gi, gj, q);
+}
+// sum_m op(P)[i][m] Q[m][j]; P conjugate-transposed when CP
+template <bool CP>
+__device__ __forceinline__ Q4 tile_dot(const Tile& P, const Tile& Qt, int i, int j) {
+  Q4 e{0.0, 0.0, 0.0, 0.0}, o{0.0, 0.0, 0.0, 0.0};  // two chains for ILP
+#pragma unroll
+  for (int m = 0; m < CTB; m += 2) {
+    const Q4 a0 = CP ? qconj(P[m][i]) : P[i][m];
+    const Q4 a1 = CP ? qconj(P[m + 1][i]) : P[i][m + 1];
+    qacc(e, qmul(a0, Qt[m][j]), 1.0);
+    qacc(o, qmul(a1, Qt[m + 1][j]), 1.0);
+  }
+  qacc(e, o, 1.0);
+  return e;
+}
+
+__global__ void __cluster_dims__(CHC, 1, 1) __launch_bounds__(256) k_chol_inv_cluster(CholArgs A) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  extern __shared__ __align__(16) unsigned char dsm[];
+  const int s = (int)A.g.rows, nb = (s + CTB - 1) / CTB, me = (int)cl.block_rank();
+  Tile* col = reinterpret_cast<Tile*>(dsm);  // nb tiles: R_IJ, I < J
+  Tile* buf = col + nb;                       // CHB streamed tiles
+  Tile& ta = buf[CHB];                        // work
+  Tile& rjj = buf[CHB + 1];
+  Tile& xjj = buf[CHB + 2];
+  __shared__ double dg[CTB];
+  const int t = threadIdx.x, i = t >> 4, j = t & 15;
+  const Q4 zero{0.0, 0.0, 0.0, 0.0};
+  for (int I = 1; I < nb; ++I)
+    for (int J = 0; J < I; ++J)
+      if (chc_owner(I, J, nb) == me) {
+        tile_put(A.r, I, J, s, i, j, zero);
+        tile_put(A.x, I, J, s, i, j, zero);
+      }
+  for (int J = 0; J < nb; ++J) {
+    for (int I = 0; I < J; ++I) col[I][i][j] = tile_get(A.r, I, J, s, i, j);
+    Q4 a = tile_get(A.g, J, J, s, i, j);
+    __syncthreads();
+    for (int I = 0; I < J; ++I) qacc(a, tile_dot<true>(col[I], col[I], i, j), -1.0);
+    ta[i][j] = a;
+    __syncthreads();
+    // Factor and invert A_JJ in one sweep: Hermitian elimination of [A | I]
+    // (left row operations, no pivoting) turns it into [U | L^{-1}] with
+    // U = D L^*, D = diag(u_kk) real; then R = D^{-1/2} U and
+    // X = R^{-1} = L^{-*} D^{-1/2}.  Column k below the pivot is left
+    // untouched at step k (it holds the multipliers being read).
+    xjj[i][j] = Q4{i == j ? 1.0 : 0.0, 0.0, 0.0, 0.0};
+    __syncthreads();
+    int bad = 0;
+    for (int k = 0; k < CTB; ++k) {
+      const double akk = ta[k][k].w;
+      if (!(akk > 0.0)) { bad = J * CTB + k + 1; break; }
+      if (i > k) {
+        const double inv = 1.0 / akk;
+        const Q4 l0 = ta[i][k];
+        const Q4 l{l0.w * inv, l0.x * inv, l0.y * inv, l0.z * inv};
+        if (j > k) qacc(ta[i][j], qmul(l, ta[k][j]), -1.0);
+        if (j <= k) qacc(xjj[i][j], qmul(l, xjj[k][j]), -1.0);
+      }
+      __syncthreads();
+    }
+    if (bad) {  // uniform: every CTA saw the same pivots
+      if (me == 0 && t == 0) *A.info = bad;
+      return;
+    }
+    if (t < CTB) dg[t] = sqrt(ta[t][t].w);
+    __syncthreads();
+    {
+      Q4 q = zero;
+      if (j > i) {
+        const double sc = 1.0 / dg[i];
+        q = Q4{ta[i][j].w * sc, ta[i][j].x * sc, ta[i][j].y * sc, ta[i][j].z * sc};
+      } else if (j == i) {
+        q = Q4{dg[i], 0.0, 0.0, 0.0};
+      }
+      rjj[i][j] = q;
+      // X[i][j] = conj(Linv[j][i]) / d_j  (upper)
+      Q4 xq = zero;
+      if (j >= i) {
+        const Q4 li = xjj[j][i];
+        const double sc = 1.0 / dg[j];
+        xq = Q4{li.w * sc, -li.x * sc, -li.y * sc, -li.z * sc};
+      }
+      __syncthreads();
+      xjj[i][j] = xq;
+    }
+    __syncthreads();
+    if (chc_owner(J, J, nb) == me) {
+      tile_put(A.r, J, J, s, i, j, rjj[i][j]);
+      tile_put(A.x, J, J, s, i, j, j >= i ? xjj[i][j] : zero);
+      if (j == 0 && J * CTB + i < s && A.rdiag) A.rdiag[J * CTB + i] = dg[i];
+    }
+    // row tiles R_JK = X_JJ^* (G_JK - sum_{I<J} R_IJ^* R_IK)
+    for (int K = J + 1; K < nb; ++K) {
+      if (chc_owner(J, K, nb) != me) continue;
+      Q4 acc = tile_get(A.g, J, K, s, i, j);
+      for (int I0 = 0; I0 < J; I0 += CHB) {
+        const int nbat = min(CHB, J - I0);
+        for (int c = 0; c < nbat; ++c) buf[c][i][j] = tile_get(A.r, I0 + c, K, s, i, j);
+        __syncthreads();
+        for (int c = 0; c < nbat; ++c) qacc(acc, tile_dot<true>(col[I0 + c], buf[c], i, j), -1.0);
+        __syncthreads();
+      }
+      ta[i][j] = acc;
+      __syncthreads();
+      const Q4 q = tile_dot<true>(xjj, ta, i, j);
+      __syncthreads();
+      tile_put(A.r, J, K, s, i, j, q);
+    }
+    // X tiles X_IJ = -(sum_{K=I}^{J-1} X_IK R_KJ) X_JJ
+    for (int I = 0; I < J; ++I) {
+      if (chc_owner(I, J, nb) != me) continue;
+      Q4 acc = zero;
+      for (int K0 = I; K0 < J; K0 += CHB) {
+        const int nbat = min(CHB, J - K0);
+        for (int c = 0; c < nbat; ++c) buf[c][i][j] = tile_get(A.x, I, K0 + c, s, i, j);
+        __syncthreads();
+        for (int c = 0; c < nbat; ++c) qacc(acc, tile_dot<false>(buf[c], col[K0 + c], i, j), 1.0);
+        __syncthreads();
+      }
+      ta[i][j] = acc;
+      __syncthreads();
+      const Q4 q = tile_dot<false>(ta, xjj, i, j);
+      __syncthreads();
+      tile_put(A.x, I, J, s, i, j, Q4{-q.w, -q.x, -q.y, -q.z});
+    }
+    cl.sync();
+  }
+  if (me == 0 && t == 0) *A.info = 0;
+}
+
 }  // namespace
 
 void small_chi_from_quat(Ctx& ctx, const QView& g, double2* chi, int64_t ldc) {
@@ -1477,6 +1706,38 @@ bool blocked_chol_inv(Ctx& ctx, const QView& g, const QView& rinv, std::vector<d
                       const QView* r_out) {
   const int64_t s = g.rows;
   if (s == 0) return true;
+  if (s <= CHC_MAX) {
+    DevQMat rw;
+    QView rv;
+    if (r_out) {
+      rv = *r_out;
+    } else {
+      rw = DevQMat(ctx, s, s);
+      rv = rw.v;
+    }
+    DeviceBuffer info(ctx, sizeof(int));
+    DeviceBuffer dg(ctx, sizeof(double) * (size_t)s);
+    CholArgs a{g, rv, rinv, dg.as<double>(), info.as<int>()};
+    const int64_t nbt = (s + CTB - 1) / CTB;
+    const size_t csm = sizeof(Tile) * (size_t)(nbt + CHB + 3);
+    static size_t cattr = 0;
+    if (csm > 48 * 1024 && csm > cattr) {
+      QLRA_CUDA(cudaFuncSetAttribute(k_chol_inv_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm));
+      cattr = csm;
+    }
+    k_chol_inv_cluster<<<CHC, 256, csm, ctx.stream>>>(a);
+    QLRA_LAUNCH_CHECK();
+    count_launch();
+    int inf = 0;
+    QLRA_CUDA(cudaMemcpyAsync(&inf, info.ptr, sizeof(int), cudaMemcpyDeviceToHost, ctx.stream));
+    QLRA_CUDA(cudaStreamSynchronize(ctx.stream));
+    if (inf != 0) return false;
+    if (rdiag) {
+      rdiag->resize(s);
+      QLRA_CUDA(cudaMemcpy(rdiag->data(), dg.ptr, sizeof(double) * s, cudaMemcpyDeviceToHost));
+    }
+    return true;
+  }
   static bool attr = false;
   const size_t smem = sizeof(Q4) * CB * CB;
   if (!attr) {

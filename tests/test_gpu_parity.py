@@ -212,6 +212,16 @@ def test_pseudo_svd_orthonormal_range(ctx):  # test_rangefinders.cpp:105-117, 19
 
 
 # ----------------------------------------------------------- core solve ---
+@pytest.mark.parametrize("n", [17, 100, 256, 300])
+def test_solve_paths_vs_oracle(ctx, n):
+    """solve_quaternion_linear through the one-launch cluster Cholesky (n <=
+    256, tile edges 16) and the blocked multi-launch path (n > 256)."""
+    from paper_2404_14783_b200 import qlra as Q
+    a, b = random_gaussian(n + 40, n, 50 + n), random_gaussian(n + 40, 3, 51 + n)
+    x = host(Q.solve_quaternion_linear(dev(a), dev(b)))
+    assert rel_diff(x, O.solve_quaternion_linear(a, b)) < 1e-11
+
+
 def test_solve_quaternion_linear_on_device(ctx):  # test_complex_bridge.cpp:90-127
     from paper_2404_14783_b200 import qlra as Q
     assert rel_diff(host(Q.solve_quaternion_linear(dev(scalar(0, 0, 1)), dev(scalar(0, 0, 0, 1)))),
