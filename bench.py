@@ -276,13 +276,13 @@ def main():
         h_host = torch.empty((4, r1 - r0, cfg.s), dtype=torch.float64, pin_memory=True)
         x_host = torch.empty((4, cfg.s, cfg.n), dtype=torch.float64, pin_memory=True)
 
+        e2e_opts = Q.OnePassOptions(r=cfg.s - 5, s=cfg.s, l=cfg.l, rangefinder=method, embedding=cfg.kind)
+
         def e2e_step():
-            # public streaming API: A from pinned host memory, H2D overlapped
-            st = Q.make_sketch_host(a_host, opts.r, opts.s, opts.l, opts.omega_seed, opts.psi_seed,
-                                    cfg.kind, ctx=ctx, row0=r0, m_global=cfg.m)
-            q = Q.qb_stage(st, method, ctx=ctx)
-            h_host.copy_(q.h, non_blocking=True)
-            x_host.copy_(q.x, non_blocking=True)
+            # public host-in/host-out API (one C-ABI call): A streams from
+            # pinned host memory with the H2D overlapped by the sketch, H is
+            # copied back while the core solve runs, then X
+            Q.one_pass_qb_host(a_host, e2e_opts, ctx=ctx, row0=r0, m_global=cfg.m, h_out=h_host, x_out=x_host)
 
         for _ in range(max(1, args.warmup // 2)):
             e2e_step()

@@ -187,6 +187,22 @@ int qlra_pseudo_svd(qlra_ctx_t* ctx, const qlra_qmat_t* y, uint64_t seed, qlra_q
 int qlra_qb_solve(qlra_ctx_t* ctx, const qlra_spec_t* psi, int64_t row0, const qlra_qmat_t* h,
                   const qlra_qmat_t* w, qlra_qmat_t* x);
 
+/* ------------------------------------------------ host-side one-pass --- */
+/* one_pass_approx through the QB stage (sketching.cpp:250-263) for a host
+ * resident row shard of A (pinned memory overlaps best): the sketch streams A
+ * through the overlapped H2D + fused-sketch pipeline (block_rows as in
+ * sketch_from_source, 0 = automatic), W is all-reduced, the rangefinder
+ * (`method` = QLRA_PSEUDO_QR / QLRA_PSEUDO_SVD, `rangefinder_seed` for the
+ * latter, `cfg` may be NULL) forms H, and H is copied back on a side stream
+ * while the core solve computes X.  h_host (rows x s) and x_host (s x n) are
+ * host views.  Replaces the QB half of one_pass_approx
+ * (proj/include/qlra/sketching.hpp:143, sketching.cpp:250-263).  syncs. */
+int qlra_one_pass_qb_host(qlra_ctx_t* ctx, const qlra_qmat_t* a_host, int64_t row0,
+                          const qlra_spec_t* omega, const qlra_spec_t* psi, int method,
+                          uint64_t rangefinder_seed, const qlra_pseudo_qr_config_t* cfg,
+                          int64_t block_rows, qlra_qmat_t* h_host, qlra_qmat_t* x_host,
+                          qlra_rangefinder_report_t* report);
+
 /* ------------------------------------------------ truncation (next) --- */
 /* qsvd (factorizations.hpp:44, factorizations.cpp:166-295) of a replicated
  * A (m x n): u m x k, v n x k, k = min(m, n); sigma (host, k) nonincreasing;

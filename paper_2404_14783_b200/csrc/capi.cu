@@ -83,6 +83,21 @@ int64_t global_rows(Ctx& ctx, int64_t local) {
   return (int64_t)llround(to_host(ctx, b.as<double>(), 1)[0]);
 }
 
+// First global row of this rank's contiguous row shard (exclusive prefix sum
+// of the shard heights in rank order).
+int64_t global_row0(Ctx& ctx, int64_t local) {
+  if (ctx.nranks <= 1) return 0;
+  DeviceBuffer b(ctx, sizeof(double) * (size_t)ctx.nranks);
+  std::vector<double> v((size_t)ctx.nranks, 0.0);
+  v[(size_t)ctx.rank] = (double)local;
+  QLRA_CUDA(cudaMemcpyAsync(b.ptr, v.data(), sizeof(double) * v.size(), cudaMemcpyHostToDevice, ctx.stream));
+  allreduce_sum(ctx, b.as<double>(), v.size());
+  const std::vector<double> all = to_host(ctx, b.as<double>(), v.size());
+  int64_t r0 = 0;
+  for (int i = 0; i < ctx.rank; ++i) r0 += (int64_t)llround(all[(size_t)i]);
+  return r0;
+}
+
 // G = op(A)^* op(A) reduced over (row-sharded) rows: s x s.
 void gram(Ctx& ctx, const QView& h, const QView& g) {
   qgemm(ctx, QLRA_OP_C, QLRA_OP_N, 1.0, h, h, 0.0, g);
@@ -382,6 +397,94 @@ void lstsq(Ctx& ctx, const QView& p, const QView& b, const QView& x) {
   DevQMat t(ctx, l, s);
   qgemm(ctx, QLRA_OP_N, QLRA_OP_C, 1.0, q.v, rinv.v, 0.0, t.v);
   qgemm(ctx, QLRA_OP_C, QLRA_OP_N, 1.0, t.v, b, 0.0, x);
+}
+
+// ------------------------------------------------- rangefinders, solve ---
+// Device bodies of pseudo_qr / pseudo_svd / qb_solve (Y, H row-sharded over
+// the ranks; shapes validated by the callers).
+void pseudo_qr_dev(Ctx& c, const QView& Y, const QView& H, const qlra_pseudo_qr_config_t& cfg,
+                   qlra_rangefinder_report_t* rep) {
+  const int64_t s = Y.cols;
+  const int64_t m = global_rows(c, Y.rows);
+  if (m <= s) fail(QLRA_ERR_PARAMETER, "pseudo_qr: sketch must be tall (rows > cols)");
+  if (cfg.max_correction_steps < 0) fail(QLRA_ERR_PARAMETER, "pseudo_qr: negative correction step count");
+  if (!(cfg.delta_budget >= 1.0 && cfg.delta_budget <= std::sqrt(7.0) / 2.0 + 1e-12))
+    fail(QLRA_ERR_PARAMETER, "pseudo_qr: delta_budget outside [1, sqrt(7)/2]");
+  // Y = Q0 R_q by quaternion CholeskyQR2 -- the only factorisation of the
+  // tall sketch.  Writing Y = Q0 R_q in compact form, compact(Y) =
+  // U compact(R_q) with U (2m x 2s) the compact image of Q0, orthonormal
+  // columns; so the reference's complex_qr(to_compact(Y))
+  // (rangefinders.cpp:117) has the R factor R_c of compact(R_q), and its
+  // basis is H0 = Q0 C with C = R_q R_c^{-1}: a complex-mode CholeskyQR2 of
+  // the small s x s R_q.  Every correction step then acts on the s x s
+  // coefficient matrix (H_k = Q0 C_k, kappa(H_k) = kappa(C_k) because Q0 is
+  // orthonormal), and one tall product H = Q0 C_k closes the pass.  H lies in
+  // range(Q0) = range(H0) to rounding, which is what the reference's
+  // re-projection (rangefinders.cpp:142-153) restores.
+  DevQMat q0(c, Y.rows, s), rq;
+  if (!cholesky_qr(c, Y, q0.v, /*complex_mode=*/false, m, nullptr, /*distributed=*/true, nullptr, &rq))
+    fail(QLRA_ERR_RANK, "pseudo_qr: sketch numerically rank-deficient; use pseudo_svd");
+  DevQMat cm(c, s, s);
+  std::vector<double> rd;
+  if (!cholesky_qr(c, rq.v, cm.v, /*complex_mode=*/true, s, &rd, /*distributed=*/false))
+    fail(QLRA_ERR_RANK, "pseudo_qr: sketch numerically rank-deficient; use pseudo_svd");
+  rank_check(rd);  // |diag R_c|, rangefinders.cpp:118-126
+  qlra_rangefinder_report_t r{};
+  r.method = QLRA_PSEUDO_QR;
+  DevQMat g(c, s, s), mk(c, s, s);
+  qgemm(c, QLRA_OP_C, QLRA_OP_N, 1.0, cm.v, cm.v, 0.0, g.v);  // H0^* H0 = C^* C
+  r.kappa_before = kappa_from_eigs(quat_eigs(c, g.v));
+  double kappa = r.kappa_before;
+  try {
+    while (r.correction_steps_used < cfg.max_correction_steps && kappa > kKappaTarget) {
+      // one inverse serves estimate_epsilon and correction_step (both
+      // factor the same H^*H, rangefinders.cpp:68,102)
+      check_gram_rcond(kappa, 1e-15, "estimate_epsilon: H*H numerically singular");
+      DevQMat ginv = gram_inverse(c, g.v, kappa, 1e-14, "solve_quaternion_linear: singular system");
+      const double eps = estimate_epsilon_from_inverse(c, ginv.v, cfg.power_iters_for_epsilon);
+      if (!(eps > 0.0 && eps < 1.0))
+        fail(QLRA_ERR_PARAMETER, "correction_step: epsilon must lie in (0,1)");
+      // H_{k+1} = H_k ((1-eps) I + eps G_k^{-1})  (rangefinders.cpp:99-105)
+      small_axpby_identity(c, 1.0 - eps, eps, ginv.v, mk.v);
+      DevQMat cn(c, s, s);
+      qgemm(c, QLRA_OP_N, QLRA_OP_N, 1.0, cm.v, mk.v, 0.0, cn.v);
+      cm = std::move(cn);
+      qgemm(c, QLRA_OP_C, QLRA_OP_N, 1.0, cm.v, cm.v, 0.0, g.v);
+      kappa = kappa_from_eigs(quat_eigs(c, g.v));
+      ++r.correction_steps_used;
+    }
+  } catch (const Status& e) {
+    if (e.code != QLRA_ERR_SINGULAR) throw;
+    fail(QLRA_ERR_RANK, "pseudo_qr: sketch numerically rank-deficient; use pseudo_svd");
+  }
+  qgemm(c, QLRA_OP_N, QLRA_OP_N, 1.0, q0.v, cm.v, 0.0, H);
+  r.kappa_after = kappa;
+  if (rep) *rep = r;
+}
+
+void pseudo_svd_dev(Ctx& c, const QView& Y, const QView& H, uint64_t seed, qlra_rangefinder_report_t* rep) {
+  const int64_t s = Y.cols;
+  const int64_t m = global_rows(c, Y.rows);
+  if (m <= s) fail(QLRA_ERR_PARAMETER, "pseudo_svd: sketch must be tall (rows > cols)");
+  qlra_rangefinder_report_t r{};
+  r.method = QLRA_PSEUDO_SVD;
+  r.kappa_before = condition_number_dev(c, Y);
+  // Full-rank sketches: quaternion CholeskyQR2 (shifted CholeskyQR3 when
+  // needed).  Rank-deficient ones: eigen route + orthonormal completion.
+  if (!std::isfinite(r.kappa_before) || !cholesky_qr(c, Y, H, /*complex_mode=*/false, m, nullptr))
+    pseudo_svd_rank_deficient(c, Y, H, m, global_row0(c, Y.rows), seed);
+  r.kappa_after = condition_number_dev(c, H);
+  if (rep) *rep = r;
+}
+
+void qb_solve_dev(Ctx& c, const qlra_spec_t& psi, int64_t row0, const QView& H, const QView& W, const QView& X) {
+  const int64_t s = H.cols, l = psi.rows;
+  DevQMat ps(c, l, H.rows);
+  launch_gen(c.stream, psi, 0, row0, l, H.rows, ps.v, false);
+  DevQMat p(c, l, s);
+  qgemm(c, QLRA_OP_N, QLRA_OP_N, 1.0, ps.v, H, 0.0, p.v);
+  allreduce_qmat(c, p.v);
+  lstsq(c, p.v, W, X);
 }
 
 void check_view(const qlra_qmat_t* m, const char* who) {
@@ -710,64 +813,8 @@ int qlra_pseudo_qr(qlra_ctx_t* ctx, const qlra_qmat_t* y, const qlra_pseudo_qr_c
     check_view(h, "pseudo_qr");
     qlra_pseudo_qr_config_t cfg{3, 3, 1.2};
     if (cfg_in) cfg = *cfg_in;
-    const int64_t s = y->cols;
-    const int64_t m = global_rows(c, y->rows);
-    if (m <= s) fail(QLRA_ERR_PARAMETER, "pseudo_qr: sketch must be tall (rows > cols)");
-    if (cfg.max_correction_steps < 0) fail(QLRA_ERR_PARAMETER, "pseudo_qr: negative correction step count");
-    if (!(cfg.delta_budget >= 1.0 && cfg.delta_budget <= std::sqrt(7.0) / 2.0 + 1e-12))
-      fail(QLRA_ERR_PARAMETER, "pseudo_qr: delta_budget outside [1, sqrt(7)/2]");
-    if (h->rows != y->rows || h->cols != s) fail(QLRA_ERR_SHAPE, "pseudo_qr: output shape mismatch");
-    const QView Y = view_of(y), H = view_of(h);
-    // Y = Q0 R_q by quaternion CholeskyQR2 -- the only factorisation of the
-    // tall sketch.  Writing Y = Q0 R_q in compact form, compact(Y) =
-    // U compact(R_q) with U (2m x 2s) the compact image of Q0, orthonormal
-    // columns; so the reference's complex_qr(to_compact(Y))
-    // (rangefinders.cpp:117) has the R factor R_c of compact(R_q), and its
-    // basis is H0 = Q0 C with C = R_q R_c^{-1}: a complex-mode CholeskyQR2 of
-    // the small s x s R_q.  Every correction step then acts on the s x s
-    // coefficient matrix (H_k = Q0 C_k, kappa(H_k) = kappa(C_k) because Q0 is
-    // orthonormal), and one tall product H = Q0 C_k closes the pass.  H lies in
-    // range(Q0) = range(H0) to rounding, which is what the reference's
-    // re-projection (rangefinders.cpp:142-153) restores.
-    DevQMat q0(c, Y.rows, s), rq;
-    if (!cholesky_qr(c, Y, q0.v, /*complex_mode=*/false, m, nullptr, /*distributed=*/true, nullptr, &rq))
-      fail(QLRA_ERR_RANK, "pseudo_qr: sketch numerically rank-deficient; use pseudo_svd");
-    DevQMat cm(c, s, s);
-    std::vector<double> rd;
-    if (!cholesky_qr(c, rq.v, cm.v, /*complex_mode=*/true, s, &rd, /*distributed=*/false))
-      fail(QLRA_ERR_RANK, "pseudo_qr: sketch numerically rank-deficient; use pseudo_svd");
-    rank_check(rd);  // |diag R_c|, rangefinders.cpp:118-126
-    qlra_rangefinder_report_t r{};
-    r.method = QLRA_PSEUDO_QR;
-    DevQMat g(c, s, s), mk(c, s, s);
-    qgemm(c, QLRA_OP_C, QLRA_OP_N, 1.0, cm.v, cm.v, 0.0, g.v);  // H0^* H0 = C^* C
-    r.kappa_before = kappa_from_eigs(quat_eigs(c, g.v));
-    double kappa = r.kappa_before;
-    try {
-      while (r.correction_steps_used < cfg.max_correction_steps && kappa > kKappaTarget) {
-        // one inverse serves estimate_epsilon and correction_step (both
-        // factor the same H^*H, rangefinders.cpp:68,102)
-        check_gram_rcond(kappa, 1e-15, "estimate_epsilon: H*H numerically singular");
-        DevQMat ginv = gram_inverse(c, g.v, kappa, 1e-14, "solve_quaternion_linear: singular system");
-        const double eps = estimate_epsilon_from_inverse(c, ginv.v, cfg.power_iters_for_epsilon);
-        if (!(eps > 0.0 && eps < 1.0))
-          fail(QLRA_ERR_PARAMETER, "correction_step: epsilon must lie in (0,1)");
-        // H_{k+1} = H_k ((1-eps) I + eps G_k^{-1})  (rangefinders.cpp:99-105)
-        small_axpby_identity(c, 1.0 - eps, eps, ginv.v, mk.v);
-        DevQMat cn(c, s, s);
-        qgemm(c, QLRA_OP_N, QLRA_OP_N, 1.0, cm.v, mk.v, 0.0, cn.v);
-        cm = std::move(cn);
-        qgemm(c, QLRA_OP_C, QLRA_OP_N, 1.0, cm.v, cm.v, 0.0, g.v);
-        kappa = kappa_from_eigs(quat_eigs(c, g.v));
-        ++r.correction_steps_used;
-      }
-    } catch (const Status& e) {
-      if (e.code != QLRA_ERR_SINGULAR) throw;
-      fail(QLRA_ERR_RANK, "pseudo_qr: sketch numerically rank-deficient; use pseudo_svd");
-    }
-    qgemm(c, QLRA_OP_N, QLRA_OP_N, 1.0, q0.v, cm.v, 0.0, H);
-    r.kappa_after = kappa;
-    if (rep) *rep = r;
+    if (h->rows != y->rows || h->cols != y->cols) fail(QLRA_ERR_SHAPE, "pseudo_qr: output shape mismatch");
+    pseudo_qr_dev(c, view_of(y), view_of(h), cfg, rep);
   });
 }
 
@@ -776,21 +823,16 @@ int qlra_pseudo_svd(qlra_ctx_t* ctx, const qlra_qmat_t* y, uint64_t seed, qlra_q
   return guarded(ctx, [&](Ctx& c) {
     check_view(y, "pseudo_svd");
     check_view(h, "pseudo_svd");
-    const int64_t s = y->cols;
-    const int64_t m = global_rows(c, y->rows);
-    if (m <= s) fail(QLRA_ERR_PARAMETER, "pseudo_svd: sketch must be tall (rows > cols)");
-    if (h->rows != y->rows || h->cols != s) fail(QLRA_ERR_SHAPE, "pseudo_svd: output shape mismatch");
-    const QView Y = view_of(y), H = view_of(h);
-    qlra_rangefinder_report_t r{};
-    r.method = QLRA_PSEUDO_SVD;
-    r.kappa_before = condition_number_dev(c, Y);
-    // Full-rank sketches: quaternion CholeskyQR2 (shifted CholeskyQR3 when
-    // needed).  Rank-deficient ones: eigen route + orthonormal completion.
-    if (!std::isfinite(r.kappa_before) || !cholesky_qr(c, Y, H, /*complex_mode=*/false, m, nullptr))
-      pseudo_svd_rank_deficient(c, Y, H, m, /*row0=*/0, seed);
-    r.kappa_after = condition_number_dev(c, H);
-    if (rep) *rep = r;
+    if (h->rows != y->rows || h->cols != y->cols) fail(QLRA_ERR_SHAPE, "pseudo_svd: output shape mismatch");
+    pseudo_svd_dev(c, view_of(y), view_of(h), seed, rep);
   });
+}
+
+void check_solve_shapes(const qlra_spec_t* psi, int64_t row0, const qlra_qmat_t* h, const qlra_qmat_t* w,
+                        const qlra_qmat_t* x) {
+  const int64_t s = h->cols, l = psi->rows, n = w->cols;
+  if (w->rows != l || x->rows != s || x->cols != n) fail(QLRA_ERR_SHAPE, "qb_stage: shape mismatch");
+  if (row0 < 0 || row0 + h->rows > psi->cols) fail(QLRA_ERR_SHAPE, "qb_stage: Psi shape mismatch");
 }
 
 int qlra_qb_solve(qlra_ctx_t* ctx, const qlra_spec_t* psi, int64_t row0, const qlra_qmat_t* h,
@@ -800,15 +842,65 @@ int qlra_qb_solve(qlra_ctx_t* ctx, const qlra_spec_t* psi, int64_t row0, const q
     check_view(h, "qb_solve");
     check_view(w, "qb_solve");
     check_view(x, "qb_solve");
-    const int64_t s = h->cols, l = psi->rows, n = w->cols;
-    if (w->rows != l || x->rows != s || x->cols != n) fail(QLRA_ERR_SHAPE, "qb_stage: shape mismatch");
-    if (row0 < 0 || row0 + h->rows > psi->cols) fail(QLRA_ERR_SHAPE, "qb_stage: Psi shape mismatch");
-    DevQMat ps(c, l, h->rows);
-    launch_gen(c.stream, *psi, 0, row0, l, h->rows, ps.v, false);
-    DevQMat p(c, l, s);
-    qgemm(c, QLRA_OP_N, QLRA_OP_N, 1.0, ps.v, view_of(h), 0.0, p.v);
-    allreduce_qmat(c, p.v);
-    lstsq(c, p.v, view_of(w), view_of(x));
+    check_solve_shapes(psi, row0, h, w, x);
+    qb_solve_dev(c, *psi, row0, view_of(h), view_of(w), view_of(x));
+  });
+}
+
+// Host in, host out: one_pass_approx through the QB stage
+// (sketching.cpp:250-263) on a host row shard.  A streams through the
+// overlapped H2D + fused-sketch pipeline; H is copied back on a side stream
+// while the core solve runs; X follows.
+int qlra_one_pass_qb_host(qlra_ctx_t* ctx, const qlra_qmat_t* a_host, int64_t row0, const qlra_spec_t* omega,
+                          const qlra_spec_t* psi, int method, uint64_t rangefinder_seed,
+                          const qlra_pseudo_qr_config_t* cfg_in, int64_t block_rows, qlra_qmat_t* h_host,
+                          qlra_qmat_t* x_host, qlra_rangefinder_report_t* rep) {
+  return guarded(ctx, [&](Ctx& c) {
+    validate_spec(omega);
+    validate_spec(psi);
+    check_view(a_host, "one_pass_qb");
+    check_view(h_host, "one_pass_qb");
+    check_view(x_host, "one_pass_qb");
+    const int64_t rows = a_host->rows, n = a_host->cols, s = omega->cols, l = psi->rows;
+    if (omega->rows != n || psi->cols < row0 + rows || row0 < 0)
+      fail(QLRA_ERR_SHAPE, "one_pass_qb: test matrix shape mismatch");
+    if (h_host->rows != rows || h_host->cols != s || x_host->rows != s || x_host->cols != n)
+      fail(QLRA_ERR_SHAPE, "one_pass_qb: output shape mismatch");
+    if (block_rows < 0) fail(QLRA_ERR_PARAMETER, "sketch_from_source: block_rows must be >= 1");
+    if (method != QLRA_PSEUDO_QR && method != QLRA_PSEUDO_SVD)
+      fail(QLRA_ERR_PARAMETER, "one_pass_qb: unknown rangefinder");
+    qlra_pseudo_qr_config_t cfg{3, 3, 1.2};
+    if (cfg_in) cfg = *cfg_in;
+    DevQMat y(c, rows, s), w(c, l, n), h(c, rows, s), x(c, s, n);
+    y.zero(c);
+    w.zero(c);
+    sketch_update_rows_host(c, *omega, *psi, row0, view_of(a_host), y.v, w.v, block_rows);
+    allreduce_qmat(c, w.v);
+    if (method == QLRA_PSEUDO_QR) pseudo_qr_dev(c, y.v, h.v, cfg, rep);
+    else pseudo_svd_dev(c, y.v, h.v, rangefinder_seed, rep);
+    // H is final: copy it back on a side stream while the solve runs
+    cudaStream_t side = nullptr;
+    cudaEvent_t ready = nullptr, copied = nullptr;
+    QLRA_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+    QLRA_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+    QLRA_CUDA(cudaEventCreateWithFlags(&copied, cudaEventDisableTiming));
+    QLRA_CUDA(cudaEventRecord(ready, c.stream));
+    QLRA_CUDA(cudaStreamWaitEvent(side, ready, 0));
+    const QView hv = view_of(h_host), xv = view_of(x_host);
+    for (int p = 0; p < 4; ++p)
+      QLRA_CUDA(cudaMemcpy2DAsync(hv.p[p], sizeof(double) * hv.ld, h.v.p[p], sizeof(double) * h.v.ld,
+                                  sizeof(double) * s, (size_t)rows, cudaMemcpyDeviceToHost, side));
+    QLRA_CUDA(cudaEventRecord(copied, side));
+    qb_solve_dev(c, *psi, row0, h.v, w.v, x.v);
+    for (int p = 0; p < 4; ++p)
+      QLRA_CUDA(cudaMemcpy2DAsync(xv.p[p], sizeof(double) * xv.ld, x.v.p[p], sizeof(double) * x.v.ld,
+                                  sizeof(double) * n, (size_t)s, cudaMemcpyDeviceToHost, c.stream));
+    // h's device buffer is released on c.stream: order it after the copy
+    QLRA_CUDA(cudaStreamWaitEvent(c.stream, copied, 0));
+    QLRA_CUDA(cudaStreamSynchronize(c.stream));
+    cudaEventDestroy(ready);
+    cudaEventDestroy(copied);
+    cudaStreamDestroy(side);
   });
 }
 

@@ -273,47 +273,113 @@ __global__ void k_bisect(const double* d, const double* e, int64_t n, double* w,
 // Extreme eigenvalues of the symmetric tridiagonal (d, e) by parallel
 // multisection: half the CTA brackets the largest, half the smallest; each
 // round evaluates 511 Sturm counts and shrinks the bracket 512-fold.
-__global__ void __launch_bounds__(1024) k_multisect_extremes(const double* d, const double* e,
-                                                             int64_t n, double* w) {
-  __shared__ double s_lo[2], s_hi[2];
-  __shared__ int s_first[2];
-  const int t = threadIdx.x, half = t >> 9, j = t & 511;
-  if (t == 0) {
-    double lo = d[0], hi = d[0];
-    for (int64_t i = 0; i < n; ++i) {
-      const double r = (i > 0 ? fabs(e[i - 1]) : 0.0) + (i + 1 < n ? fabs(e[i]) : 0.0);
-      lo = fmin(lo, d[i] - r);
-      hi = fmax(hi, d[i] + r);
+// Sturm count by the three-term recurrence of the leading principal minors,
+// p_i = (d_i - x) p_{i-1} - e_{i-1}^2 p_{i-2} (eigenvalues < x = sign changes
+// in p_0 = 1, p_1, ..., p_n): two dependent FMAs per step instead of a
+// division.  Exact power-of-two rescaling keeps p in range; a zero minor
+// takes the sign of its predecessor (as the quotient form's 1e-300 does).
+// d, e2 in shared memory, already divided by a power of two.
+__device__ __forceinline__ int sturm_count_poly(const double* d, const double* e2, int n, double x) {
+  double pm = 1.0, p = d[0] - x;
+  if (p == 0.0) p = 0x1p-200;
+  int cnt = p < 0.0;
+  for (int i = 1; i < n; ++i) {
+    double pn = fma(d[i] - x, p, -e2[i - 1] * pm);
+    if (pn == 0.0) pn = p * 0x1p-200;  // same sign, negligible
+    cnt += (pn < 0.0) != (p < 0.0);
+    pm = p;
+    p = pn;
+    const double ap = fabs(p);
+    if (ap > 0x1p+400 || ap < 0x1p-400) {
+      const double sc = ap > 0x1p+400 ? 0x1p-400 : 0x1p+400;
+      p *= sc;
+      pm *= sc;
     }
-    const double pad = 2.2e-16 * fmax(fabs(lo), fabs(hi)) * (double)n + 1e-300;
+  }
+  return cnt;
+}
+
+// Extreme eigenvalues of the symmetric tridiagonal (d, e) by multisection:
+// two groups of 4 warps narrow [lo, hi] around the largest (w[0]) and the
+// smallest (w[n-1]) eigenvalue, 127 probes (7 bits) per round.  The counts
+// are latency-bound chains, so few warps per SM cost nothing and avoid the
+// issue contention of a full 1024-thread CTA.
+constexpr int MS_PROBES = 128;
+__global__ void __launch_bounds__(2 * MS_PROBES) k_multisect_extremes(const double* d, const double* e,
+                                                                      int64_t n, double* w) {
+  extern __shared__ double ts[];  // d (n), e^2 (n), scaled
+  double* sd = ts;
+  double* se2 = ts + n;
+  __shared__ double s_lo[2], s_hi[2], s_scale;
+  __shared__ int s_first[2];
+  const int t = threadIdx.x, half = t / MS_PROBES, j = t % MS_PROBES;
+  if (t < 32) {
+    double mx = 0.0;
+    for (int64_t i = t; i < n; i += 32) {
+      mx = fmax(mx, fabs(d[i]));
+      if (i + 1 < n) mx = fmax(mx, fabs(e[i]));
+    }
+    for (int off = 16; off > 0; off >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+    if (t == 0) {
+      int ex = 0;
+      frexp(mx > 0.0 ? mx : 1.0, &ex);
+      s_scale = mx > 0.0 ? ldexp(1.0, -ex) : 0.0;  // exact power of two; |entries| < 1 after scaling
+    }
+  }
+  __syncthreads();
+  const double sc = s_scale;
+  if (sc == 0.0) {  // zero matrix: every eigenvalue is exactly 0
+    if (t == 0) {
+      w[0] = 0.0;
+      w[n - 1] = 0.0;
+    }
+    return;
+  }
+  for (int64_t i = t; i < n; i += blockDim.x) {
+    sd[i] = d[i] * sc;
+    const double ei = i + 1 < n ? e[i] * sc : 0.0;
+    se2[i] = ei * ei;
+  }
+  __syncthreads();
+  if (t == 0) {
+    double lo = sd[0], hi = sd[0];
+    for (int64_t i = 0; i < n; ++i) {
+      const double r = (i > 0 ? sqrt(se2[i - 1]) : 0.0) + (i + 1 < n ? sqrt(se2[i]) : 0.0);
+      lo = fmin(lo, sd[i] - r);
+      hi = fmax(hi, sd[i] + r);
+    }
+    const double pad = 2.2e-16 * fmax(fabs(lo), fabs(hi)) * (double)n + 0x1p-300;
     s_lo[0] = s_lo[1] = lo - pad;
     s_hi[0] = s_hi[1] = hi + pad;
   }
   __syncthreads();
   // half 0: k = n-1 (largest), half 1: k = 0 (smallest); want smallest x with count(x) > k
-  const int64_t k = half == 0 ? n - 1 : 0;
-  for (int round = 0; round < 9; ++round) {
+  const int k = half == 0 ? (int)n - 1 : 0;
+  for (int round = 0; round < 24; ++round) {
     const double lo = s_lo[half], hi = s_hi[half];
     const bool done = !(hi - lo > 4.4e-16 * fmax(fabs(lo), fabs(hi)));
-    if (j == 0) s_first[half] = 512;
+    const bool done0 = !(s_hi[0] - s_lo[0] > 4.4e-16 * fmax(fabs(s_lo[0]), fabs(s_hi[0])));
+    const bool done1 = !(s_hi[1] - s_lo[1] > 4.4e-16 * fmax(fabs(s_lo[1]), fabs(s_hi[1])));
+    if (done0 && done1) break;  // both converged (same decision in every thread)
+    if (j == 0) s_first[half] = MS_PROBES;
     __syncthreads();
-    if (!done && j < 511) {
-      const double x = lo + (hi - lo) * (double)(j + 1) / 512.0;
-      if (x > lo && x < hi && sturm_count(d, e, n, x) > k) atomicMin(&s_first[half], j);
+    if (!done && j < MS_PROBES - 1) {
+      const double x = lo + (hi - lo) * (double)(j + 1) / (double)MS_PROBES;
+      if (x > lo && x < hi && sturm_count_poly(sd, se2, (int)n, x) > k) atomicMin(&s_first[half], j);
     }
     __syncthreads();
     if (!done && j == 0) {
-      const int f = s_first[half];  // first point with count > k (512: none)
-      const double nlo = f == 0 ? lo : lo + (hi - lo) * (double)f / 512.0;
-      const double nhi = f == 512 ? hi : lo + (hi - lo) * (double)(f + 1) / 512.0;
+      const int f = s_first[half];  // first probe with count > k (MS_PROBES: none)
+      const double nlo = f == 0 ? lo : lo + (hi - lo) * (double)f / (double)MS_PROBES;
+      const double nhi = f == MS_PROBES ? hi : lo + (hi - lo) * (double)(f + 1) / (double)MS_PROBES;
       s_lo[half] = nlo;
       s_hi[half] = nhi;
     }
     __syncthreads();
   }
   if (t == 0) {
-    w[0] = 0.5 * (s_lo[0] + s_hi[0]);
-    w[n - 1] = 0.5 * (s_lo[1] + s_hi[1]);
+    w[0] = 0.5 * (s_lo[0] + s_hi[0]) / sc;
+    w[n - 1] = 0.5 * (s_lo[1] + s_hi[1]) / sc;
   }
 }
 
@@ -480,12 +546,14 @@ __global__ void __launch_bounds__(SNT) k_power_inverse(QView ginv, int iters, do
   __syncthreads();
   double rho = 0.0;
   for (int it = 0; it < iters; ++it) {
-    // w = chi_{M} z, chi_M = [[M0, M1], [-conj M1, conj M0]]
-    for (int64_t r = t; r < n; r += blockDim.x) {
+    // w = chi_{M} z, chi_M = [[M0, M1], [-conj M1, conj M0]]; warp per row,
+    // lanes over columns (coalesced plane loads), fixed-order shuffle sum
+    const int lane = t & 31, wid = t >> 5, nwarp = blockDim.x >> 5;
+    for (int64_t r = wid; r < n; r += nwarp) {
       double2 acc = make_double2(0.0, 0.0);
       const bool top = r < s;
       const int64_t i = top ? r : r - s;
-      for (int64_t c = 0; c < s; ++c) {
+      for (int64_t c = lane; c < s; c += 32) {
         const int64_t o = i * ginv.ld + c;
         const double2 m0 = make_double2(ginv.p[0][o], ginv.p[1][o]);
         const double2 m1 = make_double2(ginv.p[2][o], ginv.p[3][o]);
@@ -495,7 +563,9 @@ __global__ void __launch_bounds__(SNT) k_power_inverse(QView ginv, int iters, do
           acc = cadd(acc, csub(cmul(cconj(m0), z[s + c]), cmul(cconj(m1), z[c])));
         }
       }
-      w[r] = acc;
+      acc.x = warp_sum(acc.x);
+      acc.y = warp_sum(acc.y);
+      if (lane == 0) w[r] = acc;
     }
     __syncthreads();
     double pr = 0.0, nw = 0.0;
@@ -1654,7 +1724,7 @@ void small_quat_herm_eigvals(Ctx& ctx, const QView& a, double* d_w, bool extreme
   }
   if (extremes_only) {
     // w[0] = max, w[n-1] = min; the middle stays untouched
-    k_multisect_extremes<<<1, 1024, 0, ctx.stream>>>(d, e, n, d_w);
+    k_multisect_extremes<<<1, 2 * MS_PROBES, sizeof(double) * 2 * (size_t)n, ctx.stream>>>(d, e, n, d_w);
   } else {
     k_bisect<<<(unsigned)((n + 255) / 256), 256, 0, ctx.stream>>>(d, e, n, d_w, 0);
   }

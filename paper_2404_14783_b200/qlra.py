@@ -569,6 +569,31 @@ def one_pass_qb(a, opts: OnePassOptions, ctx=None, row0=0, m_global=None, residu
                                            solve_s=qb.solve_s))
 
 
+def one_pass_qb_host(a_host, opts: OnePassOptions, ctx=None, row0=0, m_global=None, block_rows=0,
+                     h_out=None, x_out=None) -> QbResult:
+    """one_pass_approx through the QB stage (sketching.cpp:250-263), host in and
+    host out: A (pinned) streams through the overlapped H2D + sketch pipeline,
+    H comes back while the core solve runs, then X.  One C-ABI call."""
+    ctx = _ctx(ctx)
+    o = resolve_defaults(opts)
+    rows, n = a_host.shape[1], a_host.shape[2]
+    m = rows if m_global is None else m_global
+    validate_sketch_sizes(m, n, o.r, o.s, o.l)
+    om = TestMatrixSpec(o.embedding, n, o.s, o.omega_seed, o.density).c()
+    ps = TestMatrixSpec(o.embedding, o.l, m, o.psi_seed, o.density).c()
+    h = h_out if h_out is not None else torch.empty((4, rows, o.s), dtype=torch.float64, pin_memory=True)
+    x = x_out if x_out is not None else torch.empty((4, o.s, n), dtype=torch.float64, pin_memory=True)
+    cfg = L.PseudoQrConfig(o.qr_cfg.max_correction_steps, o.qr_cfg.power_iters_for_epsilon,
+                           o.qr_cfg.delta_budget)
+    rep = L.Report()
+    ctx._check(ctx.lib.qlra_one_pass_qb_host(ctx.h, C.byref(_qm(a_host, True)), row0, C.byref(om),
+                                             C.byref(ps), o.rangefinder, o.rangefinder_seed, C.byref(cfg),
+                                             block_rows, C.byref(_qm(h, True)), C.byref(_qm(x, True)),
+                                             C.byref(rep)))
+    r = RangefinderReport(h, rep.kappa_before, rep.kappa_after, rep.correction_steps_used, rep.method)
+    return QbResult(h, x, r, 0.0, 0.0)
+
+
 # --------------------------------------------------------- truncation ---
 def qsvd(a, ctx=None):
     """qsvd (factorizations.cpp:166-295): (U, sigma, V) with A = U diag(sigma) V^*."""

@@ -293,6 +293,30 @@ def test_host_streaming_sketch_matches_device(ctx):  # sketching.cpp:156-167 str
         assert rel_diff(host(st.w), host(whole.w)) < 1e-13
 
 
+@pytest.mark.parametrize("method", [0, 1])
+def test_one_pass_qb_host_matches_device_path(ctx, method):
+    """qlra_one_pass_qb_host (host A in, host H/X out, H copied back during
+    the solve) equals the device-resident sketch + qb_stage path."""
+    from paper_2404_14783_b200 import configs, qlra as Q
+    cfg = configs.CONFIGS["C1"]
+    a = configs.build_matrix(cfg, ctx=ctx)
+    opts = Q.OnePassOptions(r=cfg.s - 5, s=cfg.s, l=cfg.l, rangefinder=method)
+    ref = Q.one_pass_qb(a, opts, ctx=ctx, residual=False)
+    a_host = a.cpu().pin_memory()
+    for br in (0, 128):
+        got = Q.one_pass_qb_host(a_host, opts, ctx=ctx, block_rows=br)
+        # the host-streamed sketch differs from the device one at ~1e-14 (other
+        # panel split); the basis H carries that times kappa(Y) ~ 2e4, so
+        # compare the basis-independent quantities: range(H) and H X
+        assert got.report.correction_steps_used == ref.qb.report.correction_steps_used
+        assert abs(got.report.kappa_before / ref.qb.report.kappa_before - 1) < 1e-6
+        hg, hr = got.h.numpy(), host(ref.qb.h)
+        assert largest_principal_angle(hg, hr) < 1e-8
+        assert rel_diff(O.qmat_mul(hg, got.x.numpy()), O.qmat_mul(hr, host(ref.qb.x))) < 1e-10
+    with pytest.raises(Q.ShapeError):
+        Q.one_pass_qb_host(a_host, opts, ctx=ctx, h_out=torch.empty((4, 3, cfg.s), dtype=torch.float64))
+
+
 # ------------------------------------------------- pseudo-SVD bad blocks ---
 def test_pseudo_svd_rank_deficient(ctx):  # test_rangefinders.cpp:119-141, test_sketching.cpp:256-277
     from paper_2404_14783_b200 import qlra as Q
