@@ -42,7 +42,7 @@ def lib():
     global _lib
     if _lib is not None:
         return _lib
-    path = _build.LIB
+    path = os.environ.get("QLRA_LIB_PATH") or _build.LIB  # override: A/B builds in tools/
     if not os.path.exists(path):
         _build.build()
     L = C.CDLL(path)

@@ -124,18 +124,61 @@ __device__ __forceinline__ constexpr int hsign(int q, int p) {
                              : (p == 0 || p == 1 ? -1 : 1);
 }
 
-// acc += op(A) op(B) over k in [kbeg, kend).  CA/CB: op = adjoint, which
-// requires the i-fast / k-fast layouts (AK = !CA, BJ = !CB).  The caller must
-// __syncthreads() between successive calls that reuse `smem`.
-template <bool CA, bool CB>
-__device__ __forceinline__ void mma_tile(const Operands& g, double* smem, int64_t i0, int64_t j0,
+// One BK slice of the tile product from shared memory for the first NRB
+// row blocks and NCB column blocks of the warp (the valid ones are always a
+// prefix).  Instantiated per (NRB, NCB) so the DMMA stream carries no
+// predicates -- predicated-off DMMAs still occupy the tensor pipe.
+template <bool CA, bool CB, bool AK, bool BJ, int NRB, int NCB>
+__device__ __forceinline__ void kstep(const double* As, const double* Bs, int wr, int wc, int gid, int tig,
+                                      Acc& acc) {
+#pragma unroll
+  for (int kk = 0; kk < BK / 4; ++kk) {
+    const int k = 4 * kk + tig;
+    double a[NRB][4];  // [rb][q]
+#pragma unroll
+    for (int rb = 0; rb < NRB; ++rb) {
+      const int x = 16 * wr + 8 * rb + gid;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) a[rb][q] = AK ? As[(q * BM + x) * LDK + k] : As[(q * BK + k) * LDX + x];
+    }
+    double bp[NCB][4], bn[NCB][4];  // + and - copies, [cb][plane]
+#pragma unroll
+    for (int cb = 0; cb < NCB; ++cb) {
+      const int x = 16 * wc + 8 * cb + gid;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        bp[cb][q] = BJ ? Bs[(q * BK + k) * LDX + x] : Bs[(q * BN + x) * LDK + k];
+        bn[cb][q] = -bp[cb][q];
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int rb = 0; rb < NRB; ++rb)
+#pragma unroll
+        for (int cb = 0; cb < NCB; ++cb)
+#pragma unroll
+          for (int p = 0; p < 4; ++p) {
+            const int bq = hplane(q, p);
+            // conj(A): a_x,y,z negated -> flip terms q >= 1;
+            // conj(B): b_x,y,z negated -> flip when the B plane is not w.
+            int sg = hsign(q, p);
+            if (CA && q > 0) sg = -sg;
+            if (CB && bq > 0) sg = -sg;
+            dmma(acc[rb][cb][p], a[rb][q], sg > 0 ? bp[cb][bq] : bn[cb][bq]);
+          }
+  }
+}
+
+// The cp.async ring and the k loop for one (NRB, NCB) instance.
+template <bool CA, bool CB, int NRB, int NCB>
+__device__ __forceinline__ void mma_loop(const Operands& g, double* smem, int64_t i0, int64_t j0,
                                          int64_t kbeg, int64_t kend, Acc& acc) {
   constexpr bool AK = !CA, BJ = !CB;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int wr = w >> 2, wc = w & 3;
   const int gid = lane >> 2, tig = lane & 3;
   const int nk = kend > kbeg ? (int)((kend - kbeg + BK - 1) / BK) : 0;
-
 #pragma unroll
   for (int s = 0; s < STAGES - 1; ++s) {
     if (s < nk)
@@ -156,46 +199,31 @@ __device__ __forceinline__ void mma_tile(const Operands& g, double* smem, int64_
     }
     const double* As = smem + (kt % STAGES) * STAGE;
     const double* Bs = As + OP_STAGE;
-#pragma unroll
-    for (int kk = 0; kk < BK / 4; ++kk) {
-      const int k = 4 * kk + tig;
-      double a[WRB][4];  // [rb][q]
-#pragma unroll
-      for (int rb = 0; rb < WRB; ++rb) {
-        const int x = 16 * wr + 8 * rb + gid;
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-          a[rb][q] = AK ? As[(q * BM + x) * LDK + k] : As[(q * BK + k) * LDX + x];
-      }
-      double bp[WCB][4], bn[WCB][4];  // + and - copies, [cb][plane]
-#pragma unroll
-      for (int cb = 0; cb < WCB; ++cb) {
-        const int x = 16 * wc + 8 * cb + gid;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          bp[cb][q] = BJ ? Bs[(q * BK + k) * LDX + x] : Bs[(q * BN + x) * LDK + k];
-          bn[cb][q] = -bp[cb][q];
-        }
-      }
-#pragma unroll
-      for (int q = 0; q < 4; ++q)
-#pragma unroll
-        for (int rb = 0; rb < WRB; ++rb)
-#pragma unroll
-          for (int cb = 0; cb < WCB; ++cb)
-#pragma unroll
-            for (int p = 0; p < 4; ++p) {
-              const int bq = hplane(q, p);
-              // conj(A): a_x,y,z negated -> flip terms q >= 1;
-              // conj(B): b_x,y,z negated -> flip when the B plane is not w.
-              int sg = hsign(q, p);
-              if (CA && q > 0) sg = -sg;
-              if (CB && bq > 0) sg = -sg;
-              dmma(acc[rb][cb][p], a[rb][q], sg > 0 ? bp[cb][bq] : bn[cb][bq]);
-            }
-    }
+    if (NRB > 0 && NCB > 0) kstep<CA, CB, AK, BJ, (NRB > 0 ? NRB : 1), (NCB > 0 ? NCB : 1)>(As, Bs, wr, wc, gid, tig, acc);
   }
   cp_async_wait<0>();
+}
+
+// acc += op(A) op(B) over k in [kbeg, kend).  CA/CB: op = adjoint, which
+// requires the i-fast / k-fast layouts (AK = !CA, BJ = !CB).  The caller must
+// __syncthreads() between successive calls that reuse `smem`.  8x8 blocks
+// entirely past M or N (l, s not multiples of 64) issue no DMMA: each warp
+// runs the loop instance for its count of valid row/column blocks (a warp-
+// uniform choice made once), so edge tiles finish early and free the SM.
+template <bool CA, bool CB>
+__device__ __forceinline__ void mma_tile(const Operands& g, double* smem, int64_t i0, int64_t j0,
+                                         int64_t kbeg, int64_t kend, Acc& acc) {
+  const int w = threadIdx.x >> 5;
+  const int64_t r0w = i0 + 16 * (w >> 2), c0w = j0 + 16 * (w & 3);
+  const int nrb = r0w >= g.M ? 0 : r0w + 8 >= g.M ? 1 : 2;
+  const int ncb = c0w >= g.N ? 0 : c0w + 8 >= g.N ? 1 : 2;
+  switch (nrb * 4 + ncb) {
+    case 2 * 4 + 2: mma_loop<CA, CB, 2, 2>(g, smem, i0, j0, kbeg, kend, acc); break;
+    case 2 * 4 + 1: mma_loop<CA, CB, 2, 1>(g, smem, i0, j0, kbeg, kend, acc); break;
+    case 1 * 4 + 2: mma_loop<CA, CB, 1, 2>(g, smem, i0, j0, kbeg, kend, acc); break;
+    case 1 * 4 + 1: mma_loop<CA, CB, 1, 1>(g, smem, i0, j0, kbeg, kend, acc); break;
+    default: mma_loop<CA, CB, 0, 0>(g, smem, i0, j0, kbeg, kend, acc); break;  // loads + barriers only
+  }
 }
 
 }  // namespace qt

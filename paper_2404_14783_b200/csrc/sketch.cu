@@ -15,6 +15,13 @@
 // go to workspaces reduced in fixed order afterwards: deterministic, no
 // atomics.  Omega (n x s) and the Psi column slice (l x b) are generated on
 // device by K1 (embed.cu) from the reference's counter RNG.
+#include <array>
+#include <cstdlib>
+#include <functional>
+#include <map>
+#include <queue>
+#include <vector>
+
 #include "common.cuh"
 #include "kernels.cuh"
 #include "qtile.cuh"
@@ -36,6 +43,7 @@ struct FusedArgs {
   int64_t ky_chunk;
   int w_tm, w_tn, zw;
   int64_t kw_chunk;
+  int y_tnf, w_tmf;  // full (no padding) Y column tiles / W row tiles
   double* y[4];
   int64_t ldy;
   double* yp;  // [zy][4][My][Ny] partials when zy > 1
@@ -71,25 +79,44 @@ __device__ __forceinline__ void store_tile(const qt::Acc& acc, int64_t i0, int64
   }
 }
 
+// Task order = longest first (LPT list scheduling by the hardware CTA
+// dispatcher): full W tiles, full Y tiles, then the Y tiles of the padded
+// last column tile (s % 64 != 0) and the W tiles of the padded last row tile
+// (l % 64 != 0), whose out-of-range 8x8 blocks issue no DMMA (qtile.cuh).
 __global__ void __launch_bounds__(NT, 1) sketch_fused_kernel(FusedArgs f) {
   extern __shared__ __align__(16) double smem[];
   qt::Acc acc;
   qt::zero_acc(acc);
-  const int ny = f.y_tm * f.y_tn * f.zy;
+  const int nwf = f.w_tmf * f.w_tn * f.zw;
+  const int nyf = f.y_tm * f.y_tnf * f.zy;
+  const int nyp = f.y_tm * (f.y_tn - f.y_tnf) * f.zy;
   int t = blockIdx.x;
-  if (t < ny) {
-    const int z = t % f.zy;
-    t /= f.zy;
-    const int tn = t % f.y_tn, tm = t / f.y_tn;
+  bool is_w;
+  int tm, tn, z;
+  if (t < nwf) {
+    is_w = true;
+    z = t % f.zw; t /= f.zw;
+    tm = t % f.w_tmf; tn = t / f.w_tmf;  // a-tiles fastest: neighbours share A columns
+  } else if ((t -= nwf) < nyf) {
+    is_w = false;
+    z = t % f.zy; t /= f.zy;
+    tn = t % f.y_tnf; tm = t / f.y_tnf;
+  } else if ((t -= nyf) < nyp) {
+    is_w = false;
+    z = t % f.zy; t /= f.zy;
+    tn = f.y_tnf + t % (f.y_tn - f.y_tnf); tm = t / (f.y_tn - f.y_tnf);
+  } else {
+    t -= nyp;
+    is_w = true;
+    z = t % f.zw; t /= f.zw;
+    tm = f.w_tmf + t % (f.w_tm - f.w_tmf); tn = t / (f.w_tm - f.w_tmf);
+  }
+  if (!is_w) {
     const int64_t kb = (int64_t)z * f.ky_chunk, ke = min(f.ky, kb + f.ky_chunk);
     qt::mma_tile<false, false>(f.yop, smem, (int64_t)tm * BM, (int64_t)tn * BN, kb, ke, acc);
     double* part = f.zy > 1 ? f.yp + (int64_t)z * 4 * f.yop.M * f.yop.N : nullptr;
     store_tile(acc, (int64_t)tm * BM, (int64_t)tn * BN, f.yop.M, f.yop.N, f.y, f.ldy, part, true);
   } else {
-    t -= ny;
-    const int z = t % f.zw;
-    t /= f.zw;
-    const int tm = t % f.w_tm, tn = t / f.w_tm;  // a-tiles fastest: neighbours share A columns
     const int64_t kb = (int64_t)z * f.kw_chunk, ke = min(f.kw, kb + f.kw_chunk);
     qt::mma_tile<false, false>(f.wop, smem, (int64_t)tm * BM, (int64_t)tn * BN, kb, ke, acc);
     double* part = f.zw > 1 ? f.wp + (int64_t)z * 4 * f.wop.M * f.wop.N : nullptr;
@@ -97,7 +124,6 @@ __global__ void __launch_bounds__(NT, 1) sketch_fused_kernel(FusedArgs f) {
   }
 }
 
-constexpr double kL2Budget = 48e6;  // bytes of A panel kept L2-resident
 
 }  // namespace
 
@@ -108,6 +134,57 @@ namespace {
 struct SketchWork {
   DeviceBuffer yp, wp;  // split-K partial workspaces, grown on demand
 };
+
+// Makespan of one fused launch under greedy list scheduling on 148 SMs
+// (1 CTA per SM), tasks in kernel order.
+double simulate_panel(int64_t rp, int64_t n, int64_t s, int64_t l, int zy, int zw) {
+  const int64_t kyc = ((n + zy - 1) / zy + BK - 1) / BK * BK, kwc = ((rp + zw - 1) / zw + BK - 1) / BK * BK;
+  const int64_t ny_chunks = (n + kyc - 1) / kyc, nw_chunks = (rp + kwc - 1) / kwc;
+  const int64_t y_tm = (rp + BM - 1) / BM, y_tn = (s + BN - 1) / BN, w_tm = (l + BM - 1) / BM,
+                w_tn = (n + BN - 1) / BN;
+  const int64_t y_tnf = s / BN, w_tmf = l / BM;
+  auto frac = [](int64_t valid) { return (double)((valid + 7) / 8) / 8.0; };  // 8-blocks of 64
+  const double y_part = frac(s - y_tnf * BN), w_part = frac(l - w_tmf * BM);
+  struct Group { int64_t count; double cost; };
+  const Group groups[4] = {{w_tmf * w_tn * nw_chunks, (double)(kwc / BK)},
+                           {y_tm * y_tnf * ny_chunks, (double)(kyc / BK)},
+                           {y_tm * (y_tn - y_tnf) * ny_chunks, (double)(kyc / BK) * y_part},
+                           {(w_tm - w_tmf) * w_tn * nw_chunks, (double)(kwc / BK) * w_part}};
+  std::priority_queue<double, std::vector<double>, std::greater<double>> sm;
+  for (int i = 0; i < 148; ++i) sm.push(0.0);
+  double mk = 0.0;
+  for (const Group& g : groups)
+    for (int64_t c = 0; c < g.count; ++c) {
+      const double t0 = sm.top();
+      sm.pop();
+      const double t1 = t0 + g.cost + 2.0;  // + prologue/epilogue (~2 k-steps)
+      mk = std::max(mk, t1);
+      sm.push(t1);
+    }
+  // split-K partials cost a reduction pass over zy Y / zw W copies
+  // (~1 k-step of time per 25 MB of partials)
+  const double red = (zy > 1 ? (double)zy * rp * s : 0.0) + (zw > 1 ? (double)zw * l * n : 0.0);
+  return mk + red * 32.0 / 25e6;
+}
+
+std::pair<int, int> choose_panel_splits(int64_t rp, int64_t n, int64_t s, int64_t l) {
+  static std::map<std::array<int64_t, 4>, std::pair<int, int>> cache;
+  const std::array<int64_t, 4> key{rp, n, s, l};
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  const int64_t wt = ((l + BM - 1) / BM) * ((n + BN - 1) / BN);
+  const int zw_max = (int)std::max<int64_t>(1, std::min<int64_t>(wt >= 148 ? 8 : 64, rp / 64));
+  const int zy_max = (int)std::max<int64_t>(1, std::min<int64_t>(256, n / 32));
+  double best = 1e300;
+  std::pair<int, int> arg{1, 1};
+  for (int zw = 1; zw <= zw_max; ++zw)
+    for (int zy = 1; zy <= zy_max; ++zy) {
+      const double mk = simulate_panel(rp, n, s, l, zy, zw);
+      if (mk < best - 1e-9) { best = mk; arg = {zy, zw}; }
+    }
+  cache[key] = arg;
+  return arg;
+}
 
 // One fused launch (+ ordered partial reductions) for a row panel `ap` of A
 // whose Psi columns are ps[:, pc0 : pc0 + ap.rows].
@@ -139,26 +216,14 @@ void sketch_panel(Ctx& ctx, const QView& om, const QView& ps, int64_t pc0, const
     f.y_tn = (int)((s + BN - 1) / BN);
     f.w_tm = w_tm;
     f.w_tn = w_tn;
-    // Task lengths (in k-steps) are balanced with a makespan model: every
-    // CTA runs one task, the launch takes ~waves * (longest task), and we
-    // maximise useful work / (148 * waves * longest).  W is split over the
-    // panel rows only when its tiles cannot fill the GPU (C5-like shapes).
-    const int64_t wt = (int64_t)w_tm * w_tn, yt = (int64_t)f.y_tm * f.y_tn;
-    const double work = (double)yt * n + (double)wt * rp;
-    double best = -1.0;
-    int best_zw = 1, best_zy = 1;
-    const int zw_max = wt >= 148 ? 1 : (int)std::max<int64_t>(1, std::min<int64_t>(64, rp / 64));
-    for (int zw = 1; zw <= zw_max; ++zw) {
-      const int64_t kwc = ((rp + zw - 1) / zw + BK - 1) / BK * BK;
-      const int zy_max = (int)std::max<int64_t>(1, std::min<int64_t>(512, n / 32));
-      for (int zy = 1; zy <= zy_max; ++zy) {
-        const int64_t kyc = ((n + zy - 1) / zy + BK - 1) / BK * BK;
-        const int64_t ctas = yt * ((n + kyc - 1) / kyc) + wt * ((rp + kwc - 1) / kwc);
-        const int64_t waves = (ctas + 147) / 148;
-        const double score = work / (148.0 * (double)waves * (double)std::max(kyc, kwc) + 16.0 * ctas);
-        if (score > best) { best = score; best_zw = zw; best_zy = zy; }
-      }
-    }
+    // Split counts (zy over n, zw over the panel rows) from a simulation of
+    // the dispatcher: CTAs in kernel order (longest first) go to the SM that
+    // frees first; cost = k-steps x fraction of 8x8 blocks inside M x N.
+    // Cached per panel shape.
+    f.y_tnf = (int)(s / BN);
+    f.w_tmf = (int)(l / BM);
+    const auto choice = choose_panel_splits(rp, n, s, l);
+    const int best_zy = choice.first, best_zw = choice.second;
     f.kw_chunk = ((rp + best_zw - 1) / best_zw + BK - 1) / BK * BK;
     f.zw = (int)((rp + f.kw_chunk - 1) / f.kw_chunk);
     f.ky_chunk = ((n + best_zy - 1) / best_zy + BK - 1) / BK * BK;
@@ -173,7 +238,7 @@ void sketch_panel(Ctx& ctx, const QView& om, const QView& ps, int64_t pc0, const
       if (wp.bytes < need) wp = DeviceBuffer(ctx, need);
       f.wp = wp.as<double>();
     }
-    const int64_t ctas = yt * f.zy + wt * f.zw;
+    const int64_t ctas = (int64_t)f.y_tm * f.y_tn * f.zy + (int64_t)w_tm * w_tn * f.zw;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (ctx.ktimer.on) {
       QLRA_CUDA(cudaEventCreate(&e0));
@@ -204,11 +269,32 @@ void set_kernel_attrs() {
   }
 }
 
-// Panel rows: L2 budget, multiple of 64, at least 256 (keeps W tasks dense).
-int64_t panel_rows(int64_t n, int64_t b) {
-  int64_t R = (int64_t)(kL2Budget / (32.0 * (double)n));
+// Rows per fused launch.  Device-resident A: panels of up to kPanelBytes --
+// the kernel does ~300 flop per byte of A, so an A tile re-read from HBM
+// instead of L2 costs nothing measurable, while one long launch balances the
+// CTAs over the SMs far better than many short ones (C2: 16.3 ms as one
+// launch vs 19.9 ms as 32 L2-sized panels).  Host-streamed A: chunks of
+// kStreamBytes so the H2D copy of the next chunk overlaps the sketch of this
+// one.  Multiples of 64 rows, at least 256.  QLRA_PANEL_BYTES /
+// QLRA_STREAM_BYTES override (tuning).
+constexpr double kPanelBytes = 2e9;
+constexpr double kStreamBytes = 48e6;
+double env_or(const char* name, double dflt) {
+  const char* e = std::getenv(name);
+  return e ? std::atof(e) : dflt;
+}
+int64_t rows_for(double bytes, int64_t n, int64_t b) {
+  int64_t R = (int64_t)(bytes / (32.0 * (double)n));
   R = std::max<int64_t>(256, (R / 64) * 64);
   return std::min<int64_t>(R, ((b + 63) / 64) * 64);
+}
+int64_t panel_rows(int64_t n, int64_t b) {
+  static const double bytes = env_or("QLRA_PANEL_BYTES", kPanelBytes);
+  return rows_for(bytes, n, b);
+}
+int64_t stream_rows(int64_t n, int64_t b) {
+  static const double bytes = env_or("QLRA_STREAM_BYTES", kStreamBytes);
+  return rows_for(bytes, n, b);
 }
 
 }  // namespace
@@ -244,7 +330,7 @@ void sketch_update_rows_host(Ctx& ctx, const qlra_spec_t& omega, const qlra_spec
   launch_gen(ctx.stream, omega, 0, 0, n, s, om.v, false);
   DevQMat ps(ctx, l, b);
   launch_gen(ctx.stream, psi, 0, row0, l, b, ps.v, false);
-  int64_t R = block_rows > 0 ? block_rows : panel_rows(n, b);
+  int64_t R = block_rows > 0 ? block_rows : stream_rows(n, b);
   R = std::min(R, b);
   DevQMat buf[2] = {DevQMat(ctx, R, n), DevQMat(ctx, R, n)};
   cudaStream_t cs;
