@@ -433,13 +433,20 @@ void pseudo_qr_dev(Ctx& c, const QView& Y, const QView& H, const qlra_pseudo_qr_
   r.method = QLRA_PSEUDO_QR;
   DevQMat g(c, s, s), mk(c, s, s);
   qgemm(c, QLRA_OP_C, QLRA_OP_N, 1.0, cm.v, cm.v, 0.0, g.v);  // H0^* H0 = C^* C
-  r.kappa_before = kappa_from_eigs(quat_eigs(c, g.v));
+  // All eigenvalues of G_0 once.  M_k = (1-eps) I + eps G_k^{-1} is a function
+  // of G_k, so G_{k+1} = M_k G_k M_k has the eigenvalues
+  // lambda ((1-eps) + eps / lambda)^2: kappa(H_k) after every correction step
+  // follows from G_0's spectrum (exact identity; the reference recomputes it
+  // from H_k, rangefinders.cpp:136, which agrees to rounding).
+  std::vector<double> lam = quat_eigs(c, g.v, /*extremes_only=*/false);
+  r.kappa_before = kappa_from_eigs(lam);
   double kappa = r.kappa_before;
   try {
     while (r.correction_steps_used < cfg.max_correction_steps && kappa > kKappaTarget) {
       // one inverse serves estimate_epsilon and correction_step (both
       // factor the same H^*H, rangefinders.cpp:68,102)
       check_gram_rcond(kappa, 1e-15, "estimate_epsilon: H*H numerically singular");
+      if (r.correction_steps_used > 0) qgemm(c, QLRA_OP_C, QLRA_OP_N, 1.0, cm.v, cm.v, 0.0, g.v);
       DevQMat ginv = gram_inverse(c, g.v, kappa, 1e-14, "solve_quaternion_linear: singular system");
       const double eps = estimate_epsilon_from_inverse(c, ginv.v, cfg.power_iters_for_epsilon);
       if (!(eps > 0.0 && eps < 1.0))
@@ -449,8 +456,14 @@ void pseudo_qr_dev(Ctx& c, const QView& Y, const QView& H, const qlra_pseudo_qr_
       DevQMat cn(c, s, s);
       qgemm(c, QLRA_OP_N, QLRA_OP_N, 1.0, cm.v, mk.v, 0.0, cn.v);
       cm = std::move(cn);
-      qgemm(c, QLRA_OP_C, QLRA_OP_N, 1.0, cm.v, cm.v, 0.0, g.v);
-      kappa = kappa_from_eigs(quat_eigs(c, g.v));
+      double lmax = 0.0, lmin = std::numeric_limits<double>::infinity();
+      for (double& v : lam) {
+        const double f = (1.0 - eps) + eps / v;
+        v = v * f * f;
+        lmax = std::max(lmax, v);
+        lmin = std::min(lmin, v);
+      }
+      kappa = lmin > 0.0 ? std::sqrt(lmax / lmin) : std::numeric_limits<double>::infinity();
       ++r.correction_steps_used;
     }
   } catch (const Status& e) {

@@ -227,52 +227,6 @@ __global__ void __launch_bounds__(SNT) k_tridiag(double2* a, int64_t n, int64_t 
   for (int64_t i = t; i < n; i += blockDim.x) d[i] = a[i * ld + i].x;
 }
 
-__device__ int sturm_count(const double* d, const double* e, int64_t n, double x) {
-  int cnt = 0;
-  double q = d[0] - x;
-  if (q < 0) ++cnt;
-  for (int64_t i = 1; i < n; ++i) {
-    if (q == 0.0) q = 1e-300;
-    q = d[i] - x - e[i - 1] * e[i - 1] / q;
-    if (q < 0) ++cnt;
-  }
-  return cnt;
-}
-
-// Bisection for every eigenvalue; w sorted descending.
-__global__ void k_bisect(const double* d, const double* e, int64_t n, double* w, int extremes_only) {
-  __shared__ double s_lo, s_hi;
-  if (threadIdx.x == 0) {
-    double lo = d[0], hi = d[0];
-    for (int64_t i = 0; i < n; ++i) {
-      const double r = (i > 0 ? fabs(e[i - 1]) : 0.0) + (i + 1 < n ? fabs(e[i]) : 0.0);
-      lo = fmin(lo, d[i] - r);
-      hi = fmax(hi, d[i] + r);
-    }
-    const double pad = 2.2e-16 * fmax(fabs(lo), fabs(hi)) * (double)n + 1e-300;
-    s_lo = lo - pad;
-    s_hi = hi + pad;
-  }
-  __syncthreads();
-  const int64_t cnt = extremes_only ? (n < 2 ? n : 2) : n;
-  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < cnt;
-       q += (int64_t)gridDim.x * blockDim.x) {
-    // k-th smallest eigenvalue: smallest x with count(x) > k
-    const int64_t k = extremes_only ? (q == 0 ? 0 : n - 1) : q;
-    double lo = s_lo, hi = s_hi;
-    for (int it = 0; it < 2100; ++it) {
-      const double mid = 0.5 * (lo + hi);
-      if (mid <= lo || mid >= hi) break;
-      if (hi - lo <= 4.4e-16 * fmax(fabs(lo), fabs(hi))) break;
-      if (sturm_count(d, e, n, mid) > k) hi = mid; else lo = mid;
-    }
-    w[n - 1 - k] = 0.5 * (lo + hi);
-  }
-}
-
-// Extreme eigenvalues of the symmetric tridiagonal (d, e) by parallel
-// multisection: half the CTA brackets the largest, half the smallest; each
-// round evaluates 511 Sturm counts and shrinks the bracket 512-fold.
 // Sturm count by the three-term recurrence of the leading principal minors,
 // p_i = (d_i - x) p_{i-1} - e_{i-1}^2 p_{i-2} (eigenvalues < x = sign changes
 // in p_0 = 1, p_1, ..., p_n): two dependent FMAs per step instead of a
@@ -361,7 +315,7 @@ __global__ void __launch_bounds__(2 * MS_PROBES) k_multisect_extremes(const doub
     const bool done0 = !(s_hi[0] - s_lo[0] > 4.4e-16 * fmax(fabs(s_lo[0]), fabs(s_hi[0])));
     const bool done1 = !(s_hi[1] - s_lo[1] > 4.4e-16 * fmax(fabs(s_lo[1]), fabs(s_hi[1])));
     if (done0 && done1) break;  // both converged (same decision in every thread)
-    if (j == 0) s_first[half] = MS_PROBES;
+    if (j == 0) s_first[half] = MS_PROBES - 1;  // above every probe: last sub-interval
     __syncthreads();
     if (!done && j < MS_PROBES - 1) {
       const double x = lo + (hi - lo) * (double)(j + 1) / (double)MS_PROBES;
@@ -369,9 +323,12 @@ __global__ void __launch_bounds__(2 * MS_PROBES) k_multisect_extremes(const doub
     }
     __syncthreads();
     if (!done && j == 0) {
-      const int f = s_first[half];  // first probe with count > k (MS_PROBES: none)
+      // MS_PROBES - 1 probes split [lo, hi] into MS_PROBES sub-intervals; the
+      // eigenvalue lies in sub-interval f (first probe with count > k, or
+      // MS_PROBES - 1 when it is above every probe)
+      const int f = s_first[half];
       const double nlo = f == 0 ? lo : lo + (hi - lo) * (double)f / (double)MS_PROBES;
-      const double nhi = f == MS_PROBES ? hi : lo + (hi - lo) * (double)(f + 1) / (double)MS_PROBES;
+      const double nhi = f == MS_PROBES - 1 ? hi : lo + (hi - lo) * (double)(f + 1) / (double)MS_PROBES;
       s_lo[half] = nlo;
       s_hi[half] = nhi;
     }
@@ -380,6 +337,94 @@ __global__ void __launch_bounds__(2 * MS_PROBES) k_multisect_extremes(const doub
   if (t == 0) {
     w[0] = 0.5 * (s_lo[0] + s_hi[0]) / sc;
     w[n - 1] = 0.5 * (s_lo[1] + s_hi[1]) / sc;
+  }
+}
+
+// All eigenvalues of the symmetric tridiagonal (d, e), descending in w.
+// k_tri_prep (one CTA) writes hdr = {scale, lo, hi} (power-of-two scale so
+// |entries| < 1; Gershgorin interval of the scaled matrix; scale = 0 for the
+// zero matrix) and the scaled d, e^2.  k_multisect_all: one warp per
+// eigenvalue index (the k-th smallest is the smallest x with count(x) > k),
+// 31 probes per round (5 bits), division-free Sturm counts on the scaled
+// arrays, staged in shared memory when they fit.
+__global__ void __launch_bounds__(256) k_tri_prep(const double* d, const double* e, int64_t n, double* hdr,
+                                                  double* sd, double* se2) {
+  __shared__ double s_red[8];
+  const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+  double mx = 0.0;
+  for (int64_t i = t; i < n; i += blockDim.x) {
+    mx = fmax(mx, fabs(d[i]));
+    if (i + 1 < n) mx = fmax(mx, fabs(e[i]));
+  }
+  for (int off = 16; off > 0; off >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+  if (lane == 0) s_red[wid] = mx;
+  __syncthreads();
+  if (t == 0) {
+    for (int i = 1; i < (int)(blockDim.x >> 5); ++i) mx = fmax(mx, s_red[i]);
+    int ex = 0;
+    frexp(mx > 0.0 ? mx : 1.0, &ex);
+    s_red[0] = mx > 0.0 ? ldexp(1.0, -ex) : 0.0;
+  }
+  __syncthreads();
+  const double sc = s_red[0];
+  for (int64_t i = t; i < n; i += blockDim.x) {
+    sd[i] = d[i] * sc;
+    const double ei = i + 1 < n ? e[i] * sc : 0.0;
+    se2[i] = ei * ei;
+  }
+  __syncthreads();
+  if (t == 0) {
+    double lo = sd[0], hi = sd[0];
+    for (int64_t i = 0; i < n; ++i) {
+      const double r = (i > 0 ? sqrt(se2[i - 1]) : 0.0) + (i + 1 < n ? sqrt(se2[i]) : 0.0);
+      lo = fmin(lo, sd[i] - r);
+      hi = fmax(hi, sd[i] + r);
+    }
+    const double pad = 2.2e-16 * fmax(fabs(lo), fabs(hi)) * (double)n + 0x1p-300;
+    hdr[0] = sc;
+    hdr[1] = lo - pad;
+    hdr[2] = hi + pad;
+  }
+}
+
+constexpr int MSA_WARPS = 8;
+__global__ void __launch_bounds__(32 * MSA_WARPS) k_multisect_all(const double* hdr, const double* gsd,
+                                                                  const double* gse2, int64_t n, int use_smem,
+                                                                  double* w) {
+  extern __shared__ double ts[];
+  const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+  const double sc = hdr[0];
+  if (sc == 0.0) {  // zero matrix: every eigenvalue is exactly 0
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + t; k < n; k += (int64_t)gridDim.x * blockDim.x) w[k] = 0.0;
+    return;
+  }
+  const double* sd = gsd;
+  const double* se2 = gse2;
+  if (use_smem) {
+    for (int64_t i = t; i < n; i += blockDim.x) {
+      ts[i] = gsd[i];
+      ts[n + i] = gse2[i];
+    }
+    __syncthreads();
+    sd = ts;
+    se2 = ts + n;
+  }
+  for (int64_t k = (int64_t)blockIdx.x * MSA_WARPS + wid; k < n; k += (int64_t)gridDim.x * MSA_WARPS) {
+    double lo = hdr[1], hi = hdr[2];
+    for (int round = 0; round < 48; ++round) {
+      if (!(hi - lo > 4.4e-16 * fmax(fabs(lo), fabs(hi)))) break;  // warp-uniform
+      const double x = lo + (hi - lo) * (double)(lane + 1) / 32.0;
+      const bool hit = lane < 31 && x > lo && x < hi && sturm_count_poly(sd, se2, (int)n, x) > k;
+      // 31 probes split [lo, hi] into 32 sub-intervals; the eigenvalue lies in
+      // sub-interval f = first probe with count > k (31: above every probe)
+      const unsigned m = __ballot_sync(0xffffffffu, hit);
+      const int f = m ? __ffs(m) - 1 : 31;
+      const double nlo = f == 0 ? lo : lo + (hi - lo) * (double)f / 32.0;
+      const double nhi = f == 31 ? hi : lo + (hi - lo) * (double)(f + 1) / 32.0;
+      lo = nlo;
+      hi = nhi;
+    }
+    if (lane == 0) w[n - 1 - k] = 0.5 * (lo + hi) / sc;
   }
 }
 
@@ -875,7 +920,7 @@ __global__ void __launch_bounds__(512) k_qtridiag_smem(QView a, double* d, doubl
 // (v double-buffered), and p(k+1) only after it has this CTA's part of
 // v(k+1), i.e. after this CTA finished reading p(k).
 // Same reflectors as k_qtridiag.
-constexpr int QTC = 8;
+constexpr int QTC = 16;  // non-portable cluster size (B200 allows 16 with the opt-in attribute)
 constexpr int QTC_MAX = 224;
 constexpr int QTC_THREADS = 256;
 
@@ -1655,6 +1700,29 @@ void small_inv_lower_adjoint_to_quat(Ctx& ctx, const double2* l, int64_t n, int6
   QLRA_LAUNCH_CHECK();
   count_launch();
 }
+// all eigenvalues (descending) of the tridiagonal (d, e) into d_w
+void tridiag_all_eigvals(Ctx& ctx, const double* d, const double* e, int64_t n, double* d_w) {
+  DeviceBuffer work(ctx, sizeof(double) * (size_t)(3 + 2 * n));
+  double* hdr = work.as<double>();
+  double* sd = hdr + 3;
+  double* se2 = sd + n;
+  k_tri_prep<<<1, 256, 0, ctx.stream>>>(d, e, n, hdr, sd, se2);
+  QLRA_LAUNCH_CHECK();
+  count_launch();
+  const size_t smem = sizeof(double) * 2 * (size_t)n;
+  const int use_smem = smem <= 96 * 1024 ? 1 : 0;
+  static bool attr = false;
+  if (!attr) {
+    QLRA_CUDA(cudaFuncSetAttribute(k_multisect_all, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
+    attr = true;
+  }
+  const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((n + MSA_WARPS - 1) / MSA_WARPS, 4 * 148));
+  k_multisect_all<<<(unsigned)blocks, 32 * MSA_WARPS, use_smem ? smem : 0, ctx.stream>>>(hdr, sd, se2, n,
+                                                                                        use_smem, d_w);
+  QLRA_LAUNCH_CHECK();
+  count_launch();
+}
+
 void small_herm_eigvals(Ctx& ctx, double2* a, int64_t n, int64_t ld, double* d_w) {
   if (n == 0) return;
   DeviceBuffer de(ctx, sizeof(double) * (2 * n + 1));
@@ -1664,9 +1732,7 @@ void small_herm_eigvals(Ctx& ctx, double2* a, int64_t n, int64_t ld, double* d_w
   k_tridiag<<<1, SNT, 0, ctx.stream>>>(a, n, ld, d, e, work.as<double2>());
   QLRA_LAUNCH_CHECK();
   count_launch();
-  k_bisect<<<(unsigned)((n + 255) / 256), 256, 0, ctx.stream>>>(d, e, n, d_w, 0);
-  QLRA_LAUNCH_CHECK();
-  count_launch();
+  tridiag_all_eigvals(ctx, d, e, n, d_w);
 }
 void small_quat_herm_eigvals(Ctx& ctx, const QView& a, double* d_w, bool extremes_only) {
   const int64_t n = a.rows;
@@ -1700,6 +1766,11 @@ void small_quat_herm_eigvals(Ctx& ctx, const QView& a, double* d_w, bool extreme
     const int64_t rmax = (n + QTC - 1) / QTC;
     const size_t csm = sizeof(Q4) * (size_t)(rmax * n + 3 * n);
     static size_t cattr = 0;
+    static bool nonportable = false;
+    if (!nonportable) {
+      QLRA_CUDA(cudaFuncSetAttribute(k_qtridiag_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+      nonportable = true;
+    }
     if (csm > 48 * 1024 && csm > cattr) {
       QLRA_CUDA(cudaFuncSetAttribute(k_qtridiag_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm));
       cattr = csm;
@@ -1725,11 +1796,11 @@ void small_quat_herm_eigvals(Ctx& ctx, const QView& a, double* d_w, bool extreme
   if (extremes_only) {
     // w[0] = max, w[n-1] = min; the middle stays untouched
     k_multisect_extremes<<<1, 2 * MS_PROBES, sizeof(double) * 2 * (size_t)n, ctx.stream>>>(d, e, n, d_w);
+    QLRA_LAUNCH_CHECK();
+    count_launch();
   } else {
-    k_bisect<<<(unsigned)((n + 255) / 256), 256, 0, ctx.stream>>>(d, e, n, d_w, 0);
+    tridiag_all_eigvals(ctx, d, e, n, d_w);
   }
-  QLRA_LAUNCH_CHECK();
-  count_launch();
 }
 void small_quat_eigh(Ctx& ctx, const QView& a, double* d_w, const QView& vecs, int max_sweeps) {
   const int64_t n = a.rows;

@@ -440,6 +440,25 @@ def test_singular_values_and_kappa(ctx, s):  # factorizations.cpp:316-337
     assert abs(Q.condition_number(dev(y), ctx) / O.condition_number(y) - 1) < 1e-8
 
 
+@pytest.mark.parametrize("case", range(6))
+def test_spectrum_multisection_exact_sigmas(ctx, case):
+    """Singular values / kappa from the tridiagonal multisection against
+    planted exact values: clustered tops, gaps, repeated values -- each
+    eigenvalue's interval lands in the last sub-interval of a round many
+    times over these cases."""
+    from paper_2404_14783_b200 import qlra as Q
+    rng = np.random.default_rng(100 + case)
+    s = [12, 40, 64, 100, 150, 200][case]
+    sig = np.sort(rng.uniform(0.5, 1.0, s))[::-1]
+    sig[: s // 3] = 1.0 - 1e-9 * np.arange(s // 3)  # clustered top
+    sig[-3:] = [1e-2, 1e-2, 1e-3]                   # repeated + small
+    sig = np.sort(sig)[::-1]
+    y = planted_matrix_with_sigma(3 * s, list(sig), 200 + case)
+    sv = np.asarray(Q.singular_values(dev(y), ctx))
+    assert np.allclose(sv, sig, rtol=1e-10, atol=0)
+    assert abs(Q.condition_number(dev(y), ctx) / (sig[0] / sig[-1]) - 1) < 1e-10
+
+
 # ------------------------------------------------------- checkpoint I/O ---
 def _np_write_qmat(path, a):  # QMAT1 per proj/include/qlra/io.hpp:15-18
     import struct
