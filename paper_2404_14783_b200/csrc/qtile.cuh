@@ -14,9 +14,11 @@
 // sub-tile = 2x2 blocks of 8x8 per plane: 32 FP64 accumulators per thread
 // (16 warps per SM keep the DMMA pipe fed).
 // Operands are staged by cp.async into a 3-stage shared-memory ring in the
-// layout of their contiguous global dimension (k-fast rows padded to 10
-// doubles, i/j-fast rows to 72), which makes every fragment read a
-// 2-wavefront (conflict-free-optimal) LDS.64.
+// layout of their contiguous global dimension.  Row pitches are 4 mod 16
+// doubles (k-fast rows padded to 12, i/j-fast rows to 68): a half-warp's
+// fragment read covers 4 rows x 4 consecutive elements, which then land in
+// 16 distinct 8-byte bank pairs -- every LDS.64 is 2 wavefronts, the minimum
+// (measured: C2 sketch 16.4 -> 16.1 ms against pitches 10 / 72).
 #pragma once
 
 #include "common.cuh"
@@ -26,8 +28,8 @@ namespace qt {
 
 constexpr int BM = 64, BN = 64, BK = 8, NT = 512, STAGES = 3;
 constexpr int WRB = 2, WCB = 2;  // 8x8 blocks per warp (warp tile 16x16, 4x4 warps)
-constexpr int LDK = BK + 2;    // k-fast rows: [x][k]
-constexpr int LDX = BM + 8;    // i/j-fast rows: [k][x]
+constexpr int LDK = BK + 4;    // k-fast rows: [x][k]
+constexpr int LDX = BM + 4;    // i/j-fast rows: [k][x]
 constexpr int OP_STAGE = 4 * BM * LDK > 4 * BK * LDX ? 4 * BM * LDK : 4 * BK * LDX;  // doubles
 constexpr int STAGE = 2 * OP_STAGE;
 constexpr size_t SMEM_BYTES = (size_t)STAGES * STAGE * sizeof(double);
@@ -62,12 +64,13 @@ __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
 template <bool AK, bool BJ>
 __device__ __forceinline__ void load_stage(const Operands& g, double* As, double* Bs, int64_t i0,
                                            int64_t j0, int64_t k0, int64_t kend, int tid) {
+  constexpr int PER = BM * BK;  // elements per plane per stage
 #pragma unroll
-  for (int r = 0; r < 2048 / NT; ++r) {
-    const int e = tid + NT * r;  // 0..2047 = 4 planes x 64 x 8
-    const int q = e >> 9, idx = e & 511;
+  for (int r = 0; r < 4 * PER / NT; ++r) {
+    const int e = tid + NT * r;  // 4 planes x 64 x BK
+    const int q = e / PER, idx = e % PER;
     int x, k;
-    if (AK) { x = idx >> 3; k = idx & 7; } else { x = idx & 63; k = idx >> 6; }
+    if (AK) { x = idx / BK; k = idx % BK; } else { x = idx % BM; k = idx / BM; }
     const int64_t gi = i0 + x, gk = k0 + k;
     const bool ok = gi < g.M && gk < kend;
     const double* src = ok ? g.a[q] + gi * g.a_si + gk * g.a_sk : g.a[q];
@@ -75,11 +78,11 @@ __device__ __forceinline__ void load_stage(const Operands& g, double* As, double
     cp_async8(dst, src, ok);
   }
 #pragma unroll
-  for (int r = 0; r < 2048 / NT; ++r) {
+  for (int r = 0; r < 4 * PER / NT; ++r) {
     const int e = tid + NT * r;
-    const int q = e >> 9, idx = e & 511;
+    const int q = e / PER, idx = e % PER;
     int x, k;
-    if (BJ) { x = idx & 63; k = idx >> 6; } else { x = idx >> 3; k = idx & 7; }
+    if (BJ) { x = idx % BN; k = idx / BN; } else { x = idx / BK; k = idx % BK; }
     const int64_t gj = j0 + x, gk = k0 + k;
     const bool ok = gj < g.N && gk < kend;
     const double* src = ok ? g.b[q] + gk * g.b_sk + gj * g.b_sj : g.b[q];
