@@ -900,9 +900,14 @@ int qlra_one_pass_qb_host(qlra_ctx_t* ctx, const qlra_qmat_t* a_host, int64_t ro
     QLRA_CUDA(cudaEventRecord(ready, c.stream));
     QLRA_CUDA(cudaStreamWaitEvent(side, ready, 0));
     const QView hv = view_of(h_host), xv = view_of(x_host);
-    for (int p = 0; p < 4; ++p)
-      QLRA_CUDA(cudaMemcpy2DAsync(hv.p[p], sizeof(double) * hv.ld, h.v.p[p], sizeof(double) * h.v.ld,
-                                  sizeof(double) * s, (size_t)rows, cudaMemcpyDeviceToHost, side));
+    for (int p = 0; p < 4; ++p) {
+      if (hv.ld == s)  // contiguous: one linear DMA (h is dense)
+        QLRA_CUDA(cudaMemcpyAsync(hv.p[p], h.v.p[p], sizeof(double) * (size_t)(rows * s), cudaMemcpyDeviceToHost,
+                                  side));
+      else
+        QLRA_CUDA(cudaMemcpy2DAsync(hv.p[p], sizeof(double) * hv.ld, h.v.p[p], sizeof(double) * h.v.ld,
+                                    sizeof(double) * s, (size_t)rows, cudaMemcpyDeviceToHost, side));
+    }
     QLRA_CUDA(cudaEventRecord(copied, side));
     qb_solve_dev(c, *psi, row0, h.v, w.v, x.v);
     for (int p = 0; p < 4; ++p)

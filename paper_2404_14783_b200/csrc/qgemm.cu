@@ -343,7 +343,9 @@ GemmArgs make_args(int op_a, int op_b, double alpha, const QView& A, const QView
 int64_t choose_splits(int64_t tiles, int64_t K, int64_t other_ctas) {
   // Split K so the launch fills whole waves of 148 SMs (1 CTA/SM): maximise
   // ctas / (waves * 148) with a small per-split penalty, >= 24 k-steps each.
-  const int64_t maxs = std::max<int64_t>(1, std::min<int64_t>(64, K / (24 * BK)));
+  // up to two waves of splits: single-tile products with huge K (C5's Grams,
+  // 40 x 40 over 2M rows) need them, and their partials are tiny
+  const int64_t maxs = std::max<int64_t>(1, std::min<int64_t>(296, K / (24 * BK)));
   int64_t best = 1;
   double best_score = -1.0;
   for (int64_t z = 1; z <= maxs; ++z) {

@@ -19,7 +19,6 @@
 #include <cstdlib>
 #include <functional>
 #include <map>
-#include <queue>
 #include <vector>
 
 #include "common.cuh"
@@ -150,17 +149,25 @@ double simulate_panel(int64_t rp, int64_t n, int64_t s, int64_t l, int zy, int z
                            {y_tm * y_tnf * ny_chunks, (double)(kyc / BK)},
                            {y_tm * (y_tn - y_tnf) * ny_chunks, (double)(kyc / BK) * y_part},
                            {(w_tm - w_tmf) * w_tn * nw_chunks, (double)(kwc / BK) * w_part}};
-  std::priority_queue<double, std::vector<double>, std::greater<double>> sm;
-  for (int i = 0; i < 148; ++i) sm.push(0.0);
-  double mk = 0.0;
-  for (const Group& g : groups)
-    for (int64_t c = 0; c < g.count; ++c) {
-      const double t0 = sm.top();
-      sm.pop();
-      const double t1 = t0 + g.cost + 2.0;  // + prologue/epilogue (~2 k-steps)
-      mk = std::max(mk, t1);
-      sm.push(t1);
+  // Greedy assignment on buckets of SMs that free at the same time (tasks of
+  // a group cost the same, so whole buckets advance together): O(tasks/148)
+  // per group instead of a heap operation per CTA.
+  std::map<double, int64_t> sm{{0.0, 148}};
+  for (const Group& g : groups) {
+    const double d = g.cost + 2.0;  // + prologue/epilogue (~2 k-steps)
+    int64_t c = g.count;
+    while (c > 0) {
+      auto it = sm.begin();
+      const double t0 = it->first;
+      const int64_t k = it->second;
+      sm.erase(it);
+      const int64_t take = std::min(c, k);
+      if (k > take) sm[t0] += k - take;
+      sm[t0 + d] += take;
+      c -= take;
     }
+  }
+  const double mk = sm.rbegin()->first;
   // split-K partials cost a reduction pass over zy Y / zw W copies
   // (~1 k-step of time per 25 MB of partials)
   const double red = (zy > 1 ? (double)zy * rp * s : 0.0) + (zw > 1 ? (double)zw * l * n : 0.0);
@@ -173,12 +180,21 @@ std::pair<int, int> choose_panel_splits(int64_t rp, int64_t n, int64_t s, int64_
   auto it = cache.find(key);
   if (it != cache.end()) return it->second;
   const int64_t wt = ((l + BM - 1) / BM) * ((n + BN - 1) / BN);
-  const int zw_max = (int)std::max<int64_t>(1, std::min<int64_t>(wt >= 148 ? 8 : 64, rp / 64));
+  // W split-K only while W has fewer than 4 waves of tiles (its partials are
+  // l x n each: 868 MB at C4)
+  const int zw_max = wt >= 4 * 148 ? 1 : (int)std::max<int64_t>(1, std::min<int64_t>(wt >= 148 ? 8 : 64, rp / 64));
   const int zy_max = (int)std::max<int64_t>(1, std::min<int64_t>(256, n / 32));
+  // candidates: every value up to 16, then geometric steps of ~12%
+  auto candidates = [](int hi) {
+    std::vector<int> v;
+    for (int z = 1; z <= hi; z = z < 16 ? z + 1 : std::max(z + 1, z * 9 / 8)) v.push_back(z);
+    if (v.back() != hi) v.push_back(hi);
+    return v;
+  };
   double best = 1e300;
   std::pair<int, int> arg{1, 1};
-  for (int zw = 1; zw <= zw_max; ++zw)
-    for (int zy = 1; zy <= zy_max; ++zy) {
+  for (int zw : candidates(zw_max))
+    for (int zy : candidates(zy_max)) {
       const double mk = simulate_panel(rp, n, s, l, zy, zw);
       if (mk < best - 1e-9) { best = mk; arg = {zy, zw}; }
     }
@@ -275,8 +291,9 @@ void set_kernel_attrs() {
 // CTAs over the SMs far better than many short ones (C2: 16.3 ms as one
 // launch vs 19.9 ms as 32 L2-sized panels).  Host-streamed A: chunks of
 // kStreamBytes so the H2D copy of the next chunk overlaps the sketch of this
-// one.  Multiples of 64 rows, at least 256.  QLRA_PANEL_BYTES /
-// QLRA_STREAM_BYTES override (tuning).
+// one (about 32 chunks per block, at least kStreamBytes each).  Multiples of
+// 64 rows, at least 256.  QLRA_PANEL_BYTES / QLRA_STREAM_BYTES override
+// (tuning).
 constexpr double kPanelBytes = 2e9;
 constexpr double kStreamBytes = 48e6;
 double env_or(const char* name, double dflt) {
@@ -293,7 +310,10 @@ int64_t panel_rows(int64_t n, int64_t b) {
   return rows_for(bytes, n, b);
 }
 int64_t stream_rows(int64_t n, int64_t b) {
-  static const double bytes = env_or("QLRA_STREAM_BYTES", kStreamBytes);
+  // ~32 chunks per block (overlap granularity), never below kStreamBytes:
+  // small chunks of a narrow A (C5: n = 300) make short, inefficient launches
+  static const double floor_bytes = env_or("QLRA_STREAM_BYTES", kStreamBytes);
+  const double bytes = std::max(floor_bytes, 32.0 * (double)n * (double)b / 32.0);
   return rows_for(bytes, n, b);
 }
 
@@ -349,11 +369,18 @@ void sketch_update_rows_host(Ctx& ctx, const qlra_spec_t& omega, const qlra_spec
     const int64_t rp = std::min(R, b - r0);
     const QView dst = sub(buf[idx].v, 0, 0, rp, n);
     QLRA_CUDA(cudaStreamWaitEvent(cs, freed[idx], 0));
-    for (int p = 0; p < 4; ++p)
-      QLRA_CUDA(cudaMemcpy2DAsync(dst.p[p], (size_t)dst.ld * sizeof(double),
-                                  host_block.p[p] + r0 * host_block.ld,
-                                  (size_t)host_block.ld * sizeof(double),
-                                  (size_t)n * sizeof(double), (size_t)rp, cudaMemcpyHostToDevice, cs));
+    for (int p = 0; p < 4; ++p) {
+      const double* src = host_block.p[p] + r0 * host_block.ld;
+      if (host_block.ld == n && dst.ld == n) {
+        // contiguous rows: one linear DMA (2D copies of narrow rows, e.g.
+        // C5's 2400-byte rows, run far below PCIe bandwidth)
+        QLRA_CUDA(cudaMemcpyAsync(dst.p[p], src, sizeof(double) * (size_t)(rp * n), cudaMemcpyHostToDevice, cs));
+      } else {
+        QLRA_CUDA(cudaMemcpy2DAsync(dst.p[p], (size_t)dst.ld * sizeof(double), src,
+                                    (size_t)host_block.ld * sizeof(double), (size_t)n * sizeof(double),
+                                    (size_t)rp, cudaMemcpyHostToDevice, cs));
+      }
+    }
     QLRA_CUDA(cudaEventRecord(copied[idx], cs));
     QLRA_CUDA(cudaStreamWaitEvent(ctx.stream, copied[idx], 0));
     sketch_panel(ctx, om.v, ps.v, r0, dst, sub(y_rows, r0, 0, rp, s), w, ws);
