@@ -205,6 +205,9 @@ def main():
     r0, r1 = Q.shard_rows(cfg.m, world, rank)
     a = build_matrix(cfg, (r0, r1), ctx)
     torch.cuda.synchronize()
+    # release the generator's temporaries held in torch's cache (C5: tens of
+    # GB), which otherwise crowd the library's stream-ordered pool
+    torch.cuda.empty_cache()
     method = Q.PSEUDO_QR if args.rangefinder == "pseudo_qr" else Q.PSEUDO_SVD
     opts = Q.OnePassOptions(r=cfg.s - 5, s=cfg.s, l=cfg.l, rangefinder=method, embedding=cfg.kind)
     stream = torch.cuda.current_stream()
