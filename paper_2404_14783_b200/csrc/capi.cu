@@ -172,10 +172,16 @@ bool cqr_pass(Ctx& ctx, const QView& y, const QView& hout, bool complex_mode, do
   if (shift != 0.0) small_add_diag(ctx, g.v, shift);
   DevQMat rinv(ctx, s, s);
   if (!blocked_chol_inv(ctx, g.v, rinv.v, rdiag, r_out)) return false;
-  qgemm(ctx, QLRA_OP_N, QLRA_OP_N, 1.0, y, rinv.v, 0.0, hout);
+  if (hout.p[0]) qgemm(ctx, QLRA_OP_N, QLRA_OP_N, 1.0, y, rinv.v, 0.0, hout);  // else: deferred by the caller
   if (rinv_out) copy_qmat(ctx, rinv.v, *rinv_out);
   return true;
 }
+
+// The last CholeskyQR pass's tall product left to the caller: Q = base * rinv_last.
+struct DeferredQ {
+  DevQMat base;       // input of the last pass (rows x s)
+  DevQMat rinv_last;  // R^{-1} of the last pass (s x s)
+};
 
 // r <- next * r (R = R_last ... R_1)
 void chain_r(Ctx& ctx, DevQMat& r, const QView& next) {
@@ -194,11 +200,19 @@ void chain_rinv(Ctx& ctx, DevQMat& rinv, const QView& next) {
 // CholeskyQR2, or shifted CholeskyQR3 (Fukaya et al.) when the first Gram is
 // not numerically positive definite.  rdiag = diag of the full R factor;
 // optional rinv (s x s) = R^{-1} and rfac = R of y = h R.
+// defer (optional): do not form Q in the last pass; return its input and
+// R^{-1} instead (Q = defer->base * defer->rinv_last), so a caller that only
+// needs Q times a small matrix saves one tall product.
 bool cholesky_qr(Ctx& ctx, const QView& y, const QView& h, bool complex_mode, int64_t m_global,
                  std::vector<double>* rdiag, bool distributed = true, DevQMat* rinv = nullptr,
-                 DevQMat* rfac = nullptr) {
+                 DevQMat* rfac = nullptr, DeferredQ* defer = nullptr) {
   const int64_t s = y.cols;
   DevQMat t1(ctx, y.rows, s);
+  QView hq = h;
+  if (defer) {
+    hq = QView{};  // no output product in the last pass
+    defer->rinv_last = DevQMat(ctx, s, s);
+  }
   DevQMat ri[3], rf[3];
   for (int i = 0; i < 2; ++i) {
     if (rinv) ri[i] = DevQMat(ctx, s, s);
@@ -209,7 +223,9 @@ bool cholesky_qr(Ctx& ctx, const QView& y, const QView& h, bool complex_mode, in
   std::vector<double> d1, d2, d3;
   double tr = 0.0;
   if (cqr_pass(ctx, y, t1.v, complex_mode, 0.0, &d1, &tr, distributed, pi(0), pf(0))) {
-    if (!cqr_pass(ctx, t1.v, h, complex_mode, 0.0, &d2, nullptr, distributed, pi(1), pf(1))) return false;
+    const QView* last_inv = defer ? &defer->rinv_last.v : pi(1);
+    if (!cqr_pass(ctx, t1.v, hq, complex_mode, 0.0, &d2, nullptr, distributed, last_inv, pf(1))) return false;
+    if (defer && rinv) copy_qmat(ctx, defer->rinv_last.v, ri[1].v);
     if (rdiag) {
       rdiag->resize(s);
       for (int64_t k = 0; k < s; ++k) (*rdiag)[k] = d1[k] * d2[k];
@@ -222,6 +238,7 @@ bool cholesky_qr(Ctx& ctx, const QView& y, const QView& h, bool complex_mode, in
       *rfac = std::move(rf[0]);
       chain_r(ctx, *rfac, rf[1].v);
     }
+    if (defer) defer->base = std::move(t1);
     return true;
   }
   const double dim = complex_mode ? 2.0 : 4.0;
@@ -232,7 +249,9 @@ bool cholesky_qr(Ctx& ctx, const QView& y, const QView& h, bool complex_mode, in
   if (!cqr_pass(ctx, y, t1.v, complex_mode, shift, &d1, nullptr, distributed, pi(0), pf(0))) return false;
   DevQMat t2(ctx, y.rows, s);
   if (!cqr_pass(ctx, t1.v, t2.v, complex_mode, 0.0, &d2, nullptr, distributed, pi(1), pf(1))) return false;
-  if (!cqr_pass(ctx, t2.v, h, complex_mode, 0.0, &d3, nullptr, distributed, pi(2), pf(2))) return false;
+  const QView* last_inv = defer ? &defer->rinv_last.v : pi(2);
+  if (!cqr_pass(ctx, t2.v, hq, complex_mode, 0.0, &d3, nullptr, distributed, last_inv, pf(2))) return false;
+  if (defer && rinv) copy_qmat(ctx, defer->rinv_last.v, ri[2].v);
   if (rdiag) {
     rdiag->resize(s);
     // y = t1 R1 = t2 R2 R1 = h R3 R2 R1 holds exactly whatever the shift, so
@@ -249,6 +268,7 @@ bool cholesky_qr(Ctx& ctx, const QView& y, const QView& h, bool complex_mode, in
     chain_r(ctx, *rfac, rf[1].v);
     chain_r(ctx, *rfac, rf[2].v);
   }
+  if (defer) defer->base = std::move(t2);
   return true;
 }
 
@@ -421,8 +441,12 @@ void pseudo_qr_dev(Ctx& c, const QView& Y, const QView& H, const qlra_pseudo_qr_
   // orthonormal), and one tall product H = Q0 C_k closes the pass.  H lies in
   // range(Q0) = range(H0) to rounding, which is what the reference's
   // re-projection (rangefinders.cpp:142-153) restores.
-  DevQMat q0(c, Y.rows, s), rq;
-  if (!cholesky_qr(c, Y, q0.v, /*complex_mode=*/false, m, nullptr, /*distributed=*/true, nullptr, &rq))
+  // Q0 itself is never formed: Q0 = base * rinv_last, and the pass closes
+  // with H = base * (rinv_last * C_k) -- one tall product fewer, same
+  // accuracy (rinv_last is the well-conditioned last CholeskyQR factor).
+  DevQMat rq;
+  DeferredQ q0;
+  if (!cholesky_qr(c, Y, QView{}, /*complex_mode=*/false, m, nullptr, /*distributed=*/true, nullptr, &rq, &q0))
     fail(QLRA_ERR_RANK, "pseudo_qr: sketch numerically rank-deficient; use pseudo_svd");
   DevQMat cm(c, s, s);
   std::vector<double> rd;
@@ -470,7 +494,11 @@ void pseudo_qr_dev(Ctx& c, const QView& Y, const QView& H, const qlra_pseudo_qr_
     if (e.code != QLRA_ERR_SINGULAR) throw;
     fail(QLRA_ERR_RANK, "pseudo_qr: sketch numerically rank-deficient; use pseudo_svd");
   }
-  qgemm(c, QLRA_OP_N, QLRA_OP_N, 1.0, q0.v, cm.v, 0.0, H);
+  {
+    DevQMat coef(c, s, s);
+    qgemm(c, QLRA_OP_N, QLRA_OP_N, 1.0, q0.rinv_last.v, cm.v, 0.0, coef.v);
+    qgemm(c, QLRA_OP_N, QLRA_OP_N, 1.0, q0.base.v, coef.v, 0.0, H);
+  }
   r.kappa_after = kappa;
   if (rep) *rep = r;
 }
