@@ -16,6 +16,7 @@
 // atomics.  Omega (n x s) and the Psi column slice (l x b) are generated on
 // device by K1 (embed.cu) from the reference's counter RNG.
 #include <array>
+#include <cstdio>
 #include <cstdlib>
 #include <functional>
 #include <map>
@@ -199,6 +200,17 @@ std::pair<int, int> choose_panel_splits(int64_t rp, int64_t n, int64_t s, int64_
       if (mk < best - 1e-9) { best = mk; arg = {zy, zw}; }
     }
   cache[key] = arg;
+  if (std::getenv("QLRA_DEBUG_SPLITS")) {
+    // ideal = total cost / 148 (perfect balance, no per-CTA overhead)
+    const int64_t y_tm = (rp + BM - 1) / BM, y_tn = (s + BN - 1) / BN, w_tm = (l + BM - 1) / BM,
+                  w_tn = (n + BN - 1) / BN;
+    auto frac = [](int64_t valid) { return (double)((valid + 7) / 8) / 8.0; };
+    const double yc = (double)y_tm * ((double)(s / BN) + (y_tn > s / BN ? frac(s - (s / BN) * BN) : 0.0)) * (double)n / BK;
+    const double wc = (double)w_tn * ((double)(l / BM) + (w_tm > l / BM ? frac(l - (l / BM) * BM) : 0.0)) * (double)rp / BK;
+    std::fprintf(stderr, "[qlra] panel %lldx%lld s=%lld l=%lld: zy=%d zw=%d makespan %.0f ideal %.0f (%.1f%%)\n",
+                 (long long)rp, (long long)n, (long long)s, (long long)l, arg.first, arg.second, best,
+                 (yc + wc) / 148.0, 100.0 * (yc + wc) / 148.0 / best);
+  }
   return arg;
 }
 
