@@ -117,6 +117,59 @@ std::vector<double> quat_eigs(Ctx& ctx, const QView& g, bool extremes_only = tru
   return ev;
 }
 
+// All eigenvalues of a quaternion Hermitian G computed on a side stream and
+// read back asynchronously: the host issues other work on ctx.stream and
+// collects the values with get().  G is copied on ctx.stream first, so the
+// caller may overwrite it afterwards.
+class SideEigs {
+ public:
+  SideEigs(Ctx& c, const QView& g) : c_(c), n_(g.rows) {
+    QLRA_CUDA(cudaStreamCreateWithFlags(&side_, cudaStreamNonBlocking));
+    QLRA_CUDA(cudaEventCreateWithFlags(&fork_, cudaEventDisableTiming));
+    QLRA_CUDA(cudaEventCreateWithFlags(&done_, cudaEventDisableTiming));
+    QLRA_CUDA(cudaMallocHost(&host_, sizeof(double) * (size_t)std::max<int64_t>(1, n_)));
+    work_ = DevQMat(c, n_, n_);
+    copy_qmat(c, g, work_.v);
+    QLRA_CUDA(cudaEventRecord(fork_, c.stream));
+    QLRA_CUDA(cudaStreamWaitEvent(side_, fork_, 0));
+    cudaStream_t main = c.stream;
+    c.stream = side_;  // every launch and stream-ordered buffer below lives on side_
+    try {
+      DeviceBuffer w(c, sizeof(double) * (size_t)std::max<int64_t>(1, n_));
+      QLRA_CUDA(cudaMemsetAsync(w.ptr, 0, w.bytes, c.stream));
+      small_quat_herm_eigvals(c, work_.v, w.as<double>(), /*extremes_only=*/false);
+      QLRA_CUDA(cudaMemcpyAsync(host_, w.ptr, sizeof(double) * (size_t)n_, cudaMemcpyDeviceToHost, c.stream));
+    } catch (...) {
+      c.stream = main;
+      throw;
+    }
+    c.stream = main;
+    QLRA_CUDA(cudaEventRecord(done_, side_));
+  }
+  std::vector<double> get() {
+    QLRA_CUDA(cudaEventSynchronize(done_));
+    return std::vector<double>(host_, host_ + n_);
+  }
+  ~SideEigs() {
+    if (done_) cudaStreamWaitEvent(c_.stream, done_, 0);  // work_ is released on ctx.stream
+    if (side_) cudaStreamSynchronize(side_);
+    if (host_) cudaFreeHost(host_);
+    if (fork_) cudaEventDestroy(fork_);
+    if (done_) cudaEventDestroy(done_);
+    if (side_) cudaStreamDestroy(side_);
+  }
+  SideEigs(const SideEigs&) = delete;
+  SideEigs& operator=(const SideEigs&) = delete;
+
+ private:
+  Ctx& c_;
+  int64_t n_;
+  cudaStream_t side_ = nullptr;
+  cudaEvent_t fork_ = nullptr, done_ = nullptr;
+  double* host_ = nullptr;
+  DevQMat work_;
+};
+
 double kappa_from_eigs(const std::vector<double>& ev) {
   if (ev.empty()) return std::numeric_limits<double>::infinity();
   const double lmax = ev.front(), lmin = ev.back();
@@ -397,7 +450,13 @@ void correction_from_inverse(Ctx& ctx, const QView& h, const QView& ginv, double
 // complex_bridge.cpp:80-90): P = Q R by CholeskyQR2 (shifted CholeskyQR3 if
 // needed), T = Q R^{-*} (small), X = T^* B = R^{-1} Q^* B -- one wide product.
 // Accuracy ~ u kappa(P) like a Householder solve (no normal equations).
+DevQMat lstsq_operator(Ctx& ctx, const QView& p);
 void lstsq(Ctx& ctx, const QView& p, const QView& b, const QView& x) {
+  DevQMat t = lstsq_operator(ctx, p);
+  qgemm(ctx, QLRA_OP_C, QLRA_OP_N, 1.0, t.v, b, 0.0, x);
+}
+// T (l x s) with argmin ||P X - B|| = T^* B.
+DevQMat lstsq_operator(Ctx& ctx, const QView& p) {
   const int64_t s = p.cols, l = p.rows;
   DevQMat q(ctx, l, s), rinv;
   std::vector<double> rd;
@@ -416,7 +475,7 @@ void lstsq(Ctx& ctx, const QView& p, const QView& b, const QView& x) {
          rmin > 0 ? rmax / rmin : std::numeric_limits<double>::infinity());
   DevQMat t(ctx, l, s);
   qgemm(ctx, QLRA_OP_N, QLRA_OP_C, 1.0, q.v, rinv.v, 0.0, t.v);
-  qgemm(ctx, QLRA_OP_C, QLRA_OP_N, 1.0, t.v, b, 0.0, x);
+  return t;
 }
 
 // ------------------------------------------------- rangefinders, solve ---
@@ -462,7 +521,37 @@ void pseudo_qr_dev(Ctx& c, const QView& Y, const QView& H, const qlra_pseudo_qr_
   // lambda ((1-eps) + eps / lambda)^2: kappa(H_k) after every correction step
   // follows from G_0's spectrum (exact identity; the reference recomputes it
   // from H_k, rangefinders.cpp:136, which agrees to rounding).
-  std::vector<double> lam = quat_eigs(c, g.v, /*extremes_only=*/false);
+  //
+  // G_0's spectrum is computed on a side stream while the first correction
+  // step's inverse and epsilon are computed speculatively here (almost every
+  // sketch needs that step); they are discarded if kappa_0 <= 10, and any
+  // error they raised surfaces only where the sequential order would raise it.
+  std::vector<double> lam;
+  DevQMat ginv0;
+  double eps0 = 0.0;
+  bool spec_ok = false;
+  int spec_code = 0;
+  std::string spec_msg;
+  double spec_cond = 0.0;
+  {
+    SideEigs eig(c, g.v);
+    if (cfg.max_correction_steps > 0) {
+      try {
+        ginv0 = DevQMat(c, s, s);
+        if (!hpd_inverse(c, g.v, ginv0.v, nullptr))
+          fail(QLRA_ERR_SINGULAR, "solve_quaternion_linear: singular system", std::numeric_limits<double>::infinity());
+        eps0 = estimate_epsilon_from_inverse(c, ginv0.v, cfg.power_iters_for_epsilon);
+        spec_ok = true;
+      } catch (const Status& e) {
+        // only the numerical outcomes of the sequential flow are deferred
+        if (e.code != QLRA_ERR_SINGULAR && e.code != QLRA_ERR_PARAMETER) throw;
+        spec_code = e.code;
+        spec_msg = e.what();
+        spec_cond = e.cond;
+      }
+    }
+    lam = eig.get();
+  }
   r.kappa_before = kappa_from_eigs(lam);
   double kappa = r.kappa_before;
   try {
@@ -470,9 +559,18 @@ void pseudo_qr_dev(Ctx& c, const QView& Y, const QView& H, const qlra_pseudo_qr_
       // one inverse serves estimate_epsilon and correction_step (both
       // factor the same H^*H, rangefinders.cpp:68,102)
       check_gram_rcond(kappa, 1e-15, "estimate_epsilon: H*H numerically singular");
-      if (r.correction_steps_used > 0) qgemm(c, QLRA_OP_C, QLRA_OP_N, 1.0, cm.v, cm.v, 0.0, g.v);
-      DevQMat ginv = gram_inverse(c, g.v, kappa, 1e-14, "solve_quaternion_linear: singular system");
-      const double eps = estimate_epsilon_from_inverse(c, ginv.v, cfg.power_iters_for_epsilon);
+      DevQMat ginv;
+      double eps = 0.0;
+      if (r.correction_steps_used == 0) {
+        check_gram_rcond(kappa, 1e-14, "solve_quaternion_linear: singular system");
+        if (!spec_ok) fail(spec_code, spec_msg, spec_cond);
+        ginv = std::move(ginv0);
+        eps = eps0;
+      } else {
+        qgemm(c, QLRA_OP_C, QLRA_OP_N, 1.0, cm.v, cm.v, 0.0, g.v);
+        ginv = gram_inverse(c, g.v, kappa, 1e-14, "solve_quaternion_linear: singular system");
+        eps = estimate_epsilon_from_inverse(c, ginv.v, cfg.power_iters_for_epsilon);
+      }
       if (!(eps > 0.0 && eps < 1.0))
         fail(QLRA_ERR_PARAMETER, "correction_step: epsilon must lie in (0,1)");
       // H_{k+1} = H_k ((1-eps) I + eps G_k^{-1})  (rangefinders.cpp:99-105)
@@ -518,14 +616,20 @@ void pseudo_svd_dev(Ctx& c, const QView& Y, const QView& H, uint64_t seed, qlra_
   if (rep) *rep = r;
 }
 
-void qb_solve_dev(Ctx& c, const qlra_spec_t& psi, int64_t row0, const QView& H, const QView& W, const QView& X) {
+// The core solve's operator T (l x s): X = T^* W (qb_stage_with_psi,
+// sketching.cpp:184-185: P = Psi H, X = P \ W through a QR of P).
+DevQMat qb_solve_operator(Ctx& c, const qlra_spec_t& psi, int64_t row0, const QView& H) {
   const int64_t s = H.cols, l = psi.rows;
   DevQMat ps(c, l, H.rows);
   launch_gen(c.stream, psi, 0, row0, l, H.rows, ps.v, false);
   DevQMat p(c, l, s);
   qgemm(c, QLRA_OP_N, QLRA_OP_N, 1.0, ps.v, H, 0.0, p.v);
   allreduce_qmat(c, p.v);
-  lstsq(c, p.v, W, X);
+  return lstsq_operator(c, p.v);
+}
+void qb_solve_dev(Ctx& c, const qlra_spec_t& psi, int64_t row0, const QView& H, const QView& W, const QView& X) {
+  DevQMat t = qb_solve_operator(c, psi, row0, H);
+  qgemm(c, QLRA_OP_C, QLRA_OP_N, 1.0, t.v, W, 0.0, X);
 }
 
 void check_view(const qlra_qmat_t* m, const char* who) {
@@ -936,12 +1040,22 @@ int qlra_one_pass_qb_host(qlra_ctx_t* ctx, const qlra_qmat_t* a_host, int64_t ro
         QLRA_CUDA(cudaMemcpy2DAsync(hv.p[p], sizeof(double) * hv.ld, h.v.p[p], sizeof(double) * h.v.ld,
                                     sizeof(double) * s, (size_t)rows, cudaMemcpyDeviceToHost, side));
     }
+    // X = T^* W in column blocks; each block is copied back on the side
+    // stream while the next one is computed
+    DevQMat t = qb_solve_operator(c, *psi, row0, h.v);
+    const int64_t nblk = n >= 2048 ? 4 : 1;
+    const int64_t bw = (n + nblk - 1) / nblk;
+    for (int64_t j0 = 0; j0 < n; j0 += bw) {
+      const int64_t nj = std::min(bw, n - j0);
+      qgemm(c, QLRA_OP_C, QLRA_OP_N, 1.0, t.v, sub(w.v, 0, j0, l, nj), 0.0, sub(x.v, 0, j0, s, nj));
+      QLRA_CUDA(cudaEventRecord(ready, c.stream));
+      QLRA_CUDA(cudaStreamWaitEvent(side, ready, 0));
+      for (int p = 0; p < 4; ++p)
+        QLRA_CUDA(cudaMemcpy2DAsync(xv.p[p] + j0, sizeof(double) * xv.ld, x.v.p[p] + j0, sizeof(double) * x.v.ld,
+                                    sizeof(double) * nj, (size_t)s, cudaMemcpyDeviceToHost, side));
+    }
     QLRA_CUDA(cudaEventRecord(copied, side));
-    qb_solve_dev(c, *psi, row0, h.v, w.v, x.v);
-    for (int p = 0; p < 4; ++p)
-      QLRA_CUDA(cudaMemcpy2DAsync(xv.p[p], sizeof(double) * xv.ld, x.v.p[p], sizeof(double) * x.v.ld,
-                                  sizeof(double) * n, (size_t)s, cudaMemcpyDeviceToHost, c.stream));
-    // h's device buffer is released on c.stream: order it after the copy
+    // device buffers are released on c.stream: order that after the copies
     QLRA_CUDA(cudaStreamWaitEvent(c.stream, copied, 0));
     QLRA_CUDA(cudaStreamSynchronize(c.stream));
     cudaEventDestroy(ready);

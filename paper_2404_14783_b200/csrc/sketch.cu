@@ -358,12 +358,9 @@ void sketch_update_rows_host(Ctx& ctx, const qlra_spec_t& omega, const qlra_spec
   const int64_t b = host_block.rows, n = host_block.cols, s = omega.cols, l = psi.rows;
   if (b == 0 || n == 0) return;
   set_kernel_attrs();
-  DevQMat om(ctx, n, s);
-  launch_gen(ctx.stream, omega, 0, 0, n, s, om.v, false);
-  DevQMat ps(ctx, l, b);
-  launch_gen(ctx.stream, psi, 0, row0, l, b, ps.v, false);
   int64_t R = block_rows > 0 ? block_rows : stream_rows(n, b);
   R = std::min(R, b);
+  DevQMat om(ctx, n, s), ps(ctx, l, b);
   DevQMat buf[2] = {DevQMat(ctx, R, n), DevQMat(ctx, R, n)};
   cudaStream_t cs;
   QLRA_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
@@ -372,13 +369,22 @@ void sketch_update_rows_host(Ctx& ctx, const qlra_spec_t& omega, const qlra_spec
     QLRA_CUDA(cudaEventCreateWithFlags(&copied[i], cudaEventDisableTiming));
     QLRA_CUDA(cudaEventCreateWithFlags(&freed[i], cudaEventDisableTiming));
   }
-  // buffers were allocated on ctx.stream: make the copy stream wait for that
+  // the buffers were allocated on ctx.stream: the copy stream waits for
+  // that, and only that -- Omega / Psi generation below overlaps the first
+  // H2D chunk
   QLRA_CUDA(cudaEventRecord(freed[0], ctx.stream));
   QLRA_CUDA(cudaEventRecord(freed[1], ctx.stream));
+  launch_gen(ctx.stream, omega, 0, 0, n, s, om.v, false);
+  launch_gen(ctx.stream, psi, 0, row0, l, b, ps.v, false);
   SketchWork ws;
+  // The last R rows go in quarter-size chunks: the sketch of the final chunk
+  // is the one part of the pipeline nothing overlaps (the copy stream is the
+  // bottleneck before it), so it should be short.
+  const int64_t tail_start = b > 2 * R ? b - R : b;
+  const int64_t Rt = std::max<int64_t>(64, ((R / 4 + 63) / 64) * 64);
   int idx = 0;
-  for (int64_t r0 = 0; r0 < b; r0 += R, idx ^= 1) {
-    const int64_t rp = std::min(R, b - r0);
+  for (int64_t r0 = 0, rp = 0; r0 < b; r0 += rp, idx ^= 1) {
+    rp = std::min(r0 >= tail_start ? Rt : std::min(R, tail_start - r0), b - r0);
     const QView dst = sub(buf[idx].v, 0, 0, rp, n);
     QLRA_CUDA(cudaStreamWaitEvent(cs, freed[idx], 0));
     for (int p = 0; p < 4; ++p) {
