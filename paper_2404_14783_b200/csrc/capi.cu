@@ -124,10 +124,19 @@ std::vector<double> quat_eigs(Ctx& ctx, const QView& g, bool extremes_only = tru
 class SideEigs {
  public:
   SideEigs(Ctx& c, const QView& g) : c_(c), n_(g.rows) {
-    QLRA_CUDA(cudaStreamCreateWithFlags(&side_, cudaStreamNonBlocking));
+    if (!c.side) QLRA_CUDA(cudaStreamCreateWithFlags(&c.side, cudaStreamNonBlocking));
+    side_ = c.side;
+    const size_t need = (size_t)std::max<int64_t>(1, n_);
+    if (c.side_pinned_n < need) {
+      if (c.side_pinned) QLRA_CUDA(cudaFreeHost(c.side_pinned));
+      c.side_pinned = nullptr;
+      c.side_pinned_n = 0;
+      QLRA_CUDA(cudaMallocHost(&c.side_pinned, sizeof(double) * std::max<size_t>(need, 1024)));
+      c.side_pinned_n = std::max<size_t>(need, 1024);
+    }
+    host_ = c.side_pinned;
     QLRA_CUDA(cudaEventCreateWithFlags(&fork_, cudaEventDisableTiming));
     QLRA_CUDA(cudaEventCreateWithFlags(&done_, cudaEventDisableTiming));
-    QLRA_CUDA(cudaMallocHost(&host_, sizeof(double) * (size_t)std::max<int64_t>(1, n_)));
     work_ = DevQMat(c, n_, n_);
     copy_qmat(c, g, work_.v);
     QLRA_CUDA(cudaEventRecord(fork_, c.stream));
@@ -152,11 +161,9 @@ class SideEigs {
   }
   ~SideEigs() {
     if (done_) cudaStreamWaitEvent(c_.stream, done_, 0);  // work_ is released on ctx.stream
-    if (side_) cudaStreamSynchronize(side_);
-    if (host_) cudaFreeHost(host_);
+    if (done_) cudaEventSynchronize(done_);                // the pinned buffer is reused
     if (fork_) cudaEventDestroy(fork_);
     if (done_) cudaEventDestroy(done_);
-    if (side_) cudaStreamDestroy(side_);
   }
   SideEigs(const SideEigs&) = delete;
   SideEigs& operator=(const SideEigs&) = delete;
@@ -256,9 +263,63 @@ void chain_rinv(Ctx& ctx, DevQMat& rinv, const QView& next) {
 // defer (optional): do not form Q in the last pass; return its input and
 // R^{-1} instead (Q = defer->base * defer->rinv_last), so a caller that only
 // needs Q times a small matrix saves one tall product.
+bool cholesky_qr_general(Ctx& ctx, const QView& y, const QView& h, bool complex_mode, int64_t m_global,
+                         std::vector<double>* rdiag, bool distributed, DevQMat* rinv, DevQMat* rfac,
+                         DeferredQ* defer);
+
+// CholeskyQR2 with both passes queued back to back and ONE host sync for
+// both pass statuses and diagonals (s <= the single-launch Cholesky limit);
+// a breakdown of pass 1 falls back to the general path (shifted CholeskyQR3).
 bool cholesky_qr(Ctx& ctx, const QView& y, const QView& h, bool complex_mode, int64_t m_global,
                  std::vector<double>* rdiag, bool distributed = true, DevQMat* rinv = nullptr,
                  DevQMat* rfac = nullptr, DeferredQ* defer = nullptr) {
+  const int64_t s = y.cols;
+  if (s == 0 || s > chol_inv_async_max())
+    return cholesky_qr_general(ctx, y, h, complex_mode, m_global, rdiag, distributed, rinv, rfac, defer);
+  DevQMat g1(ctx, s, s), g2(ctx, s, s), t1(ctx, y.rows, s);
+  DevQMat r1(ctx, s, s), r2(ctx, s, s), r1inv(ctx, s, s), r2inv(ctx, s, s);
+  DeviceBuffer info(ctx, 2 * sizeof(int)), dg(ctx, 2 * sizeof(double) * (size_t)s);
+  auto gram_of = [&](const QView& a, const QView& g) {
+    if (distributed) gram(ctx, a, g);
+    else qgemm(ctx, QLRA_OP_C, QLRA_OP_N, 1.0, a, a, 0.0, g);
+    if (complex_mode) zero_jk_planes(ctx, g);
+  };
+  gram_of(y, g1.v);
+  chol_inv_launch(ctx, g1.v, r1.v, r1inv.v, info.as<int>(), dg.as<double>());
+  qgemm(ctx, QLRA_OP_N, QLRA_OP_N, 1.0, y, r1inv.v, 0.0, t1.v);
+  gram_of(t1.v, g2.v);
+  chol_inv_launch(ctx, g2.v, r2.v, r2inv.v, info.as<int>() + 1, dg.as<double>() + s);
+  if (!defer) qgemm(ctx, QLRA_OP_N, QLRA_OP_N, 1.0, t1.v, r2inv.v, 0.0, h);
+  int inf[2] = {0, 0};
+  std::vector<double> d((size_t)(2 * s));
+  QLRA_CUDA(cudaMemcpyAsync(inf, info.ptr, 2 * sizeof(int), cudaMemcpyDeviceToHost, ctx.stream));
+  QLRA_CUDA(cudaMemcpyAsync(d.data(), dg.ptr, 2 * sizeof(double) * (size_t)s, cudaMemcpyDeviceToHost, ctx.stream));
+  QLRA_CUDA(cudaStreamSynchronize(ctx.stream));
+  if (inf[0] != 0)  // pass 1 broke down: shifted CholeskyQR3
+    return cholesky_qr_general(ctx, y, h, complex_mode, m_global, rdiag, distributed, rinv, rfac, defer);
+  if (inf[1] != 0) return false;
+  if (rdiag) {
+    rdiag->resize((size_t)s);
+    for (int64_t k = 0; k < s; ++k) (*rdiag)[k] = d[k] * d[s + k];
+  }
+  if (rinv) {
+    *rinv = std::move(r1inv);
+    chain_rinv(ctx, *rinv, r2inv.v);
+  }
+  if (rfac) {
+    *rfac = std::move(r1);
+    chain_r(ctx, *rfac, r2.v);
+  }
+  if (defer) {
+    defer->base = std::move(t1);
+    defer->rinv_last = std::move(r2inv);
+  }
+  return true;
+}
+
+bool cholesky_qr_general(Ctx& ctx, const QView& y, const QView& h, bool complex_mode, int64_t m_global,
+                         std::vector<double>* rdiag, bool distributed, DevQMat* rinv, DevQMat* rfac,
+                         DeferredQ* defer) {
   const int64_t s = y.cols;
   DevQMat t1(ctx, y.rows, s);
   QView hq = h;
@@ -716,6 +777,11 @@ int qlra_ctx_destroy(qlra_ctx_t* ctx) {
   if (ctx->c.own_stream && ctx->c.stream) cudaStreamDestroy(ctx->c.stream);
   if (ctx->c.pinned) cudaFreeHost(ctx->c.pinned);
   if (ctx->c.tile_cnt) cudaFree(ctx->c.tile_cnt);
+  if (ctx->c.side) {
+    cudaStreamSynchronize(ctx->c.side);
+    cudaStreamDestroy(ctx->c.side);
+  }
+  if (ctx->c.side_pinned) cudaFreeHost(ctx->c.side_pinned);
   delete ctx;
   return QLRA_OK;
 }

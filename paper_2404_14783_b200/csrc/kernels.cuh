@@ -32,6 +32,11 @@ struct Ctx {
   // the last CTA of a tile sets its counter back to 0)
   unsigned* tile_cnt = nullptr;
   int64_t tile_cnt_n = 0;
+  // side stream for overlapped small work, and its pinned read-back buffer
+  // (created on first use, kept for the context's lifetime)
+  cudaStream_t side = nullptr;
+  double* side_pinned = nullptr;
+  size_t side_pinned_n = 0;
   // Optional per-launch timing of the fused sketch kernel (bench evidence):
   // CUDA events bracket every launch on the launching stream.
   struct KernelTimer {
@@ -169,6 +174,11 @@ void qsvd_phase(Ctx& ctx, const QView& u, const QView& v);
 // numerically PD.
 bool blocked_chol_inv(Ctx& ctx, const QView& g, const QView& rinv, std::vector<double>* rdiag,
                       const QView* r_out = nullptr);
+// Single-launch cluster Cholesky+inverse for s <= chol_inv_async_max(), no
+// host sync: *d_info = 0 or the first failing column (1-based); r may be a
+// workspace (R is written there); d_rdiag = diag(R).
+int64_t chol_inv_async_max();
+void chol_inv_launch(Ctx& ctx, const QView& g, const QView& r, const QView& rinv, int* d_info, double* d_rdiag);
 // zero the j, k planes (restrict a quaternion matrix to its complex part)
 void zero_jk_planes(Ctx& ctx, const QView& g);
 // Quaternion Cholesky G = R^*R in place (upper triangle), *d_info as above.

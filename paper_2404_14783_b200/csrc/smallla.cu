@@ -1843,6 +1843,25 @@ void qsvd_phase(Ctx& ctx, const QView& u, const QView& v) {
 // R_12 = R_11^{-*} G_12 and trailing updates G_22 -= R_12^* R_12 run on the
 // DMMA GEMM, and R^{-1} follows by block back-substitution
 // X_{i, i+1:} = -R_ii^{-1} (R_{i, i+1:} X_{i+1:, i+1:}).
+int64_t chol_inv_async_max() { return CHC_MAX; }
+
+// One launch of the cluster Cholesky+inverse (s <= CHC_MAX), no host sync:
+// *d_info = 0 or the first failing column (1-based), d_rdiag = diag(R).
+void chol_inv_launch(Ctx& ctx, const QView& g, const QView& r, const QView& rinv, int* d_info, double* d_rdiag) {
+  const int64_t s = g.rows;
+  CholArgs a{g, r, rinv, d_rdiag, d_info};
+  const int64_t nbt = (s + CTB - 1) / CTB;
+  const size_t csm = sizeof(Tile) * (size_t)(nbt + CHB + 3);
+  static size_t cattr = 0;
+  if (csm > 48 * 1024 && csm > cattr) {
+    QLRA_CUDA(cudaFuncSetAttribute(k_chol_inv_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm));
+    cattr = csm;
+  }
+  k_chol_inv_cluster<<<CHC, 256, csm, ctx.stream>>>(a);
+  QLRA_LAUNCH_CHECK();
+  count_launch();
+}
+
 bool blocked_chol_inv(Ctx& ctx, const QView& g, const QView& rinv, std::vector<double>* rdiag,
                       const QView* r_out) {
   const int64_t s = g.rows;
@@ -1858,17 +1877,7 @@ bool blocked_chol_inv(Ctx& ctx, const QView& g, const QView& rinv, std::vector<d
     }
     DeviceBuffer info(ctx, sizeof(int));
     DeviceBuffer dg(ctx, sizeof(double) * (size_t)s);
-    CholArgs a{g, rv, rinv, dg.as<double>(), info.as<int>()};
-    const int64_t nbt = (s + CTB - 1) / CTB;
-    const size_t csm = sizeof(Tile) * (size_t)(nbt + CHB + 3);
-    static size_t cattr = 0;
-    if (csm > 48 * 1024 && csm > cattr) {
-      QLRA_CUDA(cudaFuncSetAttribute(k_chol_inv_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm));
-      cattr = csm;
-    }
-    k_chol_inv_cluster<<<CHC, 256, csm, ctx.stream>>>(a);
-    QLRA_LAUNCH_CHECK();
-    count_launch();
+    chol_inv_launch(ctx, g, rv, rinv, info.as<int>(), dg.as<double>());
     int inf = 0;
     QLRA_CUDA(cudaMemcpyAsync(&inf, info.ptr, sizeof(int), cudaMemcpyDeviceToHost, ctx.stream));
     QLRA_CUDA(cudaStreamSynchronize(ctx.stream));
