@@ -270,9 +270,11 @@ bool cholesky_qr_general(Ctx& ctx, const QView& y, const QView& h, bool complex_
 // CholeskyQR2 with both passes queued back to back and ONE host sync for
 // both pass statuses and diagonals (s <= the single-launch Cholesky limit);
 // a breakdown of pass 1 falls back to the general path (shifted CholeskyQR3).
+// gram1 (optional): the already reduced Gram of y (quaternion; the complex
+// part is taken here when complex_mode), saving the first tall product.
 bool cholesky_qr(Ctx& ctx, const QView& y, const QView& h, bool complex_mode, int64_t m_global,
                  std::vector<double>* rdiag, bool distributed = true, DevQMat* rinv = nullptr,
-                 DevQMat* rfac = nullptr, DeferredQ* defer = nullptr) {
+                 DevQMat* rfac = nullptr, DeferredQ* defer = nullptr, const QView* gram1 = nullptr) {
   const int64_t s = y.cols;
   if (s == 0 || s > chol_inv_async_max())
     return cholesky_qr_general(ctx, y, h, complex_mode, m_global, rdiag, distributed, rinv, rfac, defer);
@@ -284,7 +286,12 @@ bool cholesky_qr(Ctx& ctx, const QView& y, const QView& h, bool complex_mode, in
     else qgemm(ctx, QLRA_OP_C, QLRA_OP_N, 1.0, a, a, 0.0, g);
     if (complex_mode) zero_jk_planes(ctx, g);
   };
-  gram_of(y, g1.v);
+  if (gram1) {
+    copy_qmat(ctx, *gram1, g1.v);
+    if (complex_mode) zero_jk_planes(ctx, g1.v);
+  } else {
+    gram_of(y, g1.v);
+  }
   chol_inv_launch(ctx, g1.v, r1.v, r1inv.v, info.as<int>(), dg.as<double>());
   qgemm(ctx, QLRA_OP_N, QLRA_OP_N, 1.0, y, r1inv.v, 0.0, t1.v);
   gram_of(t1.v, g2.v);
@@ -668,10 +675,21 @@ void pseudo_svd_dev(Ctx& c, const QView& Y, const QView& H, uint64_t seed, qlra_
   if (m <= s) fail(QLRA_ERR_PARAMETER, "pseudo_svd: sketch must be tall (rows > cols)");
   qlra_rangefinder_report_t r{};
   r.method = QLRA_PSEUDO_SVD;
-  r.kappa_before = condition_number_dev(c, Y);
   // Full-rank sketches: quaternion CholeskyQR2 (shifted CholeskyQR3 when
   // needed).  Rank-deficient ones: eigen route + orthonormal completion.
-  if (!std::isfinite(r.kappa_before) || !cholesky_qr(c, Y, H, /*complex_mode=*/false, m, nullptr))
+  // kappa(Y) comes from the eigenvalues of the same Gram CholeskyQR2 starts
+  // from, computed on the side stream while CholeskyQR2 runs; a non-finite
+  // kappa routes to the rank-deficient path as before.
+  DevQMat g(c, s, s);
+  gram(c, Y, g.v);
+  bool qr_ok = false;
+  {
+    SideEigs eig(c, g.v);
+    qr_ok = cholesky_qr(c, Y, H, /*complex_mode=*/false, m, nullptr, /*distributed=*/true, nullptr, nullptr,
+                        nullptr, &g.v);
+    r.kappa_before = kappa_from_eigs(eig.get());
+  }
+  if (!std::isfinite(r.kappa_before) || !qr_ok)
     pseudo_svd_rank_deficient(c, Y, H, m, global_row0(c, Y.rows), seed);
   r.kappa_after = condition_number_dev(c, H);
   if (rep) *rep = r;
