@@ -9,6 +9,7 @@
 #include <nccl.h>
 
 #include <cmath>
+#include <memory>
 #include <cstring>
 #include <limits>
 #include <vector>
@@ -669,7 +670,10 @@ void pseudo_qr_dev(Ctx& c, const QView& Y, const QView& H, const qlra_pseudo_qr_
   if (rep) *rep = r;
 }
 
-void pseudo_svd_dev(Ctx& c, const QView& Y, const QView& H, uint64_t seed, qlra_rangefinder_report_t* rep) {
+// kappa_after_async (optional): leave kappa(H) to the caller as a pending
+// side-stream eigenvalue computation instead of waiting for it here.
+void pseudo_svd_dev(Ctx& c, const QView& Y, const QView& H, uint64_t seed, qlra_rangefinder_report_t* rep,
+                    std::unique_ptr<SideEigs>* kappa_after_async = nullptr) {
   const int64_t s = Y.cols;
   const int64_t m = global_rows(c, Y.rows);
   if (m <= s) fail(QLRA_ERR_PARAMETER, "pseudo_svd: sketch must be tall (rows > cols)");
@@ -691,7 +695,14 @@ void pseudo_svd_dev(Ctx& c, const QView& Y, const QView& H, uint64_t seed, qlra_
   }
   if (!std::isfinite(r.kappa_before) || !qr_ok)
     pseudo_svd_rank_deficient(c, Y, H, m, global_row0(c, Y.rows), seed);
-  r.kappa_after = condition_number_dev(c, H);
+  if (kappa_after_async) {
+    // the caller overlaps kappa(H)'s eigenvalues with its next work
+    DevQMat gh(c, s, s);
+    gram(c, H, gh.v);
+    kappa_after_async->reset(new SideEigs(c, gh.v));
+  } else {
+    r.kappa_after = condition_number_dev(c, H);
+  }
   if (rep) *rep = r;
 }
 
@@ -1105,8 +1116,10 @@ int qlra_one_pass_qb_host(qlra_ctx_t* ctx, const qlra_qmat_t* a_host, int64_t ro
     w.zero(c);
     sketch_update_rows_host(c, *omega, *psi, row0, view_of(a_host), y.v, w.v, block_rows);
     allreduce_qmat(c, w.v);
-    if (method == QLRA_PSEUDO_QR) pseudo_qr_dev(c, y.v, h.v, cfg, rep);
-    else pseudo_svd_dev(c, y.v, h.v, rangefinder_seed, rep);
+    std::unique_ptr<SideEigs> kappa_after;  // pseudo-SVD: kappa(H) overlapped with the solve
+    qlra_rangefinder_report_t rr{};
+    if (method == QLRA_PSEUDO_QR) pseudo_qr_dev(c, y.v, h.v, cfg, &rr);
+    else pseudo_svd_dev(c, y.v, h.v, rangefinder_seed, &rr, &kappa_after);
     // H is final: copy it back on a side stream while the solve runs
     cudaStream_t side = nullptr;
     cudaEvent_t ready = nullptr, copied = nullptr;
@@ -1139,6 +1152,11 @@ int qlra_one_pass_qb_host(qlra_ctx_t* ctx, const qlra_qmat_t* a_host, int64_t ro
                                     sizeof(double) * nj, (size_t)s, cudaMemcpyDeviceToHost, side));
     }
     QLRA_CUDA(cudaEventRecord(copied, side));
+    if (kappa_after) {
+      rr.kappa_after = kappa_from_eigs(kappa_after->get());
+      kappa_after.reset();
+    }
+    if (rep) *rep = rr;
     // device buffers are released on c.stream: order that after the copies
     QLRA_CUDA(cudaStreamWaitEvent(c.stream, copied, 0));
     QLRA_CUDA(cudaStreamSynchronize(c.stream));
