@@ -173,38 +173,74 @@ __device__ __forceinline__ void kstep(const double* As, const double* Bs, int wr
   }
 }
 
-// The cp.async ring and the k loop for one (NRB, NCB) instance.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "QT_WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra QT_WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+// arrive on `bar` once all of this thread's earlier cp.async copies landed
+__device__ __forceinline__ void cp_async_arrive(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// The cp.async ring and the k loop for one (NRB, NCB) instance.  Stage
+// handoff by mbarriers instead of a CTA barrier per stage: each thread's
+// copies of stage k arrive on full[k % S] when they land; each warp arrives
+// on empty[k % S] when it has read stage k.  Prefetch distance 1 over S = 3
+// slots: refilling a slot waits only for the consumption two stages back,
+// so warps drift up to two stages apart instead of meeting every stage.
 template <bool CA, bool CB, int NRB, int NCB>
 __device__ __forceinline__ void mma_loop(const Operands& g, double* smem, int64_t i0, int64_t j0,
-                                         int64_t kbeg, int64_t kend, Acc& acc) {
+                                         int64_t kbeg, int64_t kend, Acc& acc, uint64_t* full, uint64_t* empty) {
   constexpr bool AK = !CA, BJ = !CB;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int wr = w >> 2, wc = w & 3;
   const int gid = lane >> 2, tig = lane & 3;
   const int nk = kend > kbeg ? (int)((kend - kbeg + BK - 1) / BK) : 0;
+  if (tid == 0) {
 #pragma unroll
-  for (int s = 0; s < STAGES - 1; ++s) {
-    if (s < nk)
-      load_stage<AK, BJ>(g, smem + s * STAGE, smem + s * STAGE + OP_STAGE, i0, j0, kbeg + s * BK, kend, tid);
-    cp_async_commit();
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], NT);
+      mbar_init(&empty[s], NT / 32);
+    }
+  }
+  __syncthreads();
+  if (nk > 0) {
+    load_stage<AK, BJ>(g, smem, smem + OP_STAGE, i0, j0, kbeg, kend, tid);
+    cp_async_arrive(&full[0]);
   }
   for (int kt = 0; kt < nk; ++kt) {
-    cp_async_wait<STAGES - 2>();
-    __syncthreads();
-    {
-      const int nxt = kt + STAGES - 1;
-      if (nxt < nk) {
-        const int s = nxt % STAGES;
-        load_stage<AK, BJ>(g, smem + s * STAGE, smem + s * STAGE + OP_STAGE, i0, j0,
-                           kbeg + (int64_t)nxt * BK, kend, tid);
-      }
-      cp_async_commit();
+    const int s = kt % STAGES;
+    const int nxt = kt + 1;
+    if (nxt < nk) {
+      const int sn = nxt % STAGES;
+      if (nxt >= STAGES) mbar_wait_parity(&empty[sn], (unsigned)((nxt / STAGES - 1) & 1));
+      load_stage<AK, BJ>(g, smem + sn * STAGE, smem + sn * STAGE + OP_STAGE, i0, j0,
+                         kbeg + (int64_t)nxt * BK, kend, tid);
+      cp_async_arrive(&full[sn]);
     }
-    const double* As = smem + (kt % STAGES) * STAGE;
+    mbar_wait_parity(&full[s], (unsigned)((kt / STAGES) & 1));
+    const double* As = smem + s * STAGE;
     const double* Bs = As + OP_STAGE;
     if (NRB > 0 && NCB > 0) kstep<CA, CB, AK, BJ, (NRB > 0 ? NRB : 1), (NCB > 0 ? NCB : 1)>(As, Bs, wr, wc, gid, tig, acc);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
   }
   cp_async_wait<0>();
+  __syncthreads();  // the ring (and the barriers) may be reused by the caller
 }
 
 // acc += op(A) op(B) over k in [kbeg, kend).  CA/CB: op = adjoint, which
@@ -216,16 +252,19 @@ __device__ __forceinline__ void mma_loop(const Operands& g, double* smem, int64_
 template <bool CA, bool CB>
 __device__ __forceinline__ void mma_tile(const Operands& g, double* smem, int64_t i0, int64_t j0,
                                          int64_t kbeg, int64_t kend, Acc& acc) {
+  // stage barriers shared by every warp of the CTA, whichever loop instance
+  // it runs
+  __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES];
   const int w = threadIdx.x >> 5;
   const int64_t r0w = i0 + 16 * (w >> 2), c0w = j0 + 16 * (w & 3);
   const int nrb = r0w >= g.M ? 0 : r0w + 8 >= g.M ? 1 : 2;
   const int ncb = c0w >= g.N ? 0 : c0w + 8 >= g.N ? 1 : 2;
   switch (nrb * 4 + ncb) {
-    case 2 * 4 + 2: mma_loop<CA, CB, 2, 2>(g, smem, i0, j0, kbeg, kend, acc); break;
-    case 2 * 4 + 1: mma_loop<CA, CB, 2, 1>(g, smem, i0, j0, kbeg, kend, acc); break;
-    case 1 * 4 + 2: mma_loop<CA, CB, 1, 2>(g, smem, i0, j0, kbeg, kend, acc); break;
-    case 1 * 4 + 1: mma_loop<CA, CB, 1, 1>(g, smem, i0, j0, kbeg, kend, acc); break;
-    default: mma_loop<CA, CB, 0, 0>(g, smem, i0, j0, kbeg, kend, acc); break;  // loads + barriers only
+    case 2 * 4 + 2: mma_loop<CA, CB, 2, 2>(g, smem, i0, j0, kbeg, kend, acc, full, empty); break;
+    case 2 * 4 + 1: mma_loop<CA, CB, 2, 1>(g, smem, i0, j0, kbeg, kend, acc, full, empty); break;
+    case 1 * 4 + 2: mma_loop<CA, CB, 1, 2>(g, smem, i0, j0, kbeg, kend, acc, full, empty); break;
+    case 1 * 4 + 1: mma_loop<CA, CB, 1, 1>(g, smem, i0, j0, kbeg, kend, acc, full, empty); break;
+    default: mma_loop<CA, CB, 0, 0>(g, smem, i0, j0, kbeg, kend, acc, full, empty); break;  // loads + barriers only
   }
 }
 
