@@ -26,7 +26,7 @@
 namespace qlra_dev {
 namespace qt {
 
-constexpr int BM = 64, BN = 64, BK = 8, NT = 512, STAGES = 3;
+constexpr int BM = 64, BN = 64, BK = 8, NT = 512, STAGES = 4;
 constexpr int WRB = 2, WCB = 2;  // 8x8 blocks per warp (warp tile 16x16, 4x4 warps)
 constexpr int LDK = BK + 4;    // k-fast rows: [x][k]
 constexpr int LDX = BM + 4;    // i/j-fast rows: [k][x]
