@@ -247,8 +247,10 @@ int qlra_sketch_from_qmat_file(qlra_ctx_t* ctx, const char* path, const qlra_spe
                                int64_t block_rows);
 
 /* ---------------------------------------------------------- diagnostics --- */
-/* Measured FP64 throughput of this GPU: mode 0 = DFMA, 1 = DMMA (m8n8k4).
- * Runs ~`ms` milliseconds; syncs. */
+/* Measured FP64 throughput of this GPU: mode 0 = DFMA, 1 = DMMA (m8n8k4),
+ * 2 = half the warps DMMA and half DFMA (pipe-sharing probe: on B200 it lands
+ * between the two, 35.0 TF/s, so the FP64 CUDA-core and tensor paths share one
+ * pipe).  Runs ~`ms` milliseconds; syncs. */
 int qlra_measure_fp64_peak(qlra_ctx_t* ctx, int mode, double ms, double* tflops);
 /* Name of the kernel variant the sketch uses for the given shape. */
 const char* qlra_sketch_kernel_name(void);
