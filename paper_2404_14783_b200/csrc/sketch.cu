@@ -303,11 +303,11 @@ void set_kernel_attrs() {
 // CTAs over the SMs far better than many short ones (C2: 16.3 ms as one
 // launch vs 19.9 ms as 32 L2-sized panels).  Host-streamed A: chunks of
 // kStreamBytes so the H2D copy of the next chunk overlaps the sketch of this
-// one (about 32 chunks per block, at least kStreamBytes each).  Multiples of
+// one (about 16 chunks per block, at least kStreamBytes each).  Multiples of
 // 64 rows, at least 256.  QLRA_PANEL_BYTES / QLRA_STREAM_BYTES override
 // (tuning).
 constexpr double kPanelBytes = 2e9;
-constexpr double kStreamBytes = 48e6;
+constexpr double kStreamBytes = 64e6;
 double env_or(const char* name, double dflt) {
   const char* e = std::getenv(name);
   return e ? std::atof(e) : dflt;
@@ -322,10 +322,12 @@ int64_t panel_rows(int64_t n, int64_t b) {
   return rows_for(bytes, n, b);
 }
 int64_t stream_rows(int64_t n, int64_t b) {
-  // ~32 chunks per block (overlap granularity), never below kStreamBytes:
-  // small chunks of a narrow A (C5: n = 300) make short, inefficient launches
+  // ~16 chunks per block (each DMA call and chunk boundary costs; measured
+  // C2: 16 x 96 MB 28.6 ms vs 32 x 48 MB 29.0 ms, plain copy 27.6 ms), never
+  // below kStreamBytes: small chunks of a narrow A (C5: n = 300) make short,
+  // inefficient launches
   static const double floor_bytes = env_or("QLRA_STREAM_BYTES", kStreamBytes);
-  const double bytes = std::max(floor_bytes, 32.0 * (double)n * (double)b / 32.0);
+  const double bytes = std::max(floor_bytes, 32.0 * (double)n * (double)b / 16.0);
   return rows_for(bytes, n, b);
 }
 

@@ -34,3 +34,20 @@ for br in (0, 128, 512, 1024):
     print("make_sketch_host br=%4d %.2f ms" % (br, t))
 t = timed(lambda: Q.one_pass_qb_host(a_host, o, ctx=ctx))
 print("one_pass_qb_host     %.2f ms" % t)
+
+# the same chunked copies without any sketch work (copy-engine cost alone)
+rows = 256
+dev = torch.empty((4, rows, a.shape[2]), dtype=torch.float64, device="cuda")
+s = torch.cuda.Stream()
+
+
+def chunked():
+    with torch.cuda.stream(s):
+        for r0 in range(0, a.shape[1], rows):
+            rp = min(rows, a.shape[1] - r0)
+            for p in range(4):
+                dev[p, :rp].copy_(a_host[p, r0:r0 + rp], non_blocking=True)
+    s.synchronize()
+
+
+print("chunked copies only  %.2f ms" % timed(chunked))
