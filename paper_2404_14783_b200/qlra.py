@@ -667,6 +667,24 @@ def one_pass_approx(a, opts: OnePassOptions, ctx=None) -> ApproxResult:
     return res
 
 
+def one_pass_approx_from_sketch(state: SketchState, opts: OnePassOptions, ctx=None) -> ApproxResult:
+    """one_pass_approx(const SketchState&, opts) (sketching.cpp:220-246,
+    run_pipeline): QB stage + truncation from a sketch; A is never touched, so
+    the residual diagnostics are absent."""
+    ctx = _ctx(ctx)
+    o = resolve_defaults(opts)
+    qb = qb_stage(state, o.rangefinder, o.rangefinder_seed, o.qr_cfg, ctx)
+    t0 = time.perf_counter()
+    res = truncate_stage(qb.h, qb.x, o.r, ctx)
+    ctx.synchronize()
+    res.diagnostics = dict(kappa_h=qb.report.kappa_after, kappa_before=qb.report.kappa_before,
+                           correction_steps=qb.report.correction_steps_used, qb_residual=None,
+                           relative_error=None,
+                           times=dict(sketch_s=0.0, rangefinder_s=qb.rangefinder_s, solve_s=qb.solve_s,
+                                      truncate_s=time.perf_counter() - t0))
+    return res
+
+
 # ------------------------------------------------------- checkpoint I/O ---
 def write_qmat(path, m, ctx=None):
     """write_qmat (io.cpp:77-88): QMAT1 file from a device QMatrix."""
