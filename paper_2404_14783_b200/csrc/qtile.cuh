@@ -199,9 +199,9 @@ __device__ __forceinline__ void cp_async_arrive(uint64_t* bar) {
 // The cp.async ring and the k loop for one (NRB, NCB) instance.  Stage
 // handoff by mbarriers instead of a CTA barrier per stage: each thread's
 // copies of stage k arrive on full[k % S] when they land; each warp arrives
-// on empty[k % S] when it has read stage k.  Prefetch distance 1 over S = 3
-// slots: refilling a slot waits only for the consumption two stages back,
-// so warps drift up to two stages apart instead of meeting every stage.
+// on empty[k % S] when it has read stage k.  Prefetch distance 1 over S = 4
+// slots: refilling a slot waits only for the consumption three stages back,
+// so warps drift up to three stages apart instead of meeting every stage.
 template <bool CA, bool CB, int NRB, int NCB>
 __device__ __forceinline__ void mma_loop(const Operands& g, double* smem, int64_t i0, int64_t j0,
                                          int64_t kbeg, int64_t kend, Acc& acc, uint64_t* full, uint64_t* empty) {
@@ -218,13 +218,20 @@ __device__ __forceinline__ void mma_loop(const Operands& g, double* smem, int64_
     }
   }
   __syncthreads();
-  if (nk > 0) {
-    load_stage<AK, BJ>(g, smem, smem + OP_STAGE, i0, j0, kbeg, kend, tid);
-    cp_async_arrive(&full[0]);
-  }
+  // prefetch distance 1: a refill waits only for the consumption STAGES - 1
+  // stages back (measured: distance 2 is slower -- the waits are on slow
+  // warps, not on data)
+  constexpr int PF = 1;
+#pragma unroll
+  for (int p = 0; p < PF; ++p)
+    if (p < nk) {
+      load_stage<AK, BJ>(g, smem + p * STAGE, smem + p * STAGE + OP_STAGE, i0, j0, kbeg + (int64_t)p * BK, kend,
+                         tid);
+      cp_async_arrive(&full[p]);
+    }
   for (int kt = 0; kt < nk; ++kt) {
     const int s = kt % STAGES;
-    const int nxt = kt + 1;
+    const int nxt = kt + PF;
     if (nxt < nk) {
       const int sn = nxt % STAGES;
       if (nxt >= STAGES) mbar_wait_parity(&empty[sn], (unsigned)((nxt / STAGES - 1) & 1));
