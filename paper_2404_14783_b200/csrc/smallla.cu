@@ -1516,7 +1516,7 @@ unsigned grid_for(int64_t total) {
 // tiles come in batches of CHB (one L2 round trip per batch).  Tile (I, J)
 // belongs to CTA (linear upper-triangle index) % CHC.  Elements past s act as
 // the identity (padded tiles factor trivially and are never stored).
-constexpr int CHC = 8;
+constexpr int CHC = 16;  // non-portable cluster size (opt-in attribute)
 constexpr int CTB = 16;
 constexpr int CHC_MAX = 256;
 constexpr int CHB = 4;
@@ -1853,6 +1853,11 @@ void chol_inv_launch(Ctx& ctx, const QView& g, const QView& r, const QView& rinv
   const int64_t nbt = (s + CTB - 1) / CTB;
   const size_t csm = sizeof(Tile) * (size_t)(nbt + CHB + 3);
   static size_t cattr = 0;
+  static bool nonportable = false;
+  if (!nonportable) {
+    QLRA_CUDA(cudaFuncSetAttribute(k_chol_inv_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    nonportable = true;
+  }
   if (csm > 48 * 1024 && csm > cattr) {
     QLRA_CUDA(cudaFuncSetAttribute(k_chol_inv_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm));
     cattr = csm;
