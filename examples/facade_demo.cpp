@@ -45,6 +45,12 @@ int main() {
   QbResult qb2 = qb_stage(ctx, st2, RangefinderMethod::kPseudoSvd);
   auto [res, an] = qb_residual(ctx, ad, qb);
   auto [res2, an2] = qb_residual(ctx, ad, qb2);
+  // host in / host out in one call: same seeds as make_sketch above
+  HostQb hq = one_pass_qb_host(ctx, ah, r, s, l, RangefinderMethod::kPseudoQr, 1, 2);
+  QbResult qb3;
+  qb3.h = DeviceQMatrix::upload(HostQView{{&hq.h[0], &hq.h[m * s], &hq.h[2 * m * s], &hq.h[3 * m * s]}, m, s, s});
+  qb3.x = DeviceQMatrix::upload(HostQView{{&hq.x[0], &hq.x[s * n], &hq.x[2 * s * n], &hq.x[3 * s * n]}, s, n, n});
+  auto [res3, an3] = qb_residual(ctx, ad, qb3);
   bool threw = false;
   try {
     DeviceQMatrix zero(3, 3), rhs(3, 1);
@@ -52,7 +58,8 @@ int main() {
   } catch (const SingularMatrixError& e) {
     threw = e.estimated_condition > 1e14;
   }
-  std::printf("rel_error=%.3e rel_error_svd=%.3e kappa=%.4f singular_threw=%d\n", res / an,
-              res2 / an2, qb.report.kappa_after, (int)threw);
-  return (res / an < 1e-2 && res2 / an2 < 1e-2 && threw) ? 0 : 1;
+  std::printf("rel_error=%.3e rel_error_svd=%.3e rel_error_host=%.3e kappa=%.4f singular_threw=%d\n", res / an,
+              res2 / an2, res3 / an3, qb.report.kappa_after, (int)threw);
+  const bool host_ok = std::fabs(res3 / an3 - res / an) <= 1e-8 * (res / an);
+  return (res / an < 1e-2 && res2 / an2 < 1e-2 && threw && host_ok) ? 0 : 1;
 }

@@ -302,5 +302,51 @@ inline std::pair<double, double> qb_residual(Context& ctx, const DeviceQMatrix& 
   return {r, n};
 }
 
+// one_pass_approx up to the QB stage (sketching.cpp:250-263) for a host-
+// resident A, in one call: the sketch streams A (H2D overlapped), and H and
+// X come back into the caller's host buffers (4 planes each; pinned memory
+// overlaps best).  Seeds and s, l defaults as OnePassOptions
+// (sketching.hpp:130-141, sketching.cpp:222-227: s = r + 5, l = 2 s).
+struct HostQb {
+  std::vector<double> h, x;  // 4 planes each: h rows x s, x s x n
+  Index rows = 0, s = 0, n = 0;
+  RangefinderReport report;
+};
+inline HostQb one_pass_qb_host(Context& ctx, const HostQView& a, Index r, Index s = -1, Index l = -1,
+                               RangefinderMethod method = RangefinderMethod::kPseudoQr,
+                               std::uint64_t omega_seed = 1, std::uint64_t psi_seed = 2,
+                               std::uint64_t rangefinder_seed = kDefaultRangefinderSeed,
+                               TestMatrixKind kind = TestMatrixKind::kGaussian, double density = 1.0,
+                               const PseudoQrConfig& cfg = {}, Index block_rows = 0) {
+  if (s < 0) s = r + 5;
+  if (l < 0) l = 2 * s;
+  HostQb out;
+  out.rows = a.rows;
+  out.s = s;
+  out.n = a.cols;
+  out.h.assign((size_t)(4 * a.rows * s), 0.0);
+  out.x.assign((size_t)(4 * s * a.cols), 0.0);
+  const qlra_spec_t om{(int32_t)kind, a.cols, s, omega_seed, density};
+  const qlra_spec_t ps{(int32_t)kind, l, a.rows, psi_seed, density};
+  const qlra_pseudo_qr_config_t c{cfg.max_correction_steps, cfg.power_iters_for_epsilon, cfg.delta_budget};
+  qlra_qmat_t av, hv, xv;
+  for (int p = 0; p < 4; ++p) {
+    av.p[p] = const_cast<double*>(a.p[p]);
+    hv.p[p] = out.h.data() + (size_t)p * a.rows * s;
+    xv.p[p] = out.x.data() + (size_t)p * s * a.cols;
+  }
+  av.rows = a.rows; av.cols = a.cols; av.ld = a.ld;
+  hv.rows = a.rows; hv.cols = s; hv.ld = s;
+  xv.rows = s; xv.cols = a.cols; xv.ld = a.cols;
+  qlra_rangefinder_report_t rep{};
+  ctx.check(qlra_one_pass_qb_host(ctx.get(), &av, 0, &om, &ps, (int)method, rangefinder_seed, &c, block_rows, &hv,
+                                  &xv, &rep));
+  out.report.kappa_before = rep.kappa_before;
+  out.report.kappa_after = rep.kappa_after;
+  out.report.correction_steps_used = rep.correction_steps_used;
+  out.report.method = method;
+  return out;
+}
+
 }  // namespace gpu
 }  // namespace qlra
