@@ -14,6 +14,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import gc
 import os
 import subprocess
 import sys
@@ -54,24 +55,35 @@ class ClockSampler:
         self.device = device
         self.samples = []
         self._stop = threading.Event()
-        self._t = threading.Thread(target=self._run, daemon=True)
-
-    def _run(self):
+        self._ready = threading.Event()
+        # NVML is imported and initialised here, before the timed region: a
+        # cold `import pynvml` inside it holds the GIL and stalls the thread
+        # that launches the kernels (seen as +30 ms steps)
+        self._nvml = None
         try:
             import pynvml
             pynvml.nvmlInit()
-            h = pynvml.nvmlDeviceGetHandleByIndex(self.device)
-            mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            h = pynvml.nvmlDeviceGetHandleByIndex(device)
+            self._nvml = (pynvml, h, pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM))
+        except Exception:
+            self._nvml = None
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        if self._nvml is not None:
+            pynvml, h, mx = self._nvml
             bits = [("hw_slowdown", 0x8), ("hw_thermal_slowdown", 0x40), ("sw_thermal_slowdown", 0x20),
                     ("sw_power_cap", 0x4)]
-            while not self._stop.is_set():
-                sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
-                r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
-                self.samples.append([str(sm), str(mx)] + ["Active" if r & b else "Not Active" for _, b in bits])
-                self._stop.wait(0.02)
-            return
-        except Exception:
-            pass
+            try:
+                while not self._stop.is_set():
+                    sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                    r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                    self.samples.append([str(sm), str(mx)] + ["Active" if r & b else "Not Active" for _, b in bits])
+                    self._ready.set()
+                    self._stop.wait(0.02)
+                return
+            except Exception:
+                pass
         while not self._stop.is_set():
             try:
                 out = subprocess.run(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
@@ -81,15 +93,21 @@ class ClockSampler:
                     self.samples.append([x.strip() for x in out.split(",")])
             except Exception:
                 pass
+            self._ready.set()
             self._stop.wait(0.2)
 
     def __enter__(self):
+        if os.environ.get("QLRA_BENCH_NO_CLOCKS"):  # A/B of the sampler's own interference
+            return self
         self._t.start()
+        self._ready.wait(timeout=10)  # sampling is running before timing starts
+        self.samples.clear()          # keep only samples from inside the timed region
         return self
 
     def __exit__(self, *a):
         self._stop.set()
-        self._t.join(timeout=10)
+        if self._t.is_alive():
+            self._t.join(timeout=10)
 
     def summary(self):
         if not self.samples:
@@ -219,6 +237,8 @@ def main():
         torch.cuda.synchronize()
 
     sk_events = []
+    host_ms = []
+    dev_allocs = []
 
     used = {"rangefinder": args.rangefinder}
 
@@ -226,8 +246,13 @@ def main():
         nonlocal method
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
+        h0 = time.perf_counter()
         st = Q.make_sketch(a_dev, opts.r, opts.s, opts.l, opts.omega_seed, opts.psi_seed, cfg.kind,
                            ctx=ctx, row0=r0, m_global=cfg.m)
+        host_ms.append(1e3 * (time.perf_counter() - h0))
+        if os.environ.get("QLRA_BENCH_STEPTIMES"):
+            ms_ = torch.cuda.memory_stats()
+            dev_allocs.append((ms_.get("num_device_alloc", -1), ms_.get("num_alloc_retries", -1)))
         e1.record(stream)
         sk_events.append((e0, e1))
         try:
@@ -245,8 +270,16 @@ def main():
         step(a)
     barrier()
     sk_events.clear()
+    # torch's caching allocator only settles after a few steps of this
+    # allocation pattern (two generations of Y, W, H, X alive); a reserved
+    # segment carved up by later allocations keeps cudaMalloc -- which blocks
+    # the host -- out of the timed region
+    _reserve = torch.empty(int(512e6) // 8, dtype=torch.float64, device="cuda")
+    del _reserve
     ctx.kernel_timing(True)
     launches0 = ctx.launch_count()
+    gc.collect()
+    gc.disable()  # no collector pause inside the timed region (it stalls the launching thread)
     with ClockSampler(local) as clk:
         t0 = torch.cuda.Event(enable_timing=True)
         t1 = torch.cuda.Event(enable_timing=True)
@@ -255,7 +288,12 @@ def main():
             st, qb = step(a)
         t1.record(stream)
         barrier()
+    gc.enable()
     launches = ctx.launch_count() - launches0
+    if os.environ.get("QLRA_BENCH_STEPTIMES") and rank == 0:
+        sys.stderr.write("sketch per step ms: " + " ".join("%.2f" % e0.elapsed_time(e1) for e0, e1 in sk_events) + "\n")
+        sys.stderr.write("make_sketch host ms: " + " ".join("%.2f" % v for v in host_ms[-len(sk_events):]) + "\n")
+        sys.stderr.write("torch device allocs/retries: " + " ".join("%d/%d" % v for v in dev_allocs) + "\n")
     kst = ctx.kernel_stats()
     ctx.kernel_timing(False)
     ms = t0.elapsed_time(t1) / args.steps
@@ -287,16 +325,21 @@ def main():
             # copied back while the core solve runs, then X
             Q.one_pass_qb_host(a_host, e2e_opts, ctx=ctx, row0=r0, m_global=cfg.m, h_out=h_host, x_out=x_host)
 
-        for _ in range(max(1, args.warmup // 2)):
+        for _ in range(args.warmup):
             e2e_step()
         barrier()
         s0 = torch.cuda.Event(enable_timing=True)
         s1 = torch.cuda.Event(enable_timing=True)
+        _reserve = torch.empty(int(512e6) // 8, dtype=torch.float64, device="cuda")
+        del _reserve
+        gc.collect()
+        gc.disable()
         s0.record(stream)
         for _ in range(args.steps):
             e2e_step()
         s1.record(stream)
         barrier()
+        gc.enable()
         e2e_ms = torch.tensor([s0.elapsed_time(s1) / args.steps], dtype=torch.float64, device="cuda")
         if world > 1:
             dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)

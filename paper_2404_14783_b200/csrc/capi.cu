@@ -798,6 +798,16 @@ int qlra_ctx_create(qlra_ctx_t** out, int device, int rank, int nranks, const vo
   return QLRA_OK;
 }
 
+static void drop_events(Ctx& c) {
+  for (auto& e : c.ktimer.ev) {
+    cudaEventDestroy(e.first);
+    cudaEventDestroy(e.second);
+  }
+  c.ktimer.ev.clear();
+  c.ktimer.flops = c.ktimer.a_bytes = 0.0;
+  c.ktimer.launches = 0;
+}
+
 int qlra_ctx_destroy(qlra_ctx_t* ctx) {
   if (!ctx) return QLRA_OK;
   cudaSetDevice(ctx->c.device);
@@ -811,6 +821,11 @@ int qlra_ctx_destroy(qlra_ctx_t* ctx) {
     cudaStreamDestroy(ctx->c.side);
   }
   if (ctx->c.side_pinned) cudaFreeHost(ctx->c.side_pinned);
+  drop_events(ctx->c);
+  for (auto& e : ctx->c.ktimer.pool) {
+    cudaEventDestroy(e.first);
+    cudaEventDestroy(e.second);
+  }
   delete ctx;
   return QLRA_OK;
 }
@@ -839,20 +854,17 @@ const char* qlra_last_error(const qlra_ctx_t* ctx, double* cond) {
 
 int64_t qlra_ctx_launch_count(const qlra_ctx_t*) { return launch_counter().load(); }
 
-static void drop_events(Ctx& c) {
-  for (auto& e : c.ktimer.ev) {
-    cudaEventDestroy(e.first);
-    cudaEventDestroy(e.second);
-  }
-  c.ktimer.ev.clear();
-  c.ktimer.flops = c.ktimer.a_bytes = 0.0;
-  c.ktimer.launches = 0;
-}
-
 int qlra_ctx_kernel_timing(qlra_ctx_t* ctx, int enable) {
   return guarded(ctx, [&](Ctx& c) {
     drop_events(c);
     c.ktimer.on = enable != 0;
+    if (c.ktimer.on)  // events for up to 256 launches created now, outside any timed region
+      while (c.ktimer.pool.size() < 256) {
+        cudaEvent_t a = nullptr, b = nullptr;
+        QLRA_CUDA(cudaEventCreate(&a));
+        QLRA_CUDA(cudaEventCreate(&b));
+        c.ktimer.pool.emplace_back(a, b);
+      }
   });
 }
 

@@ -41,7 +41,8 @@ struct Ctx {
   // CUDA events bracket every launch on the launching stream.
   struct KernelTimer {
     bool on = false;
-    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;  // recorded pairs
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pool;  // created up front (no driver call per launch)
     double flops = 0.0, a_bytes = 0.0;
     int64_t launches = 0;
   } ktimer;

@@ -269,8 +269,14 @@ void sketch_panel(Ctx& ctx, const QView& om, const QView& ps, int64_t pc0, const
     const int64_t ctas = (int64_t)f.y_tm * f.y_tn * f.zy + (int64_t)w_tm * w_tn * f.zw;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (ctx.ktimer.on) {
-      QLRA_CUDA(cudaEventCreate(&e0));
-      QLRA_CUDA(cudaEventCreate(&e1));
+      if (!ctx.ktimer.pool.empty()) {
+        e0 = ctx.ktimer.pool.back().first;
+        e1 = ctx.ktimer.pool.back().second;
+        ctx.ktimer.pool.pop_back();
+      } else {
+        QLRA_CUDA(cudaEventCreate(&e0));
+        QLRA_CUDA(cudaEventCreate(&e1));
+      }
       QLRA_CUDA(cudaEventRecord(e0, ctx.stream));
     }
     sketch_fused_kernel<<<(unsigned)ctas, NT, qt::SMEM_BYTES, ctx.stream>>>(f);
