@@ -108,6 +108,17 @@ class ClockSampler:
         self._stop.set()
         if self._t.is_alive():
             self._t.join(timeout=10)
+            if not self.samples and self._nvml is not None:
+                # timed region shorter than the sampling period (C1): one
+                # sample at its end
+                try:
+                    pynvml, h, mx = self._nvml
+                    sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                    r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                    self.samples.append([str(sm), str(mx)] + ["Active" if r & b else "Not Active"
+                                                              for b in (0x8, 0x40, 0x20, 0x4)])
+                except Exception:
+                    pass
 
     def summary(self):
         if not self.samples:
