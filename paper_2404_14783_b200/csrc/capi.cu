@@ -68,12 +68,6 @@ std::vector<double> diag_to_host(Ctx& ctx, const double* p, int64_t ld, int64_t 
   }
   return h;
 }
-int info_to_host(Ctx& ctx, const int* d) {
-  int h = 0;
-  QLRA_CUDA(cudaMemcpyAsync(&h, d, sizeof(int), cudaMemcpyDeviceToHost, ctx.stream));
-  QLRA_CUDA(cudaStreamSynchronize(ctx.stream));
-  return h;
-}
 
 int64_t global_rows(Ctx& ctx, int64_t local) {
   if (ctx.nranks <= 1) return local;

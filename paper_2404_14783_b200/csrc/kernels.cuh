@@ -132,19 +132,6 @@ void sketch_update_rows_host(Ctx& ctx, const qlra_spec_t& omega, const qlra_spec
                              const QView& w, int64_t block_rows);
 const char* sketch_kernel_name();
 
-// ---------------------------------------------------------- smallla.cu ---
-// All "small" matrices are s x s (or 2s x 2s complex), s <= ~1000, resident
-// in L2; kernels run on one CTA unless noted.
-// Complex matrices: row-major double2 with leading dimension ld.
-void small_chi_from_quat(Ctx& ctx, const QView& g, double2* chi, int64_t ldc);
-void small_complex_part(Ctx& ctx, const QView& g, double2* c, int64_t ldc);
-// Lower Cholesky in place; *d_info = 0 or first failing column (1-based).
-void small_cholesky(Ctx& ctx, double2* a, int64_t n, int64_t ld, int* d_info);
-// out = (L^{-1})^*  (upper), written as a quaternion with zero j,k planes.
-void small_inv_lower_adjoint_to_quat(Ctx& ctx, const double2* l, int64_t n, int64_t ld,
-                                     const QView& out);
-// Eigenvalues (descending) of a Hermitian complex matrix (destroyed).
-void small_herm_eigvals(Ctx& ctx, double2* a, int64_t n, int64_t ld, double* d_w);
 // Gauss-Jordan with partial pivoting on quaternion A (n x n): B <- A^{-1} B,
 // A destroyed.  d_stat[0] = info (0 ok, k+1 = zero pivot at k),
 // d_stat[1..2] = min/max pivot norm (doubles via reinterpret).
@@ -182,12 +169,7 @@ int64_t chol_inv_async_max();
 void chol_inv_launch(Ctx& ctx, const QView& g, const QView& r, const QView& rinv, int* d_info, double* d_rdiag);
 // zero the j, k planes (restrict a quaternion matrix to its complex part)
 void zero_jk_planes(Ctx& ctx, const QView& g);
-// Quaternion Cholesky G = R^*R in place (upper triangle), *d_info as above.
-void small_quat_cholesky(Ctx& ctx, const QView& g, int* d_info);
-// x = r^{-1}, r upper triangular quaternion with real diagonal.
-void small_quat_triinv_upper(Ctx& ctx, const QView& r, const QView& x);
 void small_add_diag(Ctx& ctx, const QView& g, double shift);
-void small_add_diag_complex(Ctx& ctx, double2* a, int64_t n, int64_t ld, double shift);
 // dst = src (same shape)
 void copy_qmat(Ctx& ctx, const QView& src, const QView& dst);
 void scale_add_qmat(Ctx& ctx, double a, const QView& x, double b, const QView& y,

@@ -25,16 +25,9 @@ constexpr int SNT = 1024;
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
   return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
 }
-__device__ __forceinline__ double2 cmulc(double2 a, double2 b) {  // a * conj(b)
-  return make_double2(a.x * b.x + a.y * b.y, a.y * b.x - a.x * b.y);
-}
 __device__ __forceinline__ double2 cconj(double2 a) { return make_double2(a.x, -a.y); }
 __device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
 __device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
-__device__ __forceinline__ double2 cdiv(double2 a, double2 b) {
-  const double d = b.x * b.x + b.y * b.y;
-  return make_double2((a.x * b.x + a.y * b.y) / d, (a.y * b.x - a.x * b.y) / d);
-}
 
 // Fixed-order block sum (shuffle trees within and across warps), result
 // broadcast; deterministic for a given blockDim.  sh needs 32 doubles.
@@ -73,159 +66,10 @@ __device__ __forceinline__ void qstore(const QView& m, int64_t i, int64_t j, Q4 
   m.p[3][o] = q.z;
 }
 
-// ------------------------------------------------------------ kernels ---
-__global__ void k_chi_from_quat(QView g, double2* chi, int64_t ldc) {
-  const int64_t n = g.rows;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n * n;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = e / n, j = e % n;
-    const Q4 q = qload(g, i, j);
-    const double2 q0 = make_double2(q.w, q.x), q1 = make_double2(q.y, q.z);
-    chi[i * ldc + j] = q0;
-    chi[i * ldc + n + j] = q1;
-    chi[(n + i) * ldc + j] = make_double2(-q1.x, q1.y);  // -conj(q1)
-    chi[(n + i) * ldc + n + j] = cconj(q0);
-  }
-}
 
-__global__ void k_complex_part(QView g, double2* c, int64_t ldc) {
-  const int64_t n = g.rows, m = g.cols;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n * m;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = e / m, j = e % m;
-    c[i * ldc + j] = make_double2(g.p[0][i * g.ld + j], g.p[1][i * g.ld + j]);
-  }
-}
 
-// Right-looking lower Cholesky, one CTA.  Only the lower triangle is read.
-__global__ void __launch_bounds__(SNT) k_cholesky(double2* a, int64_t n, int64_t ld, int* info) {
-  __shared__ double s_piv;
-  __shared__ int s_bad;
-  const int t = threadIdx.x;
-  if (t == 0) { *info = 0; s_bad = 0; }
-  for (int64_t k = 0; k < n; ++k) {
-    if (t == 0) {
-      const double d = a[k * ld + k].x;
-      if (!(d > 0.0)) {
-        s_bad = (int)k + 1;
-        *info = (int)k + 1;
-      } else {
-        s_piv = sqrt(d);
-        a[k * ld + k] = make_double2(s_piv, 0.0);
-      }
-    }
-    __syncthreads();
-    if (s_bad) return;
-    const double inv = 1.0 / s_piv;
-    for (int64_t i = k + 1 + t; i < n; i += blockDim.x) {
-      double2 v = a[i * ld + k];
-      a[i * ld + k] = make_double2(v.x * inv, v.y * inv);
-    }
-    __syncthreads();
-    const int64_t r = n - k - 1;
-    for (int64_t e = t; e < r * r; e += blockDim.x) {
-      const int64_t i = k + 1 + e / r, j = k + 1 + e % r;
-      if (j > i) continue;
-      const double2 lik = a[i * ld + k], ljk = a[j * ld + k];
-      a[i * ld + j] = csub(a[i * ld + j], cmulc(lik, ljk));
-    }
-    __syncthreads();
-  }
-}
 
-// out(i, j) = conj(Linv(j, i)) for i <= j (upper), as quaternion w/x planes.
-// Column-parallel forward substitution: thread j owns column j of L^{-1}.
-__global__ void __launch_bounds__(SNT) k_inv_lower_adj(const double2* l, int64_t n, int64_t ld, QView out) {
-  for (int64_t j = threadIdx.x; j < n; j += blockDim.x) {
-    for (int64_t i = 0; i < n; ++i) {
-      // column j of L^{-1} is x; out row j col i = conj(x_i)
-      for (int p = 0; p < 4; ++p) out.p[p][i * out.ld + j] = 0.0;
-    }
-  }
-  __syncthreads();
-  for (int64_t j = threadIdx.x; j < n; j += blockDim.x) {
-    // x_i for i >= j stored into out(j, i) as conj
-    for (int64_t i = j; i < n; ++i) {
-      double2 s = make_double2(i == j ? 1.0 : 0.0, 0.0);
-      for (int64_t k = j; k < i; ++k) {
-        const double2 xk = make_double2(out.p[0][j * out.ld + k], -out.p[1][j * out.ld + k]);
-        s = csub(s, cmul(l[i * ld + k], xk));
-      }
-      const double2 xi = cdiv(s, l[i * ld + i]);
-      out.p[0][j * out.ld + i] = xi.x;
-      out.p[1][j * out.ld + i] = -xi.y;
-    }
-  }
-}
 
-// Householder tridiagonalisation (LAPACK zhetd2, lower) of a full Hermitian
-// matrix, one CTA; d (n), e (n-1) out.  work: 2n double2.
-__global__ void __launch_bounds__(SNT) k_tridiag(double2* a, int64_t n, int64_t ld, double* d,
-                                                 double* e, double2* work) {
-  __shared__ double sh[SNT];
-  __shared__ double2 s_tau, s_alpha2;
-  __shared__ int s_skip;
-  const int t = threadIdx.x;
-  double2* v = work;
-  double2* x = work + n;
-  for (int64_t k = 0; k + 1 < n; ++k) {
-    const int64_t len = n - k - 1;
-    double part = 0.0;
-    for (int64_t i = k + 2 + t; i < n; i += blockDim.x) {
-      const double2 q = a[i * ld + k];
-      part += q.x * q.x + q.y * q.y;
-    }
-    const double xnorm2 = block_sum(part, sh);
-    if (t == 0) {
-      const double2 alpha = a[(k + 1) * ld + k];
-      if (xnorm2 == 0.0 && alpha.y == 0.0) {
-        s_skip = 1;
-        e[k] = alpha.x;
-        s_tau = make_double2(0.0, 0.0);
-      } else {
-        s_skip = 0;
-        const double beta = -copysign(sqrt(alpha.x * alpha.x + alpha.y * alpha.y + xnorm2), alpha.x);
-        s_tau = make_double2((beta - alpha.x) / beta, -alpha.y / beta);
-        s_alpha2 = cdiv(make_double2(1.0, 0.0), make_double2(alpha.x - beta, alpha.y));
-        e[k] = beta;
-      }
-    }
-    __syncthreads();
-    if (s_skip) continue;
-    const double2 scal = s_alpha2, tau = s_tau;
-    for (int64_t i = t; i < len; i += blockDim.x)
-      v[i] = i == 0 ? make_double2(1.0, 0.0) : cmul(a[(k + 1 + i) * ld + k], scal);
-    __syncthreads();
-    // x = tau * A22 v
-    for (int64_t r = t; r < len; r += blockDim.x) {
-      double2 s = make_double2(0.0, 0.0);
-      const double2* row = a + (k + 1 + r) * ld + (k + 1);
-      for (int64_t c = 0; c < len; ++c) s = cadd(s, cmul(row[c], v[c]));
-      x[r] = cmul(tau, s);
-    }
-    __syncthreads();
-    // alpha = -1/2 tau (x^H v)
-    double pr = 0.0, pi = 0.0;
-    for (int64_t r = t; r < len; r += blockDim.x) {
-      const double2 q = cmul(cconj(x[r]), v[r]);
-      pr += q.x;
-      pi += q.y;
-    }
-    const double dr = block_sum(pr, sh);
-    const double di = block_sum(pi, sh);
-    const double2 al = cmul(make_double2(-0.5 * tau.x, -0.5 * tau.y), make_double2(dr, di));
-    for (int64_t r = t; r < len; r += blockDim.x) x[r] = cadd(x[r], cmul(al, v[r]));
-    __syncthreads();
-    // A22 -= v x^H + x v^H
-    for (int64_t q = t; q < len * len; q += blockDim.x) {
-      const int64_t r = q / len, c = q % len;
-      double2* p = a + (k + 1 + r) * ld + (k + 1 + c);
-      *p = csub(*p, cadd(cmulc(v[r], x[c]), cmulc(x[r], v[c])));
-    }
-    __syncthreads();
-  }
-  for (int64_t i = t; i < n; i += blockDim.x) d[i] = a[i * ld + i].x;
-}
 
 // Sturm count by the three-term recurrence of the leading principal minors,
 // p_i = (d_i - x) p_{i-1} - e_{i-1}^2 p_{i-2} (eigenvalues < x = sign changes
@@ -627,195 +471,30 @@ __global__ void __launch_bounds__(SNT) k_power_inverse(QView ginv, int iters, do
   if (t == 0) *rho_out = rho;
 }
 
-// Quaternion Cholesky G = R^* R (R upper, real positive diagonal), in place on
-// the upper triangle of g (lower triangle ignored), one CTA.
-__global__ void __launch_bounds__(SNT) k_quat_cholesky(QView g, int* info) {
-  __shared__ double s_piv;
-  __shared__ int s_bad;
-  const int t = threadIdx.x;
-  const int64_t n = g.rows;
-  if (t == 0) { *info = 0; s_bad = 0; }
-  for (int64_t k = 0; k < n; ++k) {
-    if (t == 0) {
-      const double d = g.p[0][k * g.ld + k];
-      if (!(d > 0.0)) {
-        s_bad = (int)k + 1;
-        *info = (int)k + 1;
-      } else {
-        s_piv = sqrt(d);
-        qstore(g, k, k, Q4{s_piv, 0.0, 0.0, 0.0});
-      }
-    }
-    __syncthreads();
-    if (s_bad) return;
-    const double inv = 1.0 / s_piv;
-    for (int64_t j = k + 1 + t; j < n; j += blockDim.x) {
-      Q4 q = qload(g, k, j);
-      qstore(g, k, j, Q4{q.w * inv, q.x * inv, q.y * inv, q.z * inv});
-    }
-    __syncthreads();
-    const int64_t r = n - k - 1;
-    for (int64_t e = t; e < r * r; e += blockDim.x) {
-      const int64_t i = k + 1 + e / r, j = k + 1 + e % r;
-      if (j < i) continue;
-      Q4 a = qload(g, k, i), b = qload(g, k, j);
-      a.x = -a.x; a.y = -a.y; a.z = -a.z;  // R_ki^*
-      const Q4 pq = qmul(a, b);
-      Q4 c = qload(g, i, j);
-      c.w -= pq.w; c.x -= pq.x; c.y -= pq.y; c.z -= pq.z;
-      qstore(g, i, j, c);
-    }
-    __syncthreads();
-  }
-}
 
-// X = R^{-1} for upper-triangular quaternion R with real diagonal.  One warp
-// per column j: X_jj = 1/R_jj, then for i = j-1 .. 0,
-// X_ij = -R_ii^{-1} sum_{k=i+1..j} R_ik X_kj with the sum split across the
-// 32 lanes (fixed-order shuffle reduction).  X must not alias R.
-__global__ void __launch_bounds__(SNT) k_quat_triinv_upper(QView r, QView x) {
-  const int64_t n = r.rows;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  for (int64_t j = wid; j < n; j += nw) {
-    for (int64_t i = lane; i < n; i += 32) qstore(x, i, j, Q4{0.0, 0.0, 0.0, 0.0});
-    __syncwarp();
-    if (lane == 0) qstore(x, j, j, Q4{1.0 / r.p[0][j * r.ld + j], 0.0, 0.0, 0.0});
-    __syncwarp();
-    for (int64_t i = j - 1; i >= 0; --i) {
-      Q4 acc{0.0, 0.0, 0.0, 0.0};
-      for (int64_t k = i + 1 + lane; k <= j; k += 32) {
-        const Q4 pq = qmul(qload(r, i, k), qload(x, k, j));
-        acc.w += pq.w; acc.x += pq.x; acc.y += pq.y; acc.z += pq.z;
-      }
-      acc.w = warp_sum(acc.w);
-      acc.x = warp_sum(acc.x);
-      acc.y = warp_sum(acc.y);
-      acc.z = warp_sum(acc.z);
-      if (lane == 0) {
-        const double inv = -1.0 / r.p[0][i * r.ld + i];
-        qstore(x, i, j, Q4{acc.w * inv, acc.x * inv, acc.y * inv, acc.z * inv});
-      }
-      __syncwarp();
-    }
-  }
-}
 
 __global__ void k_add_diag(QView g, double shift) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < g.rows;
        i += (int64_t)gridDim.x * blockDim.x)
     g.p[0][i * g.ld + i] += shift;
 }
-__global__ void k_add_diag_c(double2* a, int64_t n, int64_t ld, double shift) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x)
-    a[i * ld + i].x += shift;
-}
 
-// Householder tridiagonalisation of a quaternion Hermitian matrix (n x n, full
-// storage, destroyed), one CTA.  Reflector H = I - beta v v^* with
+
+// Householder tridiagonalisation of a quaternion Hermitian matrix (eigenvalues
+// then follow by multisection).  Reflector H = I - beta v v^* with
 // v = x + phi*alpha*e1, phi = x1/|x1| (unit quaternion), alpha = ||x||, so
 // H x = -phi alpha e1: the subdiagonal is a quaternion of modulus alpha and a
 // diagonal unitary similarity makes it real, hence e[k] = alpha.  The update
 // H A H = A - v w^* - w v^*, w = p - (beta c/2) v, p = beta A v, c = v^* p
 // (real), is the real-Householder identity with real scalars, valid in the
-// quaternion algebra.  Work is O(n^2) per step: the matvec runs one warp per
-// row (coalesced plane loads, shuffle reduction), the rank-2 update one thread
-// per element.  Eigenvalues of the tridiagonal follow by bisection.
-__global__ void __launch_bounds__(SNT) k_qtridiag(QView a, double* d, double* e) {
-  extern __shared__ __align__(16) unsigned char dsm[];
-  const int64_t n = a.rows;
-  Q4* v = reinterpret_cast<Q4*>(dsm);
-  Q4* pv = v + n;
-  __shared__ double sh[SNT];
-  __shared__ double s_alpha, s_ax1, s_beta, s_c;
-  __shared__ Q4 s_phi;
-  const int t = threadIdx.x, lane = t & 31, wid = t >> 5, nw = blockDim.x >> 5;
-  for (int64_t k = 0; k + 1 < n; ++k) {
-    const int64_t len = n - k - 1, o = k + 1;
-    double part = 0.0;
-    for (int64_t i = t; i < len; i += blockDim.x) {
-      const Q4 q = qload(a, o + i, k);
-      part += q.w * q.w + q.x * q.x + q.y * q.y + q.z * q.z;
-    }
-    const double nrm2 = block_sum(part, sh);
-    if (t == 0) {
-      const Q4 x1 = qload(a, o, k);
-      const double ax1 = sqrt(x1.w * x1.w + x1.x * x1.x + x1.y * x1.y + x1.z * x1.z);
-      const double alpha = sqrt(nrm2);
-      s_alpha = alpha;
-      s_ax1 = ax1;
-      s_phi = ax1 > 0.0 ? Q4{x1.w / ax1, x1.x / ax1, x1.y / ax1, x1.z / ax1} : Q4{1.0, 0.0, 0.0, 0.0};
-      e[k] = alpha;
-      s_beta = alpha > 0.0 ? 2.0 / (2.0 * alpha * alpha + 2.0 * alpha * ax1) : 0.0;
-    }
-    __syncthreads();
-    const double beta = s_beta;
-    if (beta == 0.0) continue;  // column already reduced
-    for (int64_t i = t; i < len; i += blockDim.x) {
-      Q4 q = qload(a, o + i, k);
-      if (i == 0) {
-        q.w += s_phi.w * s_alpha; q.x += s_phi.x * s_alpha;
-        q.y += s_phi.y * s_alpha; q.z += s_phi.z * s_alpha;
-      }
-      v[i] = q;
-    }
-    __syncthreads();
-    // p = beta * A22 v  (warp per row)
-    for (int64_t r = wid; r < len; r += nw) {
-      Q4 acc{0.0, 0.0, 0.0, 0.0};
-      const int64_t row = (o + r) * a.ld + o;
-      for (int64_t c = lane; c < len; c += 32) {
-        const Q4 av{a.p[0][row + c], a.p[1][row + c], a.p[2][row + c], a.p[3][row + c]};
-        const Q4 pq = qmul(av, v[c]);
-        acc.w += pq.w; acc.x += pq.x; acc.y += pq.y; acc.z += pq.z;
-      }
-#pragma unroll
-      for (int off = 16; off > 0; off >>= 1) {
-        acc.w += __shfl_xor_sync(0xffffffffu, acc.w, off);
-        acc.x += __shfl_xor_sync(0xffffffffu, acc.x, off);
-        acc.y += __shfl_xor_sync(0xffffffffu, acc.y, off);
-        acc.z += __shfl_xor_sync(0xffffffffu, acc.z, off);
-      }
-      if (lane == 0) pv[r] = Q4{beta * acc.w, beta * acc.x, beta * acc.y, beta * acc.z};
-    }
-    __syncthreads();
-    // c = Re(v^* p)
-    double cp = 0.0;
-    for (int64_t i = t; i < len; i += blockDim.x)
-      cp += v[i].w * pv[i].w + v[i].x * pv[i].x + v[i].y * pv[i].y + v[i].z * pv[i].z;
-    const double c = block_sum(cp, sh);
-    const double hk = 0.5 * beta * c;
-    for (int64_t i = t; i < len; i += blockDim.x) {
-      const Q4 q = pv[i], vi = v[i];
-      pv[i] = Q4{q.w - hk * vi.w, q.x - hk * vi.x, q.y - hk * vi.y, q.z - hk * vi.z};
-    }
-    __syncthreads();
-    // A22 -= v w^* + w v^*
-    for (int64_t q = t; q < len * len; q += blockDim.x) {
-      const int64_t r = q / len, cc = q % len;
-      const Q4 vr = v[r], wr = pv[r];
-      Q4 wc = pv[cc], vc = v[cc];
-      wc.x = -wc.x; wc.y = -wc.y; wc.z = -wc.z;
-      vc.x = -vc.x; vc.y = -vc.y; vc.z = -vc.z;
-      const Q4 t1 = qmul(vr, wc), t2 = qmul(wr, vc);
-      const int64_t off = (o + r) * a.ld + o + cc;
-      a.p[0][off] -= t1.w + t2.w;
-      a.p[1][off] -= t1.x + t2.x;
-      a.p[2][off] -= t1.y + t2.y;
-      a.p[3][off] -= t1.z + t2.z;
-    }
-    __syncthreads();
-  }
-  for (int64_t i = t; i < n; i += blockDim.x) d[i] = a.p[0][i * a.ld + i];
-}
-
-// Shared-memory variant of k_qtridiag for n <= QT_SMEM_MAX: the Hermitian
-// matrix lives in shared memory as its packed lower triangle (A[r][c], r >= c,
-// at r(r+1)/2 + c; the upper half is the conjugate).  Same reflectors and the
-// same arithmetic as k_qtridiag; three barriers per step: warp 0 forms the
-// reflector, the matvec runs one warp per row, every warp recomputes
-// c = Re(v^* p) itself and the rank-2 update touches only the lower triangle.
-constexpr int QT_SMEM_MAX = 112;
+// quaternion algebra.  Three kernels apply it: this single-CTA one (n <= 48),
+// a cluster one (48 < n <= QTC_MAX) and a cooperative grid one (larger n).
+//
+// Single-CTA form: the matrix lives in shared memory as its packed lower
+// triangle (A[r][c], r >= c, at r(r+1)/2 + c; the upper half is the
+// conjugate).  Three barriers per step: warp 0 forms the reflector, the
+// matvec runs one warp per row, every warp recomputes c = Re(v^* p) itself
+// and the rank-2 update touches only the lower triangle.
 __device__ __forceinline__ int tri(int r, int c) { return r * (r + 1) / 2 + c; }
 __global__ void __launch_bounds__(512) k_qtridiag_smem(QView a, double* d, double* e) {
   extern __shared__ __align__(16) unsigned char dsm[];
@@ -904,7 +583,7 @@ __global__ void __launch_bounds__(512) k_qtridiag_smem(QView a, double* d, doubl
   for (int i = t; i < n; i += blockDim.x) d[i] = L[tri(i, i)].w;
 }
 
-// Cluster variant of k_qtridiag for 48 < n <= QTC_MAX: one cluster of QTC
+// Cluster tridiagonalisation for 48 < n <= QTC_MAX: one cluster of QTC
 // CTAs on QTC SMs (the single-CTA kernel is bound by one SM's FP64 pipe).
 // Row r lives in the shared memory of CTA r % QTC (full rows, both
 // triangles).  Step k: every CTA all-gathers x = A[k+1:, k] -- each owner
@@ -919,7 +598,7 @@ __global__ void __launch_bounds__(512) k_qtridiag_smem(QView a, double* d, doubl
 // it has this CTA's p(k+1), i.e. after this CTA finished step k with v(k)
 // (v double-buffered), and p(k+1) only after it has this CTA's part of
 // v(k+1), i.e. after this CTA finished reading p(k).
-// Same reflectors as k_qtridiag.
+// Same reflectors as k_qtridiag_smem.
 constexpr int QTC = 16;  // non-portable cluster size (B200 allows 16 with the opt-in attribute)
 constexpr int QTC_MAX = 224;
 constexpr int QTC_THREADS = 256;
@@ -1401,7 +1080,7 @@ __global__ void k_zero_jk(QView g) {
   }
 }
 
-// Cooperative multi-CTA version of k_qtridiag for large n (every CTA is
+// Cooperative multi-CTA tridiagonalisation for large n (every CTA is
 // resident; grid.sync() separates the phases of each Householder step).
 // Reductions: per-CTA partial sums in fixed order, then every CTA sums the
 // partials in CTA order, so all CTAs hold bitwise-identical scalars.  The
@@ -1678,28 +1357,6 @@ __global__ void __cluster_dims__(CHC, 1, 1) __launch_bounds__(256) k_chol_inv_cl
 
 }  // namespace
 
-void small_chi_from_quat(Ctx& ctx, const QView& g, double2* chi, int64_t ldc) {
-  k_chi_from_quat<<<grid_for(g.rows * g.rows), 256, 0, ctx.stream>>>(g, chi, ldc);
-  QLRA_LAUNCH_CHECK();
-  count_launch();
-}
-void small_complex_part(Ctx& ctx, const QView& g, double2* c, int64_t ldc) {
-  k_complex_part<<<grid_for(g.rows * g.cols), 256, 0, ctx.stream>>>(g, c, ldc);
-  QLRA_LAUNCH_CHECK();
-  count_launch();
-}
-void small_cholesky(Ctx& ctx, double2* a, int64_t n, int64_t ld, int* d_info) {
-  k_cholesky<<<1, SNT, 0, ctx.stream>>>(a, n, ld, d_info);
-  QLRA_LAUNCH_CHECK();
-  count_launch();
-}
-void small_inv_lower_adjoint_to_quat(Ctx& ctx, const double2* l, int64_t n, int64_t ld,
-                                     const QView& out) {
-  // j,k planes zero
-  k_inv_lower_adj<<<1, SNT, 0, ctx.stream>>>(l, n, ld, out);
-  QLRA_LAUNCH_CHECK();
-  count_launch();
-}
 // all eigenvalues (descending) of the tridiagonal (d, e) into d_w
 void tridiag_all_eigvals(Ctx& ctx, const double* d, const double* e, int64_t n, double* d_w) {
   DeviceBuffer work(ctx, sizeof(double) * (size_t)(3 + 2 * n));
@@ -1723,29 +1380,12 @@ void tridiag_all_eigvals(Ctx& ctx, const double* d, const double* e, int64_t n, 
   count_launch();
 }
 
-void small_herm_eigvals(Ctx& ctx, double2* a, int64_t n, int64_t ld, double* d_w) {
-  if (n == 0) return;
-  DeviceBuffer de(ctx, sizeof(double) * (2 * n + 1));
-  DeviceBuffer work(ctx, sizeof(double2) * 2 * n);
-  double* d = de.as<double>();
-  double* e = d + n;
-  k_tridiag<<<1, SNT, 0, ctx.stream>>>(a, n, ld, d, e, work.as<double2>());
-  QLRA_LAUNCH_CHECK();
-  count_launch();
-  tridiag_all_eigvals(ctx, d, e, n, d_w);
-}
 void small_quat_herm_eigvals(Ctx& ctx, const QView& a, double* d_w, bool extremes_only) {
   const int64_t n = a.rows;
   if (n == 0) return;
   DeviceBuffer de(ctx, sizeof(double) * (2 * n + 1));
   double* d = de.as<double>();
   double* e = d + n;
-  const size_t smem = sizeof(double) * 8 * (size_t)n;
-  static size_t attr = 0;
-  if (smem > 48 * 1024 && smem > attr) {
-    QLRA_CUDA(cudaFuncSetAttribute(k_qtridiag, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = smem;
-  }
   if (n > QTC_MAX) {
     // large n: cooperative grid over all SMs
     int dev = 0, sms = 148, per_sm = 0;
@@ -1778,7 +1418,7 @@ void small_quat_herm_eigvals(Ctx& ctx, const QView& a, double* d_w, bool extreme
     k_qtridiag_cluster<<<QTC, QTC_THREADS, csm, ctx.stream>>>(a, d, e);
     QLRA_LAUNCH_CHECK();
     count_launch();
-  } else if (n <= QT_SMEM_MAX) {
+  } else {  // n <= 48: one CTA, packed triangle in shared memory
     const size_t tsm = sizeof(Q4) * (size_t)(n * (n + 1) / 2 + 2 * n);
     static size_t tattr = 0;
     if (tsm > 48 * 1024 && tsm > tattr) {
@@ -1786,10 +1426,6 @@ void small_quat_herm_eigvals(Ctx& ctx, const QView& a, double* d_w, bool extreme
       tattr = tsm;
     }
     k_qtridiag_smem<<<1, 512, tsm, ctx.stream>>>(a, d, e);
-    QLRA_LAUNCH_CHECK();
-    count_launch();
-  } else {
-    k_qtridiag<<<1, SNT, smem, ctx.stream>>>(a, d, e);
     QLRA_LAUNCH_CHECK();
     count_launch();
   }
@@ -1976,23 +1612,8 @@ void small_power_iter_inverse(Ctx& ctx, const QView& ginv, int iters, double* d_
   QLRA_LAUNCH_CHECK();
   count_launch();
 }
-void small_quat_cholesky(Ctx& ctx, const QView& g, int* d_info) {
-  k_quat_cholesky<<<1, SNT, 0, ctx.stream>>>(g, d_info);
-  QLRA_LAUNCH_CHECK();
-  count_launch();
-}
-void small_quat_triinv_upper(Ctx& ctx, const QView& r, const QView& x) {
-  k_quat_triinv_upper<<<1, SNT, 0, ctx.stream>>>(r, x);
-  QLRA_LAUNCH_CHECK();
-  count_launch();
-}
 void small_add_diag(Ctx& ctx, const QView& g, double shift) {
   k_add_diag<<<1, 256, 0, ctx.stream>>>(g, shift);
-  QLRA_LAUNCH_CHECK();
-  count_launch();
-}
-void small_add_diag_complex(Ctx& ctx, double2* a, int64_t n, int64_t ld, double shift) {
-  k_add_diag_c<<<1, 256, 0, ctx.stream>>>(a, n, ld, shift);
   QLRA_LAUNCH_CHECK();
   count_launch();
 }
