@@ -104,13 +104,22 @@ __device__ __forceinline__ void zero_acc(Acc& acc) {
       for (int p = 0; p < 4; ++p) acc[rb][cb][p][0] = acc[rb][cb][p][1] = 0.0;
 }
 
+// Warp w owns the 16x16 sub-tile (warp_row(w), warp_col(w)).  Warps issue on
+// SMSP w % 4; the diagonal column assignment gives every SMSP one warp of
+// each row band AND each column band, so the 8x8 blocks skipped in tiles
+// padded along either M or N take work off all four tensor pipes evenly (with
+// wc = w % 4, a tile padded along N left one SMSP idle and the CTA waited on
+// the other three).
+__device__ __forceinline__ int warp_row(int w) { return w >> 2; }
+__device__ __forceinline__ int warp_col(int w) { return (w + (w >> 2)) & 3; }
+
 __device__ __forceinline__ int acc_row(int rb) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  return 16 * (w >> 2) + 8 * rb + (lane >> 2);
+  return 16 * warp_row(w) + 8 * rb + (lane >> 2);
 }
 __device__ __forceinline__ int acc_col(int cb) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  return 16 * (w & 3) + 8 * cb + 2 * (lane & 3);
+  return 16 * warp_col(w) + 8 * cb + 2 * (lane & 3);
 }
 
 // Hamilton table in (term q, output plane p) -> (B plane, sign):
@@ -207,7 +216,7 @@ __device__ __forceinline__ void mma_loop(const Operands& g, double* smem, int64_
                                          int64_t kbeg, int64_t kend, Acc& acc, uint64_t* full, uint64_t* empty) {
   constexpr bool AK = !CA, BJ = !CB;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  const int wr = w >> 2, wc = w & 3;
+  const int wr = warp_row(w), wc = warp_col(w);
   const int gid = lane >> 2, tig = lane & 3;
   const int nk = kend > kbeg ? (int)((kend - kbeg + BK - 1) / BK) : 0;
   if (tid == 0) {
@@ -263,7 +272,7 @@ __device__ __forceinline__ void mma_tile(const Operands& g, double* smem, int64_
   // it runs
   __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES];
   const int w = threadIdx.x >> 5;
-  const int64_t r0w = i0 + 16 * (w >> 2), c0w = j0 + 16 * (w & 3);
+  const int64_t r0w = i0 + 16 * warp_row(w), c0w = j0 + 16 * warp_col(w);
   const int nrb = r0w >= g.M ? 0 : r0w + 8 >= g.M ? 1 : 2;
   const int ncb = c0w >= g.N ? 0 : c0w + 8 >= g.N ? 1 : 2;
   switch (nrb * 4 + ncb) {
