@@ -9,6 +9,10 @@
 // writes per-split partials to a workspace reduced in fixed split order
 // (deterministic, no atomics).  Epilogue variants: store, or residual (sum of
 // squares of R - op(A)op(B) and of R, for ||A - HX||_F without forming HX).
+#include <algorithm>
+#include <array>
+#include <map>
+#include <vector>
 #include "common.cuh"
 #include "kernels.cuh"
 #include "qtile.cuh"
@@ -30,23 +34,44 @@ struct GemmArgs {
   int64_t ldc, ldr;
   double alpha, beta;
   int64_t kchunk;       // k range per split (multiple of BK)
-  double* ws;           // split partials [z][4][M][N]  (nullptr if gridDim.z == 1)
-  double* red;          // residual partials [blocks][2]
+  double* ws;           // split partials [z][4][M][N]  (nullptr if nsplit == 1)
+  double* red;          // residual partials [tiles][2]
+  // CTA order, longest first: up to 4 groups of tiles (full, then the tiles
+  // padded along N / M / both, by decreasing cost), each group's CTAs =
+  // its tiles x nsplit, split index fastest, then tile row
+  int nsplit, ngroups, tn_all;
+  int g_tm0[4], g_tm1[4], g_tn0[4], g_tn1[4];
+  int64_t g_start[5];
 };
+
+// blockIdx.x -> (tile row, tile column, split)
+__device__ __forceinline__ void gemm_task(const GemmArgs& g, int& tm, int& tn, int& z) {
+  const int64_t t = blockIdx.x;
+  int gi = 0;
+  while (gi + 1 < g.ngroups && t >= g.g_start[gi + 1]) ++gi;
+  int64_t local = t - g.g_start[gi];
+  z = (int)(local % g.nsplit);
+  local /= g.nsplit;
+  const int nr = g.g_tm1[gi] - g.g_tm0[gi];
+  tm = g.g_tm0[gi] + (int)(local % nr);
+  tn = g.g_tn0[gi] + (int)(local / nr);
+}
 
 template <bool CA, bool CB, int MODE>
 __global__ void __launch_bounds__(NT, 1) qgemm_kernel(GemmArgs g) {
   extern __shared__ __align__(16) double smem[];
   const int64_t M = g.op.M, N = g.op.N;
-  const int64_t i0 = (int64_t)blockIdx.y * BM, j0 = (int64_t)blockIdx.x * BN;
-  const int64_t kbeg = (int64_t)blockIdx.z * g.kchunk;
+  int tm, tn, zs;
+  gemm_task(g, tm, tn, zs);
+  const int64_t i0 = (int64_t)tm * BM, j0 = (int64_t)tn * BN;
+  const int64_t kbeg = (int64_t)zs * g.kchunk;
   const int64_t kend = min(g.K, kbeg + g.kchunk);
   qt::Acc acc;
   qt::zero_acc(acc);
   qt::mma_tile<CA, CB>(g.op, smem, i0, j0, kbeg, kend, acc);
 
   if (MODE == 0) {
-    const bool split = gridDim.z > 1;
+    const bool split = g.nsplit > 1;
 #pragma unroll
     for (int rb = 0; rb < qt::WRB; ++rb) {
       const int64_t gi = i0 + qt::acc_row(rb);
@@ -58,7 +83,7 @@ __global__ void __launch_bounds__(NT, 1) qgemm_kernel(GemmArgs g) {
           const int64_t gj = j0 + qt::acc_col(cb) + h;
           if (gj >= N) continue;
           if (split) {
-            double* w = g.ws + (int64_t)blockIdx.z * 4 * M * N;
+            double* w = g.ws + (int64_t)zs * 4 * M * N;
 #pragma unroll
             for (int p = 0; p < 4; ++p) w[(int64_t)p * M * N + gi * N + gj] = acc[rb][cb][p][h];
           } else {
@@ -107,7 +132,7 @@ __global__ void __launch_bounds__(NT, 1) qgemm_kernel(GemmArgs g) {
       __syncthreads();
     }
     if (tid == 0) {
-      const int64_t b = (int64_t)blockIdx.y * gridDim.x + blockIdx.x;
+      const int64_t b = (int64_t)tm * g.tn_all + tn;
       g.red[2 * b] = red[0];
       g.red[2 * b + 1] = red[NT];
     }
@@ -343,8 +368,6 @@ GemmArgs make_args(int op_a, int op_b, double alpha, const QView& A, const QView
 int64_t choose_splits(int64_t tiles, int64_t K, int64_t other_ctas) {
   // Split K so the launch fills whole waves of 148 SMs (1 CTA/SM): maximise
   // ctas / (waves * 148) with a small per-split penalty, >= 24 k-steps each.
-  // up to two waves of splits: single-tile products with huge K (C5's Grams,
-  // 40 x 40 over 2M rows) need them, and their partials are tiny
   const int64_t maxs = std::max<int64_t>(1, std::min<int64_t>(296, K / (24 * BK)));
   int64_t best = 1;
   double best_score = -1.0;
@@ -359,6 +382,95 @@ int64_t choose_splits(int64_t tiles, int64_t K, int64_t other_ctas) {
   }
   return best;
 }
+
+namespace {
+
+// Tile groups of an M x N output in 64x64 tiles, by decreasing cost: full
+// tiles, then those padded along N / M / both (cost = the fraction of 8x8
+// blocks inside M x N -- padded blocks issue no DMMA, qtile.cuh).
+struct TileGroup {
+  int tm0, tm1, tn0, tn1;
+  double cost;
+};
+std::vector<TileGroup> tile_groups(int64_t M, int64_t N) {
+  const int tm = (int)((M + BM - 1) / BM), tn = (int)((N + BN - 1) / BN);
+  const int tmf = (int)(M / BM), tnf = (int)(N / BN);
+  auto frac = [](int64_t valid) { return (double)((valid + 7) / 8) / 8.0; };
+  const double fr = frac(M - (int64_t)tmf * BM), fc = frac(N - (int64_t)tnf * BN);
+  std::vector<TileGroup> g;
+  if (tmf > 0 && tnf > 0) g.push_back({0, tmf, 0, tnf, 1.0});
+  if (tn > tnf && tmf > 0) g.push_back({0, tmf, tnf, tn, fc});
+  if (tm > tmf && tnf > 0) g.push_back({tmf, tm, 0, tnf, fr});
+  if (tm > tmf && tn > tnf) g.push_back({tmf, tm, tnf, tn, fr * fc});
+  std::stable_sort(g.begin(), g.end(), [](const TileGroup& a, const TileGroup& b) { return a.cost > b.cost; });
+  return g;
+}
+
+// Makespan (in k-steps of a full tile) of the launch under greedy list
+// scheduling on 148 SMs, CTAs in kernel order; plus the split-K reduction.
+double simulate_gemm(const std::vector<TileGroup>& groups, int64_t M, int64_t N, int64_t K, int64_t z) {
+  const int64_t kc = ((K + z - 1) / z + BK - 1) / BK * BK;
+  const int64_t nz = (K + kc - 1) / kc;
+  std::map<double, int64_t> sm{{0.0, 148}};
+  for (const TileGroup& g : groups) {
+    const double d = (double)(kc / BK) * g.cost + 3.0;  // + prologue / epilogue
+    int64_t c = (int64_t)(g.tm1 - g.tm0) * (g.tn1 - g.tn0) * nz;
+    while (c > 0) {
+      auto it = sm.begin();
+      const double t0 = it->first;
+      const int64_t k = it->second;
+      sm.erase(it);
+      const int64_t take = std::min(c, k);
+      if (k > take) sm[t0] += k - take;
+      sm[t0 + d] += take;
+      c -= take;
+    }
+  }
+  const double red = nz > 1 ? (double)nz * (double)M * (double)N * 32.0 / 25e6 : 0.0;
+  return sm.rbegin()->first + red;
+}
+
+int64_t choose_gemm_splits(int64_t M, int64_t N, int64_t K) {
+  static std::map<std::array<int64_t, 3>, int64_t> cache;
+  const std::array<int64_t, 3> key{M, N, K};
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  const std::vector<TileGroup> groups = tile_groups(M, N);
+  const int64_t maxs = std::max<int64_t>(1, std::min<int64_t>(296, K / (8 * BK)));
+  int64_t best = 1;
+  double best_t = 1e300;
+  for (int64_t z = 1; z <= maxs; z = z < 16 ? z + 1 : std::max(z + 1, z * 9 / 8)) {
+    const double t = simulate_gemm(groups, M, N, K, z);
+    if (t < best_t - 1e-9) {
+      best_t = t;
+      best = z;
+    }
+  }
+  cache[key] = best;
+  return best;
+}
+
+// Fill the CTA schedule of g (groups in cost order, nsplit CTAs per tile);
+// returns the number of CTAs.
+int64_t fill_schedule(GemmArgs& g, int64_t M, int64_t N, int nsplit) {
+  const std::vector<TileGroup> groups = tile_groups(M, N);
+  g.nsplit = nsplit;
+  g.ngroups = (int)groups.size();
+  g.tn_all = (int)((N + BN - 1) / BN);
+  int64_t start = 0;
+  for (int i = 0; i < g.ngroups; ++i) {
+    g.g_tm0[i] = groups[i].tm0;
+    g.g_tm1[i] = groups[i].tm1;
+    g.g_tn0[i] = groups[i].tn0;
+    g.g_tn1[i] = groups[i].tn1;
+    g.g_start[i] = start;
+    start += (int64_t)(groups[i].tm1 - groups[i].tm0) * (groups[i].tn1 - groups[i].tn0) * nsplit;
+  }
+  g.g_start[g.ngroups] = start;
+  return start;
+}
+
+}  // namespace
 
 void splitk_reduce(Ctx& ctx, const double* ws, int nz, const QView& C, double alpha, double beta) {
   const int64_t total = 4 * C.rows * C.cols;
@@ -391,14 +503,15 @@ void qgemm(Ctx& ctx, int op_a, int op_b, double alpha, const QView& A, const QVi
   if (force_splits > 0) {
     nsplit = force_splits;
   } else if (K > 0) {
-    nsplit = choose_splits(tiles, K, 1);
+    nsplit = choose_gemm_splits(M, N, K);
   }
   int64_t kchunk = (K + nsplit - 1) / nsplit;
   kchunk = ((kchunk + BK - 1) / BK) * BK;
   if (kchunk == 0) kchunk = BK;
   nsplit = K > 0 ? (K + kchunk - 1) / kchunk : 1;
   g.kchunk = kchunk;
-  dim3 grid((unsigned)tn, (unsigned)tm, (unsigned)nsplit);
+  const int64_t ctas = fill_schedule(g, M, N, (int)nsplit);
+  dim3 grid((unsigned)ctas);
   if (nsplit > 1) {
     DeviceBuffer ws(ctx, (size_t)nsplit * 4 * M * N * sizeof(double));
     g.ws = ws.as<double>();
@@ -420,8 +533,10 @@ void qgemm_residual(Ctx& ctx, const QView& R, const QView& H, const QView& X, do
   if (g.kchunk == 0) g.kchunk = BK;
   DeviceBuffer red(ctx, (size_t)tm * tn * 2 * sizeof(double));
   g.red = red.as<double>();
-  dim3 grid((unsigned)tn, (unsigned)tm, 1);
-  if (M > 0 && N > 0) dispatch<1>(false, false, grid, ctx.stream, g);
+  if (M > 0 && N > 0) {
+    dim3 grid((unsigned)fill_schedule(g, M, N, 1));
+    dispatch<1>(false, false, grid, ctx.stream, g);
+  }
   residual_finish_kernel<<<1, 32, 0, ctx.stream>>>(g.red, tm * tn, d_out2);
   QLRA_LAUNCH_CHECK();
   count_launch();
