@@ -403,7 +403,8 @@ def main():
                          "peak_source": "FP64 measured in this run (DMMA m8n8k4 / DFMA microbenchmarks; "
                                         "MEASURED_PEAKS.json has no FP64 entry): " + json.dumps(peaks),
                          "note": "FP64 tensor pipe (DMMA); per-unit = 32 flop per quaternion MAC, "
-                                 "a launch covers one L2-resident row panel: 32*rows*n*(s+l) flop"},
+                                 "a launch covers one row panel of A (<= 2 GB; C2: the whole block): "
+                                 "32*rows*n*(s+l) flop"},
             "rangefinder_used": used["rangefinder"], "rel_error": res / an, "e2e": e2e, "gpu_launches": int(launches), "clocks": clk.summary(),
             "cpu_baseline": cpu,
         }

@@ -127,7 +127,7 @@ __global__ void __launch_bounds__(NT, 1) sketch_fused_kernel(FusedArgs f) {
 
 }  // namespace
 
-const char* sketch_kernel_name() { return "sketch_fused_kernel(dmma_64x64x8,L2-panel)"; }
+const char* sketch_kernel_name() { return "sketch_fused_kernel(dmma_64x64x8, mbarrier ring, panels <= 2 GB)"; }
 
 namespace {
 
