@@ -10,6 +10,9 @@
 
 #include <cmath>
 #include <memory>
+#include <tuple>
+#include <mutex>
+#include <map>
 #include <cstring>
 #include <limits>
 #include <vector>
@@ -26,6 +29,22 @@ namespace qlra_dev {
 std::atomic<int64_t>& launch_counter() {
   static std::atomic<int64_t> c{0};
   return c;
+}
+
+// Kernel attributes apply per device; set each (device, function, attribute)
+// once to the largest value requested, under a lock (contexts on several
+// devices or host threads may race here).
+void set_func_attr(const void* func, cudaFuncAttribute attr, int value) {
+  static std::mutex mu;
+  static std::map<std::tuple<int, const void*, int>, int> done;
+  int dev = 0;
+  QLRA_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(mu);
+  const auto key = std::make_tuple(dev, func, (int)attr);
+  auto it = done.find(key);
+  if (it != done.end() && it->second >= value) return;
+  QLRA_CUDA(cudaFuncSetAttribute(func, attr, value));
+  done[key] = value;
 }
 
 void allreduce_sum(Ctx& ctx, double* buf, size_t count) {

@@ -16,6 +16,8 @@ namespace qlra_dev {
 
 // Launch counter (evidence of device work; exported via qlra_ctx_launch_count).
 std::atomic<int64_t>& launch_counter();
+// thread-safe, per-device cudaFuncSetAttribute (largest value wins)
+void set_func_attr(const void* func, cudaFuncAttribute attr, int value);
 inline void count_launch() { launch_counter().fetch_add(1, std::memory_order_relaxed); }
 
 // One context per (host thread, device): stream, NCCL communicator, errors.

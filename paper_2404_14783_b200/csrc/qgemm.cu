@@ -12,6 +12,7 @@
 #include <algorithm>
 #include <array>
 #include <map>
+#include <mutex>
 #include <vector>
 #include "common.cuh"
 #include "kernels.cuh"
@@ -323,12 +324,8 @@ void small_gemm(Ctx& ctx, bool ca, bool cb, const GemmArgs& ga, int64_t M, int64
 
 template <bool CA, bool CB, int MODE>
 void set_attr() {
-  static bool done = false;
-  if (!done) {
-    QLRA_CUDA(cudaFuncSetAttribute(qgemm_kernel<CA, CB, MODE>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)qt::SMEM_BYTES));
-    done = true;
-  }
+  set_func_attr((const void*)qgemm_kernel<CA, CB, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                (int)qt::SMEM_BYTES);
 }
 
 template <int MODE>
@@ -431,10 +428,14 @@ double simulate_gemm(const std::vector<TileGroup>& groups, int64_t M, int64_t N,
 }
 
 int64_t choose_gemm_splits(int64_t M, int64_t N, int64_t K) {
+  static std::mutex mu;
   static std::map<std::array<int64_t, 3>, int64_t> cache;
   const std::array<int64_t, 3> key{M, N, K};
-  auto it = cache.find(key);
-  if (it != cache.end()) return it->second;
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+  }
   const std::vector<TileGroup> groups = tile_groups(M, N);
   const int64_t maxs = std::max<int64_t>(1, std::min<int64_t>(296, K / (8 * BK)));
   int64_t best = 1;
@@ -446,6 +447,7 @@ int64_t choose_gemm_splits(int64_t M, int64_t N, int64_t K) {
       best = z;
     }
   }
+  std::lock_guard<std::mutex> lock(mu);
   cache[key] = best;
   return best;
 }

@@ -20,6 +20,7 @@
 #include <cstdlib>
 #include <functional>
 #include <map>
+#include <mutex>
 #include <vector>
 
 #include "common.cuh"
@@ -176,10 +177,14 @@ double simulate_panel(int64_t rp, int64_t n, int64_t s, int64_t l, int zy, int z
 }
 
 std::pair<int, int> choose_panel_splits(int64_t rp, int64_t n, int64_t s, int64_t l) {
+  static std::mutex mu;
   static std::map<std::array<int64_t, 4>, std::pair<int, int>> cache;
   const std::array<int64_t, 4> key{rp, n, s, l};
-  auto it = cache.find(key);
-  if (it != cache.end()) return it->second;
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+  }
   const int64_t wt = ((l + BM - 1) / BM) * ((n + BN - 1) / BN);
   // W split-K only while W has fewer than 4 waves of tiles (its partials are
   // l x n each: 868 MB at C4)
@@ -199,7 +204,10 @@ std::pair<int, int> choose_panel_splits(int64_t rp, int64_t n, int64_t s, int64_
       const double mk = simulate_panel(rp, n, s, l, zy, zw);
       if (mk < best - 1e-9) { best = mk; arg = {zy, zw}; }
     }
-  cache[key] = arg;
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    cache[key] = arg;
+  }
   if (std::getenv("QLRA_DEBUG_SPLITS")) {
     // ideal = total cost / 148 (perfect balance, no per-CTA overhead)
     const int64_t y_tm = (rp + BM - 1) / BM, y_tn = (s + BN - 1) / BN, w_tm = (l + BM - 1) / BM,
@@ -295,12 +303,8 @@ void sketch_panel(Ctx& ctx, const QView& om, const QView& ps, int64_t pc0, const
 }
 
 void set_kernel_attrs() {
-  static bool attr = false;
-  if (!attr) {
-    QLRA_CUDA(cudaFuncSetAttribute(sketch_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)qt::SMEM_BYTES));
-    attr = true;
-  }
+  set_func_attr((const void*)sketch_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                (int)qt::SMEM_BYTES);
 }
 
 // Rows per fused launch.  Device-resident A: panels of up to kPanelBytes --

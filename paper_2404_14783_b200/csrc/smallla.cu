@@ -1368,11 +1368,7 @@ void tridiag_all_eigvals(Ctx& ctx, const double* d, const double* e, int64_t n, 
   count_launch();
   const size_t smem = sizeof(double) * 2 * (size_t)n;
   const int use_smem = smem <= 96 * 1024 ? 1 : 0;
-  static bool attr = false;
-  if (!attr) {
-    QLRA_CUDA(cudaFuncSetAttribute(k_multisect_all, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
-    attr = true;
-  }
+  set_func_attr((const void*)k_multisect_all, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
   const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((n + MSA_WARPS - 1) / MSA_WARPS, 4 * 148));
   k_multisect_all<<<(unsigned)blocks, 32 * MSA_WARPS, use_smem ? smem : 0, ctx.stream>>>(hdr, sd, se2, n,
                                                                                         use_smem, d_w);
@@ -1405,26 +1401,16 @@ void small_quat_herm_eigvals(Ctx& ctx, const QView& a, double* d_w, bool extreme
   } else if (n > 48 && n <= QTC_MAX) {
     const int64_t rmax = (n + QTC - 1) / QTC;
     const size_t csm = sizeof(Q4) * (size_t)(rmax * n + 3 * n);
-    static size_t cattr = 0;
-    static bool nonportable = false;
-    if (!nonportable) {
-      QLRA_CUDA(cudaFuncSetAttribute(k_qtridiag_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-      nonportable = true;
-    }
-    if (csm > 48 * 1024 && csm > cattr) {
-      QLRA_CUDA(cudaFuncSetAttribute(k_qtridiag_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm));
-      cattr = csm;
-    }
+    set_func_attr((const void*)k_qtridiag_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (csm > 48 * 1024)
+      set_func_attr((const void*)k_qtridiag_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm);
     k_qtridiag_cluster<<<QTC, QTC_THREADS, csm, ctx.stream>>>(a, d, e);
     QLRA_LAUNCH_CHECK();
     count_launch();
   } else {  // n <= 48: one CTA, packed triangle in shared memory
     const size_t tsm = sizeof(Q4) * (size_t)(n * (n + 1) / 2 + 2 * n);
-    static size_t tattr = 0;
-    if (tsm > 48 * 1024 && tsm > tattr) {
-      QLRA_CUDA(cudaFuncSetAttribute(k_qtridiag_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm));
-      tattr = tsm;
-    }
+    if (tsm > 48 * 1024)
+      set_func_attr((const void*)k_qtridiag_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm);
     k_qtridiag_smem<<<1, 512, tsm, ctx.stream>>>(a, d, e);
     QLRA_LAUNCH_CHECK();
     count_launch();
@@ -1443,11 +1429,8 @@ void small_quat_eigh(Ctx& ctx, const QView& a, double* d_w, const QView& vecs, i
   if (n == 0) return;
   const int64_t np = n + (n & 1);
   const size_t smem = ((np * sizeof(int) + 15) / 16) * 16 + sizeof(double) * 6 * (size_t)(np / 2 + 1);
-  static size_t attr = 0;
-  if (smem > 48 * 1024 && smem > attr) {
-    QLRA_CUDA(cudaFuncSetAttribute(k_quat_jacobi, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = smem;
-  }
+  if (smem > 48 * 1024)
+    set_func_attr((const void*)k_quat_jacobi, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   DevQMat v(ctx, n, n);
   DeviceBuffer w(ctx, sizeof(double) * (size_t)n);
   k_quat_jacobi<<<1, SNT, smem, ctx.stream>>>(a, v.v, w.as<double>(), max_sweeps, nullptr);
@@ -1488,16 +1471,9 @@ void chol_inv_launch(Ctx& ctx, const QView& g, const QView& r, const QView& rinv
   CholArgs a{g, r, rinv, d_rdiag, d_info};
   const int64_t nbt = (s + CTB - 1) / CTB;
   const size_t csm = sizeof(Tile) * (size_t)(nbt + CHB + 3);
-  static size_t cattr = 0;
-  static bool nonportable = false;
-  if (!nonportable) {
-    QLRA_CUDA(cudaFuncSetAttribute(k_chol_inv_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    nonportable = true;
-  }
-  if (csm > 48 * 1024 && csm > cattr) {
-    QLRA_CUDA(cudaFuncSetAttribute(k_chol_inv_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm));
-    cattr = csm;
-  }
+  set_func_attr((const void*)k_chol_inv_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  if (csm > 48 * 1024)
+    set_func_attr((const void*)k_chol_inv_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm);
   k_chol_inv_cluster<<<CHC, 256, csm, ctx.stream>>>(a);
   QLRA_LAUNCH_CHECK();
   count_launch();
@@ -1529,12 +1505,8 @@ bool blocked_chol_inv(Ctx& ctx, const QView& g, const QView& rinv, std::vector<d
     }
     return true;
   }
-  static bool attr = false;
   const size_t smem = sizeof(Q4) * CB * CB;
-  if (!attr) {
-    QLRA_CUDA(cudaFuncSetAttribute(k_qchol_block, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = true;
-  }
+  set_func_attr((const void*)k_qchol_block, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   DevQMat work(ctx, s, s), r(ctx, s, s);
   copy_qmat(ctx, g, work.v);
   r.zero(ctx);

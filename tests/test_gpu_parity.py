@@ -502,3 +502,40 @@ def test_sketch_from_qmat_file(ctx, tmp_path):  # CS-2: qlra sketch --input A.qm
     st = Q.sketch_from_qmat_file(tmp_path / "a.qmat", 5, 10, 20, 7, 8, block_rows=256, ctx=ctx)
     y, w = O.make_sketch(a, 5, 10, 20, 7, 8)
     assert rel_diff(host(st.y), y) < 1e-13 and rel_diff(host(st.w), w) < 1e-13
+
+
+def test_two_contexts_two_threads(ctx):
+    """One context per host thread (SURVEY 8(b) threading contract): two
+    threads drive their own contexts concurrently -- shared caches and kernel
+    attributes are locked -- and reproduce the sequential results bitwise."""
+    import threading
+
+    from paper_2404_14783_b200 import qlra as Q
+    jobs = [planted_conditioned_matrix(600 + 50 * k, 40 + 10 * k, 1e3, 300 + k) for k in range(2)]
+
+    def run(y, c):
+        rep = Q.pseudo_qr(dev(y), ctx=c)
+        g = Q.qmat_mul(rep.h, rep.h, op_a=Q.OP_C, ctx=c)
+        c.synchronize()
+        return host(rep.h), host(g)
+
+    seq = [run(y, ctx) for y in jobs]
+    streams = [torch.cuda.Stream() for _ in jobs]
+    contexts = []
+    for st in streams:  # each context on its own stream, shared with torch in its thread
+        c = Q.Context(0, use_torch_stream=False)
+        c.set_stream(st)
+        contexts.append(c)
+    out = [None, None]
+
+    def worker(k):
+        with torch.cuda.stream(streams[k]):
+            out[k] = run(jobs[k], contexts[k])
+
+    th = [threading.Thread(target=worker, args=(k,)) for k in range(2)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    for k in range(2):
+        assert np.array_equal(out[k][0], seq[k][0]) and np.array_equal(out[k][1], seq[k][1])
