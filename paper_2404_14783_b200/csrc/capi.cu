@@ -432,38 +432,73 @@ void orthonormal_completion(Ctx& ctx, const QView& hr, const QView& c_out, int64
     fail(QLRA_ERR_INTERNAL, "orthonormal completion failed");
 }
 
-// pseudo_svd for numerically rank-deficient Y (where CholeskyQR breaks
-// down): the reference's bad-block route (rangefinders.cpp:33-41,
-// factorizations.cpp:83-152) becomes, in quaternion arithmetic, an
-// eigendecomposition G = Y^*Y = V L V^* (Jacobi, no pair splitting), the
-// range basis Y V_r L_r^{-1/2} for the numerically nonzero part
-// (re-orthonormalised), and an orthonormal completion for the rest.
-void pseudo_svd_rank_deficient(Ctx& ctx, const QView& y, const QView& h, int64_t m_global,
-                               int64_t row0, uint64_t seed) {
-  const int64_t s = y.cols;
+// pseudo_svd for sketches CholeskyQR cannot take (numerically rank-deficient
+// or with kappa(Y)^2 beyond double precision): the reference's SVD-and-pairs
+// route (rangefinders.cpp:18-62, factorizations.cpp:60-81) keeps every
+// singular pair above kPairFloorRel * sigma_1 (= 1e-13) and completes the
+// rest.  A Gram eigendecomposition resolves only sigma_i >~ 3e-7 sigma_max,
+// so the range is taken in graded levels: at each level the eigenvectors of
+// G_k = Y_k^* Y_k with lambda > 64 u s lambda_max(G_k) (and above the floor)
+// give the block Y_k V L^{-1/2}, which is re-projected against the basis so
+// far (twice), orthonormalised, appended, and projected out of Y_k (twice).
+// A kappa=1e12 sketch needs two levels.  Returns sqrt(lambda_1 / lambda_min)
+// over the kept directions when all s are kept (the sigma estimates of each
+// level are the singular values of the deflated remainder), else inf.
+double pseudo_svd_graded(Ctx& ctx, const QView& y, const QView& h, int64_t m_global, int64_t row0,
+                         uint64_t seed) {
+  const int64_t s = y.cols, rows = y.rows;
+  constexpr double kFloorRel = 1e-13;  // kPairFloorRel, factorizations.hpp:64
+  DevQMat yk(ctx, rows, s);
+  copy_qmat(ctx, y, yk.v);
   DevQMat g(ctx, s, s), vec(ctx, s, s);
-  gram(ctx, y, g.v);
   DeviceBuffer w(ctx, sizeof(double) * (size_t)s);
-  small_quat_eigh(ctx, g.v, w.as<double>(), vec.v);
-  const std::vector<double> lam = to_host(ctx, w.as<double>(), (size_t)s);
-  const double lmax = std::max(0.0, lam[0]);
-  const double thr = std::max(64.0 * kUnit * (double)s * lmax, 1e-300);
   int64_t r = 0;
-  while (r < s && lam[r] > thr) ++r;
-  if (r > 0) {
-    DevQMat t(ctx, y.rows, r), sq(ctx, 1, 1);
-    qgemm(ctx, QLRA_OP_N, QLRA_OP_N, 1.0, y, sub(vec.v, 0, 0, s, r), 0.0, t.v);
-    std::vector<double> is(r);
-    for (int64_t i = 0; i < r; ++i) is[i] = 1.0 / std::sqrt(lam[i]);
-    DeviceBuffer d_is(ctx, sizeof(double) * (size_t)r);
-    QLRA_CUDA(cudaMemcpyAsync(d_is.ptr, is.data(), sizeof(double) * r, cudaMemcpyHostToDevice, ctx.stream));
+  double lam1 = 0.0, lam_min = std::numeric_limits<double>::infinity();
+  for (int level = 0; r < s && level < 8; ++level) {
+    gram(ctx, yk.v, g.v);
+    small_quat_eigh(ctx, g.v, w.as<double>(), vec.v);
+    const std::vector<double> lam = to_host(ctx, w.as<double>(), (size_t)s);
+    if (level == 0) lam1 = std::max(0.0, lam[0]);
+    const double thr = std::max({64.0 * kUnit * (double)s * std::max(0.0, lam[0]),
+                                 kFloorRel * kFloorRel * lam1, 1e-300});
+    int64_t cnt = 0;
+    while (cnt < s - r && lam[cnt] > thr) ++cnt;
+    if (cnt == 0) break;
+    lam_min = std::min(lam_min, lam[cnt - 1]);
+    DevQMat t(ctx, rows, cnt);
+    qgemm(ctx, QLRA_OP_N, QLRA_OP_N, 1.0, yk.v, sub(vec.v, 0, 0, s, cnt), 0.0, t.v);
+    std::vector<double> is(cnt);
+    for (int64_t i = 0; i < cnt; ++i) is[i] = 1.0 / std::sqrt(lam[i]);
+    DeviceBuffer d_is(ctx, sizeof(double) * (size_t)cnt);
+    QLRA_CUDA(cudaMemcpyAsync(d_is.ptr, is.data(), sizeof(double) * cnt, cudaMemcpyHostToDevice, ctx.stream));
     scale_cols(ctx, t.v, d_is.as<double>(), false, 0.0, t.v);
-    if (!cholesky_qr(ctx, t.v, sub(h, 0, 0, y.rows, r), false, m_global, nullptr))
+    const QView hp = sub(h, 0, 0, rows, r);
+    if (r > 0) {
+      DevQMat c(ctx, r, cnt);
+      for (int pass = 0; pass < 2; ++pass) {
+        qgemm(ctx, QLRA_OP_C, QLRA_OP_N, 1.0, hp, t.v, 0.0, c.v);
+        allreduce_qmat(ctx, c.v);
+        qgemm(ctx, QLRA_OP_N, QLRA_OP_N, -1.0, hp, c.v, 1.0, t.v);
+      }
+    }
+    const QView hn = sub(h, 0, r, rows, cnt);
+    if (!cholesky_qr(ctx, t.v, hn, false, m_global, nullptr))
       fail(QLRA_ERR_INTERNAL, "pseudo_svd: range basis orthonormalisation failed");
+    r += cnt;
+    if (r == s) break;
+    // Y_{k+1} = (I - H H^*) Y_k over the basis so far, twice
+    const QView hr = sub(h, 0, 0, rows, r);
+    DevQMat c(ctx, r, s);
+    for (int pass = 0; pass < 2; ++pass) {
+      qgemm(ctx, QLRA_OP_C, QLRA_OP_N, 1.0, hr, yk.v, 0.0, c.v);
+      allreduce_qmat(ctx, c.v);
+      qgemm(ctx, QLRA_OP_N, QLRA_OP_N, -1.0, hr, c.v, 1.0, yk.v);
+    }
   }
   if (r < s)
-    orthonormal_completion(ctx, sub(h, 0, 0, y.rows, r), sub(h, 0, r, y.rows, s - r), row0, m_global,
+    orthonormal_completion(ctx, sub(h, 0, 0, rows, r), sub(h, 0, r, rows, s - r), row0, m_global,
                            rng_substream(rng_key(seed), 0x6261645F626C6BULL));
+  return r == s && lam_min > 0.0 ? std::sqrt(lam1 / lam_min) : std::numeric_limits<double>::infinity();
 }
 
 void rank_check(const std::vector<double>& d) {
@@ -693,10 +728,10 @@ void pseudo_svd_dev(Ctx& c, const QView& Y, const QView& H, uint64_t seed, qlra_
   qlra_rangefinder_report_t r{};
   r.method = QLRA_PSEUDO_SVD;
   // Full-rank sketches: quaternion CholeskyQR2 (shifted CholeskyQR3 when
-  // needed).  Rank-deficient ones: eigen route + orthonormal completion.
+  // needed).  Others: graded eigen route + orthonormal completion.
   // kappa(Y) comes from the eigenvalues of the same Gram CholeskyQR2 starts
   // from, computed on the side stream while CholeskyQR2 runs; a non-finite
-  // kappa routes to the rank-deficient path as before.
+  // kappa (kappa^2 past 1/u) or a CholeskyQR breakdown takes the graded route.
   DevQMat g(c, s, s);
   gram(c, Y, g.v);
   bool qr_ok = false;
@@ -707,7 +742,7 @@ void pseudo_svd_dev(Ctx& c, const QView& Y, const QView& H, uint64_t seed, qlra_
     r.kappa_before = kappa_from_eigs(eig.get());
   }
   if (!std::isfinite(r.kappa_before) || !qr_ok)
-    pseudo_svd_rank_deficient(c, Y, H, m, global_row0(c, Y.rows), seed);
+    r.kappa_before = pseudo_svd_graded(c, Y, H, m, global_row0(c, Y.rows), seed);
   if (kappa_after_async) {
     // the caller overlaps kappa(H)'s eigenvalues with its next work
     DevQMat gh(c, s, s);
