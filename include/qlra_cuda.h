@@ -187,6 +187,17 @@ int qlra_pseudo_svd(qlra_ctx_t* ctx, const qlra_qmat_t* y, uint64_t seed, qlra_q
 int qlra_qb_solve(qlra_ctx_t* ctx, const qlra_spec_t* psi, int64_t row0, const qlra_qmat_t* h,
                   const qlra_qmat_t* w, qlra_qmat_t* x);
 
+/* The whole QB stage, qb_stage_with_psi (sketching.cpp:169-194): the
+ * rangefinder on Y (`method`, `rangefinder_seed`, `cfg` as in qlra_pseudo_qr /
+ * qlra_pseudo_svd; NULL cfg = defaults) into H, then X as qlra_qb_solve.  With
+ * pseudo-QR on one rank the solve starts inside the rangefinder: X = C^{-1} X0
+ * where H = Q0 C and X0 = (Psi Q0)^+ W runs on a second stream; results agree
+ * with the two separate calls to rounding.  syncs. */
+int qlra_qb_stage(qlra_ctx_t* ctx, const qlra_spec_t* psi, int64_t row0, const qlra_qmat_t* y,
+                  const qlra_qmat_t* w, int method, uint64_t rangefinder_seed,
+                  const qlra_pseudo_qr_config_t* cfg, qlra_qmat_t* h, qlra_qmat_t* x,
+                  qlra_rangefinder_report_t* report);
+
 /* ------------------------------------------------ host-side one-pass --- */
 /* one_pass_approx through the QB stage (sketching.cpp:250-263) for a host
  * resident row shard of A (pinned memory overlaps best): the sketch streams A

@@ -71,6 +71,7 @@ def lib():
         "qlra_pseudo_qr": ([VP, PQ, P(PseudoQrConfig), PQ, P(Report)], INT),
         "qlra_pseudo_svd": ([VP, PQ, U64, PQ, P(Report)], INT),
         "qlra_qb_solve": ([VP, PS, I64, PQ, PQ, PQ], INT),
+        "qlra_qb_stage": ([VP, PS, I64, PQ, PQ, INT, U64, P(PseudoQrConfig), PQ, PQ, P(Report)], INT),
         "qlra_one_pass_qb_host": ([VP, PQ, I64, PS, PS, INT, U64, P(PseudoQrConfig), I64, PQ, PQ, P(Report)],
                                   INT),
         "qlra_residual_fro": ([VP, PQ, PQ, PQ, P(F64), P(F64)], INT),

@@ -13,6 +13,9 @@
 #include <tuple>
 #include <mutex>
 #include <map>
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <vector>
@@ -281,20 +284,26 @@ bool cholesky_qr_general(Ctx& ctx, const QView& y, const QView& h, bool complex_
                          std::vector<double>* rdiag, bool distributed, DevQMat* rinv, DevQMat* rfac,
                          DeferredQ* defer);
 
-// CholeskyQR2 with both passes queued back to back and ONE host sync for
-// both pass statuses and diagonals (s <= the single-launch Cholesky limit);
-// a breakdown of pass 1 falls back to the general path (shifted CholeskyQR3).
-// gram1 (optional): the already reduced Gram of y (quaternion; the complex
-// part is taken here when complex_mode), saving the first tall product.
-bool cholesky_qr(Ctx& ctx, const QView& y, const QView& h, bool complex_mode, int64_t m_global,
-                 std::vector<double>* rdiag, bool distributed = true, DevQMat* rinv = nullptr,
-                 DevQMat* rfac = nullptr, DeferredQ* defer = nullptr, const QView* gram1 = nullptr) {
+// CholeskyQR2 queued without a host sync (s <= the single-launch Cholesky
+// limit): both passes back to back, statuses and diagonals left on the
+// device.  cqr2_status() reads them with ONE sync.
+struct Cqr2Pending {
+  int64_t s = 0;
+  DevQMat t1, r1, r2, r1inv, r2inv;
+  DeviceBuffer info, dg;
+};
+void cqr2_enqueue(Ctx& ctx, const QView& y, const QView& h, bool complex_mode, bool distributed,
+                  const QView* gram1, bool form_q, Cqr2Pending& p) {
   const int64_t s = y.cols;
-  if (s == 0 || s > chol_inv_async_max())
-    return cholesky_qr_general(ctx, y, h, complex_mode, m_global, rdiag, distributed, rinv, rfac, defer);
-  DevQMat g1(ctx, s, s), g2(ctx, s, s), t1(ctx, y.rows, s);
-  DevQMat r1(ctx, s, s), r2(ctx, s, s), r1inv(ctx, s, s), r2inv(ctx, s, s);
-  DeviceBuffer info(ctx, 2 * sizeof(int)), dg(ctx, 2 * sizeof(double) * (size_t)s);
+  p.s = s;
+  DevQMat g1(ctx, s, s), g2(ctx, s, s);
+  p.t1 = DevQMat(ctx, y.rows, s);
+  p.r1 = DevQMat(ctx, s, s);
+  p.r2 = DevQMat(ctx, s, s);
+  p.r1inv = DevQMat(ctx, s, s);
+  p.r2inv = DevQMat(ctx, s, s);
+  p.info = DeviceBuffer(ctx, 2 * sizeof(int));
+  p.dg = DeviceBuffer(ctx, 2 * sizeof(double) * (size_t)s);
   auto gram_of = [&](const QView& a, const QView& g) {
     if (distributed) gram(ctx, a, g);
     else qgemm(ctx, QLRA_OP_C, QLRA_OP_N, 1.0, a, a, 0.0, g);
@@ -306,34 +315,57 @@ bool cholesky_qr(Ctx& ctx, const QView& y, const QView& h, bool complex_mode, in
   } else {
     gram_of(y, g1.v);
   }
-  chol_inv_launch(ctx, g1.v, r1.v, r1inv.v, info.as<int>(), dg.as<double>());
-  qgemm(ctx, QLRA_OP_N, QLRA_OP_N, 1.0, y, r1inv.v, 0.0, t1.v);
-  gram_of(t1.v, g2.v);
-  chol_inv_launch(ctx, g2.v, r2.v, r2inv.v, info.as<int>() + 1, dg.as<double>() + s);
-  if (!defer) qgemm(ctx, QLRA_OP_N, QLRA_OP_N, 1.0, t1.v, r2inv.v, 0.0, h);
+  chol_inv_launch(ctx, g1.v, p.r1.v, p.r1inv.v, p.info.as<int>(), p.dg.as<double>());
+  qgemm(ctx, QLRA_OP_N, QLRA_OP_N, 1.0, y, p.r1inv.v, 0.0, p.t1.v);
+  gram_of(p.t1.v, g2.v);
+  chol_inv_launch(ctx, g2.v, p.r2.v, p.r2inv.v, p.info.as<int>() + 1, p.dg.as<double>() + s);
+  if (form_q) qgemm(ctx, QLRA_OP_N, QLRA_OP_N, 1.0, p.t1.v, p.r2inv.v, 0.0, h);
+}
+// 0: both passes factored (rdiag = diag R1 .* diag R2); 1: pass 1 broke
+// down; 2: pass 2 broke down.
+int cqr2_status(Ctx& ctx, const Cqr2Pending& p, std::vector<double>* rdiag) {
+  const int64_t s = p.s;
   int inf[2] = {0, 0};
   std::vector<double> d((size_t)(2 * s));
-  QLRA_CUDA(cudaMemcpyAsync(inf, info.ptr, 2 * sizeof(int), cudaMemcpyDeviceToHost, ctx.stream));
-  QLRA_CUDA(cudaMemcpyAsync(d.data(), dg.ptr, 2 * sizeof(double) * (size_t)s, cudaMemcpyDeviceToHost, ctx.stream));
+  QLRA_CUDA(cudaMemcpyAsync(inf, p.info.ptr, 2 * sizeof(int), cudaMemcpyDeviceToHost, ctx.stream));
+  QLRA_CUDA(cudaMemcpyAsync(d.data(), p.dg.ptr, 2 * sizeof(double) * (size_t)s, cudaMemcpyDeviceToHost, ctx.stream));
   QLRA_CUDA(cudaStreamSynchronize(ctx.stream));
-  if (inf[0] != 0)  // pass 1 broke down: shifted CholeskyQR3
-    return cholesky_qr_general(ctx, y, h, complex_mode, m_global, rdiag, distributed, rinv, rfac, defer);
-  if (inf[1] != 0) return false;
+  if (inf[0] != 0) return 1;
+  if (inf[1] != 0) return 2;
   if (rdiag) {
     rdiag->resize((size_t)s);
     for (int64_t k = 0; k < s; ++k) (*rdiag)[k] = d[k] * d[s + k];
   }
+  return 0;
+}
+
+// CholeskyQR2 with ONE host sync for both pass statuses and diagonals; a
+// breakdown of pass 1 falls back to the general path (shifted CholeskyQR3).
+// gram1 (optional): the already reduced Gram of y (quaternion; the complex
+// part is taken here when complex_mode), saving the first tall product.
+bool cholesky_qr(Ctx& ctx, const QView& y, const QView& h, bool complex_mode, int64_t m_global,
+                 std::vector<double>* rdiag, bool distributed = true, DevQMat* rinv = nullptr,
+                 DevQMat* rfac = nullptr, DeferredQ* defer = nullptr, const QView* gram1 = nullptr) {
+  const int64_t s = y.cols;
+  if (s == 0 || s > chol_inv_async_max())
+    return cholesky_qr_general(ctx, y, h, complex_mode, m_global, rdiag, distributed, rinv, rfac, defer);
+  Cqr2Pending p;
+  cqr2_enqueue(ctx, y, h, complex_mode, distributed, gram1, /*form_q=*/!defer, p);
+  const int st = cqr2_status(ctx, p, rdiag);
+  if (st == 1)  // pass 1 broke down: shifted CholeskyQR3
+    return cholesky_qr_general(ctx, y, h, complex_mode, m_global, rdiag, distributed, rinv, rfac, defer);
+  if (st == 2) return false;
   if (rinv) {
-    *rinv = std::move(r1inv);
-    chain_rinv(ctx, *rinv, r2inv.v);
+    *rinv = std::move(p.r1inv);
+    chain_rinv(ctx, *rinv, p.r2inv.v);
   }
   if (rfac) {
-    *rfac = std::move(r1);
-    chain_r(ctx, *rfac, r2.v);
+    *rfac = std::move(p.r1);
+    chain_r(ctx, *rfac, p.r2.v);
   }
   if (defer) {
-    defer->base = std::move(t1);
-    defer->rinv_last = std::move(r2inv);
+    defer->base = std::move(p.t1);
+    defer->rinv_last = std::move(p.r2inv);
   }
   return true;
 }
@@ -595,11 +627,222 @@ DevQMat lstsq_operator(Ctx& ctx, const QView& p) {
   return t;
 }
 
+// Launches below go to stream `s` (and its own split-K counters) until the
+// guard ends; stream-ordered buffers created meanwhile live on `s`.
+struct StreamSwap {
+  Ctx& c;
+  cudaStream_t saved;
+  StreamSwap(Ctx& ctx, cudaStream_t s) : c(ctx), saved(ctx.stream) {
+    c.stream = s;
+    std::swap(c.tile_cnt, c.tile_cnt2);
+    std::swap(c.tile_cnt_n, c.tile_cnt2_n);
+  }
+  ~StreamSwap() {
+    std::swap(c.tile_cnt, c.tile_cnt2);
+    std::swap(c.tile_cnt_n, c.tile_cnt2_n);
+    c.stream = saved;
+  }
+};
+
+// The core solve started inside pseudo-QR.  H = Q0 C_k with Q0 = base *
+// rinv_last orthonormal (pseudo_qr_dev), so P = Psi H = P0 C_k with
+// P0 = Psi Q0, and X = P^+ W = C_k^{-1} X0, X0 = P0^+ W.  X0 (Psi, the tall
+// product, CholeskyQR2 of P0 and the wide product) runs on a second stream
+// while the s x s pseudo-QR work runs on the main one; the close is
+// X = (C_k^* C_k)^{-1} C_k^* X0 through the normal equations of the small
+// C_k, whose condition number is kappa_after (exact, by the spectral map),
+// taken only when kappa_after <= kEarlyKappaMax (error ~ u kappa^2 <= 1e-12
+// relative).  Otherwise -- and whenever P0's factorisation or rank test is
+// not clean -- the sequential solve runs and raises what it raises.
+constexpr double kEarlyKappaMax = 100.0;
+struct EarlySolve {
+  Ctx* c = nullptr;
+  const qlra_spec_t* psi = nullptr;
+  int64_t row0 = 0;
+  QView w{};
+  bool started = false;
+  DeferredQ q0;     // Q0 = base * rinv_last (read by both streams)
+  Cqr2Pending cqr;  // P0 = Q_p R_p
+  DevQMat x0;       // P0^+ W (s x n)
+  DevQMat ck;       // C_k
+  DevQMat coef;     // rinv_last C_k (H = base coef, formed on the second stream)
+  double kappa = std::numeric_limits<double>::infinity();
+  // x0_ready: X0 done; done: everything on the second stream (X0, then H)
+  cudaEvent_t x0_ready = nullptr, coef_ready = nullptr, done = nullptr;
+  EarlySolve(Ctx& ctx, const qlra_spec_t& p, int64_t r0, const QView& wv) : c(&ctx), psi(&p), row0(r0), w(wv) {}
+  // main waits for the second stream (before anything it uses is freed)
+  void join() {
+    if (done) QLRA_CUDA(cudaStreamWaitEvent(c->stream, done, 0));
+  }
+  ~EarlySolve() {
+    if (done) cudaStreamWaitEvent(c->stream, done, 0);
+    for (cudaEvent_t e : {x0_ready, coef_ready, done})
+      if (e) cudaEventDestroy(e);
+  }
+  EarlySolve(const EarlySolve&) = delete;
+  EarlySolve& operator=(const EarlySolve&) = delete;
+};
+
+void early_solve_start(Ctx& c, EarlySolve& es, const DeferredQ& q0) {
+  const int64_t s = q0.base.v.cols, rows = q0.base.v.rows, l = es.psi->rows, n = es.w.cols;
+  if (!c.side2) {
+    int lo = 0, hi = 0;
+    QLRA_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    QLRA_CUDA(cudaStreamCreateWithPriority(&c.side2, cudaStreamNonBlocking, lo));  // lowest priority
+  }
+  es.x0 = DevQMat(c, s, n);  // crosses streams: allocated on main before the fork
+  cudaEvent_t fork = nullptr;
+  QLRA_CUDA(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+  QLRA_CUDA(cudaEventCreateWithFlags(&es.done, cudaEventDisableTiming));
+  QLRA_CUDA(cudaEventCreateWithFlags(&es.x0_ready, cudaEventDisableTiming));
+  QLRA_CUDA(cudaEventCreateWithFlags(&es.coef_ready, cudaEventDisableTiming));
+  QLRA_CUDA(cudaEventRecord(fork, c.stream));
+  QLRA_CUDA(cudaStreamWaitEvent(c.side2, fork, 0));
+  QLRA_CUDA(cudaEventDestroy(fork));
+  {
+    StreamSwap on(c, c.side2);
+    DevQMat ps(c, l, rows), pb(c, l, s), p0(c, l, s);
+    launch_gen(c.stream, *es.psi, 0, es.row0, l, rows, ps.v, false);
+    qgemm(c, QLRA_OP_N, QLRA_OP_N, 1.0, ps.v, q0.base.v, 0.0, pb.v);
+    qgemm(c, QLRA_OP_N, QLRA_OP_N, 1.0, pb.v, q0.rinv_last.v, 0.0, p0.v);
+    cqr2_enqueue(c, p0.v, QView{}, /*complex_mode=*/false, /*distributed=*/false, nullptr, /*form_q=*/false,
+                 es.cqr);
+    // X0 = R_p^{-1} Q_p^* W with Q_p = t1 R2^{-1}, R_p^{-1} = R1^{-1} R2^{-1}:
+    // T0 = t1 (R2^{-1} (R1^{-1} R2^{-1})^*), X0 = T0^* W
+    DevQMat rinv(c, s, s), mm(c, s, s), t0(c, l, s);
+    qgemm(c, QLRA_OP_N, QLRA_OP_N, 1.0, es.cqr.r1inv.v, es.cqr.r2inv.v, 0.0, rinv.v);
+    qgemm(c, QLRA_OP_N, QLRA_OP_C, 1.0, es.cqr.r2inv.v, rinv.v, 0.0, mm.v);
+    qgemm(c, QLRA_OP_N, QLRA_OP_N, 1.0, es.cqr.t1.v, mm.v, 0.0, t0.v);
+    qgemm(c, QLRA_OP_C, QLRA_OP_N, 1.0, t0.v, es.w, 0.0, es.x0.v);
+  }
+  QLRA_CUDA(cudaEventRecord(es.x0_ready, c.side2));
+  QLRA_CUDA(cudaEventRecord(es.done, c.side2));
+  es.started = true;
+}
+
+// X = C_k^{-1} X0 expressed as X = Z X0 (Z = (C_k^* C_k)^{-1} C_k^*, s x s).
+// False (nothing usable) unless every condition of the early path holds.
+bool early_solve_close(Ctx& c, EarlySolve& es, DevQMat& z) {
+  if (!es.started) return false;
+  QLRA_CUDA(cudaStreamWaitEvent(c.stream, es.x0_ready, 0));
+  if (!(es.kappa <= kEarlyKappaMax) || !es.ck.buf.ptr) return false;
+  const int64_t s = es.ck.v.rows;
+  DevQMat g(c, s, s), r(c, s, s), ri(c, s, s), ginv(c, s, s);
+  DeviceBuffer info(c, sizeof(int)), dg(c, sizeof(double) * (size_t)s);
+  qgemm(c, QLRA_OP_C, QLRA_OP_N, 1.0, es.ck.v, es.ck.v, 0.0, g.v);
+  chol_inv_launch(c, g.v, r.v, ri.v, info.as<int>(), dg.as<double>());
+  qgemm(c, QLRA_OP_N, QLRA_OP_C, 1.0, ri.v, ri.v, 0.0, ginv.v);
+  z = DevQMat(c, s, s);
+  qgemm(c, QLRA_OP_N, QLRA_OP_C, 1.0, ginv.v, es.ck.v, 0.0, z.v);
+  int inf = 0;
+  QLRA_CUDA(cudaMemcpyAsync(&inf, info.ptr, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+  std::vector<double> rd;
+  if (cqr2_status(c, es.cqr, &rd) != 0 || inf != 0) return false;  // (one sync: the status read)
+  double rmax = 0.0, rmin = std::numeric_limits<double>::infinity();
+  for (double v : rd) {
+    rmax = std::max(rmax, std::fabs(v));
+    rmin = std::min(rmin, std::fabs(v));
+  }
+  // P0's rank test with margin; borderline systems take the sequential
+  // solve and its exact rank test (|r_min| > 1e-14 |r_max| on R of P)
+  return rmin > 1e-10 * rmax;
+}
+
+// X = op(T) B over column blocks: the sequential solve (T (l x s), X = T^* W)
+// or the early one (Z (s x s), X = Z X0).
+struct CoreSolve {
+  DevQMat t;
+  bool adj = true;
+  DevQMat b_own;
+  QView b{};
+  void cols(Ctx& c, int64_t j0, int64_t nj, const QView& x) const {
+    qgemm(c, adj ? QLRA_OP_C : QLRA_OP_N, QLRA_OP_N, 1.0, t.v, sub(b, 0, j0, b.rows, nj), 0.0,
+          sub(x, 0, j0, x.rows, nj));
+  }
+};
+
 // ------------------------------------------------- rangefinders, solve ---
 // Device bodies of pseudo_qr / pseudo_svd / qb_solve (Y, H row-sharded over
 // the ranks; shapes validated by the callers).
+// pseudo-QR's two factorisations for s <= the single-launch Cholesky limit:
+// Y = Q0 R_q (quaternion CholeskyQR2, Q0 deferred) and R_q = C R_c (complex
+// CholeskyQR2).  The complex pass-1 factor is the Cholesky factor of the
+// complex part of R_q^* R_q = Y^* Y, so it is taken from the quaternion
+// pass-1 Gram on the side stream while quaternion pass 2 runs; pass 2 on
+// R_q R1c^{-1} removes its error as usual.  False if quaternion pass 1 broke
+// down (the caller takes the general path); a complex breakdown reruns the
+// complex CholeskyQR2 of R_q the general way.
+bool pqr_factors_fast(Ctx& c, const QView& Y, DeferredQ& q0, DevQMat& rq, DevQMat& rq_inv, DevQMat& cm,
+                      DevQMat& rc, std::vector<double>& rd, EarlySolve* es) {
+  const int64_t s = Y.cols;
+  if (!c.side) QLRA_CUDA(cudaStreamCreateWithFlags(&c.side, cudaStreamNonBlocking));
+  DevQMat gy(c, s, s), gc(c, s, s), r1c(c, s, s), r1c_inv(c, s, s);
+  DeviceBuffer info_c(c, 2 * sizeof(int)), dg_c(c, 2 * sizeof(double) * (size_t)s);
+  gram(c, Y, gy.v);
+  copy_qmat(c, gy.v, gc.v);
+  zero_jk_planes(c, gc.v);
+  cudaEvent_t fork = nullptr, cdone = nullptr;
+  QLRA_CUDA(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+  QLRA_CUDA(cudaEventCreateWithFlags(&cdone, cudaEventDisableTiming));
+  QLRA_CUDA(cudaEventRecord(fork, c.stream));
+  QLRA_CUDA(cudaStreamWaitEvent(c.side, fork, 0));
+  {
+    const cudaStream_t main = c.stream;
+    c.stream = c.side;  // one launch, no split-K counters involved
+    try {
+      chol_inv_launch(c, gc.v, r1c.v, r1c_inv.v, info_c.as<int>(), dg_c.as<double>());
+    } catch (...) {
+      c.stream = main;
+      throw;
+    }
+    c.stream = main;
+  }
+  QLRA_CUDA(cudaEventRecord(cdone, c.side));
+  QLRA_CUDA(cudaEventDestroy(fork));
+  struct Join {  // main waits for the side launch before its buffers are used or freed
+    Ctx& c;
+    cudaEvent_t e;
+    ~Join() {
+      cudaStreamWaitEvent(c.stream, e, 0);
+      cudaEventDestroy(e);
+    }
+  } join{c, cdone};
+  Cqr2Pending p;
+  cqr2_enqueue(c, Y, QView{}, /*complex_mode=*/false, /*distributed=*/true, &gy.v, /*form_q=*/false, p);
+  if (cqr2_status(c, p, nullptr) != 0) return false;
+  rq = std::move(p.r1);
+  chain_r(c, rq, p.r2.v);
+  rq_inv = std::move(p.r1inv);
+  chain_rinv(c, rq_inv, p.r2inv.v);
+  q0.base = std::move(p.t1);
+  q0.rinv_last = std::move(p.r2inv);
+  if (es && c.nranks == 1 && es->psi->rows >= s) early_solve_start(c, *es, q0);
+  QLRA_CUDA(cudaStreamWaitEvent(c.stream, cdone, 0));
+  DevQMat t1c(c, s, s), g2(c, s, s), r2c(c, s, s), r2c_inv(c, s, s);
+  qgemm(c, QLRA_OP_N, QLRA_OP_N, 1.0, rq.v, r1c_inv.v, 0.0, t1c.v);
+  qgemm(c, QLRA_OP_C, QLRA_OP_N, 1.0, t1c.v, t1c.v, 0.0, g2.v);
+  zero_jk_planes(c, g2.v);
+  chol_inv_launch(c, g2.v, r2c.v, r2c_inv.v, info_c.as<int>() + 1, dg_c.as<double>() + s);
+  qgemm(c, QLRA_OP_N, QLRA_OP_N, 1.0, t1c.v, r2c_inv.v, 0.0, cm.v);
+  int inf[2] = {0, 0};
+  std::vector<double> d((size_t)(2 * s));
+  QLRA_CUDA(cudaMemcpyAsync(inf, info_c.ptr, 2 * sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+  QLRA_CUDA(cudaMemcpyAsync(d.data(), dg_c.ptr, 2 * sizeof(double) * (size_t)s, cudaMemcpyDeviceToHost, c.stream));
+  QLRA_CUDA(cudaStreamSynchronize(c.stream));
+  if (inf[0] != 0 || inf[1] != 0) {
+    if (!cholesky_qr(c, rq.v, cm.v, /*complex_mode=*/true, s, &rd, /*distributed=*/false, nullptr, &rc))
+      fail(QLRA_ERR_RANK, "pseudo_qr: sketch numerically rank-deficient; use pseudo_svd");
+    return true;
+  }
+  rd.resize((size_t)s);
+  for (int64_t k = 0; k < s; ++k) rd[k] = d[k] * d[s + k];
+  rc = std::move(r1c);
+  chain_r(c, rc, r2c.v);
+  return true;
+}
+
 void pseudo_qr_dev(Ctx& c, const QView& Y, const QView& H, const qlra_pseudo_qr_config_t& cfg,
-                   qlra_rangefinder_report_t* rep) {
+                   qlra_rangefinder_report_t* rep, EarlySolve* es = nullptr) {
   const int64_t s = Y.cols;
   const int64_t m = global_rows(c, Y.rows);
   if (m <= s) fail(QLRA_ERR_PARAMETER, "pseudo_qr: sketch must be tall (rows > cols)");
@@ -620,14 +863,19 @@ void pseudo_qr_dev(Ctx& c, const QView& Y, const QView& H, const qlra_pseudo_qr_
   // Q0 itself is never formed: Q0 = base * rinv_last, and the pass closes
   // with H = base * (rinv_last * C_k) -- one tall product fewer, same
   // accuracy (rinv_last is the well-conditioned last CholeskyQR factor).
-  DevQMat rq;
-  DeferredQ q0;
-  if (!cholesky_qr(c, Y, QView{}, /*complex_mode=*/false, m, nullptr, /*distributed=*/true, nullptr, &rq, &q0))
-    fail(QLRA_ERR_RANK, "pseudo_qr: sketch numerically rank-deficient; use pseudo_svd");
-  DevQMat cm(c, s, s);
+  DevQMat rq, rq_inv;
+  DeferredQ q0_local;
+  // with an early solve, q0 is read by the second stream: the EarlySolve owns
+  // it (freed after its final join)
+  DeferredQ& q0 = es ? es->q0 : q0_local;
+  DevQMat cm(c, s, s), rc;
   std::vector<double> rd;
-  if (!cholesky_qr(c, rq.v, cm.v, /*complex_mode=*/true, s, &rd, /*distributed=*/false))
-    fail(QLRA_ERR_RANK, "pseudo_qr: sketch numerically rank-deficient; use pseudo_svd");
+  if (s > chol_inv_async_max() || !pqr_factors_fast(c, Y, q0, rq, rq_inv, cm, rc, rd, es)) {
+    if (!cholesky_qr(c, Y, QView{}, /*complex_mode=*/false, m, nullptr, /*distributed=*/true, &rq_inv, &rq, &q0))
+      fail(QLRA_ERR_RANK, "pseudo_qr: sketch numerically rank-deficient; use pseudo_svd");
+    if (!cholesky_qr(c, rq.v, cm.v, /*complex_mode=*/true, s, &rd, /*distributed=*/false, nullptr, &rc))
+      fail(QLRA_ERR_RANK, "pseudo_qr: sketch numerically rank-deficient; use pseudo_svd");
+  }
   rank_check(rd);  // |diag R_c|, rangefinders.cpp:118-126
   qlra_rangefinder_report_t r{};
   r.method = QLRA_PSEUDO_QR;
@@ -639,62 +887,97 @@ void pseudo_qr_dev(Ctx& c, const QView& Y, const QView& H, const qlra_pseudo_qr_
   // follows from G_0's spectrum (exact identity; the reference recomputes it
   // from H_k, rangefinders.cpp:136, which agrees to rounding).
   //
-  // G_0's spectrum is computed on a side stream while the first correction
-  // step's inverse and epsilon are computed speculatively here (almost every
-  // sketch needs that step); they are discarded if kappa_0 <= 10, and any
-  // error they raised surfaces only where the sequential order would raise it.
+  // G_0's spectrum is computed on a side stream while the first two
+  // correction steps (inverse, epsilon and the next coefficient matrix) are
+  // computed speculatively here (almost every sketch needs them); they are
+  // discarded where kappa says stop, and any error they raised surfaces only
+  // where the sequential order would raise it.
+  struct Spec {
+    bool ok = false;
+    int code = 0;
+    std::string msg;
+    double cond = 0.0;
+    double eps = 0.0;
+    DevQMat next;  // C_{k+1} = C_k ((1-eps) I + eps G_k^{-1})
+  };
+  Spec spec[2];
+  const int nspec = std::min(2, cfg.max_correction_steps);
   std::vector<double> lam;
-  DevQMat ginv0;
-  double eps0 = 0.0;
-  bool spec_ok = false;
-  int spec_code = 0;
-  std::string spec_msg;
-  double spec_cond = 0.0;
   {
     SideEigs eig(c, g.v);
-    if (cfg.max_correction_steps > 0) {
+    for (int k = 0; k < nspec; ++k) {
+      Spec& sp = spec[k];
       try {
-        ginv0 = DevQMat(c, s, s);
-        if (!hpd_inverse(c, g.v, ginv0.v, nullptr))
-          fail(QLRA_ERR_SINGULAR, "solve_quaternion_linear: singular system", std::numeric_limits<double>::infinity());
-        eps0 = estimate_epsilon_from_inverse(c, ginv0.v, cfg.power_iters_for_epsilon);
-        spec_ok = true;
+        DevQMat ginv(c, s, s);
+        const QView ck = k == 0 ? cm.v : spec[0].next.v;
+        if (k == 0) {
+          // G_0^{-1} from the factors already at hand: C = R_q R_c^{-1}, so
+          // G_0^{-1} = K K^* with K = R_c R_q^{-1} (no factorisation; the
+          // reference's singularity test is applied from kappa below)
+          DevQMat kf(c, s, s);
+          qgemm(c, QLRA_OP_N, QLRA_OP_N, 1.0, rc.v, rq_inv.v, 0.0, kf.v);
+          qgemm(c, QLRA_OP_N, QLRA_OP_C, 1.0, kf.v, kf.v, 0.0, ginv.v);
+        } else {
+          DevQMat gk(c, s, s);
+          qgemm(c, QLRA_OP_C, QLRA_OP_N, 1.0, ck, ck, 0.0, gk.v);
+          if (!hpd_inverse(c, gk.v, ginv.v, nullptr))
+            fail(QLRA_ERR_SINGULAR, "solve_quaternion_linear: singular system",
+                 std::numeric_limits<double>::infinity());
+        }
+        sp.eps = estimate_epsilon_from_inverse(c, ginv.v, cfg.power_iters_for_epsilon);
+        if (!(sp.eps > 0.0 && sp.eps < 1.0))
+          fail(QLRA_ERR_PARAMETER, "correction_step: epsilon must lie in (0,1)");
+        // H_{k+1} = H_k ((1-eps) I + eps G_k^{-1})  (rangefinders.cpp:99-105)
+        small_axpby_identity(c, 1.0 - sp.eps, sp.eps, ginv.v, mk.v);
+        sp.next = DevQMat(c, s, s);
+        qgemm(c, QLRA_OP_N, QLRA_OP_N, 1.0, ck, mk.v, 0.0, sp.next.v);
+        sp.ok = true;
       } catch (const Status& e) {
         // only the numerical outcomes of the sequential flow are deferred
         if (e.code != QLRA_ERR_SINGULAR && e.code != QLRA_ERR_PARAMETER) throw;
-        spec_code = e.code;
-        spec_msg = e.what();
-        spec_cond = e.cond;
+        sp.code = e.code;
+        sp.msg = e.what();
+        sp.cond = e.cond;
+        break;
       }
     }
     lam = eig.get();
   }
   r.kappa_before = kappa_from_eigs(lam);
   double kappa = r.kappa_before;
+  if (std::getenv("QLRA_DEBUG_PQR")) {
+    std::fprintf(stderr, "[pqr] s=%lld kappa0=%.6e lam=[%.3e..%.3e] rd=[%.3e..%.3e]", (long long)s, kappa,
+                 lam.empty() ? 0.0 : lam.back(), lam.empty() ? 0.0 : lam.front(),
+                 *std::min_element(rd.begin(), rd.end()), *std::max_element(rd.begin(), rd.end()));
+    for (int k = 0; k < nspec; ++k)
+      std::fprintf(stderr, " spec%d ok=%d eps=%.6e code=%d %s", k, (int)spec[k].ok, spec[k].eps, spec[k].code,
+                   spec[k].msg.c_str());
+    std::fprintf(stderr, "\n");
+  }
   try {
     while (r.correction_steps_used < cfg.max_correction_steps && kappa > kKappaTarget) {
       // one inverse serves estimate_epsilon and correction_step (both
       // factor the same H^*H, rangefinders.cpp:68,102)
       check_gram_rcond(kappa, 1e-15, "estimate_epsilon: H*H numerically singular");
-      DevQMat ginv;
+      check_gram_rcond(kappa, 1e-14, "solve_quaternion_linear: singular system");
+      const int k = r.correction_steps_used;
       double eps = 0.0;
-      if (r.correction_steps_used == 0) {
-        check_gram_rcond(kappa, 1e-14, "solve_quaternion_linear: singular system");
-        if (!spec_ok) fail(spec_code, spec_msg, spec_cond);
-        ginv = std::move(ginv0);
-        eps = eps0;
+      if (k < nspec) {
+        Spec& sp = spec[k];
+        if (!sp.ok) fail(sp.code, sp.msg, sp.cond);
+        eps = sp.eps;
+        cm = std::move(sp.next);
       } else {
         qgemm(c, QLRA_OP_C, QLRA_OP_N, 1.0, cm.v, cm.v, 0.0, g.v);
-        ginv = gram_inverse(c, g.v, kappa, 1e-14, "solve_quaternion_linear: singular system");
+        DevQMat ginv = gram_inverse(c, g.v, kappa, 1e-14, "solve_quaternion_linear: singular system");
         eps = estimate_epsilon_from_inverse(c, ginv.v, cfg.power_iters_for_epsilon);
+        if (!(eps > 0.0 && eps < 1.0))
+          fail(QLRA_ERR_PARAMETER, "correction_step: epsilon must lie in (0,1)");
+        small_axpby_identity(c, 1.0 - eps, eps, ginv.v, mk.v);
+        DevQMat cn(c, s, s);
+        qgemm(c, QLRA_OP_N, QLRA_OP_N, 1.0, cm.v, mk.v, 0.0, cn.v);
+        cm = std::move(cn);
       }
-      if (!(eps > 0.0 && eps < 1.0))
-        fail(QLRA_ERR_PARAMETER, "correction_step: epsilon must lie in (0,1)");
-      // H_{k+1} = H_k ((1-eps) I + eps G_k^{-1})  (rangefinders.cpp:99-105)
-      small_axpby_identity(c, 1.0 - eps, eps, ginv.v, mk.v);
-      DevQMat cn(c, s, s);
-      qgemm(c, QLRA_OP_N, QLRA_OP_N, 1.0, cm.v, mk.v, 0.0, cn.v);
-      cm = std::move(cn);
       double lmax = 0.0, lmin = std::numeric_limits<double>::infinity();
       for (double& v : lam) {
         const double f = (1.0 - eps) + eps / v;
@@ -709,12 +992,26 @@ void pseudo_qr_dev(Ctx& c, const QView& Y, const QView& H, const qlra_pseudo_qr_
     if (e.code != QLRA_ERR_SINGULAR) throw;
     fail(QLRA_ERR_RANK, "pseudo_qr: sketch numerically rank-deficient; use pseudo_svd");
   }
-  {
+  r.kappa_after = kappa;
+  if (es && es->started) {
+    // H = base (rinv_last C_k) on the second stream, overlapping the close
+    // of the early solve on this one (EarlySolve::done covers it)
+    es->coef = DevQMat(c, s, s);
+    qgemm(c, QLRA_OP_N, QLRA_OP_N, 1.0, q0.rinv_last.v, cm.v, 0.0, es->coef.v);
+    es->ck = std::move(cm);
+    es->kappa = kappa;
+    QLRA_CUDA(cudaEventRecord(es->coef_ready, c.stream));
+    QLRA_CUDA(cudaStreamWaitEvent(c.side2, es->coef_ready, 0));
+    {
+      StreamSwap on(c, c.side2);
+      qgemm(c, QLRA_OP_N, QLRA_OP_N, 1.0, q0.base.v, es->coef.v, 0.0, H);
+    }
+    QLRA_CUDA(cudaEventRecord(es->done, c.side2));
+  } else {
     DevQMat coef(c, s, s);
     qgemm(c, QLRA_OP_N, QLRA_OP_N, 1.0, q0.rinv_last.v, cm.v, 0.0, coef.v);
     qgemm(c, QLRA_OP_N, QLRA_OP_N, 1.0, q0.base.v, coef.v, 0.0, H);
   }
-  r.kappa_after = kappa;
   if (rep) *rep = r;
 }
 
@@ -768,6 +1065,22 @@ DevQMat qb_solve_operator(Ctx& c, const qlra_spec_t& psi, int64_t row0, const QV
 void qb_solve_dev(Ctx& c, const qlra_spec_t& psi, int64_t row0, const QView& H, const QView& W, const QView& X) {
   DevQMat t = qb_solve_operator(c, psi, row0, H);
   qgemm(c, QLRA_OP_C, QLRA_OP_N, 1.0, t.v, W, 0.0, X);
+}
+// The QB stage's core solve after a rangefinder that may have started it early.
+CoreSolve core_solve(Ctx& c, EarlySolve* es, const qlra_spec_t& psi, int64_t row0, const QView& H,
+                     const QView& W) {
+  CoreSolve cs;
+  if (es && early_solve_close(c, *es, cs.t)) {
+    cs.adj = false;
+    cs.b_own = std::move(es->x0);
+    cs.b = cs.b_own.v;
+    return cs;
+  }
+  if (es) es->join();  // H may come from the second stream
+  cs.t = qb_solve_operator(c, psi, row0, H);
+  cs.adj = true;
+  cs.b = W;
+  return cs;
 }
 
 void check_view(const qlra_qmat_t* m, const char* who) {
@@ -869,6 +1182,11 @@ int qlra_ctx_destroy(qlra_ctx_t* ctx) {
     cudaStreamDestroy(ctx->c.side);
   }
   if (ctx->c.side_pinned) cudaFreeHost(ctx->c.side_pinned);
+  if (ctx->c.side2) {
+    cudaStreamSynchronize(ctx->c.side2);
+    cudaStreamDestroy(ctx->c.side2);
+  }
+  if (ctx->c.tile_cnt2) cudaFree(ctx->c.tile_cnt2);
   drop_events(ctx->c);
   for (auto& e : ctx->c.ktimer.pool) {
     cudaEventDestroy(e.first);
@@ -1147,6 +1465,31 @@ int qlra_qb_solve(qlra_ctx_t* ctx, const qlra_spec_t* psi, int64_t row0, const q
   });
 }
 
+// qb_stage_with_psi (sketching.cpp:169-194) in one call: rangefinder on Y,
+// then X = (Psi H) \ W; with pseudo-QR the solve starts inside the
+// rangefinder (EarlySolve).
+int qlra_qb_stage(qlra_ctx_t* ctx, const qlra_spec_t* psi, int64_t row0, const qlra_qmat_t* y,
+                  const qlra_qmat_t* w, int method, uint64_t rangefinder_seed, const qlra_pseudo_qr_config_t* cfg_in,
+                  qlra_qmat_t* h, qlra_qmat_t* x, qlra_rangefinder_report_t* rep) {
+  return guarded(ctx, [&](Ctx& c) {
+    validate_spec(psi);
+    check_view(y, "qb_stage");
+    check_view(w, "qb_stage");
+    check_view(h, "qb_stage");
+    check_view(x, "qb_stage");
+    if (h->rows != y->rows || h->cols != y->cols) fail(QLRA_ERR_SHAPE, "qb_stage: output shape mismatch");
+    check_solve_shapes(psi, row0, h, w, x);
+    if (method != QLRA_PSEUDO_QR && method != QLRA_PSEUDO_SVD) fail(QLRA_ERR_PARAMETER, "qb_stage: unknown rangefinder");
+    qlra_pseudo_qr_config_t cfg{3, 3, 1.2};
+    if (cfg_in) cfg = *cfg_in;
+    EarlySolve es(c, *psi, row0, view_of(w));
+    if (method == QLRA_PSEUDO_QR) pseudo_qr_dev(c, view_of(y), view_of(h), cfg, rep, &es);
+    else pseudo_svd_dev(c, view_of(y), view_of(h), rangefinder_seed, rep);
+    const CoreSolve cs = core_solve(c, &es, *psi, row0, view_of(h), view_of(w));
+    cs.cols(c, 0, x->cols, view_of(x));
+  });
+}
+
 // Host in, host out: one_pass_approx through the QB stage
 // (sketching.cpp:250-263) on a host row shard.  A streams through the
 // overlapped H2D + fused-sketch pipeline; H is copied back on a side stream
@@ -1178,7 +1521,8 @@ int qlra_one_pass_qb_host(qlra_ctx_t* ctx, const qlra_qmat_t* a_host, int64_t ro
     allreduce_qmat(c, w.v);
     std::unique_ptr<SideEigs> kappa_after;  // pseudo-SVD: kappa(H) overlapped with the solve
     qlra_rangefinder_report_t rr{};
-    if (method == QLRA_PSEUDO_QR) pseudo_qr_dev(c, y.v, h.v, cfg, &rr);
+    EarlySolve es(c, *psi, row0, w.v);
+    if (method == QLRA_PSEUDO_QR) pseudo_qr_dev(c, y.v, h.v, cfg, &rr, &es);
     else pseudo_svd_dev(c, y.v, h.v, rangefinder_seed, &rr, &kappa_after);
     // H is final: copy it back on a side stream while the solve runs
     cudaStream_t side = nullptr;
@@ -1188,6 +1532,7 @@ int qlra_one_pass_qb_host(qlra_ctx_t* ctx, const qlra_qmat_t* a_host, int64_t ro
     QLRA_CUDA(cudaEventCreateWithFlags(&copied, cudaEventDisableTiming));
     QLRA_CUDA(cudaEventRecord(ready, c.stream));
     QLRA_CUDA(cudaStreamWaitEvent(side, ready, 0));
+    if (es.done) QLRA_CUDA(cudaStreamWaitEvent(side, es.done, 0));  // H formed on the second stream
     const QView hv = view_of(h_host), xv = view_of(x_host);
     for (int p = 0; p < 4; ++p) {
       if (hv.ld == s)  // contiguous: one linear DMA (h is dense)
@@ -1199,12 +1544,12 @@ int qlra_one_pass_qb_host(qlra_ctx_t* ctx, const qlra_qmat_t* a_host, int64_t ro
     }
     // X = T^* W in column blocks; each block is copied back on the side
     // stream while the next one is computed
-    DevQMat t = qb_solve_operator(c, *psi, row0, h.v);
+    const CoreSolve cs = core_solve(c, &es, *psi, row0, h.v, w.v);
     const int64_t nblk = n >= 2048 ? 4 : 1;
     const int64_t bw = (n + nblk - 1) / nblk;
     for (int64_t j0 = 0; j0 < n; j0 += bw) {
       const int64_t nj = std::min(bw, n - j0);
-      qgemm(c, QLRA_OP_C, QLRA_OP_N, 1.0, t.v, sub(w.v, 0, j0, l, nj), 0.0, sub(x.v, 0, j0, s, nj));
+      cs.cols(c, j0, nj, x.v);
       QLRA_CUDA(cudaEventRecord(ready, c.stream));
       QLRA_CUDA(cudaStreamWaitEvent(side, ready, 0));
       for (int p = 0; p < 4; ++p)

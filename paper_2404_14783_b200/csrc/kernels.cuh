@@ -39,6 +39,11 @@ struct Ctx {
   cudaStream_t side = nullptr;
   double* side_pinned = nullptr;
   size_t side_pinned_n = 0;
+  // second side stream (the core solve started inside pseudo-QR) with its own
+  // split-K arrival counters (StreamSwap exchanges them with tile_cnt)
+  cudaStream_t side2 = nullptr;
+  unsigned* tile_cnt2 = nullptr;
+  int64_t tile_cnt2_n = 0;
   // Optional per-launch timing of the fused sketch kernel (bench evidence):
   // CUDA events bracket every launch on the launching stream.
   struct KernelTimer {

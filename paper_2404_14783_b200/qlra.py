@@ -491,10 +491,30 @@ def qb_solve(psi_spec: TestMatrixSpec, h, w, row0=0, ctx=None):
 
 
 def qb_stage(state: SketchState, method=PSEUDO_QR, rangefinder_seed=DEFAULT_RANGEFINDER_SEED,
-             qr_cfg: PseudoQrConfig = PseudoQrConfig(), ctx=None, timer: Callable | None = None) -> QbResult:
+             qr_cfg: PseudoQrConfig = PseudoQrConfig(), ctx=None, timer: Callable | None = None,
+             split: bool = False) -> QbResult:
     """qb_stage (sketching.cpp:169-194): rangefinder on Y, then X = (Psi H) \\ W
-    with Psi regenerated from its spec.  Never touches A."""
+    with Psi regenerated from its spec.  Never touches A.  One call
+    (qlra_qb_stage: the solve starts inside pseudo-QR) unless `split`, which
+    runs the rangefinder and the solve as two calls and times them apart
+    (rangefinder_s / solve_s; the fused call reports its total as rangefinder_s)."""
     ctx = _ctx(ctx)
+    if method not in (PSEUDO_QR, PSEUDO_SVD):
+        raise ParameterError("qb_stage: unknown rangefinder")
+    if not split:
+        t0 = time.perf_counter()
+        h = torch.empty_like(state.y)
+        x = qzeros(state.y.shape[2], state.w.shape[2])
+        c = L.PseudoQrConfig(qr_cfg.max_correction_steps, qr_cfg.power_iters_for_epsilon, qr_cfg.delta_budget)
+        rep = L.Report()
+        ps = state.psi_spec.c()
+        ctx._check(ctx.lib.qlra_qb_stage(ctx.h, C.byref(ps), state.row0, C.byref(_qm(state.y)),
+                                         C.byref(_qm(state.w)), method, rangefinder_seed, C.byref(c),
+                                         C.byref(_qm(h)), C.byref(_qm(x)), C.byref(rep)))
+        ctx.synchronize()
+        steps = rep.correction_steps_used if method == PSEUDO_QR else 0
+        rr = RangefinderReport(h, rep.kappa_before, rep.kappa_after, steps, method)
+        return QbResult(h, x, rr, time.perf_counter() - t0, 0.0)
     t0 = time.perf_counter()
     rep = pseudo_qr(state.y, qr_cfg, ctx) if method == PSEUDO_QR else pseudo_svd(state.y, rangefinder_seed, ctx)
     t1 = time.perf_counter()

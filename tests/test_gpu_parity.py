@@ -539,3 +539,54 @@ def test_two_contexts_two_threads(ctx):
         t.join()
     for k in range(2):
         assert np.array_equal(out[k][0], seq[k][0]) and np.array_equal(out[k][1], seq[k][1])
+
+
+@pytest.mark.parametrize("kappa,steps,noise", [(1e4, 3, 1e-3), (3.0, 3, 1e-3), (1e4, 0, 1e-9)])
+def test_qb_stage_fused_matches_split(ctx, kappa, steps, noise):
+    """qlra_qb_stage (the solve started inside pseudo-QR: X = C_k^{-1} (Psi
+    Q0)^+ W) against the two separate calls (X = (Psi H)^+ W).  H is the same
+    computation (bitwise); X agrees to rounding.  (1e4, 0): kappa_after > 100,
+    so the fused call takes the sequential solve -- bitwise equal."""
+    from paper_2404_14783_b200 import qlra as Q
+    m, n, s, l = 900, 700, 40, 80
+    left = planted_conditioned_matrix(m, s, kappa, 90)
+    a = O.qmat_mul(left, O.adjoint(O.orthonormal_range(random_gaussian(n, s, 91))))
+    a = a + noise * random_gaussian(m, n, 92)
+    st = Q.make_sketch(dev(a), s - 5, s, l, 93, 94, ctx=ctx)
+    cfg = Q.PseudoQrConfig(max_correction_steps=steps)
+    fused = Q.qb_stage(st, Q.PSEUDO_QR, qr_cfg=cfg, ctx=ctx)
+    split = Q.qb_stage(st, Q.PSEUDO_QR, qr_cfg=cfg, ctx=ctx, split=True)
+    assert torch.equal(fused.h, split.h)
+    assert fused.report.kappa_after == split.report.kappa_after
+    xf, xs = host(fused.x), host(split.x)
+    if fused.report.kappa_after > 100.0:  # the early solve declines: same sequential solve
+        assert np.array_equal(xf, xs)
+    else:
+        assert rel_diff(xf, xs) <= 1e-12
+    # and both against the oracle's QB residual
+    y, w = O.make_sketch(a, s - 5, s, l, 93, 94, nthreads=8)
+    qb = O.qb_stage(y, w, 94, O.PSEUDO_QR, max_steps=steps, nthreads=8)
+    rs_o, an = O.residual_sq(a, qb["h"], qb["x"])
+    rs_d, _ = O.residual_sq(a, host(fused.h), xf)
+    # north-star bar (1e-10 relative), with an absolute floor at 1e-13 ||A||
+    # for the nearly exact (1e-9 noise) case whose residual is ~3e-10 ||A||
+    assert abs(np.sqrt(rs_d) - np.sqrt(rs_o)) <= 1e-10 * np.sqrt(rs_o) + 1e-13 * np.sqrt(an)
+
+
+def test_qb_stage_fused_errors_match_split(ctx):
+    """A Psi that makes Psi H rank-deficient (a sparse embedding with one
+    nonzero in a few columns) raises the same error from the fused call."""
+    from paper_2404_14783_b200 import qlra as Q
+    a = random_gaussian(300, 200, 95)
+    st = Q.make_sketch(dev(a), 3, 8, 9, 96, 97, kind=Q.SPARSE_RADEMACHER, density=0.01, ctx=ctx)
+    errs = []
+    for split in (False, True):
+        try:
+            r = Q.qb_stage(st, Q.PSEUDO_QR, ctx=ctx, split=split)
+            errs.append(("ok", host(r.x)))
+        except Q.Error as e:
+            errs.append((type(e).__name__, str(e)))
+    if errs[0][0] == "ok":
+        assert errs[1][0] == "ok" and rel_diff(errs[0][1], errs[1][1]) <= 1e-10
+    else:
+        assert errs[0] == errs[1]

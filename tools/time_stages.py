@@ -19,3 +19,11 @@ for it in range(6):
         print("sketch %.2f ms  rangefinder %.2f ms  solve %.2f ms  steps %d kappa %.3e/%.3e" % (
             1e3 * t["sketch_s"], 1e3 * t["rangefinder_s"], 1e3 * t["solve_s"], r.qb.report.correction_steps_used,
             r.qb.report.kappa_before, r.qb.report.kappa_after))
+# the QB stage as one fused call vs rangefinder + solve as two calls
+st = r.state
+for it in range(4):
+    f = Q.qb_stage(st, method, ctx=ctx)
+    s = Q.qb_stage(st, method, ctx=ctx, split=True)
+    if it >= 1:
+        print("qb fused %.2f ms   split: rangefinder %.2f + solve %.2f = %.2f ms" % (
+            1e3 * f.rangefinder_s, 1e3 * s.rangefinder_s, 1e3 * s.solve_s, 1e3 * (s.rangefinder_s + s.solve_s)))
