@@ -295,11 +295,19 @@ def main():
         t0 = torch.cuda.Event(enable_timing=True)
         t1 = torch.cuda.Event(enable_timing=True)
         t0.record(stream)
+        vstep_ev = []
         for _ in range(args.steps):
+            if os.environ.get("QLRA_BENCH_STEPTIMES"):
+                vstep_ev.append(torch.cuda.Event(enable_timing=True))
+                vstep_ev[-1].record(stream)
             st, qb = step(a)
         t1.record(stream)
         barrier()
     gc.enable()
+    if vstep_ev and rank == 0:
+        vstep_ev.append(t1)
+        sys.stderr.write("value per step ms: " + " ".join(
+            "%.2f" % vstep_ev[i].elapsed_time(vstep_ev[i + 1]) for i in range(len(vstep_ev) - 1)) + "\n")
     launches = ctx.launch_count() - launches0
     if os.environ.get("QLRA_BENCH_STEPTIMES") and rank == 0:
         sys.stderr.write("sketch per step ms: " + " ".join("%.2f" % e0.elapsed_time(e1) for e0, e1 in sk_events) + "\n")
@@ -346,11 +354,19 @@ def main():
         gc.collect()
         gc.disable()
         s0.record(stream)
+        step_ev = []
         for _ in range(args.steps):
+            if os.environ.get("QLRA_BENCH_STEPTIMES"):
+                step_ev.append(torch.cuda.Event(enable_timing=True))
+                step_ev[-1].record(stream)
             e2e_step()
         s1.record(stream)
         barrier()
         gc.enable()
+        if step_ev and rank == 0:
+            step_ev.append(s1)
+            sys.stderr.write("e2e per step ms: " + " ".join(
+                "%.2f" % step_ev[i].elapsed_time(step_ev[i + 1]) for i in range(len(step_ev) - 1)) + "\n")
         e2e_ms = torch.tensor([s0.elapsed_time(s1) / args.steps], dtype=torch.float64, device="cuda")
         if world > 1:
             dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)

@@ -816,7 +816,8 @@ bool pqr_factors_fast(Ctx& c, const QView& Y, DeferredQ& q0, DevQMat& rq, DevQMa
   chain_rinv(c, rq_inv, p.r2inv.v);
   q0.base = std::move(p.t1);
   q0.rinv_last = std::move(p.r2inv);
-  if (es && c.nranks == 1 && es->psi->rows >= s) early_solve_start(c, *es, q0);
+  if (es && c.nranks == 1 && es->psi->rows >= s && !std::getenv("QLRA_NO_EARLY_SOLVE"))
+    early_solve_start(c, *es, q0);
   QLRA_CUDA(cudaStreamWaitEvent(c.stream, cdone, 0));
   DevQMat t1c(c, s, s), g2(c, s, s), r2c(c, s, s), r2c_inv(c, s, s);
   qgemm(c, QLRA_OP_N, QLRA_OP_N, 1.0, rq.v, r1c_inv.v, 0.0, t1c.v);
@@ -1521,8 +1522,11 @@ int qlra_one_pass_qb_host(qlra_ctx_t* ctx, const qlra_qmat_t* a_host, int64_t ro
     allreduce_qmat(c, w.v);
     std::unique_ptr<SideEigs> kappa_after;  // pseudo-SVD: kappa(H) overlapped with the solve
     qlra_rangefinder_report_t rr{};
-    EarlySolve es(c, *psi, row0, w.v);
-    if (method == QLRA_PSEUDO_QR) pseudo_qr_dev(c, y.v, h.v, cfg, &rr, &es);
+    // No early solve here: H's read-back already hides the solve (C2:
+    // 31.55 ms either way; C5: the early solve's side-stream work delays H
+    // and so its 49 ms read-back, 433 -> 446 ms).
+    EarlySolve* esp = nullptr;
+    if (method == QLRA_PSEUDO_QR) pseudo_qr_dev(c, y.v, h.v, cfg, &rr, esp);
     else pseudo_svd_dev(c, y.v, h.v, rangefinder_seed, &rr, &kappa_after);
     // H is final: copy it back on a side stream while the solve runs
     cudaStream_t side = nullptr;
@@ -1532,7 +1536,6 @@ int qlra_one_pass_qb_host(qlra_ctx_t* ctx, const qlra_qmat_t* a_host, int64_t ro
     QLRA_CUDA(cudaEventCreateWithFlags(&copied, cudaEventDisableTiming));
     QLRA_CUDA(cudaEventRecord(ready, c.stream));
     QLRA_CUDA(cudaStreamWaitEvent(side, ready, 0));
-    if (es.done) QLRA_CUDA(cudaStreamWaitEvent(side, es.done, 0));  // H formed on the second stream
     const QView hv = view_of(h_host), xv = view_of(x_host);
     for (int p = 0; p < 4; ++p) {
       if (hv.ld == s)  // contiguous: one linear DMA (h is dense)
@@ -1544,7 +1547,7 @@ int qlra_one_pass_qb_host(qlra_ctx_t* ctx, const qlra_qmat_t* a_host, int64_t ro
     }
     // X = T^* W in column blocks; each block is copied back on the side
     // stream while the next one is computed
-    const CoreSolve cs = core_solve(c, &es, *psi, row0, h.v, w.v);
+    const CoreSolve cs = core_solve(c, esp, *psi, row0, h.v, w.v);
     const int64_t nblk = n >= 2048 ? 4 : 1;
     const int64_t bw = (n + nblk - 1) / nblk;
     for (int64_t j0 = 0; j0 < n; j0 += bw) {
