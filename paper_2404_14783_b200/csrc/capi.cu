@@ -117,7 +117,7 @@ int64_t global_row0(Ctx& ctx, int64_t local) {
 
 // G = op(A)^* op(A) reduced over (row-sharded) rows: s x s.
 void gram(Ctx& ctx, const QView& h, const QView& g) {
-  qgemm(ctx, QLRA_OP_C, QLRA_OP_N, 1.0, h, h, 0.0, g);
+  qgemm_gram(ctx, h, g);
   allreduce_qmat(ctx, g);
 }
 
@@ -236,7 +236,7 @@ bool cqr_pass(Ctx& ctx, const QView& y, const QView& hout, bool complex_mode, do
   const int64_t s = y.cols;
   DevQMat g(ctx, s, s);
   if (distributed) gram(ctx, y, g.v);
-  else qgemm(ctx, QLRA_OP_C, QLRA_OP_N, 1.0, y, y, 0.0, g.v);
+  else qgemm_gram(ctx, y, g.v);
   if (trace_g) {
     const std::vector<double> d = diag_to_host(ctx, g.v.p[0], g.v.ld, s);
     double t = 0.0;
@@ -306,7 +306,7 @@ void cqr2_enqueue(Ctx& ctx, const QView& y, const QView& h, bool complex_mode, b
   p.dg = DeviceBuffer(ctx, 2 * sizeof(double) * (size_t)s);
   auto gram_of = [&](const QView& a, const QView& g) {
     if (distributed) gram(ctx, a, g);
-    else qgemm(ctx, QLRA_OP_C, QLRA_OP_N, 1.0, a, a, 0.0, g);
+    else qgemm_gram(ctx, a, g);
     if (complex_mode) zero_jk_planes(ctx, g);
   };
   if (gram1) {
@@ -701,9 +701,9 @@ void early_solve_start(Ctx& c, EarlySolve& es, const DeferredQ& q0) {
   QLRA_CUDA(cudaEventDestroy(fork));
   {
     StreamSwap on(c, c.side2);
-    DevQMat ps(c, l, rows), pb(c, l, s), p0(c, l, s);
-    launch_gen(c.stream, *es.psi, 0, es.row0, l, rows, ps.v, false);
-    qgemm(c, QLRA_OP_N, QLRA_OP_N, 1.0, ps.v, q0.base.v, 0.0, pb.v);
+    DevQMat ps_tmp, pb(c, l, s), p0(c, l, s);
+    const QView ps = psi_for_solve(c, *es.psi, es.row0, rows, ps_tmp);
+    qgemm(c, QLRA_OP_N, QLRA_OP_N, 1.0, ps, q0.base.v, 0.0, pb.v);
     qgemm(c, QLRA_OP_N, QLRA_OP_N, 1.0, pb.v, q0.rinv_last.v, 0.0, p0.v);
     cqr2_enqueue(c, p0.v, QView{}, /*complex_mode=*/false, /*distributed=*/false, nullptr, /*form_q=*/false,
                  es.cqr);
@@ -1056,10 +1056,10 @@ void pseudo_svd_dev(Ctx& c, const QView& Y, const QView& H, uint64_t seed, qlra_
 // sketching.cpp:184-185: P = Psi H, X = P \ W through a QR of P).
 DevQMat qb_solve_operator(Ctx& c, const qlra_spec_t& psi, int64_t row0, const QView& H) {
   const int64_t s = H.cols, l = psi.rows;
-  DevQMat ps(c, l, H.rows);
-  launch_gen(c.stream, psi, 0, row0, l, H.rows, ps.v, false);
+  DevQMat ps_tmp;
+  const QView ps = psi_for_solve(c, psi, row0, H.rows, ps_tmp);
   DevQMat p(c, l, s);
-  qgemm(c, QLRA_OP_N, QLRA_OP_N, 1.0, ps.v, H, 0.0, p.v);
+  qgemm(c, QLRA_OP_N, QLRA_OP_N, 1.0, ps, H, 0.0, p.v);
   allreduce_qmat(c, p.v);
   return lstsq_operator(c, p.v);
 }
@@ -1173,7 +1173,10 @@ static void drop_events(Ctx& c) {
 int qlra_ctx_destroy(qlra_ctx_t* ctx) {
   if (!ctx) return QLRA_OK;
   cudaSetDevice(ctx->c.device);
-  if (ctx->c.stream) cudaStreamSynchronize(ctx->c.stream);
+  if (ctx->c.stream) {
+    psi_keep_release(ctx->c);
+    cudaStreamSynchronize(ctx->c.stream);
+  }
   if (ctx->c.comm) ncclCommDestroy(ctx->c.comm);
   if (ctx->c.own_stream && ctx->c.stream) cudaStreamDestroy(ctx->c.stream);
   if (ctx->c.pinned) cudaFreeHost(ctx->c.pinned);

@@ -64,6 +64,7 @@ __global__ void __launch_bounds__(NT, 1) qgemm_kernel(GemmArgs g) {
   const int64_t M = g.op.M, N = g.op.N;
   int tm, tn, zs;
   gemm_task(g, tm, tn, zs);
+  if (MODE == 0 && g.op.herm && tm > tn) return;  // lower tile of a Hermitian product: mirrored later
   const int64_t i0 = (int64_t)tm * BM, j0 = (int64_t)tn * BN;
   const int64_t kbeg = (int64_t)zs * g.kchunk;
   const int64_t kend = min(g.K, kbeg + g.kchunk);
@@ -485,8 +486,35 @@ void splitk_reduce(Ctx& ctx, const double* ws, int nz, const QView& C, double al
   count_launch();
 }
 
+// C(i, j) = conj(C(j, i)) for i > j: completes a Hermitian product of
+// which only the upper triangle was computed.
+__global__ void k_mirror_upper(QView c) {
+  const int64_t n = c.rows;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n * n; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = t / n, j = t % n;
+    if (i <= j) continue;
+    const int64_t src = j * c.ld + i, dst = i * c.ld + j;
+    c.p[0][dst] = c.p[0][src];
+    c.p[1][dst] = -c.p[1][src];
+    c.p[2][dst] = -c.p[2][src];
+    c.p[3][dst] = -c.p[3][src];
+  }
+}
+
 void qgemm(Ctx& ctx, int op_a, int op_b, double alpha, const QView& A, const QView& B,
            double beta, const QView& C, int force_splits) {
+  qgemm_ex(ctx, op_a, op_b, alpha, A, B, beta, C, force_splits, false);
+}
+
+// C = A^* A (Hermitian): on the 64x64 DMMA path only the tiles and warp
+// tiles on or above the diagonal are computed and the rest is mirrored
+// (about half the tensor work of a Gram; exactly Hermitian result).
+void qgemm_gram(Ctx& ctx, const QView& A, const QView& C) {
+  qgemm_ex(ctx, QLRA_OP_C, QLRA_OP_N, 1.0, A, A, 0.0, C, 0, true);
+}
+
+void qgemm_ex(Ctx& ctx, int op_a, int op_b, double alpha, const QView& A, const QView& B,
+              double beta, const QView& C, int force_splits, bool herm) {
   int64_t M, N, K;
   GemmArgs g = make_args(op_a, op_b, alpha, A, B, beta, M, N, K);
   if (C.rows != M || C.cols != N) fail(QLRA_ERR_SHAPE, "qmat_mul: output shape mismatch");
@@ -514,6 +542,7 @@ void qgemm(Ctx& ctx, int op_a, int op_b, double alpha, const QView& A, const QVi
   g.kchunk = kchunk;
   const int64_t ctas = fill_schedule(g, M, N, (int)nsplit);
   dim3 grid((unsigned)ctas);
+  g.op.herm = herm && M == N && beta == 0.0 ? 1 : 0;
   if (nsplit > 1) {
     DeviceBuffer ws(ctx, (size_t)nsplit * 4 * M * N * sizeof(double));
     g.ws = ws.as<double>();
@@ -521,6 +550,11 @@ void qgemm(Ctx& ctx, int op_a, int op_b, double alpha, const QView& A, const QVi
     splitk_reduce(ctx, g.ws, (int)nsplit, C, alpha, beta);
   } else {
     dispatch<0>(op_a == QLRA_OP_C, op_b == QLRA_OP_C, grid, ctx.stream, g);
+  }
+  if (g.op.herm) {
+    k_mirror_upper<<<(unsigned)std::min<int64_t>((M * M + 255) / 256, 148 * 4), 256, 0, ctx.stream>>>(C);
+    QLRA_LAUNCH_CHECK();
+    count_launch();
   }
 }
 

@@ -40,6 +40,9 @@ struct Operands {
   const double* b[4];
   int64_t a_si, a_sk, b_sk, b_sj;
   int64_t M, N;
+  // Hermitian product (C = A^* A): warp tiles strictly below the diagonal
+  // issue no DMMA (the caller mirrors the upper triangle)
+  int herm = 0;
 };
 
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool pred) {
@@ -105,13 +108,15 @@ __device__ __forceinline__ void zero_acc(Acc& acc) {
 }
 
 // Warp w owns the 16x16 sub-tile (warp_row(w), warp_col(w)).  Warps issue on
-// SMSP w % 4; the diagonal column assignment gives every SMSP one warp of
-// each row band AND each column band, so the 8x8 blocks skipped in tiles
-// padded along either M or N take work off all four tensor pipes evenly (with
-// wc = w % 4, a tile padded along N left one SMSP idle and the CTA waited on
-// the other three).
+// SMSP w % 4 = (row + col) % 4: this anti-diagonal assignment gives every
+// SMSP one warp of each row band AND each column band, so the 8x8 blocks
+// skipped in tiles padded along either M or N take work off all four tensor
+// pipes evenly (with wc = w % 4, a tile padded along N left one SMSP idle and
+// the CTA waited on the other three), and it also spreads the upper triangle
+// of a Hermitian product's diagonal tile (4 x 4 warp tiles: 3/2/3/2 per SMSP;
+// the (col - row) % 4 assignment put all four diagonal warp tiles on SMSP 0).
 __device__ __forceinline__ int warp_row(int w) { return w >> 2; }
-__device__ __forceinline__ int warp_col(int w) { return (w + (w >> 2)) & 3; }
+__device__ __forceinline__ int warp_col(int w) { return ((w & 3) - (w >> 2)) & 3; }
 
 __device__ __forceinline__ int acc_row(int rb) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -273,7 +278,7 @@ __device__ __forceinline__ void mma_tile(const Operands& g, double* smem, int64_
   __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES];
   const int w = threadIdx.x >> 5;
   const int64_t r0w = i0 + 16 * warp_row(w), c0w = j0 + 16 * warp_col(w);
-  const int nrb = r0w >= g.M ? 0 : r0w + 8 >= g.M ? 1 : 2;
+  const int nrb = r0w >= g.M || (g.herm && r0w >= c0w + 16) ? 0 : r0w + 8 >= g.M ? 1 : 2;
   const int ncb = c0w >= g.N ? 0 : c0w + 8 >= g.N ? 1 : 2;
   switch (nrb * 4 + ncb) {
     case 2 * 4 + 2: mma_loop<CA, CB, 2, 2>(g, smem, i0, j0, kbeg, kend, acc, full, empty); break;
@@ -281,6 +286,7 @@ __device__ __forceinline__ void mma_tile(const Operands& g, double* smem, int64_
     case 1 * 4 + 2: mma_loop<CA, CB, 1, 2>(g, smem, i0, j0, kbeg, kend, acc, full, empty); break;
     case 1 * 4 + 1: mma_loop<CA, CB, 1, 1>(g, smem, i0, j0, kbeg, kend, acc, full, empty); break;
     default: mma_loop<CA, CB, 0, 0>(g, smem, i0, j0, kbeg, kend, acc, full, empty); break;  // loads + barriers only
+    // (nrb = 0 with ncb > 0 -- a Hermitian product's lower warp tiles -- lands here too)
   }
 }
 

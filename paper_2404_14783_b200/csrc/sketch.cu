@@ -343,20 +343,74 @@ int64_t stream_rows(int64_t n, int64_t b) {
 
 }  // namespace
 
+namespace {
+QView view_of_buf(double* base, int64_t rows, int64_t cols) {
+  QView v{};
+  for (int p = 0; p < 4; ++p) v.p[p] = base + (size_t)p * rows * cols;
+  v.rows = rows;
+  v.cols = cols;
+  v.ld = cols;
+  return v;
+}
+bool same_spec(const qlra_spec_t& a, const qlra_spec_t& b) {
+  return a.kind == b.kind && a.rows == b.rows && a.cols == b.cols && a.seed == b.seed && a.density == b.density;
+}
+}  // namespace
+
+QView psi_for_sketch(Ctx& ctx, const qlra_spec_t& psi, int64_t row0, int64_t rows, DevQMat& tmp) {
+  static const double cap = env_or("QLRA_PSI_KEEP_BYTES", 8e9);
+  const int64_t l = psi.rows;
+  const size_t bytes = (size_t)4 * l * rows * sizeof(double);
+  Ctx::PsiKeep& k = ctx.psi_keep;
+  k.valid = false;
+  if ((double)bytes > cap || bytes == 0) {
+    tmp = DevQMat(ctx, l, rows);
+    launch_gen(ctx.stream, psi, 0, row0, l, rows, tmp.v, false);
+    return tmp.v;
+  }
+  if (k.bytes < bytes) {
+    if (k.buf) QLRA_CUDA(cudaFreeAsync(k.buf, ctx.stream));
+    k.buf = nullptr;
+    k.bytes = 0;
+    QLRA_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&k.buf), bytes, ctx.stream));
+    k.bytes = bytes;
+  }
+  const QView v = view_of_buf(k.buf, l, rows);
+  launch_gen(ctx.stream, psi, 0, row0, l, rows, v, false);
+  k.valid = true;
+  k.spec = psi;
+  k.row0 = row0;
+  k.rows = rows;
+  return v;
+}
+
+QView psi_for_solve(Ctx& ctx, const qlra_spec_t& psi, int64_t row0, int64_t rows, DevQMat& tmp) {
+  const Ctx::PsiKeep& k = ctx.psi_keep;
+  if (k.valid && same_spec(k.spec, psi) && k.row0 == row0 && k.rows == rows) return view_of_buf(k.buf, psi.rows, rows);
+  tmp = DevQMat(ctx, psi.rows, rows);
+  launch_gen(ctx.stream, psi, 0, row0, psi.rows, rows, tmp.v, false);
+  return tmp.v;
+}
+
+void psi_keep_release(Ctx& ctx) {
+  Ctx::PsiKeep& k = ctx.psi_keep;
+  if (k.buf) cudaFreeAsync(k.buf, ctx.stream);
+  k = Ctx::PsiKeep{};
+}
+
 void sketch_update_rows(Ctx& ctx, const qlra_spec_t& omega, const qlra_spec_t& psi, int64_t row0,
                         const QView& block, const QView& y_rows, const QView& w) {
   const int64_t b = block.rows, n = block.cols, s = omega.cols, l = psi.rows;
   if (b == 0 || n == 0) return;
   set_kernel_attrs();
-  DevQMat om(ctx, n, s);
+  DevQMat om(ctx, n, s), ps_tmp;
   launch_gen(ctx.stream, omega, 0, 0, n, s, om.v, false);
-  DevQMat ps(ctx, l, b);
-  launch_gen(ctx.stream, psi, 0, row0, l, b, ps.v, false);
+  const QView ps = psi_for_sketch(ctx, psi, row0, b, ps_tmp);
   const int64_t R = panel_rows(n, b);
   SketchWork ws;
   for (int64_t r0 = 0; r0 < b; r0 += R) {
     const int64_t rp = std::min(R, b - r0);
-    sketch_panel(ctx, om.v, ps.v, r0, sub(block, r0, 0, rp, n), sub(y_rows, r0, 0, rp, s), w, ws);
+    sketch_panel(ctx, om.v, ps, r0, sub(block, r0, 0, rp, n), sub(y_rows, r0, 0, rp, s), w, ws);
   }
 }
 
@@ -372,7 +426,7 @@ void sketch_update_rows_host(Ctx& ctx, const qlra_spec_t& omega, const qlra_spec
   set_kernel_attrs();
   int64_t R = block_rows > 0 ? block_rows : stream_rows(n, b);
   R = std::min(R, b);
-  DevQMat om(ctx, n, s), ps(ctx, l, b);
+  DevQMat om(ctx, n, s), ps_tmp;
   DevQMat buf[2] = {DevQMat(ctx, R, n), DevQMat(ctx, R, n)};
   cudaStream_t cs;
   QLRA_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
@@ -387,7 +441,7 @@ void sketch_update_rows_host(Ctx& ctx, const qlra_spec_t& omega, const qlra_spec
   QLRA_CUDA(cudaEventRecord(freed[0], ctx.stream));
   QLRA_CUDA(cudaEventRecord(freed[1], ctx.stream));
   launch_gen(ctx.stream, omega, 0, 0, n, s, om.v, false);
-  launch_gen(ctx.stream, psi, 0, row0, l, b, ps.v, false);
+  const QView ps = psi_for_sketch(ctx, psi, row0, b, ps_tmp);
   SketchWork ws;
   // The last R rows go in quarter-size chunks: the sketch of the final chunk
   // is the one part of the pipeline nothing overlaps (the copy stream is the
@@ -413,7 +467,7 @@ void sketch_update_rows_host(Ctx& ctx, const qlra_spec_t& omega, const qlra_spec
     }
     QLRA_CUDA(cudaEventRecord(copied[idx], cs));
     QLRA_CUDA(cudaStreamWaitEvent(ctx.stream, copied[idx], 0));
-    sketch_panel(ctx, om.v, ps.v, r0, dst, sub(y_rows, r0, 0, rp, s), w, ws);
+    sketch_panel(ctx, om.v, ps, r0, dst, sub(y_rows, r0, 0, rp, s), w, ws);
     QLRA_CUDA(cudaEventRecord(freed[idx], ctx.stream));
   }
   QLRA_CUDA(cudaStreamSynchronize(cs));
