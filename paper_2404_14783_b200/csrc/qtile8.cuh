@@ -1,0 +1,295 @@
+// qtile8.cuh -- the sketch's tile engine: quaternion products with EIGHT real
+// matrix products instead of sixteen.
+//
+// A quaternion product c = a b (Hamilton table, proj/include/qlra/
+// quaternion.hpp:33-38) is a real bilinear map of rank 8 (Howell & Lafon,
+// 1975).  With planes (w, x, y, z) = (0, 1, 2, 3):
+//
+//   m1 = (a0 + a1)(b0 + b1)      m5 = (a1 + a3)(b1 + b2)/2
+//   m2 = (a3 - a2)(b2 - b3)      m6 = (a1 - a3)(b1 - b2)/2
+//   m3 = (a0 - a1)(b2 + b3)      m7 = (a0 + a2)(b0 - b3)/2
+//   m4 = (a2 + a3)(b0 - b1)      m8 = (a0 - a2)(b0 + b3)/2
+//
+//   c0 = m2 - m5 - m6 + m7 + m8      c1 = m1 - m5 - m6 - m7 - m8
+//   c2 = m3 + m5 - m6 + m7 - m8      c3 = m4 + m5 - m6 - m7 + m8
+//
+// Every m_i keeps a on the left and b on the right, so the identity holds for
+// matrix entries as well: a quaternion GEMM is 8 real GEMMs of plane
+// combinations, 8 accumulators per output element.  On B200 the FP64 tensor
+// op (DMMA.8x8x4) and DFMA share one pipe of 64 FMA/clk/SM, so the DMMA count
+// is the cost: half of the 16-product engine (qtile.cuh), plus the pairwise
+// sums that form the combinations (DADD, 1/8 of a DMMA each).
+//
+// The sketch products are Y = A Omega and W = Psi A.  The embedding side is
+// combined ONCE in HBM (8 planes, halves folded into combinations 5..8:
+// exact, a power of two), the A side in registers from the 4 staged planes
+// (A is read once and never rewritten):
+//
+//   YT (Y task): C 64x32 = A (k-fast, 4 planes) x Omega~ (j-fast, 8 planes),
+//                warp tile 16x8 (2x1 blocks of 8x8);
+//   WT (W task): C 32x64 = Psi~ (k-fast, 8 planes) x A (j-fast, 4 planes),
+//                warp tile 8x16 (1x2 blocks).
+//
+// 512 threads as 4x4 warps, 8 products x 2 blocks x 2 = 32 FP64 accumulators
+// per thread, as in qtile.cuh.  Rounding: every product and sum is an IEEE
+// operation in a fixed order (deterministic); the combination sums add at
+// most a few ulp of |a||b| per term, the same order as the 16-product sum
+// (the sketch is compared with the oracle at 1e-13 relative).
+#pragma once
+
+#include "qtile.cuh"
+
+namespace qlra_dev {
+namespace qt8 {
+
+constexpr int NT = 512, BK = 8, STAGES = 4;
+constexpr int LDK = BK + 4;  // k-fast rows, pitch 12 (4 mod 16: conflict-free fragments)
+
+template <bool LPRE>
+struct Cfg;
+template <>
+struct Cfg<false> {  // Y task: left operand A (on the fly), right Omega~ (combined)
+  static constexpr int TM = 64, TN = 32, WRB = 2, WCB = 1, LP = 4, RP = 8;
+};
+template <>
+struct Cfg<true> {  // W task: left Psi~ (combined), right operand A (on the fly)
+  static constexpr int TM = 32, TN = 64, WRB = 1, WCB = 2, LP = 8, RP = 4;
+};
+template <bool LPRE>
+struct Layout {
+  using C = Cfg<LPRE>;
+  static constexpr int LDX = C::TN + 4;  // j-fast rows: 36 / 68 (4 mod 16)
+  static constexpr int L_ELEMS = C::LP * C::TM * LDK;
+  static constexpr int R_ELEMS = C::RP * BK * LDX;
+};
+constexpr int STAGE = (Layout<false>::L_ELEMS + Layout<false>::R_ELEMS) > (Layout<true>::L_ELEMS + Layout<true>::R_ELEMS)
+                          ? (Layout<false>::L_ELEMS + Layout<false>::R_ELEMS)
+                          : (Layout<true>::L_ELEMS + Layout<true>::R_ELEMS);
+constexpr size_t SMEM_BYTES = (size_t)STAGES * STAGE * sizeof(double);
+
+// op(L)(i, k) = l[q][i * l_si + k];  op(R)(k, j) = r[q][k * r_sk + j]
+struct Operands {
+  const double* l[8];
+  const double* r[8];
+  int64_t l_si, r_sk;
+  int64_t M, N;
+};
+
+// combination i of a's planes (left side, on the fly: no halves)
+__device__ __forceinline__ double lcomb(int i, const double (&a)[4]) {
+  switch (i) {
+    case 0: return a[0] + a[1];
+    case 1: return a[3] - a[2];
+    case 2: return a[0] - a[1];
+    case 3: return a[2] + a[3];
+    case 4: return a[1] + a[3];
+    case 5: return a[1] - a[3];
+    case 6: return a[0] + a[2];
+    default: return a[0] - a[2];
+  }
+}
+// combination i of b's planes (right side, on the fly: no halves)
+__device__ __forceinline__ double rcomb(int i, const double (&b)[4]) {
+  switch (i) {
+    case 0: return b[0] + b[1];
+    case 1: return b[2] - b[3];
+    case 2: return b[2] + b[3];
+    case 3: return b[0] - b[1];
+    case 4: return b[1] + b[2];
+    case 5: return b[1] - b[2];
+    case 6: return b[0] - b[3];
+    default: return b[0] + b[3];
+  }
+}
+
+// Accumulators: acc[i][rb][cb][h] = product m_{i+1} at row
+// 8*WRB*warp_row + 8*rb + lane/4, col 8*WCB*warp_col + 8*cb + 2*(lane%4) + h.
+template <bool LPRE>
+using Acc = double[8][Cfg<LPRE>::WRB][Cfg<LPRE>::WCB][2];
+
+template <bool LPRE>
+__device__ __forceinline__ void zero_acc(Acc<LPRE>& acc) {
+  using C = Cfg<LPRE>;
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int rb = 0; rb < C::WRB; ++rb)
+#pragma unroll
+      for (int cb = 0; cb < C::WCB; ++cb) acc[i][rb][cb][0] = acc[i][rb][cb][1] = 0.0;
+}
+
+// the quaternion planes of one accumulator element (fixed summation order)
+__device__ __forceinline__ void combine(const double (&m)[8], double (&c)[4]) {
+  const double s56 = m[4] + m[5], d78 = m[6] - m[7];
+  c[0] = m[1] - s56 + (m[6] + m[7]);
+  c[1] = m[0] - s56 - (m[6] + m[7]);
+  c[2] = m[2] + (m[4] - m[5]) + d78;
+  c[3] = m[3] + (m[4] - m[5]) - d78;
+}
+
+using qt::warp_col;
+using qt::warp_row;
+
+template <bool LPRE>
+__device__ __forceinline__ int acc_row(int rb) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  return 8 * Cfg<LPRE>::WRB * warp_row(w) + 8 * rb + (lane >> 2);
+}
+template <bool LPRE>
+__device__ __forceinline__ int acc_col(int cb) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  return 8 * Cfg<LPRE>::WCB * warp_col(w) + 8 * cb + 2 * (lane & 3);
+}
+
+template <bool LPRE>
+__device__ __forceinline__ void load_stage(const Operands& g, double* Ls, double* Rs, int64_t i0, int64_t j0,
+                                           int64_t k0, int64_t kend, int tid) {
+  using C = Cfg<LPRE>;
+  using Lay = Layout<LPRE>;
+  constexpr int LPER = C::TM * BK, RPER = BK * C::TN;
+#pragma unroll
+  for (int r = 0; r < C::LP * LPER / NT; ++r) {
+    const int e = tid + NT * r;
+    const int q = e / LPER, idx = e % LPER;
+    const int x = idx / BK, k = idx % BK;
+    const int64_t gi = i0 + x, gk = k0 + k;
+    const bool ok = gi < g.M && gk < kend;
+    const double* src = ok ? g.l[q] + gi * g.l_si + gk : g.l[q];
+    qt::cp_async8(Ls + (q * C::TM + x) * LDK + k, src, ok);
+  }
+#pragma unroll
+  for (int r = 0; r < C::RP * RPER / NT; ++r) {
+    const int e = tid + NT * r;
+    const int q = e / RPER, idx = e % RPER;
+    const int x = idx % C::TN, k = idx / C::TN;
+    const int64_t gj = j0 + x, gk = k0 + k;
+    const bool ok = gj < g.N && gk < kend;
+    const double* src = ok ? g.r[q] + gk * g.r_sk + gj : g.r[q];
+    qt::cp_async8(Rs + (q * BK + k) * Lay::LDX + x, src, ok);
+  }
+}
+
+// One BK slice for the first NRB row blocks and NCB column blocks of the warp.
+template <bool LPRE, int NRB, int NCB>
+__device__ __forceinline__ void kstep(const double* Ls, const double* Rs, int wr, int wc, int gid, int tig,
+                                      Acc<LPRE>& acc) {
+  using C = Cfg<LPRE>;
+  constexpr int LDX = Layout<LPRE>::LDX;
+#pragma unroll
+  for (int kk = 0; kk < BK / 4; ++kk) {
+    const int k = 4 * kk + tig;
+    if (!LPRE) {
+      // left = A: 4 planes per row block, combined in registers
+      double a[NRB][4];
+#pragma unroll
+      for (int rb = 0; rb < NRB; ++rb) {
+        const int x = 8 * C::WRB * wr + 8 * rb + gid;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) a[rb][q] = Ls[(q * C::TM + x) * LDK + k];
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        double bv[NCB];
+#pragma unroll
+        for (int cb = 0; cb < NCB; ++cb) bv[cb] = Rs[(i * BK + k) * LDX + 8 * C::WCB * wc + 8 * cb + gid];
+#pragma unroll
+        for (int rb = 0; rb < NRB; ++rb) {
+          const double av = lcomb(i, a[rb]);
+#pragma unroll
+          for (int cb = 0; cb < NCB; ++cb) qt::dmma(acc[i][rb][cb], av, bv[cb]);
+        }
+      }
+    } else {
+      // right = A: 4 planes per column block, combined in registers
+      double b[NCB][4];
+#pragma unroll
+      for (int cb = 0; cb < NCB; ++cb) {
+        const int x = 8 * C::WCB * wc + 8 * cb + gid;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) b[cb][q] = Rs[(q * BK + k) * LDX + x];
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        double av[NRB];
+#pragma unroll
+        for (int rb = 0; rb < NRB; ++rb) av[rb] = Ls[(i * C::TM + 8 * C::WRB * wr + 8 * rb + gid) * LDK + k];
+#pragma unroll
+        for (int cb = 0; cb < NCB; ++cb) {
+          const double bv = rcomb(i, b[cb]);
+#pragma unroll
+          for (int rb = 0; rb < NRB; ++rb) qt::dmma(acc[i][rb][cb], av[rb], bv);
+        }
+      }
+    }
+  }
+}
+
+// The cp.async ring with mbarrier stage handoff (as qtile.cuh's mma_loop).
+template <bool LPRE, int NRB, int NCB>
+__device__ __forceinline__ void mma_loop(const Operands& g, double* smem, int64_t i0, int64_t j0, int64_t kbeg,
+                                         int64_t kend, Acc<LPRE>& acc, uint64_t* full, uint64_t* empty) {
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int wr = warp_row(w), wc = warp_col(w);
+  const int gid = lane >> 2, tig = lane & 3;
+  const int nk = kend > kbeg ? (int)((kend - kbeg + BK - 1) / BK) : 0;
+  constexpr int LOFF = Layout<LPRE>::L_ELEMS;
+  if (tid == 0) {
+#pragma unroll
+    for (int s = 0; s < STAGES; ++s) {
+      qt::mbar_init(&full[s], NT);
+      qt::mbar_init(&empty[s], NT / 32);
+    }
+  }
+  __syncthreads();
+  if (nk > 0) {
+    load_stage<LPRE>(g, smem, smem + LOFF, i0, j0, kbeg, kend, tid);
+    qt::cp_async_arrive(&full[0]);
+  }
+  for (int kt = 0; kt < nk; ++kt) {
+    const int s = kt % STAGES;
+    const int nxt = kt + 1;
+    if (nxt < nk) {
+      const int sn = nxt % STAGES;
+      if (nxt >= STAGES) qt::mbar_wait_parity(&empty[sn], (unsigned)((nxt / STAGES - 1) & 1));
+      load_stage<LPRE>(g, smem + sn * STAGE, smem + sn * STAGE + LOFF, i0, j0, kbeg + (int64_t)nxt * BK, kend, tid);
+      qt::cp_async_arrive(&full[sn]);
+    }
+    qt::mbar_wait_parity(&full[s], (unsigned)((kt / STAGES) & 1));
+    const double* Ls = smem + s * STAGE;
+    if (NRB > 0 && NCB > 0)
+      kstep<LPRE, (NRB > 0 ? NRB : 1), (NCB > 0 ? NCB : 1)>(Ls, Ls + LOFF, wr, wc, gid, tig, acc);
+    __syncwarp();
+    if (lane == 0) qt::mbar_arrive(&empty[s]);
+  }
+  qt::cp_async_wait<0>();
+  __syncthreads();
+}
+
+// acc (8 products) over k in [kbeg, kend) for the tile at (i0, j0).  Warp
+// blocks past M or N issue no DMMA (the loop instance is chosen per warp).
+template <bool LPRE>
+__device__ __forceinline__ void mma_tile(const Operands& g, double* smem, int64_t i0, int64_t j0, int64_t kbeg,
+                                         int64_t kend, Acc<LPRE>& acc) {
+  using C = Cfg<LPRE>;
+  __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES];
+  const int w = threadIdx.x >> 5;
+  const int64_t r0w = i0 + 8 * C::WRB * warp_row(w), c0w = j0 + 8 * C::WCB * warp_col(w);
+  const int nrb = r0w >= g.M ? 0 : (int)min((int64_t)C::WRB, (g.M - r0w + 7) / 8);
+  const int ncb = c0w >= g.N ? 0 : (int)min((int64_t)C::WCB, (g.N - c0w + 7) / 8);
+  if (!LPRE) {  // WRB = 2, WCB = 1
+    switch (nrb * 4 + ncb) {
+      case 2 * 4 + 1: mma_loop<LPRE, 2, 1>(g, smem, i0, j0, kbeg, kend, acc, full, empty); break;
+      case 1 * 4 + 1: mma_loop<LPRE, 1, 1>(g, smem, i0, j0, kbeg, kend, acc, full, empty); break;
+      default: mma_loop<LPRE, 0, 0>(g, smem, i0, j0, kbeg, kend, acc, full, empty); break;
+    }
+  } else {  // WRB = 1, WCB = 2
+    switch (nrb * 4 + ncb) {
+      case 1 * 4 + 2: mma_loop<LPRE, 1, 2>(g, smem, i0, j0, kbeg, kend, acc, full, empty); break;
+      case 1 * 4 + 1: mma_loop<LPRE, 1, 1>(g, smem, i0, j0, kbeg, kend, acc, full, empty); break;
+      default: mma_loop<LPRE, 0, 0>(g, smem, i0, j0, kbeg, kend, acc, full, empty); break;
+    }
+  }
+}
+
+}  // namespace qt8
+}  // namespace qlra_dev

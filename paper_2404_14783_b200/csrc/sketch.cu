@@ -26,6 +26,7 @@
 #include "common.cuh"
 #include "kernels.cuh"
 #include "qtile.cuh"
+#include "qtile8.cuh"
 
 namespace qlra_dev {
 
@@ -126,9 +127,136 @@ __global__ void __launch_bounds__(NT, 1) sketch_fused_kernel(FusedArgs f) {
 }
 
 
+// ---- the 8-product path (qtile8.cuh) --------------------------------------
+// Y-tasks: 64x32 tiles of A * Omega~; W-tasks: 32x64 tiles of Psi~ * A.
+constexpr int Y8M = qt8::Cfg<false>::TM, Y8N = qt8::Cfg<false>::TN;
+constexpr int W8M = qt8::Cfg<true>::TM, W8N = qt8::Cfg<true>::TN;
+
+struct Fused8Args {
+  qt8::Operands yop;  // A_panel (k-fast) x Omega~ (8 planes, j-fast): M = panel rows, N = s, K = n
+  qt8::Operands wop;  // Psi~_panel (8 planes, k-fast) x A_panel (j-fast): M = l, N = n, K = panel rows
+  int64_t ky, kw;
+  int y_tm, y_tn, zy;
+  int64_t ky_chunk;
+  int w_tm, w_tn, zw;
+  int64_t kw_chunk;
+  int y_tnf, w_tmf;
+  double* y[4];
+  int64_t ldy;
+  double* yp;
+  double* w[4];
+  int64_t ldw;
+  double* wp;
+};
+
+template <bool LPRE>
+__device__ __forceinline__ void store_tile8(const qt8::Acc<LPRE>& acc, int64_t i0, int64_t j0, int64_t M, int64_t N,
+                                            double* const* c, int64_t ldc, double* part) {
+  using C = qt8::Cfg<LPRE>;
+#pragma unroll
+  for (int rb = 0; rb < C::WRB; ++rb) {
+    const int64_t gi = i0 + qt8::acc_row<LPRE>(rb);
+    if (gi >= M) continue;
+#pragma unroll
+    for (int cb = 0; cb < C::WCB; ++cb)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int64_t gj = j0 + qt8::acc_col<LPRE>(cb) + h;
+        if (gj >= N) continue;
+        double m[8], q[4];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) m[i] = acc[i][rb][cb][h];
+        qt8::combine(m, q);
+        if (part) {
+#pragma unroll
+          for (int p = 0; p < 4; ++p) part[(int64_t)p * M * N + gi * N + gj] = q[p];
+        } else {
+#pragma unroll
+          for (int p = 0; p < 4; ++p) {
+            double* dst = c[p] + gi * ldc + gj;
+            *dst = *dst + q[p];
+          }
+        }
+      }
+  }
+}
+
+// Task order as sketch_fused_kernel: full W tiles, full Y tiles, padded Y
+// column tiles, padded W row tiles.
+__global__ void __launch_bounds__(qt8::NT, 1) sketch8_kernel(Fused8Args f) {
+  extern __shared__ __align__(16) double smem[];
+  const int nwf = f.w_tmf * f.w_tn * f.zw;
+  const int nyf = f.y_tm * f.y_tnf * f.zy;
+  const int nyp = f.y_tm * (f.y_tn - f.y_tnf) * f.zy;
+  int t = blockIdx.x;
+  bool is_w;
+  int tm, tn, z;
+  if (t < nwf) {
+    is_w = true;
+    z = t % f.zw; t /= f.zw;
+    tm = t % f.w_tmf; tn = t / f.w_tmf;
+  } else if ((t -= nwf) < nyf) {
+    is_w = false;
+    z = t % f.zy; t /= f.zy;
+    tn = t % f.y_tnf; tm = t / f.y_tnf;
+  } else if ((t -= nyf) < nyp) {
+    is_w = false;
+    z = t % f.zy; t /= f.zy;
+    tn = f.y_tnf + t % (f.y_tn - f.y_tnf); tm = t / (f.y_tn - f.y_tnf);
+  } else {
+    t -= nyp;
+    is_w = true;
+    z = t % f.zw; t /= f.zw;
+    tm = f.w_tmf + t % (f.w_tm - f.w_tmf); tn = t / (f.w_tm - f.w_tmf);
+  }
+  if (!is_w) {
+    qt8::Acc<false> acc;
+    qt8::zero_acc<false>(acc);
+    const int64_t kb = (int64_t)z * f.ky_chunk, ke = min(f.ky, kb + f.ky_chunk);
+    qt8::mma_tile<false>(f.yop, smem, (int64_t)tm * Y8M, (int64_t)tn * Y8N, kb, ke, acc);
+    double* part = f.zy > 1 ? f.yp + (int64_t)z * 4 * f.yop.M * f.yop.N : nullptr;
+    store_tile8<false>(acc, (int64_t)tm * Y8M, (int64_t)tn * Y8N, f.yop.M, f.yop.N, f.y, f.ldy, part);
+  } else {
+    qt8::Acc<true> acc;
+    qt8::zero_acc<true>(acc);
+    const int64_t kb = (int64_t)z * f.kw_chunk, ke = min(f.kw, kb + f.kw_chunk);
+    qt8::mma_tile<true>(f.wop, smem, (int64_t)tm * W8M, (int64_t)tn * W8N, kb, ke, acc);
+    double* part = f.zw > 1 ? f.wp + (int64_t)z * 4 * f.wop.M * f.wop.N : nullptr;
+    store_tile8<true>(acc, (int64_t)tm * W8M, (int64_t)tn * W8N, f.wop.M, f.wop.N, f.w, f.ldw, part);
+  }
+}
+
+// out plane i (rows x cols, ld = cols) = combination i of in's planes, the
+// left (Psi) or right (Omega) set, halves folded into i >= 4
+__global__ void combine8_kernel(QView in, double* out, int left) {
+  const int64_t rows = in.rows, cols = in.cols, total = rows * cols;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / cols, j = e % cols;
+    double v[4];
+#pragma unroll
+    for (int p = 0; p < 4; ++p) v[p] = in.p[p][i * in.ld + j];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const double x = left ? qt8::lcomb(c, v) : qt8::rcomb(c, v);
+      out[(int64_t)c * total + e] = c >= 4 ? 0.5 * x : x;
+    }
+  }
+}
+
 }  // namespace
 
-const char* sketch_kernel_name() { return "sketch_fused_kernel(dmma_64x64x8, mbarrier ring, panels <= 2 GB)"; }
+bool sketch_use8() {
+  static const bool v = [] {
+    const char* e = std::getenv("QLRA_SKETCH16");
+    return !(e && std::atoi(e) != 0);
+  }();
+  return v;
+}
+
+const char* sketch_kernel_name() {
+  return sketch_use8() ? "sketch8_kernel(8-product quaternion GEMM on DMMA, 64x32/32x64 tiles, mbarrier ring, panels <= 2 GB)"
+                       : "sketch_fused_kernel(dmma_64x64x8, mbarrier ring, panels <= 2 GB)";
+}
 
 namespace {
 
@@ -136,16 +264,25 @@ struct SketchWork {
   DeviceBuffer yp, wp;  // split-K partial workspaces, grown on demand
 };
 
+// Tile geometry of a fused launch: Y tiles ym x yn, W tiles wm x wn, each
+// made of 8x8 blocks (padded blocks cost nothing).
+struct Geom {
+  int ym, yn, wm, wn;
+};
+constexpr Geom kGeom16{BM, BN, BM, BN};
+constexpr Geom kGeom8{Y8M, Y8N, W8M, W8N};
+
 // Makespan of one fused launch under greedy list scheduling on 148 SMs
-// (1 CTA per SM), tasks in kernel order.
-double simulate_panel(int64_t rp, int64_t n, int64_t s, int64_t l, int zy, int zw) {
+// (1 CTA per SM), tasks in kernel order.  Cost unit: one BK k-step of a full
+// tile (both engines' Y and W tiles cost the same per k-step).
+double simulate_panel(const Geom& G, int64_t rp, int64_t n, int64_t s, int64_t l, int zy, int zw) {
   const int64_t kyc = ((n + zy - 1) / zy + BK - 1) / BK * BK, kwc = ((rp + zw - 1) / zw + BK - 1) / BK * BK;
   const int64_t ny_chunks = (n + kyc - 1) / kyc, nw_chunks = (rp + kwc - 1) / kwc;
-  const int64_t y_tm = (rp + BM - 1) / BM, y_tn = (s + BN - 1) / BN, w_tm = (l + BM - 1) / BM,
-                w_tn = (n + BN - 1) / BN;
-  const int64_t y_tnf = s / BN, w_tmf = l / BM;
-  auto frac = [](int64_t valid) { return (double)((valid + 7) / 8) / 8.0; };  // 8-blocks of 64
-  const double y_part = frac(s - y_tnf * BN), w_part = frac(l - w_tmf * BM);
+  const int64_t y_tm = (rp + G.ym - 1) / G.ym, y_tn = (s + G.yn - 1) / G.yn, w_tm = (l + G.wm - 1) / G.wm,
+                w_tn = (n + G.wn - 1) / G.wn;
+  const int64_t y_tnf = s / G.yn, w_tmf = l / G.wm;
+  auto frac = [](int64_t valid, int dim) { return (double)((valid + 7) / 8) / (dim / 8); };
+  const double y_part = frac(s - y_tnf * G.yn, G.yn), w_part = frac(l - w_tmf * G.wm, G.wm);
   struct Group { int64_t count; double cost; };
   const Group groups[4] = {{w_tmf * w_tn * nw_chunks, (double)(kwc / BK)},
                            {y_tm * y_tnf * ny_chunks, (double)(kyc / BK)},
@@ -171,21 +308,21 @@ double simulate_panel(int64_t rp, int64_t n, int64_t s, int64_t l, int zy, int z
   }
   const double mk = sm.rbegin()->first;
   // split-K partials cost a reduction pass over zy Y / zw W copies
-  // (~1 k-step of time per 25 MB of partials)
+  // (~1 k-step of a 64x64 tile per 25 MB of partials; scaled by tile area)
   const double red = (zy > 1 ? (double)zy * rp * s : 0.0) + (zw > 1 ? (double)zw * l * n : 0.0);
-  return mk + red * 32.0 / 25e6;
+  return mk + red * 32.0 / 25e6 * (double)(BM * BN) / (double)(G.ym * G.yn);
 }
 
-std::pair<int, int> choose_panel_splits(int64_t rp, int64_t n, int64_t s, int64_t l) {
+std::pair<int, int> choose_panel_splits(const Geom& G, int64_t rp, int64_t n, int64_t s, int64_t l) {
   static std::mutex mu;
-  static std::map<std::array<int64_t, 4>, std::pair<int, int>> cache;
-  const std::array<int64_t, 4> key{rp, n, s, l};
+  static std::map<std::array<int64_t, 5>, std::pair<int, int>> cache;
+  const std::array<int64_t, 5> key{rp, n, s, l, (int64_t)G.ym * 1000 + G.yn};
   {
     std::lock_guard<std::mutex> lock(mu);
     auto it = cache.find(key);
     if (it != cache.end()) return it->second;
   }
-  const int64_t wt = ((l + BM - 1) / BM) * ((n + BN - 1) / BN);
+  const int64_t wt = ((l + G.wm - 1) / G.wm) * ((n + G.wn - 1) / G.wn);
   // W split-K only while W has fewer than 4 waves of tiles (its partials are
   // l x n each: 868 MB at C4)
   const int zw_max = wt >= 4 * 148 ? 1 : (int)std::max<int64_t>(1, std::min<int64_t>(wt >= 148 ? 8 : 64, rp / 64));
@@ -201,7 +338,7 @@ std::pair<int, int> choose_panel_splits(int64_t rp, int64_t n, int64_t s, int64_
   std::pair<int, int> arg{1, 1};
   for (int zw : candidates(zw_max))
     for (int zy : candidates(zy_max)) {
-      const double mk = simulate_panel(rp, n, s, l, zy, zw);
+      const double mk = simulate_panel(G, rp, n, s, l, zy, zw);
       if (mk < best - 1e-9) { best = mk; arg = {zy, zw}; }
     }
   {
@@ -210,101 +347,174 @@ std::pair<int, int> choose_panel_splits(int64_t rp, int64_t n, int64_t s, int64_
   }
   if (std::getenv("QLRA_DEBUG_SPLITS")) {
     // ideal = total cost / 148 (perfect balance, no per-CTA overhead)
-    const int64_t y_tm = (rp + BM - 1) / BM, y_tn = (s + BN - 1) / BN, w_tm = (l + BM - 1) / BM,
-                  w_tn = (n + BN - 1) / BN;
-    auto frac = [](int64_t valid) { return (double)((valid + 7) / 8) / 8.0; };
-    const double yc = (double)y_tm * ((double)(s / BN) + (y_tn > s / BN ? frac(s - (s / BN) * BN) : 0.0)) * (double)n / BK;
-    const double wc = (double)w_tn * ((double)(l / BM) + (w_tm > l / BM ? frac(l - (l / BM) * BM) : 0.0)) * (double)rp / BK;
-    std::fprintf(stderr, "[qlra] panel %lldx%lld s=%lld l=%lld: zy=%d zw=%d makespan %.0f ideal %.0f (%.1f%%)\n",
-                 (long long)rp, (long long)n, (long long)s, (long long)l, arg.first, arg.second, best,
-                 (yc + wc) / 148.0, 100.0 * (yc + wc) / 148.0 / best);
+    const int64_t y_tm = (rp + G.ym - 1) / G.ym, y_tn = (s + G.yn - 1) / G.yn, w_tm = (l + G.wm - 1) / G.wm,
+                  w_tn = (n + G.wn - 1) / G.wn;
+    auto frac = [](int64_t valid, int dim) { return (double)((valid + 7) / 8) / (dim / 8); };
+    const double yc = (double)y_tm * ((double)(s / G.yn) + (y_tn > s / G.yn ? frac(s - (s / G.yn) * G.yn, G.yn) : 0.0)) * (double)n / BK;
+    const double wc = (double)w_tn * ((double)(l / G.wm) + (w_tm > l / G.wm ? frac(l - (l / G.wm) * G.wm, G.wm) : 0.0)) * (double)rp / BK;
+    std::fprintf(stderr, "[qlra] panel %lldx%lld s=%lld l=%lld tiles %dx%d/%dx%d: zy=%d zw=%d makespan %.0f ideal %.0f (%.1f%%)\n",
+                 (long long)rp, (long long)n, (long long)s, (long long)l, G.ym, G.yn, G.wm, G.wn, arg.first, arg.second,
+                 best, (yc + wc) / 148.0, 100.0 * (yc + wc) / 148.0 / best);
   }
   return arg;
 }
 
+// The embeddings of one sketch call: Omega (n x s) and the Psi column block
+// (l x b), plain (16-product engine) or as their 8 plane combinations
+// (8-product engine; planes of rows x cols each, ld = cols).
+struct Emb {
+  QView om, ps;
+  const double* om8 = nullptr;  // 8 x (n x s)
+  const double* ps8 = nullptr;  // 8 x (l x b)
+};
+
+// Event-timed launch bracket (bench evidence, ctx.ktimer).
+struct LaunchTimer {
+  Ctx& ctx;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  explicit LaunchTimer(Ctx& c) : ctx(c) {
+    if (!ctx.ktimer.on) return;
+    if (!ctx.ktimer.pool.empty()) {
+      e0 = ctx.ktimer.pool.back().first;
+      e1 = ctx.ktimer.pool.back().second;
+      ctx.ktimer.pool.pop_back();
+    } else {
+      QLRA_CUDA(cudaEventCreate(&e0));
+      QLRA_CUDA(cudaEventCreate(&e1));
+    }
+    QLRA_CUDA(cudaEventRecord(e0, ctx.stream));
+  }
+  void done(int64_t rp, int64_t n, int64_t s, int64_t l) {
+    if (!ctx.ktimer.on) return;
+    QLRA_CUDA(cudaEventRecord(e1, ctx.stream));
+    ctx.ktimer.ev.emplace_back(e0, e1);
+    ctx.ktimer.flops += 32.0 * (double)rp * (double)n * (double)(s + l);
+    ctx.ktimer.a_bytes += 32.0 * (double)rp * (double)n;
+    ++ctx.ktimer.launches;
+  }
+};
+
+template <class Args>
+void set_splits(Args& f, const Geom& G, int64_t rp, int64_t n, int64_t s, int64_t l, Ctx& ctx, SketchWork& ws) {
+  f.y_tm = (int)((rp + G.ym - 1) / G.ym);
+  f.y_tn = (int)((s + G.yn - 1) / G.yn);
+  f.w_tm = (int)((l + G.wm - 1) / G.wm);
+  f.w_tn = (int)((n + G.wn - 1) / G.wn);
+  f.y_tnf = (int)(s / G.yn);
+  f.w_tmf = (int)(l / G.wm);
+  // Split counts (zy over n, zw over the panel rows) from a simulation of
+  // the dispatcher: CTAs in kernel order (longest first) go to the SM that
+  // frees first; cost = k-steps x fraction of 8x8 blocks inside M x N.
+  // Cached per panel shape.
+  const auto choice = choose_panel_splits(G, rp, n, s, l);
+  f.kw_chunk = ((rp + choice.second - 1) / choice.second + BK - 1) / BK * BK;
+  f.zw = (int)((rp + f.kw_chunk - 1) / f.kw_chunk);
+  f.ky_chunk = ((n + choice.first - 1) / choice.first + BK - 1) / BK * BK;
+  f.zy = (int)((n + f.ky_chunk - 1) / f.ky_chunk);
+  if (f.zy > 1) {
+    const size_t need = (size_t)f.zy * 4 * rp * s * sizeof(double);
+    if (ws.yp.bytes < need) ws.yp = DeviceBuffer(ctx, need);
+    f.yp = ws.yp.as<double>();
+  }
+  if (f.zw > 1) {
+    const size_t need = (size_t)f.zw * 4 * l * n * sizeof(double);
+    if (ws.wp.bytes < need) ws.wp = DeviceBuffer(ctx, need);
+    f.wp = ws.wp.as<double>();
+  }
+}
+
 // One fused launch (+ ordered partial reductions) for a row panel `ap` of A
 // whose Psi columns are ps[:, pc0 : pc0 + ap.rows].
-void sketch_panel(Ctx& ctx, const QView& om, const QView& ps, int64_t pc0, const QView& ap,
-                  const QView& yv, const QView& w, SketchWork& ws) {
-  const int64_t rp = ap.rows, n = ap.cols, s = om.cols, l = ps.rows;
-  const int w_tm = (int)((l + BM - 1) / BM), w_tn = (int)((n + BN - 1) / BN);
-  DeviceBuffer& yp = ws.yp;
-  DeviceBuffer& wp = ws.wp;
-  {
-    FusedArgs f{};
+void sketch_panel(Ctx& ctx, const Emb& e, int64_t pc0, const QView& ap, const QView& yv, const QView& w,
+                  SketchWork& ws) {
+  const int64_t rp = ap.rows, n = ap.cols, s = e.om.cols, l = e.ps.rows;
+  if (e.om8) {
+    Fused8Args f{};
+    const int64_t pb = e.ps.cols;  // Psi block columns (ld of the combined planes)
     for (int p = 0; p < 4; ++p) {
-      f.yop.a[p] = ap.p[p];
-      f.yop.b[p] = om.p[p];
-      f.wop.a[p] = ps.p[p] + pc0;  // Psi[:, pc0:pc0+rp]
-      f.wop.b[p] = ap.p[p];
+      f.yop.l[p] = ap.p[p];
+      f.wop.r[p] = ap.p[p];
       f.y[p] = yv.p[p];
       f.w[p] = w.p[p];
     }
-    f.yop.a_si = ap.ld; f.yop.a_sk = 1; f.yop.b_sk = om.ld; f.yop.b_sj = 1;
+    for (int i = 0; i < 8; ++i) {
+      f.yop.r[i] = e.om8 + (size_t)i * n * s;
+      f.wop.l[i] = e.ps8 + (size_t)i * l * pb + pc0;  // Psi~[:, pc0:pc0+rp]
+    }
+    f.yop.l_si = ap.ld; f.yop.r_sk = s;
     f.yop.M = rp; f.yop.N = s;
-    f.wop.a_si = ps.ld; f.wop.a_sk = 1; f.wop.b_sk = ap.ld; f.wop.b_sj = 1;
+    f.wop.l_si = pb; f.wop.r_sk = ap.ld;
     f.wop.M = l; f.wop.N = n;
     f.ky = n;
     f.kw = rp;
     f.ldy = yv.ld;
     f.ldw = w.ld;
-    f.y_tm = (int)((rp + BM - 1) / BM);
-    f.y_tn = (int)((s + BN - 1) / BN);
-    f.w_tm = w_tm;
-    f.w_tn = w_tn;
-    // Split counts (zy over n, zw over the panel rows) from a simulation of
-    // the dispatcher: CTAs in kernel order (longest first) go to the SM that
-    // frees first; cost = k-steps x fraction of 8x8 blocks inside M x N.
-    // Cached per panel shape.
-    f.y_tnf = (int)(s / BN);
-    f.w_tmf = (int)(l / BM);
-    const auto choice = choose_panel_splits(rp, n, s, l);
-    const int best_zy = choice.first, best_zw = choice.second;
-    f.kw_chunk = ((rp + best_zw - 1) / best_zw + BK - 1) / BK * BK;
-    f.zw = (int)((rp + f.kw_chunk - 1) / f.kw_chunk);
-    f.ky_chunk = ((n + best_zy - 1) / best_zy + BK - 1) / BK * BK;
-    f.zy = (int)((n + f.ky_chunk - 1) / f.ky_chunk);
-    if (f.zy > 1) {
-      const size_t need = (size_t)f.zy * 4 * rp * s * sizeof(double);
-      if (yp.bytes < need) yp = DeviceBuffer(ctx, need);
-      f.yp = yp.as<double>();
-    }
-    if (f.zw > 1) {
-      const size_t need = (size_t)f.zw * 4 * l * n * sizeof(double);
-      if (wp.bytes < need) wp = DeviceBuffer(ctx, need);
-      f.wp = wp.as<double>();
-    }
-    const int64_t ctas = (int64_t)f.y_tm * f.y_tn * f.zy + (int64_t)w_tm * w_tn * f.zw;
-    cudaEvent_t e0 = nullptr, e1 = nullptr;
-    if (ctx.ktimer.on) {
-      if (!ctx.ktimer.pool.empty()) {
-        e0 = ctx.ktimer.pool.back().first;
-        e1 = ctx.ktimer.pool.back().second;
-        ctx.ktimer.pool.pop_back();
-      } else {
-        QLRA_CUDA(cudaEventCreate(&e0));
-        QLRA_CUDA(cudaEventCreate(&e1));
-      }
-      QLRA_CUDA(cudaEventRecord(e0, ctx.stream));
-    }
-    sketch_fused_kernel<<<(unsigned)ctas, NT, qt::SMEM_BYTES, ctx.stream>>>(f);
+    set_splits(f, kGeom8, rp, n, s, l, ctx, ws);
+    const int64_t ctas = (int64_t)f.y_tm * f.y_tn * f.zy + (int64_t)f.w_tm * f.w_tn * f.zw;
+    LaunchTimer lt(ctx);
+    sketch8_kernel<<<(unsigned)ctas, qt8::NT, qt8::SMEM_BYTES, ctx.stream>>>(f);
     QLRA_LAUNCH_CHECK();
     count_launch();
-    if (ctx.ktimer.on) {
-      QLRA_CUDA(cudaEventRecord(e1, ctx.stream));
-      ctx.ktimer.ev.emplace_back(e0, e1);
-      ctx.ktimer.flops += 32.0 * (double)rp * (double)n * (double)(s + l);
-      ctx.ktimer.a_bytes += 32.0 * (double)rp * (double)n;
-      ++ctx.ktimer.launches;
-    }
+    lt.done(rp, n, s, l);
     if (f.zy > 1) splitk_reduce(ctx, f.yp, f.zy, yv, 1.0, 1.0);
     if (f.zw > 1) splitk_reduce(ctx, f.wp, f.zw, w, 1.0, 1.0);
+    return;
   }
+  FusedArgs f{};
+  for (int p = 0; p < 4; ++p) {
+    f.yop.a[p] = ap.p[p];
+    f.yop.b[p] = e.om.p[p];
+    f.wop.a[p] = e.ps.p[p] + pc0;  // Psi[:, pc0:pc0+rp]
+    f.wop.b[p] = ap.p[p];
+    f.y[p] = yv.p[p];
+    f.w[p] = w.p[p];
+  }
+  f.yop.a_si = ap.ld; f.yop.a_sk = 1; f.yop.b_sk = e.om.ld; f.yop.b_sj = 1;
+  f.yop.M = rp; f.yop.N = s;
+  f.wop.a_si = e.ps.ld; f.wop.a_sk = 1; f.wop.b_sk = ap.ld; f.wop.b_sj = 1;
+  f.wop.M = l; f.wop.N = n;
+  f.ky = n;
+  f.kw = rp;
+  f.ldy = yv.ld;
+  f.ldw = w.ld;
+  set_splits(f, kGeom16, rp, n, s, l, ctx, ws);
+  const int64_t ctas = (int64_t)f.y_tm * f.y_tn * f.zy + (int64_t)f.w_tm * f.w_tn * f.zw;
+  LaunchTimer lt(ctx);
+  sketch_fused_kernel<<<(unsigned)ctas, NT, qt::SMEM_BYTES, ctx.stream>>>(f);
+  QLRA_LAUNCH_CHECK();
+  count_launch();
+  lt.done(rp, n, s, l);
+  if (f.zy > 1) splitk_reduce(ctx, f.yp, f.zy, yv, 1.0, 1.0);
+  if (f.zw > 1) splitk_reduce(ctx, f.wp, f.zw, w, 1.0, 1.0);
+}
+
+// Plane combinations of an embedding for the 8-product engine.
+void launch_combine8(Ctx& ctx, const QView& in, double* out, bool left) {
+  const int64_t total = in.rows * in.cols;
+  if (total == 0) return;
+  const int threads = 256;
+  const int64_t blocks = std::min<int64_t>((total + threads - 1) / threads, 148 * 16);
+  combine8_kernel<<<(unsigned)blocks, threads, 0, ctx.stream>>>(in, out, left ? 1 : 0);
+  QLRA_LAUNCH_CHECK();
+  count_launch();
+}
+
+// Fill e.om8 / e.ps8 (when the 8-product engine is on) into `store`.
+void prepare_emb(Ctx& ctx, Emb& e, DeviceBuffer& store) {
+  if (!sketch_use8()) return;
+  const size_t no = (size_t)8 * e.om.rows * e.om.cols, np = (size_t)8 * e.ps.rows * e.ps.cols;
+  store = DeviceBuffer(ctx, (no + np) * sizeof(double));
+  double* base = store.as<double>();
+  launch_combine8(ctx, e.om, base, false);
+  launch_combine8(ctx, e.ps, base + no, true);
+  e.om8 = base;
+  e.ps8 = base + no;
 }
 
 void set_kernel_attrs() {
   set_func_attr((const void*)sketch_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                 (int)qt::SMEM_BYTES);
+  set_func_attr((const void*)sketch8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)qt8::SMEM_BYTES);
 }
 
 // Rows per fused launch.  Device-resident A: panels of up to kPanelBytes --
@@ -405,12 +615,16 @@ void sketch_update_rows(Ctx& ctx, const qlra_spec_t& omega, const qlra_spec_t& p
   set_kernel_attrs();
   DevQMat om(ctx, n, s), ps_tmp;
   launch_gen(ctx.stream, omega, 0, 0, n, s, om.v, false);
-  const QView ps = psi_for_sketch(ctx, psi, row0, b, ps_tmp);
+  Emb e;
+  e.om = om.v;
+  e.ps = psi_for_sketch(ctx, psi, row0, b, ps_tmp);
+  DeviceBuffer comb;
+  prepare_emb(ctx, e, comb);
   const int64_t R = panel_rows(n, b);
   SketchWork ws;
   for (int64_t r0 = 0; r0 < b; r0 += R) {
     const int64_t rp = std::min(R, b - r0);
-    sketch_panel(ctx, om.v, ps, r0, sub(block, r0, 0, rp, n), sub(y_rows, r0, 0, rp, s), w, ws);
+    sketch_panel(ctx, e, r0, sub(block, r0, 0, rp, n), sub(y_rows, r0, 0, rp, s), w, ws);
   }
 }
 
@@ -441,7 +655,11 @@ void sketch_update_rows_host(Ctx& ctx, const qlra_spec_t& omega, const qlra_spec
   QLRA_CUDA(cudaEventRecord(freed[0], ctx.stream));
   QLRA_CUDA(cudaEventRecord(freed[1], ctx.stream));
   launch_gen(ctx.stream, omega, 0, 0, n, s, om.v, false);
-  const QView ps = psi_for_sketch(ctx, psi, row0, b, ps_tmp);
+  Emb e;
+  e.om = om.v;
+  e.ps = psi_for_sketch(ctx, psi, row0, b, ps_tmp);
+  DeviceBuffer comb;
+  prepare_emb(ctx, e, comb);
   SketchWork ws;
   // The last R rows go in quarter-size chunks: the sketch of the final chunk
   // is the one part of the pipeline nothing overlaps (the copy stream is the
@@ -467,7 +685,7 @@ void sketch_update_rows_host(Ctx& ctx, const qlra_spec_t& omega, const qlra_spec
     }
     QLRA_CUDA(cudaEventRecord(copied[idx], cs));
     QLRA_CUDA(cudaStreamWaitEvent(ctx.stream, copied[idx], 0));
-    sketch_panel(ctx, om.v, ps, r0, dst, sub(y_rows, r0, 0, rp, s), w, ws);
+    sketch_panel(ctx, e, r0, dst, sub(y_rows, r0, 0, rp, s), w, ws);
     QLRA_CUDA(cudaEventRecord(freed[idx], ctx.stream));
   }
   QLRA_CUDA(cudaStreamSynchronize(cs));
