@@ -37,6 +37,8 @@
 // (the sketch is compared with the oracle at 1e-13 relative).
 #pragma once
 
+#include <cuda.h>
+
 #include "qtile.cuh"
 
 namespace qlra_dev {
@@ -141,33 +143,54 @@ __device__ __forceinline__ int acc_col(int cb) {
   return 8 * Cfg<LPRE>::WCB * warp_col(w) + 8 * cb + 2 * (lane & 3);
 }
 
+// Per-thread copy plan of one tile, fixed for the whole k loop: each thread
+// copies the same (row, k) / (k, col) position of LP / RP planes every stage,
+// so a stage costs a pointer add per operand and the k bound test (the
+// general address arithmetic once per tile, not once per element per stage).
 template <bool LPRE>
-__device__ __forceinline__ void load_stage(const Operands& g, double* Ls, double* Rs, int64_t i0, int64_t j0,
-                                           int64_t k0, int64_t kend, int tid) {
+struct Loader {
   using C = Cfg<LPRE>;
   using Lay = Layout<LPRE>;
-  constexpr int LPER = C::TM * BK, RPER = BK * C::TN;
-#pragma unroll
-  for (int r = 0; r < C::LP * LPER / NT; ++r) {
-    const int e = tid + NT * r;
-    const int q = e / LPER, idx = e % LPER;
-    const int x = idx / BK, k = idx % BK;
-    const int64_t gi = i0 + x, gk = k0 + k;
-    const bool ok = gi < g.M && gk < kend;
-    const double* src = ok ? g.l[q] + gi * g.l_si + gk : g.l[q];
-    qt::cp_async8(Ls + (q * C::TM + x) * LDK + k, src, ok);
+  static constexpr int LPER = C::TM * BK, RPER = BK * C::TN;  // elements per plane per stage
+  static constexpr int LSPLIT = NT / LPER, RSPLIT = NT / RPER;   // threads groups per copy round
+  static_assert(NT % LPER == 0 && NT % RPER == 0, "copy plan");
+  static_assert(C::LP % LSPLIT == 0 && C::RP % RSPLIT == 0, "copy plan");
+  static constexpr int LCOPIES = C::LP / LSPLIT, RCOPIES = C::RP / RSPLIT;
+  int64_t loff, roff, rstep;
+  int lk, rk, lhi, rhi, ldst, rdst;
+  bool lrow, rcol;
+  __device__ __forceinline__ Loader(const Operands& g, int64_t i0, int64_t j0, int64_t kbeg, int tid) {
+    const int lidx = tid % LPER, ridx = tid % RPER;
+    lhi = tid / LPER;
+    rhi = tid / RPER;
+    const int lx = lidx / BK, rx = ridx % C::TN;
+    lk = lidx % BK;
+    rk = ridx / C::TN;
+    lrow = i0 + lx < g.M;
+    rcol = j0 + rx < g.N;
+    loff = (lrow ? (i0 + lx) * g.l_si : 0) + kbeg + lk;
+    roff = (kbeg + rk) * g.r_sk + (rcol ? j0 + rx : 0);
+    rstep = (int64_t)BK * g.r_sk;
+    ldst = (lhi * C::TM + lx) * LDK + lk;
+    rdst = (rhi * BK + rk) * Lay::LDX + rx;
   }
+  // copy stage starting at k0 (the offsets are then advanced to k0 + BK)
+  __device__ __forceinline__ void stage(const Operands& g, double* Ls, double* Rs, int64_t k0, int64_t kend) {
+    const bool lok = lrow && k0 + lk < kend, rok = rcol && k0 + rk < kend;
 #pragma unroll
-  for (int r = 0; r < C::RP * RPER / NT; ++r) {
-    const int e = tid + NT * r;
-    const int q = e / RPER, idx = e % RPER;
-    const int x = idx % C::TN, k = idx / C::TN;
-    const int64_t gj = j0 + x, gk = k0 + k;
-    const bool ok = gj < g.N && gk < kend;
-    const double* src = ok ? g.r[q] + gk * g.r_sk + gj : g.r[q];
-    qt::cp_async8(Rs + (q * BK + k) * Lay::LDX + x, src, ok);
+    for (int r = 0; r < LCOPIES; ++r) {
+      const double* base = LSPLIT == 1 ? g.l[r] : (lhi ? g.l[LSPLIT * r + 1] : g.l[LSPLIT * r]);
+      qt::cp_async8(Ls + ldst + r * LSPLIT * C::TM * LDK, lok ? base + loff : base, lok);
+    }
+#pragma unroll
+    for (int r = 0; r < RCOPIES; ++r) {
+      const double* base = RSPLIT == 1 ? g.r[r] : (rhi ? g.r[RSPLIT * r + 1] : g.r[RSPLIT * r]);
+      qt::cp_async8(Rs + rdst + r * RSPLIT * BK * Lay::LDX, rok ? base + roff : base, rok);
+    }
+    loff += BK;
+    roff += rstep;
   }
-}
+};
 
 // One BK slice for the first NRB row blocks and NCB column blocks of the warp.
 template <bool LPRE, int NRB, int NCB>
@@ -241,8 +264,9 @@ __device__ __forceinline__ void mma_loop(const Operands& g, double* smem, int64_
     }
   }
   __syncthreads();
+  Loader<LPRE> ld(g, i0, j0, kbeg, tid);
   if (nk > 0) {
-    load_stage<LPRE>(g, smem, smem + LOFF, i0, j0, kbeg, kend, tid);
+    ld.stage(g, smem, smem + LOFF, kbeg, kend);
     qt::cp_async_arrive(&full[0]);
   }
   for (int kt = 0; kt < nk; ++kt) {
@@ -251,7 +275,7 @@ __device__ __forceinline__ void mma_loop(const Operands& g, double* smem, int64_
     if (nxt < nk) {
       const int sn = nxt % STAGES;
       if (nxt >= STAGES) qt::mbar_wait_parity(&empty[sn], (unsigned)((nxt / STAGES - 1) & 1));
-      load_stage<LPRE>(g, smem + sn * STAGE, smem + sn * STAGE + LOFF, i0, j0, kbeg + (int64_t)nxt * BK, kend, tid);
+      ld.stage(g, smem + sn * STAGE, smem + sn * STAGE + LOFF, kbeg + (int64_t)nxt * BK, kend);
       qt::cp_async_arrive(&full[sn]);
     }
     qt::mbar_wait_parity(&full[s], (unsigned)((kt / STAGES) & 1));
@@ -263,6 +287,112 @@ __device__ __forceinline__ void mma_loop(const Operands& g, double* smem, int64_
   }
   qt::cp_async_wait<0>();
   __syncthreads();
+}
+
+// ---- TMA staging ------------------------------------------------------------
+// With 3D tensor maps (inner, rows, planes) over each operand, one elected
+// thread stages a whole operand tile per stage with one
+// cp.async.bulk.tensor: no per-thread address arithmetic, and the edges
+// (rows / columns / k past the extents) come back zero-filled.  Boxes are
+// the padded smem rows themselves -- left {LDK, TM, LP}, right {LDX, BK, RP}
+// -- so the pitches stay 12 / 36 / 68 (conflict-free fragment reads); the
+// over-fetched columns are never read.  The caller creates the maps so that
+// k past the chunk end is out of bounds in at least one operand, or chunks
+// end on BK boundaries (split-K).
+struct TmaOps {
+  const CUtensorMap* lm;  // left map
+  const CUtensorMap* rm;  // right map
+  int lk_off;             // inner coordinate offset of the left map's k (Psi~ panel column)
+};
+
+__device__ __forceinline__ void tma_load3(double* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
+      ::"r"(qt::smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(0), "r"(qt::smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(qt::smem_u32(bar)), "r"(bytes) : "memory");
+}
+
+template <bool LPRE>
+__device__ __forceinline__ void tma_stage(const TmaOps& t, double* Ls, double* Rs, int64_t i0, int64_t j0, int64_t k0,
+                                          uint64_t* bar) {
+  using C = Cfg<LPRE>;
+  constexpr unsigned BYTES = (unsigned)((Layout<LPRE>::L_ELEMS + Layout<LPRE>::R_ELEMS) * sizeof(double));
+  mbar_expect_tx(bar, BYTES);
+  tma_load3(Ls, t.lm, (int)(t.lk_off + k0), (int)i0, bar);
+  tma_load3(Rs, t.rm, (int)j0, (int)k0, bar);
+}
+
+// The ring with a single producer thread (thread 0) issuing each stage PF
+// stages ahead; a refill waits for every warp's release of that slot.
+template <bool LPRE, int NRB, int NCB>
+__device__ __forceinline__ void mma_loop_tma(const TmaOps& t, double* smem, int64_t i0, int64_t j0, int64_t kbeg,
+                                             int64_t kend, Acc<LPRE>& acc, uint64_t* full, uint64_t* empty) {
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int wr = warp_row(w), wc = warp_col(w);
+  const int gid = lane >> 2, tig = lane & 3;
+  const int nk = kend > kbeg ? (int)((kend - kbeg + BK - 1) / BK) : 0;
+  constexpr int LOFF = Layout<LPRE>::L_ELEMS;
+  constexpr int PF = 2;
+  if (tid == 0) {
+#pragma unroll
+    for (int s = 0; s < STAGES; ++s) {
+      qt::mbar_init(&full[s], 1);
+      qt::mbar_init(&empty[s], NT / 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (tid == 0) {
+    for (int p = 0; p < PF && p < nk; ++p)
+      tma_stage<LPRE>(t, smem + p * STAGE, smem + p * STAGE + LOFF, i0, j0, kbeg + (int64_t)p * BK, &full[p]);
+  }
+  for (int kt = 0; kt < nk; ++kt) {
+    const int s = kt % STAGES;
+    if (tid == 0) {
+      const int nxt = kt + PF;
+      if (nxt < nk) {
+        const int sn = nxt % STAGES;
+        if (nxt >= STAGES) qt::mbar_wait_parity(&empty[sn], (unsigned)((nxt / STAGES - 1) & 1));
+        tma_stage<LPRE>(t, smem + sn * STAGE, smem + sn * STAGE + LOFF, i0, j0, kbeg + (int64_t)nxt * BK, &full[sn]);
+      }
+    }
+    __syncwarp();  // warp 0 reconverges before its DMMAs (mma.sync is .aligned)
+    qt::mbar_wait_parity(&full[s], (unsigned)((kt / STAGES) & 1));
+    const double* Ls = smem + s * STAGE;
+    if (NRB > 0 && NCB > 0)
+      kstep<LPRE, (NRB > 0 ? NRB : 1), (NCB > 0 ? NCB : 1)>(Ls, Ls + LOFF, wr, wc, gid, tig, acc);
+    __syncwarp();
+    if (lane == 0) qt::mbar_arrive(&empty[s]);
+  }
+  // every issued stage was consumed (waited on full) before the loop ended
+  __syncthreads();
+}
+
+template <bool LPRE>
+__device__ __forceinline__ void mma_tile_tma(const TmaOps& t, const Operands& g, double* smem, int64_t i0, int64_t j0,
+                                             int64_t kbeg, int64_t kend, Acc<LPRE>& acc) {
+  using C = Cfg<LPRE>;
+  __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES];
+  const int w = threadIdx.x >> 5;
+  const int64_t r0w = i0 + 8 * C::WRB * warp_row(w), c0w = j0 + 8 * C::WCB * warp_col(w);
+  const int nrb = r0w >= g.M ? 0 : (int)min((int64_t)C::WRB, (g.M - r0w + 7) / 8);
+  const int ncb = c0w >= g.N ? 0 : (int)min((int64_t)C::WCB, (g.N - c0w + 7) / 8);
+  if (!LPRE) {
+    switch (nrb * 4 + ncb) {
+      case 2 * 4 + 1: mma_loop_tma<LPRE, 2, 1>(t, smem, i0, j0, kbeg, kend, acc, full, empty); break;
+      case 1 * 4 + 1: mma_loop_tma<LPRE, 1, 1>(t, smem, i0, j0, kbeg, kend, acc, full, empty); break;
+      default: mma_loop_tma<LPRE, 0, 0>(t, smem, i0, j0, kbeg, kend, acc, full, empty); break;
+    }
+  } else {
+    switch (nrb * 4 + ncb) {
+      case 1 * 4 + 2: mma_loop_tma<LPRE, 1, 2>(t, smem, i0, j0, kbeg, kend, acc, full, empty); break;
+      case 1 * 4 + 1: mma_loop_tma<LPRE, 1, 1>(t, smem, i0, j0, kbeg, kend, acc, full, empty); break;
+      default: mma_loop_tma<LPRE, 0, 0>(t, smem, i0, j0, kbeg, kend, acc, full, empty); break;
+    }
+  }
 }
 
 // acc (8 products) over k in [kbeg, kend) for the tile at (i0, j0).  Warp

@@ -23,6 +23,8 @@
 #include <mutex>
 #include <vector>
 
+#include <cudaTypedefs.h>
+
 #include "common.cuh"
 #include "kernels.cuh"
 #include "qtile.cuh"
@@ -133,6 +135,9 @@ constexpr int Y8M = qt8::Cfg<false>::TM, Y8N = qt8::Cfg<false>::TN;
 constexpr int W8M = qt8::Cfg<true>::TM, W8N = qt8::Cfg<true>::TN;
 
 struct Fused8Args {
+  // TMA maps (sketch8_kernel<true>): Y left = A panel, Y right = Omega~,
+  // W left = Psi~ panel, W right = A panel (3D: inner, rows, planes)
+  CUtensorMap ylm, yrm, wlm, wrm;
   qt8::Operands yop;  // A_panel (k-fast) x Omega~ (8 planes, j-fast): M = panel rows, N = s, K = n
   qt8::Operands wop;  // Psi~_panel (8 planes, k-fast) x A_panel (j-fast): M = l, N = n, K = panel rows
   int64_t ky, kw;
@@ -183,8 +188,11 @@ __device__ __forceinline__ void store_tile8(const qt8::Acc<LPRE>& acc, int64_t i
 
 // Task order as sketch_fused_kernel: full W tiles, full Y tiles, padded Y
 // column tiles, padded W row tiles.
-__global__ void __launch_bounds__(qt8::NT, 1) sketch8_kernel(Fused8Args f) {
-  extern __shared__ __align__(16) double smem[];
+template <bool TMA>
+__global__ void __launch_bounds__(qt8::NT, 1) sketch8_kernel(const __grid_constant__ Fused8Args f) {
+  extern __shared__ __align__(128) double smem_raw[];
+  // TMA destinations need 128-byte alignment (the launch adds the slack)
+  double* smem = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~(uintptr_t)127);
   const int nwf = f.w_tmf * f.w_tn * f.zw;
   const int nyf = f.y_tm * f.y_tnf * f.zy;
   const int nyp = f.y_tm * (f.y_tn - f.y_tnf) * f.zy;
@@ -213,14 +221,22 @@ __global__ void __launch_bounds__(qt8::NT, 1) sketch8_kernel(Fused8Args f) {
     qt8::Acc<false> acc;
     qt8::zero_acc<false>(acc);
     const int64_t kb = (int64_t)z * f.ky_chunk, ke = min(f.ky, kb + f.ky_chunk);
-    qt8::mma_tile<false>(f.yop, smem, (int64_t)tm * Y8M, (int64_t)tn * Y8N, kb, ke, acc);
+    if (TMA)
+      qt8::mma_tile_tma<false>(qt8::TmaOps{&f.ylm, &f.yrm, 0}, f.yop, smem, (int64_t)tm * Y8M, (int64_t)tn * Y8N, kb,
+                               ke, acc);
+    else
+      qt8::mma_tile<false>(f.yop, smem, (int64_t)tm * Y8M, (int64_t)tn * Y8N, kb, ke, acc);
     double* part = f.zy > 1 ? f.yp + (int64_t)z * 4 * f.yop.M * f.yop.N : nullptr;
     store_tile8<false>(acc, (int64_t)tm * Y8M, (int64_t)tn * Y8N, f.yop.M, f.yop.N, f.y, f.ldy, part);
   } else {
     qt8::Acc<true> acc;
     qt8::zero_acc<true>(acc);
     const int64_t kb = (int64_t)z * f.kw_chunk, ke = min(f.kw, kb + f.kw_chunk);
-    qt8::mma_tile<true>(f.wop, smem, (int64_t)tm * W8M, (int64_t)tn * W8N, kb, ke, acc);
+    if (TMA)
+      qt8::mma_tile_tma<true>(qt8::TmaOps{&f.wlm, &f.wrm, 0}, f.wop, smem, (int64_t)tm * W8M, (int64_t)tn * W8N, kb,
+                              ke, acc);
+    else
+      qt8::mma_tile<true>(f.wop, smem, (int64_t)tm * W8M, (int64_t)tn * W8N, kb, ke, acc);
     double* part = f.zw > 1 ? f.wp + (int64_t)z * 4 * f.wop.M * f.wop.N : nullptr;
     store_tile8<true>(acc, (int64_t)tm * W8M, (int64_t)tn * W8N, f.wop.M, f.wop.N, f.w, f.ldw, part);
   }
@@ -228,7 +244,7 @@ __global__ void __launch_bounds__(qt8::NT, 1) sketch8_kernel(Fused8Args f) {
 
 // out plane i (rows x cols, ld = cols) = combination i of in's planes, the
 // left (Psi) or right (Omega) set, halves folded into i >= 4
-__global__ void combine8_kernel(QView in, double* out, int left) {
+__global__ void combine8_kernel(QView in, double* out, int64_t ld, int left) {
   const int64_t rows = in.rows, cols = in.cols, total = rows * cols;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = e / cols, j = e % cols;
@@ -238,7 +254,7 @@ __global__ void combine8_kernel(QView in, double* out, int left) {
 #pragma unroll
     for (int c = 0; c < 8; ++c) {
       const double x = left ? qt8::lcomb(c, v) : qt8::rcomb(c, v);
-      out[(int64_t)c * total + e] = c >= 4 ? 0.5 * x : x;
+      out[(int64_t)c * rows * ld + i * ld + j] = c >= 4 ? 0.5 * x : x;
     }
   }
 }
@@ -364,9 +380,53 @@ std::pair<int, int> choose_panel_splits(const Geom& G, int64_t rp, int64_t n, in
 // (8-product engine; planes of rows x cols each, ld = cols).
 struct Emb {
   QView om, ps;
-  const double* om8 = nullptr;  // 8 x (n x s)
-  const double* ps8 = nullptr;  // 8 x (l x b)
+  const double* om8 = nullptr;  // 8 planes of n x s, leading dimension om8_ld
+  const double* ps8 = nullptr;  // 8 planes of l x b, leading dimension ps8_ld
+  int64_t om8_ld = 0, ps8_ld = 0;  // even: 16-byte rows for TMA
 };
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda
+// link).  3D map over planes of row-major doubles: (inner, rows, planes).
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }();
+  return fn;
+}
+bool make_map3(CUtensorMap* m, const double* base, int64_t inner, int64_t rows, int64_t planes, int64_t ld,
+               int64_t pstride, int box_inner, int box_rows, int box_planes) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  const cuuint64_t dims[3] = {(cuuint64_t)inner, (cuuint64_t)rows, (cuuint64_t)planes};
+  const cuuint64_t strides[2] = {(cuuint64_t)ld * 8, (cuuint64_t)pstride * 8};
+  const cuuint32_t box[3] = {(cuuint32_t)box_inner, (cuuint32_t)box_rows, (cuuint32_t)box_planes};
+  const cuuint32_t es[3] = {1, 1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+// A's planes as one 3D tensor: 16-byte aligned rows and a uniform positive
+// plane stride (a (4, m, n) tensor with n even); else the cp.async path
+bool tma_layout(const QView& a, int64_t* pstride) {
+  const int64_t d = a.p[1] - a.p[0];
+  if (d <= 0 || d % 2 || a.ld % 2 || (reinterpret_cast<uintptr_t>(a.p[0]) & 15)) return false;
+  for (int q = 2; q < 4; ++q)
+    if (a.p[q] - a.p[0] != q * d) return false;
+  *pstride = d;
+  return true;
+}
+bool sketch_tma_enabled() {
+  static const bool v = [] {
+    const char* e = std::getenv("QLRA_SKETCH_TMA");
+    return !(e && std::atoi(e) == 0);
+  }();
+  return v;
+}
 
 // Event-timed launch bracket (bench evidence, ctx.ktimer).
 struct LaunchTimer {
@@ -437,13 +497,14 @@ void sketch_panel(Ctx& ctx, const Emb& e, int64_t pc0, const QView& ap, const QV
       f.y[p] = yv.p[p];
       f.w[p] = w.p[p];
     }
+    (void)pb;
     for (int i = 0; i < 8; ++i) {
-      f.yop.r[i] = e.om8 + (size_t)i * n * s;
-      f.wop.l[i] = e.ps8 + (size_t)i * l * pb + pc0;  // Psi~[:, pc0:pc0+rp]
+      f.yop.r[i] = e.om8 + (size_t)i * n * e.om8_ld;
+      f.wop.l[i] = e.ps8 + (size_t)i * l * e.ps8_ld + pc0;  // Psi~[:, pc0:pc0+rp]
     }
-    f.yop.l_si = ap.ld; f.yop.r_sk = s;
+    f.yop.l_si = ap.ld; f.yop.r_sk = e.om8_ld;
     f.yop.M = rp; f.yop.N = s;
-    f.wop.l_si = pb; f.wop.r_sk = ap.ld;
+    f.wop.l_si = e.ps8_ld; f.wop.r_sk = ap.ld;
     f.wop.M = l; f.wop.N = n;
     f.ky = n;
     f.kw = rp;
@@ -451,8 +512,20 @@ void sketch_panel(Ctx& ctx, const Emb& e, int64_t pc0, const QView& ap, const QV
     f.ldw = w.ld;
     set_splits(f, kGeom8, rp, n, s, l, ctx, ws);
     const int64_t ctas = (int64_t)f.y_tm * f.y_tn * f.zy + (int64_t)f.w_tm * f.w_tn * f.zw;
+    // TMA staging when A's planes form one 16-byte-aligned 3D tensor; the
+    // maps cover exactly this panel (rows past it, k past n and columns past
+    // s / n come back zero)
+    int64_t aps = 0;
+    const bool tma = sketch_tma_enabled() && tma_layout(ap, &aps) && (pc0 % 2) == 0 &&
+                     make_map3(&f.ylm, ap.p[0], n, rp, 4, ap.ld, aps, qt8::LDK, Y8M, 4) &&
+                     make_map3(&f.yrm, e.om8, s, n, 8, e.om8_ld, n * e.om8_ld, qt8::Layout<false>::LDX, qt8::BK, 8) &&
+                     make_map3(&f.wlm, e.ps8 + pc0, rp, l, 8, e.ps8_ld, l * e.ps8_ld, qt8::LDK, W8M, 8) &&
+                     make_map3(&f.wrm, ap.p[0], n, rp, 4, ap.ld, aps, qt8::Layout<true>::LDX, qt8::BK, 4);
     LaunchTimer lt(ctx);
-    sketch8_kernel<<<(unsigned)ctas, qt8::NT, qt8::SMEM_BYTES, ctx.stream>>>(f);
+    if (tma)
+      sketch8_kernel<true><<<(unsigned)ctas, qt8::NT, qt8::SMEM_BYTES + 128, ctx.stream>>>(f);
+    else
+      sketch8_kernel<false><<<(unsigned)ctas, qt8::NT, qt8::SMEM_BYTES + 128, ctx.stream>>>(f);
     QLRA_LAUNCH_CHECK();
     count_launch();
     lt.done(rp, n, s, l);
@@ -489,12 +562,12 @@ void sketch_panel(Ctx& ctx, const Emb& e, int64_t pc0, const QView& ap, const QV
 }
 
 // Plane combinations of an embedding for the 8-product engine.
-void launch_combine8(Ctx& ctx, const QView& in, double* out, bool left) {
+void launch_combine8(Ctx& ctx, const QView& in, double* out, int64_t ld, bool left) {
   const int64_t total = in.rows * in.cols;
   if (total == 0) return;
   const int threads = 256;
   const int64_t blocks = std::min<int64_t>((total + threads - 1) / threads, 148 * 16);
-  combine8_kernel<<<(unsigned)blocks, threads, 0, ctx.stream>>>(in, out, left ? 1 : 0);
+  combine8_kernel<<<(unsigned)blocks, threads, 0, ctx.stream>>>(in, out, ld, left ? 1 : 0);
   QLRA_LAUNCH_CHECK();
   count_launch();
 }
@@ -502,11 +575,13 @@ void launch_combine8(Ctx& ctx, const QView& in, double* out, bool left) {
 // Fill e.om8 / e.ps8 (when the 8-product engine is on) into `store`.
 void prepare_emb(Ctx& ctx, Emb& e, DeviceBuffer& store) {
   if (!sketch_use8()) return;
-  const size_t no = (size_t)8 * e.om.rows * e.om.cols, np = (size_t)8 * e.ps.rows * e.ps.cols;
+  e.om8_ld = (e.om.cols + 1) / 2 * 2;
+  e.ps8_ld = (e.ps.cols + 1) / 2 * 2;
+  const size_t no = (size_t)8 * e.om.rows * e.om8_ld, np = (size_t)8 * e.ps.rows * e.ps8_ld;
   store = DeviceBuffer(ctx, (no + np) * sizeof(double));
   double* base = store.as<double>();
-  launch_combine8(ctx, e.om, base, false);
-  launch_combine8(ctx, e.ps, base + no, true);
+  launch_combine8(ctx, e.om, base, e.om8_ld, false);
+  launch_combine8(ctx, e.ps, base + no, e.ps8_ld, true);
   e.om8 = base;
   e.ps8 = base + no;
 }
@@ -514,7 +589,10 @@ void prepare_emb(Ctx& ctx, Emb& e, DeviceBuffer& store) {
 void set_kernel_attrs() {
   set_func_attr((const void*)sketch_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                 (int)qt::SMEM_BYTES);
-  set_func_attr((const void*)sketch8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)qt8::SMEM_BYTES);
+  set_func_attr((const void*)sketch8_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                (int)qt8::SMEM_BYTES + 128);
+  set_func_attr((const void*)sketch8_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                (int)qt8::SMEM_BYTES + 128);
 }
 
 // Rows per fused launch.  Device-resident A: panels of up to kPanelBytes --
