@@ -44,19 +44,32 @@
 namespace qlra_dev {
 namespace qt8 {
 
-constexpr int NT = 512, BK = 8, STAGES = 4;
+constexpr int NT = 256, BK = 8, STAGES = 4;
 constexpr int LDK = BK + 4;  // k-fast rows, pitch 12 (4 mod 16: conflict-free fragments)
 
+// 8 warps of 16x16 output tiles (2x2 blocks of 8x8): 8 products x 4 blocks x 2
+// = 64 FP64 accumulators per thread, up to 255 registers at 256 threads (one
+// CTA per SM).  Against 16 warps of 16x8 tiles: half the plane sums and 3/4
+// of the fragment loads per DMMA, and room for the sums' registers (at the
+// 128-register cap of 512 threads the scheduler reused one register for
+// every sum, serialising each DADD behind the previous DMMA's operand read).
 template <bool LPRE>
 struct Cfg;
 template <>
-struct Cfg<false> {  // Y task: left operand A (on the fly), right Omega~ (combined)
-  static constexpr int TM = 64, TN = 32, WRB = 2, WCB = 1, LP = 4, RP = 8;
+struct Cfg<false> {  // Y task: left operand A (on the fly), right Omega~ (combined); 4 x 2 warps
+  static constexpr int TM = 64, TN = 32, WRB = 2, WCB = 2, LP = 4, RP = 8;
 };
 template <>
-struct Cfg<true> {  // W task: left Psi~ (combined), right operand A (on the fly)
-  static constexpr int TM = 32, TN = 64, WRB = 1, WCB = 2, LP = 8, RP = 4;
+struct Cfg<true> {  // W task: left Psi~ (combined), right operand A (on the fly); 2 x 4 warps
+  static constexpr int TM = 32, TN = 64, WRB = 2, WCB = 2, LP = 8, RP = 4;
 };
+// Warp w issues on SMSP w % 4.  The warp index runs fastest along the long
+// side of the warp grid, so the warps of a tile padded along the short side
+// (Y: s % 32, W: l % 32 valid columns / rows) still cover all four SMSPs.
+template <bool LPRE>
+__device__ __forceinline__ int warp_row(int w) { return LPRE ? w >> 2 : w & 3; }
+template <bool LPRE>
+__device__ __forceinline__ int warp_col(int w) { return LPRE ? w & 3 : w >> 2; }
 template <bool LPRE>
 struct Layout {
   using C = Cfg<LPRE>;
@@ -129,18 +142,15 @@ __device__ __forceinline__ void combine(const double (&m)[8], double (&c)[4]) {
   c[3] = m[3] + (m[4] - m[5]) - d78;
 }
 
-using qt::warp_col;
-using qt::warp_row;
-
 template <bool LPRE>
 __device__ __forceinline__ int acc_row(int rb) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  return 8 * Cfg<LPRE>::WRB * warp_row(w) + 8 * rb + (lane >> 2);
+  return 8 * Cfg<LPRE>::WRB * warp_row<LPRE>(w) + 8 * rb + (lane >> 2);
 }
 template <bool LPRE>
 __device__ __forceinline__ int acc_col(int cb) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  return 8 * Cfg<LPRE>::WCB * warp_col(w) + 8 * cb + 2 * (lane & 3);
+  return 8 * Cfg<LPRE>::WCB * warp_col<LPRE>(w) + 8 * cb + 2 * (lane & 3);
 }
 
 // Per-thread copy plan of one tile, fixed for the whole k loop: each thread
@@ -152,13 +162,16 @@ struct Loader {
   using C = Cfg<LPRE>;
   using Lay = Layout<LPRE>;
   static constexpr int LPER = C::TM * BK, RPER = BK * C::TN;  // elements per plane per stage
-  static constexpr int LSPLIT = NT / LPER, RSPLIT = NT / RPER;   // threads groups per copy round
-  static_assert(NT % LPER == 0 && NT % RPER == 0, "copy plan");
+  // NT >= PER: thread groups take different planes (SPLIT groups, one
+  // position each); NT < PER: every thread takes POS positions of each plane
+  static constexpr int LSPLIT = NT >= LPER ? NT / LPER : 1, RSPLIT = NT >= RPER ? NT / RPER : 1;
+  static constexpr int LPOS = NT >= LPER ? 1 : LPER / NT, RPOS = NT >= RPER ? 1 : RPER / NT;
+  static_assert((NT % LPER == 0 || LPER % NT == 0) && (NT % RPER == 0 || RPER % NT == 0), "copy plan");
   static_assert(C::LP % LSPLIT == 0 && C::RP % RSPLIT == 0, "copy plan");
   static constexpr int LCOPIES = C::LP / LSPLIT, RCOPIES = C::RP / RSPLIT;
-  int64_t loff, roff, rstep;
+  int64_t loff, roff, rstep, ldelta, rdelta;
   int lk, rk, lhi, rhi, ldst, rdst;
-  bool lrow, rcol;
+  unsigned lrow, rcol;  // validity bit per position
   __device__ __forceinline__ Loader(const Operands& g, int64_t i0, int64_t j0, int64_t kbeg, int tid) {
     const int lidx = tid % LPER, ridx = tid % RPER;
     lhi = tid / LPER;
@@ -166,26 +179,40 @@ struct Loader {
     const int lx = lidx / BK, rx = ridx % C::TN;
     lk = lidx % BK;
     rk = ridx / C::TN;
-    lrow = i0 + lx < g.M;
-    rcol = j0 + rx < g.N;
-    loff = (lrow ? (i0 + lx) * g.l_si : 0) + kbeg + lk;
-    roff = (kbeg + rk) * g.r_sk + (rcol ? j0 + rx : 0);
+    lrow = rcol = 0;
+#pragma unroll
+    for (int p = 0; p < LPOS; ++p) lrow |= (i0 + lx + p * (NT / BK) < g.M ? 1u : 0u) << p;
+#pragma unroll
+    for (int p = 0; p < RPOS; ++p) rcol |= (j0 + rx < g.N ? 1u : 0u) << p;
+    loff = (i0 + lx) * g.l_si + kbeg + lk;
+    ldelta = (int64_t)(NT / BK) * g.l_si;     // next position: NT / BK rows further
+    roff = (kbeg + rk) * g.r_sk + j0 + rx;
+    rdelta = (int64_t)(NT / C::TN) * g.r_sk;  // next position: NT / TN k-rows further
     rstep = (int64_t)BK * g.r_sk;
     ldst = (lhi * C::TM + lx) * LDK + lk;
     rdst = (rhi * BK + rk) * Lay::LDX + rx;
   }
   // copy stage starting at k0 (the offsets are then advanced to k0 + BK)
   __device__ __forceinline__ void stage(const Operands& g, double* Ls, double* Rs, int64_t k0, int64_t kend) {
-    const bool lok = lrow && k0 + lk < kend, rok = rcol && k0 + rk < kend;
 #pragma unroll
-    for (int r = 0; r < LCOPIES; ++r) {
-      const double* base = LSPLIT == 1 ? g.l[r] : (lhi ? g.l[LSPLIT * r + 1] : g.l[LSPLIT * r]);
-      qt::cp_async8(Ls + ldst + r * LSPLIT * C::TM * LDK, lok ? base + loff : base, lok);
+    for (int p = 0; p < LPOS; ++p) {
+      const bool ok = ((lrow >> p) & 1u) && k0 + lk < kend;
+#pragma unroll
+      for (int r = 0; r < LCOPIES; ++r) {
+        const double* base = LSPLIT == 1 ? g.l[r] : (lhi ? g.l[LSPLIT * r + 1] : g.l[LSPLIT * r]);
+        qt::cp_async8(Ls + ldst + (r * LSPLIT * C::TM + p * (NT / BK)) * LDK, ok ? base + loff + p * ldelta : base,
+                      ok);
+      }
     }
 #pragma unroll
-    for (int r = 0; r < RCOPIES; ++r) {
-      const double* base = RSPLIT == 1 ? g.r[r] : (rhi ? g.r[RSPLIT * r + 1] : g.r[RSPLIT * r]);
-      qt::cp_async8(Rs + rdst + r * RSPLIT * BK * Lay::LDX, rok ? base + roff : base, rok);
+    for (int p = 0; p < RPOS; ++p) {
+      const bool ok = ((rcol >> p) & 1u) && k0 + rk + p * (NT / C::TN) < kend;
+#pragma unroll
+      for (int r = 0; r < RCOPIES; ++r) {
+        const double* base = RSPLIT == 1 ? g.r[r] : (rhi ? g.r[RSPLIT * r + 1] : g.r[RSPLIT * r]);
+        qt::cp_async8(Rs + rdst + (r * RSPLIT * BK + p * (NT / C::TN)) * Lay::LDX,
+                      ok ? base + roff + p * rdelta : base, ok);
+      }
     }
     loff += BK;
     roff += rstep;
@@ -252,7 +279,7 @@ template <bool LPRE, int NRB, int NCB>
 __device__ __forceinline__ void mma_loop(const Operands& g, double* smem, int64_t i0, int64_t j0, int64_t kbeg,
                                          int64_t kend, Acc<LPRE>& acc, uint64_t* full, uint64_t* empty) {
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  const int wr = warp_row(w), wc = warp_col(w);
+  const int wr = warp_row<LPRE>(w), wc = warp_col<LPRE>(w);
   const int gid = lane >> 2, tig = lane & 3;
   const int nk = kend > kbeg ? (int)((kend - kbeg + BK - 1) / BK) : 0;
   constexpr int LOFF = Layout<LPRE>::L_ELEMS;
@@ -331,7 +358,7 @@ template <bool LPRE, int NRB, int NCB>
 __device__ __forceinline__ void mma_loop_tma(const TmaOps& t, double* smem, int64_t i0, int64_t j0, int64_t kbeg,
                                              int64_t kend, Acc<LPRE>& acc, uint64_t* full, uint64_t* empty) {
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  const int wr = warp_row(w), wc = warp_col(w);
+  const int wr = warp_row<LPRE>(w), wc = warp_col<LPRE>(w);
   const int gid = lane >> 2, tig = lane & 3;
   const int nk = kend > kbeg ? (int)((kend - kbeg + BK - 1) / BK) : 0;
   constexpr int LOFF = Layout<LPRE>::L_ELEMS;
@@ -377,21 +404,15 @@ __device__ __forceinline__ void mma_tile_tma(const TmaOps& t, const Operands& g,
   using C = Cfg<LPRE>;
   __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES];
   const int w = threadIdx.x >> 5;
-  const int64_t r0w = i0 + 8 * C::WRB * warp_row(w), c0w = j0 + 8 * C::WCB * warp_col(w);
+  const int64_t r0w = i0 + 8 * C::WRB * warp_row<LPRE>(w), c0w = j0 + 8 * C::WCB * warp_col<LPRE>(w);
   const int nrb = r0w >= g.M ? 0 : (int)min((int64_t)C::WRB, (g.M - r0w + 7) / 8);
   const int ncb = c0w >= g.N ? 0 : (int)min((int64_t)C::WCB, (g.N - c0w + 7) / 8);
-  if (!LPRE) {
-    switch (nrb * 4 + ncb) {
-      case 2 * 4 + 1: mma_loop_tma<LPRE, 2, 1>(t, smem, i0, j0, kbeg, kend, acc, full, empty); break;
-      case 1 * 4 + 1: mma_loop_tma<LPRE, 1, 1>(t, smem, i0, j0, kbeg, kend, acc, full, empty); break;
-      default: mma_loop_tma<LPRE, 0, 0>(t, smem, i0, j0, kbeg, kend, acc, full, empty); break;
-    }
-  } else {
-    switch (nrb * 4 + ncb) {
-      case 1 * 4 + 2: mma_loop_tma<LPRE, 1, 2>(t, smem, i0, j0, kbeg, kend, acc, full, empty); break;
-      case 1 * 4 + 1: mma_loop_tma<LPRE, 1, 1>(t, smem, i0, j0, kbeg, kend, acc, full, empty); break;
-      default: mma_loop_tma<LPRE, 0, 0>(t, smem, i0, j0, kbeg, kend, acc, full, empty); break;
-    }
+  switch (nrb * 4 + ncb) {
+    case 2 * 4 + 2: mma_loop_tma<LPRE, 2, 2>(t, smem, i0, j0, kbeg, kend, acc, full, empty); break;
+    case 2 * 4 + 1: mma_loop_tma<LPRE, 2, 1>(t, smem, i0, j0, kbeg, kend, acc, full, empty); break;
+    case 1 * 4 + 2: mma_loop_tma<LPRE, 1, 2>(t, smem, i0, j0, kbeg, kend, acc, full, empty); break;
+    case 1 * 4 + 1: mma_loop_tma<LPRE, 1, 1>(t, smem, i0, j0, kbeg, kend, acc, full, empty); break;
+    default: mma_loop_tma<LPRE, 0, 0>(t, smem, i0, j0, kbeg, kend, acc, full, empty); break;
   }
 }
 
@@ -403,21 +424,15 @@ __device__ __forceinline__ void mma_tile(const Operands& g, double* smem, int64_
   using C = Cfg<LPRE>;
   __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES];
   const int w = threadIdx.x >> 5;
-  const int64_t r0w = i0 + 8 * C::WRB * warp_row(w), c0w = j0 + 8 * C::WCB * warp_col(w);
+  const int64_t r0w = i0 + 8 * C::WRB * warp_row<LPRE>(w), c0w = j0 + 8 * C::WCB * warp_col<LPRE>(w);
   const int nrb = r0w >= g.M ? 0 : (int)min((int64_t)C::WRB, (g.M - r0w + 7) / 8);
   const int ncb = c0w >= g.N ? 0 : (int)min((int64_t)C::WCB, (g.N - c0w + 7) / 8);
-  if (!LPRE) {  // WRB = 2, WCB = 1
-    switch (nrb * 4 + ncb) {
-      case 2 * 4 + 1: mma_loop<LPRE, 2, 1>(g, smem, i0, j0, kbeg, kend, acc, full, empty); break;
-      case 1 * 4 + 1: mma_loop<LPRE, 1, 1>(g, smem, i0, j0, kbeg, kend, acc, full, empty); break;
-      default: mma_loop<LPRE, 0, 0>(g, smem, i0, j0, kbeg, kend, acc, full, empty); break;
-    }
-  } else {  // WRB = 1, WCB = 2
-    switch (nrb * 4 + ncb) {
-      case 1 * 4 + 2: mma_loop<LPRE, 1, 2>(g, smem, i0, j0, kbeg, kend, acc, full, empty); break;
-      case 1 * 4 + 1: mma_loop<LPRE, 1, 1>(g, smem, i0, j0, kbeg, kend, acc, full, empty); break;
-      default: mma_loop<LPRE, 0, 0>(g, smem, i0, j0, kbeg, kend, acc, full, empty); break;
-    }
+  switch (nrb * 4 + ncb) {
+    case 2 * 4 + 2: mma_loop<LPRE, 2, 2>(g, smem, i0, j0, kbeg, kend, acc, full, empty); break;
+    case 2 * 4 + 1: mma_loop<LPRE, 2, 1>(g, smem, i0, j0, kbeg, kend, acc, full, empty); break;
+    case 1 * 4 + 2: mma_loop<LPRE, 1, 2>(g, smem, i0, j0, kbeg, kend, acc, full, empty); break;
+    case 1 * 4 + 1: mma_loop<LPRE, 1, 1>(g, smem, i0, j0, kbeg, kend, acc, full, empty); break;
+    default: mma_loop<LPRE, 0, 0>(g, smem, i0, j0, kbeg, kend, acc, full, empty); break;
   }
 }
 

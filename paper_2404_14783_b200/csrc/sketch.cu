@@ -192,7 +192,8 @@ template <bool TMA>
 __global__ void __launch_bounds__(qt8::NT, 1) sketch8_kernel(const __grid_constant__ Fused8Args f) {
   extern __shared__ __align__(128) double smem_raw[];
   // TMA destinations need 128-byte alignment (the launch adds the slack)
-  double* smem = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~(uintptr_t)127);
+  // (offset arithmetic on the shared array keeps the accesses LDS, not generic)
+  double* smem = smem_raw + ((128u - (qt::smem_u32(smem_raw) & 127u)) & 127u) / sizeof(double);
   const int nwf = f.w_tmf * f.w_tn * f.zw;
   const int nyf = f.y_tm * f.y_tnf * f.zy;
   const int nyp = f.y_tm * (f.y_tn - f.y_tnf) * f.zy;
@@ -688,7 +689,7 @@ void psi_keep_release(Ctx& ctx) {
 
 void sketch_update_rows(Ctx& ctx, const qlra_spec_t& omega, const qlra_spec_t& psi, int64_t row0,
                         const QView& block, const QView& y_rows, const QView& w) {
-  const int64_t b = block.rows, n = block.cols, s = omega.cols, l = psi.rows;
+  const int64_t b = block.rows, n = block.cols, s = omega.cols;
   if (b == 0 || n == 0) return;
   set_kernel_attrs();
   DevQMat om(ctx, n, s), ps_tmp;
@@ -713,7 +714,7 @@ void sketch_update_rows(Ctx& ctx, const qlra_spec_t& omega, const qlra_spec_t& p
 void sketch_update_rows_host(Ctx& ctx, const qlra_spec_t& omega, const qlra_spec_t& psi,
                              int64_t row0, const QView& host_block, const QView& y_rows,
                              const QView& w, int64_t block_rows) {
-  const int64_t b = host_block.rows, n = host_block.cols, s = omega.cols, l = psi.rows;
+  const int64_t b = host_block.rows, n = host_block.cols, s = omega.cols;
   if (b == 0 || n == 0) return;
   set_kernel_attrs();
   int64_t R = block_rows > 0 ? block_rows : stream_rows(n, b);
