@@ -25,16 +25,23 @@
 // exact, a power of two), the A side in registers from the 4 staged planes
 // (A is read once and never rewritten):
 //
-//   YT (Y task): C 64x32 = A (k-fast, 4 planes) x Omega~ (j-fast, 8 planes),
-//                warp tile 16x8 (2x1 blocks of 8x8);
-//   WT (W task): C 32x64 = Psi~ (k-fast, 8 planes) x A (j-fast, 4 planes),
-//                warp tile 8x16 (1x2 blocks).
+//   Y task: C 64x32 = A (k-fast, 4 planes) x Omega~ (j-fast, 8 planes);
+//   W task: C 32x64 = Psi~ (k-fast, 8 planes) x A (j-fast, 4 planes).
 //
-// 512 threads as 4x4 warps, 8 products x 2 blocks x 2 = 32 FP64 accumulators
-// per thread, as in qtile.cuh.  Rounding: every product and sum is an IEEE
-// operation in a fixed order (deterministic); the combination sums add at
-// most a few ulp of |a||b| per term, the same order as the 16-product sum
-// (the sketch is compared with the oracle at 1e-13 relative).
+// Paired warps.  512 threads = 8 warp-tile positions (16x16 outputs, 2x2
+// blocks of 8x8) x 2 product halves: warp w covers position w & 7 and
+// products 4*(w >> 3) .. +3, so each warp holds 4 products x 4 blocks x 2 =
+// 32 FP64 accumulators (the 128-register cap of 512 threads) and forms only
+// its own 4 combinations.  Measured alternatives: 16 warps of 16x8 tiles
+// with all 8 products (one sum per DMMA, register-starved schedule) and 8
+// warps of 16x16 tiles with all 8 products (2 warps per SM sub-partition
+// cannot cover the DADD -> DMMA and LDS -> DMMA latencies) reached 61% / 70%
+// of the DMMA pipe.  The halves meet in the epilogue through shared memory.
+//
+// Rounding: every product and sum is an IEEE operation in a fixed order
+// (deterministic); the combination sums add at most a few ulp of |a||b| per
+// term, the same order as the 16-product sum (the sketch is compared with the
+// oracle at 1e-13 relative).
 #pragma once
 
 #include <cuda.h>
@@ -44,32 +51,29 @@
 namespace qlra_dev {
 namespace qt8 {
 
-constexpr int NT = 256, BK = 8, STAGES = 4;
+constexpr int NT = 512, BK = 8, STAGES = 4;
 constexpr int LDK = BK + 4;  // k-fast rows, pitch 12 (4 mod 16: conflict-free fragments)
 
-// 8 warps of 16x16 output tiles (2x2 blocks of 8x8): 8 products x 4 blocks x 2
-// = 64 FP64 accumulators per thread, up to 255 registers at 256 threads (one
-// CTA per SM).  Against 16 warps of 16x8 tiles: half the plane sums and 3/4
-// of the fragment loads per DMMA, and room for the sums' registers (at the
-// 128-register cap of 512 threads the scheduler reused one register for
-// every sum, serialising each DADD behind the previous DMMA's operand read).
 template <bool LPRE>
 struct Cfg;
 template <>
-struct Cfg<false> {  // Y task: left operand A (on the fly), right Omega~ (combined); 4 x 2 warps
+struct Cfg<false> {  // Y task: left operand A (on the fly), right Omega~ (combined); 4 x 2 positions
   static constexpr int TM = 64, TN = 32, WRB = 2, WCB = 2, LP = 4, RP = 8;
 };
 template <>
-struct Cfg<true> {  // W task: left Psi~ (combined), right operand A (on the fly); 2 x 4 warps
+struct Cfg<true> {  // W task: left Psi~ (combined), right operand A (on the fly); 2 x 4 positions
   static constexpr int TM = 32, TN = 64, WRB = 2, WCB = 2, LP = 8, RP = 4;
 };
-// Warp w issues on SMSP w % 4.  The warp index runs fastest along the long
-// side of the warp grid, so the warps of a tile padded along the short side
-// (Y: s % 32, W: l % 32 valid columns / rows) still cover all four SMSPs.
+// Warp w issues on SMSP w % 4.  The position index runs fastest along the
+// long side of the position grid, so the warps of a tile padded along the
+// short side (Y: s % 32, W: l % 32 valid columns / rows) still cover all
+// four SMSPs (two warps each: both product halves).
 template <bool LPRE>
-__device__ __forceinline__ int warp_row(int w) { return LPRE ? w >> 2 : w & 3; }
+__device__ __forceinline__ int warp_row(int w) { return LPRE ? (w & 7) >> 2 : w & 3; }
 template <bool LPRE>
-__device__ __forceinline__ int warp_col(int w) { return LPRE ? w & 3 : w >> 2; }
+__device__ __forceinline__ int warp_col(int w) { return LPRE ? w & 3 : (w & 7) >> 2; }
+__device__ __forceinline__ int warp_half(int w) { return w >> 3; }
+
 template <bool LPRE>
 struct Layout {
   using C = Cfg<LPRE>;
@@ -117,23 +121,20 @@ __device__ __forceinline__ double rcomb(int i, const double (&b)[4]) {
   }
 }
 
-// Accumulators: acc[i][rb][cb][h] = product m_{i+1} at row
-// 8*WRB*warp_row + 8*rb + lane/4, col 8*WCB*warp_col + 8*cb + 2*(lane%4) + h.
-template <bool LPRE>
-using Acc = double[8][Cfg<LPRE>::WRB][Cfg<LPRE>::WCB][2];
+// Accumulators of one warp: acc[ii][rb][cb][h] = product m_{4*half + ii + 1}
+// at row 16*warp_row + 8*rb + lane/4, col 16*warp_col + 8*cb + 2*(lane%4) + h.
+using Acc = double[4][2][2][2];
 
-template <bool LPRE>
-__device__ __forceinline__ void zero_acc(Acc<LPRE>& acc) {
-  using C = Cfg<LPRE>;
+__device__ __forceinline__ void zero_acc(Acc& acc) {
 #pragma unroll
-  for (int i = 0; i < 8; ++i)
+  for (int i = 0; i < 4; ++i)
 #pragma unroll
-    for (int rb = 0; rb < C::WRB; ++rb)
+    for (int rb = 0; rb < 2; ++rb)
 #pragma unroll
-      for (int cb = 0; cb < C::WCB; ++cb) acc[i][rb][cb][0] = acc[i][rb][cb][1] = 0.0;
+      for (int cb = 0; cb < 2; ++cb) acc[i][rb][cb][0] = acc[i][rb][cb][1] = 0.0;
 }
 
-// the quaternion planes of one accumulator element (fixed summation order)
+// the quaternion planes from the 8 products (fixed summation order)
 __device__ __forceinline__ void combine(const double (&m)[8], double (&c)[4]) {
   const double s56 = m[4] + m[5], d78 = m[6] - m[7];
   c[0] = m[1] - s56 + (m[6] + m[7]);
@@ -145,12 +146,12 @@ __device__ __forceinline__ void combine(const double (&m)[8], double (&c)[4]) {
 template <bool LPRE>
 __device__ __forceinline__ int acc_row(int rb) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  return 8 * Cfg<LPRE>::WRB * warp_row<LPRE>(w) + 8 * rb + (lane >> 2);
+  return 16 * warp_row<LPRE>(w) + 8 * rb + (lane >> 2);
 }
 template <bool LPRE>
 __device__ __forceinline__ int acc_col(int cb) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  return 8 * Cfg<LPRE>::WCB * warp_col<LPRE>(w) + 8 * cb + 2 * (lane & 3);
+  return 16 * warp_col<LPRE>(w) + 8 * cb + 2 * (lane & 3);
 }
 
 // Per-thread copy plan of one tile, fixed for the whole k loop: each thread
@@ -162,16 +163,13 @@ struct Loader {
   using C = Cfg<LPRE>;
   using Lay = Layout<LPRE>;
   static constexpr int LPER = C::TM * BK, RPER = BK * C::TN;  // elements per plane per stage
-  // NT >= PER: thread groups take different planes (SPLIT groups, one
-  // position each); NT < PER: every thread takes POS positions of each plane
-  static constexpr int LSPLIT = NT >= LPER ? NT / LPER : 1, RSPLIT = NT >= RPER ? NT / RPER : 1;
-  static constexpr int LPOS = NT >= LPER ? 1 : LPER / NT, RPOS = NT >= RPER ? 1 : RPER / NT;
-  static_assert((NT % LPER == 0 || LPER % NT == 0) && (NT % RPER == 0 || RPER % NT == 0), "copy plan");
+  static constexpr int LSPLIT = NT / LPER, RSPLIT = NT / RPER;   // thread groups per copy round
+  static_assert(NT % LPER == 0 && NT % RPER == 0, "copy plan");
   static_assert(C::LP % LSPLIT == 0 && C::RP % RSPLIT == 0, "copy plan");
   static constexpr int LCOPIES = C::LP / LSPLIT, RCOPIES = C::RP / RSPLIT;
-  int64_t loff, roff, rstep, ldelta, rdelta;
+  int64_t loff, roff, rstep;
   int lk, rk, lhi, rhi, ldst, rdst;
-  unsigned lrow, rcol;  // validity bit per position
+  bool lrow, rcol;
   __device__ __forceinline__ Loader(const Operands& g, int64_t i0, int64_t j0, int64_t kbeg, int tid) {
     const int lidx = tid % LPER, ridx = tid % RPER;
     lhi = tid / LPER;
@@ -179,105 +177,91 @@ struct Loader {
     const int lx = lidx / BK, rx = ridx % C::TN;
     lk = lidx % BK;
     rk = ridx / C::TN;
-    lrow = rcol = 0;
-#pragma unroll
-    for (int p = 0; p < LPOS; ++p) lrow |= (i0 + lx + p * (NT / BK) < g.M ? 1u : 0u) << p;
-#pragma unroll
-    for (int p = 0; p < RPOS; ++p) rcol |= (j0 + rx < g.N ? 1u : 0u) << p;
-    loff = (i0 + lx) * g.l_si + kbeg + lk;
-    ldelta = (int64_t)(NT / BK) * g.l_si;     // next position: NT / BK rows further
-    roff = (kbeg + rk) * g.r_sk + j0 + rx;
-    rdelta = (int64_t)(NT / C::TN) * g.r_sk;  // next position: NT / TN k-rows further
+    lrow = i0 + lx < g.M;
+    rcol = j0 + rx < g.N;
+    loff = (lrow ? (i0 + lx) * g.l_si : 0) + kbeg + lk;
+    roff = (kbeg + rk) * g.r_sk + (rcol ? j0 + rx : 0);
     rstep = (int64_t)BK * g.r_sk;
     ldst = (lhi * C::TM + lx) * LDK + lk;
     rdst = (rhi * BK + rk) * Lay::LDX + rx;
   }
   // copy stage starting at k0 (the offsets are then advanced to k0 + BK)
   __device__ __forceinline__ void stage(const Operands& g, double* Ls, double* Rs, int64_t k0, int64_t kend) {
+    const bool lok = lrow && k0 + lk < kend, rok = rcol && k0 + rk < kend;
 #pragma unroll
-    for (int p = 0; p < LPOS; ++p) {
-      const bool ok = ((lrow >> p) & 1u) && k0 + lk < kend;
-#pragma unroll
-      for (int r = 0; r < LCOPIES; ++r) {
-        const double* base = LSPLIT == 1 ? g.l[r] : (lhi ? g.l[LSPLIT * r + 1] : g.l[LSPLIT * r]);
-        qt::cp_async8(Ls + ldst + (r * LSPLIT * C::TM + p * (NT / BK)) * LDK, ok ? base + loff + p * ldelta : base,
-                      ok);
-      }
+    for (int r = 0; r < LCOPIES; ++r) {
+      const double* base = LSPLIT == 1 ? g.l[r] : (lhi ? g.l[LSPLIT * r + 1] : g.l[LSPLIT * r]);
+      qt::cp_async8(Ls + ldst + r * LSPLIT * C::TM * LDK, lok ? base + loff : base, lok);
     }
 #pragma unroll
-    for (int p = 0; p < RPOS; ++p) {
-      const bool ok = ((rcol >> p) & 1u) && k0 + rk + p * (NT / C::TN) < kend;
-#pragma unroll
-      for (int r = 0; r < RCOPIES; ++r) {
-        const double* base = RSPLIT == 1 ? g.r[r] : (rhi ? g.r[RSPLIT * r + 1] : g.r[RSPLIT * r]);
-        qt::cp_async8(Rs + rdst + (r * RSPLIT * BK + p * (NT / C::TN)) * Lay::LDX,
-                      ok ? base + roff + p * rdelta : base, ok);
-      }
+    for (int r = 0; r < RCOPIES; ++r) {
+      const double* base = RSPLIT == 1 ? g.r[r] : (rhi ? g.r[RSPLIT * r + 1] : g.r[RSPLIT * r]);
+      qt::cp_async8(Rs + rdst + r * RSPLIT * BK * Lay::LDX, rok ? base + roff : base, rok);
     }
     loff += BK;
     roff += rstep;
   }
 };
 
-// One BK slice for the first NRB row blocks and NCB column blocks of the warp.
-template <bool LPRE, int NRB, int NCB>
-__device__ __forceinline__ void kstep(const double* Ls, const double* Rs, int wr, int wc, int gid, int tig,
-                                      Acc<LPRE>& acc) {
+// One BK slice: products 4*HALF .. 4*HALF+3 for the warp's first NRB row and
+// NCB column blocks.  Per k4 step all fragments are loaded and the warp's 4
+// combinations formed before its 4*NRB*NCB DMMAs.
+template <bool LPRE, int HALF, int NRB, int NCB>
+__device__ __forceinline__ void kstep(const double* Ls, const double* Rs, int wr, int wc, int gid, int tig, Acc& acc) {
   using C = Cfg<LPRE>;
   constexpr int LDX = Layout<LPRE>::LDX;
 #pragma unroll
   for (int kk = 0; kk < BK / 4; ++kk) {
     const int k = 4 * kk + tig;
+    double lv[4][NRB], rv[4][NCB];
     if (!LPRE) {
       // left = A: 4 planes per row block, combined in registers
       double a[NRB][4];
 #pragma unroll
       for (int rb = 0; rb < NRB; ++rb) {
-        const int x = 8 * C::WRB * wr + 8 * rb + gid;
+        const int x = 16 * wr + 8 * rb + gid;
 #pragma unroll
         for (int q = 0; q < 4; ++q) a[rb][q] = Ls[(q * C::TM + x) * LDK + k];
       }
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        double bv[NCB];
+      for (int ii = 0; ii < 4; ++ii)
 #pragma unroll
-        for (int cb = 0; cb < NCB; ++cb) bv[cb] = Rs[(i * BK + k) * LDX + 8 * C::WCB * wc + 8 * cb + gid];
+        for (int cb = 0; cb < NCB; ++cb) rv[ii][cb] = Rs[((4 * HALF + ii) * BK + k) * LDX + 16 * wc + 8 * cb + gid];
 #pragma unroll
-        for (int rb = 0; rb < NRB; ++rb) {
-          const double av = lcomb(i, a[rb]);
+      for (int ii = 0; ii < 4; ++ii)
 #pragma unroll
-          for (int cb = 0; cb < NCB; ++cb) qt::dmma(acc[i][rb][cb], av, bv[cb]);
-        }
-      }
+        for (int rb = 0; rb < NRB; ++rb) lv[ii][rb] = lcomb(4 * HALF + ii, a[rb]);
     } else {
       // right = A: 4 planes per column block, combined in registers
       double b[NCB][4];
 #pragma unroll
       for (int cb = 0; cb < NCB; ++cb) {
-        const int x = 8 * C::WCB * wc + 8 * cb + gid;
+        const int x = 16 * wc + 8 * cb + gid;
 #pragma unroll
         for (int q = 0; q < 4; ++q) b[cb][q] = Rs[(q * BK + k) * LDX + x];
       }
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        double av[NRB];
+      for (int ii = 0; ii < 4; ++ii)
 #pragma unroll
-        for (int rb = 0; rb < NRB; ++rb) av[rb] = Ls[(i * C::TM + 8 * C::WRB * wr + 8 * rb + gid) * LDK + k];
+        for (int rb = 0; rb < NRB; ++rb) lv[ii][rb] = Ls[((4 * HALF + ii) * C::TM + 16 * wr + 8 * rb + gid) * LDK + k];
 #pragma unroll
-        for (int cb = 0; cb < NCB; ++cb) {
-          const double bv = rcomb(i, b[cb]);
+      for (int ii = 0; ii < 4; ++ii)
 #pragma unroll
-          for (int rb = 0; rb < NRB; ++rb) qt::dmma(acc[i][rb][cb], av[rb], bv);
-        }
-      }
+        for (int cb = 0; cb < NCB; ++cb) rv[ii][cb] = rcomb(4 * HALF + ii, b[cb]);
     }
+#pragma unroll
+    for (int ii = 0; ii < 4; ++ii)
+#pragma unroll
+      for (int rb = 0; rb < NRB; ++rb)
+#pragma unroll
+        for (int cb = 0; cb < NCB; ++cb) qt::dmma(acc[ii][rb][cb], lv[ii][rb], rv[ii][cb]);
   }
 }
 
 // The cp.async ring with mbarrier stage handoff (as qtile.cuh's mma_loop).
-template <bool LPRE, int NRB, int NCB>
+template <bool LPRE, int HALF, int NRB, int NCB>
 __device__ __forceinline__ void mma_loop(const Operands& g, double* smem, int64_t i0, int64_t j0, int64_t kbeg,
-                                         int64_t kend, Acc<LPRE>& acc, uint64_t* full, uint64_t* empty) {
+                                         int64_t kend, Acc& acc, uint64_t* full, uint64_t* empty) {
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int wr = warp_row<LPRE>(w), wc = warp_col<LPRE>(w);
   const int gid = lane >> 2, tig = lane & 3;
@@ -308,7 +292,7 @@ __device__ __forceinline__ void mma_loop(const Operands& g, double* smem, int64_
     qt::mbar_wait_parity(&full[s], (unsigned)((kt / STAGES) & 1));
     const double* Ls = smem + s * STAGE;
     if (NRB > 0 && NCB > 0)
-      kstep<LPRE, (NRB > 0 ? NRB : 1), (NCB > 0 ? NCB : 1)>(Ls, Ls + LOFF, wr, wc, gid, tig, acc);
+      kstep<LPRE, HALF, (NRB > 0 ? NRB : 1), (NCB > 0 ? NCB : 1)>(Ls, Ls + LOFF, wr, wc, gid, tig, acc);
     __syncwarp();
     if (lane == 0) qt::mbar_arrive(&empty[s]);
   }
@@ -326,10 +310,12 @@ __device__ __forceinline__ void mma_loop(const Operands& g, double* smem, int64_
 // over-fetched columns are never read.  The caller creates the maps so that
 // k past the chunk end is out of bounds in at least one operand, or chunks
 // end on BK boundaries (split-K).
+constexpr int MAX_STAGES = 6;
 struct TmaOps {
   const CUtensorMap* lm;  // left map
   const CUtensorMap* rm;  // right map
   int lk_off;             // inner coordinate offset of the left map's k (Psi~ panel column)
+  int stages, pf;         // ring slots (<= MAX_STAGES, smem sized by the launch) and prefetch distance (< stages)
 };
 
 __device__ __forceinline__ void tma_load3(double* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
@@ -345,7 +331,6 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
 template <bool LPRE>
 __device__ __forceinline__ void tma_stage(const TmaOps& t, double* Ls, double* Rs, int64_t i0, int64_t j0, int64_t k0,
                                           uint64_t* bar) {
-  using C = Cfg<LPRE>;
   constexpr unsigned BYTES = (unsigned)((Layout<LPRE>::L_ELEMS + Layout<LPRE>::R_ELEMS) * sizeof(double));
   mbar_expect_tx(bar, BYTES);
   tma_load3(Ls, t.lm, (int)(t.lk_off + k0), (int)i0, bar);
@@ -354,18 +339,17 @@ __device__ __forceinline__ void tma_stage(const TmaOps& t, double* Ls, double* R
 
 // The ring with a single producer thread (thread 0) issuing each stage PF
 // stages ahead; a refill waits for every warp's release of that slot.
-template <bool LPRE, int NRB, int NCB>
+template <bool LPRE, int HALF, int NRB, int NCB>
 __device__ __forceinline__ void mma_loop_tma(const TmaOps& t, double* smem, int64_t i0, int64_t j0, int64_t kbeg,
-                                             int64_t kend, Acc<LPRE>& acc, uint64_t* full, uint64_t* empty) {
+                                             int64_t kend, Acc& acc, uint64_t* full, uint64_t* empty) {
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int wr = warp_row<LPRE>(w), wc = warp_col<LPRE>(w);
   const int gid = lane >> 2, tig = lane & 3;
   const int nk = kend > kbeg ? (int)((kend - kbeg + BK - 1) / BK) : 0;
   constexpr int LOFF = Layout<LPRE>::L_ELEMS;
-  constexpr int PF = 2;
+  const int S = t.stages, PF = t.pf;
   if (tid == 0) {
-#pragma unroll
-    for (int s = 0; s < STAGES; ++s) {
+    for (int s = 0; s < S; ++s) {
       qt::mbar_init(&full[s], 1);
       qt::mbar_init(&empty[s], NT / 32);
     }
@@ -376,64 +360,93 @@ __device__ __forceinline__ void mma_loop_tma(const TmaOps& t, double* smem, int6
     for (int p = 0; p < PF && p < nk; ++p)
       tma_stage<LPRE>(t, smem + p * STAGE, smem + p * STAGE + LOFF, i0, j0, kbeg + (int64_t)p * BK, &full[p]);
   }
+  // slot s and its phase parity advance with kt (no division per stage)
+  int s = 0, ph = 0, sn = PF % S, phn = PF / S;
   for (int kt = 0; kt < nk; ++kt) {
-    const int s = kt % STAGES;
     if (tid == 0) {
       const int nxt = kt + PF;
       if (nxt < nk) {
-        const int sn = nxt % STAGES;
-        if (nxt >= STAGES) qt::mbar_wait_parity(&empty[sn], (unsigned)((nxt / STAGES - 1) & 1));
+        if (nxt >= S) qt::mbar_wait_parity(&empty[sn], (unsigned)((phn - 1) & 1));
         tma_stage<LPRE>(t, smem + sn * STAGE, smem + sn * STAGE + LOFF, i0, j0, kbeg + (int64_t)nxt * BK, &full[sn]);
       }
+      if (++sn == S) { sn = 0; ++phn; }
     }
     __syncwarp();  // warp 0 reconverges before its DMMAs (mma.sync is .aligned)
-    qt::mbar_wait_parity(&full[s], (unsigned)((kt / STAGES) & 1));
+    qt::mbar_wait_parity(&full[s], (unsigned)(ph & 1));
     const double* Ls = smem + s * STAGE;
     if (NRB > 0 && NCB > 0)
-      kstep<LPRE, (NRB > 0 ? NRB : 1), (NCB > 0 ? NCB : 1)>(Ls, Ls + LOFF, wr, wc, gid, tig, acc);
+      kstep<LPRE, HALF, (NRB > 0 ? NRB : 1), (NCB > 0 ? NCB : 1)>(Ls, Ls + LOFF, wr, wc, gid, tig, acc);
     __syncwarp();
     if (lane == 0) qt::mbar_arrive(&empty[s]);
+    if (++s == S) { s = 0; ++ph; }
   }
   // every issued stage was consumed (waited on full) before the loop ended
   __syncthreads();
 }
 
+// The warp's loop instance: product half, and the count of its 8x8 row /
+// column blocks inside M x N (blocks past the edge issue no DMMA).
 template <bool LPRE>
-__device__ __forceinline__ void mma_tile_tma(const TmaOps& t, const Operands& g, double* smem, int64_t i0, int64_t j0,
-                                             int64_t kbeg, int64_t kend, Acc<LPRE>& acc) {
-  using C = Cfg<LPRE>;
-  __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES];
+__device__ __forceinline__ int instance(const Operands& g, int64_t i0, int64_t j0) {
   const int w = threadIdx.x >> 5;
-  const int64_t r0w = i0 + 8 * C::WRB * warp_row<LPRE>(w), c0w = j0 + 8 * C::WCB * warp_col<LPRE>(w);
-  const int nrb = r0w >= g.M ? 0 : (int)min((int64_t)C::WRB, (g.M - r0w + 7) / 8);
-  const int ncb = c0w >= g.N ? 0 : (int)min((int64_t)C::WCB, (g.N - c0w + 7) / 8);
-  switch (nrb * 4 + ncb) {
-    case 2 * 4 + 2: mma_loop_tma<LPRE, 2, 2>(t, smem, i0, j0, kbeg, kend, acc, full, empty); break;
-    case 2 * 4 + 1: mma_loop_tma<LPRE, 2, 1>(t, smem, i0, j0, kbeg, kend, acc, full, empty); break;
-    case 1 * 4 + 2: mma_loop_tma<LPRE, 1, 2>(t, smem, i0, j0, kbeg, kend, acc, full, empty); break;
-    case 1 * 4 + 1: mma_loop_tma<LPRE, 1, 1>(t, smem, i0, j0, kbeg, kend, acc, full, empty); break;
-    default: mma_loop_tma<LPRE, 0, 0>(t, smem, i0, j0, kbeg, kend, acc, full, empty); break;
-  }
+  const int64_t r0w = i0 + 16 * warp_row<LPRE>(w), c0w = j0 + 16 * warp_col<LPRE>(w);
+  const int nrb = r0w >= g.M ? 0 : (int)min((int64_t)2, (g.M - r0w + 7) / 8);
+  const int ncb = c0w >= g.N ? 0 : (int)min((int64_t)2, (g.N - c0w + 7) / 8);
+  return (nrb == 0 || ncb == 0) ? 0 : warp_half(w) * 16 + nrb * 4 + ncb;
 }
 
-// acc (8 products) over k in [kbeg, kend) for the tile at (i0, j0).  Warp
-// blocks past M or N issue no DMMA (the loop instance is chosen per warp).
+#define QT8_DISPATCH(LOOP, ...)                                             \
+  switch (instance<LPRE>(g, i0, j0)) {                                      \
+    case 0 * 16 + 2 * 4 + 2: LOOP<LPRE, 0, 2, 2>(__VA_ARGS__); break;       \
+    case 0 * 16 + 2 * 4 + 1: LOOP<LPRE, 0, 2, 1>(__VA_ARGS__); break;       \
+    case 0 * 16 + 1 * 4 + 2: LOOP<LPRE, 0, 1, 2>(__VA_ARGS__); break;       \
+    case 0 * 16 + 1 * 4 + 1: LOOP<LPRE, 0, 1, 1>(__VA_ARGS__); break;       \
+    case 1 * 16 + 2 * 4 + 2: LOOP<LPRE, 1, 2, 2>(__VA_ARGS__); break;       \
+    case 1 * 16 + 2 * 4 + 1: LOOP<LPRE, 1, 2, 1>(__VA_ARGS__); break;       \
+    case 1 * 16 + 1 * 4 + 2: LOOP<LPRE, 1, 1, 2>(__VA_ARGS__); break;       \
+    case 1 * 16 + 1 * 4 + 1: LOOP<LPRE, 1, 1, 1>(__VA_ARGS__); break;       \
+    default: LOOP<LPRE, 0, 0, 0>(__VA_ARGS__); break; /* loads + barriers */ \
+  }
+
+// acc (the warp's 4 products) over k in [kbeg, kend) for the tile at (i0, j0).
 template <bool LPRE>
 __device__ __forceinline__ void mma_tile(const Operands& g, double* smem, int64_t i0, int64_t j0, int64_t kbeg,
-                                         int64_t kend, Acc<LPRE>& acc) {
-  using C = Cfg<LPRE>;
+                                         int64_t kend, Acc& acc) {
   __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES];
-  const int w = threadIdx.x >> 5;
-  const int64_t r0w = i0 + 8 * C::WRB * warp_row<LPRE>(w), c0w = j0 + 8 * C::WCB * warp_col<LPRE>(w);
-  const int nrb = r0w >= g.M ? 0 : (int)min((int64_t)C::WRB, (g.M - r0w + 7) / 8);
-  const int ncb = c0w >= g.N ? 0 : (int)min((int64_t)C::WCB, (g.N - c0w + 7) / 8);
-  switch (nrb * 4 + ncb) {
-    case 2 * 4 + 2: mma_loop<LPRE, 2, 2>(g, smem, i0, j0, kbeg, kend, acc, full, empty); break;
-    case 2 * 4 + 1: mma_loop<LPRE, 2, 1>(g, smem, i0, j0, kbeg, kend, acc, full, empty); break;
-    case 1 * 4 + 2: mma_loop<LPRE, 1, 2>(g, smem, i0, j0, kbeg, kend, acc, full, empty); break;
-    case 1 * 4 + 1: mma_loop<LPRE, 1, 1>(g, smem, i0, j0, kbeg, kend, acc, full, empty); break;
-    default: mma_loop<LPRE, 0, 0>(g, smem, i0, j0, kbeg, kend, acc, full, empty); break;
+  QT8_DISPATCH(mma_loop, g, smem, i0, j0, kbeg, kend, acc, full, empty)
+}
+template <bool LPRE>
+__device__ __forceinline__ void mma_tile_tma(const TmaOps& t, const Operands& g, double* smem, int64_t i0, int64_t j0,
+                                             int64_t kbeg, int64_t kend, Acc& acc) {
+  __shared__ __align__(8) uint64_t full[MAX_STAGES], empty[MAX_STAGES];
+  QT8_DISPATCH(mma_loop_tma, t, smem, i0, j0, kbeg, kend, acc, full, empty)
+}
+#undef QT8_DISPATCH
+
+// Epilogue exchange: the product-half-1 warps hand their accumulators to the
+// half-0 warp of the same position through shared memory (lane-major,
+// conflict-free).  `xbuf` needs 8 * 32 * 32 doubles; call after the k loop
+// (which ends with a CTA barrier).  Returns the lane's slot for the half-0
+// warps (read with other_product), nullptr for the half-1 warps.
+__device__ __forceinline__ const double* exchange_products(const Acc& acc, double* xbuf) {
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* slot = xbuf + (w & 7) * 32 * 32 + lane;
+  if (warp_half(w) == 1) {
+#pragma unroll
+    for (int ii = 0; ii < 4; ++ii)
+#pragma unroll
+      for (int rb = 0; rb < 2; ++rb)
+#pragma unroll
+        for (int cb = 0; cb < 2; ++cb)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) slot[32 * (((ii * 2 + rb) * 2 + cb) * 2 + h)] = acc[ii][rb][cb][h];
   }
+  __syncthreads();
+  return warp_half(w) == 1 ? nullptr : slot;
+}
+// product m_{5 + ii} of element (rb, cb, h) from the exchange slot
+__device__ __forceinline__ double other_product(const double* slot, int ii, int rb, int cb, int h) {
+  return slot[32 * (((ii * 2 + rb) * 2 + cb) * 2 + h)];
 }
 
 }  // namespace qt8

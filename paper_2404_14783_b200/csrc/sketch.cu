@@ -138,6 +138,7 @@ struct Fused8Args {
   // TMA maps (sketch8_kernel<true>): Y left = A panel, Y right = Omega~,
   // W left = Psi~ panel, W right = A panel (3D: inner, rows, planes)
   CUtensorMap ylm, yrm, wlm, wrm;
+  int stages, pf;  // TMA ring slots / prefetch distance
   qt8::Operands yop;  // A_panel (k-fast) x Omega~ (8 planes, j-fast): M = panel rows, N = s, K = n
   qt8::Operands wop;  // Psi~_panel (8 planes, k-fast) x A_panel (j-fast): M = l, N = n, K = panel rows
   int64_t ky, kw;
@@ -154,23 +155,29 @@ struct Fused8Args {
   double* wp;
 };
 
+// Epilogue: the half-0 warps gather the other half's products (qtile8.cuh),
+// form the quaternion planes and add them to C (or write the split-K partial).
 template <bool LPRE>
-__device__ __forceinline__ void store_tile8(const qt8::Acc<LPRE>& acc, int64_t i0, int64_t j0, int64_t M, int64_t N,
-                                            double* const* c, int64_t ldc, double* part) {
-  using C = qt8::Cfg<LPRE>;
+__device__ __forceinline__ void store_tile8(const qt8::Acc& acc, double* xbuf, int64_t i0, int64_t j0, int64_t M,
+                                            int64_t N, double* const* c, int64_t ldc, double* part) {
+  const double* slot = qt8::exchange_products(acc, xbuf);
+  if (!slot) return;
 #pragma unroll
-  for (int rb = 0; rb < C::WRB; ++rb) {
+  for (int rb = 0; rb < 2; ++rb) {
     const int64_t gi = i0 + qt8::acc_row<LPRE>(rb);
     if (gi >= M) continue;
 #pragma unroll
-    for (int cb = 0; cb < C::WCB; ++cb)
+    for (int cb = 0; cb < 2; ++cb)
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int64_t gj = j0 + qt8::acc_col<LPRE>(cb) + h;
         if (gj >= N) continue;
         double m[8], q[4];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) m[i] = acc[i][rb][cb][h];
+        for (int ii = 0; ii < 4; ++ii) {
+          m[ii] = acc[ii][rb][cb][h];
+          m[4 + ii] = qt8::other_product(slot, ii, rb, cb, h);
+        }
         qt8::combine(m, q);
         if (part) {
 #pragma unroll
@@ -219,27 +226,27 @@ __global__ void __launch_bounds__(qt8::NT, 1) sketch8_kernel(const __grid_consta
     tm = f.w_tmf + t % (f.w_tm - f.w_tmf); tn = t / (f.w_tm - f.w_tmf);
   }
   if (!is_w) {
-    qt8::Acc<false> acc;
-    qt8::zero_acc<false>(acc);
+    qt8::Acc acc;
+    qt8::zero_acc(acc);
     const int64_t kb = (int64_t)z * f.ky_chunk, ke = min(f.ky, kb + f.ky_chunk);
     if (TMA)
-      qt8::mma_tile_tma<false>(qt8::TmaOps{&f.ylm, &f.yrm, 0}, f.yop, smem, (int64_t)tm * Y8M, (int64_t)tn * Y8N, kb,
+      qt8::mma_tile_tma<false>(qt8::TmaOps{&f.ylm, &f.yrm, 0, f.stages, f.pf}, f.yop, smem, (int64_t)tm * Y8M, (int64_t)tn * Y8N, kb,
                                ke, acc);
     else
       qt8::mma_tile<false>(f.yop, smem, (int64_t)tm * Y8M, (int64_t)tn * Y8N, kb, ke, acc);
     double* part = f.zy > 1 ? f.yp + (int64_t)z * 4 * f.yop.M * f.yop.N : nullptr;
-    store_tile8<false>(acc, (int64_t)tm * Y8M, (int64_t)tn * Y8N, f.yop.M, f.yop.N, f.y, f.ldy, part);
+    store_tile8<false>(acc, smem, (int64_t)tm * Y8M, (int64_t)tn * Y8N, f.yop.M, f.yop.N, f.y, f.ldy, part);
   } else {
-    qt8::Acc<true> acc;
-    qt8::zero_acc<true>(acc);
+    qt8::Acc acc;
+    qt8::zero_acc(acc);
     const int64_t kb = (int64_t)z * f.kw_chunk, ke = min(f.kw, kb + f.kw_chunk);
     if (TMA)
-      qt8::mma_tile_tma<true>(qt8::TmaOps{&f.wlm, &f.wrm, 0}, f.wop, smem, (int64_t)tm * W8M, (int64_t)tn * W8N, kb,
+      qt8::mma_tile_tma<true>(qt8::TmaOps{&f.wlm, &f.wrm, 0, f.stages, f.pf}, f.wop, smem, (int64_t)tm * W8M, (int64_t)tn * W8N, kb,
                               ke, acc);
     else
       qt8::mma_tile<true>(f.wop, smem, (int64_t)tm * W8M, (int64_t)tn * W8N, kb, ke, acc);
     double* part = f.zw > 1 ? f.wp + (int64_t)z * 4 * f.wop.M * f.wop.N : nullptr;
-    store_tile8<true>(acc, (int64_t)tm * W8M, (int64_t)tn * W8N, f.wop.M, f.wop.N, f.w, f.ldw, part);
+    store_tile8<true>(acc, smem, (int64_t)tm * W8M, (int64_t)tn * W8N, f.wop.M, f.wop.N, f.w, f.ldw, part);
   }
 }
 
@@ -421,6 +428,23 @@ bool tma_layout(const QView& a, int64_t* pstride) {
   *pstride = d;
   return true;
 }
+// TMA ring: slots and prefetch distance (QLRA_Q8_STAGES / QLRA_Q8_PF override)
+int tma_stages() {
+  static const int v = [] {
+    const char* e = std::getenv("QLRA_Q8_STAGES");
+    const int s = e ? std::atoi(e) : 5;
+    return std::max(2, std::min(s, std::min(qt8::MAX_STAGES, (int)((227 * 1024 - 256) / (qt8::STAGE * sizeof(double))))));
+  }();
+  return v;
+}
+int tma_prefetch() {
+  static const int v = [] {
+    const char* e = std::getenv("QLRA_Q8_PF");
+    const int p = e ? std::atoi(e) : 3;
+    return std::max(1, std::min(p, tma_stages() - 1));
+  }();
+  return v;
+}
 bool sketch_tma_enabled() {
   static const bool v = [] {
     const char* e = std::getenv("QLRA_SKETCH_TMA");
@@ -523,8 +547,11 @@ void sketch_panel(Ctx& ctx, const Emb& e, int64_t pc0, const QView& ap, const QV
                      make_map3(&f.wlm, e.ps8 + pc0, rp, l, 8, e.ps8_ld, l * e.ps8_ld, qt8::LDK, W8M, 8) &&
                      make_map3(&f.wrm, ap.p[0], n, rp, 4, ap.ld, aps, qt8::Layout<true>::LDX, qt8::BK, 4);
     LaunchTimer lt(ctx);
+    f.stages = tma_stages();
+    f.pf = tma_prefetch();
     if (tma)
-      sketch8_kernel<true><<<(unsigned)ctas, qt8::NT, qt8::SMEM_BYTES + 128, ctx.stream>>>(f);
+      sketch8_kernel<true><<<(unsigned)ctas, qt8::NT, (size_t)f.stages * qt8::STAGE * sizeof(double) + 128,
+                             ctx.stream>>>(f);
     else
       sketch8_kernel<false><<<(unsigned)ctas, qt8::NT, qt8::SMEM_BYTES + 128, ctx.stream>>>(f);
     QLRA_LAUNCH_CHECK();
@@ -593,7 +620,7 @@ void set_kernel_attrs() {
   set_func_attr((const void*)sketch8_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                 (int)qt8::SMEM_BYTES + 128);
   set_func_attr((const void*)sketch8_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                (int)qt8::SMEM_BYTES + 128);
+                (int)(tma_stages() * qt8::STAGE * sizeof(double)) + 128);
 }
 
 // Rows per fused launch.  Device-resident A: panels of up to kPanelBytes --
