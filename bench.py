@@ -285,7 +285,9 @@ def main():
     # allocation pattern (two generations of Y, W, H, X alive); a reserved
     # segment carved up by later allocations keeps cudaMalloc -- which blocks
     # the host -- out of the timed region
-    _reserve = torch.empty(int(512e6) // 8, dtype=torch.float64, device="cuda")
+    # (sized for two generations of this config's Y, W, H and X)
+    per_step = 32 * ((r1 - r0) * cfg.s * 2 + cfg.l * cfg.n + cfg.s * cfg.n)
+    _reserve = torch.empty(int(max(512e6, 2.2 * per_step)) // 8, dtype=torch.float64, device="cuda")
     del _reserve
     ctx.kernel_timing(True)
     launches0 = ctx.launch_count()
@@ -349,7 +351,9 @@ def main():
         barrier()
         s0 = torch.cuda.Event(enable_timing=True)
         s1 = torch.cuda.Event(enable_timing=True)
-        _reserve = torch.empty(int(512e6) // 8, dtype=torch.float64, device="cuda")
+        # (sized for two generations of this config's Y, W, H and X)
+        per_step = 32 * ((r1 - r0) * cfg.s * 2 + cfg.l * cfg.n + cfg.s * cfg.n)
+        _reserve = torch.empty(int(max(512e6, 2.2 * per_step)) // 8, dtype=torch.float64, device="cuda")
         del _reserve
         gc.collect()
         gc.disable()

@@ -153,13 +153,15 @@ struct Fused8Args {
   double* w[4];
   int64_t ldw;
   double* wp;
+  double alpha, beta;  // C = alpha * product + beta * C (sketch: 1, 1); partials are plain
 };
 
 // Epilogue: the half-0 warps gather the other half's products (qtile8.cuh),
 // form the quaternion planes and add them to C (or write the split-K partial).
 template <bool LPRE>
 __device__ __forceinline__ void store_tile8(const qt8::Acc& acc, double* xbuf, int64_t i0, int64_t j0, int64_t M,
-                                            int64_t N, double* const* c, int64_t ldc, double* part) {
+                                            int64_t N, double* const* c, int64_t ldc, double* part, double alpha,
+                                            double beta) {
   const double* slot = qt8::exchange_products(acc, xbuf);
   if (!slot) return;
 #pragma unroll
@@ -186,7 +188,7 @@ __device__ __forceinline__ void store_tile8(const qt8::Acc& acc, double* xbuf, i
 #pragma unroll
           for (int p = 0; p < 4; ++p) {
             double* dst = c[p] + gi * ldc + gj;
-            *dst = *dst + q[p];
+            *dst = beta == 1.0 && alpha == 1.0 ? *dst + q[p] : (beta != 0.0 ? fma(beta, *dst, alpha * q[p]) : alpha * q[p]);
           }
         }
       }
@@ -235,7 +237,7 @@ __global__ void __launch_bounds__(qt8::NT, 1) sketch8_kernel(const __grid_consta
     else
       qt8::mma_tile<false>(f.yop, smem, (int64_t)tm * Y8M, (int64_t)tn * Y8N, kb, ke, acc);
     double* part = f.zy > 1 ? f.yp + (int64_t)z * 4 * f.yop.M * f.yop.N : nullptr;
-    store_tile8<false>(acc, smem, (int64_t)tm * Y8M, (int64_t)tn * Y8N, f.yop.M, f.yop.N, f.y, f.ldy, part);
+    store_tile8<false>(acc, smem, (int64_t)tm * Y8M, (int64_t)tn * Y8N, f.yop.M, f.yop.N, f.y, f.ldy, part, f.alpha, f.beta);
   } else {
     qt8::Acc acc;
     qt8::zero_acc(acc);
@@ -246,7 +248,7 @@ __global__ void __launch_bounds__(qt8::NT, 1) sketch8_kernel(const __grid_consta
     else
       qt8::mma_tile<true>(f.wop, smem, (int64_t)tm * W8M, (int64_t)tn * W8N, kb, ke, acc);
     double* part = f.zw > 1 ? f.wp + (int64_t)z * 4 * f.wop.M * f.wop.N : nullptr;
-    store_tile8<true>(acc, smem, (int64_t)tm * W8M, (int64_t)tn * W8N, f.wop.M, f.wop.N, f.w, f.ldw, part);
+    store_tile8<true>(acc, smem, (int64_t)tm * W8M, (int64_t)tn * W8N, f.wop.M, f.wop.N, f.w, f.ldw, part, f.alpha, f.beta);
   }
 }
 
@@ -457,8 +459,9 @@ bool sketch_tma_enabled() {
 struct LaunchTimer {
   Ctx& ctx;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
-  explicit LaunchTimer(Ctx& c) : ctx(c) {
-    if (!ctx.ktimer.on) return;
+  bool on;
+  explicit LaunchTimer(Ctx& c, bool timed = true) : ctx(c), on(timed && c.ktimer.on) {
+    if (!on) return;
     if (!ctx.ktimer.pool.empty()) {
       e0 = ctx.ktimer.pool.back().first;
       e1 = ctx.ktimer.pool.back().second;
@@ -470,7 +473,7 @@ struct LaunchTimer {
     QLRA_CUDA(cudaEventRecord(e0, ctx.stream));
   }
   void done(int64_t rp, int64_t n, int64_t s, int64_t l) {
-    if (!ctx.ktimer.on) return;
+    if (!on) return;
     QLRA_CUDA(cudaEventRecord(e1, ctx.stream));
     ctx.ktimer.ev.emplace_back(e0, e1);
     ctx.ktimer.flops += 32.0 * (double)rp * (double)n * (double)(s + l);
@@ -508,57 +511,91 @@ void set_splits(Args& f, const Geom& G, int64_t rp, int64_t n, int64_t s, int64_
   }
 }
 
+// One launch of the 8-product engine (+ ordered split-K reductions).
+//   Y part: C (M x N) = alpha * A (M x K) * B~ (K x N) + beta * C,
+//           A on the fly (4 planes), B~ the 8 combined right planes of B;
+//   W part: C (M x N) = alpha * P~ (M x K) * A (K x N) + beta * C,
+//           P~ the 8 combined left planes of P (from column col0), A on the fly.
+// Either part may be absent.  The sketch launches both (the same A block as
+// the Y part's left and the W part's right operand), the 8-product qgemm one.
+struct Q8Part {
+  QView a;                  // the on-the-fly operand
+  const double* comb;       // combined planes (8 x rows x comb_ld)
+  int64_t comb_ld, col0;    // leading dimension (even), first column used (even)
+  QView c;                  // output
+};
+void launch8(Ctx& ctx, const Q8Part* y, const Q8Part* w, double alpha, double beta, SketchWork& ws, bool timed) {
+  Fused8Args f{};
+  f.alpha = alpha;
+  f.beta = beta;
+  // split simulation extents: rp = Y's M and W's K, n = Y's K and W's N
+  const int64_t rp = y ? y->a.rows : w->a.rows, n = y ? y->a.cols : w->a.cols;
+  const int64_t s = y ? y->c.cols : 0, l = w ? w->c.rows : 0;
+  if (y && w && (w->a.rows != rp || w->a.cols != n)) fail(QLRA_ERR_SHAPE, "launch8: coupled parts differ");
+  static const double kNull = 0.0;
+  for (int p = 0; p < 4; ++p) {
+    f.yop.l[p] = y ? y->a.p[p] : &kNull;
+    f.wop.r[p] = w ? w->a.p[p] : &kNull;
+    f.y[p] = y ? y->c.p[p] : nullptr;
+    f.w[p] = w ? w->c.p[p] : nullptr;
+  }
+  for (int i = 0; i < 8; ++i) {
+    f.yop.r[i] = y ? y->comb + (size_t)i * n * y->comb_ld : &kNull;
+    f.wop.l[i] = w ? w->comb + (size_t)i * l * w->comb_ld + w->col0 : &kNull;
+  }
+  if (y) {
+    f.yop.l_si = y->a.ld; f.yop.r_sk = y->comb_ld;
+    f.yop.M = rp; f.yop.N = s;
+    f.ldy = y->c.ld;
+  }
+  if (w) {
+    f.wop.l_si = w->comb_ld; f.wop.r_sk = w->a.ld;
+    f.wop.M = l; f.wop.N = n;
+    f.ldw = w->c.ld;
+  }
+  f.ky = n;
+  f.kw = rp;
+  set_splits(f, kGeom8, rp, n, s, l, ctx, ws);
+  if (!y) f.y_tm = f.y_tn = f.y_tnf = 0;
+  if (!w) f.w_tm = f.w_tn = f.w_tmf = 0;
+  const int64_t ctas = (int64_t)f.y_tm * f.y_tn * f.zy + (int64_t)f.w_tm * f.w_tn * f.zw;
+  if (ctas == 0) return;
+  // TMA staging when each on-the-fly operand's planes form one
+  // 16-byte-aligned 3D tensor; the maps cover exactly the operands (rows past
+  // them, k past K and columns past N come back zero)
+  int64_t yps = 0, wps = 0;
+  bool tma = sketch_tma_enabled();
+  if (tma && y)
+    tma = tma_layout(y->a, &yps) && make_map3(&f.ylm, y->a.p[0], n, rp, 4, y->a.ld, yps, qt8::LDK, Y8M, 4) &&
+          make_map3(&f.yrm, y->comb, s, n, 8, y->comb_ld, n * y->comb_ld, qt8::Layout<false>::LDX, qt8::BK, 8);
+  if (tma && w)
+    tma = tma_layout(w->a, &wps) && (w->col0 % 2) == 0 &&
+          make_map3(&f.wlm, w->comb + w->col0, rp, l, 8, w->comb_ld, l * w->comb_ld, qt8::LDK, W8M, 8) &&
+          make_map3(&f.wrm, w->a.p[0], n, rp, 4, w->a.ld, wps, qt8::Layout<true>::LDX, qt8::BK, 4);
+  f.stages = tma_stages();
+  f.pf = tma_prefetch();
+  LaunchTimer lt(ctx, timed);
+  if (tma)
+    sketch8_kernel<true><<<(unsigned)ctas, qt8::NT, (size_t)f.stages * qt8::STAGE * sizeof(double) + 128,
+                           ctx.stream>>>(f);
+  else
+    sketch8_kernel<false><<<(unsigned)ctas, qt8::NT, qt8::SMEM_BYTES + 128, ctx.stream>>>(f);
+  QLRA_LAUNCH_CHECK();
+  count_launch();
+  lt.done(rp, n, s, l);
+  if (y && f.zy > 1) splitk_reduce(ctx, f.yp, f.zy, y->c, alpha, beta);
+  if (w && f.zw > 1) splitk_reduce(ctx, f.wp, f.zw, w->c, alpha, beta);
+}
+
 // One fused launch (+ ordered partial reductions) for a row panel `ap` of A
 // whose Psi columns are ps[:, pc0 : pc0 + ap.rows].
 void sketch_panel(Ctx& ctx, const Emb& e, int64_t pc0, const QView& ap, const QView& yv, const QView& w,
                   SketchWork& ws) {
   const int64_t rp = ap.rows, n = ap.cols, s = e.om.cols, l = e.ps.rows;
   if (e.om8) {
-    Fused8Args f{};
-    const int64_t pb = e.ps.cols;  // Psi block columns (ld of the combined planes)
-    for (int p = 0; p < 4; ++p) {
-      f.yop.l[p] = ap.p[p];
-      f.wop.r[p] = ap.p[p];
-      f.y[p] = yv.p[p];
-      f.w[p] = w.p[p];
-    }
-    (void)pb;
-    for (int i = 0; i < 8; ++i) {
-      f.yop.r[i] = e.om8 + (size_t)i * n * e.om8_ld;
-      f.wop.l[i] = e.ps8 + (size_t)i * l * e.ps8_ld + pc0;  // Psi~[:, pc0:pc0+rp]
-    }
-    f.yop.l_si = ap.ld; f.yop.r_sk = e.om8_ld;
-    f.yop.M = rp; f.yop.N = s;
-    f.wop.l_si = e.ps8_ld; f.wop.r_sk = ap.ld;
-    f.wop.M = l; f.wop.N = n;
-    f.ky = n;
-    f.kw = rp;
-    f.ldy = yv.ld;
-    f.ldw = w.ld;
-    set_splits(f, kGeom8, rp, n, s, l, ctx, ws);
-    const int64_t ctas = (int64_t)f.y_tm * f.y_tn * f.zy + (int64_t)f.w_tm * f.w_tn * f.zw;
-    // TMA staging when A's planes form one 16-byte-aligned 3D tensor; the
-    // maps cover exactly this panel (rows past it, k past n and columns past
-    // s / n come back zero)
-    int64_t aps = 0;
-    const bool tma = sketch_tma_enabled() && tma_layout(ap, &aps) && (pc0 % 2) == 0 &&
-                     make_map3(&f.ylm, ap.p[0], n, rp, 4, ap.ld, aps, qt8::LDK, Y8M, 4) &&
-                     make_map3(&f.yrm, e.om8, s, n, 8, e.om8_ld, n * e.om8_ld, qt8::Layout<false>::LDX, qt8::BK, 8) &&
-                     make_map3(&f.wlm, e.ps8 + pc0, rp, l, 8, e.ps8_ld, l * e.ps8_ld, qt8::LDK, W8M, 8) &&
-                     make_map3(&f.wrm, ap.p[0], n, rp, 4, ap.ld, aps, qt8::Layout<true>::LDX, qt8::BK, 4);
-    LaunchTimer lt(ctx);
-    f.stages = tma_stages();
-    f.pf = tma_prefetch();
-    if (tma)
-      sketch8_kernel<true><<<(unsigned)ctas, qt8::NT, (size_t)f.stages * qt8::STAGE * sizeof(double) + 128,
-                             ctx.stream>>>(f);
-    else
-      sketch8_kernel<false><<<(unsigned)ctas, qt8::NT, qt8::SMEM_BYTES + 128, ctx.stream>>>(f);
-    QLRA_LAUNCH_CHECK();
-    count_launch();
-    lt.done(rp, n, s, l);
-    if (f.zy > 1) splitk_reduce(ctx, f.yp, f.zy, yv, 1.0, 1.0);
-    if (f.zw > 1) splitk_reduce(ctx, f.wp, f.zw, w, 1.0, 1.0);
+    const Q8Part yp{ap, e.om8, e.om8_ld, 0, yv};
+    const Q8Part wq{ap, e.ps8, e.ps8_ld, pc0, w};
+    launch8(ctx, &yp, &wq, 1.0, 1.0, ws, true);
     return;
   }
   FusedArgs f{};
@@ -600,14 +637,23 @@ void launch_combine8(Ctx& ctx, const QView& in, double* out, int64_t ld, bool le
   count_launch();
 }
 
-// Fill e.om8 / e.ps8 (when the 8-product engine is on) into `store`.
-void prepare_emb(Ctx& ctx, Emb& e, DeviceBuffer& store) {
+// Fill e.om8 / e.ps8 (when the 8-product engine is on) into the context's
+// kept combination buffer.
+void prepare_emb(Ctx& ctx, Emb& e) {
   if (!sketch_use8()) return;
   e.om8_ld = (e.om.cols + 1) / 2 * 2;
   e.ps8_ld = (e.ps.cols + 1) / 2 * 2;
   const size_t no = (size_t)8 * e.om.rows * e.om8_ld, np = (size_t)8 * e.ps.rows * e.ps8_ld;
-  store = DeviceBuffer(ctx, (no + np) * sizeof(double));
-  double* base = store.as<double>();
+  const size_t bytes = (no + np) * sizeof(double);
+  Ctx::CombKeep& k = ctx.comb_keep;
+  if (k.bytes < bytes) {
+    if (k.buf) QLRA_CUDA(cudaFreeAsync(k.buf, ctx.stream));
+    k.buf = nullptr;
+    k.bytes = 0;
+    QLRA_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&k.buf), bytes, ctx.stream));
+    k.bytes = bytes;
+  }
+  double* base = k.buf;
   launch_combine8(ctx, e.om, base, e.om8_ld, false);
   launch_combine8(ctx, e.ps, base + no, e.ps8_ld, true);
   e.om8 = base;
@@ -673,6 +719,40 @@ bool same_spec(const qlra_spec_t& a, const qlra_spec_t& b) {
 }
 }  // namespace
 
+// C = alpha * A B + beta * C on the 8-product engine when one factor is much
+// smaller than the other (the tall products of the rangefinders and the core
+// solve: Y R^-1, Q0 C, Psi Q0, ...): the small factor is combined into its 8
+// planes (one pass over it), the large one streams through the kernel as
+// the sketch's A does.  Returns false (nothing launched) when the shapes do
+// not fit that pattern; the caller then runs the 16-product qgemm.
+bool q8gemm_try(Ctx& ctx, double alpha, const QView& A, const QView& B, double beta, const QView& C) {
+  static const bool enabled = [] {
+    const char* e = std::getenv("QLRA_Q8GEMM");
+    return !(e && std::atoi(e) == 0);
+  }();
+  if (!enabled || !sketch_use8()) return false;
+  const int64_t M = A.rows, K = A.cols, N = B.cols;
+  if (B.rows != K || C.rows != M || C.cols != N || M == 0 || N == 0 || K == 0) return false;
+  const double a_el = (double)M * (double)K, b_el = (double)K * (double)N;
+  const bool right = b_el * 4.0 <= a_el, left = !right && a_el * 4.0 <= b_el;
+  if (!right && !left) return false;
+  set_kernel_attrs();
+  const QView& small = right ? B : A;
+  const int64_t ld = (small.cols + 1) / 2 * 2;
+  DeviceBuffer comb(ctx, (size_t)8 * small.rows * ld * sizeof(double));
+  launch_combine8(ctx, small, comb.as<double>(), ld, left);
+  SketchWork ws;
+  if (right) {
+    const Q8Part y{A, comb.as<double>(), ld, 0, C};
+    launch8(ctx, &y, nullptr, alpha, beta, ws, false);
+  } else {
+    const Q8Part w{B, comb.as<double>(), ld, 0, C};
+    launch8(ctx, nullptr, &w, alpha, beta, ws, false);
+  }
+  return true;
+}
+
+
 QView psi_for_sketch(Ctx& ctx, const qlra_spec_t& psi, int64_t row0, int64_t rows, DevQMat& tmp) {
   static const double cap = env_or("QLRA_PSI_KEEP_BYTES", 8e9);
   const int64_t l = psi.rows;
@@ -712,6 +792,8 @@ void psi_keep_release(Ctx& ctx) {
   Ctx::PsiKeep& k = ctx.psi_keep;
   if (k.buf) cudaFreeAsync(k.buf, ctx.stream);
   k = Ctx::PsiKeep{};
+  if (ctx.comb_keep.buf) cudaFreeAsync(ctx.comb_keep.buf, ctx.stream);
+  ctx.comb_keep = Ctx::CombKeep{};
 }
 
 void sketch_update_rows(Ctx& ctx, const qlra_spec_t& omega, const qlra_spec_t& psi, int64_t row0,
@@ -724,8 +806,7 @@ void sketch_update_rows(Ctx& ctx, const qlra_spec_t& omega, const qlra_spec_t& p
   Emb e;
   e.om = om.v;
   e.ps = psi_for_sketch(ctx, psi, row0, b, ps_tmp);
-  DeviceBuffer comb;
-  prepare_emb(ctx, e, comb);
+  prepare_emb(ctx, e);
   const int64_t R = panel_rows(n, b);
   SketchWork ws;
   for (int64_t r0 = 0; r0 < b; r0 += R) {
@@ -764,8 +845,7 @@ void sketch_update_rows_host(Ctx& ctx, const qlra_spec_t& omega, const qlra_spec
   Emb e;
   e.om = om.v;
   e.ps = psi_for_sketch(ctx, psi, row0, b, ps_tmp);
-  DeviceBuffer comb;
-  prepare_emb(ctx, e, comb);
+  prepare_emb(ctx, e);
   SketchWork ws;
   // The last R rows go in quarter-size chunks: the sketch of the final chunk
   // is the one part of the pipeline nothing overlaps (the copy stream is the

@@ -121,6 +121,22 @@ def test_sketch_c1_vs_oracle(ctx, kind):
     assert rel_diff(host(st.w), w) < 1e-13
 
 
+@pytest.mark.parametrize("m,n,s,l", [
+    (333, 257, 13, 29),   # odd n: A rows not 16-byte aligned -> cp.async staging
+    (520, 300, 40, 80),   # C5-like widths, TMA staging, padded 8x8 blocks in both tiles
+    (130, 66, 33, 65),    # s, l one past the 32-wide tile edge
+    (65, 7, 3, 5),        # tiny: a single partial tile of each kind
+])
+def test_sketch_engine_shapes_vs_oracle(ctx, m, n, s, l):
+    """8-product sketch engine (qtile8.cuh) at ragged shapes, both staging paths."""
+    from paper_2404_14783_b200 import qlra as Q
+    a = random_gaussian(m, n, 1000 + m + n)
+    st = Q.make_sketch(dev(a), min(s, 3), s, l, 7, 8, ctx=ctx)
+    y, w = O.make_sketch(a, min(s, 3), s, l, 7, 8, nthreads=8)
+    assert rel_diff(host(st.y), y) < 1e-13
+    assert rel_diff(host(st.w), w) < 1e-13
+
+
 def test_streaming_equals_monolithic(ctx):  # test_sketching.cpp:120-129
     from paper_2404_14783_b200 import qlra as Q
     a = dev(random_gaussian(400, 300, 39))
