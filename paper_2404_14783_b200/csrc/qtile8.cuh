@@ -52,6 +52,9 @@ namespace qlra_dev {
 namespace qt8 {
 
 constexpr int NT = 512, BK = 8, STAGES = 4;
+// TMA launches add one producer warp (warp 16) that only issues the stage
+// copies, so no compute warp ever waits on a slot's release
+constexpr int NT_TMA = NT + 32;
 constexpr int LDK = BK + 4;  // k-fast rows, pitch 12 (4 mod 16: conflict-free fragments)
 
 template <bool LPRE>
@@ -315,7 +318,7 @@ struct TmaOps {
   const CUtensorMap* lm;  // left map
   const CUtensorMap* rm;  // right map
   int lk_off;             // inner coordinate offset of the left map's k (Psi~ panel column)
-  int stages, pf;         // ring slots (<= MAX_STAGES, smem sized by the launch) and prefetch distance (< stages)
+  int stages;             // ring slots (<= MAX_STAGES, smem sized by the launch)
 };
 
 __device__ __forceinline__ void tma_load3(double* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
@@ -337,8 +340,39 @@ __device__ __forceinline__ void tma_stage(const TmaOps& t, double* Ls, double* R
   tma_load3(Rs, t.rm, (int)j0, (int)k0, bar);
 }
 
-// The ring with a single producer thread (thread 0) issuing each stage PF
-// stages ahead; a refill waits for every warp's release of that slot.
+// The ring fed by a dedicated producer warp (warp 16, one elected lane):
+// it issues stage k + PF once every compute warp has released the slot's
+// previous stage; the 16 compute warps only wait for data.
+template <bool LPRE>
+__device__ __forceinline__ void tma_init(const TmaOps& t, uint64_t* full, uint64_t* empty) {
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < t.stages; ++s) {
+      qt::mbar_init(&full[s], 1);
+      qt::mbar_init(&empty[s], NT / 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+}
+
+template <bool LPRE>
+__device__ __forceinline__ void tma_producer(const TmaOps& t, double* smem, int64_t i0, int64_t j0, int64_t kbeg,
+                                             int64_t kend, uint64_t* full, uint64_t* empty) {
+  constexpr int LOFF = Layout<LPRE>::L_ELEMS;
+  const int nk = kend > kbeg ? (int)((kend - kbeg + BK - 1) / BK) : 0;
+  if ((threadIdx.x & 31) == 0) {
+    const int S = t.stages;
+    int s = 0, ph = 0;
+    for (int kt = 0; kt < nk; ++kt) {
+      if (kt >= S) qt::mbar_wait_parity(&empty[s], (unsigned)((ph - 1) & 1));
+      tma_stage<LPRE>(t, smem + s * STAGE, smem + s * STAGE + LOFF, i0, j0, kbeg + (int64_t)kt * BK, &full[s]);
+      if (++s == S) { s = 0; ++ph; }
+    }
+  }
+  __syncwarp();
+  __syncthreads();  // pairs with the compute warps' closing barrier
+}
+
 template <bool LPRE, int HALF, int NRB, int NCB>
 __device__ __forceinline__ void mma_loop_tma(const TmaOps& t, double* smem, int64_t i0, int64_t j0, int64_t kbeg,
                                              int64_t kend, Acc& acc, uint64_t* full, uint64_t* empty) {
@@ -347,31 +381,9 @@ __device__ __forceinline__ void mma_loop_tma(const TmaOps& t, double* smem, int6
   const int gid = lane >> 2, tig = lane & 3;
   const int nk = kend > kbeg ? (int)((kend - kbeg + BK - 1) / BK) : 0;
   constexpr int LOFF = Layout<LPRE>::L_ELEMS;
-  const int S = t.stages, PF = t.pf;
-  if (tid == 0) {
-    for (int s = 0; s < S; ++s) {
-      qt::mbar_init(&full[s], 1);
-      qt::mbar_init(&empty[s], NT / 32);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-  if (tid == 0) {
-    for (int p = 0; p < PF && p < nk; ++p)
-      tma_stage<LPRE>(t, smem + p * STAGE, smem + p * STAGE + LOFF, i0, j0, kbeg + (int64_t)p * BK, &full[p]);
-  }
-  // slot s and its phase parity advance with kt (no division per stage)
-  int s = 0, ph = 0, sn = PF % S, phn = PF / S;
+  const int S = t.stages;
+  int s = 0, ph = 0;
   for (int kt = 0; kt < nk; ++kt) {
-    if (tid == 0) {
-      const int nxt = kt + PF;
-      if (nxt < nk) {
-        if (nxt >= S) qt::mbar_wait_parity(&empty[sn], (unsigned)((phn - 1) & 1));
-        tma_stage<LPRE>(t, smem + sn * STAGE, smem + sn * STAGE + LOFF, i0, j0, kbeg + (int64_t)nxt * BK, &full[sn]);
-      }
-      if (++sn == S) { sn = 0; ++phn; }
-    }
-    __syncwarp();  // warp 0 reconverges before its DMMAs (mma.sync is .aligned)
     qt::mbar_wait_parity(&full[s], (unsigned)(ph & 1));
     const double* Ls = smem + s * STAGE;
     if (NRB > 0 && NCB > 0)
@@ -419,6 +431,11 @@ template <bool LPRE>
 __device__ __forceinline__ void mma_tile_tma(const TmaOps& t, const Operands& g, double* smem, int64_t i0, int64_t j0,
                                              int64_t kbeg, int64_t kend, Acc& acc) {
   __shared__ __align__(8) uint64_t full[MAX_STAGES], empty[MAX_STAGES];
+  tma_init<LPRE>(t, full, empty);
+  if ((threadIdx.x >> 5) == NT / 32) {
+    tma_producer<LPRE>(t, smem, i0, j0, kbeg, kend, full, empty);
+    return;
+  }
   QT8_DISPATCH(mma_loop_tma, t, smem, i0, j0, kbeg, kend, acc, full, empty)
 }
 #undef QT8_DISPATCH
@@ -430,6 +447,10 @@ __device__ __forceinline__ void mma_tile_tma(const TmaOps& t, const Operands& g,
 // warps (read with other_product), nullptr for the half-1 warps.
 __device__ __forceinline__ const double* exchange_products(const Acc& acc, double* xbuf) {
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (w >= NT / 32) {  // the TMA producer warp holds no products
+    __syncthreads();
+    return nullptr;
+  }
   double* slot = xbuf + (w & 7) * 32 * 32 + lane;
   if (warp_half(w) == 1) {
 #pragma unroll

@@ -138,7 +138,7 @@ struct Fused8Args {
   // TMA maps (sketch8_kernel<true>): Y left = A panel, Y right = Omega~,
   // W left = Psi~ panel, W right = A panel (3D: inner, rows, planes)
   CUtensorMap ylm, yrm, wlm, wrm;
-  int stages, pf;  // TMA ring slots / prefetch distance
+  int stages;  // TMA ring slots
   qt8::Operands yop;  // A_panel (k-fast) x Omega~ (8 planes, j-fast): M = panel rows, N = s, K = n
   qt8::Operands wop;  // Psi~_panel (8 planes, k-fast) x A_panel (j-fast): M = l, N = n, K = panel rows
   int64_t ky, kw;
@@ -198,7 +198,7 @@ __device__ __forceinline__ void store_tile8(const qt8::Acc& acc, double* xbuf, i
 // Task order as sketch_fused_kernel: full W tiles, full Y tiles, padded Y
 // column tiles, padded W row tiles.
 template <bool TMA>
-__global__ void __launch_bounds__(qt8::NT, 1) sketch8_kernel(const __grid_constant__ Fused8Args f) {
+__global__ void __launch_bounds__(TMA ? qt8::NT_TMA : qt8::NT, 1) sketch8_kernel(const __grid_constant__ Fused8Args f) {
   extern __shared__ __align__(128) double smem_raw[];
   // TMA destinations need 128-byte alignment (the launch adds the slack)
   // (offset arithmetic on the shared array keeps the accesses LDS, not generic)
@@ -232,7 +232,7 @@ __global__ void __launch_bounds__(qt8::NT, 1) sketch8_kernel(const __grid_consta
     qt8::zero_acc(acc);
     const int64_t kb = (int64_t)z * f.ky_chunk, ke = min(f.ky, kb + f.ky_chunk);
     if (TMA)
-      qt8::mma_tile_tma<false>(qt8::TmaOps{&f.ylm, &f.yrm, 0, f.stages, f.pf}, f.yop, smem, (int64_t)tm * Y8M, (int64_t)tn * Y8N, kb,
+      qt8::mma_tile_tma<false>(qt8::TmaOps{&f.ylm, &f.yrm, 0, f.stages}, f.yop, smem, (int64_t)tm * Y8M, (int64_t)tn * Y8N, kb,
                                ke, acc);
     else
       qt8::mma_tile<false>(f.yop, smem, (int64_t)tm * Y8M, (int64_t)tn * Y8N, kb, ke, acc);
@@ -243,7 +243,7 @@ __global__ void __launch_bounds__(qt8::NT, 1) sketch8_kernel(const __grid_consta
     qt8::zero_acc(acc);
     const int64_t kb = (int64_t)z * f.kw_chunk, ke = min(f.kw, kb + f.kw_chunk);
     if (TMA)
-      qt8::mma_tile_tma<true>(qt8::TmaOps{&f.wlm, &f.wrm, 0, f.stages, f.pf}, f.wop, smem, (int64_t)tm * W8M, (int64_t)tn * W8N, kb,
+      qt8::mma_tile_tma<true>(qt8::TmaOps{&f.wlm, &f.wrm, 0, f.stages}, f.wop, smem, (int64_t)tm * W8M, (int64_t)tn * W8N, kb,
                               ke, acc);
     else
       qt8::mma_tile<true>(f.wop, smem, (int64_t)tm * W8M, (int64_t)tn * W8N, kb, ke, acc);
@@ -430,20 +430,12 @@ bool tma_layout(const QView& a, int64_t* pstride) {
   *pstride = d;
   return true;
 }
-// TMA ring: slots and prefetch distance (QLRA_Q8_STAGES / QLRA_Q8_PF override)
+// TMA ring slots (QLRA_Q8_STAGES overrides; the producer warp refills a slot as soon as it is released)
 int tma_stages() {
   static const int v = [] {
     const char* e = std::getenv("QLRA_Q8_STAGES");
-    const int s = e ? std::atoi(e) : 5;
+    const int s = e ? std::atoi(e) : 4;
     return std::max(2, std::min(s, std::min(qt8::MAX_STAGES, (int)((227 * 1024 - 256) / (qt8::STAGE * sizeof(double))))));
-  }();
-  return v;
-}
-int tma_prefetch() {
-  static const int v = [] {
-    const char* e = std::getenv("QLRA_Q8_PF");
-    const int p = e ? std::atoi(e) : 3;
-    return std::max(1, std::min(p, tma_stages() - 1));
   }();
   return v;
 }
@@ -573,10 +565,9 @@ void launch8(Ctx& ctx, const Q8Part* y, const Q8Part* w, double alpha, double be
           make_map3(&f.wlm, w->comb + w->col0, rp, l, 8, w->comb_ld, l * w->comb_ld, qt8::LDK, W8M, 8) &&
           make_map3(&f.wrm, w->a.p[0], n, rp, 4, w->a.ld, wps, qt8::Layout<true>::LDX, qt8::BK, 4);
   f.stages = tma_stages();
-  f.pf = tma_prefetch();
   LaunchTimer lt(ctx, timed);
   if (tma)
-    sketch8_kernel<true><<<(unsigned)ctas, qt8::NT, (size_t)f.stages * qt8::STAGE * sizeof(double) + 128,
+    sketch8_kernel<true><<<(unsigned)ctas, qt8::NT_TMA, (size_t)f.stages * qt8::STAGE * sizeof(double) + 128,
                            ctx.stream>>>(f);
   else
     sketch8_kernel<false><<<(unsigned)ctas, qt8::NT, qt8::SMEM_BYTES + 128, ctx.stream>>>(f);
