@@ -341,7 +341,7 @@ __device__ __forceinline__ void tma_stage(const TmaOps& t, double* Ls, double* R
 }
 
 // The ring fed by a dedicated producer warp (warp 16, one elected lane):
-// it issues stage k + PF once every compute warp has released the slot's
+// it issues stage k as soon as every compute warp has released the slot's
 // previous stage; the 16 compute warps only wait for data.
 template <bool LPRE>
 __device__ __forceinline__ void tma_init(const TmaOps& t, uint64_t* full, uint64_t* empty) {

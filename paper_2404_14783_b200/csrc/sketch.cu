@@ -791,6 +791,16 @@ void sketch_update_rows(Ctx& ctx, const qlra_spec_t& omega, const qlra_spec_t& p
                         const QView& block, const QView& y_rows, const QView& w) {
   const int64_t b = block.rows, n = block.cols, s = omega.cols;
   if (b == 0 || n == 0) return;
+  int64_t pstride = 0;
+  if (sketch_use8() && sketch_tma_enabled() && !tma_layout(block, &pstride) && n >= 1024) {
+    // A's rows are not 16-byte aligned (n odd, e.g. C4's 27125): stream the
+    // block through even-pitched staging buffers (device-to-device copies
+    // overlapped with the sketch of the previous chunk) so the TMA path
+    // applies (C4: the staged copies overlap the previous panel's sketch;
+    // sketch 693 ms against 723 ms on the cp.async path)
+    sketch_update_rows_host(ctx, omega, psi, row0, block, y_rows, w, 0, true);
+    return;
+  }
   set_kernel_attrs();
   DevQMat om(ctx, n, s), ps_tmp;
   launch_gen(ctx.stream, omega, 0, 0, n, s, om.v, false);
@@ -809,17 +819,33 @@ void sketch_update_rows(Ctx& ctx, const qlra_spec_t& omega, const qlra_spec_t& p
 // Streaming ingestion (sketch_from_source, sketching.cpp:156-167, with the
 // source in host memory): row panels are copied H2D on a dedicated stream into
 // a double buffer while the previous panel is sketched, so the PCIe transfer
-// of A overlaps the FP64 work.  A is still read exactly once.
+// of A overlaps the FP64 work.  A is still read exactly once.  (Also the
+// relayout path for a device-resident A whose rows are not 16-byte aligned:
+// the copies are then device-to-device.)
 void sketch_update_rows_host(Ctx& ctx, const qlra_spec_t& omega, const qlra_spec_t& psi,
                              int64_t row0, const QView& host_block, const QView& y_rows,
-                             const QView& w, int64_t block_rows) {
+                             const QView& w, int64_t block_rows, bool relayout) {
   const int64_t b = host_block.rows, n = host_block.cols, s = omega.cols;
   if (b == 0 || n == 0) return;
   set_kernel_attrs();
-  int64_t R = block_rows > 0 ? block_rows : stream_rows(n, b);
+  // (relayout of a device-resident A: panel-sized chunks, no short tail --
+  // a device-to-device copy never bounds the pipeline)
+  int64_t R = block_rows > 0 ? block_rows : relayout ? panel_rows(n, b) : stream_rows(n, b);
   R = std::min(R, b);
   DevQMat om(ctx, n, s), ps_tmp;
-  DevQMat buf[2] = {DevQMat(ctx, R, n), DevQMat(ctx, R, n)};
+  // Staging buffers with an even leading dimension: the H2D copy lands A in
+  // the layout the TMA path needs (16-byte rows) even when n is odd (C4's
+  // 27125), at the cost of a pitched copy -- fine for wide rows.
+  const int64_t ldb = (n % 2 == 0 || n < 1024) ? n : n + 1;
+  DeviceBuffer bufmem[2] = {DeviceBuffer(ctx, (size_t)4 * R * ldb * sizeof(double)),
+                            DeviceBuffer(ctx, (size_t)4 * R * ldb * sizeof(double))};
+  QView buf[2];
+  for (int i = 0; i < 2; ++i) {
+    for (int p = 0; p < 4; ++p) buf[i].p[p] = bufmem[i].as<double>() + (size_t)p * R * ldb;
+    buf[i].rows = R;
+    buf[i].cols = n;
+    buf[i].ld = ldb;
+  }
   cudaStream_t cs;
   QLRA_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
   cudaEvent_t copied[2], freed[2];
@@ -841,23 +867,23 @@ void sketch_update_rows_host(Ctx& ctx, const qlra_spec_t& omega, const qlra_spec
   // The last R rows go in quarter-size chunks: the sketch of the final chunk
   // is the one part of the pipeline nothing overlaps (the copy stream is the
   // bottleneck before it), so it should be short.
-  const int64_t tail_start = b > 2 * R ? b - R : b;
+  const int64_t tail_start = !relayout && b > 2 * R ? b - R : b;
   const int64_t Rt = std::max<int64_t>(64, ((R / 4 + 63) / 64) * 64);
   int idx = 0;
   for (int64_t r0 = 0, rp = 0; r0 < b; r0 += rp, idx ^= 1) {
     rp = std::min(r0 >= tail_start ? Rt : std::min(R, tail_start - r0), b - r0);
-    const QView dst = sub(buf[idx].v, 0, 0, rp, n);
+    const QView dst = sub(buf[idx], 0, 0, rp, n);
     QLRA_CUDA(cudaStreamWaitEvent(cs, freed[idx], 0));
     for (int p = 0; p < 4; ++p) {
       const double* src = host_block.p[p] + r0 * host_block.ld;
       if (host_block.ld == n && dst.ld == n) {
         // contiguous rows: one linear DMA (2D copies of narrow rows, e.g.
         // C5's 2400-byte rows, run far below PCIe bandwidth)
-        QLRA_CUDA(cudaMemcpyAsync(dst.p[p], src, sizeof(double) * (size_t)(rp * n), cudaMemcpyHostToDevice, cs));
+        QLRA_CUDA(cudaMemcpyAsync(dst.p[p], src, sizeof(double) * (size_t)(rp * n), cudaMemcpyDefault, cs));
       } else {
         QLRA_CUDA(cudaMemcpy2DAsync(dst.p[p], (size_t)dst.ld * sizeof(double), src,
                                     (size_t)host_block.ld * sizeof(double), (size_t)n * sizeof(double),
-                                    (size_t)rp, cudaMemcpyHostToDevice, cs));
+                                    (size_t)rp, cudaMemcpyDefault, cs));
       }
     }
     QLRA_CUDA(cudaEventRecord(copied[idx], cs));
