@@ -833,6 +833,7 @@ void sketch_update_rows_host(Ctx& ctx, const qlra_spec_t& omega, const qlra_spec
   int64_t R = block_rows > 0 ? block_rows : relayout ? panel_rows(n, b) : stream_rows(n, b);
   R = std::min(R, b);
   DevQMat om(ctx, n, s), ps_tmp;
+  const cudaMemcpyKind kind = relayout ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
   // Staging buffers with an even leading dimension: the H2D copy lands A in
   // the layout the TMA path needs (16-byte rows) even when n is odd (C4's
   // 27125), at the cost of a pitched copy -- fine for wide rows.
@@ -879,11 +880,11 @@ void sketch_update_rows_host(Ctx& ctx, const qlra_spec_t& omega, const qlra_spec
       if (host_block.ld == n && dst.ld == n) {
         // contiguous rows: one linear DMA (2D copies of narrow rows, e.g.
         // C5's 2400-byte rows, run far below PCIe bandwidth)
-        QLRA_CUDA(cudaMemcpyAsync(dst.p[p], src, sizeof(double) * (size_t)(rp * n), cudaMemcpyDefault, cs));
+        QLRA_CUDA(cudaMemcpyAsync(dst.p[p], src, sizeof(double) * (size_t)(rp * n), kind, cs));
       } else {
         QLRA_CUDA(cudaMemcpy2DAsync(dst.p[p], (size_t)dst.ld * sizeof(double), src,
                                     (size_t)host_block.ld * sizeof(double), (size_t)n * sizeof(double),
-                                    (size_t)rp, cudaMemcpyDefault, cs));
+                                    (size_t)rp, kind, cs));
       }
     }
     QLRA_CUDA(cudaEventRecord(copied[idx], cs));
