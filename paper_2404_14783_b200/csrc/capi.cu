@@ -702,8 +702,10 @@ void early_solve_start(Ctx& c, EarlySolve& es, const DeferredQ& q0) {
   {
     StreamSwap on(c, c.side2);
     DevQMat ps_tmp, pb(c, l, s), p0(c, l, s);
-    const QView ps = psi_for_solve(c, *es.psi, es.row0, rows, ps_tmp);
-    qgemm(c, QLRA_OP_N, QLRA_OP_N, 1.0, ps, q0.base.v, 0.0, pb.v);
+    if (!psi8_gemm(c, *es.psi, es.row0, q0.base.v, pb.v)) {
+      const QView ps = psi_for_solve(c, *es.psi, es.row0, rows, ps_tmp);
+      qgemm(c, QLRA_OP_N, QLRA_OP_N, 1.0, ps, q0.base.v, 0.0, pb.v);
+    }
     qgemm(c, QLRA_OP_N, QLRA_OP_N, 1.0, pb.v, q0.rinv_last.v, 0.0, p0.v);
     cqr2_enqueue(c, p0.v, QView{}, /*complex_mode=*/false, /*distributed=*/false, nullptr, /*form_q=*/false,
                  es.cqr);
@@ -1057,9 +1059,11 @@ void pseudo_svd_dev(Ctx& c, const QView& Y, const QView& H, uint64_t seed, qlra_
 DevQMat qb_solve_operator(Ctx& c, const qlra_spec_t& psi, int64_t row0, const QView& H) {
   const int64_t s = H.cols, l = psi.rows;
   DevQMat ps_tmp;
-  const QView ps = psi_for_solve(c, psi, row0, H.rows, ps_tmp);
   DevQMat p(c, l, s);
-  qgemm(c, QLRA_OP_N, QLRA_OP_N, 1.0, ps, H, 0.0, p.v);
+  if (!psi8_gemm(c, psi, row0, H, p.v)) {
+    const QView ps = psi_for_solve(c, psi, row0, H.rows, ps_tmp);
+    qgemm(c, QLRA_OP_N, QLRA_OP_N, 1.0, ps, H, 0.0, p.v);
+  }
   allreduce_qmat(c, p.v);
   return lstsq_operator(c, p.v);
 }

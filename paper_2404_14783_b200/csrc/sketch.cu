@@ -630,7 +630,8 @@ void launch_combine8(Ctx& ctx, const QView& in, double* out, int64_t ld, bool le
 
 // Fill e.om8 / e.ps8 (when the 8-product engine is on) into the context's
 // kept combination buffer.
-void prepare_emb(Ctx& ctx, Emb& e) {
+void prepare_emb(Ctx& ctx, Emb& e, const qlra_spec_t& psi, int64_t row0) {
+  ctx.comb_keep.psi_valid = false;
   if (!sketch_use8()) return;
   e.om8_ld = (e.om.cols + 1) / 2 * 2;
   e.ps8_ld = (e.ps.cols + 1) / 2 * 2;
@@ -649,6 +650,12 @@ void prepare_emb(Ctx& ctx, Emb& e) {
   launch_combine8(ctx, e.ps, base + no, e.ps8_ld, true);
   e.om8 = base;
   e.ps8 = base + no;
+  k.psi_valid = true;
+  k.psi = psi;
+  k.row0 = row0;
+  k.rows = e.ps.cols;
+  k.ps8 = e.ps8;
+  k.ps8_ld = e.ps8_ld;
 }
 
 void set_kernel_attrs() {
@@ -779,6 +786,18 @@ QView psi_for_solve(Ctx& ctx, const qlra_spec_t& psi, int64_t row0, int64_t rows
   return tmp.v;
 }
 
+bool psi8_gemm(Ctx& ctx, const qlra_spec_t& psi, int64_t row0, const QView& B, const QView& C) {
+  const Ctx::CombKeep& k = ctx.comb_keep;
+  if (!k.psi_valid || !same_spec(k.psi, psi) || k.row0 != row0 || k.rows != B.rows || C.rows != psi.rows ||
+      C.cols != B.cols || B.rows == 0 || B.cols == 0)
+    return false;
+  set_kernel_attrs();
+  SketchWork ws;
+  const Q8Part w{B, k.ps8, k.ps8_ld, 0, C};
+  launch8(ctx, nullptr, &w, 1.0, 0.0, ws, false);
+  return true;
+}
+
 void psi_keep_release(Ctx& ctx) {
   Ctx::PsiKeep& k = ctx.psi_keep;
   if (k.buf) cudaFreeAsync(k.buf, ctx.stream);
@@ -807,7 +826,7 @@ void sketch_update_rows(Ctx& ctx, const qlra_spec_t& omega, const qlra_spec_t& p
   Emb e;
   e.om = om.v;
   e.ps = psi_for_sketch(ctx, psi, row0, b, ps_tmp);
-  prepare_emb(ctx, e);
+  prepare_emb(ctx, e, psi, row0);
   const int64_t R = panel_rows(n, b);
   SketchWork ws;
   for (int64_t r0 = 0; r0 < b; r0 += R) {
@@ -863,7 +882,7 @@ void sketch_update_rows_host(Ctx& ctx, const qlra_spec_t& omega, const qlra_spec
   Emb e;
   e.om = om.v;
   e.ps = psi_for_sketch(ctx, psi, row0, b, ps_tmp);
-  prepare_emb(ctx, e);
+  prepare_emb(ctx, e, psi, row0);
   SketchWork ws;
   // The last R rows go in quarter-size chunks: the sketch of the final chunk
   // is the one part of the pipeline nothing overlaps (the copy stream is the
