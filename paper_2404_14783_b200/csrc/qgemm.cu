@@ -529,10 +529,9 @@ void qgemm_ex(Ctx& ctx, int op_a, int op_b, double alpha, const QView& A, const 
     small_gemm(ctx, op_a == QLRA_OP_C, op_b == QLRA_OP_C, g, M, N, K, C);
     return;
   }
-  // tall x small / small x tall products (no adjoint): 8 real products per
-  // quaternion MAC instead of 16 (qtile8.cuh)
-  if (force_splits <= 0 && !herm && op_a == QLRA_OP_N && op_b == QLRA_OP_N && q8gemm_try(ctx, alpha, A, B, beta, C))
-    return;
+  // tall x small / small x tall products (an adjoint only on the small
+  // factor): 8 real products per quaternion MAC instead of 16 (qtile8.cuh)
+  if (force_splits <= 0 && !herm && q8gemm_try(ctx, op_a, op_b, alpha, A, B, beta, C)) return;
   int64_t nsplit = 1;
   if (force_splits > 0) {
     nsplit = force_splits;

@@ -254,13 +254,17 @@ __global__ void __launch_bounds__(TMA ? qt8::NT_TMA : qt8::NT, 1) sketch8_kernel
 
 // out plane i (rows x cols, ld = cols) = combination i of in's planes, the
 // left (Psi) or right (Omega) set, halves folded into i >= 4
-__global__ void combine8_kernel(QView in, double* out, int64_t ld, int left) {
-  const int64_t rows = in.rows, cols = in.cols, total = rows * cols;
+__global__ void combine8_kernel(QView in, double* out, int64_t ld, int left, int adj) {
+  // adj: combine op(in) = in^* (rows x cols of the adjoint)
+  const int64_t rows = adj ? in.cols : in.rows, cols = adj ? in.rows : in.cols, total = rows * cols;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = e / cols, j = e % cols;
     double v[4];
 #pragma unroll
-    for (int p = 0; p < 4; ++p) v[p] = in.p[p][i * in.ld + j];
+    for (int p = 0; p < 4; ++p) {
+      const double x = adj ? in.p[p][j * in.ld + i] : in.p[p][i * in.ld + j];
+      v[p] = adj && p > 0 ? -x : x;
+    }
 #pragma unroll
     for (int c = 0; c < 8; ++c) {
       const double x = left ? qt8::lcomb(c, v) : qt8::rcomb(c, v);
@@ -618,12 +622,12 @@ void sketch_panel(Ctx& ctx, const Emb& e, int64_t pc0, const QView& ap, const QV
 }
 
 // Plane combinations of an embedding for the 8-product engine.
-void launch_combine8(Ctx& ctx, const QView& in, double* out, int64_t ld, bool left) {
+void launch_combine8(Ctx& ctx, const QView& in, double* out, int64_t ld, bool left, bool adj = false) {
   const int64_t total = in.rows * in.cols;
   if (total == 0) return;
   const int threads = 256;
   const int64_t blocks = std::min<int64_t>((total + threads - 1) / threads, 148 * 16);
-  combine8_kernel<<<(unsigned)blocks, threads, 0, ctx.stream>>>(in, out, ld, left ? 1 : 0);
+  combine8_kernel<<<(unsigned)blocks, threads, 0, ctx.stream>>>(in, out, ld, left ? 1 : 0, adj ? 1 : 0);
   QLRA_LAUNCH_CHECK();
   count_launch();
 }
@@ -723,22 +727,30 @@ bool same_spec(const qlra_spec_t& a, const qlra_spec_t& b) {
 // planes (one pass over it), the large one streams through the kernel as
 // the sketch's A does.  Returns false (nothing launched) when the shapes do
 // not fit that pattern; the caller then runs the 16-product qgemm.
-bool q8gemm_try(Ctx& ctx, double alpha, const QView& A, const QView& B, double beta, const QView& C) {
+bool q8gemm_try(Ctx& ctx, int op_a, int op_b, double alpha, const QView& A, const QView& B, double beta,
+                const QView& C) {
   static const bool enabled = [] {
     const char* e = std::getenv("QLRA_Q8GEMM");
     return !(e && std::atoi(e) == 0);
   }();
   if (!enabled || !sketch_use8()) return false;
-  const int64_t M = A.rows, K = A.cols, N = B.cols;
-  if (B.rows != K || C.rows != M || C.cols != N || M == 0 || N == 0 || K == 0) return false;
+  const bool ca = op_a == QLRA_OP_C, cb = op_b == QLRA_OP_C;
+  if (ca && cb) return false;
+  const int64_t M = ca ? A.cols : A.rows, K = ca ? A.rows : A.cols;
+  const int64_t Kb = cb ? B.cols : B.rows, N = cb ? B.rows : B.cols;
+  if (Kb != K || C.rows != M || C.cols != N || M == 0 || N == 0 || K == 0) return false;
   const double a_el = (double)M * (double)K, b_el = (double)K * (double)N;
-  const bool right = b_el * 4.0 <= a_el, left = !right && a_el * 4.0 <= b_el;
+  // the combined (small) factor may be an adjoint -- it is materialised by
+  // the combine pass; the streamed (large) factor must be plain
+  const bool right = !ca && b_el * 4.0 <= a_el, left = !right && !cb && a_el * 4.0 <= b_el;
   if (!right && !left) return false;
   set_kernel_attrs();
   const QView& small = right ? B : A;
-  const int64_t ld = (small.cols + 1) / 2 * 2;
-  DeviceBuffer comb(ctx, (size_t)8 * small.rows * ld * sizeof(double));
-  launch_combine8(ctx, small, comb.as<double>(), ld, left);
+  const bool adj = right ? cb : ca;
+  const int64_t srows = adj ? small.cols : small.rows, scols = adj ? small.rows : small.cols;
+  const int64_t ld = (scols + 1) / 2 * 2;
+  DeviceBuffer comb(ctx, (size_t)8 * srows * ld * sizeof(double));
+  launch_combine8(ctx, small, comb.as<double>(), ld, left, adj);
   SketchWork ws;
   if (right) {
     const Q8Part y{A, comb.as<double>(), ld, 0, C};

@@ -66,7 +66,10 @@ def test_qmat_mul_adjoint_ops(ctx):
 
 
 @pytest.mark.parametrize("m,k,n", [(100, 100, 100), (100, 200, 100), (36, 64, 64), (16, 5000, 16),
-                                   (300, 1000, 100)])
+                                   (300, 1000, 100),
+                                   # tall x small / small x wide: the 8-product engine (qtile8.cuh) with the
+                                   # small factor (or its adjoint) combined once, alpha / beta in its epilogue
+                                   (3000, 40, 37), (40, 500, 3000), (2000, 64, 130)])
 @pytest.mark.parametrize("op_a,op_b", [(0, 0), (1, 0), (0, 1), (1, 1)])
 def test_qmat_mul_small_and_split_paths(ctx, m, k, n, op_a, op_b):
     """Both product paths (16x16-tile split-K with in-kernel ordered
