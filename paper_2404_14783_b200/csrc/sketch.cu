@@ -209,23 +209,28 @@ __global__ void __launch_bounds__(TMA ? qt8::NT_TMA : qt8::NT, 1) sketch8_kernel
   int t = blockIdx.x;
   bool is_w;
   int tm, tn, z;
+  // L2-aware order (groups still longest first: full W, Y, padded W):
+  // W CTAs sharing a K chunk are adjacent -- the l-row tiles of an A column
+  // tile read the same A rows, the n-column tiles of a Psi~ row tile the
+  // same Psi~ columns -- and the column tiles of a Y row tile (full and
+  // padded) are adjacent, so each A row tile comes from DRAM once.  (C5,
+  // n = 300, s = 40: the old order re-read A and Psi~ ~7x per launch.)
+  const int wtf = f.w_tmf * f.w_tn, wtp = (f.w_tm - f.w_tmf) * f.w_tn;
   if (t < nwf) {
     is_w = true;
-    z = t % f.zw; t /= f.zw;
-    tm = t % f.w_tmf; tn = t / f.w_tmf;
-  } else if ((t -= nwf) < nyf) {
+    const int tile = t % wtf;
+    z = t / wtf;
+    tm = tile % f.w_tmf; tn = tile / f.w_tmf;
+  } else if ((t -= nwf) < nyf + nyp) {
     is_w = false;
     z = t % f.zy; t /= f.zy;
-    tn = t % f.y_tnf; tm = t / f.y_tnf;
-  } else if ((t -= nyf) < nyp) {
-    is_w = false;
-    z = t % f.zy; t /= f.zy;
-    tn = f.y_tnf + t % (f.y_tn - f.y_tnf); tm = t / (f.y_tn - f.y_tnf);
+    tn = t % f.y_tn; tm = t / f.y_tn;
   } else {
-    t -= nyp;
+    t -= nyf + nyp;
     is_w = true;
-    z = t % f.zw; t /= f.zw;
-    tm = f.w_tmf + t % (f.w_tm - f.w_tmf); tn = t / (f.w_tm - f.w_tmf);
+    const int tile = t % wtp;
+    z = t / wtp;
+    tm = f.w_tmf + tile % (f.w_tm - f.w_tmf); tn = tile / (f.w_tm - f.w_tmf);
   }
   if (!is_w) {
     qt8::Acc acc;
