@@ -57,36 +57,48 @@ constexpr int NT = 512, BK = 8, STAGES = 4;
 constexpr int NT_TMA = NT + 32;
 constexpr int LDK = BK + 4;  // k-fast rows, pitch 12 (4 mod 16: conflict-free fragments)
 
-template <bool LPRE>
-struct Cfg;
-template <>
-struct Cfg<false> {  // Y task: left operand A (on the fly), right Omega~ (combined); 4 x 2 positions
-  static constexpr int TM = 64, TN = 32, WRB = 2, WCB = 2, LP = 4, RP = 8;
-};
-template <>
-struct Cfg<true> {  // W task: left Psi~ (combined), right operand A (on the fly); 2 x 4 positions
-  static constexpr int TM = 32, TN = 64, WRB = 2, WCB = 2, LP = 8, RP = 4;
+// Tile configurations (MODE): 8 positions of 16x16 outputs as PR x PC.
+//   0 Y : 64 x 32, left A on the fly (k-fast), right Omega~ (8 planes)
+//   1 W : 32 x 64, left Psi~ (8 planes), right A on the fly (j-fast)
+//   2 YN: 128 x 16, as Y -- the last Y column tile when s % 32 <= 16
+//   3 WN: 16 x 128, as W -- the last W row tile when l % 32 <= 16
+// The narrow modes keep all 16 warps busy on a remainder that would leave
+// half of a regular tile's warps without a valid 8x8 block.
+template <int MODE>
+struct Cfg {
+  static constexpr bool LPRE = (MODE & 1) != 0;
+  static constexpr int PR = MODE == 0 ? 4 : MODE == 1 ? 2 : MODE == 2 ? 8 : 1;
+  static constexpr int PC = 8 / PR;
+  static constexpr int TM = 16 * PR, TN = 16 * PC, WRB = 2, WCB = 2;
+  static constexpr int LP = LPRE ? 8 : 4, RP = LPRE ? 4 : 8;
 };
 // Warp w issues on SMSP w % 4.  The position index runs fastest along the
 // long side of the position grid, so the warps of a tile padded along the
-// short side (Y: s % 32, W: l % 32 valid columns / rows) still cover all
-// four SMSPs (two warps each: both product halves).
-template <bool LPRE>
-__device__ __forceinline__ int warp_row(int w) { return LPRE ? (w & 7) >> 2 : w & 3; }
-template <bool LPRE>
-__device__ __forceinline__ int warp_col(int w) { return LPRE ? w & 3 : (w & 7) >> 2; }
+// short side still cover all four SMSPs (two warps each: both product halves).
+template <int MODE>
+__device__ __forceinline__ int warp_row(int w) {
+  using C = Cfg<MODE>;
+  return C::PR >= C::PC ? (w & 7) % C::PR : (w & 7) / C::PC;
+}
+template <int MODE>
+__device__ __forceinline__ int warp_col(int w) {
+  using C = Cfg<MODE>;
+  return C::PR >= C::PC ? (w & 7) / C::PR : (w & 7) % C::PC;
+}
 __device__ __forceinline__ int warp_half(int w) { return w >> 3; }
 
-template <bool LPRE>
+template <int MODE>
 struct Layout {
-  using C = Cfg<LPRE>;
-  static constexpr int LDX = C::TN + 4;  // j-fast rows: 36 / 68 (4 mod 16)
+  using C = Cfg<MODE>;
+  static constexpr int LDX = C::TN + 4;  // j-fast rows: 36 / 68 / 20 / 132 (4 mod 16)
   static constexpr int L_ELEMS = C::LP * C::TM * LDK;
   static constexpr int R_ELEMS = C::RP * BK * LDX;
+  static constexpr int ELEMS = L_ELEMS + R_ELEMS;
 };
-constexpr int STAGE = (Layout<false>::L_ELEMS + Layout<false>::R_ELEMS) > (Layout<true>::L_ELEMS + Layout<true>::R_ELEMS)
-                          ? (Layout<false>::L_ELEMS + Layout<false>::R_ELEMS)
-                          : (Layout<true>::L_ELEMS + Layout<true>::R_ELEMS);
+constexpr int cmax(int a, int b) { return a > b ? a : b; }
+// stage stride of the cp.async path (regular modes only) and of the TMA path
+constexpr int STAGE = cmax(Layout<0>::ELEMS, Layout<1>::ELEMS);
+constexpr int STAGE_TMA = cmax(STAGE, cmax(Layout<2>::ELEMS, Layout<3>::ELEMS));
 constexpr size_t SMEM_BYTES = (size_t)STAGES * STAGE * sizeof(double);
 
 // op(L)(i, k) = l[q][i * l_si + k];  op(R)(k, j) = r[q][k * r_sk + j]
@@ -146,25 +158,25 @@ __device__ __forceinline__ void combine(const double (&m)[8], double (&c)[4]) {
   c[3] = m[3] + (m[4] - m[5]) - d78;
 }
 
-template <bool LPRE>
+template <int MODE>
 __device__ __forceinline__ int acc_row(int rb) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  return 16 * warp_row<LPRE>(w) + 8 * rb + (lane >> 2);
+  return 16 * warp_row<MODE>(w) + 8 * rb + (lane >> 2);
 }
-template <bool LPRE>
+template <int MODE>
 __device__ __forceinline__ int acc_col(int cb) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  return 16 * warp_col<LPRE>(w) + 8 * cb + 2 * (lane & 3);
+  return 16 * warp_col<MODE>(w) + 8 * cb + 2 * (lane & 3);
 }
 
 // Per-thread copy plan of one tile, fixed for the whole k loop: each thread
 // copies the same (row, k) / (k, col) position of LP / RP planes every stage,
 // so a stage costs a pointer add per operand and the k bound test (the
 // general address arithmetic once per tile, not once per element per stage).
-template <bool LPRE>
+template <int MODE>
 struct Loader {
-  using C = Cfg<LPRE>;
-  using Lay = Layout<LPRE>;
+  using C = Cfg<MODE>;
+  using Lay = Layout<MODE>;
   static constexpr int LPER = C::TM * BK, RPER = BK * C::TN;  // elements per plane per stage
   static constexpr int LSPLIT = NT / LPER, RSPLIT = NT / RPER;   // thread groups per copy round
   static_assert(NT % LPER == 0 && NT % RPER == 0, "copy plan");
@@ -209,15 +221,15 @@ struct Loader {
 // One BK slice: products 4*HALF .. 4*HALF+3 for the warp's first NRB row and
 // NCB column blocks.  Per k4 step all fragments are loaded and the warp's 4
 // combinations formed before its 4*NRB*NCB DMMAs.
-template <bool LPRE, int HALF, int NRB, int NCB>
+template <int MODE, int HALF, int NRB, int NCB>
 __device__ __forceinline__ void kstep(const double* Ls, const double* Rs, int wr, int wc, int gid, int tig, Acc& acc) {
-  using C = Cfg<LPRE>;
-  constexpr int LDX = Layout<LPRE>::LDX;
+  using C = Cfg<MODE>;
+  constexpr int LDX = Layout<MODE>::LDX;
 #pragma unroll
   for (int kk = 0; kk < BK / 4; ++kk) {
     const int k = 4 * kk + tig;
     double lv[4][NRB], rv[4][NCB];
-    if (!LPRE) {
+    if (!C::LPRE) {
       // left = A: 4 planes per row block, combined in registers
       double a[NRB][4];
 #pragma unroll
@@ -262,14 +274,14 @@ __device__ __forceinline__ void kstep(const double* Ls, const double* Rs, int wr
 }
 
 // The cp.async ring with mbarrier stage handoff (as qtile.cuh's mma_loop).
-template <bool LPRE, int HALF, int NRB, int NCB>
+template <int MODE, int HALF, int NRB, int NCB>
 __device__ __forceinline__ void mma_loop(const Operands& g, double* smem, int64_t i0, int64_t j0, int64_t kbeg,
                                          int64_t kend, Acc& acc, uint64_t* full, uint64_t* empty) {
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  const int wr = warp_row<LPRE>(w), wc = warp_col<LPRE>(w);
+  const int wr = warp_row<MODE>(w), wc = warp_col<MODE>(w);
   const int gid = lane >> 2, tig = lane & 3;
   const int nk = kend > kbeg ? (int)((kend - kbeg + BK - 1) / BK) : 0;
-  constexpr int LOFF = Layout<LPRE>::L_ELEMS;
+  constexpr int LOFF = Layout<MODE>::L_ELEMS;
   if (tid == 0) {
 #pragma unroll
     for (int s = 0; s < STAGES; ++s) {
@@ -278,7 +290,7 @@ __device__ __forceinline__ void mma_loop(const Operands& g, double* smem, int64_
     }
   }
   __syncthreads();
-  Loader<LPRE> ld(g, i0, j0, kbeg, tid);
+  Loader<MODE> ld(g, i0, j0, kbeg, tid);
   if (nk > 0) {
     ld.stage(g, smem, smem + LOFF, kbeg, kend);
     qt::cp_async_arrive(&full[0]);
@@ -295,7 +307,7 @@ __device__ __forceinline__ void mma_loop(const Operands& g, double* smem, int64_
     qt::mbar_wait_parity(&full[s], (unsigned)((kt / STAGES) & 1));
     const double* Ls = smem + s * STAGE;
     if (NRB > 0 && NCB > 0)
-      kstep<LPRE, HALF, (NRB > 0 ? NRB : 1), (NCB > 0 ? NCB : 1)>(Ls, Ls + LOFF, wr, wc, gid, tig, acc);
+      kstep<MODE, HALF, (NRB > 0 ? NRB : 1), (NCB > 0 ? NCB : 1)>(Ls, Ls + LOFF, wr, wc, gid, tig, acc);
     __syncwarp();
     if (lane == 0) qt::mbar_arrive(&empty[s]);
   }
@@ -319,6 +331,7 @@ struct TmaOps {
   const CUtensorMap* rm;  // right map
   int lk_off;             // inner coordinate offset of the left map's k (Psi~ panel column)
   int stages;             // ring slots (<= MAX_STAGES, smem sized by the launch)
+  int stride;             // doubles per slot (STAGE, or STAGE_TMA when the launch has narrow tiles)
 };
 
 __device__ __forceinline__ void tma_load3(double* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
@@ -331,10 +344,10 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(qt::smem_u32(bar)), "r"(bytes) : "memory");
 }
 
-template <bool LPRE>
+template <int MODE>
 __device__ __forceinline__ void tma_stage(const TmaOps& t, double* Ls, double* Rs, int64_t i0, int64_t j0, int64_t k0,
                                           uint64_t* bar) {
-  constexpr unsigned BYTES = (unsigned)((Layout<LPRE>::L_ELEMS + Layout<LPRE>::R_ELEMS) * sizeof(double));
+  constexpr unsigned BYTES = (unsigned)((Layout<MODE>::L_ELEMS + Layout<MODE>::R_ELEMS) * sizeof(double));
   mbar_expect_tx(bar, BYTES);
   tma_load3(Ls, t.lm, (int)(t.lk_off + k0), (int)i0, bar);
   tma_load3(Rs, t.rm, (int)j0, (int)k0, bar);
@@ -343,7 +356,7 @@ __device__ __forceinline__ void tma_stage(const TmaOps& t, double* Ls, double* R
 // The ring fed by a dedicated producer warp (warp 16, one elected lane):
 // it issues stage k as soon as every compute warp has released the slot's
 // previous stage; the 16 compute warps only wait for data.
-template <bool LPRE>
+template <int MODE>
 __device__ __forceinline__ void tma_init(const TmaOps& t, uint64_t* full, uint64_t* empty) {
   if (threadIdx.x == 0) {
     for (int s = 0; s < t.stages; ++s) {
@@ -355,17 +368,17 @@ __device__ __forceinline__ void tma_init(const TmaOps& t, uint64_t* full, uint64
   __syncthreads();
 }
 
-template <bool LPRE>
+template <int MODE>
 __device__ __forceinline__ void tma_producer(const TmaOps& t, double* smem, int64_t i0, int64_t j0, int64_t kbeg,
                                              int64_t kend, uint64_t* full, uint64_t* empty) {
-  constexpr int LOFF = Layout<LPRE>::L_ELEMS;
+  constexpr int LOFF = Layout<MODE>::L_ELEMS;
   const int nk = kend > kbeg ? (int)((kend - kbeg + BK - 1) / BK) : 0;
   if ((threadIdx.x & 31) == 0) {
     const int S = t.stages;
     int s = 0, ph = 0;
     for (int kt = 0; kt < nk; ++kt) {
       if (kt >= S) qt::mbar_wait_parity(&empty[s], (unsigned)((ph - 1) & 1));
-      tma_stage<LPRE>(t, smem + s * STAGE, smem + s * STAGE + LOFF, i0, j0, kbeg + (int64_t)kt * BK, &full[s]);
+      tma_stage<MODE>(t, smem + s * t.stride, smem + s * t.stride + LOFF, i0, j0, kbeg + (int64_t)kt * BK, &full[s]);
       if (++s == S) { s = 0; ++ph; }
     }
   }
@@ -373,21 +386,21 @@ __device__ __forceinline__ void tma_producer(const TmaOps& t, double* smem, int6
   __syncthreads();  // pairs with the compute warps' closing barrier
 }
 
-template <bool LPRE, int HALF, int NRB, int NCB>
+template <int MODE, int HALF, int NRB, int NCB>
 __device__ __forceinline__ void mma_loop_tma(const TmaOps& t, double* smem, int64_t i0, int64_t j0, int64_t kbeg,
                                              int64_t kend, Acc& acc, uint64_t* full, uint64_t* empty) {
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  const int wr = warp_row<LPRE>(w), wc = warp_col<LPRE>(w);
+  const int wr = warp_row<MODE>(w), wc = warp_col<MODE>(w);
   const int gid = lane >> 2, tig = lane & 3;
   const int nk = kend > kbeg ? (int)((kend - kbeg + BK - 1) / BK) : 0;
-  constexpr int LOFF = Layout<LPRE>::L_ELEMS;
+  constexpr int LOFF = Layout<MODE>::L_ELEMS;
   const int S = t.stages;
   int s = 0, ph = 0;
   for (int kt = 0; kt < nk; ++kt) {
     qt::mbar_wait_parity(&full[s], (unsigned)(ph & 1));
-    const double* Ls = smem + s * STAGE;
+    const double* Ls = smem + s * t.stride;
     if (NRB > 0 && NCB > 0)
-      kstep<LPRE, HALF, (NRB > 0 ? NRB : 1), (NCB > 0 ? NCB : 1)>(Ls, Ls + LOFF, wr, wc, gid, tig, acc);
+      kstep<MODE, HALF, (NRB > 0 ? NRB : 1), (NCB > 0 ? NCB : 1)>(Ls, Ls + LOFF, wr, wc, gid, tig, acc);
     __syncwarp();
     if (lane == 0) qt::mbar_arrive(&empty[s]);
     if (++s == S) { s = 0; ++ph; }
@@ -398,42 +411,42 @@ __device__ __forceinline__ void mma_loop_tma(const TmaOps& t, double* smem, int6
 
 // The warp's loop instance: product half, and the count of its 8x8 row /
 // column blocks inside M x N (blocks past the edge issue no DMMA).
-template <bool LPRE>
+template <int MODE>
 __device__ __forceinline__ int instance(const Operands& g, int64_t i0, int64_t j0) {
   const int w = threadIdx.x >> 5;
-  const int64_t r0w = i0 + 16 * warp_row<LPRE>(w), c0w = j0 + 16 * warp_col<LPRE>(w);
+  const int64_t r0w = i0 + 16 * warp_row<MODE>(w), c0w = j0 + 16 * warp_col<MODE>(w);
   const int nrb = r0w >= g.M ? 0 : (int)min((int64_t)2, (g.M - r0w + 7) / 8);
   const int ncb = c0w >= g.N ? 0 : (int)min((int64_t)2, (g.N - c0w + 7) / 8);
   return (nrb == 0 || ncb == 0) ? 0 : warp_half(w) * 16 + nrb * 4 + ncb;
 }
 
 #define QT8_DISPATCH(LOOP, ...)                                             \
-  switch (instance<LPRE>(g, i0, j0)) {                                      \
-    case 0 * 16 + 2 * 4 + 2: LOOP<LPRE, 0, 2, 2>(__VA_ARGS__); break;       \
-    case 0 * 16 + 2 * 4 + 1: LOOP<LPRE, 0, 2, 1>(__VA_ARGS__); break;       \
-    case 0 * 16 + 1 * 4 + 2: LOOP<LPRE, 0, 1, 2>(__VA_ARGS__); break;       \
-    case 0 * 16 + 1 * 4 + 1: LOOP<LPRE, 0, 1, 1>(__VA_ARGS__); break;       \
-    case 1 * 16 + 2 * 4 + 2: LOOP<LPRE, 1, 2, 2>(__VA_ARGS__); break;       \
-    case 1 * 16 + 2 * 4 + 1: LOOP<LPRE, 1, 2, 1>(__VA_ARGS__); break;       \
-    case 1 * 16 + 1 * 4 + 2: LOOP<LPRE, 1, 1, 2>(__VA_ARGS__); break;       \
-    case 1 * 16 + 1 * 4 + 1: LOOP<LPRE, 1, 1, 1>(__VA_ARGS__); break;       \
-    default: LOOP<LPRE, 0, 0, 0>(__VA_ARGS__); break; /* loads + barriers */ \
+  switch (instance<MODE>(g, i0, j0)) {                                      \
+    case 0 * 16 + 2 * 4 + 2: LOOP<MODE, 0, 2, 2>(__VA_ARGS__); break;       \
+    case 0 * 16 + 2 * 4 + 1: LOOP<MODE, 0, 2, 1>(__VA_ARGS__); break;       \
+    case 0 * 16 + 1 * 4 + 2: LOOP<MODE, 0, 1, 2>(__VA_ARGS__); break;       \
+    case 0 * 16 + 1 * 4 + 1: LOOP<MODE, 0, 1, 1>(__VA_ARGS__); break;       \
+    case 1 * 16 + 2 * 4 + 2: LOOP<MODE, 1, 2, 2>(__VA_ARGS__); break;       \
+    case 1 * 16 + 2 * 4 + 1: LOOP<MODE, 1, 2, 1>(__VA_ARGS__); break;       \
+    case 1 * 16 + 1 * 4 + 2: LOOP<MODE, 1, 1, 2>(__VA_ARGS__); break;       \
+    case 1 * 16 + 1 * 4 + 1: LOOP<MODE, 1, 1, 1>(__VA_ARGS__); break;       \
+    default: LOOP<MODE, 0, 0, 0>(__VA_ARGS__); break; /* loads + barriers */ \
   }
 
 // acc (the warp's 4 products) over k in [kbeg, kend) for the tile at (i0, j0).
-template <bool LPRE>
+template <int MODE>
 __device__ __forceinline__ void mma_tile(const Operands& g, double* smem, int64_t i0, int64_t j0, int64_t kbeg,
                                          int64_t kend, Acc& acc) {
   __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES];
   QT8_DISPATCH(mma_loop, g, smem, i0, j0, kbeg, kend, acc, full, empty)
 }
-template <bool LPRE>
+template <int MODE>
 __device__ __forceinline__ void mma_tile_tma(const TmaOps& t, const Operands& g, double* smem, int64_t i0, int64_t j0,
                                              int64_t kbeg, int64_t kend, Acc& acc) {
   __shared__ __align__(8) uint64_t full[MAX_STAGES], empty[MAX_STAGES];
-  tma_init<LPRE>(t, full, empty);
+  tma_init<MODE>(t, full, empty);
   if ((threadIdx.x >> 5) == NT / 32) {
-    tma_producer<LPRE>(t, smem, i0, j0, kbeg, kend, full, empty);
+    tma_producer<MODE>(t, smem, i0, j0, kbeg, kend, full, empty);
     return;
   }
   QT8_DISPATCH(mma_loop_tma, t, smem, i0, j0, kbeg, kend, acc, full, empty)

@@ -48,6 +48,7 @@ struct FusedArgs {
   int w_tm, w_tn, zw;
   int64_t kw_chunk;
   int y_tnf, w_tmf;  // full (no padding) Y column tiles / W row tiles
+  int yn_t, wn_t;    // (unused: the narrow remainder tiles are 8-product only)
   double* y[4];
   int64_t ldy;
   double* yp;  // [zy][4][My][Ny] partials when zy > 1
@@ -131,14 +132,18 @@ __global__ void __launch_bounds__(NT, 1) sketch_fused_kernel(FusedArgs f) {
 
 // ---- the 8-product path (qtile8.cuh) --------------------------------------
 // Y-tasks: 64x32 tiles of A * Omega~; W-tasks: 32x64 tiles of Psi~ * A.
-constexpr int Y8M = qt8::Cfg<false>::TM, Y8N = qt8::Cfg<false>::TN;
-constexpr int W8M = qt8::Cfg<true>::TM, W8N = qt8::Cfg<true>::TN;
+constexpr int Y8M = qt8::Cfg<0>::TM, Y8N = qt8::Cfg<0>::TN;
+constexpr int W8M = qt8::Cfg<1>::TM, W8N = qt8::Cfg<1>::TN;
+constexpr int YNM = qt8::Cfg<2>::TM, YNN = qt8::Cfg<2>::TN;  // narrow remainder tiles
+constexpr int WNM = qt8::Cfg<3>::TM, WNN = qt8::Cfg<3>::TN;
 
 struct Fused8Args {
   // TMA maps (sketch8_kernel<true>): Y left = A panel, Y right = Omega~,
   // W left = Psi~ panel, W right = A panel (3D: inner, rows, planes)
   CUtensorMap ylm, yrm, wlm, wrm;
-  int stages;  // TMA ring slots
+  CUtensorMap ynlm, ynrm, wnlm, wnrm;  // the narrow remainder tiles (modes 2 / 3)
+  int stages, stride;  // TMA ring slots and doubles per slot
+  int yn_t, wn_t;  // narrow remainder tiles: YN row tiles, WN column tiles (0: none)
   qt8::Operands yop;  // A_panel (k-fast) x Omega~ (8 planes, j-fast): M = panel rows, N = s, K = n
   qt8::Operands wop;  // Psi~_panel (8 planes, k-fast) x A_panel (j-fast): M = l, N = n, K = panel rows
   int64_t ky, kw;
@@ -158,7 +163,7 @@ struct Fused8Args {
 
 // Epilogue: the half-0 warps gather the other half's products (qtile8.cuh),
 // form the quaternion planes and add them to C (or write the split-K partial).
-template <bool LPRE>
+template <int MODE>
 __device__ __forceinline__ void store_tile8(const qt8::Acc& acc, double* xbuf, int64_t i0, int64_t j0, int64_t M,
                                             int64_t N, double* const* c, int64_t ldc, double* part, double alpha,
                                             double beta) {
@@ -166,13 +171,13 @@ __device__ __forceinline__ void store_tile8(const qt8::Acc& acc, double* xbuf, i
   if (!slot) return;
 #pragma unroll
   for (int rb = 0; rb < 2; ++rb) {
-    const int64_t gi = i0 + qt8::acc_row<LPRE>(rb);
+    const int64_t gi = i0 + qt8::acc_row<MODE>(rb);
     if (gi >= M) continue;
 #pragma unroll
     for (int cb = 0; cb < 2; ++cb)
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        const int64_t gj = j0 + qt8::acc_col<LPRE>(cb) + h;
+        const int64_t gj = j0 + qt8::acc_col<MODE>(cb) + h;
         if (gj >= N) continue;
         double m[8], q[4];
 #pragma unroll
@@ -195,66 +200,70 @@ __device__ __forceinline__ void store_tile8(const qt8::Acc& acc, double* xbuf, i
   }
 }
 
-// Task order as sketch_fused_kernel: full W tiles, full Y tiles, padded Y
-// column tiles, padded W row tiles.
+// One task of mode MODE (qtile8.cuh) at tile origin (i0, j0), split z.
+template <int MODE, bool TMA>
+__device__ __forceinline__ void run_task(const Fused8Args& f, double* smem, int64_t i0, int64_t j0, int z) {
+  constexpr bool W = (MODE & 1) != 0;
+  const qt8::Operands& op = W ? f.wop : f.yop;
+  const int64_t kc = W ? f.kw_chunk : f.ky_chunk, K = W ? f.kw : f.ky;
+  const int zs = W ? f.zw : f.zy;
+  const int64_t kb = (int64_t)z * kc, ke = min(K, kb + kc);
+  qt8::Acc acc;
+  qt8::zero_acc(acc);
+  if constexpr (TMA) {
+    const CUtensorMap* lm = MODE == 0 ? &f.ylm : MODE == 1 ? &f.wlm : MODE == 2 ? &f.ynlm : &f.wnlm;
+    const CUtensorMap* rm = MODE == 0 ? &f.yrm : MODE == 1 ? &f.wrm : MODE == 2 ? &f.ynrm : &f.wnrm;
+    qt8::mma_tile_tma<MODE>(qt8::TmaOps{lm, rm, 0, f.stages, f.stride}, op, smem, i0, j0, kb, ke, acc);
+  } else if constexpr (MODE < 2) {
+    qt8::mma_tile<MODE>(op, smem, i0, j0, kb, ke, acc);
+  }
+  double* part = zs > 1 ? (W ? f.wp : f.yp) + (int64_t)z * 4 * op.M * op.N : nullptr;
+  store_tile8<MODE>(acc, smem, i0, j0, op.M, op.N, W ? f.w : f.y, W ? f.ldw : f.ldy, part, f.alpha, f.beta);
+}
+
+// Task order, longest first: full W tiles, narrow W remainder tiles, Y
+// tiles, narrow Y remainder tiles, padded W row tiles.  Within the groups
+// the order is L2-aware: W CTAs sharing a K chunk are adjacent (the l-row
+// tiles of an A column tile read the same A rows, the n-column tiles of a
+// Psi~ row tile the same Psi~ columns), and the column tiles of a Y row tile
+// are adjacent, so each A row tile comes from DRAM about once.
 template <bool TMA>
 __global__ void __launch_bounds__(TMA ? qt8::NT_TMA : qt8::NT, 1) sketch8_kernel(const __grid_constant__ Fused8Args f) {
   extern __shared__ __align__(128) double smem_raw[];
   // TMA destinations need 128-byte alignment (the launch adds the slack)
   // (offset arithmetic on the shared array keeps the accesses LDS, not generic)
   double* smem = smem_raw + ((128u - (qt::smem_u32(smem_raw) & 127u)) & 127u) / sizeof(double);
-  const int nwf = f.w_tmf * f.w_tn * f.zw;
-  const int nyf = f.y_tm * f.y_tnf * f.zy;
-  const int nyp = f.y_tm * (f.y_tn - f.y_tnf) * f.zy;
-  int t = blockIdx.x;
-  bool is_w;
-  int tm, tn, z;
-  // L2-aware order (groups still longest first: full W, Y, padded W):
-  // W CTAs sharing a K chunk are adjacent -- the l-row tiles of an A column
-  // tile read the same A rows, the n-column tiles of a Psi~ row tile the
-  // same Psi~ columns -- and the column tiles of a Y row tile (full and
-  // padded) are adjacent, so each A row tile comes from DRAM once.  (C5,
-  // n = 300, s = 40: the old order re-read A and Psi~ ~7x per launch.)
   const int wtf = f.w_tmf * f.w_tn, wtp = (f.w_tm - f.w_tmf) * f.w_tn;
+  const int nwf = wtf * f.zw, nwn = f.wn_t * f.zw;
+  const int nyr = f.y_tm * f.y_tn * f.zy, nyn = f.yn_t * f.zy;
+  int t = blockIdx.x;
   if (t < nwf) {
-    is_w = true;
-    const int tile = t % wtf;
-    z = t / wtf;
-    tm = tile % f.w_tmf; tn = tile / f.w_tmf;
-  } else if ((t -= nwf) < nyf + nyp) {
-    is_w = false;
-    z = t % f.zy; t /= f.zy;
-    tn = t % f.y_tn; tm = t / f.y_tn;
-  } else {
-    t -= nyf + nyp;
-    is_w = true;
-    const int tile = t % wtp;
-    z = t / wtp;
-    tm = f.w_tmf + tile % (f.w_tm - f.w_tmf); tn = tile / (f.w_tm - f.w_tmf);
+    const int tile = t % wtf, z = t / wtf;
+    run_task<1, TMA>(f, smem, (int64_t)(tile % f.w_tmf) * W8M, (int64_t)(tile / f.w_tmf) * W8N, z);
+    return;
   }
-  if (!is_w) {
-    qt8::Acc acc;
-    qt8::zero_acc(acc);
-    const int64_t kb = (int64_t)z * f.ky_chunk, ke = min(f.ky, kb + f.ky_chunk);
-    if (TMA)
-      qt8::mma_tile_tma<false>(qt8::TmaOps{&f.ylm, &f.yrm, 0, f.stages}, f.yop, smem, (int64_t)tm * Y8M, (int64_t)tn * Y8N, kb,
-                               ke, acc);
-    else
-      qt8::mma_tile<false>(f.yop, smem, (int64_t)tm * Y8M, (int64_t)tn * Y8N, kb, ke, acc);
-    double* part = f.zy > 1 ? f.yp + (int64_t)z * 4 * f.yop.M * f.yop.N : nullptr;
-    store_tile8<false>(acc, smem, (int64_t)tm * Y8M, (int64_t)tn * Y8N, f.yop.M, f.yop.N, f.y, f.ldy, part, f.alpha, f.beta);
-  } else {
-    qt8::Acc acc;
-    qt8::zero_acc(acc);
-    const int64_t kb = (int64_t)z * f.kw_chunk, ke = min(f.kw, kb + f.kw_chunk);
-    if (TMA)
-      qt8::mma_tile_tma<true>(qt8::TmaOps{&f.wlm, &f.wrm, 0, f.stages}, f.wop, smem, (int64_t)tm * W8M, (int64_t)tn * W8N, kb,
-                              ke, acc);
-    else
-      qt8::mma_tile<true>(f.wop, smem, (int64_t)tm * W8M, (int64_t)tn * W8N, kb, ke, acc);
-    double* part = f.zw > 1 ? f.wp + (int64_t)z * 4 * f.wop.M * f.wop.N : nullptr;
-    store_tile8<true>(acc, smem, (int64_t)tm * W8M, (int64_t)tn * W8N, f.wop.M, f.wop.N, f.w, f.ldw, part, f.alpha, f.beta);
+  t -= nwf;
+  if (TMA && t < nwn) {
+    const int tile = t % f.wn_t, z = t / f.wn_t;
+    run_task<3, TMA>(f, smem, (int64_t)f.w_tmf * W8M, (int64_t)tile * WNN, z);
+    return;
   }
+  t -= nwn;
+  if (t < nyr) {
+    const int z = t % f.zy;
+    t /= f.zy;
+    run_task<0, TMA>(f, smem, (int64_t)(t / f.y_tn) * Y8M, (int64_t)(t % f.y_tn) * Y8N, z);
+    return;
+  }
+  t -= nyr;
+  if (TMA && t < nyn) {
+    run_task<2, TMA>(f, smem, (int64_t)(t / f.zy) * YNM, (int64_t)f.y_tnf * Y8N, t % f.zy);
+    return;
+  }
+  t -= nyn;
+  const int tile = t % wtp, z = t / wtp;
+  run_task<1, TMA>(f, smem, (int64_t)(f.w_tmf + tile % (f.w_tm - f.w_tmf)) * W8M,
+                   (int64_t)(tile / (f.w_tm - f.w_tmf)) * W8N, z);
 }
 
 // out plane i (rows x cols, ld = cols) = combination i of in's planes, the
@@ -303,9 +312,13 @@ struct SketchWork {
 // made of 8x8 blocks (padded blocks cost nothing).
 struct Geom {
   int ym, yn, wm, wn;
+  bool ynarrow = false, wnarrow = false;  // remainder as 128x16 / 16x128 tiles (8-product TMA path)
 };
 constexpr Geom kGeom16{BM, BN, BM, BN};
 constexpr Geom kGeom8{Y8M, Y8N, W8M, W8N};
+// the narrow remainder tiles pay off when they hold at most half a regular
+// tile's columns (Y) / rows (W)
+inline bool narrow_rem(int64_t ext, int tile) { return ext % tile != 0 && ext % tile <= tile / 2; }
 
 // Makespan of one fused launch under greedy list scheduling on 148 SMs
 // (1 CTA per SM), tasks in kernel order.  Cost unit: one BK k-step of a full
@@ -318,11 +331,17 @@ double simulate_panel(const Geom& G, int64_t rp, int64_t n, int64_t s, int64_t l
   const int64_t y_tnf = s / G.yn, w_tmf = l / G.wm;
   auto frac = [](int64_t valid, int dim) { return (double)((valid + 7) / 8) / (dim / 8); };
   const double y_part = frac(s - y_tnf * G.yn, G.yn), w_part = frac(l - w_tmf * G.wm, G.wm);
+  // narrow remainder tiles: valid 8x8 blocks over a regular tile's 32
+  const int64_t yn_t = G.ynarrow ? (rp + YNM - 1) / YNM : 0, wn_t = G.wnarrow ? (n + WNN - 1) / WNN : 0;
+  const double yn_cost = (double)((s - y_tnf * G.yn + 7) / 8) * (YNM / 8) / 32.0;
+  const double wn_cost = (double)((l - w_tmf * G.wm + 7) / 8) * (WNN / 8) / 32.0;
   struct Group { int64_t count; double cost; };
-  const Group groups[4] = {{w_tmf * w_tn * nw_chunks, (double)(kwc / BK)},
+  const Group groups[6] = {{w_tmf * w_tn * nw_chunks, (double)(kwc / BK)},
+                           {wn_t * nw_chunks, (double)(kwc / BK) * wn_cost},
                            {y_tm * y_tnf * ny_chunks, (double)(kyc / BK)},
-                           {y_tm * (y_tn - y_tnf) * ny_chunks, (double)(kyc / BK) * y_part},
-                           {(w_tm - w_tmf) * w_tn * nw_chunks, (double)(kwc / BK) * w_part}};
+                           {G.ynarrow ? 0 : y_tm * (y_tn - y_tnf) * ny_chunks, (double)(kyc / BK) * y_part},
+                           {yn_t * ny_chunks, (double)(kyc / BK) * yn_cost},
+                           {G.wnarrow ? 0 : (w_tm - w_tmf) * w_tn * nw_chunks, (double)(kwc / BK) * w_part}};
   // Greedy assignment on buckets of SMs that free at the same time (tasks of
   // a group cost the same, so whole buckets advance together): O(tasks/148)
   // per group instead of a heap operation per CTA.
@@ -351,7 +370,8 @@ double simulate_panel(const Geom& G, int64_t rp, int64_t n, int64_t s, int64_t l
 std::pair<int, int> choose_panel_splits(const Geom& G, int64_t rp, int64_t n, int64_t s, int64_t l) {
   static std::mutex mu;
   static std::map<std::array<int64_t, 5>, std::pair<int, int>> cache;
-  const std::array<int64_t, 5> key{rp, n, s, l, (int64_t)G.ym * 1000 + G.yn};
+  const std::array<int64_t, 5> key{rp, n, s, l, (int64_t)G.ym * 1000 + G.yn + (G.ynarrow ? 1000000 : 0) +
+                                                  (G.wnarrow ? 2000000 : 0)};
   {
     std::lock_guard<std::mutex> lock(mu);
     auto it = cache.find(key);
@@ -440,13 +460,12 @@ bool tma_layout(const QView& a, int64_t* pstride) {
   return true;
 }
 // TMA ring slots (QLRA_Q8_STAGES overrides; the producer warp refills a slot as soon as it is released)
-int tma_stages() {
-  static const int v = [] {
+int tma_stages(int stride) {
+  static const int req = [] {
     const char* e = std::getenv("QLRA_Q8_STAGES");
-    const int s = e ? std::atoi(e) : 4;
-    return std::max(2, std::min(s, std::min(qt8::MAX_STAGES, (int)((227 * 1024 - 256) / (qt8::STAGE * sizeof(double))))));
+    return e ? std::atoi(e) : 4;
   }();
-  return v;
+  return std::max(2, std::min(req, std::min(qt8::MAX_STAGES, (int)((227 * 1024 - 512) / (stride * sizeof(double))))));
 }
 bool sketch_tma_enabled() {
   static const bool v = [] {
@@ -491,6 +510,14 @@ void set_splits(Args& f, const Geom& G, int64_t rp, int64_t n, int64_t s, int64_
   f.w_tn = (int)((n + G.wn - 1) / G.wn);
   f.y_tnf = (int)(s / G.yn);
   f.w_tmf = (int)(l / G.wm);
+  if (G.ynarrow) {
+    f.y_tn = f.y_tnf;
+    f.yn_t = (int)((rp + YNM - 1) / YNM);
+  }
+  if (G.wnarrow) {
+    f.w_tm = f.w_tmf;
+    f.wn_t = (int)((n + WNN - 1) / WNN);
+  }
   // Split counts (zy over n, zw over the panel rows) from a simulation of
   // the dispatcher: CTAs in kernel order (longest first) go to the SM that
   // frees first; cost = k-steps x fraction of 8x8 blocks inside M x N.
@@ -556,11 +583,6 @@ void launch8(Ctx& ctx, const Q8Part* y, const Q8Part* w, double alpha, double be
   }
   f.ky = n;
   f.kw = rp;
-  set_splits(f, kGeom8, rp, n, s, l, ctx, ws);
-  if (!y) f.y_tm = f.y_tn = f.y_tnf = 0;
-  if (!w) f.w_tm = f.w_tn = f.w_tmf = 0;
-  const int64_t ctas = (int64_t)f.y_tm * f.y_tn * f.zy + (int64_t)f.w_tm * f.w_tn * f.zw;
-  if (ctas == 0) return;
   // TMA staging when each on-the-fly operand's planes form one
   // 16-byte-aligned 3D tensor; the maps cover exactly the operands (rows past
   // them, k past K and columns past N come back zero)
@@ -568,15 +590,31 @@ void launch8(Ctx& ctx, const Q8Part* y, const Q8Part* w, double alpha, double be
   bool tma = sketch_tma_enabled();
   if (tma && y)
     tma = tma_layout(y->a, &yps) && make_map3(&f.ylm, y->a.p[0], n, rp, 4, y->a.ld, yps, qt8::LDK, Y8M, 4) &&
-          make_map3(&f.yrm, y->comb, s, n, 8, y->comb_ld, n * y->comb_ld, qt8::Layout<false>::LDX, qt8::BK, 8);
+          make_map3(&f.yrm, y->comb, s, n, 8, y->comb_ld, n * y->comb_ld, qt8::Layout<0>::LDX, qt8::BK, 8) &&
+          make_map3(&f.ynlm, y->a.p[0], n, rp, 4, y->a.ld, yps, qt8::LDK, YNM, 4) &&
+          make_map3(&f.ynrm, y->comb, s, n, 8, y->comb_ld, n * y->comb_ld, qt8::Layout<2>::LDX, qt8::BK, 8);
   if (tma && w)
     tma = tma_layout(w->a, &wps) && (w->col0 % 2) == 0 &&
           make_map3(&f.wlm, w->comb + w->col0, rp, l, 8, w->comb_ld, l * w->comb_ld, qt8::LDK, W8M, 8) &&
-          make_map3(&f.wrm, w->a.p[0], n, rp, 4, w->a.ld, wps, qt8::Layout<true>::LDX, qt8::BK, 4);
-  f.stages = tma_stages();
+          make_map3(&f.wrm, w->a.p[0], n, rp, 4, w->a.ld, wps, qt8::Layout<1>::LDX, qt8::BK, 4) &&
+          make_map3(&f.wnlm, w->comb + w->col0, rp, l, 8, w->comb_ld, l * w->comb_ld, qt8::LDK, WNM, 8) &&
+          make_map3(&f.wnrm, w->a.p[0], n, rp, 4, w->a.ld, wps, qt8::Layout<3>::LDX, qt8::BK, 4);
+  Geom G = kGeom8;
+  G.ynarrow = tma && y && narrow_rem(s, Y8N);
+  G.wnarrow = tma && w && narrow_rem(l, W8M);
+  set_splits(f, G, rp, n, s, l, ctx, ws);
+  if (!y) f.y_tm = f.y_tn = f.y_tnf = f.yn_t = 0;
+  if (!w) f.w_tm = f.w_tn = f.w_tmf = f.wn_t = 0;
+  const int64_t ctas = (int64_t)f.y_tm * f.y_tn * f.zy + (int64_t)f.yn_t * f.zy + (int64_t)f.w_tm * f.w_tn * f.zw +
+                       (int64_t)f.wn_t * f.zw;
+  if (ctas == 0) return;
+  // ring slots sized for the modes present: the narrow tiles need 7424
+  // doubles per slot (3 slots), the regular ones 5376 (4 slots)
+  f.stride = (f.yn_t || f.wn_t) ? qt8::STAGE_TMA : qt8::STAGE;
+  f.stages = tma_stages(f.stride);
   LaunchTimer lt(ctx, timed);
   if (tma)
-    sketch8_kernel<true><<<(unsigned)ctas, qt8::NT_TMA, (size_t)f.stages * qt8::STAGE * sizeof(double) + 128,
+    sketch8_kernel<true><<<(unsigned)ctas, qt8::NT_TMA, (size_t)f.stages * f.stride * sizeof(double) + 128,
                            ctx.stream>>>(f);
   else
     sketch8_kernel<false><<<(unsigned)ctas, qt8::NT, qt8::SMEM_BYTES + 128, ctx.stream>>>(f);
@@ -673,7 +711,7 @@ void set_kernel_attrs() {
   set_func_attr((const void*)sketch8_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                 (int)qt8::SMEM_BYTES + 128);
   set_func_attr((const void*)sketch8_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                (int)(tma_stages() * qt8::STAGE * sizeof(double)) + 128);
+                (int)(227 * 1024 - 512));
 }
 
 // Rows per fused launch.  Device-resident A: panels of up to kPanelBytes --
