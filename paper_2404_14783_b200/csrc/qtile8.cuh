@@ -483,5 +483,102 @@ __device__ __forceinline__ double other_product(const double* slot, int ii, int 
   return slot[32 * (((ii * 2 + rb) * 2 + cb) * 2 + h)];
 }
 
+// ---- multi-tile streaming (small K) ---------------------------------------
+// For products whose K spans only a few stages (Y R^-1: K = s), a CTA runs
+// `ntiles` consecutive row tiles of one column tile with ONE continuous
+// stage stream: the producer warp keeps loading the next tile's stages
+// while the compute warps finish a tile and store it, so the TMA pipeline
+// never drains and the per-CTA set-up is paid once.  The half exchange uses
+// its own buffer (xbuf, outside the ring) and a named barrier of the 16
+// compute warps (the producer warp never joins it).
+__device__ __forceinline__ void compute_bar() { asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory"); }
+
+template <int MODE, int HALF, int NRB, int NCB>
+__device__ __forceinline__ void consume_tile(const TmaOps& t, const double* smem, int nk, int& s, int& ph, Acc& acc,
+                                             uint64_t* full, uint64_t* empty) {
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int wr = warp_row<MODE>(w), wc = warp_col<MODE>(w);
+  const int gid = lane >> 2, tig = lane & 3;
+  constexpr int LOFF = Layout<MODE>::L_ELEMS;
+  for (int kt = 0; kt < nk; ++kt) {
+    qt::mbar_wait_parity(&full[s], (unsigned)(ph & 1));
+    const double* Ls = smem + s * t.stride;
+    if (NRB > 0 && NCB > 0)
+      kstep<MODE, HALF, (NRB > 0 ? NRB : 1), (NCB > 0 ? NCB : 1)>(Ls, Ls + LOFF, wr, wc, gid, tig, acc);
+    __syncwarp();
+    if (lane == 0) qt::mbar_arrive(&empty[s]);
+    if (++s == t.stages) { s = 0; ++ph; }
+  }
+}
+
+// Row tiles i0 = i00 + r * TM (r < ntiles) at column j0 over k in [kbeg,
+// kend); `store(acc, slot, i0)` runs on the compute warps after each tile
+// (slot: exchange slot for half 0, nullptr for half 1).  xbuf: 8*32*32
+// doubles outside the ring.
+template <int MODE, class Store>
+__device__ __forceinline__ void stream_tiles(const TmaOps& t, const Operands& g, double* smem, double* xbuf,
+                                             int64_t i00, int ntiles, int64_t j0, int64_t kbeg, int64_t kend,
+                                             Store store) {
+  using C = Cfg<MODE>;
+  __shared__ __align__(8) uint64_t full[MAX_STAGES], empty[MAX_STAGES];
+  tma_init<MODE>(t, full, empty);
+  const int nk = kend > kbeg ? (int)((kend - kbeg + BK - 1) / BK) : 0;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (w == NT / 32) {
+    constexpr int LOFF = Layout<MODE>::L_ELEMS;
+    if (lane == 0) {
+      int s = 0, ph = 0, issued = 0;
+      for (int r = 0; r < ntiles; ++r)
+        for (int kt = 0; kt < nk; ++kt, ++issued) {
+          if (issued >= t.stages) qt::mbar_wait_parity(&empty[s], (unsigned)((ph - 1) & 1));
+          tma_stage<MODE>(t, smem + s * t.stride, smem + s * t.stride + LOFF, i00 + (int64_t)r * C::TM, j0,
+                          kbeg + (int64_t)kt * BK, &full[s]);
+          if (++s == t.stages) { s = 0; ++ph; }
+        }
+    }
+    __syncwarp();
+    __syncthreads();
+    return;
+  }
+  int s = 0, ph = 0;
+  for (int r = 0; r < ntiles; ++r) {
+    const int64_t i0 = i00 + (int64_t)r * C::TM;
+    Acc acc;
+    zero_acc(acc);
+    // the warp's instance for this tile (the last row tile may be partial)
+    const int64_t r0w = i0 + 16 * warp_row<MODE>(w), c0w = j0 + 16 * warp_col<MODE>(w);
+    const int nrb = r0w >= g.M ? 0 : (int)min((int64_t)2, (g.M - r0w + 7) / 8);
+    const int ncb = c0w >= g.N ? 0 : (int)min((int64_t)2, (g.N - c0w + 7) / 8);
+    const int inst = (nrb == 0 || ncb == 0) ? 0 : warp_half(w) * 16 + nrb * 4 + ncb;
+    switch (inst) {
+      case 0 * 16 + 2 * 4 + 2: consume_tile<MODE, 0, 2, 2>(t, smem, nk, s, ph, acc, full, empty); break;
+      case 0 * 16 + 2 * 4 + 1: consume_tile<MODE, 0, 2, 1>(t, smem, nk, s, ph, acc, full, empty); break;
+      case 0 * 16 + 1 * 4 + 2: consume_tile<MODE, 0, 1, 2>(t, smem, nk, s, ph, acc, full, empty); break;
+      case 0 * 16 + 1 * 4 + 1: consume_tile<MODE, 0, 1, 1>(t, smem, nk, s, ph, acc, full, empty); break;
+      case 1 * 16 + 2 * 4 + 2: consume_tile<MODE, 1, 2, 2>(t, smem, nk, s, ph, acc, full, empty); break;
+      case 1 * 16 + 2 * 4 + 1: consume_tile<MODE, 1, 2, 1>(t, smem, nk, s, ph, acc, full, empty); break;
+      case 1 * 16 + 1 * 4 + 2: consume_tile<MODE, 1, 1, 2>(t, smem, nk, s, ph, acc, full, empty); break;
+      case 1 * 16 + 1 * 4 + 1: consume_tile<MODE, 1, 1, 1>(t, smem, nk, s, ph, acc, full, empty); break;
+      default: consume_tile<MODE, 0, 0, 0>(t, smem, nk, s, ph, acc, full, empty); break;
+    }
+    // exchange the product halves (compute warps only), then store
+    double* slot = xbuf + (w & 7) * 32 * 32 + lane;
+    if (warp_half(w) == 1) {
+#pragma unroll
+      for (int ii = 0; ii < 4; ++ii)
+#pragma unroll
+        for (int rb = 0; rb < 2; ++rb)
+#pragma unroll
+          for (int cb = 0; cb < 2; ++cb)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) slot[32 * (((ii * 2 + rb) * 2 + cb) * 2 + h)] = acc[ii][rb][cb][h];
+    }
+    compute_bar();
+    store(acc, warp_half(w) == 1 ? nullptr : slot, i0);
+    compute_bar();  // the slots are free for the next tile's exchange
+  }
+  __syncthreads();
+}
+
 }  // namespace qt8
 }  // namespace qlra_dev

@@ -144,6 +144,7 @@ struct Fused8Args {
   CUtensorMap ynlm, ynrm, wnlm, wnrm;  // the narrow remainder tiles (modes 2 / 3)
   int stages, stride;  // TMA ring slots and doubles per slot
   int yn_t, wn_t;  // narrow remainder tiles: YN row tiles, WN column tiles (0: none)
+  int y_rep;       // consecutive Y row tiles per CTA (stream_tiles, small K; 1: one tile)
   qt8::Operands yop;  // A_panel (k-fast) x Omega~ (8 planes, j-fast): M = panel rows, N = s, K = n
   qt8::Operands wop;  // Psi~_panel (8 planes, k-fast) x A_panel (j-fast): M = l, N = n, K = panel rows
   int64_t ky, kw;
@@ -164,10 +165,9 @@ struct Fused8Args {
 // Epilogue: the half-0 warps gather the other half's products (qtile8.cuh),
 // form the quaternion planes and add them to C (or write the split-K partial).
 template <int MODE>
-__device__ __forceinline__ void store_tile8(const qt8::Acc& acc, double* xbuf, int64_t i0, int64_t j0, int64_t M,
+__device__ __forceinline__ void store_slot8(const qt8::Acc& acc, const double* slot, int64_t i0, int64_t j0, int64_t M,
                                             int64_t N, double* const* c, int64_t ldc, double* part, double alpha,
                                             double beta) {
-  const double* slot = qt8::exchange_products(acc, xbuf);
   if (!slot) return;
 #pragma unroll
   for (int rb = 0; rb < 2; ++rb) {
@@ -200,6 +200,13 @@ __device__ __forceinline__ void store_tile8(const qt8::Acc& acc, double* xbuf, i
   }
 }
 
+template <int MODE>
+__device__ __forceinline__ void store_tile8(const qt8::Acc& acc, double* xbuf, int64_t i0, int64_t j0, int64_t M,
+                                            int64_t N, double* const* c, int64_t ldc, double* part, double alpha,
+                                            double beta) {
+  store_slot8<MODE>(acc, qt8::exchange_products(acc, xbuf), i0, j0, M, N, c, ldc, part, alpha, beta);
+}
+
 // One task of mode MODE (qtile8.cuh) at tile origin (i0, j0), split z.
 template <int MODE, bool TMA>
 __device__ __forceinline__ void run_task(const Fused8Args& f, double* smem, int64_t i0, int64_t j0, int z) {
@@ -221,6 +228,21 @@ __device__ __forceinline__ void run_task(const Fused8Args& f, double* smem, int6
   store_tile8<MODE>(acc, smem, i0, j0, op.M, op.N, W ? f.w : f.y, W ? f.ldw : f.ldy, part, f.alpha, f.beta);
 }
 
+// Y tiles g0 .. g0 + ntiles - 1 (row tiles of mode MODE) at column j0 as one
+// TMA stage stream (stream_tiles); Y-only launches with small K and zy = 1.
+template <int MODE>
+__device__ __forceinline__ void run_stream(const Fused8Args& f, double* smem, int g0, int ntiles, int64_t j0) {
+  constexpr int TM = qt8::Cfg<MODE>::TM;
+  const CUtensorMap* lm = MODE == 0 ? &f.ylm : &f.ynlm;
+  const CUtensorMap* rm = MODE == 0 ? &f.yrm : &f.ynrm;
+  double* xbuf = smem + (size_t)f.stages * f.stride;
+  qt8::stream_tiles<MODE>(qt8::TmaOps{lm, rm, 0, f.stages, f.stride}, f.yop, smem, xbuf, (int64_t)g0 * TM, ntiles, j0,
+                          0, f.ky, [&](const qt8::Acc& acc, const double* slot, int64_t i0) {
+                            store_slot8<MODE>(acc, slot, i0, j0, f.yop.M, f.yop.N, f.y, f.ldy, nullptr, f.alpha,
+                                              f.beta);
+                          });
+}
+
 // Task order, longest first: full W tiles, narrow W remainder tiles, Y
 // tiles, narrow Y remainder tiles, padded W row tiles.  Within the groups
 // the order is L2-aware: W CTAs sharing a K chunk are adjacent (the l-row
@@ -235,7 +257,8 @@ __global__ void __launch_bounds__(TMA ? qt8::NT_TMA : qt8::NT, 1) sketch8_kernel
   double* smem = smem_raw + ((128u - (qt::smem_u32(smem_raw) & 127u)) & 127u) / sizeof(double);
   const int wtf = f.w_tmf * f.w_tn, wtp = (f.w_tm - f.w_tmf) * f.w_tn;
   const int nwf = wtf * f.zw, nwn = f.wn_t * f.zw;
-  const int nyr = f.y_tm * f.y_tn * f.zy, nyn = f.yn_t * f.zy;
+  const int yg = (f.y_tm + f.y_rep - 1) / f.y_rep, yng = (f.yn_t + f.y_rep - 1) / f.y_rep;
+  const int nyr = yg * f.y_tn * f.zy, nyn = yng * f.zy;
   int t = blockIdx.x;
   if (t < nwf) {
     const int tile = t % wtf, z = t / wtf;
@@ -252,12 +275,26 @@ __global__ void __launch_bounds__(TMA ? qt8::NT_TMA : qt8::NT, 1) sketch8_kernel
   if (t < nyr) {
     const int z = t % f.zy;
     t /= f.zy;
-    run_task<0, TMA>(f, smem, (int64_t)(t / f.y_tn) * Y8M, (int64_t)(t % f.y_tn) * Y8N, z);
+    const int tn = t % f.y_tn, g0 = (t / f.y_tn) * f.y_rep;
+    if constexpr (TMA) {
+      if (f.y_rep > 1) {
+        run_stream<0>(f, smem, g0, min(f.y_rep, f.y_tm - g0), (int64_t)tn * Y8N);
+        return;
+      }
+    }
+    run_task<0, TMA>(f, smem, (int64_t)g0 * Y8M, (int64_t)tn * Y8N, z);
     return;
   }
   t -= nyr;
   if (TMA && t < nyn) {
-    run_task<2, TMA>(f, smem, (int64_t)(t / f.zy) * YNM, (int64_t)f.y_tnf * Y8N, t % f.zy);
+    const int z = t % f.zy, g0 = (t / f.zy) * f.y_rep;
+    if constexpr (TMA) {
+      if (f.y_rep > 1) {
+        run_stream<2>(f, smem, g0, min(f.y_rep, f.yn_t - g0), (int64_t)f.y_tnf * Y8N);
+        return;
+      }
+    }
+    run_task<2, TMA>(f, smem, (int64_t)g0 * YNM, (int64_t)f.y_tnf * Y8N, z);
     return;
   }
   t -= nyn;
@@ -460,12 +497,14 @@ bool tma_layout(const QView& a, int64_t* pstride) {
   return true;
 }
 // TMA ring slots (QLRA_Q8_STAGES overrides; the producer warp refills a slot as soon as it is released)
-int tma_stages(int stride) {
+// dynamic shared memory of the TMA kernel: 227 KB less its static barriers
+constexpr size_t kDynSmemMax = 227 * 1024 - 1024;
+int tma_stages(int stride, size_t extra_bytes) {
   static const int req = [] {
     const char* e = std::getenv("QLRA_Q8_STAGES");
     return e ? std::atoi(e) : 4;
   }();
-  return std::max(2, std::min(req, std::min(qt8::MAX_STAGES, (int)((227 * 1024 - 512) / (stride * sizeof(double))))));
+  return std::max(2, std::min(req, std::min(qt8::MAX_STAGES, (int)((kDynSmemMax - 128 - extra_bytes) / (stride * sizeof(double))))));
 }
 bool sketch_tma_enabled() {
   static const bool v = [] {
@@ -605,16 +644,28 @@ void launch8(Ctx& ctx, const Q8Part* y, const Q8Part* w, double alpha, double be
   set_splits(f, G, rp, n, s, l, ctx, ws);
   if (!y) f.y_tm = f.y_tn = f.y_tnf = f.yn_t = 0;
   if (!w) f.w_tm = f.w_tn = f.w_tmf = f.wn_t = 0;
-  const int64_t ctas = (int64_t)f.y_tm * f.y_tn * f.zy + (int64_t)f.yn_t * f.zy + (int64_t)f.w_tm * f.w_tn * f.zw +
+  // Y-only launches with few k-steps (Y R^-1, H = base M: K = s): stream
+  // several row tiles per CTA so the TMA pipeline does not drain per tile,
+  // keeping >= 2 waves of CTAs
+  f.y_rep = 1;
+  if (tma && y && !w && f.zy == 1) {
+    const int64_t nk = (n + qt8::BK - 1) / qt8::BK;
+    const int64_t tiles = (int64_t)f.y_tm * f.y_tn + f.yn_t;
+    if (nk <= 32) f.y_rep = (int)std::max<int64_t>(1, std::min<int64_t>({(64 + nk - 1) / nk, 32, tiles / 296}));
+  }
+  const int64_t ctas = (int64_t)((f.y_tm + f.y_rep - 1) / f.y_rep) * f.y_tn * f.zy +
+                       (int64_t)((f.yn_t + f.y_rep - 1) / f.y_rep) * f.zy + (int64_t)f.w_tm * f.w_tn * f.zw +
                        (int64_t)f.wn_t * f.zw;
   if (ctas == 0) return;
   // ring slots sized for the modes present: the narrow tiles need 7424
   // doubles per slot (3 slots), the regular ones 5376 (4 slots)
   f.stride = (f.yn_t || f.wn_t) ? qt8::STAGE_TMA : qt8::STAGE;
-  f.stages = tma_stages(f.stride);
+  // (streamed launches keep a separate 64 KB exchange buffer after the ring)
+  const size_t xbytes = f.y_rep > 1 ? (size_t)8 * 32 * 32 * sizeof(double) : 0;
+  f.stages = tma_stages(f.stride, xbytes);
   LaunchTimer lt(ctx, timed);
   if (tma)
-    sketch8_kernel<true><<<(unsigned)ctas, qt8::NT_TMA, (size_t)f.stages * f.stride * sizeof(double) + 128,
+    sketch8_kernel<true><<<(unsigned)ctas, qt8::NT_TMA, (size_t)f.stages * f.stride * sizeof(double) + xbytes + 128,
                            ctx.stream>>>(f);
   else
     sketch8_kernel<false><<<(unsigned)ctas, qt8::NT, qt8::SMEM_BYTES + 128, ctx.stream>>>(f);
@@ -711,7 +762,7 @@ void set_kernel_attrs() {
   set_func_attr((const void*)sketch8_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                 (int)qt8::SMEM_BYTES + 128);
   set_func_attr((const void*)sketch8_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                (int)(227 * 1024 - 512));
+                (int)kDynSmemMax);
 }
 
 // Rows per fused launch.  Device-resident A: panels of up to kPanelBytes --
