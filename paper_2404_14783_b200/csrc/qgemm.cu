@@ -510,7 +510,15 @@ void qgemm(Ctx& ctx, int op_a, int op_b, double alpha, const QView& A, const QVi
 // tiles on or above the diagonal are computed and the rest is mirrored
 // (about half the tensor work of a Gram; exactly Hermitian result).
 void qgemm_gram(Ctx& ctx, const QView& A, const QView& C) {
+  if (q8gram(ctx, A, C)) return;  // tall A: 8 real products per MAC (qtile8.cuh mode 4)
   qgemm_ex(ctx, QLRA_OP_C, QLRA_OP_N, 1.0, A, A, 0.0, C, 0, true);
+}
+
+void mirror_upper(Ctx& ctx, const QView& C) {
+  const int64_t M = C.rows;
+  k_mirror_upper<<<(unsigned)std::min<int64_t>((M * M + 255) / 256, 148 * 4), 256, 0, ctx.stream>>>(C);
+  QLRA_LAUNCH_CHECK();
+  count_launch();
 }
 
 void qgemm_ex(Ctx& ctx, int op_a, int op_b, double alpha, const QView& A, const QView& B,

@@ -62,15 +62,19 @@ constexpr int LDK = BK + 4;  // k-fast rows, pitch 12 (4 mod 16: conflict-free f
 //   1 W : 32 x 64, left Psi~ (8 planes), right A on the fly (j-fast)
 //   2 YN: 128 x 16, as Y -- the last Y column tile when s % 32 <= 16
 //   3 WN: 16 x 128, as W -- the last W row tile when l % 32 <= 16
+//   4 G : 64 x 32 of a Gram Y^* Y -- both operands on the fly from Y's 4
+//         planes, the left one as the adjoint (i-fast in memory, conjugated
+//         in registers); warp positions below the diagonal issue no DMMA
 // The narrow modes keep all 16 warps busy on a remainder that would leave
 // half of a regular tile's warps without a valid 8x8 block.
 template <int MODE>
 struct Cfg {
-  static constexpr bool LPRE = (MODE & 1) != 0;
-  static constexpr int PR = MODE == 0 ? 4 : MODE == 1 ? 2 : MODE == 2 ? 8 : 1;
+  static constexpr bool GRAM = MODE == 4;
+  static constexpr bool LPRE = !GRAM && (MODE & 1) != 0;
+  static constexpr int PR = MODE == 0 || GRAM ? 4 : MODE == 1 ? 2 : MODE == 2 ? 8 : 1;
   static constexpr int PC = 8 / PR;
   static constexpr int TM = 16 * PR, TN = 16 * PC, WRB = 2, WCB = 2;
-  static constexpr int LP = LPRE ? 8 : 4, RP = LPRE ? 4 : 8;
+  static constexpr int LP = LPRE ? 8 : 4, RP = LPRE || GRAM ? 4 : 8;
 };
 // Warp w issues on SMSP w % 4.  The position index runs fastest along the
 // long side of the position grid, so the warps of a tile padded along the
@@ -91,7 +95,8 @@ template <int MODE>
 struct Layout {
   using C = Cfg<MODE>;
   static constexpr int LDX = C::TN + 4;  // j-fast rows: 36 / 68 / 20 / 132 (4 mod 16)
-  static constexpr int L_ELEMS = C::LP * C::TM * LDK;
+  static constexpr int LDL = C::TM + 4;  // i-fast left rows (Gram): 68
+  static constexpr int L_ELEMS = C::GRAM ? C::LP * BK * LDL : C::LP * C::TM * LDK;
   static constexpr int R_ELEMS = C::RP * BK * LDX;
   static constexpr int ELEMS = L_ELEMS + R_ELEMS;
 };
@@ -229,7 +234,33 @@ __device__ __forceinline__ void kstep(const double* Ls, const double* Rs, int wr
   for (int kk = 0; kk < BK / 4; ++kk) {
     const int k = 4 * kk + tig;
     double lv[4][NRB], rv[4][NCB];
-    if (!C::LPRE) {
+    if constexpr (C::GRAM) {
+      // left = Y^* (i-fast, conjugated), right = Y (j-fast): both combined here
+      constexpr int LDL = Layout<MODE>::LDL;
+      double a[NRB][4], b[NCB][4];
+#pragma unroll
+      for (int rb = 0; rb < NRB; ++rb) {
+        const int x = 16 * wr + 8 * rb + gid;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const double v = Ls[(q * BK + k) * LDL + x];
+          a[rb][q] = q == 0 ? v : -v;
+        }
+      }
+#pragma unroll
+      for (int cb = 0; cb < NCB; ++cb) {
+        const int x = 16 * wc + 8 * cb + gid;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) b[cb][q] = Rs[(q * BK + k) * LDX + x];
+      }
+#pragma unroll
+      for (int ii = 0; ii < 4; ++ii) {
+#pragma unroll
+        for (int rb = 0; rb < NRB; ++rb) lv[ii][rb] = lcomb(4 * HALF + ii, a[rb]);
+#pragma unroll
+        for (int cb = 0; cb < NCB; ++cb) rv[ii][cb] = rcomb(4 * HALF + ii, b[cb]);
+      }
+    } else if (!C::LPRE) {
       // left = A: 4 planes per row block, combined in registers
       double a[NRB][4];
 #pragma unroll
@@ -349,7 +380,10 @@ __device__ __forceinline__ void tma_stage(const TmaOps& t, double* Ls, double* R
                                           uint64_t* bar) {
   constexpr unsigned BYTES = (unsigned)((Layout<MODE>::L_ELEMS + Layout<MODE>::R_ELEMS) * sizeof(double));
   mbar_expect_tx(bar, BYTES);
-  tma_load3(Ls, t.lm, (int)(t.lk_off + k0), (int)i0, bar);
+  if constexpr (Cfg<MODE>::GRAM)
+    tma_load3(Ls, t.lm, (int)i0, (int)k0, bar);  // Y rows k, columns i (the adjoint's rows)
+  else
+    tma_load3(Ls, t.lm, (int)(t.lk_off + k0), (int)i0, bar);
   tma_load3(Rs, t.rm, (int)j0, (int)k0, bar);
 }
 
@@ -417,6 +451,7 @@ __device__ __forceinline__ int instance(const Operands& g, int64_t i0, int64_t j
   const int64_t r0w = i0 + 16 * warp_row<MODE>(w), c0w = j0 + 16 * warp_col<MODE>(w);
   const int nrb = r0w >= g.M ? 0 : (int)min((int64_t)2, (g.M - r0w + 7) / 8);
   const int ncb = c0w >= g.N ? 0 : (int)min((int64_t)2, (g.N - c0w + 7) / 8);
+  if (Cfg<MODE>::GRAM && r0w >= c0w + 16) return 0;  // strictly below the diagonal: mirrored later
   return (nrb == 0 || ncb == 0) ? 0 : warp_half(w) * 16 + nrb * 4 + ncb;
 }
 

@@ -184,6 +184,7 @@ __device__ __forceinline__ void store_slot8(const qt8::Acc& acc, const double* s
         for (int ii = 0; ii < 4; ++ii) {
           m[ii] = acc[ii][rb][cb][h];
           m[4 + ii] = qt8::other_product(slot, ii, rb, cb, h);
+          if constexpr (qt8::Cfg<MODE>::GRAM) m[4 + ii] *= 0.5;  // no combined side to carry the halves
         }
         qt8::combine(m, q);
         if (part) {
@@ -301,6 +302,34 @@ __global__ void __launch_bounds__(TMA ? qt8::NT_TMA : qt8::NT, 1) sketch8_kernel
   const int tile = t % wtp, z = t / wtp;
   run_task<1, TMA>(f, smem, (int64_t)(f.w_tmf + tile % (f.w_tm - f.w_tmf)) * W8M,
                    (int64_t)(tile / (f.w_tm - f.w_tmf)) * W8N, z);
+}
+
+// ---- Gram Y^* Y on the 8-product engine (mode 4) ---------------------------
+constexpr int GRAM_MAXT = 160;  // upper tiles of an s x s Gram, s <= 512
+struct Gram8Args {
+  CUtensorMap lm, rm;  // both over Y: boxes {68, BK, 4} (adjoint side) / {36, BK, 4}
+  int stages, stride;
+  qt8::Operands op;    // M = N = s (bounds only; the data comes through the maps)
+  int64_t K, kchunk;
+  int ntiles, zk;
+  unsigned short tm[GRAM_MAXT], tn[GRAM_MAXT];
+  double* g[4];
+  int64_t ldg;
+  double* part;        // [zk][4][s][s] when zk > 1
+};
+
+__global__ void __launch_bounds__(qt8::NT_TMA, 1) gram8_kernel(const __grid_constant__ Gram8Args f) {
+  extern __shared__ __align__(128) double smem_raw[];
+  double* smem = smem_raw + ((128u - (qt::smem_u32(smem_raw) & 127u)) & 127u) / sizeof(double);
+  const int tile = blockIdx.x % f.ntiles, z = blockIdx.x / f.ntiles;
+  const int64_t i0 = (int64_t)f.tm[tile] * qt8::Cfg<4>::TM, j0 = (int64_t)f.tn[tile] * qt8::Cfg<4>::TN;
+  const int64_t kb = (int64_t)z * f.kchunk, ke = min(f.K, kb + f.kchunk);
+  qt8::Acc acc;
+  qt8::zero_acc(acc);
+  qt8::mma_tile_tma<4>(qt8::TmaOps{&f.lm, &f.rm, 0, f.stages, f.stride}, f.op, smem, i0, j0, kb, ke, acc);
+  const int64_t s = f.op.M;
+  double* part = f.zk > 1 ? f.part + (int64_t)z * 4 * s * s : nullptr;
+  store_tile8<4>(acc, smem, i0, j0, s, s, f.g, f.ldg, part, 1.0, 0.0);
 }
 
 // out plane i (rows x cols, ld = cols) = combination i of in's planes, the
@@ -761,6 +790,7 @@ void set_kernel_attrs() {
                 (int)qt::SMEM_BYTES);
   set_func_attr((const void*)sketch8_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                 (int)qt8::SMEM_BYTES + 128);
+  set_func_attr((const void*)gram8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDynSmemMax);
   set_func_attr((const void*)sketch8_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                 (int)kDynSmemMax);
 }
@@ -901,6 +931,64 @@ bool psi8_gemm(Ctx& ctx, const qlra_spec_t& psi, int64_t row0, const QView& B, c
   SketchWork ws;
   const Q8Part w{B, k.ps8, k.ps8_ld, 0, C};
   launch8(ctx, nullptr, &w, 1.0, 0.0, ws, false);
+  return true;
+}
+
+bool q8gram(Ctx& ctx, const QView& Y, const QView& G) {
+  const int64_t m = Y.rows, s = Y.cols;
+  int64_t pstride = 0;
+  // s >= 128: narrower Grams leave most of the 64 x 32 tiles' warps without
+  // a block (C5, s = 40: 3.5 -> 4.7 ms); the 16-product 64 x 64 Hermitian
+  // path is faster there
+  if (!sketch_use8() || !sketch_tma_enabled() || s < 128 || s > 512 || m < 4 * s || G.rows != s || G.cols != s ||
+      !tma_layout(Y, &pstride))
+    return false;
+  static const bool enabled = [] {
+    const char* e = std::getenv("QLRA_Q8GEMM");
+    return !(e && std::atoi(e) == 0);
+  }();
+  if (!enabled) return false;
+  using CG = qt8::Cfg<4>;
+  Gram8Args f{};
+  if (!make_map3(&f.lm, Y.p[0], s, m, 4, Y.ld, pstride, qt8::Layout<4>::LDL, qt8::BK, 4) ||
+      !make_map3(&f.rm, Y.p[0], s, m, 4, Y.ld, pstride, qt8::Layout<4>::LDX, qt8::BK, 4))
+    return false;
+  int nt = 0;
+  for (int tn = 0; tn < (int)((s + CG::TN - 1) / CG::TN); ++tn)
+    for (int tm = 0; tm < (int)((s + CG::TM - 1) / CG::TM); ++tm)
+      if ((int64_t)tm * CG::TM < (int64_t)(tn + 1) * CG::TN) {  // touches the upper triangle
+        if (nt == GRAM_MAXT) return false;
+        f.tm[nt] = (unsigned short)tm;
+        f.tn[nt] = (unsigned short)tn;
+        ++nt;
+      }
+  f.ntiles = nt;
+  for (int p = 0; p < 4; ++p) {
+    f.op.l[p] = Y.p[p];
+    f.op.r[p] = Y.p[p];
+    f.g[p] = G.p[p];
+  }
+  f.op.M = f.op.N = s;
+  f.ldg = G.ld;
+  f.K = m;
+  // split K so that about two waves of CTAs run, >= 16 k-steps each
+  int64_t zk = std::max<int64_t>(1, std::min<int64_t>((296 + nt - 1) / nt, m / (16 * qt8::BK)));
+  f.kchunk = ((m + zk - 1) / zk + qt8::BK - 1) / qt8::BK * qt8::BK;
+  f.zk = (int)((m + f.kchunk - 1) / f.kchunk);
+  DeviceBuffer part;
+  if (f.zk > 1) {
+    part = DeviceBuffer(ctx, (size_t)f.zk * 4 * s * s * sizeof(double));
+    f.part = part.as<double>();
+  }
+  f.stride = qt8::STAGE;
+  f.stages = tma_stages(f.stride, 0);
+  set_kernel_attrs();
+  gram8_kernel<<<(unsigned)(nt * f.zk), qt8::NT_TMA, (size_t)f.stages * f.stride * sizeof(double) + 128, ctx.stream>>>(
+      f);
+  QLRA_LAUNCH_CHECK();
+  count_launch();
+  if (f.zk > 1) splitk_reduce(ctx, f.part, f.zk, G, 1.0, 0.0);
+  mirror_upper(ctx, G);
   return true;
 }
 
