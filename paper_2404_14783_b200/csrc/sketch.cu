@@ -937,10 +937,15 @@ bool psi8_gemm(Ctx& ctx, const qlra_spec_t& psi, int64_t row0, const QView& B, c
 bool q8gram(Ctx& ctx, const QView& Y, const QView& G) {
   const int64_t m = Y.rows, s = Y.cols;
   int64_t pstride = 0;
-  // s >= 128: narrower Grams leave most of the 64 x 32 tiles' warps without
-  // a block (C5, s = 40: 3.5 -> 4.7 ms); the 16-product 64 x 64 Hermitian
-  // path is faster there
-  if (!sketch_use8() || !sketch_tma_enabled() || s < 128 || s > 512 || m < 4 * s || G.rows != s || G.cols != s ||
+  // s >= 96 (QLRA_Q8GRAM_MIN_S): narrower Grams leave most of the 64 x 32
+  // tiles' warps without a block (C5, s = 40: 3.5 -> 4.7 ms); the
+  // 16-product 64 x 64 Hermitian path is faster there (C2, s = 100: 8-product
+  // one-pass 9.68 ms vs 9.74)
+  static const int64_t smin = [] {
+    const char* e = std::getenv("QLRA_Q8GRAM_MIN_S");
+    return e ? std::atoll(e) : 96;
+  }();
+  if (!sketch_use8() || !sketch_tma_enabled() || s < smin || s > 512 || m < 4 * s || G.rows != s || G.cols != s ||
       !tma_layout(Y, &pstride))
     return false;
   static const bool enabled = [] {
