@@ -21,6 +21,7 @@
 #include <functional>
 #include <map>
 #include <mutex>
+#include <type_traits>
 #include <vector>
 
 #include <cudaTypedefs.h>
@@ -48,7 +49,6 @@ struct FusedArgs {
   int w_tm, w_tn, zw;
   int64_t kw_chunk;
   int y_tnf, w_tmf;  // full (no padding) Y column tiles / W row tiles
-  int yn_t, wn_t;    // (unused: the narrow remainder tiles are 8-product only)
   double* y[4];
   int64_t ldy;
   double* yp;  // [zy][4][My][Ny] partials when zy > 1
@@ -578,13 +578,15 @@ void set_splits(Args& f, const Geom& G, int64_t rp, int64_t n, int64_t s, int64_
   f.w_tn = (int)((n + G.wn - 1) / G.wn);
   f.y_tnf = (int)(s / G.yn);
   f.w_tmf = (int)(l / G.wm);
-  if (G.ynarrow) {
-    f.y_tn = f.y_tnf;
-    f.yn_t = (int)((rp + YNM - 1) / YNM);
-  }
-  if (G.wnarrow) {
-    f.w_tm = f.w_tmf;
-    f.wn_t = (int)((n + WNN - 1) / WNN);
+  if constexpr (std::is_same_v<Args, Fused8Args>) {  // narrow remainder tiles: 8-product engine only
+    if (G.ynarrow) {
+      f.y_tn = f.y_tnf;
+      f.yn_t = (int)((rp + YNM - 1) / YNM);
+    }
+    if (G.wnarrow) {
+      f.w_tm = f.w_tmf;
+      f.wn_t = (int)((n + WNN - 1) / WNN);
+    }
   }
   // Split counts (zy over n, zw over the panel rows) from a simulation of
   // the dispatcher: CTAs in kernel order (longest first) go to the SM that
