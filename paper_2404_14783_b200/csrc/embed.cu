@@ -23,8 +23,9 @@ struct GenArgs {
   int transposed;  // write out(j, i) instead of out(i, j)
 };
 
-__device__ __forceinline__ double entry_value(uint64_t key, int kind, double density,
-                                              uint64_t idx) {
+template <int KIND>
+__device__ __forceinline__ double entry_value(uint64_t key, double density, uint64_t idx) {
+  constexpr int kind = KIND;
   const uint64_t base = 4 * idx;
   switch (kind) {
     case QLRA_GAUSSIAN:
@@ -41,6 +42,9 @@ __device__ __forceinline__ double entry_value(uint64_t key, int kind, double den
   }
 }
 
+// one instantiation per kind: the four planes' draws of an entry are
+// independent and interleave (no runtime switch between them)
+template <int KIND>
 __global__ void gen_kernel(GenArgs a) {
   const int64_t cols = a.ncols;
   const int64_t total = a.nrows * a.ncols;
@@ -51,7 +55,7 @@ __global__ void gen_kernel(GenArgs a) {
     const int64_t off = a.transposed ? j * a.out.ld + i : i * a.out.ld + j;
 #pragma unroll
     for (int p = 0; p < 4; ++p)
-      a.out.p[p][off] = entry_value(a.key[p], a.kind, a.density, idx);
+      a.out.p[p][off] = entry_value<KIND>(a.key[p], a.density, idx);
   }
 }
 
@@ -76,7 +80,12 @@ void launch_gen(cudaStream_t st, const qlra_spec_t& spec, int64_t r0, int64_t c0
   const int threads = 256;
   int64_t blocks = (total + threads - 1) / threads;
   if (blocks > 148 * 16) blocks = 148 * 16;
-  gen_kernel<<<(unsigned)blocks, threads, 0, st>>>(a);
+  switch (spec.kind) {
+    case QLRA_GAUSSIAN: gen_kernel<QLRA_GAUSSIAN><<<(unsigned)blocks, threads, 0, st>>>(a); break;
+    case QLRA_RADEMACHER: gen_kernel<QLRA_RADEMACHER><<<(unsigned)blocks, threads, 0, st>>>(a); break;
+    case QLRA_SPARSE_GAUSSIAN: gen_kernel<QLRA_SPARSE_GAUSSIAN><<<(unsigned)blocks, threads, 0, st>>>(a); break;
+    default: gen_kernel<QLRA_SPARSE_RADEMACHER><<<(unsigned)blocks, threads, 0, st>>>(a); break;
+  }
   QLRA_LAUNCH_CHECK();
   count_launch();
 }
