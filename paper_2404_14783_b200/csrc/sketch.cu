@@ -630,16 +630,16 @@ void launch8(Ctx& ctx, const Q8Part* y, const Q8Part* w, double alpha, double be
   const int64_t rp = y ? y->a.rows : w->a.rows, n = y ? y->a.cols : w->a.cols;
   const int64_t s = y ? y->c.cols : 0, l = w ? w->c.rows : 0;
   if (y && w && (w->a.rows != rp || w->a.cols != n)) fail(QLRA_ERR_SHAPE, "launch8: coupled parts differ");
-  static const double kNull = 0.0;
+  // (an absent part launches no task, so its operand pointers are never read)
   for (int p = 0; p < 4; ++p) {
-    f.yop.l[p] = y ? y->a.p[p] : &kNull;
-    f.wop.r[p] = w ? w->a.p[p] : &kNull;
+    f.yop.l[p] = y ? y->a.p[p] : nullptr;
+    f.wop.r[p] = w ? w->a.p[p] : nullptr;
     f.y[p] = y ? y->c.p[p] : nullptr;
     f.w[p] = w ? w->c.p[p] : nullptr;
   }
   for (int i = 0; i < 8; ++i) {
-    f.yop.r[i] = y ? y->comb + (size_t)i * n * y->comb_ld : &kNull;
-    f.wop.l[i] = w ? w->comb + (size_t)i * l * w->comb_ld + w->col0 : &kNull;
+    f.yop.r[i] = y ? y->comb + (size_t)i * n * y->comb_ld : nullptr;
+    f.wop.l[i] = w ? w->comb + (size_t)i * l * w->comb_ld + w->col0 : nullptr;
   }
   if (y) {
     f.yop.l_si = y->a.ld; f.yop.r_sk = y->comb_ld;
