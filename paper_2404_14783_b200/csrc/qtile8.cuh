@@ -65,14 +65,18 @@ constexpr int LDK = BK + 4;  // k-fast rows, pitch 12 (4 mod 16: conflict-free f
 //   4 G : 64 x 32 of a Gram Y^* Y -- both operands on the fly from Y's 4
 //         planes, the left one as the adjoint (i-fast in memory, conjugated
 //         in registers); warp positions below the diagonal issue no DMMA
+//   5 SG: the whole Gram of a narrow Y (s <= 48) in one tile: the 6 upper
+//         16x16 blocks of a 3 x 3 grid as 6 positions, both operands read
+//         from ONE staged k-slice of Y (one TMA box per stage)
 // The narrow modes keep all 16 warps busy on a remainder that would leave
 // half of a regular tile's warps without a valid 8x8 block.
 template <int MODE>
 struct Cfg {
-  static constexpr bool GRAM = MODE == 4;
+  static constexpr bool GRAM = MODE == 4 || MODE == 5;
+  static constexpr bool SMALL = MODE == 5;
   static constexpr bool LPRE = !GRAM && (MODE & 1) != 0;
-  static constexpr int PR = MODE == 0 || GRAM ? 4 : MODE == 1 ? 2 : MODE == 2 ? 8 : 1;
-  static constexpr int PC = 8 / PR;
+  static constexpr int PR = MODE == 0 || MODE == 4 ? 4 : MODE == 1 ? 2 : MODE == 2 ? 8 : MODE == 5 ? 3 : 1;
+  static constexpr int PC = MODE == 5 ? 3 : 8 / PR;
   static constexpr int TM = 16 * PR, TN = 16 * PC, WRB = 2, WCB = 2;
   static constexpr int LP = LPRE ? 8 : 4, RP = LPRE || GRAM ? 4 : 8;
 };
@@ -82,11 +86,13 @@ struct Cfg {
 template <int MODE>
 __device__ __forceinline__ int warp_row(int w) {
   using C = Cfg<MODE>;
+  if constexpr (C::SMALL) return (0x33211000u >> (4 * (w & 7))) & 0xF;  // upper blocks of 3x3; 6, 7 -> 3 (idle)
   return C::PR >= C::PC ? (w & 7) % C::PR : (w & 7) / C::PC;
 }
 template <int MODE>
 __device__ __forceinline__ int warp_col(int w) {
   using C = Cfg<MODE>;
+  if constexpr (C::SMALL) return (0x33221210u >> (4 * (w & 7))) & 0xF;
   return C::PR >= C::PC ? (w & 7) / C::PR : (w & 7) % C::PC;
 }
 __device__ __forceinline__ int warp_half(int w) { return w >> 3; }
@@ -95,9 +101,9 @@ template <int MODE>
 struct Layout {
   using C = Cfg<MODE>;
   static constexpr int LDX = C::TN + 4;  // j-fast rows: 36 / 68 / 20 / 132 (4 mod 16)
-  static constexpr int LDL = C::TM + 4;  // i-fast left rows (Gram): 68
+  static constexpr int LDL = C::TM + 4;  // i-fast left rows (Gram): 68 / 52
   static constexpr int L_ELEMS = C::GRAM ? C::LP * BK * LDL : C::LP * C::TM * LDK;
-  static constexpr int R_ELEMS = C::RP * BK * LDX;
+  static constexpr int R_ELEMS = C::SMALL ? 0 : C::RP * BK * LDX;  // SG: the right operand is the same slice
   static constexpr int ELEMS = L_ELEMS + R_ELEMS;
 };
 constexpr int cmax(int a, int b) { return a > b ? a : b; }
@@ -237,6 +243,8 @@ __device__ __forceinline__ void kstep(const double* Ls, const double* Rs, int wr
     if constexpr (C::GRAM) {
       // left = Y^* (i-fast, conjugated), right = Y (j-fast): both combined here
       constexpr int LDL = Layout<MODE>::LDL;
+      const double* Rt = C::SMALL ? Ls : Rs;
+      constexpr int LDR = C::SMALL ? LDL : LDX;
       double a[NRB][4], b[NCB][4];
 #pragma unroll
       for (int rb = 0; rb < NRB; ++rb) {
@@ -251,7 +259,7 @@ __device__ __forceinline__ void kstep(const double* Ls, const double* Rs, int wr
       for (int cb = 0; cb < NCB; ++cb) {
         const int x = 16 * wc + 8 * cb + gid;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) b[cb][q] = Rs[(q * BK + k) * LDX + x];
+        for (int q = 0; q < 4; ++q) b[cb][q] = Rt[(q * BK + k) * LDR + x];
       }
 #pragma unroll
       for (int ii = 0; ii < 4; ++ii) {
@@ -384,7 +392,7 @@ __device__ __forceinline__ void tma_stage(const TmaOps& t, double* Ls, double* R
     tma_load3(Ls, t.lm, (int)i0, (int)k0, bar);  // Y rows k, columns i (the adjoint's rows)
   else
     tma_load3(Ls, t.lm, (int)(t.lk_off + k0), (int)i0, bar);
-  tma_load3(Rs, t.rm, (int)j0, (int)k0, bar);
+  if constexpr (!Cfg<MODE>::SMALL) tma_load3(Rs, t.rm, (int)j0, (int)k0, bar);
 }
 
 // The ring fed by a dedicated producer warp (warp 16, one elected lane):

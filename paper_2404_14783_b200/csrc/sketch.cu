@@ -318,18 +318,19 @@ struct Gram8Args {
   double* part;        // [zk][4][s][s] when zk > 1
 };
 
+template <int MODE>
 __global__ void __launch_bounds__(qt8::NT_TMA, 1) gram8_kernel(const __grid_constant__ Gram8Args f) {
   extern __shared__ __align__(128) double smem_raw[];
   double* smem = smem_raw + ((128u - (qt::smem_u32(smem_raw) & 127u)) & 127u) / sizeof(double);
   const int tile = blockIdx.x % f.ntiles, z = blockIdx.x / f.ntiles;
-  const int64_t i0 = (int64_t)f.tm[tile] * qt8::Cfg<4>::TM, j0 = (int64_t)f.tn[tile] * qt8::Cfg<4>::TN;
+  const int64_t i0 = (int64_t)f.tm[tile] * qt8::Cfg<MODE>::TM, j0 = (int64_t)f.tn[tile] * qt8::Cfg<MODE>::TN;
   const int64_t kb = (int64_t)z * f.kchunk, ke = min(f.K, kb + f.kchunk);
   qt8::Acc acc;
   qt8::zero_acc(acc);
-  qt8::mma_tile_tma<4>(qt8::TmaOps{&f.lm, &f.rm, 0, f.stages, f.stride}, f.op, smem, i0, j0, kb, ke, acc);
+  qt8::mma_tile_tma<MODE>(qt8::TmaOps{&f.lm, &f.rm, 0, f.stages, f.stride}, f.op, smem, i0, j0, kb, ke, acc);
   const int64_t s = f.op.M;
   double* part = f.zk > 1 ? f.part + (int64_t)z * 4 * s * s : nullptr;
-  store_tile8<4>(acc, smem, i0, j0, s, s, f.g, f.ldg, part, 1.0, 0.0);
+  store_tile8<MODE>(acc, smem, i0, j0, s, s, f.g, f.ldg, part, 1.0, 0.0);
 }
 
 // out plane i (rows x cols, ld = cols) = combination i of in's planes, the
@@ -792,7 +793,8 @@ void set_kernel_attrs() {
                 (int)qt::SMEM_BYTES);
   set_func_attr((const void*)sketch8_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                 (int)qt8::SMEM_BYTES + 128);
-  set_func_attr((const void*)gram8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDynSmemMax);
+  set_func_attr((const void*)gram8_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDynSmemMax);
+  set_func_attr((const void*)gram8_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDynSmemMax);
   set_func_attr((const void*)sketch8_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                 (int)kDynSmemMax);
 }
@@ -947,7 +949,9 @@ bool q8gram(Ctx& ctx, const QView& Y, const QView& G) {
     const char* e = std::getenv("QLRA_Q8GRAM_MIN_S");
     return e ? std::atoll(e) : 96;
   }();
-  if (!sketch_use8() || !sketch_tma_enabled() || s < smin || s > 512 || m < 4 * s || G.rows != s || G.cols != s ||
+  const bool small = s <= qt8::Cfg<5>::TM;  // whole Gram in one tile (mode 5)
+  if (!sketch_use8() || !sketch_tma_enabled() || (!small && s < smin) || s > 512 || m < 4 * s || G.rows != s ||
+      G.cols != s ||
       !tma_layout(Y, &pstride))
     return false;
   static const bool enabled = [] {
@@ -957,11 +961,16 @@ bool q8gram(Ctx& ctx, const QView& Y, const QView& G) {
   if (!enabled) return false;
   using CG = qt8::Cfg<4>;
   Gram8Args f{};
-  if (!make_map3(&f.lm, Y.p[0], s, m, 4, Y.ld, pstride, qt8::Layout<4>::LDL, qt8::BK, 4) ||
-      !make_map3(&f.rm, Y.p[0], s, m, 4, Y.ld, pstride, qt8::Layout<4>::LDX, qt8::BK, 4))
+  if (small ? !make_map3(&f.lm, Y.p[0], s, m, 4, Y.ld, pstride, qt8::Layout<5>::LDL, qt8::BK, 4)
+            : (!make_map3(&f.lm, Y.p[0], s, m, 4, Y.ld, pstride, qt8::Layout<4>::LDL, qt8::BK, 4) ||
+               !make_map3(&f.rm, Y.p[0], s, m, 4, Y.ld, pstride, qt8::Layout<4>::LDX, qt8::BK, 4)))
     return false;
   int nt = 0;
-  for (int tn = 0; tn < (int)((s + CG::TN - 1) / CG::TN); ++tn)
+  if (small) {
+    f.tm[0] = f.tn[0] = 0;
+    nt = 1;
+  }
+  for (int tn = 0; !small && tn < (int)((s + CG::TN - 1) / CG::TN); ++tn)
     for (int tm = 0; tm < (int)((s + CG::TM - 1) / CG::TM); ++tm)
       if ((int64_t)tm * CG::TM < (int64_t)(tn + 1) * CG::TN) {  // touches the upper triangle
         if (nt == GRAM_MAXT) return false;
@@ -990,8 +999,11 @@ bool q8gram(Ctx& ctx, const QView& Y, const QView& G) {
   f.stride = qt8::STAGE;
   f.stages = tma_stages(f.stride, 0);
   set_kernel_attrs();
-  gram8_kernel<<<(unsigned)(nt * f.zk), qt8::NT_TMA, (size_t)f.stages * f.stride * sizeof(double) + 128, ctx.stream>>>(
-      f);
+  const size_t smem = (size_t)f.stages * f.stride * sizeof(double) + 128;
+  if (small)
+    gram8_kernel<5><<<(unsigned)(nt * f.zk), qt8::NT_TMA, smem, ctx.stream>>>(f);
+  else
+    gram8_kernel<4><<<(unsigned)(nt * f.zk), qt8::NT_TMA, smem, ctx.stream>>>(f);
   QLRA_LAUNCH_CHECK();
   count_launch();
   if (f.zk > 1) splitk_reduce(ctx, f.part, f.zk, G, 1.0, 0.0);
