@@ -140,6 +140,28 @@ def test_sketch_engine_shapes_vs_oracle(ctx, m, n, s, l):
     assert rel_diff(host(st.w), w) < 1e-13
 
 
+def test_sketch_odd_width_relayout_vs_oracle(ctx):
+    """n odd and >= 1024 (C4's case): the device-resident block is relaid
+    through even-pitched staging panels so the TMA path applies."""
+    from paper_2404_14783_b200 import qlra as Q
+    a = random_gaussian(700, 1025, 77)
+    st = Q.make_sketch(dev(a), 5, 12, 30, 3, 4, ctx=ctx)
+    y, w = O.make_sketch(a, 5, 12, 30, 3, 4, nthreads=8)
+    assert rel_diff(host(st.y), y) < 1e-13
+    assert rel_diff(host(st.w), w) < 1e-13
+
+
+def test_tall_small_product_streams_vs_oracle(ctx):
+    """A tall x small product with few k-steps and enough row tiles that the
+    8-product engine streams several row tiles per CTA (stream_tiles)."""
+    from paper_2404_14783_b200 import qlra as Q
+    a, b = random_gaussian(30000, 40, 61), random_gaussian(40, 40, 62)
+    c0 = random_gaussian(30000, 40, 63)
+    out = dev(c0)
+    Q.qmat_mul(dev(a), dev(b), alpha=0.5, beta=-1.0, out=out)
+    assert rel_diff(host(out), 0.5 * O.qmat_mul(a, b) - c0) < 1e-13
+
+
 def test_streaming_equals_monolithic(ctx):  # test_sketching.cpp:120-129
     from paper_2404_14783_b200 import qlra as Q
     a = dev(random_gaussian(400, 300, 39))
