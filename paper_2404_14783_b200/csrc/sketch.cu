@@ -144,6 +144,7 @@ struct Fused8Args {
   CUtensorMap ynlm, ynrm, wnlm, wnrm;  // the narrow remainder tiles (modes 2 / 3)
   int stages, stride;  // TMA ring slots and doubles per slot
   int yn_t, wn_t;  // narrow remainder tiles: YN row tiles, WN column tiles (0: none)
+  int y_ilv;       // Y and YN tiles interleaved by 128-row block (QLRA_Y_INTERLEAVE)
   int y_rep;       // consecutive Y row tiles per CTA (stream_tiles, small K; 1: one tile)
   qt8::Operands yop;  // A_panel (k-fast) x Omega~ (8 planes, j-fast): M = panel rows, N = s, K = n
   qt8::Operands wop;  // Psi~_panel (8 planes, k-fast) x A_panel (j-fast): M = l, N = n, K = panel rows
@@ -273,6 +274,24 @@ __global__ void __launch_bounds__(TMA ? qt8::NT_TMA : qt8::NT, 1) sketch8_kernel
     return;
   }
   t -= nwn;
+  if (TMA && f.y_rep == 1 && f.yn_t > 0 && f.y_ilv && t < nyr + nyn) {
+    // interleaved: each 128-row block's regular Y tiles, then its narrow
+    // tile, so the block's A rows are re-read from L2 rather than DRAM
+    const int per = (2 * f.y_tn + 1) * f.zy;  // tasks of a full block
+    int blk = t / per, r = t % per;
+    if (blk >= f.yn_t - 1) {  // the last block may hold one regular row tile
+      blk = f.yn_t - 1;
+      r = t - blk * per;
+    }
+    const int nreg = min(2, f.y_tm - 2 * blk) * f.y_tn * f.zy;
+    if (r < nreg) {
+      const int z = r % f.zy, q = r / f.zy;
+      run_task<0, TMA>(f, smem, (int64_t)(2 * blk + q / f.y_tn) * Y8M, (int64_t)(q % f.y_tn) * Y8N, z);
+    } else {
+      run_task<2, TMA>(f, smem, (int64_t)blk * YNM, (int64_t)f.y_tnf * Y8N, r - nreg);
+    }
+    return;
+  }
   if (t < nyr) {
     const int z = t % f.zy;
     t /= f.zy;
@@ -691,6 +710,11 @@ void launch8(Ctx& ctx, const Q8Part* y, const Q8Part* w, double alpha, double be
   if (ctas == 0) return;
   // ring slots sized for the modes present: the narrow tiles need 7424
   // doubles per slot (3 slots), the regular ones 5376 (4 slots)
+  static const int ilv = [] {
+    const char* e = std::getenv("QLRA_Y_INTERLEAVE");  // (C5 sketch -1%, C2 DRAM reads -5%)
+    return e ? std::atoi(e) : 1;
+  }();
+  f.y_ilv = ilv;
   f.stride = (f.yn_t || f.wn_t) ? qt8::STAGE_TMA : qt8::STAGE;
   // (streamed launches keep a separate 64 KB exchange buffer after the ring)
   const size_t xbytes = f.y_rep > 1 ? (size_t)8 * 32 * 32 * sizeof(double) : 0;
