@@ -4,17 +4,22 @@
 // gen_test_matrix(Omega) + qmat_mul_accumulate_ordered(Y, A, Omega) +
 // gen_test_matrix_cols(Psi, rows) + qmat_mul_accumulate_ordered(W, Psi, A).
 //
-// The block of A is walked in row panels sized to stay resident in the 126 MB
-// L2.  Each panel is ONE launch of sketch_fused_kernel whose CTAs are either
-// Y-tasks (64x64 tile of Y_panel = A_panel * Omega over a K-chunk of the n
-// columns) or W-tasks (64x64 tile of W += Psi[:, panel] * A_panel over a
-// chunk of the panel rows), both on the DMMA tile core (qtile.cuh).  The
-// panel is read from HBM once and re-served from L2 to every task that
-// stages it, so HBM traffic for A is 32*m*n bytes -- the "A is read once"
-// contract of the one-pass method.  Split-K partials
-// go to workspaces reduced in fixed order afterwards: deterministic, no
+// The block of A is walked in row panels of up to 2 GB (one launch for C2).
+// Each panel is ONE launch of sketch8_kernel (8 real products per
+// quaternion MAC, qtile8.cuh) whose CTAs are either Y-tasks (tiles of
+// Y_panel = A_panel * Omega~ over a K-chunk of the n columns) or W-tasks
+// (tiles of W += Psi~[:, panel] * A_panel over a chunk of the panel rows);
+// Omega~ / Psi~ are the embeddings' 8 plane combinations, formed once per
+// call.  A is never rewritten: its tiles are staged by TMA (one producer
+// warp) and combined in registers.  The kernel does ~300 flop per byte of
+// A, so the re-reads of an unsplit panel by the tiles that share it cost no
+// time on this FP64-bound path.  Split-K partials go
+// to workspaces reduced in fixed order afterwards: deterministic, no
 // atomics.  Omega (n x s) and the Psi column slice (l x b) are generated on
-// device by K1 (embed.cu) from the reference's counter RNG.
+// device by K1 (embed.cu) from the reference's counter RNG.  The same
+// engine (launch8) runs the tall x small products of the rangefinders and
+// the core solve, and the Grams (gram8_kernel).  The 16-product
+// sketch_fused_kernel (qtile.cuh) stays selectable with QLRA_SKETCH16=1.
 #include <array>
 #include <cstdio>
 #include <cstdlib>
