@@ -5,7 +5,7 @@
 // Replaces the 16 real plane GEMMs of qmat_mul (proj/src/qmatrix.cpp:165-197)
 // and the ordered triple loop qmat_mul_accumulate_ordered
 // (proj/src/qmatrix.cpp:203-242).  The tile core is qtile.cuh (64x64
-// quaternion tile per CTA, DMMA.8x8x4, 3-stage cp.async ring).  Split-K
+// quaternion tile per CTA, DMMA.8x8x4, 4-stage cp.async ring).  Split-K
 // writes per-split partials to a workspace reduced in fixed split order
 // (deterministic, no atomics).  Epilogue variants: store, or residual (sum of
 // squares of R - op(A)op(B) and of R, for ||A - HX||_F without forming HX).

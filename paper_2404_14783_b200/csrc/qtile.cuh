@@ -13,7 +13,7 @@
 // Warp layout: 4 (rows) x 4 (cols) warps, each owning a 16x16 quaternion
 // sub-tile = 2x2 blocks of 8x8 per plane: 32 FP64 accumulators per thread
 // (16 warps per SM keep the DMMA pipe fed).
-// Operands are staged by cp.async into a 3-stage shared-memory ring in the
+// Operands are staged by cp.async into a 4-stage shared-memory ring in the
 // layout of their contiguous global dimension.  Row pitches are 4 mod 16
 // doubles (k-fast rows padded to 12, i/j-fast rows to 68): a half-warp's
 // fragment read covers 4 rows x 4 consecutive elements, which then land in
