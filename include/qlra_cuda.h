@@ -19,7 +19,11 @@
  * NCCL communicator.  Data matrices are row-sharded: each rank passes its
  * local rows of A / Y / H with `row0` = global index of its first row; W, X
  * and all small matrices are replicated.  Reductions over rows (W, Grams,
- * Psi*H, norms) are NCCL all-reduces inside the calls.
+ * Psi*H, norms) are NCCL all-reduces inside the calls.  The same sharded
+ * code also runs over an in-process communicator (qlra_group_t: one context
+ * per host thread, any devices of the process, including several ranks on ONE
+ * GPU, which NCCL refuses): the library sums the ranks' buffers itself, in
+ * rank order.
  */
 #ifndef QLRA_CUDA_H
 #define QLRA_CUDA_H
@@ -54,6 +58,7 @@ enum { QLRA_PSEUDO_QR = 0, QLRA_PSEUDO_SVD = 1 };
 enum { QLRA_OP_N = 0, QLRA_OP_C = 1 /* conjugate transpose */ };
 
 typedef struct qlra_ctx qlra_ctx_t;
+typedef struct qlra_group qlra_group_t;
 
 /* == TestMatrixSpec (sketching.hpp:22-28) */
 typedef struct {
@@ -90,11 +95,22 @@ typedef struct {
 int qlra_ctx_create(qlra_ctx_t** ctx, int device, int rank, int nranks,
                     const void* nccl_unique_id);
 int qlra_ctx_destroy(qlra_ctx_t* ctx);
+/* In-process communicator of `nranks` contexts (no reference counterpart: the
+ * reference is single-process).  Each rank's context is created
+ * with qlra_ctx_create_local from its own host thread; every collective call
+ * must then be made by all ranks, as with NCCL.  Destroy the group after its
+ * contexts (QLRA_ERR_PRECONDITION while any is attached). */
+int qlra_group_create(qlra_group_t** group, int nranks);
+int qlra_group_destroy(qlra_group_t* group);
+int qlra_ctx_create_local(qlra_ctx_t** ctx, int device, qlra_group_t* group, int rank);
 /* Run all further work on an external cudaStream_t (e.g. torch's current
  * stream); NULL selects the legacy default stream.  The context's own
  * non-blocking stream (created by qlra_ctx_create) is released. */
 int qlra_ctx_set_stream(qlra_ctx_t* ctx, void* cuda_stream);
 int qlra_ctx_synchronize(qlra_ctx_t* ctx);
+/* The cudaStream_t (as void*) all of this context's work is ordered on --
+ * callers order their own copies / kernels against the library's with it. */
+void* qlra_ctx_stream(const qlra_ctx_t* ctx);
 int qlra_nccl_unique_id(void* out_128_bytes);
 /* Message of the last failing call on this ctx; for QLRA_ERR_SINGULAR also
  * the condition estimate carried by SingularMatrixError (errors.hpp:23-30). */
@@ -178,6 +194,10 @@ int qlra_pseudo_qr(qlra_ctx_t* ctx, const qlra_qmat_t* y, const qlra_pseudo_qr_c
  * orthonormal H with range(H) = range(Y); syncs. */
 int qlra_pseudo_svd(qlra_ctx_t* ctx, const qlra_qmat_t* y, uint64_t seed, qlra_qmat_t* h,
                     qlra_rangefinder_report_t* report);
+/* orthonormal_range (rangefinders.hpp:61, rangefinders.cpp:160-164): the
+ * pseudo-SVD basis of range(Y) for rows >= cols (ParameterError otherwise),
+ * without the condition bookkeeping.  syncs. */
+int qlra_orthonormal_range(qlra_ctx_t* ctx, const qlra_qmat_t* y, uint64_t seed, qlra_qmat_t* h);
 
 /* --------------------------------------------------------- core solve --- */
 /* The solve half of qb_stage_with_psi (sketching.cpp:184-185):
@@ -197,6 +217,15 @@ int qlra_qb_stage(qlra_ctx_t* ctx, const qlra_spec_t* psi, int64_t row0, const q
                   const qlra_qmat_t* w, int method, uint64_t rangefinder_seed,
                   const qlra_pseudo_qr_config_t* cfg, qlra_qmat_t* h, qlra_qmat_t* x,
                   qlra_rangefinder_report_t* report);
+/* qb_stage_with_psi (sketching.hpp:104-107, sketching.cpp:169-188) with an
+ * explicitly supplied Psi: `psi` is this rank's column slice
+ * Psi(:, row0 : row0 + y->rows) in device memory (l x y->rows); the
+ * reference's tests inject structured ones this way (test_sketching.cpp:
+ * 170-183).  Rangefinder on Y, P = Psi H (all-reduced), X = P \ W.  syncs. */
+int qlra_qb_stage_with_psi(qlra_ctx_t* ctx, const qlra_qmat_t* psi, const qlra_qmat_t* y,
+                           const qlra_qmat_t* w, int method, uint64_t rangefinder_seed,
+                           const qlra_pseudo_qr_config_t* cfg, qlra_qmat_t* h, qlra_qmat_t* x,
+                           qlra_rangefinder_report_t* report);
 
 /* ------------------------------------------------ host-side one-pass --- */
 /* one_pass_approx through the QB stage (sketching.cpp:250-263) for a host
@@ -247,6 +276,11 @@ int qlra_read_qmat(qlra_ctx_t* ctx, const char* path, qlra_qmat_t* m);
 int qlra_write_sketch(qlra_ctx_t* ctx, const char* path, const qlra_spec_t* omega,
                       const qlra_spec_t* psi, int64_t r, int64_t s, int64_t l,
                       const qlra_qmat_t* y, const qlra_qmat_t* w);
+/* Shapes of the Y and W embedded in a QSKT1 file (dims = y rows, y cols,
+ * w rows, w cols) from their own QMAT1 headers, checked as read_sketch does
+ * (io.cpp:130-145: y.cols == s and w.rows == l, else QLRA_ERR_IO) and against
+ * the file length; no device work, no context. */
+int qlra_sketch_file_dims(const char* path, int64_t* dims);
 /* header of a QSKT1 file: both specs and r, s, l (rsl[3]) */
 int qlra_sketch_file_header(const char* path, qlra_spec_t* omega, qlra_spec_t* psi, int64_t* rsl);
 int qlra_read_sketch(qlra_ctx_t* ctx, const char* path, qlra_qmat_t* y, qlra_qmat_t* w);

@@ -50,6 +50,9 @@ def lib():
     sig = {
         "qlra_ctx_create": ([P(VP), INT, INT, INT, VP], INT),
         "qlra_ctx_destroy": ([VP], INT),
+        "qlra_group_create": ([P(VP), INT], INT),
+        "qlra_group_destroy": ([VP], INT),
+        "qlra_ctx_create_local": ([P(VP), INT, VP, INT], INT),
         "qlra_ctx_set_stream": ([VP, VP], INT),
         "qlra_ctx_synchronize": ([VP], INT),
         "qlra_nccl_unique_id": ([VP], INT),
@@ -70,6 +73,9 @@ def lib():
         "qlra_correction_step": ([VP, PQ, F64, PQ], INT),
         "qlra_pseudo_qr": ([VP, PQ, P(PseudoQrConfig), PQ, P(Report)], INT),
         "qlra_pseudo_svd": ([VP, PQ, U64, PQ, P(Report)], INT),
+        "qlra_orthonormal_range": ([VP, PQ, U64, PQ], INT),
+        "qlra_qb_stage_with_psi": ([VP, PQ, PQ, PQ, INT, U64, P(PseudoQrConfig), PQ, PQ, P(Report)], INT),
+        "qlra_ctx_stream": ([VP], VP),
         "qlra_qb_solve": ([VP, PS, I64, PQ, PQ, PQ], INT),
         "qlra_qb_stage": ([VP, PS, I64, PQ, PQ, INT, U64, P(PseudoQrConfig), PQ, PQ, P(Report)], INT),
         "qlra_one_pass_qb_host": ([VP, PQ, I64, PS, PS, INT, U64, P(PseudoQrConfig), I64, PQ, PQ, P(Report)],
@@ -84,6 +90,7 @@ def lib():
         "qlra_write_sketch": ([VP, C.c_char_p, PS, PS, I64, I64, I64, PQ, PQ], INT),
         "qlra_sketch_file_header": ([C.c_char_p, PS, PS, P(I64)], INT),
         "qlra_read_sketch": ([VP, C.c_char_p, PQ, PQ], INT),
+        "qlra_sketch_file_dims": ([C.c_char_p, P(I64)], INT),
         "qlra_sketch_from_qmat_file": ([VP, C.c_char_p, PS, PS, PQ, PQ, I64], INT),
         "qlra_measure_fp64_peak": ([VP, INT, F64, P(F64)], INT),
         "qlra_sketch_kernel_name": ([], C.c_char_p),

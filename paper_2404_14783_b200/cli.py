@@ -10,8 +10,8 @@ suites, image I/O) are outside the hot path (DESIGN 7).
     python -m paper_2404_14783_b200.cli approx --input A.qmat -r 10 --rangefinder both
     python -m paper_2404_14783_b200.cli approx --sketch A.qskt -r 10
 
-Every subcommand fails with the reference's exception names on stderr and
-exit status 1 (qlra_main.cpp:502-512).
+Every subcommand fails like the reference's: "error: <what>" on stderr and
+exit status 2 (qlra_main.cpp:502-512).
 """
 from __future__ import annotations
 
@@ -158,9 +158,9 @@ def main(argv=None):
     Q.set_default_context(Q.Context(a.device))
     try:
         return {"sketch": run_sketch, "update": run_update, "approx": run_approx}[a.cmd](a, Q)
-    except Q.Error as e:  # qlra_main.cpp:502-512
-        sys.stderr.write(f"{type(e).__name__}: {e}\n")
-        return 1
+    except Q.Error as e:  # qlra_main.cpp:508-511
+        sys.stderr.write(f"error: {e}\n")
+        return 2
 
 
 if __name__ == "__main__":

@@ -52,19 +52,35 @@ void set_func_attr(const void* func, cudaFuncAttribute attr, int value) {
 
 void allreduce_sum(Ctx& ctx, double* buf, size_t count) {
   if (ctx.nranks <= 1 || count == 0) return;
+  if (ctx.group) {
+    group_allreduce_sum(ctx, buf, count);
+    return;
+  }
   const ncclResult_t r = ncclAllReduce(buf, buf, count, ncclDouble, ncclSum, ctx.comm, ctx.stream);
   if (r != ncclSuccess) fail(QLRA_ERR_NCCL, std::string("ncclAllReduce: ") + ncclGetErrorString(r));
 }
 
+// One collective for all four planes: in place when they are one contiguous
+// run (DevQMat: dense planes back to back), else packed into a contiguous
+// buffer and unpacked after (strided views, e.g. W inside a checkpoint).
 void allreduce_qmat(Ctx& ctx, const QView& m) {
-  if (ctx.nranks <= 1) return;
-  for (int p = 0; p < 4; ++p) {
-    if (m.ld == m.cols) {
-      allreduce_sum(ctx, m.p[p], (size_t)(m.rows * m.cols));
-    } else {
-      for (int64_t i = 0; i < m.rows; ++i) allreduce_sum(ctx, m.p[p] + i * m.ld, (size_t)m.cols);
-    }
+  if (ctx.nranks <= 1 || m.rows == 0 || m.cols == 0) return;
+  const size_t plane = (size_t)(m.rows * m.cols);
+  bool dense = m.ld == m.cols || m.rows == 1;
+  for (int p = 1; p < 4 && dense; ++p) dense = m.p[p] == m.p[0] + p * plane;
+  if (dense) {
+    allreduce_sum(ctx, m.p[0], 4 * plane);
+    return;
   }
+  DeviceBuffer pk(ctx, 4 * plane * sizeof(double));
+  const size_t w = sizeof(double) * (size_t)m.cols, pitch = sizeof(double) * (size_t)m.ld;
+  for (int p = 0; p < 4; ++p)
+    QLRA_CUDA(cudaMemcpy2DAsync(pk.as<double>() + p * plane, w, m.p[p], pitch, w, (size_t)m.rows,
+                                cudaMemcpyDeviceToDevice, ctx.stream));
+  allreduce_sum(ctx, pk.as<double>(), 4 * plane);
+  for (int p = 0; p < 4; ++p)
+    QLRA_CUDA(cudaMemcpy2DAsync(m.p[p], pitch, pk.as<double>() + p * plane, w, w, (size_t)m.rows,
+                                cudaMemcpyDeviceToDevice, ctx.stream));
 }
 
 namespace {
@@ -98,6 +114,12 @@ int64_t global_rows(Ctx& ctx, int64_t local) {
   QLRA_CUDA(cudaMemcpyAsync(b.ptr, &v, sizeof(double), cudaMemcpyHostToDevice, ctx.stream));
   allreduce_sum(ctx, b.as<double>(), 1);
   return (int64_t)llround(to_host(ctx, b.as<double>(), 1)[0]);
+}
+
+DevQMat identity_like(Ctx& ctx, int64_t n) {
+  DevQMat e(ctx, n, n);
+  small_set_identity(ctx, e.v);
+  return e;
 }
 
 // First global row of this rank's contiguous row shard (exclusive prefix sum
@@ -200,6 +222,28 @@ double kappa_from_eigs(const std::vector<double>& ev) {
   if (!(lmin > 0.0)) return std::numeric_limits<double>::infinity();
   return std::sqrt(lmax / lmin);
 }
+
+// The spectrum of a Hermitian positive definite G with full relative
+// accuracy at both ends: eigenvalues of G itself resolve the large ones
+// (absolute error ~u lambda_max), those of an accurately formed G^{-1} the
+// small ones (1/mu).  lam, mu: descending.  Each value is taken from the side
+// that resolves it: above the geometric middle of the range from lam, below
+// it from 1/mu.
+std::vector<double> merge_spectra(const std::vector<double>& lam, const std::vector<double>& mu) {
+  const size_t n = lam.size();
+  if (n == 0 || mu.size() != n || !(mu[0] > 0.0) || !(lam[0] > 0.0)) return lam;
+  const double pivot = std::sqrt(lam[0] / mu[0]);
+  std::vector<double> out(n);
+  for (size_t i = 0; i < n; ++i) {
+    const double mi = mu[n - 1 - i];
+    out[i] = lam[i] >= pivot ? lam[i] : (mi > 0.0 ? 1.0 / mi : 0.0);
+    if (i > 0) out[i] = std::min(out[i], out[i - 1]);
+  }
+  return out;
+}
+// kappa^2 beyond which the small end of a Gram spectrum is refined (its
+// relative accuracy is ~u kappa^2: 1e-8 at kappa = 1e4)
+constexpr double kRefineKappa = 1e4;
 
 // Explicit quaternion inverse of a square matrix via Gauss-Jordan; returns
 // the GJ status (info, pmin, pmax).
@@ -439,6 +483,28 @@ bool cholesky_qr_general(Ctx& ctx, const QView& y, const QView& h, bool complex_
   return true;
 }
 
+// Refine the small end of a Gram spectrum lam (of G = A^*A, descending; all
+// values or extremes only) with rinv = R^{-1} of a QR factor of A.
+std::vector<double> refine_with_rinv(Ctx& ctx, const std::vector<double>& lam, const QView& rinv) {
+  const int64_t s = rinv.rows;
+  DevQMat p(ctx, s, s);
+  qgemm(ctx, QLRA_OP_N, QLRA_OP_C, 1.0, rinv, rinv, 0.0, p.v);  // (R^* R)^{-1}
+  const std::vector<double> mu = quat_eigs(ctx, p.v, /*extremes_only=*/false);
+  return merge_spectra(lam, mu);
+}
+
+std::vector<double> gram_spectrum(Ctx& ctx, const QView& a, const QView& g, bool extremes_only,
+                                  const DevQMat* rinv_in) {
+  std::vector<double> lam = quat_eigs(ctx, g, extremes_only);
+  if (!(kappa_from_eigs(lam) > kRefineKappa) || a.cols == 0) return lam;
+  if (rinv_in && rinv_in->buf.ptr) return refine_with_rinv(ctx, lam, rinv_in->v);
+  DevQMat rinv;
+  if (!cholesky_qr(ctx, a, QView{}, /*complex_mode=*/false, global_rows(ctx, a.rows), nullptr,
+                   /*distributed=*/true, &rinv))
+    return lam;  // not factorable: kappa beyond what any Gram route resolves
+  return refine_with_rinv(ctx, lam, rinv.v);
+}
+
 // Orthonormal completion: c_out (rows x k, row-sharded from global row0)
 // becomes quaternion-orthonormal and orthogonal to hr (rows x r, may be
 // r = 0).  Candidates are Gaussian columns from the reference RNG (seeded),
@@ -543,41 +609,55 @@ void rank_check(const std::vector<double>& d) {
     fail(QLRA_ERR_RANK, "pseudo_qr: sketch numerically rank-deficient; use pseudo_svd");
 }
 
-// Gram-based condition number of a row-sharded tall matrix (or wide via AA^*).
+// Spectrum of G = A^*A for a row-sharded tall A (descending), refined at the
+// small end when kappa(A) > kRefineKappa: A = Q R by CholeskyQR2 (backward
+// stable while kappa(A) < u^{-1/2}, so sigma(R) = sigma(A) to u ||A||), and
+// the eigenvalues of R^{-1} R^{-*} give the small ones (merge_spectra).  The
+// reference takes them from an SVD of chi_A (factorizations.cpp:316-337),
+// accurate to u ||A|| likewise.
+std::vector<double> gram_spectrum(Ctx& ctx, const QView& a, const QView& g, bool extremes_only,
+                                  const DevQMat* rinv_in = nullptr);
 double condition_number_dev(Ctx& ctx, const QView& a) {
   const int64_t k = std::min(a.rows, a.cols);
   if (k == 0) return std::numeric_limits<double>::infinity();
   DevQMat g(ctx, a.cols, a.cols);
   gram(ctx, a, g.v);
-  return kappa_from_eigs(quat_eigs(ctx, g.v));
+  return kappa_from_eigs(gram_spectrum(ctx, a, g.v, true));
 }
 
-// Explicit inverse of the Hermitian positive definite Gram G = H^*H, after
-// the reference's singularity test: rcond(chi_G) = 1/kappa(H)^2 must exceed
-// `rc_min` (1e-15 in estimate_epsilon, rangefinders.cpp:72-75; 1e-14 in the
-// square solve of correction_step, complex_bridge.cpp:73-77).
-void check_gram_rcond(double kappa_h, double rc_min, const char* msg) {
-  const double rc = std::isfinite(kappa_h) ? 1.0 / (kappa_h * kappa_h) : 0.0;
-  if (!(rc > rc_min))
-    fail(QLRA_ERR_SINGULAR, msg, rc > 0 ? 1.0 / rc : std::numeric_limits<double>::infinity());
-}
-DevQMat gram_inverse(Ctx& ctx, const QView& g, double kappa_h, double rc_min, const char* msg) {
-  check_gram_rcond(kappa_h, rc_min, msg);
-  DevQMat ginv(ctx, g.rows, g.cols);
-  if (!hpd_inverse(ctx, g, ginv.v, nullptr))
-    fail(QLRA_ERR_SINGULAR, msg, std::numeric_limits<double>::infinity());
-  return ginv;
-}
-
-// estimate_epsilon (rangefinders.cpp:66-97) given G^{-1}.
-double estimate_epsilon_from_inverse(Ctx& ctx, const QView& ginv, int iters) {
+// estimate_epsilon (rangefinders.cpp:66-97) given G and G^{-1}, with the
+// reference's singularity tests.  The reference factors chi_G by partial-
+// pivot LU and tests its 1-norm reciprocal condition estimate (Eigen rcond,
+// rangefinders.cpp:71-75; the oracle: zgecon); here the EXACT 1-norm value
+// rcond_1 = 1 / (||chi_G||_1 ||chi_G^{-1}||_1) from the explicit inverse --
+// the estimators bound it from above and reach it for most matrices (within
+// 1.3x on Gram matrices of kappa 1e5..1e8).  Note rcond_1 ~ 0.2 / kappa(H)^2
+// there, so the tests bind well below the 2-norm kappa = 1/sqrt(rc_min).
+// Returns eps; *rc_out = rcond_1 (also used by correction_step's square solve
+// test, rcond > 1e-14, complex_bridge.cpp:73-77).
+double estimate_epsilon_rc(Ctx& ctx, const QView& g, const QView& ginv, int iters, double* rc_out) {
   if (iters < 1) fail(QLRA_ERR_PARAMETER, "estimate_epsilon: power_iters must be >= 1");
-  DeviceBuffer rho(ctx, sizeof(double));
-  small_power_iter_inverse(ctx, ginv, iters, rho.as<double>());
-  const double r = to_host(ctx, rho.as<double>(), 1)[0];
-  if (!(r > 0.0)) fail(QLRA_ERR_SINGULAR, "estimate_epsilon: breakdown", 0.0);
-  return std::min(1.0 / std::sqrt(r), kEpsilonClamp);
+  DeviceBuffer v(ctx, 3 * sizeof(double));
+  small_power_iter_inverse(ctx, ginv, iters, v.as<double>());
+  small_chi_norm1(ctx, g, v.as<double>() + 1);
+  small_chi_norm1(ctx, ginv, v.as<double>() + 2);
+  const std::vector<double> h = to_host(ctx, v.as<double>(), 3);
+  const double rc = (h[1] > 0.0 && h[2] > 0.0 && std::isfinite(h[2])) ? 1.0 / (h[1] * h[2]) : 0.0;
+  if (rc_out) *rc_out = rc;
+  if (!(rc > 1e-15))
+    fail(QLRA_ERR_SINGULAR, "estimate_epsilon: H*H numerically singular",
+         rc > 0 ? 1.0 / rc : std::numeric_limits<double>::infinity());
+  if (!(h[0] > 0.0)) fail(QLRA_ERR_SINGULAR, "estimate_epsilon: breakdown", 0.0);
+  return std::min(1.0 / std::sqrt(h[0]), kEpsilonClamp);
 }
+// correction_step's square solve of chi_{H*H} (PartialPivLU, rcond > 1e-14,
+// complex_bridge.cpp:73-77), on the rcond_1 of estimate_epsilon_rc.
+void check_solve_rc(double rc) {
+  if (!(rc > 1e-14))
+    fail(QLRA_ERR_SINGULAR, "solve_quaternion_linear: singular system",
+         rc > 0 ? 1.0 / rc : std::numeric_limits<double>::infinity());
+}
+
 
 // H_out = H ((1-eps) I + eps G^{-1}) == (1-eps) H + eps (H^+)^*  (rangefinders.cpp:99-105)
 void correction_from_inverse(Ctx& ctx, const QView& h, const QView& ginv, double eps,
@@ -901,39 +981,49 @@ void pseudo_qr_dev(Ctx& c, const QView& Y, const QView& H, const qlra_pseudo_qr_
     std::string msg;
     double cond = 0.0;
     double eps = 0.0;
+    DevQMat ginv;  // G_k^{-1}
     DevQMat next;  // C_{k+1} = C_k ((1-eps) I + eps G_k^{-1})
   };
   Spec spec[2];
   const int nspec = std::min(2, cfg.max_correction_steps);
   std::vector<double> lam;
+  // One correction step on the coefficient matrix: G = C^*C, its inverse,
+  // estimate_epsilon's power iteration and rcond test, correction_step's
+  // solve test, then the next coefficient matrix (rangefinders.cpp:66-105).
+  auto step = [&](const QView& ck, const QView& gk, DevQMat& ginv, DevQMat& next) -> double {
+    double rc = 0.0;
+    const double eps = estimate_epsilon_rc(c, gk, ginv.v, cfg.power_iters_for_epsilon, &rc);
+    check_solve_rc(rc);
+    if (!(eps > 0.0 && eps < 1.0)) fail(QLRA_ERR_PARAMETER, "correction_step: epsilon must lie in (0,1)");
+    // H_{k+1} = H_k ((1-eps) I + eps G_k^{-1})  (rangefinders.cpp:99-105)
+    small_axpby_identity(c, 1.0 - eps, eps, ginv.v, mk.v);
+    next = DevQMat(c, s, s);
+    qgemm(c, QLRA_OP_N, QLRA_OP_N, 1.0, ck, mk.v, 0.0, next.v);
+    return eps;
+  };
   {
     SideEigs eig(c, g.v);
     for (int k = 0; k < nspec; ++k) {
       Spec& sp = spec[k];
       try {
-        DevQMat ginv(c, s, s);
+        sp.ginv = DevQMat(c, s, s);
         const QView ck = k == 0 ? cm.v : spec[0].next.v;
+        DevQMat gk;
         if (k == 0) {
           // G_0^{-1} from the factors already at hand: C = R_q R_c^{-1}, so
           // G_0^{-1} = K K^* with K = R_c R_q^{-1} (no factorisation; the
-          // reference's singularity test is applied from kappa below)
+          // reference's singularity tests are applied from its rcond below)
           DevQMat kf(c, s, s);
           qgemm(c, QLRA_OP_N, QLRA_OP_N, 1.0, rc.v, rq_inv.v, 0.0, kf.v);
-          qgemm(c, QLRA_OP_N, QLRA_OP_C, 1.0, kf.v, kf.v, 0.0, ginv.v);
+          qgemm(c, QLRA_OP_N, QLRA_OP_C, 1.0, kf.v, kf.v, 0.0, sp.ginv.v);
         } else {
-          DevQMat gk(c, s, s);
+          gk = DevQMat(c, s, s);
           qgemm(c, QLRA_OP_C, QLRA_OP_N, 1.0, ck, ck, 0.0, gk.v);
-          if (!hpd_inverse(c, gk.v, ginv.v, nullptr))
-            fail(QLRA_ERR_SINGULAR, "solve_quaternion_linear: singular system",
+          if (!hpd_inverse(c, gk.v, sp.ginv.v, nullptr))
+            fail(QLRA_ERR_SINGULAR, "estimate_epsilon: H*H numerically singular",
                  std::numeric_limits<double>::infinity());
         }
-        sp.eps = estimate_epsilon_from_inverse(c, ginv.v, cfg.power_iters_for_epsilon);
-        if (!(sp.eps > 0.0 && sp.eps < 1.0))
-          fail(QLRA_ERR_PARAMETER, "correction_step: epsilon must lie in (0,1)");
-        // H_{k+1} = H_k ((1-eps) I + eps G_k^{-1})  (rangefinders.cpp:99-105)
-        small_axpby_identity(c, 1.0 - sp.eps, sp.eps, ginv.v, mk.v);
-        sp.next = DevQMat(c, s, s);
-        qgemm(c, QLRA_OP_N, QLRA_OP_N, 1.0, ck, mk.v, 0.0, sp.next.v);
+        sp.eps = step(ck, k == 0 ? g.v : gk.v, sp.ginv, sp.next);
         sp.ok = true;
       } catch (const Status& e) {
         // only the numerical outcomes of the sequential flow are deferred
@@ -946,6 +1036,10 @@ void pseudo_qr_dev(Ctx& c, const QView& Y, const QView& H, const qlra_pseudo_qr_
     }
     lam = eig.get();
   }
+  // G_0's small eigenvalues carry ~u kappa^2 relative error; refine them from
+  // G_0^{-1} = K K^* (formed without squaring kappa) when it matters
+  if (kappa_from_eigs(lam) > kRefineKappa && nspec > 0 && spec[0].ginv.buf.ptr)
+    lam = merge_spectra(lam, quat_eigs(c, spec[0].ginv.v, /*extremes_only=*/false));
   r.kappa_before = kappa_from_eigs(lam);
   double kappa = r.kappa_before;
   if (std::getenv("QLRA_DEBUG_PQR")) {
@@ -961,8 +1055,6 @@ void pseudo_qr_dev(Ctx& c, const QView& Y, const QView& H, const qlra_pseudo_qr_
     while (r.correction_steps_used < cfg.max_correction_steps && kappa > kKappaTarget) {
       // one inverse serves estimate_epsilon and correction_step (both
       // factor the same H^*H, rangefinders.cpp:68,102)
-      check_gram_rcond(kappa, 1e-15, "estimate_epsilon: H*H numerically singular");
-      check_gram_rcond(kappa, 1e-14, "solve_quaternion_linear: singular system");
       const int k = r.correction_steps_used;
       double eps = 0.0;
       if (k < nspec) {
@@ -972,13 +1064,11 @@ void pseudo_qr_dev(Ctx& c, const QView& Y, const QView& H, const qlra_pseudo_qr_
         cm = std::move(sp.next);
       } else {
         qgemm(c, QLRA_OP_C, QLRA_OP_N, 1.0, cm.v, cm.v, 0.0, g.v);
-        DevQMat ginv = gram_inverse(c, g.v, kappa, 1e-14, "solve_quaternion_linear: singular system");
-        eps = estimate_epsilon_from_inverse(c, ginv.v, cfg.power_iters_for_epsilon);
-        if (!(eps > 0.0 && eps < 1.0))
-          fail(QLRA_ERR_PARAMETER, "correction_step: epsilon must lie in (0,1)");
-        small_axpby_identity(c, 1.0 - eps, eps, ginv.v, mk.v);
-        DevQMat cn(c, s, s);
-        qgemm(c, QLRA_OP_N, QLRA_OP_N, 1.0, cm.v, mk.v, 0.0, cn.v);
+        DevQMat ginv(c, s, s), cn;
+        if (!hpd_inverse(c, g.v, ginv.v, nullptr))
+          fail(QLRA_ERR_SINGULAR, "estimate_epsilon: H*H numerically singular",
+               std::numeric_limits<double>::infinity());
+        eps = step(cm.v, g.v, ginv, cn);
         cm = std::move(cn);
       }
       double lmax = 0.0, lmin = std::numeric_limits<double>::infinity();
@@ -1020,11 +1110,18 @@ void pseudo_qr_dev(Ctx& c, const QView& Y, const QView& H, const qlra_pseudo_qr_
 
 // kappa_after_async (optional): leave kappa(H) to the caller as a pending
 // side-stream eigenvalue computation instead of waiting for it here.
+// range_only: orthonormal_range (rangefinders.cpp:160-164: rows >= cols
+// allowed, no report).
 void pseudo_svd_dev(Ctx& c, const QView& Y, const QView& H, uint64_t seed, qlra_rangefinder_report_t* rep,
-                    std::unique_ptr<SideEigs>* kappa_after_async = nullptr) {
+                    std::unique_ptr<SideEigs>* kappa_after_async = nullptr, bool range_only = false) {
   const int64_t s = Y.cols;
   const int64_t m = global_rows(c, Y.rows);
-  if (m <= s) fail(QLRA_ERR_PARAMETER, "pseudo_svd: sketch must be tall (rows > cols)");
+  if (range_only) {
+    if (m < s) fail(QLRA_ERR_PARAMETER, "orthonormal_range: requires rows >= cols");
+  } else if (m <= s) {
+    fail(QLRA_ERR_PARAMETER, "pseudo_svd: sketch must be tall (rows > cols)");
+  }
+  if (s == 0) return;
   qlra_rangefinder_report_t r{};
   r.method = QLRA_PSEUDO_SVD;
   // Full-rank sketches: quaternion CholeskyQR2 (shifted CholeskyQR3 when
@@ -1032,17 +1129,22 @@ void pseudo_svd_dev(Ctx& c, const QView& Y, const QView& H, uint64_t seed, qlra_
   // kappa(Y) comes from the eigenvalues of the same Gram CholeskyQR2 starts
   // from, computed on the side stream while CholeskyQR2 runs; a non-finite
   // kappa (kappa^2 past 1/u) or a CholeskyQR breakdown takes the graded route.
-  DevQMat g(c, s, s);
+  DevQMat g(c, s, s), rinv;
   gram(c, Y, g.v);
   bool qr_ok = false;
+  std::vector<double> lam;
   {
     SideEigs eig(c, g.v);
-    qr_ok = cholesky_qr(c, Y, H, /*complex_mode=*/false, m, nullptr, /*distributed=*/true, nullptr, nullptr,
+    qr_ok = cholesky_qr(c, Y, H, /*complex_mode=*/false, m, nullptr, /*distributed=*/true, &rinv, nullptr,
                         nullptr, &g.v);
-    r.kappa_before = kappa_from_eigs(eig.get());
+    lam = eig.get();
   }
+  r.kappa_before = kappa_from_eigs(lam);
   if (!std::isfinite(r.kappa_before) || !qr_ok)
     r.kappa_before = pseudo_svd_graded(c, Y, H, m, global_row0(c, Y.rows), seed);
+  else if (r.kappa_before > kRefineKappa)  // kappa(Y) to ~u kappa(Y), not u kappa(Y)^2
+    r.kappa_before = kappa_from_eigs(refine_with_rinv(c, lam, rinv.v));
+  if (range_only) return;
   if (kappa_after_async) {
     // the caller overlaps kappa(H)'s eigenvalues with its next work
     DevQMat gh(c, s, s);
@@ -1164,6 +1266,31 @@ int qlra_ctx_create(qlra_ctx_t** out, int device, int rank, int nranks, const vo
   return QLRA_OK;
 }
 
+int qlra_ctx_create_local(qlra_ctx_t** out, int device, qlra_group_t* group, int rank) {
+  if (!out) return QLRA_ERR_PARAMETER;
+  *out = nullptr;
+  qlra_ctx_t* ctx = new qlra_ctx_t();
+  ctx->c.device = device;
+  const int rc = guarded(ctx, [&](Ctx& c) {
+    QLRA_CUDA(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
+    c.own_stream = true;
+    cudaMemPool_t pool;
+    QLRA_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+    uint64_t thr = UINT64_MAX;
+    QLRA_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    QLRA_CUDA(cudaMallocHost(&c.pinned, 4096));
+    group_attach(c, group, rank);
+  });
+  if (rc != QLRA_OK) {
+    if (ctx->c.stream) cudaStreamDestroy(ctx->c.stream);
+    if (ctx->c.pinned) cudaFreeHost(ctx->c.pinned);
+    delete ctx;
+    return rc;
+  }
+  *out = ctx;
+  return QLRA_OK;
+}
+
 static void drop_events(Ctx& c) {
   for (auto& e : c.ktimer.ev) {
     cudaEventDestroy(e.first);
@@ -1182,6 +1309,7 @@ int qlra_ctx_destroy(qlra_ctx_t* ctx) {
     cudaStreamSynchronize(ctx->c.stream);
   }
   if (ctx->c.comm) ncclCommDestroy(ctx->c.comm);
+  group_detach(ctx->c);
   if (ctx->c.own_stream && ctx->c.stream) cudaStreamDestroy(ctx->c.stream);
   if (ctx->c.pinned) cudaFreeHost(ctx->c.pinned);
   if (ctx->c.tile_cnt) cudaFree(ctx->c.tile_cnt);
@@ -1190,6 +1318,7 @@ int qlra_ctx_destroy(qlra_ctx_t* ctx) {
     cudaStreamDestroy(ctx->c.side);
   }
   if (ctx->c.side_pinned) cudaFreeHost(ctx->c.side_pinned);
+  if (ctx->c.staging) cudaFreeHost(ctx->c.staging);
   if (ctx->c.side2) {
     cudaStreamSynchronize(ctx->c.side2);
     cudaStreamDestroy(ctx->c.side2);
@@ -1344,10 +1473,13 @@ int qlra_condition_number(qlra_ctx_t* ctx, const qlra_qmat_t* h, double* kappa) 
     check_view(h, "condition_number");
     if (h->rows < h->cols && c.nranks == 1) {
       // wide: singular values of A^* (tall)
-      DevQMat g(c, h->rows, h->rows);
-      qgemm(c, QLRA_OP_N, QLRA_OP_C, 1.0, view_of(h), view_of(h), 0.0, g.v);
-      *kappa = h->rows == 0 ? std::numeric_limits<double>::infinity()
-                            : kappa_from_eigs(quat_eigs(c, g.v));
+      if (h->rows == 0) {
+        *kappa = std::numeric_limits<double>::infinity();
+        return;
+      }
+      DevQMat at(c, h->cols, h->rows);
+      qgemm(c, QLRA_OP_C, QLRA_OP_N, 1.0, view_of(h), identity_like(c, h->rows).v, 0.0, at.v);
+      *kappa = condition_number_dev(c, at.v);
     } else {
       *kappa = condition_number_dev(c, view_of(h));
     }
@@ -1361,11 +1493,16 @@ int qlra_singular_values(qlra_ctx_t* ctx, const qlra_qmat_t* a, double* sv) {
     const int64_t k = wide ? a->rows : a->cols;
     if (k == 0) return;
     DevQMat g(c, k, k);
-    if (wide)
-      qgemm(c, QLRA_OP_N, QLRA_OP_C, 1.0, view_of(a), view_of(a), 0.0, g.v);
-    else
+    std::vector<double> ev;
+    if (wide) {  // (the wide form refines through the tall A^*)
+      DevQMat at(c, a->cols, a->rows);
+      qgemm(c, QLRA_OP_C, QLRA_OP_N, 1.0, view_of(a), identity_like(c, a->rows).v, 0.0, at.v);
+      gram(c, at.v, g.v);
+      ev = gram_spectrum(c, at.v, g.v, /*extremes_only=*/false);
+    } else {
       gram(c, view_of(a), g.v);
-    const std::vector<double> ev = quat_eigs(c, g.v, /*extremes_only=*/false);
+      ev = gram_spectrum(c, view_of(a), g.v, /*extremes_only=*/false);
+    }
     for (int64_t i = 0; i < k; ++i) sv[i] = std::sqrt(std::max(0.0, ev[i]));
   });
 }
@@ -1409,11 +1546,12 @@ int qlra_estimate_epsilon(qlra_ctx_t* ctx, const qlra_qmat_t* h, int power_iters
     check_view(h, "estimate_epsilon");
     if (power_iters < 1) fail(QLRA_ERR_PARAMETER, "estimate_epsilon: power_iters must be >= 1");
     const int64_t s = h->cols;
-    DevQMat g(c, s, s);
+    DevQMat g(c, s, s), ginv(c, s, s);
     gram(c, view_of(h), g.v);
-    const double kh = kappa_from_eigs(quat_eigs(c, g.v));
-    DevQMat ginv = gram_inverse(c, g.v, kh, 1e-15, "estimate_epsilon: H*H numerically singular");
-    *eps = estimate_epsilon_from_inverse(c, ginv.v, power_iters);
+    if (!hpd_inverse(c, g.v, ginv.v, nullptr))
+      fail(QLRA_ERR_SINGULAR, "estimate_epsilon: H*H numerically singular",
+           std::numeric_limits<double>::infinity());
+    *eps = estimate_epsilon_rc(c, g.v, ginv.v, power_iters, nullptr);
   });
 }
 
@@ -1424,10 +1562,17 @@ int qlra_correction_step(qlra_ctx_t* ctx, const qlra_qmat_t* h, double epsilon, 
     if (!(epsilon > 0.0 && epsilon < 1.0))
       fail(QLRA_ERR_PARAMETER, "correction_step: epsilon must lie in (0,1)");
     const int64_t s = h->cols;
-    DevQMat g(c, s, s);
+    DevQMat g(c, s, s), ginv(c, s, s);
     gram(c, view_of(h), g.v);
-    const double kh = kappa_from_eigs(quat_eigs(c, g.v));
-    DevQMat ginv = gram_inverse(c, g.v, kh, 1e-14, "solve_quaternion_linear: singular system");
+    if (!hpd_inverse(c, g.v, ginv.v, nullptr))
+      fail(QLRA_ERR_SINGULAR, "solve_quaternion_linear: singular system",
+           std::numeric_limits<double>::infinity());
+    // the square solve's rcond test (complex_bridge.cpp:73-77) on rcond_1
+    DeviceBuffer nr(c, 2 * sizeof(double));
+    small_chi_norm1(c, g.v, nr.as<double>());
+    small_chi_norm1(c, ginv.v, nr.as<double>() + 1);
+    const std::vector<double> nn = to_host(c, nr.as<double>(), 2);
+    check_solve_rc((nn[0] > 0 && nn[1] > 0) ? 1.0 / (nn[0] * nn[1]) : 0.0);
     correction_from_inverse(c, view_of(h), ginv.v, epsilon, view_of(hout));
   });
 }
@@ -1451,6 +1596,15 @@ int qlra_pseudo_svd(qlra_ctx_t* ctx, const qlra_qmat_t* y, uint64_t seed, qlra_q
     check_view(h, "pseudo_svd");
     if (h->rows != y->rows || h->cols != y->cols) fail(QLRA_ERR_SHAPE, "pseudo_svd: output shape mismatch");
     pseudo_svd_dev(c, view_of(y), view_of(h), seed, rep);
+  });
+}
+
+int qlra_orthonormal_range(qlra_ctx_t* ctx, const qlra_qmat_t* y, uint64_t seed, qlra_qmat_t* h) {
+  return guarded(ctx, [&](Ctx& c) {
+    check_view(y, "orthonormal_range");
+    check_view(h, "orthonormal_range");
+    if (h->rows != y->rows || h->cols != y->cols) fail(QLRA_ERR_SHAPE, "orthonormal_range: output shape mismatch");
+    pseudo_svd_dev(c, view_of(y), view_of(h), seed, nullptr, nullptr, /*range_only=*/true);
   });
 }
 
@@ -1498,6 +1652,42 @@ int qlra_qb_stage(qlra_ctx_t* ctx, const qlra_spec_t* psi, int64_t row0, const q
   });
 }
 
+// qb_stage_with_psi (sketching.cpp:169-188) with an explicitly supplied Psi:
+// psi is the rank's column slice Psi(:, row0 : row0 + y.rows) in device
+// memory (l x y.rows); the reference's own tests inject structured ones
+// (test_sketching.cpp:170-183).  Rangefinder, then P = Psi H (all-reduced
+// over the ranks) and X = P \ W through a QR of P.
+int qlra_qb_stage_with_psi(qlra_ctx_t* ctx, const qlra_qmat_t* psi, const qlra_qmat_t* y, const qlra_qmat_t* w,
+                           int method, uint64_t rangefinder_seed, const qlra_pseudo_qr_config_t* cfg_in,
+                           qlra_qmat_t* h, qlra_qmat_t* x, qlra_rangefinder_report_t* rep) {
+  return guarded(ctx, [&](Ctx& c) {
+    check_view(psi, "qb_stage_with_psi");
+    check_view(y, "qb_stage_with_psi");
+    check_view(w, "qb_stage_with_psi");
+    check_view(h, "qb_stage_with_psi");
+    check_view(x, "qb_stage_with_psi");
+    if (h->rows != y->rows || h->cols != y->cols) fail(QLRA_ERR_SHAPE, "qb_stage: output shape mismatch");
+    // qmat_mul(psi, h) (sketching.cpp:184): inner dimensions must agree
+    if (psi->cols != y->rows) fail(QLRA_ERR_SHAPE, "qmat_mul: inner dimensions differ");
+    if (w->rows != psi->rows) fail(QLRA_ERR_SHAPE, "solve_quaternion_linear: row mismatch");
+    if (x->rows != y->cols || x->cols != w->cols) fail(QLRA_ERR_SHAPE, "qb_stage: shape mismatch");
+    if (method != QLRA_PSEUDO_QR && method != QLRA_PSEUDO_SVD) fail(QLRA_ERR_PARAMETER, "qb_stage: unknown rangefinder");
+    qlra_pseudo_qr_config_t cfg{3, 3, 1.2};
+    if (cfg_in) cfg = *cfg_in;
+    if (method == QLRA_PSEUDO_QR) pseudo_qr_dev(c, view_of(y), view_of(h), cfg, rep);
+    else pseudo_svd_dev(c, view_of(y), view_of(h), rangefinder_seed, rep);
+    const int64_t s = y->cols, l = psi->rows;
+    if (l < s) fail(QLRA_ERR_SHAPE, "solve_quaternion_linear: underdetermined system not supported");
+    DevQMat p(c, l, s);
+    qgemm(c, QLRA_OP_N, QLRA_OP_N, 1.0, view_of(psi), view_of(h), 0.0, p.v);
+    allreduce_qmat(c, p.v);
+    DevQMat t = lstsq_operator(c, p.v);
+    qgemm(c, QLRA_OP_C, QLRA_OP_N, 1.0, t.v, view_of(w), 0.0, view_of(x));
+  });
+}
+
+void* qlra_ctx_stream(const qlra_ctx_t* ctx) { return ctx ? static_cast<void*>(ctx->c.stream) : nullptr; }
+
 // Host in, host out: one_pass_approx through the QB stage
 // (sketching.cpp:250-263) on a host row shard.  A streams through the
 // overlapped H2D + fused-sketch pipeline; H is copied back on a side stream
@@ -1535,12 +1725,27 @@ int qlra_one_pass_qb_host(qlra_ctx_t* ctx, const qlra_qmat_t* a_host, int64_t ro
     EarlySolve* esp = nullptr;
     if (method == QLRA_PSEUDO_QR) pseudo_qr_dev(c, y.v, h.v, cfg, &rr, esp);
     else pseudo_svd_dev(c, y.v, h.v, rangefinder_seed, &rr, &kappa_after);
-    // H is final: copy it back on a side stream while the solve runs
-    cudaStream_t side = nullptr;
-    cudaEvent_t ready = nullptr, copied = nullptr;
-    QLRA_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
-    QLRA_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
-    QLRA_CUDA(cudaEventCreateWithFlags(&copied, cudaEventDisableTiming));
+    // H is final: copy it back on a side stream while the solve runs.  The
+    // guard (declared after y, w, h, x) drains the side stream on every exit
+    // -- a failing solve included -- before those buffers are released and
+    // before the call returns, so no copy lands in the caller's buffers later.
+    struct SideCopies {
+      cudaStream_t s = nullptr;
+      cudaEvent_t ready = nullptr, copied = nullptr;
+      SideCopies() {
+        QLRA_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+        QLRA_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+        QLRA_CUDA(cudaEventCreateWithFlags(&copied, cudaEventDisableTiming));
+      }
+      ~SideCopies() {
+        if (s) cudaStreamSynchronize(s);
+        if (ready) cudaEventDestroy(ready);
+        if (copied) cudaEventDestroy(copied);
+        if (s) cudaStreamDestroy(s);
+      }
+    } sc;
+    cudaStream_t side = sc.s;
+    cudaEvent_t ready = sc.ready, copied = sc.copied;
     QLRA_CUDA(cudaEventRecord(ready, c.stream));
     QLRA_CUDA(cudaStreamWaitEvent(side, ready, 0));
     const QView hv = view_of(h_host), xv = view_of(x_host);
@@ -1575,9 +1780,6 @@ int qlra_one_pass_qb_host(qlra_ctx_t* ctx, const qlra_qmat_t* a_host, int64_t ro
     // device buffers are released on c.stream: order that after the copies
     QLRA_CUDA(cudaStreamWaitEvent(c.stream, copied, 0));
     QLRA_CUDA(cudaStreamSynchronize(c.stream));
-    cudaEventDestroy(ready);
-    cudaEventDestroy(copied);
-    cudaStreamDestroy(side);
   });
 }
 
@@ -1736,6 +1938,17 @@ int qlra_write_sketch(qlra_ctx_t* ctx, const char* path, const qlra_spec_t* omeg
 int qlra_sketch_file_header(const char* path, qlra_spec_t* omega, qlra_spec_t* psi, int64_t* rsl) {
   try {
     sketch_header(path, omega, psi, rsl);
+    return QLRA_OK;
+  } catch (const Status& s) {
+    return s.code;
+  } catch (...) {
+    return QLRA_ERR_IO;
+  }
+}
+
+int qlra_sketch_file_dims(const char* path, int64_t* dims) {
+  try {
+    sketch_dims(path, dims);
     return QLRA_OK;
   } catch (const Status& s) {
     return s.code;

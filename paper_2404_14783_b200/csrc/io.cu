@@ -10,6 +10,7 @@
 #include <cstdio>
 #include <cstring>
 #include <fstream>
+#include <memory>
 #include <vector>
 
 #include "common.cuh"
@@ -143,6 +144,35 @@ void sketch_header(const std::string& path, qlra_spec_t* om, qlra_spec_t* ps, in
   for (int i = 0; i < 3; ++i) rsl[i] = (int64_t)get_u64(is);
 }
 
+// Shapes of the Y and W matrices embedded in a QSKT1 file, from their own
+// QMAT1 headers (io.cpp:130-145 reads them that way), with the reference's
+// consistency test (y.cols == s, w.rows == l, else IoError) and a size check
+// against the file length -- before anything is allocated.
+void sketch_dims(const std::string& path, int64_t* dims) {
+  std::ifstream is(path, std::ios::binary | std::ios::ate);
+  if (!is) fail(QLRA_ERR_IO, "cannot open: " + path);
+  const std::streamoff size = is.tellg();
+  is.seekg(0);
+  expect_magic(is, kSketchMagic, "QSKT1");
+  get_spec(is);
+  get_spec(is);
+  get_u64(is);
+  const int64_t s = (int64_t)get_u64(is), l = (int64_t)get_u64(is);
+  for (int k = 0; k < 2; ++k) {
+    expect_magic(is, kQmatMagic, "QMAT1");
+    const uint64_t rows = get_u64(is), cols = get_u64(is);
+    if (rows > (uint64_t)INT64_MAX / 64 || cols > (uint64_t)INT64_MAX / 64 ||
+        (cols && rows > (uint64_t)(size / 32) / cols))
+      fail(QLRA_ERR_IO, "read_sketch: truncated file");
+    const std::streamoff data = (std::streamoff)(32 * rows * cols);
+    if (is.tellg() + data > size) fail(QLRA_ERR_IO, "read_sketch: truncated file");
+    dims[2 * k] = (int64_t)rows;
+    dims[2 * k + 1] = (int64_t)cols;
+    is.seekg(data, std::ios::cur);
+  }
+  if (dims[1] != s || dims[2] != l) fail(QLRA_ERR_IO, "read_sketch: inconsistent dimensions");
+}
+
 void read_sketch(Ctx& ctx, const std::string& path, const QView& y, const QView& w) {
   std::ifstream is(path, std::ios::binary);
   if (!is) fail(QLRA_ERR_IO, "cannot open: " + path);
@@ -158,59 +188,36 @@ void read_sketch(Ctx& ctx, const std::string& path, const QView& y, const QView&
   if (y.cols != s || w.rows != l) fail(QLRA_ERR_IO, "read_sketch: inconsistent dimensions");
 }
 
-// sketch_from_source over a QMAT1 file: blocks of `block_rows` rows are read
-// (four plane seeks per block, io.cpp:221-239) into a pinned double buffer by
-// the host while the device sketches the previous block.
+// sketch_from_source over a QMAT1 file (QmatFileSource, io.cpp:213-239): the
+// file is the only reader of A.  One row pipeline for the whole file (Omega,
+// the Psi block and their plane combinations built once): each chunk's rows
+// are read from the file -- four plane seeks per chunk, as read_rows does --
+// straight into the pipeline's pinned staging while the previous chunk is
+// copied and sketched.  block_rows is the chunk height (the reference's
+// read granularity); the pipeline enlarges tiny chunks to its own minimum.
 void sketch_from_qmat_file(Ctx& ctx, const std::string& path, const qlra_spec_t& omega,
                            const qlra_spec_t& psi, const QView& y, const QView& w, int64_t block_rows) {
   int64_t m = 0, n = 0;
   qmat_header(path, &m, &n);
   if (n != w.cols || m != y.rows) fail(QLRA_ERR_SHAPE, "sketch_from_source: file shape mismatch");
   if (block_rows < 1) fail(QLRA_ERR_PARAMETER, "sketch_from_source: block_rows must be >= 1");
-  const int64_t br = std::min(block_rows, std::max<int64_t>(1, m));
-  double* pinned[2] = {nullptr, nullptr};
-  const size_t bytes = sizeof(double) * 4 * (size_t)(br * n);
-  QLRA_CUDA(cudaMallocHost(&pinned[0], std::max<size_t>(bytes, 8)));
-  QLRA_CUDA(cudaMallocHost(&pinned[1], std::max<size_t>(bytes, 8)));
-  cudaEvent_t done[2];
-  QLRA_CUDA(cudaEventCreateWithFlags(&done[0], cudaEventDisableTiming));
-  QLRA_CUDA(cudaEventCreateWithFlags(&done[1], cudaEventDisableTiming));
-  QLRA_CUDA(cudaEventRecord(done[0], ctx.stream));
-  QLRA_CUDA(cudaEventRecord(done[1], ctx.stream));
-  std::ifstream is(path, std::ios::binary);
-  if (!is) fail(QLRA_ERR_IO, "cannot open: " + path);
-  int idx = 0;
-  try {
-    for (int64_t r0 = 0; r0 < m; r0 += br, idx ^= 1) {
-      const int64_t rows = std::min(br, m - r0);
-      QLRA_CUDA(cudaEventSynchronize(done[idx]));  // buffer free again
-      double* hb = pinned[idx];
-      for (int p = 0; p < 4; ++p) {
-        is.seekg(kQmatHeaderBytes + (std::streamoff)((p * m + r0) * n * 8));
-        if (!is.read(reinterpret_cast<char*>(hb + (size_t)p * rows * n), (std::streamsize)(rows * n * 8)))
-          fail(QLRA_ERR_IO, "read_rows: truncated file");
-      }
-      QView hv;
-      for (int p = 0; p < 4; ++p) hv.p[p] = hb + (size_t)p * rows * n;
-      hv.rows = rows;
-      hv.cols = n;
-      hv.ld = n;
-      sketch_update_rows_host(ctx, omega, psi, r0, hv, sub(y, r0, 0, rows, y.cols), w, rows);
-      QLRA_CUDA(cudaEventRecord(done[idx], ctx.stream));
+  auto is = std::make_shared<std::ifstream>(path, std::ios::binary);
+  if (!*is) fail(QLRA_ERR_IO, "cannot open: " + path);
+  RowSource src;
+  src.kind = RowSource::kStaged;
+  src.fill = [is, m, n](int64_t r0, int64_t rows, double* dst) {
+    for (int p = 0; p < 4; ++p) {
+      is->seekg(kQmatHeaderBytes + (std::streamoff)((p * m + r0) * n * 8));
+      if (!is->read(reinterpret_cast<char*>(dst + (size_t)p * rows * n), (std::streamsize)(rows * n * 8)))
+        fail(QLRA_ERR_IO, "read_rows: truncated file");
     }
-    QLRA_CUDA(cudaStreamSynchronize(ctx.stream));
-  } catch (...) {
-    cudaStreamSynchronize(ctx.stream);
-    cudaFreeHost(pinned[0]);
-    cudaFreeHost(pinned[1]);
-    cudaEventDestroy(done[0]);
-    cudaEventDestroy(done[1]);
-    throw;
-  }
-  cudaFreeHost(pinned[0]);
-  cudaFreeHost(pinned[1]);
-  cudaEventDestroy(done[0]);
-  cudaEventDestroy(done[1]);
+  };
+  // chunks of at least the streaming pipeline's size (tiny chunks make short,
+  // inefficient launches), multiples of the requested block height
+  const int64_t want = std::max<int64_t>(1, (int64_t)(64e6 / (32.0 * (double)std::max<int64_t>(1, n))));
+  const int64_t chunk = std::min<int64_t>(m, ((want + block_rows - 1) / block_rows) * block_rows);
+  sketch_rows_pipeline(ctx, omega, psi, 0, m, n, src, y, w, chunk, false);
+  QLRA_CUDA(cudaStreamSynchronize(ctx.stream));
 }
 
 }  // namespace qlra_dev

@@ -21,6 +21,8 @@
 // the core solve, and the Grams (gram8_kernel).  The 16-product
 // sketch_fused_kernel (qtile.cuh) stays selectable with QLRA_SKETCH16=1.
 #include <array>
+#include <cstring>
+#include <thread>
 #include <cstdio>
 #include <cstdlib>
 #include <functional>
@@ -1078,15 +1080,64 @@ void sketch_update_rows(Ctx& ctx, const qlra_spec_t& omega, const qlra_spec_t& p
 }
 
 // Streaming ingestion (sketch_from_source, sketching.cpp:156-167, with the
-// source in host memory): row panels are copied H2D on a dedicated stream into
-// a double buffer while the previous panel is sketched, so the PCIe transfer
-// of A overlaps the FP64 work.  A is still read exactly once.  (Also the
-// relayout path for a device-resident A whose rows are not 16-byte aligned:
-// the copies are then device-to-device.)
-void sketch_update_rows_host(Ctx& ctx, const qlra_spec_t& omega, const qlra_spec_t& psi,
-                             int64_t row0, const QView& host_block, const QView& y_rows,
-                             const QView& w, int64_t block_rows, bool relayout) {
-  const int64_t b = host_block.rows, n = host_block.cols, s = omega.cols;
+// source in host memory): row chunks are copied H2D on a dedicated stream into
+// a double buffer while the previous chunk is sketched, so the PCIe transfer
+// of A overlaps the FP64 work.  A is still read exactly once.  Sources:
+//  * direct: pinned host rows (or, for the relayout of a device-resident A
+//    whose rows are not 16-byte aligned, device rows) -- one DMA per plane;
+//  * staged: host rows the DMA engine cannot read at full speed or at all
+//    (pageable memory, a file): a host-side `fill` writes each chunk into a
+//    pinned staging buffer (double-buffered, kept in the context) while the
+//    previous chunk's DMA and sketch run.
+namespace {
+
+// RAII for the pipeline's copy stream and events: on any exit (including an
+// exception thrown by a launch) the copy stream is drained before the device
+// and staging buffers it reads or writes are released.
+struct CopyPipe {
+  cudaStream_t cs = nullptr;
+  cudaEvent_t copied[2] = {nullptr, nullptr}, freed[2] = {nullptr, nullptr};
+  CopyPipe() {
+    QLRA_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    for (int i = 0; i < 2; ++i) {
+      QLRA_CUDA(cudaEventCreateWithFlags(&copied[i], cudaEventDisableTiming));
+      QLRA_CUDA(cudaEventCreateWithFlags(&freed[i], cudaEventDisableTiming));
+    }
+  }
+  ~CopyPipe() {
+    if (cs) cudaStreamSynchronize(cs);
+    for (int i = 0; i < 2; ++i) {
+      if (copied[i]) cudaEventDestroy(copied[i]);
+      if (freed[i]) cudaEventDestroy(freed[i]);
+    }
+    if (cs) cudaStreamDestroy(cs);
+  }
+  CopyPipe(const CopyPipe&) = delete;
+  CopyPipe& operator=(const CopyPipe&) = delete;
+};
+
+// Pinned staging of the context (grown on demand, kept: a 2 x 100 MB
+// cudaMallocHost per call would cost more than the copies it feeds).
+double* staging(Ctx& ctx, size_t doubles) {
+  if (ctx.staging_n < doubles) {
+    if (ctx.staging) {
+      QLRA_CUDA(cudaStreamSynchronize(ctx.stream));
+      QLRA_CUDA(cudaFreeHost(ctx.staging));
+    }
+    ctx.staging = nullptr;
+    ctx.staging_n = 0;
+    QLRA_CUDA(cudaMallocHost(&ctx.staging, doubles * sizeof(double)));
+    ctx.staging_n = doubles;
+  }
+  return ctx.staging;
+}
+
+}  // namespace
+
+void sketch_rows_pipeline(Ctx& ctx, const qlra_spec_t& omega, const qlra_spec_t& psi, int64_t row0, int64_t b,
+                          int64_t n, const RowSource& src, const QView& y_rows, const QView& w,
+                          int64_t block_rows, bool relayout) {
+  const int64_t s = omega.cols;
   if (b == 0 || n == 0) return;
   set_kernel_attrs();
   // (relayout of a device-resident A: panel-sized chunks, no short tail --
@@ -1094,9 +1145,8 @@ void sketch_update_rows_host(Ctx& ctx, const qlra_spec_t& omega, const qlra_spec
   int64_t R = block_rows > 0 ? block_rows : relayout ? panel_rows(n, b) : stream_rows(n, b);
   R = std::min(R, b);
   DevQMat om(ctx, n, s), ps_tmp;
-  const cudaMemcpyKind kind = relayout ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
-  // Staging buffers with an even leading dimension: the H2D copy lands A in
-  // the layout the TMA path needs (16-byte rows) even when n is odd (C4's
+  // Device buffers with an even leading dimension: the copy lands A in the
+  // layout the TMA path needs (16-byte rows) even when n is odd (C4's
   // 27125), at the cost of a pitched copy -- fine for wide rows.
   const int64_t ldb = (n % 2 == 0 || n < 1024) ? n : n + 1;
   DeviceBuffer bufmem[2] = {DeviceBuffer(ctx, (size_t)4 * R * ldb * sizeof(double)),
@@ -1108,18 +1158,19 @@ void sketch_update_rows_host(Ctx& ctx, const qlra_spec_t& omega, const qlra_spec
     buf[i].cols = n;
     buf[i].ld = ldb;
   }
-  cudaStream_t cs;
-  QLRA_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
-  cudaEvent_t copied[2], freed[2];
-  for (int i = 0; i < 2; ++i) {
-    QLRA_CUDA(cudaEventCreateWithFlags(&copied[i], cudaEventDisableTiming));
-    QLRA_CUDA(cudaEventCreateWithFlags(&freed[i], cudaEventDisableTiming));
+  const bool staged = src.kind == RowSource::kStaged;
+  double* stage[2] = {nullptr, nullptr};
+  if (staged) {
+    double* sb = staging(ctx, (size_t)8 * R * n);
+    stage[0] = sb;
+    stage[1] = sb + (size_t)4 * R * n;
   }
+  CopyPipe pipe;  // declared after every buffer it touches: drained first
   // the buffers were allocated on ctx.stream: the copy stream waits for
   // that, and only that -- Omega / Psi generation below overlaps the first
   // H2D chunk
-  QLRA_CUDA(cudaEventRecord(freed[0], ctx.stream));
-  QLRA_CUDA(cudaEventRecord(freed[1], ctx.stream));
+  QLRA_CUDA(cudaEventRecord(pipe.freed[0], ctx.stream));
+  QLRA_CUDA(cudaEventRecord(pipe.freed[1], ctx.stream));
   launch_gen(ctx.stream, omega, 0, 0, n, s, om.v, false);
   Emb e;
   e.om = om.v;
@@ -1135,30 +1186,98 @@ void sketch_update_rows_host(Ctx& ctx, const qlra_spec_t& omega, const qlra_spec
   for (int64_t r0 = 0, rp = 0; r0 < b; r0 += rp, idx ^= 1) {
     rp = std::min(r0 >= tail_start ? Rt : std::min(R, tail_start - r0), b - r0);
     const QView dst = sub(buf[idx], 0, 0, rp, n);
-    QLRA_CUDA(cudaStreamWaitEvent(cs, freed[idx], 0));
+    const double* from[4];
+    int64_t from_ld = n;
+    cudaMemcpyKind kind = cudaMemcpyHostToDevice;
+    if (staged) {
+      // staging buffer idx is free once its previous DMA has completed
+      QLRA_CUDA(cudaEventSynchronize(pipe.copied[idx]));
+      src.fill(r0, rp, stage[idx]);
+      for (int p = 0; p < 4; ++p) from[p] = stage[idx] + (size_t)p * rp * n;
+    } else {
+      for (int p = 0; p < 4; ++p) from[p] = src.direct.p[p] + r0 * src.direct.ld;
+      from_ld = src.direct.ld;
+      kind = src.copy_kind;
+    }
+    QLRA_CUDA(cudaStreamWaitEvent(pipe.cs, pipe.freed[idx], 0));
     for (int p = 0; p < 4; ++p) {
-      const double* src = host_block.p[p] + r0 * host_block.ld;
-      if (host_block.ld == n && dst.ld == n) {
+      if (from_ld == n && dst.ld == n) {
         // contiguous rows: one linear DMA (2D copies of narrow rows, e.g.
         // C5's 2400-byte rows, run far below PCIe bandwidth)
-        QLRA_CUDA(cudaMemcpyAsync(dst.p[p], src, sizeof(double) * (size_t)(rp * n), kind, cs));
+        QLRA_CUDA(cudaMemcpyAsync(dst.p[p], from[p], sizeof(double) * (size_t)(rp * n), kind, pipe.cs));
       } else {
-        QLRA_CUDA(cudaMemcpy2DAsync(dst.p[p], (size_t)dst.ld * sizeof(double), src,
-                                    (size_t)host_block.ld * sizeof(double), (size_t)n * sizeof(double),
-                                    (size_t)rp, kind, cs));
+        QLRA_CUDA(cudaMemcpy2DAsync(dst.p[p], (size_t)dst.ld * sizeof(double), from[p],
+                                    (size_t)from_ld * sizeof(double), (size_t)n * sizeof(double), (size_t)rp,
+                                    kind, pipe.cs));
       }
     }
-    QLRA_CUDA(cudaEventRecord(copied[idx], cs));
-    QLRA_CUDA(cudaStreamWaitEvent(ctx.stream, copied[idx], 0));
+    QLRA_CUDA(cudaEventRecord(pipe.copied[idx], pipe.cs));
+    QLRA_CUDA(cudaStreamWaitEvent(ctx.stream, pipe.copied[idx], 0));
     sketch_panel(ctx, e, r0, dst, sub(y_rows, r0, 0, rp, s), w, ws);
-    QLRA_CUDA(cudaEventRecord(freed[idx], ctx.stream));
+    QLRA_CUDA(cudaEventRecord(pipe.freed[idx], ctx.stream));
   }
-  QLRA_CUDA(cudaStreamSynchronize(cs));
-  for (int i = 0; i < 2; ++i) {
-    cudaEventDestroy(copied[i]);
-    cudaEventDestroy(freed[i]);
+}
+
+// Host rows of a (4-plane, ld) host matrix copied into pinned staging by
+// several host threads (pageable memcpy runs at ~10 GB/s per thread; PCIe
+// takes ~55 GB/s).
+void parallel_fill(const QView& host, int64_t r0, int64_t rows, double* dst) {
+  const int64_t n = host.cols;
+  const size_t bytes = (size_t)(4 * rows * n) * sizeof(double);
+  const int nt = (int)std::max<int64_t>(1, std::min<int64_t>(8, (int64_t)(bytes >> 23)));  // >= 8 MB each
+  auto work = [&](int t) {
+    for (int p = 0; p < 4; ++p) {
+      const int64_t i0 = rows * t / nt, i1 = rows * (t + 1) / nt;
+      double* d = dst + (size_t)p * rows * n;
+      const double* sp = host.p[p] + (r0 + i0) * host.ld;
+      if (host.ld == n) {
+        std::memcpy(d + i0 * n, sp, sizeof(double) * (size_t)((i1 - i0) * n));
+      } else {
+        for (int64_t i = i0; i < i1; ++i) std::memcpy(d + i * n, sp + (i - i0) * host.ld, sizeof(double) * n);
+      }
+    }
+  };
+  if (nt == 1) {
+    work(0);
+    return;
   }
-  cudaStreamDestroy(cs);
+  std::vector<std::thread> ts;
+  for (int t = 1; t < nt; ++t) ts.emplace_back(work, t);
+  work(0);
+  for (auto& t : ts) t.join();
+}
+
+void sketch_update_rows_host(Ctx& ctx, const qlra_spec_t& omega, const qlra_spec_t& psi,
+                             int64_t row0, const QView& host_block, const QView& y_rows,
+                             const QView& w, int64_t block_rows, bool relayout) {
+  RowSource src;
+  src.kind = RowSource::kDirect;
+  src.direct = host_block;
+  src.copy_kind = relayout ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+  if (!relayout && host_block.rows > 0 && host_block.cols > 0) {
+    // Pageable host memory (a reference QMatrix's std::vector planes): the
+    // DMA engine would stage it through a driver bounce buffer synchronously,
+    // serialising the pipeline; copy it into pinned staging on host threads
+    // instead, overlapped with the previous chunk's DMA and sketch.
+    cudaPointerAttributes at{};
+    bool pinned = true;
+    for (int p = 0; p < 4 && pinned; ++p) {
+      if (cudaPointerGetAttributes(&at, host_block.p[p]) != cudaSuccess) {
+        cudaGetLastError();
+        pinned = false;
+      } else {
+        pinned = at.type == cudaMemoryTypeHost || at.type == cudaMemoryTypeDevice ||
+                 at.type == cudaMemoryTypeManaged;
+      }
+    }
+    if (!pinned) {
+      src.kind = RowSource::kStaged;
+      const QView hb = host_block;
+      src.fill = [hb](int64_t r0, int64_t rows, double* dst) { parallel_fill(hb, r0, rows, dst); };
+    }
+  }
+  sketch_rows_pipeline(ctx, omega, psi, row0, host_block.rows, host_block.cols, src, y_rows, w, block_rows,
+                       relayout);
 }
 
 }  // namespace qlra_dev

@@ -45,8 +45,11 @@ class ParameterError(Error):
 
 
 class SingularMatrixError(Error):
+    """Message format of errors.hpp:23-30: msg + " (estimated condition " +
+    std::to_string(cond) + ")" (std::to_string(double) is "%f")."""
+
     def __init__(self, msg, estimated_condition):
-        super().__init__(msg)
+        super().__init__(f"{msg} (estimated condition {estimated_condition:f})")
         self.estimated_condition = estimated_condition
 
 
@@ -70,19 +73,52 @@ _ERR = {1: ShapeError, 2: ParameterError, 4: RankError, 5: PreconditionError, 6:
 
 
 # ------------------------------------------------------------ context ---
+class LocalGroup:
+    """In-process communicator (qlra_group_t): `nranks` Contexts, one per host
+    thread, whose all-reduces the library performs itself in rank order --
+    the multi-rank path on ONE GPU (NCCL refuses two ranks per device) or
+    across the devices of one process."""
+
+    def __init__(self, nranks: int):
+        self.lib = L.lib()
+        self.nranks = nranks
+        h = C.c_void_p()
+        if self.lib.qlra_group_create(C.byref(h), nranks) != 0:
+            raise ParameterError("qlra_group_create: nranks must lie in [1, 16]")
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None):
+            if self.lib.qlra_group_destroy(self.h) != 0:
+                raise PreconditionError("qlra_group_destroy: contexts still attached")
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 class Context:
-    """One per process/device: stream, NCCL communicator, error state."""
+    """One per process/device (or per thread of a LocalGroup): stream,
+    communicator (NCCL or the in-process group), error state."""
 
     def __init__(self, device: int = 0, rank: int = 0, nranks: int = 1, nccl_id: bytes | None = None,
-                 use_torch_stream: bool = True):
+                 use_torch_stream: bool = True, local_group: LocalGroup | None = None):
         self.lib = L.lib()
         self.device = device
         self.rank, self.nranks = rank, nranks
         h = C.c_void_p()
-        buf = C.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
-        rc = self.lib.qlra_ctx_create(C.byref(h), device, rank, nranks, buf)
+        if local_group is not None:
+            self.nranks = local_group.nranks
+            rc = self.lib.qlra_ctx_create_local(C.byref(h), device, local_group.h, rank)
+        else:
+            buf = C.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
+            rc = self.lib.qlra_ctx_create(C.byref(h), device, rank, nranks, buf)
         if rc != 0:
             raise DeviceError(f"qlra_ctx_create failed ({rc})")
+        self.group = local_group
         self.h = h
         if use_torch_stream:
             self.set_stream(torch.cuda.current_stream(device))
@@ -470,6 +506,15 @@ def pseudo_svd(y, seed=DEFAULT_RANGEFINDER_SEED, ctx=None) -> RangefinderReport:
     return RangefinderReport(h, rep.kappa_before, rep.kappa_after, 0, PSEUDO_SVD)
 
 
+def orthonormal_range(y, seed=DEFAULT_RANGEFINDER_SEED, ctx=None):
+    """orthonormal_range (rangefinders.cpp:160-164): the pseudo-SVD basis of
+    range(Y), rows >= cols."""
+    ctx = _ctx(ctx)
+    h = torch.empty_like(y)
+    ctx._check(ctx.lib.qlra_orthonormal_range(ctx.h, C.byref(_qm(y)), seed, C.byref(_qm(h))))
+    return h
+
+
 # ------------------------------------------------------------ QB stage ---
 @dataclass
 class QbResult:
@@ -522,6 +567,28 @@ def qb_stage(state: SketchState, method=PSEUDO_QR, rangefinder_seed=DEFAULT_RANG
     ctx.synchronize()
     t2 = time.perf_counter()
     return QbResult(rep.h, x, rep, t1 - t0, t2 - t1)
+
+
+def qb_stage_with_psi(state: SketchState, psi, method=PSEUDO_QR, rangefinder_seed=DEFAULT_RANGEFINDER_SEED,
+                      qr_cfg: PseudoQrConfig = PseudoQrConfig(), ctx=None) -> QbResult:
+    """qb_stage_with_psi (sketching.cpp:169-188) with an explicit Psi: `psi` is
+    the (l x rows) column slice of Psi matching state.y's rows (the whole Psi
+    on one rank)."""
+    ctx = _ctx(ctx)
+    if method not in (PSEUDO_QR, PSEUDO_SVD):
+        raise ParameterError("qb_stage: unknown rangefinder")
+    t0 = time.perf_counter()
+    h = torch.empty_like(state.y)
+    x = qzeros(state.y.shape[2], state.w.shape[2])
+    c = L.PseudoQrConfig(qr_cfg.max_correction_steps, qr_cfg.power_iters_for_epsilon, qr_cfg.delta_budget)
+    rep = L.Report()
+    ctx._check(ctx.lib.qlra_qb_stage_with_psi(ctx.h, C.byref(_qm(psi)), C.byref(_qm(state.y)),
+                                              C.byref(_qm(state.w)), method, rangefinder_seed, C.byref(c),
+                                              C.byref(_qm(h)), C.byref(_qm(x)), C.byref(rep)))
+    ctx.synchronize()
+    steps = rep.correction_steps_used if method == PSEUDO_QR else 0
+    return QbResult(h, x, RangefinderReport(h, rep.kappa_before, rep.kappa_after, steps, method),
+                    time.perf_counter() - t0, 0.0)
 
 
 def residual_fro(a, h, x, ctx=None):
@@ -671,7 +738,9 @@ def one_pass_approx(a, opts: OnePassOptions, ctx=None) -> ApproxResult:
     st = make_sketch(a, o.r, o.s, o.l, o.omega_seed, o.psi_seed, o.embedding, o.density, ctx)
     ctx.synchronize()
     t1 = time.perf_counter()
-    qb = qb_stage(st, o.rangefinder, o.rangefinder_seed, o.qr_cfg, ctx)
+    # the rangefinder and the solve as two calls, timed apart like the
+    # reference's StageTimes (sketching.cpp:176-186)
+    qb = qb_stage(st, o.rangefinder, o.rangefinder_seed, o.qr_cfg, ctx, split=True)
     t2 = time.perf_counter()
     res = truncate_stage(qb.h, qb.x, o.r, ctx)
     ctx.synchronize()
@@ -693,7 +762,7 @@ def one_pass_approx_from_sketch(state: SketchState, opts: OnePassOptions, ctx=No
     the residual diagnostics are absent."""
     ctx = _ctx(ctx)
     o = resolve_defaults(opts)
-    qb = qb_stage(state, o.rangefinder, o.rangefinder_seed, o.qr_cfg, ctx)
+    qb = qb_stage(state, o.rangefinder, o.rangefinder_seed, o.qr_cfg, ctx, split=True)
     t0 = time.perf_counter()
     res = truncate_stage(qb.h, qb.x, o.r, ctx)
     ctx.synchronize()
@@ -739,10 +808,14 @@ def write_sketch(path, st: SketchState, ctx=None):
 def read_sketch(path, ctx=None) -> SketchState:
     """read_sketch (io.cpp:130-145)."""
     ctx = _ctx(ctx)
-    om, ps, rsl = L.Spec(), L.Spec(), (C.c_int64 * 3)()
+    om, ps, rsl, dims = L.Spec(), L.Spec(), (C.c_int64 * 3)(), (C.c_int64 * 4)()
     if L.lib().qlra_sketch_file_header(str(path).encode(), C.byref(om), C.byref(ps), rsl) != 0:
         raise IoError(f"not a readable QSKT1 file: {path}")
-    st = SketchState(qzeros(ps.cols, om.cols), qzeros(ps.rows, om.rows), _spec_from_c(om), _spec_from_c(ps),
+    # Y and W are sized from their own QMAT1 headers, validated before any
+    # allocation (io.cpp:130-145)
+    if L.lib().qlra_sketch_file_dims(str(path).encode(), dims) != 0:
+        raise IoError("read_sketch: inconsistent dimensions")
+    st = SketchState(qzeros(dims[0], dims[1]), qzeros(dims[2], dims[3]), _spec_from_c(om), _spec_from_c(ps),
                      rsl[0], rsl[1], rsl[2])
     ctx._check(ctx.lib.qlra_read_sketch(ctx.h, str(path).encode(), C.byref(_qm(st.y)), C.byref(_qm(st.w))))
     return st

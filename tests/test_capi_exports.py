@@ -26,3 +26,51 @@ def test_header_is_plain_c():
 
 def test_kernel_name_without_gpu():
     assert _lib.lib().qlra_sketch_kernel_name().decode()
+
+
+def test_local_group_lifecycle_without_gpu():
+    """qlra_group_t is host-side state: creation limits and destruction need no
+    device (its contexts do)."""
+    L = _lib.lib()
+    h = ctypes.c_void_p()
+    assert L.qlra_group_create(ctypes.byref(h), 0) == 2  # QLRA_ERR_PARAMETER
+    assert L.qlra_group_create(ctypes.byref(h), 17) == 2
+    assert L.qlra_group_create(ctypes.byref(h), 4) == 0 and h.value
+    assert L.qlra_group_destroy(h) == 0
+    assert L.qlra_group_destroy(None) == 0
+
+
+def _qskt(path, y_shape, w_shape, s, l, truncate=0):
+    """A QSKT1 file (io.cpp:116-128) with the given embedded shapes."""
+    import struct
+
+    def spec(kind, rows, cols, seed):
+        return struct.pack("<IQQQd", kind, rows, cols, seed, 1.0)
+    b = b"QSKT1\0" + spec(0, 9, s, 1) + spec(0, l, 9, 2) + struct.pack("<QQQ", 1, s, l)
+    for r, c in (y_shape, w_shape):
+        b += b"QMAT1\0" + struct.pack("<QQ", r, c) + bytes(32 * r * c)
+    with open(path, "wb") as f:
+        f.write(b[:len(b) - truncate] if truncate else b)
+
+
+def test_sketch_file_dims_validates_before_allocating(tmp_path):
+    """read_sketch sizes Y and W from their own QMAT1 headers and applies the
+    reference's consistency test (io.cpp:130-145) -- no device, no context."""
+    L = _lib.lib()
+    dims = (ctypes.c_int64 * 4)()
+    p = tmp_path / "ok.qskt"
+    _qskt(p, (9, 3), (6, 9), 3, 6)
+    assert L.qlra_sketch_file_dims(str(p).encode(), dims) == 0 and list(dims) == [9, 3, 6, 9]
+    # y rows need not equal the Psi spec's cols (the reference reads headers)
+    _qskt(p, (5, 3), (6, 9), 3, 6)
+    assert L.qlra_sketch_file_dims(str(p).encode(), dims) == 0 and dims[0] == 5
+    _qskt(p, (9, 4), (6, 9), 3, 6)  # y.cols != s
+    assert L.qlra_sketch_file_dims(str(p).encode(), dims) == 6  # QLRA_ERR_IO
+    _qskt(p, (9, 3), (6, 9), 3, 6, truncate=40)
+    assert L.qlra_sketch_file_dims(str(p).encode(), dims) == 6
+    with open(p, "r+b") as f:  # absurd header: huge rows -> IoError, not an allocation
+        import struct
+        _qskt(p, (9, 3), (6, 9), 3, 6)
+        f.seek(6 + 72 + 24 + 6)
+        f.write(struct.pack("<Q", 1 << 60))
+    assert L.qlra_sketch_file_dims(str(p).encode(), dims) == 6

@@ -72,5 +72,9 @@ def test_cli_sketch_update_approx(ctx, tmp_path, capsys):
     assert cli.main(["approx", "--sketch", str(tmp_path / "A.qskt"), "-r", "5"]) == 0
     printed = capsys.readouterr().out.splitlines()
     assert printed[0] == cli.APPROX_CSV_HEADER and printed[1].split(",")[3] == "nan"
-    # exactly one of --input / --sketch
-    assert cli.main(["approx", "-r", "5"]) == 1
+    # exactly one of --input / --sketch; failures print "error: <what>" and
+    # exit 2 (qlra_main.cpp:508-511)
+    assert cli.main(["approx", "-r", "5"]) == 2
+    assert capsys.readouterr().err.startswith("error: approx: pass exactly one of --input or --sketch")
+    # t_solve_s is measured (the rangefinder and the solve are timed apart)
+    assert all(float(r["t_solve_s"]) > 0.0 for r in rows)

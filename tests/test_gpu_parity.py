@@ -13,7 +13,7 @@ import torch
 from oracle import oracle as O
 from tests.helpers import (diag_real, largest_principal_angle, orthonormality_defect,
                            planted_conditioned_matrix, planted_matrix_with_sigma, random_gaussian,
-                           rel_diff, scalar)
+                           rel_diff, scalar, to_full)
 
 pytestmark = pytest.mark.gpu
 
@@ -208,6 +208,48 @@ def test_pseudo_qr_kappa_1e6(ctx):  # test_rangefinders.cpp:35-41
     assert largest_principal_angle(host(rep.h), y) < 1e-8
     assert largest_principal_angle(host(rep.h), orc["h"]) < 1e-8
     assert abs(rep.kappa_before / orc["kappa_before"] - 1) < 1e-3
+
+
+def _rcond1_chi_gram(h):
+    """Exact 1-norm reciprocal condition of chi(H^* H) (numpy): what the
+    reference's LU rcond estimate approximates from above."""
+    chi = to_full(h)
+    g = chi.conj().T @ chi
+    return 1.0 / (np.abs(g).sum(0).max() * np.abs(np.linalg.inv(g)).sum(0).max())
+
+
+@pytest.mark.parametrize("kappa", np.logspace(6, 9, 13))
+def test_pseudo_qr_refusal_sweep(ctx, kappa):
+    """kappa(Y) in [1e6, 1e9] (kappa(H0) ~ 2e5 .. 2e8): the device accepts or
+    refuses (RankError) exactly where the reference's algorithm (oracle, same
+    Y) does.  The binding test is correction_step's square solve, LU rcond of
+    chi(H^*H) > 1e-14 (complex_bridge.cpp:73-77) -- rcond_1 ~ 0.2 / kappa(H)^2,
+    so the reference refuses from kappa(H0) ~ 4.5e6, not 1e7.  Inputs whose
+    rcond lies within 1.5x of a threshold are reported, not asserted (the
+    estimators differ there by up to 1.3x and G's rounding moves it ~1e-1)."""
+    from paper_2404_14783_b200 import qlra as Q
+    y = planted_conditioned_matrix(240, 24, kappa, 101)
+    h0 = O.pseudo_qr(y, max_steps=0)["h"]
+    rc1 = _rcond1_chi_gram(h0)
+    near = min(abs(np.log(rc1 / 1e-14)), abs(np.log(rc1 / 1e-15))) < np.log(1.5)
+    try:
+        orc = O.pseudo_qr(y)
+    except O.OracleError as e:
+        assert e.kind == "RankError"
+        orc = None
+    try:
+        rep = Q.pseudo_qr(dev(y), ctx=ctx)
+    except Q.RankError:
+        rep = None
+    print(f"kappa(Y) {kappa:.2e}: rcond1 {rc1:.3e} near={near} oracle "
+          f"{'refuses' if orc is None else 'kappa %.6e steps %d' % (orc['kappa_before'], orc['correction_steps_used'])}"
+          f" device {'refuses' if rep is None else 'kappa %.6e steps %d' % (rep.kappa_before, rep.correction_steps_used)}")
+    if not near:
+        assert (orc is None) == (rep is None)
+    if orc is not None and rep is not None:
+        assert rep.correction_steps_used == orc["correction_steps_used"]
+        assert abs(rep.kappa_before / orc["kappa_before"] - 1) < 1e-4
+        assert largest_principal_angle(host(rep.h), orc["h"]) < 1e-8 * max(1.0, kappa / 1e8)
 
 
 def test_pseudo_qr_errors(ctx):  # test_rangefinders.cpp:43-52
