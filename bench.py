@@ -40,6 +40,7 @@ def parse():
     p.add_argument("--rangefinder", default="pseudo_qr", choices=["pseudo_qr", "pseudo_svd"])
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-pageable", action="store_true", help="skip the pageable-host e2e variant")
     p.add_argument("--cpu-worker", default=None, help=argparse.SUPPRESS)  # cpu_baseline child process
     return p.parse_args()
 
@@ -375,7 +376,7 @@ def main():
     res, an = Q.residual_fro(a, qb.h, qb.x, ctx)
 
     # e2e: A from pinned host memory through the public API, H and X back
-    e2e = None
+    e2e = e2e_pageable = None
     if not args.no_e2e:
         a_host = torch.empty(a.shape, dtype=torch.float64, pin_memory=True)
         a_host.copy_(a)
@@ -422,7 +423,33 @@ def main():
             dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
         e2e = {"value": float(e2e_ms) / 1e3, "unit": "s",
                "h2d_bytes_per_step": int(32 * (r1 - r0) * cfg.n),
-               "d2h_bytes_per_step": int(32 * ((r1 - r0) * cfg.s + cfg.s * cfg.n))}
+               "d2h_bytes_per_step": int(32 * ((r1 - r0) * cfg.s + cfg.s * cfg.n)),
+               "host_memory": "pinned"}
+        if not args.no_pageable:
+            # the same call from PAGEABLE host memory (a reference QMatrix's
+            # std::vector planes): the library stages it through pinned
+            # buffers on host threads, overlapped with the DMA and the sketch
+            a_page = torch.empty(a_host.shape, dtype=torch.float64)
+            a_page.copy_(a_host)
+            assert not a_page.is_pinned()
+            for _ in range(max(1, args.warmup // 2)):
+                Q.one_pass_qb_host(a_page, e2e_opts, ctx=ctx, row0=r0, m_global=cfg.m, h_out=h_host, x_out=x_host)
+            barrier()
+            gc.collect()
+            gc.disable()
+            p0 = torch.cuda.Event(enable_timing=True)
+            p1 = torch.cuda.Event(enable_timing=True)
+            p0.record(stream)
+            for _ in range(args.steps):
+                Q.one_pass_qb_host(a_page, e2e_opts, ctx=ctx, row0=r0, m_global=cfg.m, h_out=h_host, x_out=x_host)
+            p1.record(stream)
+            barrier()
+            gc.enable()
+            pg_ms = torch.tensor([p0.elapsed_time(p1) / args.steps], dtype=torch.float64, device="cuda")
+            if world > 1:
+                dist.all_reduce(pg_ms, op=dist.ReduceOp.MAX)
+            e2e_pageable = dict(e2e, value=float(pg_ms) / 1e3, host_memory="pageable (staged by the library)")
+            del a_page
         a = a_host.to("cuda")
 
     peaks = {"dfma_tflops": Q.measure_fp64_peak(0, 300.0, ctx), "dmma_tflops": Q.measure_fp64_peak(1, 300.0, ctx)}
@@ -475,7 +502,7 @@ def main():
                                   "of A (<= 2 GB): rows*n*(s+l) quaternion MACs.  traffic: DRAM bytes per "
                                   "launch from the committed ncu capture of this config "
                                   "(profiles/sketch_traffic_<config>.json), else null")},
-            "rangefinder_used": used["rangefinder"], "rel_error": res / an, "e2e": e2e, "gpu_launches": int(launches), "clocks": clk.summary(),
+            "rangefinder_used": used["rangefinder"], "rel_error": res / an, "e2e": e2e, "e2e_pageable": e2e_pageable, "gpu_launches": int(launches), "clocks": clk.summary(),
             "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)

@@ -25,6 +25,7 @@
 // tests/golden/ref_kat.json); everything else is pinned by the reference's
 // known-answer and property tests ported to tests/test_oracle_*.py.
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <complex>
@@ -64,6 +65,8 @@ void zunmqr_(const char* side, const char* trans, const int* m, const int* n, co
 void ztrsm_(const char* side, const char* uplo, const char* transa, const char* diag,
             const int* m, const int* n, const cd* alpha, const cd* a, const int* lda, cd* b,
             const int* ldb, std::size_t, std::size_t, std::size_t, std::size_t);
+void openblas_set_num_threads(int);
+int openblas_get_num_threads(void);
 void dgemm_(const char* ta, const char* tb, const int* m, const int* n, const int* k,
             const double* alpha, const double* a, const int* lda, const double* b,
             const int* ldb, const double* beta, double* c, const int* ldc, std::size_t,
@@ -456,15 +459,135 @@ CM cm_mul(const CM& a, const CM& b, char ta = 'N') {  // op(a) * b
   (void)0;
   return c;
 }
+// Long vectors (the 2m-long compact columns of C4 / C5 sketches) are reduced
+// by OpenMP threads in a fixed static partition: deterministic, and equal to
+// the serial sum to rounding -- these helpers are only the oracle's speed.
+constexpr Index kParLen = 1 << 16;
 cd dotc(const cd* q, const cd* v, Index n) {  // Eigen q.dot(v) = q^H v
-  cd s(0.0, 0.0);
-  for (Index i = 0; i < n; ++i) s += std::conj(q[i]) * v[i];
-  return s;
+  if (n < kParLen) {
+    cd s(0.0, 0.0);
+    for (Index i = 0; i < n; ++i) s += std::conj(q[i]) * v[i];
+    return s;
+  }
+  double re = 0.0, im = 0.0;
+#pragma omp parallel for schedule(static) reduction(+ : re, im)
+  for (Index i = 0; i < n; ++i) {
+    const cd t = std::conj(q[i]) * v[i];
+    re += t.real();
+    im += t.imag();
+  }
+  return cd(re, im);
 }
 double norm2(const cd* v, Index n) {
   double s = 0.0;
+  if (n < kParLen) {
+    for (Index i = 0; i < n; ++i) s += std::norm(v[i]);
+    return std::sqrt(s);
+  }
+#pragma omp parallel for schedule(static) reduction(+ : s)
   for (Index i = 0; i < n; ++i) s += std::norm(v[i]);
   return std::sqrt(s);
+}
+// v -= q * d
+void axpy_sub(cd* v, const cd* q, cd d, Index n) {
+  if (n < kParLen) {
+    for (Index i = 0; i < n; ++i) v[i] -= q[i] * d;
+    return;
+  }
+#pragma omp parallel for schedule(static)
+  for (Index i = 0; i < n; ++i) v[i] -= q[i] * d;
+}
+
+// Communication-avoiding QR of a tall matrix (TSQR): cache-sized row blocks
+// are factored in parallel (zgeqrf per block, single-threaded BLAS inside),
+// their R factors stacked and factored the same way (recursively), and
+// Q = diag(Q_i) Q_stack.  Backward stable like one Householder QR of the
+// whole; LAPACK's zgeqrf on a 4M x 80 panel is level-2 and memory-bound
+// (~50 s), this is ~20x faster.  R's diagonal phases are arbitrary; callers
+// normalise them.  Only the oracle's speed: the factorisations it feeds are
+// the reference's.
+bool tsqr_applies(Index m, Index n) { return n > 0 && m >= 32 * n && m * n >= (Index(1) << 22); }
+void householder_qr(CM& b, std::vector<cd>& tau, CM* q) {  // b is overwritten (R in its upper part)
+  const int M = static_cast<int>(b.rows), N = static_cast<int>(b.cols);
+  int info = 0, lwork = -1;
+  cd wq;
+  tau.assign(std::max(1, N), cd(0.0, 0.0));
+  zgeqrf_(&M, &N, b.a.data(), &b.ld(), tau.data(), &wq, &lwork, &info);
+  lwork = std::max(1, static_cast<int>(wq.real()));
+  std::vector<cd> work(lwork);
+  zgeqrf_(&M, &N, b.a.data(), &b.ld(), tau.data(), work.data(), &lwork, &info);
+  if (!q) return;
+  *q = b;
+  lwork = -1;
+  zungqr_(&M, &N, &N, q->a.data(), &q->ld(), tau.data(), &wq, &lwork, &info);
+  lwork = std::max(1, static_cast<int>(wq.real()));
+  work.assign(lwork, cd(0.0, 0.0));
+  zungqr_(&M, &N, &N, q->a.data(), &q->ld(), tau.data(), work.data(), &lwork, &info);
+}
+template <class F>
+void parallel_blocks(Index nb, F&& f) {
+  const int hw = std::max(1, static_cast<int>(std::thread::hardware_concurrency()));
+  const int T = static_cast<int>(std::min<Index>(hw, nb));
+  std::atomic<Index> next{0};
+  const int saved = openblas_get_num_threads();
+  openblas_set_num_threads(1);
+  auto body = [&] {
+    for (Index i = next++; i < nb; i = next++) f(i);
+  };
+  std::vector<std::thread> ts;
+  for (int t = 1; t < T; ++t) ts.emplace_back(body);
+  body();
+  for (auto& t : ts) t.join();
+  openblas_set_num_threads(saved);
+}
+void tsqr(const CM& a, CM* q, CM* r) {
+  const Index m = a.rows, n = a.cols;
+  const Index B = std::max<Index>(4096, 8 * n);
+  const Index nb = (m + B - 1) / B;
+  if (nb <= 1) {
+    CM b = a;
+    std::vector<cd> tau;
+    householder_qr(b, tau, q);
+    *r = CM(n, n);
+    for (Index j = 0; j < n; ++j)
+      for (Index i = 0; i <= std::min(j, m - 1); ++i) (*r)(i, j) = b(i, j);
+    return;
+  }
+  std::vector<CM> blk(nb);
+  std::vector<std::vector<cd>> tau(nb);
+  CM s(nb * n, n);
+  parallel_blocks(nb, [&](Index t) {
+    const Index r0 = t * B, r1 = std::min(m, r0 + B), rows = r1 - r0;
+    CM b(rows, n);
+    for (Index j = 0; j < n; ++j) std::copy(a.col(j) + r0, a.col(j) + r1, b.col(j));
+    householder_qr(b, tau[t], nullptr);
+    for (Index j = 0; j < n; ++j)
+      for (Index i = 0; i <= std::min(j, rows - 1); ++i) s(t * n + i, j) = b(i, j);
+    blk[t] = std::move(b);
+  });
+  CM qs;
+  tsqr(s, q ? &qs : nullptr, r);
+  if (!q) return;
+  *q = CM(m, n);
+  parallel_blocks(nb, [&](Index t) {
+    const Index r0 = t * B, rows = blk[t].rows;
+    CM& b = blk[t];
+    const int M = static_cast<int>(rows), N = static_cast<int>(n);
+    int info = 0, lwork = -1;
+    cd wq;
+    // Q_t * (Q_stack rows of block t): apply the block's reflectors to them
+    CM c(rows, n);
+    for (Index j = 0; j < n; ++j)
+      for (Index i = 0; i < std::min(n, rows); ++i) c(i, j) = qs(t * n + i, j);
+    const int K = static_cast<int>(std::min(n, rows));
+    zunmqr_("L", "N", &M, &N, &K, b.a.data(), &b.ld(), tau[t].data(), c.a.data(), &c.ld(), &wq, &lwork, &info,
+            1, 1);
+    lwork = std::max(1, static_cast<int>(wq.real()));
+    std::vector<cd> work(lwork);
+    zunmqr_("L", "N", &M, &N, &K, b.a.data(), &b.ld(), tau[t].data(), c.a.data(), &c.ld(), work.data(), &lwork,
+            &info, 1, 1);
+    for (Index j = 0; j < n; ++j) std::copy(c.col(j), c.col(j) + rows, q->col(j) + r0);
+  });
 }
 
 // ------------------------------------------------------ factorizations ---
@@ -476,6 +599,20 @@ ComplexQr complex_qr(const CM& mat) {
   if (mat.rows < mat.cols) shape("complex_qr: requires rows >= cols");
   const int m = static_cast<int>(mat.rows), n = static_cast<int>(mat.cols);
   ComplexQr out;
+  if (tsqr_applies(m, n)) {
+    tsqr(mat, &out.q, &out.r);
+    // the same phase convention as below (diag(R) real >= 0)
+    for (int k = 0; k < n; ++k) {
+      const cd d = out.r(k, k);
+      const double ad = std::abs(d);
+      if (ad > 0.0) {
+        const cd phase = d / ad;
+        for (int j = 0; j < n; ++j) out.r(k, j) *= std::conj(phase);
+        for (int i = 0; i < m; ++i) out.q(i, k) *= phase;
+      }
+    }
+    return out;
+  }
   CM a = mat;
   std::vector<cd> tau(std::max(1, n));
   int info = 0, lwork = -1;
@@ -516,19 +653,39 @@ struct ComplexSvd {
   std::vector<double> s;
   CM v;
 };
-ComplexSvd complex_svd(const CM& mat) {
+// want_u = false: singular values and V only (condition_number,
+// singular_values), U left zero.
+ComplexSvd complex_svd(const CM& mat, bool want_u = true) {
   const int m = static_cast<int>(mat.rows), n = static_cast<int>(mat.cols);
   const int k = std::min(m, n);
   ComplexSvd out;
-  out.u = CM(m, k);
+  out.u = CM(want_u || !tsqr_applies(m, n) ? m : 0, k);
   out.v = CM(n, k);
   out.s.assign(k, 0.0);
   if (k == 0) return out;
+  if (tsqr_applies(m, n)) {
+    // zgesdd's own path for m >> n (QR, SVD of R, U = Q U_R) with the QR
+    // done by TSQR
+    CM q, r;
+    tsqr(mat, want_u ? &q : nullptr, &r);
+    ComplexSvd sr = complex_svd(r);
+    out.s = std::move(sr.s);
+    out.v = std::move(sr.v);
+    if (want_u) {
+      const cd one(1.0, 0.0), zero(0.0, 0.0);
+      zgemm_("N", "N", &m, &n, &n, &one, q.a.data(), &q.ld(), sr.u.a.data(), &sr.u.ld(), &zero,
+             out.u.a.data(), &out.u.ld(), 1, 1);
+    }
+    return out;
+  }
   CM a = mat;
   CM vt(k, n);
   const int lda = a.ld(), ldu = out.u.ld(), ldvt = vt.ld();  // copies
-  const std::size_t lrw = static_cast<std::size_t>(k) *
-                          std::max(5 * k + 7, 2 * std::max(m, n) + 2 * k + 1);
+  // LRWORK of zgesdd (LAPACK >= 3.7): 5 mn^2 + 5 mn when mx >> mn, else
+  // max(5 mn^2 + 5 mn, 2 mx mn + 2 mn^2 + mn)
+  const std::size_t mn = static_cast<std::size_t>(k), mx = static_cast<std::size_t>(std::max(m, n));
+  const std::size_t lrw = (mx * 9 >= mn * 17) ? 5 * mn * mn + 5 * mn
+                                              : std::max(5 * mn * mn + 5 * mn, 2 * mx * mn + 2 * mn * mn + mn);
   std::vector<double> rwork(std::max<std::size_t>(1, lrw));
   std::vector<int> iwork(8 * k);
   int info = 0, lwork = -1;
@@ -579,7 +736,7 @@ Vec orthogonalize(Vec v, const std::vector<Vec>& basis) {  // factorizations.cpp
   for (int pass = 0; pass < 2; ++pass)
     for (const auto& q : basis) {
       const cd d = dotc(q.data(), v.data(), n);
-      for (Index i = 0; i < n; ++i) v[i] -= q[i] * d;
+      axpy_sub(v.data(), q.data(), d, n);
     }
   return v;
 }
@@ -657,7 +814,7 @@ CM select_bad_representatives(const CM& ub, Index s_total, const CM& context,
 std::vector<double> singular_values(const QM& a) {
   const Index k = std::min(a.rows, a.cols);
   if (k == 0) return {};
-  const ComplexSvd svd = complex_svd(to_full(a));
+  const ComplexSvd svd = complex_svd(to_full(a), /*want_u=*/false);
   std::vector<double> out(k);
   for (Index i = 0; i < k; ++i) out[i] = svd.s[2 * i];
   return out;
@@ -665,7 +822,7 @@ std::vector<double> singular_values(const QM& a) {
 double condition_number(const QM& a) {
   const Index k = std::min(a.rows, a.cols);
   if (k == 0) return std::numeric_limits<double>::infinity();
-  const ComplexSvd svd = complex_svd(to_full(a));
+  const ComplexSvd svd = complex_svd(to_full(a), /*want_u=*/false);
   const double smin = svd.s[2 * k - 1];
   if (!(smin > 0.0)) return std::numeric_limits<double>::infinity();
   return svd.s[0] / smin;
@@ -901,7 +1058,7 @@ QM assemble_orthonormal_basis(const QM& y, std::uint64_t seed) {
     for (int pass = 0; pass < 2; ++pass)
       for (const auto& q : basis) {
         const cd d = dotc(q.data(), u.data(), chi.rows);
-        for (Index i = 0; i < chi.rows; ++i) u[i] -= q[i] * d;
+        axpy_sub(u.data(), q.data(), d, chi.rows);
       }
     const double nu = norm2(u.data(), chi.rows);
     for (auto& x : u) x /= nu;

@@ -387,11 +387,20 @@ int cqr2_status(Ctx& ctx, const Cqr2Pending& p, std::vector<double>* rdiag) {
 // breakdown of pass 1 falls back to the general path (shifted CholeskyQR3).
 // gram1 (optional): the already reduced Gram of y (quaternion; the complex
 // part is taken here when complex_mode), saving the first tall product.
+// QLRA_CQR_SHIFTED=1 (A/B of the rangefinders' accuracy only): always the
+// shifted CholeskyQR3.
+bool cqr_force_shift() {
+  static const bool v = [] {
+    const char* e = std::getenv("QLRA_CQR_SHIFTED");
+    return e && std::atoi(e) != 0;
+  }();
+  return v;
+}
 bool cholesky_qr(Ctx& ctx, const QView& y, const QView& h, bool complex_mode, int64_t m_global,
                  std::vector<double>* rdiag, bool distributed = true, DevQMat* rinv = nullptr,
                  DevQMat* rfac = nullptr, DeferredQ* defer = nullptr, const QView* gram1 = nullptr) {
   const int64_t s = y.cols;
-  if (s == 0 || s > chol_inv_async_max())
+  if (s == 0 || s > chol_inv_async_max() || cqr_force_shift())
     return cholesky_qr_general(ctx, y, h, complex_mode, m_global, rdiag, distributed, rinv, rfac, defer);
   Cqr2Pending p;
   cqr2_enqueue(ctx, y, h, complex_mode, distributed, gram1, /*form_q=*/!defer, p);
@@ -433,7 +442,13 @@ bool cholesky_qr_general(Ctx& ctx, const QView& y, const QView& h, bool complex_
   auto pf = [&](int i) { return rfac ? &rf[i].v : nullptr; };
   std::vector<double> d1, d2, d3;
   double tr = 0.0;
-  if (cqr_pass(ctx, y, t1.v, complex_mode, 0.0, &d1, &tr, distributed, pi(0), pf(0))) {
+  if (cqr_force_shift()) {
+    DevQMat g(ctx, s, s);
+    if (distributed) gram(ctx, y, g.v);
+    else qgemm_gram(ctx, y, g.v);
+    const std::vector<double> dg = diag_to_host(ctx, g.v.p[0], g.v.ld, s);
+    for (double v : dg) tr += v;
+  } else if (cqr_pass(ctx, y, t1.v, complex_mode, 0.0, &d1, &tr, distributed, pi(0), pf(0))) {
     const QView* last_inv = defer ? &defer->rinv_last.v : pi(1);
     if (!cqr_pass(ctx, t1.v, hq, complex_mode, 0.0, &d2, nullptr, distributed, last_inv, pf(1))) return false;
     if (defer && rinv) copy_qmat(ctx, defer->rinv_last.v, ri[1].v);
@@ -499,8 +514,9 @@ std::vector<double> gram_spectrum(Ctx& ctx, const QView& a, const QView& g, bool
   if (!(kappa_from_eigs(lam) > kRefineKappa) || a.cols == 0) return lam;
   if (rinv_in && rinv_in->buf.ptr) return refine_with_rinv(ctx, lam, rinv_in->v);
   DevQMat rinv;
+  DeferredQ no_q;  // only R^{-1} is needed: Q is never formed
   if (!cholesky_qr(ctx, a, QView{}, /*complex_mode=*/false, global_rows(ctx, a.rows), nullptr,
-                   /*distributed=*/true, &rinv))
+                   /*distributed=*/true, &rinv, nullptr, &no_q))
     return lam;  // not factorable: kappa beyond what any Gram route resolves
   return refine_with_rinv(ctx, lam, rinv.v);
 }
@@ -1140,7 +1156,11 @@ void pseudo_svd_dev(Ctx& c, const QView& Y, const QView& H, uint64_t seed, qlra_
     lam = eig.get();
   }
   r.kappa_before = kappa_from_eigs(lam);
-  if (!std::isfinite(r.kappa_before) || !qr_ok)
+  static const bool force_graded = [] {  // QLRA_PSVD_GRADED=1: A/B of the graded route only
+    const char* e = std::getenv("QLRA_PSVD_GRADED");
+    return e && std::atoi(e) != 0;
+  }();
+  if (!std::isfinite(r.kappa_before) || !qr_ok || force_graded)
     r.kappa_before = pseudo_svd_graded(c, Y, H, m, global_row0(c, Y.rows), seed);
   else if (r.kappa_before > kRefineKappa)  // kappa(Y) to ~u kappa(Y), not u kappa(Y)^2
     r.kappa_before = kappa_from_eigs(refine_with_rinv(c, lam, rinv.v));
@@ -1813,6 +1833,25 @@ static void qsvd_dev(Ctx& c, const QView& a, const QView& u, const QView& v, dou
     qgemm(c, QLRA_OP_C, QLRA_OP_N, 1.0, a, a, 0.0, g.v);
   DeviceBuffer w(c, sizeof(double) * (size_t)k);
   small_quat_eigh(c, g.v, w.as<double>(), e.v);
+  // Second pass: B = E^* A (wide; A E when tall) has nearly orthogonal rows
+  // (columns) of norms sigma_i, computed with absolute error ~u sigma_1, so
+  // the eigenvalues of its (nearly diagonal) Gram carry sigma_i to relative
+  // accuracy ~u sigma_1 / sigma_i -- an SVD's accuracy -- where the first
+  // Gram's carry u (sigma_1 / sigma_i)^2.  E <- E E2 (the reference takes
+  // the factors from an SVD of chi(A), factorizations.cpp:166-295).
+  {
+    DevQMat b(c, wide ? k : m, wide ? n : k), e2(c, k, k), e12(c, k, k);
+    if (wide) {
+      qgemm(c, QLRA_OP_C, QLRA_OP_N, 1.0, e.v, a, 0.0, b.v);
+      qgemm(c, QLRA_OP_N, QLRA_OP_C, 1.0, b.v, b.v, 0.0, g.v);
+    } else {
+      qgemm(c, QLRA_OP_N, QLRA_OP_N, 1.0, a, e.v, 0.0, b.v);
+      qgemm(c, QLRA_OP_C, QLRA_OP_N, 1.0, b.v, b.v, 0.0, g.v);
+    }
+    small_quat_eigh(c, g.v, w.as<double>(), e2.v);
+    qgemm(c, QLRA_OP_N, QLRA_OP_N, 1.0, e.v, e2.v, 0.0, e12.v);
+    e = std::move(e12);
+  }
   std::vector<double> lam = to_host(c, w.as<double>(), (size_t)k);
   std::vector<double> sg(k);
   for (int64_t i = 0; i < k; ++i) sg[i] = std::sqrt(std::max(0.0, lam[i]));

@@ -116,8 +116,8 @@ void group_attach(Ctx& ctx, qlra_group* g, int rank) {
     if (e1 != cudaSuccess && e1 != cudaErrorPeerAccessAlreadyEnabled) QLRA_CUDA(e1);
     cudaGetLastError();
   }
-  QLRA_CUDA(cudaEventCreateWithFlags(&g->ready[rank], cudaEventDisableTiming));
-  QLRA_CUDA(cudaEventCreateWithFlags(&g->done[rank], cudaEventDisableTiming));
+  if (!g->ready[rank]) QLRA_CUDA(cudaEventCreateWithFlags(&g->ready[rank], cudaEventDisableTiming));
+  if (!g->done[rank]) QLRA_CUDA(cudaEventCreateWithFlags(&g->done[rank], cudaEventDisableTiming));
   g->devs[rank] = ctx.device;
   g->attached[rank] = 1;
   ctx.group = g;
@@ -125,13 +125,13 @@ void group_attach(Ctx& ctx, qlra_group* g, int rank) {
   ctx.nranks = g->n;
 }
 
+// A rank's events outlive its context: a slower peer may still enqueue its
+// wait on them after this rank has left the last collective.  They are
+// destroyed with the group.
 void group_detach(Ctx& ctx) {
   qlra_group* g = ctx.group;
   if (!g) return;
   std::lock_guard<std::mutex> lk(g->mu);
-  if (g->ready[ctx.rank]) cudaEventDestroy(g->ready[ctx.rank]);
-  if (g->done[ctx.rank]) cudaEventDestroy(g->done[ctx.rank]);
-  g->ready[ctx.rank] = g->done[ctx.rank] = nullptr;
   g->attached[ctx.rank] = 0;
   ctx.group = nullptr;
 }
@@ -160,6 +160,10 @@ int qlra_group_destroy(qlra_group_t* g) {
   if (!g) return QLRA_OK;
   for (int a : g->attached)
     if (a) return QLRA_ERR_PRECONDITION;  // contexts still attached
+  for (int r = 0; r < g->n; ++r) {
+    if (g->ready[r]) cudaEventDestroy(g->ready[r]);
+    if (g->done[r]) cudaEventDestroy(g->done[r]);
+  }
   delete g;
   return QLRA_OK;
 }

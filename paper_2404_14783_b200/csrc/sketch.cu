@@ -18,8 +18,9 @@
 // atomics.  Omega (n x s) and the Psi column slice (l x b) are generated on
 // device by K1 (embed.cu) from the reference's counter RNG.  The same
 // engine (launch8) runs the tall x small products of the rangefinders and
-// the core solve, and the Grams (gram8_kernel).  The 16-product
-// sketch_fused_kernel (qtile.cuh) stays selectable with QLRA_SKETCH16=1.
+// the core solve, and the Grams (gram8_kernel).  (The 16-product sketch
+// kernel of round 1 is gone: the 16-product engine, qtile.cuh, now only
+// serves qgemm.cu's products.)
 #include <array>
 #include <cstring>
 #include <thread>
@@ -46,96 +47,6 @@ using qt::BK;
 using qt::BM;
 using qt::BN;
 using qt::NT;
-
-struct FusedArgs {
-  qt::Operands yop;  // A_panel (k-fast) x Omega (j-fast): M = panel rows, N = s, K = n
-  qt::Operands wop;  // Psi_panel (k-fast) x A_panel (j-fast): M = l, N = n, K = panel rows
-  int64_t ky, kw;    // K extents
-  int y_tm, y_tn, zy;
-  int64_t ky_chunk;
-  int w_tm, w_tn, zw;
-  int64_t kw_chunk;
-  int y_tnf, w_tmf;  // full (no padding) Y column tiles / W row tiles
-  double* y[4];
-  int64_t ldy;
-  double* yp;  // [zy][4][My][Ny] partials when zy > 1
-  double* w[4];
-  int64_t ldw;
-  double* wp;  // [zw][4][l][n] partials when zw > 1
-};
-
-__device__ __forceinline__ void store_tile(const qt::Acc& acc, int64_t i0, int64_t j0, int64_t M,
-                                           int64_t N, double* const* c, int64_t ldc,
-                                           double* part, bool rmw) {
-#pragma unroll
-  for (int rb = 0; rb < qt::WRB; ++rb) {
-    const int64_t gi = i0 + qt::acc_row(rb);
-    if (gi >= M) continue;
-#pragma unroll
-    for (int cb = 0; cb < qt::WCB; ++cb)
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int64_t gj = j0 + qt::acc_col(cb) + h;
-        if (gj >= N) continue;
-        if (part) {
-#pragma unroll
-          for (int p = 0; p < 4; ++p) part[(int64_t)p * M * N + gi * N + gj] = acc[rb][cb][p][h];
-        } else {
-#pragma unroll
-          for (int p = 0; p < 4; ++p) {
-            double* dst = c[p] + gi * ldc + gj;
-            *dst = rmw ? *dst + acc[rb][cb][p][h] : acc[rb][cb][p][h];
-          }
-        }
-      }
-  }
-}
-
-// Task order = longest first (LPT list scheduling by the hardware CTA
-// dispatcher): full W tiles, full Y tiles, then the Y tiles of the padded
-// last column tile (s % 64 != 0) and the W tiles of the padded last row tile
-// (l % 64 != 0), whose out-of-range 8x8 blocks issue no DMMA (qtile.cuh).
-__global__ void __launch_bounds__(NT, 1) sketch_fused_kernel(FusedArgs f) {
-  extern __shared__ __align__(16) double smem[];
-  qt::Acc acc;
-  qt::zero_acc(acc);
-  const int nwf = f.w_tmf * f.w_tn * f.zw;
-  const int nyf = f.y_tm * f.y_tnf * f.zy;
-  const int nyp = f.y_tm * (f.y_tn - f.y_tnf) * f.zy;
-  int t = blockIdx.x;
-  bool is_w;
-  int tm, tn, z;
-  if (t < nwf) {
-    is_w = true;
-    z = t % f.zw; t /= f.zw;
-    tm = t % f.w_tmf; tn = t / f.w_tmf;  // a-tiles fastest: neighbours share A columns
-  } else if ((t -= nwf) < nyf) {
-    is_w = false;
-    z = t % f.zy; t /= f.zy;
-    tn = t % f.y_tnf; tm = t / f.y_tnf;
-  } else if ((t -= nyf) < nyp) {
-    is_w = false;
-    z = t % f.zy; t /= f.zy;
-    tn = f.y_tnf + t % (f.y_tn - f.y_tnf); tm = t / (f.y_tn - f.y_tnf);
-  } else {
-    t -= nyp;
-    is_w = true;
-    z = t % f.zw; t /= f.zw;
-    tm = f.w_tmf + t % (f.w_tm - f.w_tmf); tn = t / (f.w_tm - f.w_tmf);
-  }
-  if (!is_w) {
-    const int64_t kb = (int64_t)z * f.ky_chunk, ke = min(f.ky, kb + f.ky_chunk);
-    qt::mma_tile<false, false>(f.yop, smem, (int64_t)tm * BM, (int64_t)tn * BN, kb, ke, acc);
-    double* part = f.zy > 1 ? f.yp + (int64_t)z * 4 * f.yop.M * f.yop.N : nullptr;
-    store_tile(acc, (int64_t)tm * BM, (int64_t)tn * BN, f.yop.M, f.yop.N, f.y, f.ldy, part, true);
-  } else {
-    const int64_t kb = (int64_t)z * f.kw_chunk, ke = min(f.kw, kb + f.kw_chunk);
-    qt::mma_tile<false, false>(f.wop, smem, (int64_t)tm * BM, (int64_t)tn * BN, kb, ke, acc);
-    double* part = f.zw > 1 ? f.wp + (int64_t)z * 4 * f.wop.M * f.wop.N : nullptr;
-    store_tile(acc, (int64_t)tm * BM, (int64_t)tn * BN, f.wop.M, f.wop.N, f.w, f.ldw, part, true);
-  }
-}
-
 
 // ---- the 8-product path (qtile8.cuh) --------------------------------------
 // Y-tasks: 64x32 tiles of A * Omega~; W-tasks: 32x64 tiles of Psi~ * A.
@@ -382,17 +293,10 @@ __global__ void combine8_kernel(QView in, double* out, int64_t ld, int left, int
 
 }  // namespace
 
-bool sketch_use8() {
-  static const bool v = [] {
-    const char* e = std::getenv("QLRA_SKETCH16");
-    return !(e && std::atoi(e) != 0);
-  }();
-  return v;
-}
+bool sketch_use8() { return true; }
 
 const char* sketch_kernel_name() {
-  return sketch_use8() ? "sketch8_kernel(8-product quaternion GEMM on DMMA, 64x32/32x64 tiles, mbarrier ring, panels <= 2 GB)"
-                       : "sketch_fused_kernel(dmma_64x64x8, mbarrier ring, panels <= 2 GB)";
+  return "sketch8_kernel(8-product quaternion GEMM on DMMA, 64x32/32x64 tiles, TMA + mbarrier ring, panels <= 2 GB)";
 }
 
 namespace {
@@ -407,7 +311,6 @@ struct Geom {
   int ym, yn, wm, wn;
   bool ynarrow = false, wnarrow = false;  // remainder as 128x16 / 16x128 tiles (8-product TMA path)
 };
-constexpr Geom kGeom16{BM, BN, BM, BN};
 constexpr Geom kGeom8{Y8M, Y8N, W8M, W8N};
 // the narrow remainder tiles pay off when they hold at most half a regular
 // tile's columns (Y) / rows (W)
@@ -743,39 +646,9 @@ void launch8(Ctx& ctx, const Q8Part* y, const Q8Part* w, double alpha, double be
 // whose Psi columns are ps[:, pc0 : pc0 + ap.rows].
 void sketch_panel(Ctx& ctx, const Emb& e, int64_t pc0, const QView& ap, const QView& yv, const QView& w,
                   SketchWork& ws) {
-  const int64_t rp = ap.rows, n = ap.cols, s = e.om.cols, l = e.ps.rows;
-  if (e.om8) {
-    const Q8Part yp{ap, e.om8, e.om8_ld, 0, yv};
-    const Q8Part wq{ap, e.ps8, e.ps8_ld, pc0, w};
-    launch8(ctx, &yp, &wq, 1.0, 1.0, ws, true);
-    return;
-  }
-  FusedArgs f{};
-  for (int p = 0; p < 4; ++p) {
-    f.yop.a[p] = ap.p[p];
-    f.yop.b[p] = e.om.p[p];
-    f.wop.a[p] = e.ps.p[p] + pc0;  // Psi[:, pc0:pc0+rp]
-    f.wop.b[p] = ap.p[p];
-    f.y[p] = yv.p[p];
-    f.w[p] = w.p[p];
-  }
-  f.yop.a_si = ap.ld; f.yop.a_sk = 1; f.yop.b_sk = e.om.ld; f.yop.b_sj = 1;
-  f.yop.M = rp; f.yop.N = s;
-  f.wop.a_si = e.ps.ld; f.wop.a_sk = 1; f.wop.b_sk = ap.ld; f.wop.b_sj = 1;
-  f.wop.M = l; f.wop.N = n;
-  f.ky = n;
-  f.kw = rp;
-  f.ldy = yv.ld;
-  f.ldw = w.ld;
-  set_splits(f, kGeom16, rp, n, s, l, ctx, ws);
-  const int64_t ctas = (int64_t)f.y_tm * f.y_tn * f.zy + (int64_t)f.w_tm * f.w_tn * f.zw;
-  LaunchTimer lt(ctx);
-  sketch_fused_kernel<<<(unsigned)ctas, NT, qt::SMEM_BYTES, ctx.stream>>>(f);
-  QLRA_LAUNCH_CHECK();
-  count_launch();
-  lt.done(rp, n, s, l);
-  if (f.zy > 1) splitk_reduce(ctx, f.yp, f.zy, yv, 1.0, 1.0);
-  if (f.zw > 1) splitk_reduce(ctx, f.wp, f.zw, w, 1.0, 1.0);
+  const Q8Part yp{ap, e.om8, e.om8_ld, 0, yv};
+  const Q8Part wq{ap, e.ps8, e.ps8_ld, pc0, w};
+  launch8(ctx, &yp, &wq, 1.0, 1.0, ws, true);
 }
 
 // Plane combinations of an embedding for the 8-product engine.
@@ -793,7 +666,6 @@ void launch_combine8(Ctx& ctx, const QView& in, double* out, int64_t ld, bool le
 // kept combination buffer.
 void prepare_emb(Ctx& ctx, Emb& e, const qlra_spec_t& psi, int64_t row0) {
   ctx.comb_keep.psi_valid = false;
-  if (!sketch_use8()) return;
   e.om8_ld = (e.om.cols + 1) / 2 * 2;
   e.ps8_ld = (e.ps.cols + 1) / 2 * 2;
   const size_t no = (size_t)8 * e.om.rows * e.om8_ld, np = (size_t)8 * e.ps.rows * e.ps8_ld;
@@ -820,8 +692,6 @@ void prepare_emb(Ctx& ctx, Emb& e, const qlra_spec_t& psi, int64_t row0) {
 }
 
 void set_kernel_attrs() {
-  set_func_attr((const void*)sketch_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                (int)qt::SMEM_BYTES);
   set_func_attr((const void*)sketch8_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                 (int)qt8::SMEM_BYTES + 128);
   set_func_attr((const void*)gram8_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDynSmemMax);
