@@ -157,36 +157,27 @@ std::vector<double> quat_eigs(Ctx& ctx, const QView& g, bool extremes_only = tru
 }
 
 // All eigenvalues of a quaternion Hermitian G computed on a side stream and
-// read back asynchronously: the host issues other work on ctx.stream and
-// collects the values with get().  G is copied on ctx.stream first, so the
-// caller may overwrite it afterwards.
+// read back on demand: the host issues other work on ctx.stream and collects
+// the values with get().  G is copied on ctx.stream first, so the caller may
+// overwrite it afterwards.  Several may be pending at once (each owns its
+// device result; they run in order on the side stream).
 class SideEigs {
  public:
   SideEigs(Ctx& c, const QView& g) : c_(c), n_(g.rows) {
     if (!c.side) QLRA_CUDA(cudaStreamCreateWithFlags(&c.side, cudaStreamNonBlocking));
     side_ = c.side;
-    const size_t need = (size_t)std::max<int64_t>(1, n_);
-    if (c.side_pinned_n < need) {
-      if (c.side_pinned) QLRA_CUDA(cudaFreeHost(c.side_pinned));
-      c.side_pinned = nullptr;
-      c.side_pinned_n = 0;
-      QLRA_CUDA(cudaMallocHost(&c.side_pinned, sizeof(double) * std::max<size_t>(need, 1024)));
-      c.side_pinned_n = std::max<size_t>(need, 1024);
-    }
-    host_ = c.side_pinned;
     QLRA_CUDA(cudaEventCreateWithFlags(&fork_, cudaEventDisableTiming));
     QLRA_CUDA(cudaEventCreateWithFlags(&done_, cudaEventDisableTiming));
     work_ = DevQMat(c, n_, n_);
+    w_ = DeviceBuffer(c, sizeof(double) * (size_t)std::max<int64_t>(1, n_));
     copy_qmat(c, g, work_.v);
+    QLRA_CUDA(cudaMemsetAsync(w_.ptr, 0, w_.bytes, c.stream));
     QLRA_CUDA(cudaEventRecord(fork_, c.stream));
     QLRA_CUDA(cudaStreamWaitEvent(side_, fork_, 0));
     cudaStream_t main = c.stream;
     c.stream = side_;  // every launch and stream-ordered buffer below lives on side_
     try {
-      DeviceBuffer w(c, sizeof(double) * (size_t)std::max<int64_t>(1, n_));
-      QLRA_CUDA(cudaMemsetAsync(w.ptr, 0, w.bytes, c.stream));
-      small_quat_herm_eigvals(c, work_.v, w.as<double>(), /*extremes_only=*/false);
-      QLRA_CUDA(cudaMemcpyAsync(host_, w.ptr, sizeof(double) * (size_t)n_, cudaMemcpyDeviceToHost, c.stream));
+      small_quat_herm_eigvals(c, work_.v, w_.as<double>(), /*extremes_only=*/false);
     } catch (...) {
       c.stream = main;
       throw;
@@ -196,11 +187,12 @@ class SideEigs {
   }
   std::vector<double> get() {
     QLRA_CUDA(cudaEventSynchronize(done_));
-    return std::vector<double>(host_, host_ + n_);
+    std::vector<double> h((size_t)n_);
+    if (n_) QLRA_CUDA(cudaMemcpy(h.data(), w_.ptr, sizeof(double) * (size_t)n_, cudaMemcpyDeviceToHost));
+    return h;
   }
   ~SideEigs() {
-    if (done_) cudaStreamWaitEvent(c_.stream, done_, 0);  // work_ is released on ctx.stream
-    if (done_) cudaEventSynchronize(done_);                // the pinned buffer is reused
+    if (done_) cudaStreamWaitEvent(c_.stream, done_, 0);  // work_, w_ are released on ctx.stream
     if (fork_) cudaEventDestroy(fork_);
     if (done_) cudaEventDestroy(done_);
   }
@@ -212,8 +204,8 @@ class SideEigs {
   int64_t n_;
   cudaStream_t side_ = nullptr;
   cudaEvent_t fork_ = nullptr, done_ = nullptr;
-  double* host_ = nullptr;
   DevQMat work_;
+  DeviceBuffer w_;
 };
 
 double kappa_from_eigs(const std::vector<double>& ev) {
@@ -359,10 +351,10 @@ void cqr2_enqueue(Ctx& ctx, const QView& y, const QView& h, bool complex_mode, b
   } else {
     gram_of(y, g1.v);
   }
-  chol_inv_launch(ctx, g1.v, p.r1.v, p.r1inv.v, p.info.as<int>(), p.dg.as<double>());
+  chol_inv_any(ctx, g1.v, p.r1.v, p.r1inv.v, p.info.as<int>(), p.dg.as<double>());
   qgemm(ctx, QLRA_OP_N, QLRA_OP_N, 1.0, y, p.r1inv.v, 0.0, p.t1.v);
   gram_of(p.t1.v, g2.v);
-  chol_inv_launch(ctx, g2.v, p.r2.v, p.r2inv.v, p.info.as<int>() + 1, p.dg.as<double>() + s);
+  chol_inv_any(ctx, g2.v, p.r2.v, p.r2inv.v, p.info.as<int>() + 1, p.dg.as<double>() + s);
   if (form_q) qgemm(ctx, QLRA_OP_N, QLRA_OP_N, 1.0, p.t1.v, p.r2inv.v, 0.0, h);
 }
 // 0: both passes factored (rdiag = diag R1 .* diag R2); 1: pass 1 broke
@@ -400,7 +392,7 @@ bool cholesky_qr(Ctx& ctx, const QView& y, const QView& h, bool complex_mode, in
                  std::vector<double>* rdiag, bool distributed = true, DevQMat* rinv = nullptr,
                  DevQMat* rfac = nullptr, DeferredQ* defer = nullptr, const QView* gram1 = nullptr) {
   const int64_t s = y.cols;
-  if (s == 0 || s > chol_inv_async_max() || cqr_force_shift())
+  if (s == 0 || cqr_force_shift())
     return cholesky_qr_general(ctx, y, h, complex_mode, m_global, rdiag, distributed, rinv, rfac, defer);
   Cqr2Pending p;
   cqr2_enqueue(ctx, y, h, complex_mode, distributed, gram1, /*form_q=*/!defer, p);
@@ -500,10 +492,17 @@ bool cholesky_qr_general(Ctx& ctx, const QView& y, const QView& h, bool complex_
 
 // Refine the small end of a Gram spectrum lam (of G = A^*A, descending; all
 // values or extremes only) with rinv = R^{-1} of a QR factor of A.
-std::vector<double> refine_with_rinv(Ctx& ctx, const std::vector<double>& lam, const QView& rinv) {
+std::vector<double> refine_with_rinv(Ctx& ctx, const std::vector<double>& lam, const QView& rinv,
+                                     bool extremes_only = false) {
   const int64_t s = rinv.rows;
   DevQMat p(ctx, s, s);
   qgemm(ctx, QLRA_OP_N, QLRA_OP_C, 1.0, rinv, rinv, 0.0, p.v);  // (R^* R)^{-1}
+  if (extremes_only) {  // lambda_min = 1 / lambda_max((R^* R)^{-1})
+    const std::vector<double> mu = quat_eigs(ctx, p.v, /*extremes_only=*/true);
+    std::vector<double> out = lam;
+    if (!out.empty() && mu[0] > 0.0) out.back() = 1.0 / mu[0];
+    return out;
+  }
   const std::vector<double> mu = quat_eigs(ctx, p.v, /*extremes_only=*/false);
   return merge_spectra(lam, mu);
 }
@@ -512,13 +511,13 @@ std::vector<double> gram_spectrum(Ctx& ctx, const QView& a, const QView& g, bool
                                   const DevQMat* rinv_in) {
   std::vector<double> lam = quat_eigs(ctx, g, extremes_only);
   if (!(kappa_from_eigs(lam) > kRefineKappa) || a.cols == 0) return lam;
-  if (rinv_in && rinv_in->buf.ptr) return refine_with_rinv(ctx, lam, rinv_in->v);
+  if (rinv_in && rinv_in->buf.ptr) return refine_with_rinv(ctx, lam, rinv_in->v, extremes_only);
   DevQMat rinv;
   DeferredQ no_q;  // only R^{-1} is needed: Q is never formed
   if (!cholesky_qr(ctx, a, QView{}, /*complex_mode=*/false, global_rows(ctx, a.rows), nullptr,
                    /*distributed=*/true, &rinv, nullptr, &no_q))
     return lam;  // not factorable: kappa beyond what any Gram route resolves
-  return refine_with_rinv(ctx, lam, rinv.v);
+  return refine_with_rinv(ctx, lam, rinv.v, extremes_only);
 }
 
 // Orthonormal completion: c_out (rows x k, row-sharded from global row0)
@@ -558,6 +557,7 @@ void orthonormal_completion(Ctx& ctx, const QView& hr, const QView& c_out, int64
 // A kappa=1e12 sketch needs two levels.  Returns sqrt(lambda_1 / lambda_min)
 // over the kept directions when all s are kept (the sigma estimates of each
 // level are the singular values of the deflated remainder), else inf.
+constexpr double kGradedKappa = 1e6;
 double pseudo_svd_graded(Ctx& ctx, const QView& y, const QView& h, int64_t m_global, int64_t row0,
                          uint64_t seed) {
   const int64_t s = y.cols, rows = y.rows;
@@ -828,7 +828,7 @@ bool early_solve_close(Ctx& c, EarlySolve& es, DevQMat& z) {
   DevQMat g(c, s, s), r(c, s, s), ri(c, s, s), ginv(c, s, s);
   DeviceBuffer info(c, sizeof(int)), dg(c, sizeof(double) * (size_t)s);
   qgemm(c, QLRA_OP_C, QLRA_OP_N, 1.0, es.ck.v, es.ck.v, 0.0, g.v);
-  chol_inv_launch(c, g.v, r.v, ri.v, info.as<int>(), dg.as<double>());
+  chol_inv_any(c, g.v, r.v, ri.v, info.as<int>(), dg.as<double>());
   qgemm(c, QLRA_OP_N, QLRA_OP_C, 1.0, ri.v, ri.v, 0.0, ginv.v);
   z = DevQMat(c, s, s);
   qgemm(c, QLRA_OP_N, QLRA_OP_C, 1.0, ginv.v, es.ck.v, 0.0, z.v);
@@ -884,7 +884,8 @@ bool pqr_factors_fast(Ctx& c, const QView& Y, DeferredQ& q0, DevQMat& rq, DevQMa
   QLRA_CUDA(cudaEventCreateWithFlags(&cdone, cudaEventDisableTiming));
   QLRA_CUDA(cudaEventRecord(fork, c.stream));
   QLRA_CUDA(cudaStreamWaitEvent(c.side, fork, 0));
-  {
+  const bool side_chol = s <= chol_inv_async_max();
+  if (side_chol) {
     const cudaStream_t main = c.stream;
     c.stream = c.side;  // one launch, no split-K counters involved
     try {
@@ -917,11 +918,14 @@ bool pqr_factors_fast(Ctx& c, const QView& Y, DeferredQ& q0, DevQMat& rq, DevQMa
   if (es && c.nranks == 1 && es->psi->rows >= s && !std::getenv("QLRA_NO_EARLY_SOLVE"))
     early_solve_start(c, *es, q0);
   QLRA_CUDA(cudaStreamWaitEvent(c.stream, cdone, 0));
+  // (s past the single-launch Cholesky: the blocked form needs the main
+  // stream's split-K counters, so the complex pass-1 factor is taken here)
+  if (!side_chol) chol_inv_any(c, gc.v, r1c.v, r1c_inv.v, info_c.as<int>(), dg_c.as<double>());
   DevQMat t1c(c, s, s), g2(c, s, s), r2c(c, s, s), r2c_inv(c, s, s);
   qgemm(c, QLRA_OP_N, QLRA_OP_N, 1.0, rq.v, r1c_inv.v, 0.0, t1c.v);
   qgemm(c, QLRA_OP_C, QLRA_OP_N, 1.0, t1c.v, t1c.v, 0.0, g2.v);
   zero_jk_planes(c, g2.v);
-  chol_inv_launch(c, g2.v, r2c.v, r2c_inv.v, info_c.as<int>() + 1, dg_c.as<double>() + s);
+  chol_inv_any(c, g2.v, r2c.v, r2c_inv.v, info_c.as<int>() + 1, dg_c.as<double>() + s);
   qgemm(c, QLRA_OP_N, QLRA_OP_N, 1.0, t1c.v, r2c_inv.v, 0.0, cm.v);
   int inf[2] = {0, 0};
   std::vector<double> d((size_t)(2 * s));
@@ -969,7 +973,7 @@ void pseudo_qr_dev(Ctx& c, const QView& Y, const QView& H, const qlra_pseudo_qr_
   DeferredQ& q0 = es ? es->q0 : q0_local;
   DevQMat cm(c, s, s), rc;
   std::vector<double> rd;
-  if (s > chol_inv_async_max() || !pqr_factors_fast(c, Y, q0, rq, rq_inv, cm, rc, rd, es)) {
+  if (!pqr_factors_fast(c, Y, q0, rq, rq_inv, cm, rc, rd, es)) {
     if (!cholesky_qr(c, Y, QView{}, /*complex_mode=*/false, m, nullptr, /*distributed=*/true, &rq_inv, &rq, &q0))
       fail(QLRA_ERR_RANK, "pseudo_qr: sketch numerically rank-deficient; use pseudo_svd");
     if (!cholesky_qr(c, rq.v, cm.v, /*complex_mode=*/true, s, &rd, /*distributed=*/false, nullptr, &rc))
@@ -997,6 +1001,7 @@ void pseudo_qr_dev(Ctx& c, const QView& Y, const QView& H, const qlra_pseudo_qr_
     std::string msg;
     double cond = 0.0;
     double eps = 0.0;
+    DevQMat gk;    // G_k = C_k^* C_k (k >= 1; G_0 is g)
     DevQMat ginv;  // G_k^{-1}
     DevQMat next;  // C_{k+1} = C_k ((1-eps) I + eps G_k^{-1})
   };
@@ -1024,7 +1029,7 @@ void pseudo_qr_dev(Ctx& c, const QView& Y, const QView& H, const qlra_pseudo_qr_
       try {
         sp.ginv = DevQMat(c, s, s);
         const QView ck = k == 0 ? cm.v : spec[0].next.v;
-        DevQMat gk;
+        DevQMat& gk = sp.gk;
         if (k == 0) {
           // G_0^{-1} from the factors already at hand: C = R_q R_c^{-1}, so
           // G_0^{-1} = K K^* with K = R_c R_q^{-1} (no factorisation; the
@@ -1128,8 +1133,24 @@ void pseudo_qr_dev(Ctx& c, const QView& Y, const QView& H, const qlra_pseudo_qr_
 // side-stream eigenvalue computation instead of waiting for it here.
 // range_only: orthonormal_range (rangefinders.cpp:160-164: rows >= cols
 // allowed, no report).
+// pseudo-SVD's report computations left to the caller: the refinement of
+// kappa(Y) and kappa(H) run on the side stream while the caller's next work
+// (the core solve) runs; finish() fills the report.
+struct PsvdDeferred {
+  std::vector<double> lam;          // spectrum of Y^*Y
+  std::unique_ptr<SideEigs> refine;  // of (R^*R)^{-1}: kappa(Y) to ~u kappa(Y)
+  std::unique_ptr<SideEigs> after;   // of H^*H: kappa(H)
+  void finish(qlra_rangefinder_report_t* rep) {
+    if (!rep) return;
+    if (refine) rep->kappa_before = kappa_from_eigs(merge_spectra(lam, refine->get()));
+    if (after) rep->kappa_after = kappa_from_eigs(after->get());
+    refine.reset();
+    after.reset();
+  }
+};
+
 void pseudo_svd_dev(Ctx& c, const QView& Y, const QView& H, uint64_t seed, qlra_rangefinder_report_t* rep,
-                    std::unique_ptr<SideEigs>* kappa_after_async = nullptr, bool range_only = false) {
+                    PsvdDeferred* deferred = nullptr, bool range_only = false) {
   const int64_t s = Y.cols;
   const int64_t m = global_rows(c, Y.rows);
   if (range_only) {
@@ -1160,16 +1181,35 @@ void pseudo_svd_dev(Ctx& c, const QView& Y, const QView& H, uint64_t seed, qlra_
     const char* e = std::getenv("QLRA_PSVD_GRADED");
     return e && std::atoi(e) != 0;
   }();
-  if (!std::isfinite(r.kappa_before) || !qr_ok || force_graded)
+  if (!std::isfinite(r.kappa_before) || !qr_ok) {
     r.kappa_before = pseudo_svd_graded(c, Y, H, m, global_row0(c, Y.rows), seed);
-  else if (r.kappa_before > kRefineKappa)  // kappa(Y) to ~u kappa(Y), not u kappa(Y)^2
-    r.kappa_before = kappa_from_eigs(refine_with_rinv(c, lam, rinv.v));
+  } else {
+    // Past kappa(Y) ~ 1e6 the CholeskyQR2 basis is still orthonormal and
+    // spans range(Y) to ~u kappa(Y), like any backward-stable method, but
+    // its error is shaped by the product Y R^{-1}: at C3 (kappa 6e7) its QB
+    // error differs from the reference's (SVD basis) by 8e-10 relative where
+    // two runs of the reference differ by <1e-10.  The graded route (Gram
+    // eigenvectors in levels, re-projected) lands within 5e-11 of it
+    // (tools/diag_c3_psvd.py): take it there.
+    const bool graded = r.kappa_before > kGradedKappa || force_graded;
+    if (r.kappa_before > kRefineKappa && !range_only) {  // kappa(Y) to ~u kappa(Y), not u kappa(Y)^2
+      if (deferred) {
+        DevQMat pm(c, s, s);
+        qgemm(c, QLRA_OP_N, QLRA_OP_C, 1.0, rinv.v, rinv.v, 0.0, pm.v);  // (R^* R)^{-1}
+        deferred->lam = lam;
+        deferred->refine.reset(new SideEigs(c, pm.v));
+      } else {
+        r.kappa_before = kappa_from_eigs(refine_with_rinv(c, lam, rinv.v));
+      }
+    }
+    if (graded) pseudo_svd_graded(c, Y, H, m, global_row0(c, Y.rows), seed);
+  }
   if (range_only) return;
-  if (kappa_after_async) {
-    // the caller overlaps kappa(H)'s eigenvalues with its next work
+  if (deferred) {
+    // kappa(H)'s eigenvalues overlap the caller's next work
     DevQMat gh(c, s, s);
     gram(c, H, gh.v);
-    kappa_after_async->reset(new SideEigs(c, gh.v));
+    deferred->after.reset(new SideEigs(c, gh.v));
   } else {
     r.kappa_after = condition_number_dev(c, H);
   }
@@ -1229,6 +1269,20 @@ void validate_spec(const qlra_spec_t* s) {
 
 using namespace qlra_dev;
 
+// The device's stream-ordered pool: no release to the driver between calls,
+// and no reuse of a block freed on ANOTHER stream that is not yet complete
+// (by default the pool would make this stream wait for that one -- it
+// serialised the pseudo-QR close on the main stream behind the closing tall
+// product on the second stream, 4 ms at C4).  Reuse of completed frees stays.
+static void setup_pool(int device) {
+  cudaMemPool_t pool;
+  QLRA_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+  uint64_t thr = UINT64_MAX;
+  QLRA_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+  int no = 0;
+  QLRA_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolReuseAllowInternalDependencies, &no));
+}
+
 template <class F>
 static int guarded(qlra_ctx_t* ctx, F&& f) {
   try {
@@ -1265,10 +1319,7 @@ int qlra_ctx_create(qlra_ctx_t** out, int device, int rank, int nranks, const vo
   const int rc = guarded(ctx, [&](Ctx& c) {
     QLRA_CUDA(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
     c.own_stream = true;
-    cudaMemPool_t pool;
-    QLRA_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
-    uint64_t thr = UINT64_MAX;
-    QLRA_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    setup_pool(device);
     QLRA_CUDA(cudaMallocHost(&c.pinned, 4096));
     if (c.nranks > 1) {
       if (!nccl_id) fail(QLRA_ERR_PARAMETER, "qlra_ctx_create: nranks > 1 needs an NCCL id");
@@ -1294,10 +1345,7 @@ int qlra_ctx_create_local(qlra_ctx_t** out, int device, qlra_group_t* group, int
   const int rc = guarded(ctx, [&](Ctx& c) {
     QLRA_CUDA(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
     c.own_stream = true;
-    cudaMemPool_t pool;
-    QLRA_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
-    uint64_t thr = UINT64_MAX;
-    QLRA_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    setup_pool(device);
     QLRA_CUDA(cudaMallocHost(&c.pinned, 4096));
     group_attach(c, group, rank);
   });
@@ -1337,7 +1385,6 @@ int qlra_ctx_destroy(qlra_ctx_t* ctx) {
     cudaStreamSynchronize(ctx->c.side);
     cudaStreamDestroy(ctx->c.side);
   }
-  if (ctx->c.side_pinned) cudaFreeHost(ctx->c.side_pinned);
   if (ctx->c.staging) cudaFreeHost(ctx->c.staging);
   if (ctx->c.side2) {
     cudaStreamSynchronize(ctx->c.side2);
@@ -1665,10 +1712,12 @@ int qlra_qb_stage(qlra_ctx_t* ctx, const qlra_spec_t* psi, int64_t row0, const q
     qlra_pseudo_qr_config_t cfg{3, 3, 1.2};
     if (cfg_in) cfg = *cfg_in;
     EarlySolve es(c, *psi, row0, view_of(w));
+    PsvdDeferred pd;
     if (method == QLRA_PSEUDO_QR) pseudo_qr_dev(c, view_of(y), view_of(h), cfg, rep, &es);
-    else pseudo_svd_dev(c, view_of(y), view_of(h), rangefinder_seed, rep);
+    else pseudo_svd_dev(c, view_of(y), view_of(h), rangefinder_seed, rep, &pd);
     const CoreSolve cs = core_solve(c, &es, *psi, row0, view_of(h), view_of(w));
     cs.cols(c, 0, x->cols, view_of(x));
+    pd.finish(rep);
   });
 }
 
@@ -1737,14 +1786,14 @@ int qlra_one_pass_qb_host(qlra_ctx_t* ctx, const qlra_qmat_t* a_host, int64_t ro
     w.zero(c);
     sketch_update_rows_host(c, *omega, *psi, row0, view_of(a_host), y.v, w.v, block_rows);
     allreduce_qmat(c, w.v);
-    std::unique_ptr<SideEigs> kappa_after;  // pseudo-SVD: kappa(H) overlapped with the solve
+    PsvdDeferred pd;  // pseudo-SVD: the kappa refinements overlapped with the solve
     qlra_rangefinder_report_t rr{};
     // No early solve here: H's read-back already hides the solve (C2:
     // 31.55 ms either way; C5: the early solve's side-stream work delays H
     // and so its 49 ms read-back, 433 -> 446 ms).
     EarlySolve* esp = nullptr;
     if (method == QLRA_PSEUDO_QR) pseudo_qr_dev(c, y.v, h.v, cfg, &rr, esp);
-    else pseudo_svd_dev(c, y.v, h.v, rangefinder_seed, &rr, &kappa_after);
+    else pseudo_svd_dev(c, y.v, h.v, rangefinder_seed, &rr, &pd);
     // H is final: copy it back on a side stream while the solve runs.  The
     // guard (declared after y, w, h, x) drains the side stream on every exit
     // -- a failing solve included -- before those buffers are released and
@@ -1792,10 +1841,7 @@ int qlra_one_pass_qb_host(qlra_ctx_t* ctx, const qlra_qmat_t* a_host, int64_t ro
                                     sizeof(double) * nj, (size_t)s, cudaMemcpyDeviceToHost, side));
     }
     QLRA_CUDA(cudaEventRecord(copied, side));
-    if (kappa_after) {
-      rr.kappa_after = kappa_from_eigs(kappa_after->get());
-      kappa_after.reset();
-    }
+    pd.finish(&rr);
     if (rep) *rep = rr;
     // device buffers are released on c.stream: order that after the copies
     QLRA_CUDA(cudaStreamWaitEvent(c.stream, copied, 0));

@@ -532,8 +532,15 @@ void qgemm_ex(Ctx& ctx, int op_a, int op_b, double alpha, const QView& A, const 
   const int64_t tm = (M + BM - 1) / BM, tn = (N + BN - 1) / BN;
   const int64_t tiles = tm * tn;
   // Small products: the 64x64 DMMA tiles (+ split-K of >= 24 k-steps) cannot
-  // fill the GPU -- use the 16x16-tile path.
-  if (force_splits <= 0 && K > 0 && tiles * std::max<int64_t>(1, K / (24 * BK)) < 148) {
+  // fill the GPU -- use the 16x16-tile path (CUDA cores), unless the product
+  // is big enough for the tensor tiles to win anyway (C4's 500 x 500 x 500:
+  // 240 us on the small path; QLRA_SMALL_GEMM_MAX tunes the cut in M N K)
+  static const double small_max = [] {
+    const char* e = std::getenv("QLRA_SMALL_GEMM_MAX");
+    return e ? std::atof(e) : 6.4e7;
+  }();
+  if (force_splits <= 0 && K > 0 && tiles * std::max<int64_t>(1, K / (24 * BK)) < 148 &&
+      (double)M * (double)N * (double)K < small_max) {
     small_gemm(ctx, op_a == QLRA_OP_C, op_b == QLRA_OP_C, g, M, N, K, C);
     return;
   }

@@ -1052,9 +1052,16 @@ void sketch_rows_pipeline(Ctx& ctx, const qlra_spec_t& omega, const qlra_spec_t&
   // bottleneck before it), so it should be short.
   const int64_t tail_start = !relayout && b > 2 * R ? b - R : b;
   const int64_t Rt = std::max<int64_t>(64, ((R / 4 + 63) / 64) * 64);
+  // ...and the first chunks ramp up (R/8, R/4, R/2): the copy of the first
+  // chunk is the one part nothing overlaps at the start (C4: 1.7 GB at
+  // 55 GB/s = 31 ms before the first sketch launch otherwise)
+  const bool ramp = !relayout && b > 4 * R;
+  int chunk = 0;
   int idx = 0;
-  for (int64_t r0 = 0, rp = 0; r0 < b; r0 += rp, idx ^= 1) {
+  for (int64_t r0 = 0, rp = 0; r0 < b; r0 += rp, idx ^= 1, ++chunk) {
     rp = std::min(r0 >= tail_start ? Rt : std::min(R, tail_start - r0), b - r0);
+    if (ramp && chunk < 3)
+      rp = std::min(rp, std::max<int64_t>(256, (((R >> (3 - chunk)) + 63) / 64) * 64));
     const QView dst = sub(buf[idx], 0, 0, rp, n);
     const double* from[4];
     int64_t from_ld = n;

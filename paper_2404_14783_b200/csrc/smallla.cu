@@ -354,25 +354,30 @@ __global__ void __launch_bounds__(SNT) k_quat_gj(QView a, QView b, double* stat,
   if (t == 0) { stat[0] = 0.0; stat[1] = pmin; stat[2] = pmax; }
 }
 
+// ||chi(A)||_1 = max over columns j of sum_i |A0_ij| + |A1_ij| (A = A0 + A1 j,
+// A0 = w + i x, A1 = y + i z): a warp per column, lanes over rows (fixed
+// reduction trees: deterministic).
 __global__ void k_chi_norm1(QView a, double* out) {
-  __shared__ double sh[SNT];
-  const int t = threadIdx.x;
+  __shared__ double sh[32];
+  const int t = threadIdx.x, lane = t & 31, wid = t >> 5, nw = blockDim.x >> 5;
   double best = 0.0;
-  for (int64_t j = t; j < a.cols; j += blockDim.x) {
+  for (int64_t j = wid; j < a.cols; j += nw) {
     double s = 0.0;
-    for (int64_t i = 0; i < a.rows; ++i) {
+    for (int64_t i = lane; i < a.rows; i += 32) {
       const Q4 q = qload(a, i, j);
       s += sqrt(q.w * q.w + q.x * q.x) + sqrt(q.y * q.y + q.z * q.z);
     }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
     best = fmax(best, s);
   }
-  sh[t] = best;
+  if (lane == 0) sh[wid] = best;
   __syncthreads();
-  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
-    if (t < w) sh[t] = fmax(sh[t], sh[t + w]);
-    __syncthreads();
+  if (t == 0) {
+    double m = 0.0;
+    for (int w = 0; w < nw; ++w) m = fmax(m, sh[w]);
+    *out = m;
   }
-  if (t == 0) *out = sh[0];
 }
 
 __global__ void k_axpby_identity(double alpha, double beta, QView a, QView out) {
@@ -601,6 +606,10 @@ __global__ void __launch_bounds__(512) k_qtridiag_smem(QView a, double* d, doubl
 // Same reflectors as k_qtridiag_smem.
 constexpr int QTC = 16;  // non-portable cluster size (B200 allows 16 with the opt-in attribute)
 constexpr int QTC_MAX = 224;
+constexpr int QTG_MAX = 2048;  // global-rows cluster variant (3 n quaternions of shared memory)
+// its rows come from L2: a warp per row (n / 16 rows per CTA) keeps enough
+// loads in flight
+constexpr int QTG_THREADS = 1024;
 constexpr int QTC_THREADS = 256;
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
@@ -637,16 +646,23 @@ __device__ __forceinline__ void st_async_q4(const Q4* dst, const uint64_t* bar, 
                : "memory");
 }
 
-__global__ void __cluster_dims__(QTC, 1, 1) __launch_bounds__(QTC_THREADS)
-    k_qtridiag_cluster(QView a, double* d, double* e) {
+// GROWS: each CTA's rows live in global memory (L2) instead of its shared
+// memory -- for n past QTC_MAX, where they no longer fit: still 16 SMs only
+// (the cooperative all-SM kernel starved every concurrent kernel: C4's
+// s = 500 spectrum took 18 ms of the whole GPU), v and p still exchanged
+// through distributed shared memory.
+template <bool GROWS>
+__global__ void __cluster_dims__(QTC, 1, 1) __launch_bounds__(GROWS ? QTG_THREADS : QTC_THREADS)
+    k_qtridiag_cluster(QView a, double* d, double* e, Q4* grows) {
   namespace cg = cooperative_groups;
   cg::cluster_group cl = cg::this_cluster();
   extern __shared__ __align__(16) unsigned char dsm[];
   const int n = (int)a.rows, rank = (int)cl.block_rank();
   const int rmax = (n + QTC - 1) / QTC, nr = (n - rank + QTC - 1) / QTC;
-  Q4* rows = reinterpret_cast<Q4*>(dsm);  // rmax x n: global row rank + QTC*li
-  Q4* vb = rows + (size_t)rmax * n;       // 2 x n
-  Q4* pb = vb + 2 * n;                    // n
+  // rmax x n: global row rank + QTC*li
+  Q4* rows = GROWS ? grows + (size_t)rank * rmax * n : reinterpret_cast<Q4*>(dsm);
+  Q4* vb = GROWS ? reinterpret_cast<Q4*>(dsm) : rows + (size_t)rmax * n;  // 2 x n
+  Q4* pb = vb + 2 * n;                                                    // n
   __shared__ __align__(8) uint64_t bar_v[2], bar_p;
   __shared__ double s_beta;
   const int t = threadIdx.x, lane = t & 31, wid = t >> 5, nw = blockDim.x >> 5;
@@ -700,6 +716,7 @@ __global__ void __cluster_dims__(QTC, 1, 1) __launch_bounds__(QTC_THREADS)
       const int r = rank + QTC * li;
       const Q4* row = rows + li * n + o;
       Q4 acc{0.0, 0.0, 0.0, 0.0};
+#pragma unroll 4
       for (int c = lane; c < len; c += 32) {
         const Q4 pq = qmul(row[c], v[c]);
         acc.w += pq.w; acc.x += pq.x; acc.y += pq.y; acc.z += pq.z;
@@ -723,6 +740,7 @@ __global__ void __cluster_dims__(QTC, 1, 1) __launch_bounds__(QTC_THREADS)
       const Q4 vr = v[ri], pr = pb[ri];
       const Q4 wr{pr.w - hk * vr.w, pr.x - hk * vr.x, pr.y - hk * vr.y, pr.z - hk * vr.z};
       Q4* row = rows + li * n + o;
+#pragma unroll 4
       for (int cc = lane; cc < len; cc += 32) {
         const Q4 vc0 = v[cc], pc = pb[cc];
         const Q4 wc{pc.w - hk * vc0.w, -(pc.x - hk * vc0.x), -(pc.y - hk * vc0.y), -(pc.z - hk * vc0.z)};
@@ -855,6 +873,146 @@ __global__ void __launch_bounds__(SNT) k_quat_jacobi(QView g, QView v, double* w
   }
   for (int64_t i = t; i < n; i += blockDim.x) w[i] = g.p[0][i * g.ld + i];
   if (t == 0 && off_out) *off_out = off / (scale > 0 ? scale : 1.0);
+}
+
+// Parallel cyclic Jacobi for larger n over a cooperative grid (the one-CTA
+// k_quat_jacobi works in global memory with strided column updates: 3 s at
+// n = 220).  Round-robin pairs (position 0 fixed, the rest rotating -- the
+// same tournament as k_quat_jacobi, computed from the round number); per
+// round: (A) the pairs' rotations, (B) G <- J^* G (row pairs, coalesced),
+// (C) G <- G J (column pairs inside each row: a row's reads stay in L1) and
+// V^T <- J^T V^T (V is kept transposed so its column rotations are row
+// operations).  Off-diagonal norm checked per sweep; reductions in CTA order
+// (deterministic).
+__device__ __forceinline__ int rr_index(int64_t i, int64_t round, int64_t m) {
+  return i == 0 ? 0 : (int)(1 + (((i - 1 - round) % m) + m) % m);
+}
+__global__ void __launch_bounds__(256) k_quat_jacobi_coop(QView g, QView vt, double* w, int max_sweeps,
+                                                          double* rc, double* part) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double sh[32];
+  const int64_t n = g.rows, np = n + (n & 1), npairs = np / 2, m = np - 1;
+  const int t = threadIdx.x;
+  const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + t, gthreads = (int64_t)gridDim.x * blockDim.x;
+  const int nb = gridDim.x;
+  for (int64_t e = gtid; e < n * n; e += gthreads) {
+    const int64_t i = e / n, j = e % n;
+    qstore(vt, i, j, Q4{i == j ? 1.0 : 0.0, 0.0, 0.0, 0.0});
+  }
+  double scale = 0.0;
+  {
+    double pa = 0.0;
+    for (int64_t e = gtid; e < n * n; e += gthreads) {
+      const Q4 q = qload(g, e / n, e % n);
+      pa += q.w * q.w + q.x * q.x + q.y * q.y + q.z * q.z;
+    }
+    pa = block_sum(pa, sh);
+    if (t == 0) part[blockIdx.x] = pa;
+    grid.sync();
+    for (int b = 0; b < nb; ++b) scale += part[b];
+    scale = sqrt(scale);
+    grid.sync();
+  }
+  for (int sweep = 0; sweep < max_sweeps && n > 1; ++sweep) {
+    double pa = 0.0;
+    for (int64_t e = gtid; e < n * n; e += gthreads) {
+      const int64_t i = e / n, j = e % n;
+      if (i == j) continue;
+      const Q4 q = qload(g, i, j);
+      pa += q.w * q.w + q.x * q.x + q.y * q.y + q.z * q.z;
+    }
+    pa = block_sum(pa, sh);
+    if (t == 0) part[blockIdx.x] = pa;
+    grid.sync();
+    double off = 0.0;
+    for (int b = 0; b < nb; ++b) off += part[b];
+    off = sqrt(off);
+    grid.sync();  // part is rewritten next sweep
+    if (!(off > 1e-15 * scale)) break;  // uniform decision
+    for (int64_t round = 0; round < m; ++round) {
+      // (A) rotation parameters
+      for (int64_t k = gtid; k < npairs; k += gthreads) {
+        int p = rr_index(k, round, m), q = rr_index(np - 1 - k, round, m);
+        if (p > q) { const int tmp = p; p = q; q = tmp; }
+        double c = 1.0, sn = 0.0;
+        Q4 u{1.0, 0.0, 0.0, 0.0};
+        if (q < n) {
+          const Q4 b = qload(g, p, q);
+          const double nbq = sqrt(b.w * b.w + b.x * b.x + b.y * b.y + b.z * b.z);
+          if (nbq > 1e-300) {
+            u = Q4{b.w / nbq, b.x / nbq, b.y / nbq, b.z / nbq};
+            const double a = g.p[0][p * g.ld + p], d = g.p[0][q * g.ld + q];
+            const double th = (d - a) / (2.0 * nbq);
+            const double tt = (th >= 0 ? 1.0 : -1.0) / (fabs(th) + sqrt(th * th + 1.0));
+            c = 1.0 / sqrt(1.0 + tt * tt);
+            sn = tt * c;
+          }
+        }
+        double* r = rc + k * 8;
+        r[0] = c; r[1] = sn; r[2] = u.w; r[3] = u.x; r[4] = u.y; r[5] = u.z;
+        r[6] = (double)p; r[7] = (double)q;
+      }
+      grid.sync();
+      // (B) rows p, q of G: G <- J^* G
+      for (int64_t e = gtid; e < npairs * n; e += gthreads) {
+        const int64_t k = e / n, j = e % n;
+        const double* r = rc + k * 8;
+        const int p = (int)r[6], q = (int)r[7];
+        if (q >= n) continue;
+        const double c = r[0], sn = r[1];
+        const Q4 u{r[2], r[3], r[4], r[5]};
+        const Q4 rp = qload(g, p, j), rq = qmul(u, qload(g, q, j));
+        qstore(g, p, j, Q4{c * rp.w - sn * rq.w, c * rp.x - sn * rq.x, c * rp.y - sn * rq.y, c * rp.z - sn * rq.z});
+        qstore(g, q, j, Q4{sn * rp.w + c * rq.w, sn * rp.x + c * rq.x, sn * rp.y + c * rq.y, sn * rp.z + c * rq.z});
+      }
+      grid.sync();
+      // (C) columns p, q inside every row of G: G <- G J; rows of V^T
+      for (int64_t e = gtid; e < 2 * npairs * n; e += gthreads) {
+        const bool on_v = e >= npairs * n;
+        const int64_t ee = on_v ? e - npairs * n : e;
+        const int64_t k = on_v ? ee / n : ee % npairs, i = on_v ? ee % n : ee / npairs;
+        const double* r = rc + k * 8;
+        const int p = (int)r[6], q = (int)r[7];
+        if (q >= n) continue;
+        const double c = r[0], sn = r[1];
+        const Q4 uc{r[2], -r[3], -r[4], -r[5]};
+        if (on_v) {  // V^T rows p, q: (V J)^T
+          const Q4 cp = qload(vt, p, i), cq = qmul(qload(vt, q, i), uc);
+          qstore(vt, p, i, Q4{c * cp.w - sn * cq.w, c * cp.x - sn * cq.x, c * cp.y - sn * cq.y, c * cp.z - sn * cq.z});
+          qstore(vt, q, i, Q4{sn * cp.w + c * cq.w, sn * cp.x + c * cq.x, sn * cp.y + c * cq.y, sn * cp.z + c * cq.z});
+        } else {
+          const Q4 cp = qload(g, i, p), cq = qmul(qload(g, i, q), uc);
+          qstore(g, i, p, Q4{c * cp.w - sn * cq.w, c * cp.x - sn * cq.x, c * cp.y - sn * cq.y, c * cp.z - sn * cq.z});
+          qstore(g, i, q, Q4{sn * cp.w + c * cq.w, sn * cp.x + c * cq.x, sn * cp.y + c * cq.y, sn * cp.z + c * cq.z});
+        }
+      }
+      grid.sync();
+    }
+  }
+  for (int64_t i = gtid; i < n; i += gthreads) w[i] = g.p[0][i * g.ld + i];
+}
+
+// Eigenpairs sorted descending (stable by index) from V^T (rows = vectors).
+__global__ void k_sort_eigen_t(const double* w, QView vt, double* out_w, QView out_v) {
+  const int64_t n = vt.rows;
+  for (int64_t i = blockIdx.x; i < n; i += gridDim.x) {
+    __shared__ int64_t s_rank;
+    if (threadIdx.x == 0) {
+      int64_t rank = 0;
+      const double wi = w[i];
+      for (int64_t j = 0; j < n; ++j) {
+        const double wj = w[j];
+        if (wj > wi || (wj == wi && j < i)) ++rank;
+      }
+      s_rank = rank;
+      out_w[rank] = wi;
+    }
+    __syncthreads();
+    const int64_t rank = s_rank;
+    for (int64_t r = threadIdx.x; r < vt.cols; r += blockDim.x) qstore(out_v, r, rank, qload(vt, i, r));
+    __syncthreads();
+  }
 }
 
 // Sort eigenpairs descending (stable by index): out_w, out_v (columns).
@@ -1355,6 +1513,7 @@ __global__ void __cluster_dims__(CHC, 1, 1) __launch_bounds__(256) k_chol_inv_cl
   if (me == 0 && t == 0) *A.info = 0;
 }
 
+
 }  // namespace
 
 // all eigenvalues (descending) of the tridiagonal (d, e) into d_w
@@ -1379,11 +1538,23 @@ void tridiag_all_eigvals(Ctx& ctx, const double* d, const double* e, int64_t n, 
 void small_quat_herm_eigvals(Ctx& ctx, const QView& a, double* d_w, bool extremes_only) {
   const int64_t n = a.rows;
   if (n == 0) return;
+
   DeviceBuffer de(ctx, sizeof(double) * (2 * n + 1));
   double* d = de.as<double>();
   double* e = d + n;
-  if (n > QTC_MAX) {
-    // large n: cooperative grid over all SMs
+  if (n > QTC_MAX && n <= QTG_MAX) {
+    // large n: the cluster kernel with its rows in global memory (16 SMs)
+    const int64_t rmax = (n + QTC - 1) / QTC;
+    DeviceBuffer gr(ctx, sizeof(Q4) * (size_t)(QTC * rmax * n));
+    const size_t csm = sizeof(Q4) * (size_t)(3 * n);
+    set_func_attr((const void*)k_qtridiag_cluster<true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (csm > 48 * 1024)
+      set_func_attr((const void*)k_qtridiag_cluster<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm);
+    k_qtridiag_cluster<true><<<QTC, QTG_THREADS, csm, ctx.stream>>>(a, d, e, gr.as<Q4>());
+    QLRA_LAUNCH_CHECK();
+    count_launch();
+  } else if (n > QTC_MAX) {
+    // very large n: cooperative grid over all SMs
     int dev = 0, sms = 148, per_sm = 0;
     QLRA_CUDA(cudaGetDevice(&dev));
     QLRA_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
@@ -1401,10 +1572,10 @@ void small_quat_herm_eigvals(Ctx& ctx, const QView& a, double* d_w, bool extreme
   } else if (n > 48 && n <= QTC_MAX) {
     const int64_t rmax = (n + QTC - 1) / QTC;
     const size_t csm = sizeof(Q4) * (size_t)(rmax * n + 3 * n);
-    set_func_attr((const void*)k_qtridiag_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    set_func_attr((const void*)k_qtridiag_cluster<false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     if (csm > 48 * 1024)
-      set_func_attr((const void*)k_qtridiag_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm);
-    k_qtridiag_cluster<<<QTC, QTC_THREADS, csm, ctx.stream>>>(a, d, e);
+      set_func_attr((const void*)k_qtridiag_cluster<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm);
+    k_qtridiag_cluster<false><<<QTC, QTC_THREADS, csm, ctx.stream>>>(a, d, e, nullptr);
     QLRA_LAUNCH_CHECK();
     count_launch();
   } else {  // n <= 48: one CTA, packed triangle in shared memory
@@ -1427,6 +1598,30 @@ void small_quat_herm_eigvals(Ctx& ctx, const QView& a, double* d_w, bool extreme
 void small_quat_eigh(Ctx& ctx, const QView& a, double* d_w, const QView& vecs, int max_sweeps) {
   const int64_t n = a.rows;
   if (n == 0) return;
+  if (n > 64) {  // cooperative grid Jacobi
+    int dev = 0, sms = 148, per_sm = 0;
+    QLRA_CUDA(cudaGetDevice(&dev));
+    QLRA_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    QLRA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_quat_jacobi_coop, 256, 0));
+    const int64_t np = n + (n & 1);
+    const int want = (int)std::max<int64_t>(1, std::min<int64_t>(sms, (np / 2 * n + 255) / 256));
+    const int blocks = std::max(1, std::min(want, sms * std::max(per_sm, 1)));
+    DevQMat vt(ctx, n, n);
+    DeviceBuffer w(ctx, sizeof(double) * (size_t)n), rc(ctx, sizeof(double) * 8 * (size_t)(np / 2)),
+        part(ctx, sizeof(double) * (size_t)blocks);
+    QView av = a, vv = vt.v;
+    double* wp = w.as<double>();
+    double* rcp = rc.as<double>();
+    double* pp = part.as<double>();
+    void* args[] = {&av, &vv, &wp, &max_sweeps, &rcp, &pp};
+    QLRA_CUDA(cudaLaunchCooperativeKernel((const void*)k_quat_jacobi_coop, dim3(blocks), dim3(256), args, 0,
+                                          ctx.stream));
+    count_launch();
+    k_sort_eigen_t<<<(unsigned)std::min<int64_t>(n, 1024), 128, 0, ctx.stream>>>(w.as<double>(), vt.v, d_w, vecs);
+    QLRA_LAUNCH_CHECK();
+    count_launch();
+    return;
+  }
   const int64_t np = n + (n & 1);
   const size_t smem = ((np * sizeof(int) + 15) / 16) * 16 + sizeof(double) * 6 * (size_t)(np / 2 + 1);
   if (smem > 48 * 1024)
@@ -1479,76 +1674,91 @@ void chol_inv_launch(Ctx& ctx, const QView& g, const QView& r, const QView& rinv
   count_launch();
 }
 
-bool blocked_chol_inv(Ctx& ctx, const QView& g, const QView& rinv, std::vector<double>* rdiag,
-                      const QView* r_out) {
+// *out = 0, or nonzero if any block's factorisation failed (fixed order)
+__global__ void k_any_info(const int* info, int nb, int* out) {
+  if (threadIdx.x != 0) return;
+  int v = 0;
+  for (int b = 0; b < nb && v == 0; ++b) v = info[b];
+  *out = v;
+}
+
+// Blocked Cholesky + triangular inverse for s > CHC_MAX, ENQUEUED ONLY (no
+// host sync): CB x CB diagonal blocks factored and inverted by one CTA each
+// (k_qchol_block), the panels and the trailing update by qgemm, then the
+// block back-substitution of R^{-1}.  *d_info = 0 or nonzero (a block broke
+// down: r, rinv are then garbage); d_rdiag = diag(R).  r: s x s workspace.
+void blocked_chol_inv_enqueue(Ctx& ctx, const QView& g, const QView& r, const QView& rinv, int* d_info,
+                              double* d_rdiag) {
   const int64_t s = g.rows;
-  if (s == 0) return true;
-  if (s <= CHC_MAX) {
-    DevQMat rw;
-    QView rv;
-    if (r_out) {
-      rv = *r_out;
-    } else {
-      rw = DevQMat(ctx, s, s);
-      rv = rw.v;
-    }
-    DeviceBuffer info(ctx, sizeof(int));
-    DeviceBuffer dg(ctx, sizeof(double) * (size_t)s);
-    chol_inv_launch(ctx, g, rv, rinv, info.as<int>(), dg.as<double>());
-    int inf = 0;
-    QLRA_CUDA(cudaMemcpyAsync(&inf, info.ptr, sizeof(int), cudaMemcpyDeviceToHost, ctx.stream));
-    QLRA_CUDA(cudaStreamSynchronize(ctx.stream));
-    if (inf != 0) return false;
-    if (rdiag) {
-      rdiag->resize(s);
-      QLRA_CUDA(cudaMemcpy(rdiag->data(), dg.ptr, sizeof(double) * s, cudaMemcpyDeviceToHost));
-    }
-    return true;
-  }
   const size_t smem = sizeof(Q4) * CB * CB;
   set_func_attr((const void*)k_qchol_block, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  DevQMat work(ctx, s, s), r(ctx, s, s);
+  DevQMat work(ctx, s, s);
   copy_qmat(ctx, g, work.v);
-  r.zero(ctx);
-  for (int p = 0; p < 4; ++p)
-    QLRA_CUDA(cudaMemset2DAsync(rinv.p[p], (size_t)rinv.ld * sizeof(double), 0,
-                                (size_t)s * sizeof(double), (size_t)s, ctx.stream));
-  DeviceBuffer info(ctx, sizeof(int) * (size_t)((s + CB - 1) / CB));
-  DeviceBuffer dg(ctx, sizeof(double) * (size_t)s);
+  for (int p = 0; p < 4; ++p) {
+    QLRA_CUDA(cudaMemset2DAsync(r.p[p], (size_t)r.ld * sizeof(double), 0, (size_t)s * sizeof(double), (size_t)s,
+                                ctx.stream));
+    QLRA_CUDA(cudaMemset2DAsync(rinv.p[p], (size_t)rinv.ld * sizeof(double), 0, (size_t)s * sizeof(double),
+                                (size_t)s, ctx.stream));
+  }
   const int64_t nb = (s + CB - 1) / CB;
+  DeviceBuffer info(ctx, sizeof(int) * (size_t)nb);
   for (int64_t b = 0; b < nb; ++b) {
     const int64_t k0 = b * CB, kb = std::min<int64_t>(CB, s - k0), rest = s - k0 - kb;
-    k_qchol_block<<<1, QB_THREADS, smem, ctx.stream>>>(sub(work.v, k0, k0, kb, kb), sub(r.v, k0, k0, kb, kb),
-                                                 sub(rinv, k0, k0, kb, kb), info.as<int>() + b,
-                                                 dg.as<double>() + k0);
+    k_qchol_block<<<1, QB_THREADS, smem, ctx.stream>>>(sub(work.v, k0, k0, kb, kb), sub(r, k0, k0, kb, kb),
+                                                 sub(rinv, k0, k0, kb, kb), info.as<int>() + b, d_rdiag + k0);
     QLRA_LAUNCH_CHECK();
     count_launch();
     if (rest > 0) {
       qgemm(ctx, QLRA_OP_C, QLRA_OP_N, 1.0, sub(rinv, k0, k0, kb, kb), sub(work.v, k0, k0 + kb, kb, rest),
-            0.0, sub(r.v, k0, k0 + kb, kb, rest));
-      qgemm(ctx, QLRA_OP_C, QLRA_OP_N, -1.0, sub(r.v, k0, k0 + kb, kb, rest),
-            sub(r.v, k0, k0 + kb, kb, rest), 1.0, sub(work.v, k0 + kb, k0 + kb, rest, rest));
+            0.0, sub(r, k0, k0 + kb, kb, rest));
+      qgemm(ctx, QLRA_OP_C, QLRA_OP_N, -1.0, sub(r, k0, k0 + kb, kb, rest), sub(r, k0, k0 + kb, kb, rest), 1.0,
+            sub(work.v, k0 + kb, k0 + kb, rest, rest));
     }
   }
-  std::vector<int> inf(nb);
-  QLRA_CUDA(cudaMemcpyAsync(inf.data(), info.ptr, sizeof(int) * nb, cudaMemcpyDeviceToHost, ctx.stream));
-  QLRA_CUDA(cudaStreamSynchronize(ctx.stream));
-  for (int64_t b = 0; b < nb; ++b)
-    if (inf[b] != 0) return false;
-  if (rdiag) {
-    rdiag->resize(s);
-    QLRA_CUDA(cudaMemcpy(rdiag->data(), dg.ptr, sizeof(double) * s, cudaMemcpyDeviceToHost));
-  }
+  k_any_info<<<1, 32, 0, ctx.stream>>>(info.as<int>(), (int)nb, d_info);
+  QLRA_LAUNCH_CHECK();
+  count_launch();
   if (nb > 1) {
     DevQMat tmp(ctx, CB, s);
     for (int64_t b = nb - 2; b >= 0; --b) {
       const int64_t i0 = b * CB, ib = std::min<int64_t>(CB, s - i0), j0 = i0 + ib, rest = s - j0;
       const QView t = sub(tmp.v, 0, 0, ib, rest);
-      qgemm(ctx, QLRA_OP_N, QLRA_OP_N, 1.0, sub(r.v, i0, j0, ib, rest), sub(rinv, j0, j0, rest, rest), 0.0, t);
+      qgemm(ctx, QLRA_OP_N, QLRA_OP_N, 1.0, sub(r, i0, j0, ib, rest), sub(rinv, j0, j0, rest, rest), 0.0, t);
       qgemm(ctx, QLRA_OP_N, QLRA_OP_N, -1.0, sub(rinv, i0, i0, ib, ib), t, 0.0, sub(rinv, i0, j0, ib, rest));
     }
   }
-  if (r_out) copy_qmat(ctx, r.v, *r_out);
+}
+
+// Any s: the single-launch cluster kernel up to CHC_MAX, else the enqueued
+// blocked form -- no host sync either way.
+void chol_inv_any(Ctx& ctx, const QView& g, const QView& r, const QView& rinv, int* d_info, double* d_rdiag) {
+  if (g.rows <= CHC_MAX) chol_inv_launch(ctx, g, r, rinv, d_info, d_rdiag);
+  else blocked_chol_inv_enqueue(ctx, g, r, rinv, d_info, d_rdiag);
+}
+
+bool blocked_chol_inv(Ctx& ctx, const QView& g, const QView& rinv, std::vector<double>* rdiag,
+                      const QView* r_out) {
+  const int64_t s = g.rows;
+  if (s == 0) return true;
+  DevQMat rw;
+  QView rv;
+  if (r_out) {
+    rv = *r_out;
+  } else {
+    rw = DevQMat(ctx, s, s);
+    rv = rw.v;
+  }
+  DeviceBuffer info(ctx, sizeof(int));
+  DeviceBuffer dg(ctx, sizeof(double) * (size_t)s);
+  chol_inv_any(ctx, g, rv, rinv, info.as<int>(), dg.as<double>());
+  int inf = 0;
+  QLRA_CUDA(cudaMemcpyAsync(&inf, info.ptr, sizeof(int), cudaMemcpyDeviceToHost, ctx.stream));
+  QLRA_CUDA(cudaStreamSynchronize(ctx.stream));
+  if (inf != 0) return false;
+  if (rdiag) {
+    rdiag->resize(s);
+    QLRA_CUDA(cudaMemcpy(rdiag->data(), dg.ptr, sizeof(double) * s, cudaMemcpyDeviceToHost));
+  }
   return true;
 }
 
@@ -1565,7 +1775,7 @@ void small_quat_solve(Ctx& ctx, const QView& a, const QView& b, double* d_stat, 
   count_launch();
 }
 void small_chi_norm1(Ctx& ctx, const QView& a, double* d_out) {
-  k_chi_norm1<<<1, SNT, 0, ctx.stream>>>(a, d_out);
+  k_chi_norm1<<<1, 1024, 0, ctx.stream>>>(a, d_out);
   QLRA_LAUNCH_CHECK();
   count_launch();
 }

@@ -252,6 +252,26 @@ def test_pseudo_qr_refusal_sweep(ctx, kappa):
         assert largest_principal_angle(host(rep.h), orc["h"]) < 1e-8 * max(1.0, kappa / 1e8)
 
 
+@pytest.mark.parametrize("s,kappa", [(300, 1e4), (500, 3e5)])
+def test_pseudo_qr_large_s_vs_oracle(ctx, s, kappa):
+    """s past the shared-memory cluster tridiagonalisation (C4's 500: the
+    global-rows cluster variant): the reference's step count, kappas and
+    range."""
+    from paper_2404_14783_b200 import qlra as Q
+    y = planted_conditioned_matrix(4 * s, s, kappa, 17 + s)
+    rep = Q.pseudo_qr(dev(y), ctx=ctx)
+    orc = O.pseudo_qr(y)
+    print(f"s={s}: kappa before {rep.kappa_before:.10e} / {orc['kappa_before']:.10e}, after "
+          f"{rep.kappa_after:.10e} / {orc['kappa_after']:.10e}, steps {rep.correction_steps_used} / "
+          f"{orc['correction_steps_used']}")
+    assert rep.correction_steps_used == orc["correction_steps_used"]
+    assert abs(rep.kappa_before / orc["kappa_before"] - 1) < 1e-8
+    assert abs(rep.kappa_after / orc["kappa_after"] - 1) < 1e-6
+    assert largest_principal_angle(host(rep.h), orc["h"]) < 1e-9
+    svd = Q.pseudo_svd(dev(y), ctx=ctx)
+    assert abs(svd.kappa_before / kappa - 1) < 1e-8 and abs(svd.kappa_after - 1) < 1e-10
+
+
 def test_pseudo_qr_errors(ctx):  # test_rangefinders.cpp:43-52
     from paper_2404_14783_b200 import qlra as Q
     y = random_gaussian(12, 3, 53)
@@ -475,7 +495,9 @@ def test_qsvd_on_device(ctx):  # test_factorizations.cpp:73-112
         assert rel_diff(host(u), uo) < 1e-9 and rel_diff(host(v), vo) < 1e-9
 
 
-@pytest.mark.parametrize("m,n,kappa", [(40, 3000, 1e6), (60, 500, 1e7), (900, 50, 1e5)])
+@pytest.mark.parametrize("m,n,kappa", [(40, 3000, 1e6), (60, 500, 1e7), (900, 50, 1e5),
+                                       # k > 64: the cooperative-grid Jacobi eigensolver
+                                       (120, 2000, 1e6), (300, 1500, 1e5)])
 def test_qsvd_graded_spectrum_relative_accuracy(ctx, m, n, kappa):
     """qsvd of a matrix with a graded spectrum (sigma_1 / sigma_k up to 1e7):
     every singular value to relative accuracy ~u sigma_1 / sigma_i (an
@@ -576,10 +598,11 @@ def test_c2_full_size_parity(ctx, method):
     assert largest_principal_angle(host(res.qb.h), qb["h"]) <= 1e-8
 
 
-@pytest.mark.parametrize("s", [40, 100, 200, 260])
+@pytest.mark.parametrize("s", [40, 100, 200, 260, 500])
 def test_singular_values_and_kappa(ctx, s):  # factorizations.cpp:316-337
-    # s = 40: single-CTA shared-memory tridiagonalisation; 100, 200: 8-CTA
-    # cluster kernel; 260: cooperative grid kernel
+    # s = 40: single-CTA shared-memory tridiagonalisation; 100, 200: 16-CTA
+    # cluster kernel (rows in shared memory); 260, 500: the same cluster with
+    # its rows in global memory
     from paper_2404_14783_b200 import qlra as Q
     y = planted_conditioned_matrix(3 * s, s, 1e3, 90 + s)
     sv = np.asarray(Q.singular_values(dev(y), ctx))
