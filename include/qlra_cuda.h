@@ -74,6 +74,14 @@ typedef struct {
   int64_t rows, cols, ld;
 } qlra_qmat_t;
 
+/* Device view of a complex matrix -- the reference's CMatrix
+ * (Eigen::MatrixXcd, complex_bridge.hpp:9): column-major, interleaved
+ * (re, im) doubles, leading dimension ld >= rows. */
+typedef struct {
+  double* data;
+  int64_t rows, cols, ld;
+} qlra_cmat_t;
+
 /* == PseudoQrConfig (rangefinders.hpp:23-27) */
 typedef struct {
   int32_t max_correction_steps;    /* default 3 */
@@ -198,6 +206,32 @@ int qlra_pseudo_svd(qlra_ctx_t* ctx, const qlra_qmat_t* y, uint64_t seed, qlra_q
  * pseudo-SVD basis of range(Y) for rows >= cols (ParameterError otherwise),
  * without the condition bookkeeping.  syncs. */
 int qlra_orthonormal_range(qlra_ctx_t* ctx, const qlra_qmat_t* y, uint64_t seed, qlra_qmat_t* h);
+
+/* ------------------------------------------------ complex bridge --- */
+/* complex_bridge.hpp:22-30 (complex_bridge.cpp:11-61): Q = Q0 + Q1 j,
+ * compact Q_c = [Q0; -conj(Q1)] (2m x n), full chi = [Q0, Q1; -conj(Q1),
+ * conj(Q0)] (2m x 2n), from_compact its inverse (odd row count ->
+ * QLRA_ERR_SHAPE), j_mul_conj = J conj(u) (a block swap with one sign flip). */
+int qlra_to_compact(qlra_ctx_t* ctx, const qlra_qmat_t* a, qlra_cmat_t* out);
+int qlra_to_full(qlra_ctx_t* ctx, const qlra_qmat_t* a, qlra_cmat_t* out);
+int qlra_from_compact(qlra_ctx_t* ctx, const qlra_cmat_t* z, qlra_qmat_t* out);
+int qlra_j_mul_conj(qlra_ctx_t* ctx, const qlra_cmat_t* u, qlra_cmat_t* out);
+/* complex_qr (factorizations.hpp:20-26, factorizations.cpp:33-51): thin
+ * Q (p x q) and R (q x q) with diag(R) real and nonnegative, p >= q.  Runs
+ * as CholeskyQR2 (shifted CholeskyQR3 when needed) in the complex subalgebra
+ * of the quaternion kernels; numerically rank-deficient input (which the
+ * reference's Householder QR still factors) -> QLRA_ERR_RANK.  syncs. */
+int qlra_complex_qr(qlra_ctx_t* ctx, const qlra_cmat_t* m, qlra_cmat_t* q, qlra_cmat_t* r);
+/* complex_svd (factorizations.hpp:28-34, factorizations.cpp:53-56): compact
+ * SVD M = U diag(s) V^*, k = min(p, q), s nonincreasing (host array), through
+ * the device QSVD of M as a quaternion matrix of its complex subalgebra
+ * (whose factors stay complex).  syncs. */
+int qlra_complex_svd(qlra_ctx_t* ctx, const qlra_cmat_t* m, qlra_cmat_t* u, double* s, qlra_cmat_t* v);
+/* qmat_pinv (factorizations.hpp:72, factorizations.cpp:303-314): V S^+ U^*
+ * with singular values <= max(m, n) eps sigma_max treated as zero; out is
+ * n x m.  spectral_norm (:79, :324-327): sigma_max.  sync. */
+int qlra_qmat_pinv(qlra_ctx_t* ctx, const qlra_qmat_t* a, qlra_qmat_t* out);
+int qlra_spectral_norm(qlra_ctx_t* ctx, const qlra_qmat_t* a, double* norm);
 
 /* --------------------------------------------------------- core solve --- */
 /* The solve half of qb_stage_with_psi (sketching.cpp:184-185):

@@ -25,6 +25,11 @@ class QMat(C.Structure):
     _fields_ = [("p", C.c_void_p * 4), ("rows", C.c_int64), ("cols", C.c_int64), ("ld", C.c_int64)]
 
 
+class CMat(C.Structure):
+    """qlra_cmat_t: column-major complex matrix, interleaved (re, im)."""
+    _fields_ = [("data", C.c_void_p), ("rows", C.c_int64), ("cols", C.c_int64), ("ld", C.c_int64)]
+
+
 class PseudoQrConfig(C.Structure):
     _fields_ = [("max_correction_steps", C.c_int32), ("power_iters_for_epsilon", C.c_int32),
                 ("delta_budget", C.c_double)]
@@ -46,7 +51,7 @@ def lib():
     if not os.path.exists(path):
         _build.build()
     L = C.CDLL(path)
-    P, PS, PQ = C.POINTER, C.POINTER(Spec), C.POINTER(QMat)
+    P, PS, PQ, PC = C.POINTER, C.POINTER(Spec), C.POINTER(QMat), C.POINTER(CMat)
     sig = {
         "qlra_ctx_create": ([P(VP), INT, INT, INT, VP], INT),
         "qlra_ctx_destroy": ([VP], INT),
@@ -76,6 +81,14 @@ def lib():
         "qlra_orthonormal_range": ([VP, PQ, U64, PQ], INT),
         "qlra_qb_stage_with_psi": ([VP, PQ, PQ, PQ, INT, U64, P(PseudoQrConfig), PQ, PQ, P(Report)], INT),
         "qlra_ctx_stream": ([VP], VP),
+        "qlra_to_compact": ([VP, PQ, PC], INT),
+        "qlra_to_full": ([VP, PQ, PC], INT),
+        "qlra_from_compact": ([VP, PC, PQ], INT),
+        "qlra_j_mul_conj": ([VP, PC, PC], INT),
+        "qlra_complex_qr": ([VP, PC, PC, PC], INT),
+        "qlra_complex_svd": ([VP, PC, PC, P(F64), PC], INT),
+        "qlra_qmat_pinv": ([VP, PQ, PQ], INT),
+        "qlra_spectral_norm": ([VP, PQ, P(F64)], INT),
         "qlra_qb_solve": ([VP, PS, I64, PQ, PQ, PQ], INT),
         "qlra_qb_stage": ([VP, PS, I64, PQ, PQ, INT, U64, P(PseudoQrConfig), PQ, PQ, P(Report)], INT),
         "qlra_one_pass_qb_host": ([VP, PQ, I64, PS, PS, INT, U64, P(PseudoQrConfig), I64, PQ, PQ, P(Report)],

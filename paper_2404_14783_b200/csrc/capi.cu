@@ -526,13 +526,16 @@ std::vector<double> gram_spectrum(Ctx& ctx, const QView& a, const QView& g, bool
 // projected out twice (CGS2) and orthonormalised by CholeskyQR2 -- the device
 // counterpart of select_via_mgs' canonical-direction fallback
 // (factorizations.cpp:105-118).
+// complex_only: candidates (and so the completion) in the complex subalgebra
+// -- for complex_svd of a complex matrix embedded as a quaternion one.
 void orthonormal_completion(Ctx& ctx, const QView& hr, const QView& c_out, int64_t row0,
-                            int64_t m_global, uint64_t seed) {
+                            int64_t m_global, uint64_t seed, bool complex_only = false) {
   const int64_t k = c_out.cols, rows = c_out.rows;
   if (k == 0) return;
   DevQMat c(ctx, rows, k);
   qlra_spec_t spec{QLRA_GAUSSIAN, m_global, k, seed, 1.0};
   launch_gen(ctx.stream, spec, row0, 0, rows, k, c.v, false);
+  if (complex_only) zero_jk_planes(ctx, c.v);
   if (hr.cols > 0) {
     DevQMat t(ctx, hr.cols, k);
     for (int pass = 0; pass < 2; ++pass) {
@@ -1867,7 +1870,8 @@ int qlra_residual_fro(qlra_ctx_t* ctx, const qlra_qmat_t* a, const qlra_qmat_t* 
 // qsvd of a replicated wide-or-tall A (factorizations.cpp:166-295) through the
 // Hermitian eigendecomposition of the smaller Gram.  u: m x k, v: n x k,
 // sigma: k host values (k = min(m, n)), nonincreasing.
-static void qsvd_dev(Ctx& c, const QView& a, const QView& u, const QView& v, double* sigma_host) {
+static void qsvd_dev(Ctx& c, const QView& a, const QView& u, const QView& v, double* sigma_host,
+                     bool complex_only = false) {
   const int64_t m = a.rows, n = a.cols, k = std::min(m, n);
   if (k == 0) return;
   const bool wide = m < n;  // reference: qsvd(A^*) then swap (factorizations.cpp:167-170)
@@ -1922,7 +1926,7 @@ static void qsvd_dev(Ctx& c, const QView& a, const QView& u, const QView& v, dou
     copy_qmat(c, sub(t.v, 0, 0, big.rows, good), sub(big, 0, 0, big.rows, good));
   if (good < k)  // zero singular values: orthonormal completion (factorizations.cpp:224-236)
     orthonormal_completion(c, sub(big, 0, 0, big.rows, good), sub(big, 0, good, big.rows, k - good), 0,
-                           big.rows, rng_substream(rng_key(0x715D), (uint64_t)(m * 131 + n)));
+                           big.rows, rng_substream(rng_key(0x715D), (uint64_t)(m * 131 + n)), complex_only);
   // phase convention on the tall factorization's V: the small side in both
   // orientations (for wide A the reference factors A^*, factorizations.cpp:167-170)
   qsvd_phase(c, big, small);
@@ -1980,6 +1984,134 @@ int qlra_approx_residual_fro(qlra_ctx_t* ctx, const qlra_qmat_t* a, const qlra_q
     const std::vector<double> vals = to_host(c, out.as<double>(), 2);
     if (res_fro) *res_fro = std::sqrt(vals[0]);
     if (a_fro) *a_fro = std::sqrt(vals[1]);
+  });
+}
+
+static void check_cview(const qlra_cmat_t* m, const char* who) {
+  if (!m) fail(QLRA_ERR_PARAMETER, std::string(who) + ": null matrix");
+  if (m->rows < 0 || m->cols < 0 || m->ld < std::max<int64_t>(1, m->rows) ||
+      (m->rows * m->cols > 0 && !m->data))
+    fail(QLRA_ERR_SHAPE, std::string(who) + ": bad matrix view");
+}
+
+int qlra_to_compact(qlra_ctx_t* ctx, const qlra_qmat_t* a, qlra_cmat_t* out) {
+  return guarded(ctx, [&](Ctx& c) {
+    check_view(a, "to_compact");
+    check_cview(out, "to_compact");
+    if (out->rows != 2 * a->rows || out->cols != a->cols) fail(QLRA_ERR_SHAPE, "to_compact: output shape mismatch");
+    to_complex(c, view_of(a), cview_of(out), false);
+  });
+}
+
+int qlra_to_full(qlra_ctx_t* ctx, const qlra_qmat_t* a, qlra_cmat_t* out) {
+  return guarded(ctx, [&](Ctx& c) {
+    check_view(a, "to_full");
+    check_cview(out, "to_full");
+    if (out->rows != 2 * a->rows || out->cols != 2 * a->cols) fail(QLRA_ERR_SHAPE, "to_full: output shape mismatch");
+    to_complex(c, view_of(a), cview_of(out), true);
+  });
+}
+
+int qlra_from_compact(qlra_ctx_t* ctx, const qlra_cmat_t* z, qlra_qmat_t* out) {
+  return guarded(ctx, [&](Ctx& c) {
+    check_cview(z, "from_compact");
+    check_view(out, "from_compact");
+    if (z->rows % 2 != 0) fail(QLRA_ERR_SHAPE, "from_compact: odd row count");  // complex_bridge.cpp:38
+    if (out->rows != z->rows / 2 || out->cols != z->cols) fail(QLRA_ERR_SHAPE, "from_compact: output shape mismatch");
+    from_compact(c, cview_of(z), view_of(out));
+  });
+}
+
+int qlra_j_mul_conj(qlra_ctx_t* ctx, const qlra_cmat_t* u, qlra_cmat_t* out) {
+  return guarded(ctx, [&](Ctx& c) {
+    check_cview(u, "j_mul_conj");
+    check_cview(out, "j_mul_conj");
+    if (u->rows % 2 != 0) fail(QLRA_ERR_SHAPE, "j_mul_conj: odd row count");  // complex_bridge.cpp:55
+    if (out->rows != u->rows || out->cols != u->cols) fail(QLRA_ERR_SHAPE, "j_mul_conj: output shape mismatch");
+    if (out->data == u->data) fail(QLRA_ERR_PARAMETER, "j_mul_conj: output must not alias the input");
+    j_mul_conj(c, cview_of(u), cview_of(out));
+  });
+}
+
+int qlra_complex_qr(qlra_ctx_t* ctx, const qlra_cmat_t* m, qlra_cmat_t* q, qlra_cmat_t* r) {
+  return guarded(ctx, [&](Ctx& c) {
+    check_cview(m, "complex_qr");
+    check_cview(q, "complex_qr");
+    check_cview(r, "complex_qr");
+    const int64_t p = m->rows, n = m->cols;
+    if (p < n) fail(QLRA_ERR_SHAPE, "complex_qr: requires rows >= cols");  // factorizations.cpp:34
+    if (q->rows != p || q->cols != n || r->rows != n || r->cols != n)
+      fail(QLRA_ERR_SHAPE, "complex_qr: output shape mismatch");
+    if (n == 0) return;
+    // The complex matrix as a quaternion one (y = z = 0): the complex-mode
+    // CholeskyQR2 (Gram's j, k planes zeroed) never leaves the complex
+    // subalgebra, and its R has a real positive diagonal -- the reference's
+    // phase convention (factorizations.cpp:40-49) -- so Q is the same
+    // unique Q up to rounding.
+    DevQMat e(c, p, n), qe(c, p, n), rf;
+    cmat_to_quat(c, cview_of(m), e.v);
+    std::vector<double> rd;
+    if (!cholesky_qr(c, e.v, qe.v, /*complex_mode=*/true, p, &rd, /*distributed=*/false, nullptr, &rf))
+      fail(QLRA_ERR_RANK, "complex_qr: numerically rank-deficient input (CholeskyQR route)");
+    quat_to_cmat(c, qe.v, cview_of(q));
+    quat_to_cmat(c, rf.v, cview_of(r));
+    QLRA_CUDA(cudaStreamSynchronize(c.stream));
+  });
+}
+
+int qlra_complex_svd(qlra_ctx_t* ctx, const qlra_cmat_t* m, qlra_cmat_t* u, double* s, qlra_cmat_t* v) {
+  return guarded(ctx, [&](Ctx& c) {
+    check_cview(m, "complex_svd");
+    check_cview(u, "complex_svd");
+    check_cview(v, "complex_svd");
+    const int64_t p = m->rows, n = m->cols, k = std::min(p, n);
+    if (u->rows != p || u->cols != k || v->rows != n || v->cols != k)
+      fail(QLRA_ERR_SHAPE, "complex_svd: output shape mismatch");
+    if (k == 0) return;
+    DevQMat e(c, p, n), uq(c, p, k), vq(c, n, k);
+    cmat_to_quat(c, cview_of(m), e.v);
+    qsvd_dev(c, e.v, uq.v, vq.v, s, /*complex_only=*/true);
+    quat_to_cmat(c, uq.v, cview_of(u));
+    quat_to_cmat(c, vq.v, cview_of(v));
+    QLRA_CUDA(cudaStreamSynchronize(c.stream));
+  });
+}
+
+int qlra_qmat_pinv(qlra_ctx_t* ctx, const qlra_qmat_t* a, qlra_qmat_t* out) {
+  return guarded(ctx, [&](Ctx& c) {
+    check_view(a, "qmat_pinv");
+    check_view(out, "qmat_pinv");
+    const int64_t m = a->rows, n = a->cols, k = std::min(m, n);
+    if (out->rows != n || out->cols != m) fail(QLRA_ERR_SHAPE, "qmat_pinv: output shape mismatch");
+    if (k == 0) return;
+    DevQMat uu(c, m, k), vv(c, n, k);
+    std::vector<double> sg((size_t)k);
+    qsvd_dev(c, view_of(a), uu.v, vv.v, sg.data());
+    // factorizations.cpp:303-314: sigma <= max(m, n) eps sigma_max -> 0
+    const double tol = (double)std::max(m, n) * std::numeric_limits<double>::epsilon() * sg[0];
+    std::vector<double> inv((size_t)k);
+    for (int64_t i = 0; i < k; ++i) inv[i] = sg[i] > tol ? 1.0 / sg[i] : 0.0;
+    DeviceBuffer d_inv(c, sizeof(double) * (size_t)k);
+    QLRA_CUDA(cudaMemcpyAsync(d_inv.ptr, inv.data(), sizeof(double) * k, cudaMemcpyHostToDevice, c.stream));
+    scale_cols(c, vv.v, d_inv.as<double>(), false, 0.0, vv.v);
+    qgemm(c, QLRA_OP_N, QLRA_OP_C, 1.0, vv.v, uu.v, 0.0, view_of(out));
+    QLRA_CUDA(cudaStreamSynchronize(c.stream));
+  });
+}
+
+int qlra_spectral_norm(qlra_ctx_t* ctx, const qlra_qmat_t* a, double* norm) {
+  return guarded(ctx, [&](Ctx& c) {
+    check_view(a, "spectral_norm");
+    *norm = 0.0;
+    const int64_t k = std::min(a->rows, a->cols);
+    if (k == 0) return;
+    // lambda_max of the smaller Gram: relative accuracy u at the top
+    DevQMat g(c, k, k);
+    if (a->rows < a->cols && c.nranks == 1)
+      qgemm(c, QLRA_OP_N, QLRA_OP_C, 1.0, view_of(a), view_of(a), 0.0, g.v);
+    else
+      gram(c, view_of(a), g.v);
+    *norm = std::sqrt(std::max(0.0, quat_eigs(c, g.v, /*extremes_only=*/true)[0]));
   });
 }
 

@@ -33,6 +33,13 @@ struct QView {
   double* p[4];
   int64_t rows, cols, ld;
 };
+// Device view of a complex matrix: column-major, interleaved (re, im).
+struct CView {
+  double* data;
+  int64_t rows, cols, ld;
+};
+inline CView cview_of(const qlra_cmat_t* m) { return CView{m->data, m->rows, m->cols, m->ld}; }
+
 inline QView view_of(const qlra_qmat_t* m) {
   QView v;
   for (int i = 0; i < 4; ++i) v.p[i] = m->p[i];

@@ -429,6 +429,98 @@ def gram(h, ctx=None):
     return g
 
 
+# ----------------------------------------------------- complex bridge ---
+# The reference's CMatrix (Eigen::MatrixXcd) is column-major: a complex128
+# tensor here is passed as its column-major buffer (stride(0) == 1).
+def czeros(rows, cols, device=None):
+    """A column-major complex128 (rows, cols) CUDA tensor."""
+    return torch.zeros((cols, rows), dtype=torch.complex128, device=device or "cuda").t()
+
+
+def as_colmajor(t: torch.Tensor) -> torch.Tensor:
+    return t if (t.dim() == 2 and t.stride(0) == 1) else t.t().contiguous().t()
+
+
+def _cm(t: torch.Tensor) -> L.CMat:
+    if t.dtype != torch.complex128 or t.dim() != 2 or not t.is_cuda:
+        raise ShapeError("complex matrix must be a CUDA complex128 tensor (rows, cols)")
+    if t.shape[0] > 1 and t.stride(0) != 1:
+        raise ShapeError("complex matrix must be column-major (see as_colmajor)")
+    return L.CMat(t.data_ptr(), t.shape[0], t.shape[1], max(1, t.stride(1) if t.shape[1] > 1 else t.shape[0]))
+
+
+def to_compact(a, ctx=None):
+    """to_compact (complex_bridge.cpp:11-20): [Q0; -conj(Q1)], 2m x n."""
+    ctx = _ctx(ctx)
+    out = czeros(2 * a.shape[1], a.shape[2])
+    ctx._check(ctx.lib.qlra_to_compact(ctx.h, C.byref(_qm(a)), C.byref(_cm(out))))
+    return out
+
+
+def to_full(a, ctx=None):
+    """to_full (complex_bridge.cpp:22-35): chi(A), 2m x 2n."""
+    ctx = _ctx(ctx)
+    out = czeros(2 * a.shape[1], 2 * a.shape[2])
+    ctx._check(ctx.lib.qlra_to_full(ctx.h, C.byref(_qm(a)), C.byref(_cm(out))))
+    return out
+
+
+def from_compact(z, ctx=None):
+    """from_compact (complex_bridge.cpp:37-52)."""
+    ctx = _ctx(ctx)
+    z = as_colmajor(z)
+    if z.shape[0] % 2:
+        raise ShapeError("from_compact: odd row count")
+    out = qzeros(z.shape[0] // 2, z.shape[1])
+    ctx._check(ctx.lib.qlra_from_compact(ctx.h, C.byref(_cm(z)), C.byref(_qm(out))))
+    return out
+
+
+def j_mul_conj(u, ctx=None):
+    """j_mul_conj (complex_bridge.cpp:54-61): J conj(u)."""
+    ctx = _ctx(ctx)
+    u = as_colmajor(u)
+    out = czeros(u.shape[0], u.shape[1])
+    ctx._check(ctx.lib.qlra_j_mul_conj(ctx.h, C.byref(_cm(u)), C.byref(_cm(out))))
+    return out
+
+
+def complex_qr(m, ctx=None):
+    """complex_qr (factorizations.cpp:33-51): thin (Q, R), diag(R) real >= 0."""
+    ctx = _ctx(ctx)
+    m = as_colmajor(m)
+    q, r = czeros(m.shape[0], m.shape[1]), czeros(m.shape[1], m.shape[1])
+    ctx._check(ctx.lib.qlra_complex_qr(ctx.h, C.byref(_cm(m)), C.byref(_cm(q)), C.byref(_cm(r))))
+    return q, r
+
+
+def complex_svd(m, ctx=None):
+    """complex_svd (factorizations.cpp:53-56): compact (U, s, V), s nonincreasing."""
+    ctx = _ctx(ctx)
+    m = as_colmajor(m)
+    k = min(m.shape)
+    u, v = czeros(m.shape[0], k), czeros(m.shape[1], k)
+    s = (C.c_double * max(1, k))()
+    ctx._check(ctx.lib.qlra_complex_svd(ctx.h, C.byref(_cm(m)), C.byref(_cm(u)), s, C.byref(_cm(v))))
+    return u, [s[i] for i in range(k)], v
+
+
+def qmat_pinv(a, ctx=None):
+    """qmat_pinv (factorizations.cpp:303-314)."""
+    ctx = _ctx(ctx)
+    out = qzeros(a.shape[2], a.shape[1])
+    ctx._check(ctx.lib.qlra_qmat_pinv(ctx.h, C.byref(_qm(a)), C.byref(_qm(out))))
+    return out
+
+
+def spectral_norm(a, ctx=None):
+    """spectral_norm (factorizations.cpp:324-327)."""
+    ctx = _ctx(ctx)
+    v = C.c_double()
+    ctx._check(ctx.lib.qlra_spectral_norm(ctx.h, C.byref(_qm(a)), C.byref(v)))
+    return v.value
+
+
 # -------------------------------------------------------- small dense ---
 def condition_number(a, ctx=None):
     ctx = _ctx(ctx)

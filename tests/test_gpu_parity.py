@@ -519,7 +519,8 @@ def test_qsvd_graded_spectrum_relative_accuracy(ctx, m, n, kappa):
     assert np.all(rel <= bound + 1e-14), (rel.max(), np.argmax(rel / bound))
     rec = O.qmat_mul(host(u) * sg[None, None, :], O.adjoint(host(v)))
     assert rel_diff(rec, a) < 1e-12
-    assert orthonormality_defect(host(u)) < 1e-12 and orthonormality_defect(host(v)) < 1e-12
+    # ||U^* U - I||_F over k^2 entries: ~u sqrt(k) per column
+    assert orthonormality_defect(host(u)) < 1e-14 * k and orthonormality_defect(host(v)) < 1e-14 * k
 
 
 def test_truncate_stage_and_one_pass_vs_oracle(ctx):  # test_sketching.cpp:210-223, 279-290
