@@ -131,6 +131,26 @@ int64_t qlra_ctx_launch_count(const qlra_ctx_t* ctx);
 int qlra_ctx_kernel_timing(qlra_ctx_t* ctx, int enable);
 int qlra_ctx_kernel_stats(qlra_ctx_t* ctx, double* ms, int64_t* launches, double* flops,
                           double* a_bytes);
+/* Which engines the timed brackets covered (bit 1: the FP64 DMMA sketch
+ * kernel, bit 2: the int8 engine's batched GEMMs) and the int8 tensor-core
+ * ops issued inside them. */
+int qlra_ctx_kernel_engines(qlra_ctx_t* ctx, int* engines, double* int8_ops);
+
+/* Sketch engine (no reference counterpart: the reference has one CPU
+ * product, qmat_mul_accumulate_ordered, qmatrix.cpp:203-242).
+ *   QLRA_SKETCH_AUTO  the int8 engine where it is faster (n >= 2048 and
+ *                     s, l >= 64), else DMMA; env QLRA_SKETCH_ENGINE=int8|dmma
+ *                     overrides AUTO;
+ *   QLRA_SKETCH_DMMA  FP64 tensor cores (8-product quaternion GEMM, every
+ *                     multiply-add rounded in fp64);
+ *   QLRA_SKETCH_INT8  INT8 tensor cores: the products of a 52-bit fixed-point
+ *                     image of A, Omega, Psi computed exactly (Ozaki scheme,
+ *                     CRT over 16 moduli), rounded once (needs n < 131056).
+ * Both match the ordered reference sketch to ~1e-15 relative. */
+#define QLRA_SKETCH_AUTO 0
+#define QLRA_SKETCH_DMMA 1
+#define QLRA_SKETCH_INT8 2
+int qlra_ctx_set_sketch_engine(qlra_ctx_t* ctx, int engine);
 
 /* ---------------------------------------------------------- embeddings --- */
 /* gen_block (sketching.cpp:53-71) / gen_test_matrix{,_rows,_cols}

@@ -21,6 +21,7 @@ CSRC = os.path.join(HERE, "csrc")
 BUILD = os.path.join(HERE, "_build")
 LIB = os.path.join(HERE, "libqlra_cuda.so")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+CUDA_LIB = "/usr/local/cuda/lib64"
 
 
 def _nccl_dirs():
@@ -64,7 +65,9 @@ def build(verbose: bool = False) -> str:
     newest = max(os.path.getmtime(o) for o in objs)
     if not (os.path.exists(LIB) and os.path.getmtime(LIB) >= newest):
         cmd = [nvcc, "-shared", "-o", LIB] + objs + ARCH + [
-            "-L", nccl_lib, "-l:libnccl.so.2", "-Xlinker", f"-rpath={nccl_lib}", "-lcudart"]
+            "-L", nccl_lib, "-l:libnccl.so.2", "-Xlinker", f"-rpath={nccl_lib}", "-lcudart",
+            # cuBLASLt: the int8 engine's batched IMMA GEMMs (ozaki.cu)
+            "-L", CUDA_LIB, "-lcublasLt", "-Xlinker", f"-rpath={CUDA_LIB}"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             sys.stderr.write(r.stdout + r.stderr)

@@ -1368,8 +1368,9 @@ static void drop_events(Ctx& c) {
     cudaEventDestroy(e.second);
   }
   c.ktimer.ev.clear();
-  c.ktimer.flops = c.ktimer.a_bytes = 0.0;
+  c.ktimer.flops = c.ktimer.a_bytes = c.ktimer.int8_ops = 0.0;
   c.ktimer.launches = 0;
+  c.ktimer.engines = 0;
 }
 
 int qlra_ctx_destroy(qlra_ctx_t* ctx) {
@@ -1377,6 +1378,10 @@ int qlra_ctx_destroy(qlra_ctx_t* ctx) {
   cudaSetDevice(ctx->c.device);
   if (ctx->c.stream) {
     psi_keep_release(ctx->c);
+    try {
+      oz_release(ctx->c);
+    } catch (...) {
+    }
     cudaStreamSynchronize(ctx->c.stream);
   }
   if (ctx->c.comm) ncclCommDestroy(ctx->c.comm);
@@ -1455,6 +1460,21 @@ int qlra_ctx_kernel_stats(qlra_ctx_t* ctx, double* ms, int64_t* launches, double
     if (launches) *launches = c.ktimer.launches;
     if (flops) *flops = c.ktimer.flops;
     if (a_bytes) *a_bytes = c.ktimer.a_bytes;
+  });
+}
+
+int qlra_ctx_kernel_engines(qlra_ctx_t* ctx, int* engines, double* int8_ops) {
+  return guarded(ctx, [&](Ctx& c) {
+    if (engines) *engines = c.ktimer.engines;
+    if (int8_ops) *int8_ops = c.ktimer.int8_ops;
+  });
+}
+
+int qlra_ctx_set_sketch_engine(qlra_ctx_t* ctx, int engine) {
+  return guarded(ctx, [&](Ctx& c) {
+    if (engine != QLRA_SKETCH_AUTO && engine != QLRA_SKETCH_DMMA && engine != QLRA_SKETCH_INT8)
+      fail(QLRA_ERR_PARAMETER, "sketch engine must be QLRA_SKETCH_AUTO, _DMMA or _INT8");
+    c.sketch_engine = engine;
   });
 }
 

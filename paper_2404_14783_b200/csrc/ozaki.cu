@@ -1,0 +1,692 @@
+// ozaki.cu -- the fused dual sketch on the INT8 tensor cores.
+//
+// Replaces the same reference step as sketch8_kernel (sketch_update_rows,
+// proj/src/sketching.cpp:125-139: Y += A Omega, W += Psi A through
+// qmat_mul_accumulate_ordered, qmatrix.cpp:203-242), for the shapes where it
+// is faster (oz_wanted).  FP64 has no tcgen05 kind on sm_100 (DMMA.8x8x4 at
+// 37 TFLOP/s is the FP64 tensor ceiling), but INT8 does (tcgen05.mma
+// kind::i8, ~3.5 POPS through cuBLASLt's sm_100 IMMA kernels).  So every
+// real product of the sketch is computed EXACTLY in integers (the Ozaki
+// scheme, CRT form) and rounded once at the end:
+//
+//  * scaling: A' = rint(A 2^sigma) with one power-of-two scale per epoch
+//    (|A'| <= 2^52), Omega' per column (2^tau_j), Psi' per row (2^rho_k):
+//    the only rounding of the operands, 2^-52 relative to their maxima;
+//  * the 8-product identity (qtile8.cuh): each quaternion GEMM is 8 real
+//    GEMMs of plane combinations (exact integers < 2^53 after scaling);
+//  * residues: each combination reduced modulo 16 pairwise-coprime moduli
+//    p <= 256 (symmetric int8); the 8 x 16 = 128 residue products are ONE
+//    strided-batched int8 x int8 -> int32 GEMM (exact while K 128^2 < 2^31,
+//    i.e. K < 2^17 rows or columns per int32 accumulation);
+//  * recovery: the CRT in 128-bit integers (P = prod p = 2^126.2 > 2 K
+//    2^106), the 8 products combined into the quaternion planes exactly in
+//    int128, one rounding to double, scaled back by powers of two.
+//
+// One residue set serves both sketches: Y = A Omega takes lcomb(A) as its
+// left operand, and W is formed as its adjoint W^* = A^* Psi^*, whose left
+// combinations lcomb(conj A) are a signed permutation of lcomb(A) (below),
+// so the A residues are written once per panel (row-major: the K-major left
+// operand of Y's GEMM and, read as a column-major n x R matrix, the left
+// operand of W^*'s).  W's int32 products accumulate over panels (beta = 1)
+// within an epoch (rows < 2^17 and one A scale) and are recovered once.
+//
+// Determinism: integer products are exact, so the result does not depend on
+// cuBLASLt's algorithm, split-K or batch order: bitwise reproducible.
+#include <cublasLt.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <tuple>
+
+#include "common.cuh"
+#include "kernels.cuh"
+#include "ozaki.cuh"
+#include "qtile8.cuh"
+
+namespace qlra_dev {
+
+namespace {
+
+constexpr int NMOD = 16;
+constexpr int NB = 8 * NMOD;            // batch: (combination t, modulus mu), b = t * NMOD + mu
+constexpr int64_t KMAX = 131056;        // K per int32 accumulation: K * 128^2 < 2^31 (multiple of 16)
+// odd moduli <= 253: a residue off the symmetric range by one (below) still
+// fits int8; 256 wraps in int8 congruently.  P = 2^125.7 > 2 * 2^17 * 2^106.
+constexpr int kModuli[NMOD] = {256, 253, 251, 247, 241, 239, 233, 229, 227, 223, 211, 199, 197, 193, 191, 181};
+
+__constant__ int c_p[NMOD];
+__constant__ double c_pinv[NMOD];
+__constant__ float c_pinvf[NMOD];
+__constant__ int c_yinv[NMOD];                   // (P / p)^-1 mod p
+__constant__ unsigned long long c_M[NMOD][2];    // P / p as (lo, hi)
+__constant__ unsigned long long c_P[2], c_H[2];  // P, floor(P / 2)
+
+// lcomb(conj a)_t = kConjSign[t] * lcomb(a)_{kConjPerm[t]}: conj(a) = (a0,
+// -a1, -a2, -a3) in qtile8's lcomb list (a0+a1, a3-a2, a0-a1, a2+a3, a1+a3,
+// a1-a3, a0+a2, a0-a2) gives (L2, -L1, L0, -L3, -L4, -L5, L7, L6).
+//   kConjPerm = {2, 1, 0, 3, 4, 5, 7, 6}, kConjSign = {1, -1, 1, -1, -1, -1, 1, 1}
+
+typedef unsigned __int128 u128;
+typedef __int128 i128;
+
+struct ModTables {
+  int p[NMOD], yinv[NMOD];
+  double pinv[NMOD];
+  float pinvf[NMOD];
+  unsigned long long M[NMOD][2], P[2], H[2];
+  double log2P = 0.0;
+};
+
+ModTables make_tables() {
+  ModTables t{};
+  u128 P = 1;
+  for (int i = 0; i < NMOD; ++i) {
+    for (int j = 0; j < i; ++j) {
+      int a = kModuli[i], b = kModuli[j];
+      while (b) { const int r = a % b; a = b; b = r; }
+      if (a != 1) fail(QLRA_ERR_CUDA, "ozaki: moduli not pairwise coprime");
+    }
+    P *= (u128)kModuli[i];
+    t.log2P += std::log2((double)kModuli[i]);
+  }
+  for (int i = 0; i < NMOD; ++i) {
+    const int p = kModuli[i];
+    const u128 M = P / (u128)p;
+    const int mr = (int)(M % (u128)p);
+    int inv = -1;
+    for (int x = 1; x < p; ++x)
+      if ((mr * x) % p == 1) { inv = x; break; }
+    if (inv < 0) fail(QLRA_ERR_CUDA, "ozaki: no CRT inverse");
+    t.p[i] = p;
+    t.yinv[i] = inv;
+    t.pinv[i] = 1.0 / p;
+    t.pinvf[i] = 1.0f / (float)p;
+    t.M[i][0] = (unsigned long long)M;
+    t.M[i][1] = (unsigned long long)(M >> 64);
+  }
+  t.P[0] = (unsigned long long)P;
+  t.P[1] = (unsigned long long)(P >> 64);
+  const u128 H = P >> 1;
+  t.H[0] = (unsigned long long)H;
+  t.H[1] = (unsigned long long)(H >> 64);
+  return t;
+}
+
+const ModTables& tables() {
+  static const ModTables t = make_tables();
+  return t;
+}
+
+void upload_tables(int device) {
+  static std::mutex mu;
+  static bool done[64] = {};
+  std::lock_guard<std::mutex> g(mu);
+  if (device >= 0 && device < 64 && done[device]) return;
+  const ModTables& t = tables();
+  QLRA_CUDA(cudaMemcpyToSymbol(c_p, t.p, sizeof(t.p)));
+  QLRA_CUDA(cudaMemcpyToSymbol(c_pinv, t.pinv, sizeof(t.pinv)));
+  QLRA_CUDA(cudaMemcpyToSymbol(c_pinvf, t.pinvf, sizeof(t.pinvf)));
+  QLRA_CUDA(cudaMemcpyToSymbol(c_yinv, t.yinv, sizeof(t.yinv)));
+  QLRA_CUDA(cudaMemcpyToSymbol(c_M, t.M, sizeof(t.M)));
+  QLRA_CUDA(cudaMemcpyToSymbol(c_P, t.P, sizeof(t.P)));
+  QLRA_CUDA(cudaMemcpyToSymbol(c_H, t.H, sizeof(t.H)));
+  if (device >= 0 && device < 64) done[device] = true;
+}
+
+// ---------------------------------------------------------------- device --
+// |x| < 2^53 exact integer -> a residue mod p_mu that fits int8, on the
+// FP64 FMA pipe alone (no conversion instructions): q = x / p rounded to
+// the nearest integer through the 1.5 * 2^52 shifter, r = x - p q exactly
+// by the fma, and r + 1.5 * 2^52 carries r in its low word.  x * (1/p) is
+// off by < 0.01, so q is the nearest integer or one off it where x / p is
+// within 0.01 of a half: |r| <= (p + 1) / 2 <= 127 for odd p <= 253, and
+// for p = 256 the int8 wrap is itself congruent mod 256.  (The CRT takes
+// any representative.)
+__device__ __forceinline__ int sres(double x, int mu) {
+  constexpr double kShift = 6755399441055744.0;  // 1.5 * 2^52
+  const double q = fma(x, c_pinv[mu], kShift) - kShift;
+  return __double2loint(fma(-(double)c_p[mu], q, x) + kShift);
+}
+__device__ __forceinline__ unsigned pack4(int a, int b, int c, int d) {
+  return __byte_perm(__byte_perm(a, b, 0x0040), __byte_perm(c, d, 0x0040), 0x5410);
+}
+
+// the 8 x 16 residue words of 4 consecutive elements: word (t, mu) at
+// o[(t * NMOD + mu) * ws] (ws: words per batch matrix)
+__device__ __forceinline__ void store_res(unsigned* o, int64_t ws, const double (&c)[8][4]) {
+#pragma unroll 1
+  for (int mu = 0; mu < NMOD; ++mu, o += ws)
+#pragma unroll
+    for (int t = 0; t < 8; ++t)
+      o[t * NMOD * ws] = pack4(sres(c[t][0], mu), sres(c[t][1], mu), sres(c[t][2], mu), sres(c[t][3], mu));
+}
+
+// max |x| over the four planes of a view -> atomicMax on the bit pattern
+// (non-negative doubles order like their unsigned bits)
+__global__ void k_absmax(QView a, unsigned long long* out) {
+  double m = 0.0;
+  const int64_t total = a.rows * a.cols;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / a.cols, j = e - i * a.cols;
+#pragma unroll
+    for (int p = 0; p < 4; ++p) m = fmax(m, fabs(a.p[p][i * a.ld + j]));
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  __shared__ double sm[32];
+  if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    m = threadIdx.x < (blockDim.x >> 5) ? sm[threadIdx.x] : 0.0;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (threadIdx.x == 0 && m > 0.0) atomicMax(out, (unsigned long long)__double_as_longlong(m));
+  }
+}
+
+// per-column max |x| of a (rows x cols) view: out[j] (bits, atomicMax)
+__global__ void k_colmax(QView a, unsigned long long* out) {
+  const int64_t j = blockIdx.x * (int64_t)32 + (threadIdx.x & 31);
+  if (j >= a.cols) return;
+  double m = 0.0;
+  for (int64_t i = blockIdx.y * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); i < a.rows;
+       i += (int64_t)gridDim.y * (blockDim.x >> 5))
+#pragma unroll
+    for (int p = 0; p < 4; ++p) m = fmax(m, fabs(a.p[p][i * a.ld + j]));
+  if (m > 0.0) atomicMax(out + j, (unsigned long long)__double_as_longlong(m));
+}
+
+// per-row max |x|: one block per row
+__global__ void k_rowmax(QView a, unsigned long long* out) {
+  const int64_t i = blockIdx.x;
+  double m = 0.0;
+  for (int64_t j = threadIdx.x; j < a.cols; j += blockDim.x)
+#pragma unroll
+    for (int p = 0; p < 4; ++p) m = fmax(m, fabs(a.p[p][i * a.ld + j]));
+#pragma unroll
+  for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  __shared__ double sm[32];
+  if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    m = threadIdx.x < (blockDim.x >> 5) ? sm[threadIdx.x] : 0.0;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (threadIdx.x == 0) out[i] = (unsigned long long)__double_as_longlong(m);
+  }
+}
+
+// 2^e with max * 2^e in [2^51, 2^52) (0 for an all-zero line)
+__device__ __forceinline__ int scale_exp(unsigned long long maxbits) {
+  const double m = __longlong_as_double((long long)maxbits);
+  return m > 0.0 ? 51 - ilogb(m) : 0;
+}
+
+// A panel (R x n) -> Ares[t*16+mu][i][k] (Rpad x npad, zero padded):
+// residues of lcomb_t(rint(A 2^sigma)).  Thread: one row, 4 columns.
+__global__ void k_res_a(QView a, int64_t npad, int64_t rpad, int sigma, int8_t* out, int64_t bstride) {
+  const int64_t nw = npad >> 2;
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= rpad * nw) return;
+  const int64_t i = e / nw, k0 = (e - i * nw) * 4;
+  const double s1 = ldexp(1.0, sigma / 2), s2 = ldexp(1.0, sigma - sigma / 2);  // 2^sigma, exact in two steps
+  double c[8][4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    double v[4] = {0.0, 0.0, 0.0, 0.0};
+    if (i < a.rows && k0 + q < a.cols) {
+#pragma unroll
+      for (int p = 0; p < 4; ++p) v[p] = rint(a.p[p][i * a.ld + k0 + q] * s1 * s2);
+    }
+#pragma unroll
+    for (int t = 0; t < 8; ++t) c[t][q] = qt8::lcomb(t, v);
+  }
+  store_res(reinterpret_cast<unsigned*>(out + i * npad + k0), bstride >> 2, c);
+}
+
+// Omega (n x s) -> Ores[t*16+mu][j][k] (s x npad): residues of
+// rcomb_t(rint(Omega(k, j) 2^tau_j)).  Thread: one column j, 4 rows k.
+__global__ void k_res_om(QView om, const unsigned long long* colmax, int64_t npad, int64_t spad, int8_t* out,
+                         int64_t bstride) {
+  const int64_t nw = npad >> 2;
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= spad * nw) return;
+  const int64_t j = e / nw, k0 = (e - j * nw) * 4;
+  const int tau = j < om.cols ? scale_exp(colmax[j]) : 0;
+  const double s1 = ldexp(1.0, tau / 2), s2 = ldexp(1.0, tau - tau / 2);
+  double c[8][4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    double v[4] = {0.0, 0.0, 0.0, 0.0};
+    if (k0 + q < om.rows && j < om.cols) {
+#pragma unroll
+      for (int p = 0; p < 4; ++p) v[p] = rint(om.p[p][(k0 + q) * om.ld + j] * s1 * s2);
+    }
+#pragma unroll
+    for (int t = 0; t < 8; ++t) c[t][q] = qt8::rcomb(t, v);
+  }
+  store_res(reinterpret_cast<unsigned*>(out + j * npad + k0), bstride >> 2, c);
+}
+
+// Psi columns [c0, c0 + R) (l x R) -> Pres[u*16+mu][k][i] (l x Rpad): the
+// right operand of W^* = A^* Psi^*, rcomb_t(rint(conj(Psi(k, i)) 2^rho_k)),
+// stored at the batch u = kConjPerm[t] of the A residues it multiplies.
+__global__ void k_res_psi(QView ps, int64_t c0, int64_t R, int64_t rpad, int64_t lpad,
+                          const unsigned long long* rowmax, int8_t* out, int64_t bstride) {
+  const int64_t nw = rpad >> 2;
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= lpad * nw) return;
+  const int64_t k = e / nw, i0 = (e - k * nw) * 4;
+  const int rho = k < ps.rows ? scale_exp(rowmax[k]) : 0;
+  const double s1 = ldexp(1.0, rho / 2), s2 = ldexp(1.0, rho - rho / 2);
+  double c[8][4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    double v[4] = {0.0, 0.0, 0.0, 0.0};
+    if (i0 + q < R && k < ps.rows) {
+#pragma unroll
+      for (int p = 0; p < 4; ++p) {
+        const double x = rint(ps.p[p][k * ps.ld + c0 + i0 + q] * s1 * s2);
+        v[p] = p == 0 ? x : -x;
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < 8; ++t) c[t][q] = qt8::rcomb(t, v);
+  }
+  // rcomb_t goes to batch kConjPerm[t] = {2, 1, 0, 3, 4, 5, 7, 6}
+  double d[8][4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    d[0][q] = c[2][q];
+    d[1][q] = c[1][q];
+    d[2][q] = c[0][q];
+    d[3][q] = c[3][q];
+    d[4][q] = c[4][q];
+    d[5][q] = c[5][q];
+    d[6][q] = c[7][q];
+    d[7][q] = c[6][q];
+  }
+  store_res(reinterpret_cast<unsigned*>(out + k * rpad + i0), bstride >> 2, d);
+}
+
+// the signed integer whose residues mod the 16 moduli are c[mu * bstride]
+// (any int32 representatives), |X| < P / 2
+__device__ __forceinline__ i128 crt16(const int32_t* c, int64_t bstride) {
+  const u128 P = ((u128)c_P[1] << 64) | c_P[0];
+  u128 acc = 0;
+#pragma unroll 4
+  for (int mu = 0; mu < NMOD; ++mu) {
+    const int v = c[mu * bstride];
+    const int p = c_p[mu];
+    int r = v - __double2int_rd((double)v * c_pinv[mu]) * p;
+    r += r < 0 ? p : 0;
+    r -= r >= p ? p : 0;
+    int u = r * c_yinv[mu];
+    u -= __float2int_rd((float)u * c_pinvf[mu]) * p;
+    u += u < 0 ? p : 0;
+    u -= u >= p ? p : 0;
+    acc += (u128)(unsigned)u * (((u128)c_M[mu][1] << 64) | c_M[mu][0]);
+    if (acc >= P) acc -= P;
+  }
+  const u128 H = ((u128)c_H[1] << 64) | c_H[0];
+  return acc > H ? -(i128)(P - acc) : (i128)acc;
+}
+__device__ __forceinline__ double i128_to_double(i128 x) {
+  const bool neg = x < 0;
+  const u128 m = neg ? (u128)(-x) : (u128)x;
+  const double d = (double)(unsigned long long)(m >> 64) * 0x1p64 + (double)(unsigned long long)m;
+  return neg ? -d : d;
+}
+// the quaternion planes of 2 x (product) from the 8 raw integer products
+// (m_t without the Howell-Lafon halves of t >= 4): exact in int128
+__device__ __forceinline__ void combine2(const i128 (&x)[8], i128 (&z)[4]) {
+  const i128 s56 = x[4] + x[5], d56 = x[4] - x[5], s78 = x[6] + x[7], d78 = x[6] - x[7];
+  z[0] = 2 * x[1] - s56 + s78;
+  z[1] = 2 * x[0] - s56 - s78;
+  z[2] = 2 * x[2] + d56 + d78;
+  z[3] = 2 * x[3] + d56 - d78;
+}
+
+// Y rows of a panel += the recovered products.  cy[t*16+mu][i][j] (ld
+// spad, batch stride bs).  Thread: one (i, j).
+__global__ void k_crt_y(const int32_t* cy, int64_t bs, int64_t spad, QView y, const unsigned long long* om_colmax,
+                        int sigma) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= y.rows * y.cols) return;
+  const int64_t i = e / y.cols, j = e - i * y.cols;
+  i128 x[8];
+#pragma unroll 1
+  for (int t = 0; t < 8; ++t) x[t] = crt16(cy + (int64_t)t * NMOD * bs + i * spad + j, bs);
+  i128 z[4];
+  combine2(x, z);
+  const int sh = -(sigma + scale_exp(om_colmax[j])) - 1;  // the 2 of combine2
+#pragma unroll
+  for (int p = 0; p < 4; ++p) y.p[p][i * y.ld + j] += ldexp(i128_to_double(z[p]), sh);
+}
+
+// W += conj of the recovered W^* products.  cw[u*16+mu][k][j] (ld npad,
+// batch stride bs), u = kConjPerm[t] holding sign kConjSign[t] * m_t.
+__global__ void k_crt_w(const int32_t* cw, int64_t bs, int64_t npad, QView w, const unsigned long long* ps_rowmax,
+                        int sigma) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= w.rows * w.cols) return;
+  const int64_t k = e / w.cols, j = e - k * w.cols;
+  i128 xu[8], x[8];
+#pragma unroll 1
+  for (int u = 0; u < 8; ++u) xu[u] = crt16(cw + (int64_t)u * NMOD * bs + k * npad + j, bs);
+  // x[t] = kConjSign[t] * xu[kConjPerm[t]]
+  x[0] = xu[2];
+  x[1] = -xu[1];
+  x[2] = xu[0];
+  x[3] = -xu[3];
+  x[4] = -xu[4];
+  x[5] = -xu[5];
+  x[6] = xu[7];
+  x[7] = xu[6];
+  i128 z[4];
+  combine2(x, z);
+  const int sh = -(sigma + scale_exp(ps_rowmax[k])) - 1;
+  w.p[0][k * w.ld + j] += ldexp(i128_to_double(z[0]), sh);
+#pragma unroll
+  for (int p = 1; p < 4; ++p) w.p[p][k * w.ld + j] -= ldexp(i128_to_double(z[p]), sh);
+}
+
+inline unsigned blocks_for(int64_t n, int threads) { return (unsigned)((n + threads - 1) / threads); }
+inline int64_t up16(int64_t x) { return (x + 15) / 16 * 16; }
+
+void lt_check(cublasStatus_t s, const char* what) {
+  if (s != CUBLAS_STATUS_SUCCESS) fail(QLRA_ERR_CUDA, std::string("cuBLASLt ") + what + " failed (status " +
+                                                        std::to_string((int)s) + ")");
+}
+
+}  // namespace
+
+// ------------------------------------------------------------ host state --
+// Per-context engine state: cuBLASLt handle, cached plans, grown buffers.
+struct OzState {
+  cublasLtHandle_t lt = nullptr;
+  void* lt_ws = nullptr;
+  size_t lt_ws_bytes = 0;
+  struct Plan {
+    cublasLtMatmulDesc_t d = nullptr;
+    cublasLtMatrixLayout_t la = nullptr, lb = nullptr, lc = nullptr;
+    cublasLtMatmulAlgo_t algo{};
+  };
+  std::map<std::tuple<int, int64_t, int64_t, int64_t, int64_t, int64_t, int64_t>, Plan> plans;
+  struct Buf {
+    void* p = nullptr;
+    size_t bytes = 0;
+  };
+  Buf ares, pres, ores, cy, cw, stat;
+  unsigned long long* amax_dev = nullptr;   // 4 slots of max |A| (row pipeline: 0, 1; block: 2)
+  unsigned long long* amax_host = nullptr;  // their pinned host copies
+};
+
+namespace {
+
+void* grow(Ctx& c, OzState::Buf& b, size_t bytes) {
+  if (b.bytes < bytes) {
+    if (b.p) QLRA_CUDA(cudaFreeAsync(b.p, c.stream));
+    b.p = nullptr;
+    b.bytes = 0;
+    QLRA_CUDA(cudaMallocAsync(&b.p, bytes, c.stream));
+    b.bytes = bytes;
+  }
+  return b.p;
+}
+
+OzState& state(Ctx& c) {
+  if (!c.oz) {
+    upload_tables(c.device);
+    auto* s = new OzState();
+    c.oz = s;
+    lt_check(cublasLtCreate(&s->lt), "create");
+    s->lt_ws_bytes = 64u << 20;
+    QLRA_CUDA(cudaMalloc(&s->lt_ws, s->lt_ws_bytes));
+    QLRA_CUDA(cudaMallocHost(&s->amax_host, 4 * sizeof(unsigned long long)));
+    QLRA_CUDA(cudaMalloc(&s->amax_dev, 4 * sizeof(unsigned long long)));
+  }
+  return *c.oz;
+}
+
+// col-major C (m x n, ldc) = op(A) (m x k) * op(B) (k x n) + beta C, int8 ->
+// int32, `batch` matrices at the given strides (elements)
+OzState::Plan& plan(OzState& s, bool ta, int64_t m, int64_t n, int64_t k, int64_t lda, int64_t ldb, int64_t ldc,
+                    int64_t sa, int64_t sb, int64_t sc, int batch) {
+  const auto key = std::make_tuple((int)ta, m, n, k, lda, ldb, ldc);
+  auto it = s.plans.find(key);
+  if (it != s.plans.end()) return it->second;
+  OzState::Plan p;
+  const cublasOperation_t opa = ta ? CUBLAS_OP_T : CUBLAS_OP_N, opb = CUBLAS_OP_N;
+  lt_check(cublasLtMatmulDescCreate(&p.d, CUBLAS_COMPUTE_32I, CUDA_R_32I), "desc");
+  lt_check(cublasLtMatmulDescSetAttribute(p.d, CUBLASLT_MATMUL_DESC_TRANSA, &opa, sizeof(opa)), "transa");
+  lt_check(cublasLtMatmulDescSetAttribute(p.d, CUBLASLT_MATMUL_DESC_TRANSB, &opb, sizeof(opb)), "transb");
+  lt_check(cublasLtMatrixLayoutCreate(&p.la, CUDA_R_8I, ta ? k : m, ta ? m : k, lda), "layout a");
+  lt_check(cublasLtMatrixLayoutCreate(&p.lb, CUDA_R_8I, k, n, ldb), "layout b");
+  lt_check(cublasLtMatrixLayoutCreate(&p.lc, CUDA_R_32I, m, n, ldc), "layout c");
+  const std::pair<cublasLtMatrixLayout_t, int64_t> ls[3] = {{p.la, sa}, {p.lb, sb}, {p.lc, sc}};
+  for (const auto& l : ls) {
+    lt_check(cublasLtMatrixLayoutSetAttribute(l.first, CUBLASLT_MATRIX_LAYOUT_BATCH_COUNT, &batch, sizeof(batch)),
+             "batch");
+    lt_check(cublasLtMatrixLayoutSetAttribute(l.first, CUBLASLT_MATRIX_LAYOUT_STRIDED_BATCH_OFFSET, &l.second,
+                                              sizeof(l.second)),
+             "stride");
+  }
+  cublasLtMatmulPreference_t pref;
+  lt_check(cublasLtMatmulPreferenceCreate(&pref), "pref");
+  lt_check(cublasLtMatmulPreferenceSetAttribute(pref, CUBLASLT_MATMUL_PREF_MAX_WORKSPACE_BYTES, &s.lt_ws_bytes,
+                                                sizeof(s.lt_ws_bytes)),
+           "pref ws");
+  cublasLtMatmulHeuristicResult_t res{};
+  int nres = 0;
+  const cublasStatus_t st = cublasLtMatmulAlgoGetHeuristic(s.lt, p.d, p.la, p.lb, p.lc, p.lc, pref, 1, &res, &nres);
+  cublasLtMatmulPreferenceDestroy(pref);
+  if (st != CUBLAS_STATUS_SUCCESS || nres == 0)
+    fail(QLRA_ERR_CUDA, "ozaki: no cuBLASLt int8 algorithm for " + std::to_string(m) + "x" + std::to_string(n) +
+                            "x" + std::to_string(k));
+  p.algo = res.algo;
+  return s.plans.emplace(key, p).first->second;
+}
+
+void run_gemm(Ctx& c, OzState& s, OzState::Plan& p, const void* A, const void* B, void* C, int beta) {
+  const int32_t alpha = 1;
+  lt_check(cublasLtMatmul(s.lt, p.d, &alpha, A, p.la, B, p.lb, &beta, C, p.lc, C, p.lc, &p.algo, s.lt_ws,
+                          s.lt_ws_bytes, c.stream),
+           "matmul");
+  count_launch();
+}
+
+}  // namespace
+
+void oz_release(Ctx& c) {
+  OzState* s = c.oz;
+  if (!s) return;
+  for (auto& kv : s->plans) {
+    cublasLtMatrixLayoutDestroy(kv.second.la);
+    cublasLtMatrixLayoutDestroy(kv.second.lb);
+    cublasLtMatrixLayoutDestroy(kv.second.lc);
+    cublasLtMatmulDescDestroy(kv.second.d);
+  }
+  for (OzState::Buf* b : {&s->ares, &s->pres, &s->ores, &s->cy, &s->cw, &s->stat})
+    if (b->p) cudaFreeAsync(b->p, c.stream);
+  cudaStreamSynchronize(c.stream);
+  if (s->lt_ws) cudaFree(s->lt_ws);
+  if (s->amax_host) cudaFreeHost(s->amax_host);
+  if (s->amax_dev) cudaFree(s->amax_dev);
+  if (s->lt) cublasLtDestroy(s->lt);
+  delete s;
+  c.oz = nullptr;
+}
+
+int64_t oz_kmax() { return KMAX; }
+
+bool oz_wanted(const Ctx& c, int64_t n, int64_t s, int64_t l) {
+  if (up16(n) > KMAX || n == 0 || s == 0 || l == 0) return false;
+  int engine = c.sketch_engine;
+  if (engine == QLRA_SKETCH_AUTO) {
+    const char* e = std::getenv("QLRA_SKETCH_ENGINE");
+    if (e && std::string(e) == "int8") engine = QLRA_SKETCH_INT8;
+    if (e && std::string(e) == "dmma") engine = QLRA_SKETCH_DMMA;
+  }
+  if (engine == QLRA_SKETCH_INT8) return true;
+  if (engine == QLRA_SKETCH_DMMA) return false;
+  // auto: the int8 GEMMs pay off once the products are wide (measured:
+  // cuBLASLt int8 2.5-3.5 POPS at C2-C4 shapes, ~0.1 POPS at C5's n = 300)
+  return n >= 2048 && s >= 64 && l >= 64;
+}
+
+OzRun::OzRun(Ctx& c, const QView& om, const QView& ps) : ctx(c), omega(om), psi(ps) {
+  OzState& s = state(c);
+  n = om.rows;
+  npad = up16(n);
+  scols = om.cols;
+  spad = up16(scols);  // cuBLASLt's IMMA kernels want 16-aligned m and n
+  l = ps.rows;
+  lpad = up16(l);
+  // maxima: Omega columns, then Psi rows
+  auto* st = static_cast<unsigned long long*>(grow(c, s.stat, sizeof(unsigned long long) * (size_t)(scols + l + 1)));
+  QLRA_CUDA(cudaMemsetAsync(st, 0, sizeof(unsigned long long) * (size_t)(scols + l + 1), c.stream));
+  om_colmax = st;
+  ps_rowmax = st + scols;
+  {
+    dim3 grid((unsigned)((scols + 31) / 32), (unsigned)std::min<int64_t>(64, (n + 7) / 8));
+    k_colmax<<<grid, 256, 0, c.stream>>>(om, om_colmax);
+    QLRA_LAUNCH_CHECK();
+    count_launch();
+  }
+  if (l > 0 && ps.cols > 0) {
+    k_rowmax<<<(unsigned)l, 256, 0, c.stream>>>(ps, ps_rowmax);
+    QLRA_LAUNCH_CHECK();
+    count_launch();
+  }
+  ores = static_cast<int8_t*>(grow(c, s.ores, (size_t)NB * spad * npad));
+  k_res_om<<<blocks_for(spad * (npad / 4), 256), 256, 0, c.stream>>>(om, om_colmax, npad, spad, ores, spad * npad);
+  QLRA_LAUNCH_CHECK();
+  count_launch();
+  cw = static_cast<int32_t*>(grow(c, s.cw, sizeof(int32_t) * (size_t)NB * npad * lpad));
+}
+
+// max |A| of a view on `stream`, into panel slot `slot` (device) and its
+// pinned host copy
+void OzRun::amax_async(const QView& a, cudaStream_t stream, int slot) {
+  OzState& s = *ctx.oz;
+  unsigned long long* d = s.amax_dev + slot;
+  QLRA_CUDA(cudaMemsetAsync(d, 0, sizeof(*d), stream));
+  const int64_t total = a.rows * a.cols;
+  if (total > 0) {
+    k_absmax<<<(unsigned)std::min<int64_t>(148 * 8, (total + 255) / 256), 256, 0, stream>>>(a, d);
+    QLRA_LAUNCH_CHECK();
+    count_launch();
+  }
+  QLRA_CUDA(cudaMemcpyAsync(s.amax_host + slot, d, sizeof(*d), cudaMemcpyDeviceToHost, stream));
+}
+double OzRun::amax_host(int slot) const {
+  const unsigned long long b = ctx.oz->amax_host[slot];
+  double d;
+  std::memcpy(&d, &b, sizeof(d));
+  return d;
+}
+
+void OzRun::flush(const QView& w) {
+  if (!epoch_open) return;
+  if (epoch_rows > 0 && w.rows > 0 && w.cols > 0) {
+    k_crt_w<<<blocks_for(w.rows * w.cols, 128), 128, 0, ctx.stream>>>(cw, npad * lpad, npad, w, ps_rowmax, sigma);
+    QLRA_LAUNCH_CHECK();
+    count_launch();
+  }
+  epoch_open = false;
+  epoch_rows = 0;
+}
+
+// One row panel: A rows [pc0, pc0 + R) of the block (Psi columns likewise),
+// Y rows of the panel, W of the block; amax = max |A| over the panel (or an
+// upper bound: the block's, when it was scanned up front).
+void OzRun::panel(int64_t pc0, const QView& ap, const QView& yr, const QView& w, double amax, int headroom) {
+  OzState& s = *ctx.oz;
+  const int64_t R = ap.rows;
+  if (R == 0 || amax == 0.0) return;  // an all-zero panel adds nothing
+  if (R > KMAX) fail(QLRA_ERR_PARAMETER, "ozaki: panel taller than the int32 accumulation bound");
+  const int64_t rpad = up16(R);
+  const int e = std::ilogb(amax);
+  if (epoch_open && (e + sigma > 51 || epoch_rows + rpad > KMAX)) flush(w);
+  if (!epoch_open) {
+    sigma = 51 - e - headroom;
+    epoch_open = true;
+    epoch_rows = 0;
+  }
+  auto* ares = static_cast<int8_t*>(grow(ctx, s.ares, (size_t)NB * rpad * npad));
+  k_res_a<<<blocks_for(rpad * (npad / 4), 128), 128, 0, ctx.stream>>>(ap, npad, rpad, sigma, ares, rpad * npad);
+  QLRA_LAUNCH_CHECK();
+  count_launch();
+  int8_t* pres = nullptr;
+  if (l > 0) {
+    pres = static_cast<int8_t*>(grow(ctx, s.pres, (size_t)NB * lpad * rpad));
+    k_res_psi<<<blocks_for(lpad * (rpad / 4), 128), 128, 0, ctx.stream>>>(psi, pc0, R, rpad, lpad, ps_rowmax, pres,
+                                                                            lpad * rpad);
+    QLRA_LAUNCH_CHECK();
+    count_launch();
+  }
+  int32_t* cy = scols > 0 ? static_cast<int32_t*>(grow(ctx, s.cy, sizeof(int32_t) * (size_t)NB * rpad * spad))
+                          : nullptr;
+  {
+    // the tensor-core work of the panel (bench evidence: event-timed)
+    LaunchTimer lt(ctx);
+    // Y panel: col-major C (s x Rpad, ldc spad) = Ores^T (s x npad) * Ares (npad x Rpad)
+    if (scols > 0) {
+      OzState::Plan& py = plan(s, true, spad, rpad, npad, npad, npad, spad, spad * npad, rpad * npad, rpad * spad, NB);
+      run_gemm(ctx, s, py, ores, ares, cy, 0);
+    }
+    // W^* (npad x l, ldc npad) += Ares (npad x Rpad) * Pres (Rpad x l)
+    if (l > 0) {
+      OzState::Plan& pw =
+          plan(s, false, npad, lpad, rpad, npad, rpad, npad, rpad * npad, lpad * rpad, npad * lpad, NB);
+      run_gemm(ctx, s, pw, ares, pres, cw, epoch_rows > 0 ? 1 : 0);
+    }
+    lt.close(32.0 * (double)R * (double)n * (double)(scols + l), 32.0 * (double)R * (double)n,
+             2.0 * NB * (double)rpad * (double)npad * (double)(scols + l), 2);
+  }
+  if (scols > 0) {
+    k_crt_y<<<blocks_for(R * scols, 128), 128, 0, ctx.stream>>>(cy, rpad * spad, spad, yr, om_colmax, sigma);
+    QLRA_LAUNCH_CHECK();
+    count_launch();
+  }
+  epoch_rows += rpad;
+}
+
+void OzRun::finish(const QView& w) { flush(w); }
+
+// Whole device-resident block: one scan for max |A| (a single epoch unless
+// the block is taller than the int32 bound), then panels sized for the
+// residue buffer.
+void oz_sketch_block(Ctx& c, const QView& om, const QView& ps, const QView& block, const QView& y_rows,
+                     const QView& w) {
+  OzRun run(c, om, ps);
+  run.amax_async(block, c.stream, 2);
+  QLRA_CUDA(cudaStreamSynchronize(c.stream));
+  const double amax = run.amax_host(2);
+  static const double budget = [] {
+    const char* e = std::getenv("QLRA_OZ_PANEL_BYTES");
+    return e ? std::atof(e) : 14e9;
+  }();
+  int64_t R = (int64_t)(budget / (NB * (double)run.npad));
+  R = std::max<int64_t>(256, std::min<int64_t>(R / 16 * 16, KMAX));
+  // equal panels (no short tail)
+  const int64_t np = (block.rows + R - 1) / R;
+  R = up16((block.rows + np - 1) / np);
+  for (int64_t r0 = 0; r0 < block.rows; r0 += R) {
+    const int64_t rp = std::min(R, block.rows - r0);
+    run.panel(r0, sub(block, r0, 0, rp, block.cols), sub(y_rows, r0, 0, rp, y_rows.cols), w, amax, 0);
+  }
+  run.finish(w);
+}
+
+const char* oz_kernel_name() {
+  return "int8 tensor-core sketch (Ozaki/CRT: 16 moduli x 8 combinations, cuBLASLt sm_100 IMMA batched GEMM "
+         "+ residue/CRT kernels)";
+}
+
+}  // namespace qlra_dev

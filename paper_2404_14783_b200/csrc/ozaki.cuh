@@ -1,0 +1,45 @@
+// ozaki.cuh -- the int8 tensor-core sketch engine (ozaki.cu).
+#pragma once
+
+#include "kernels.cuh"
+
+namespace qlra_dev {
+
+// true when sketch_update_rows should take the int8 engine for these shapes
+bool oz_wanted(const Ctx& c, int64_t n, int64_t s, int64_t l);
+int64_t oz_kmax();
+const char* oz_kernel_name();
+
+// One sketch call on the int8 engine: Omega's residues and the embeddings'
+// scales are prepared at construction; panel() adds a row panel's Y rows and
+// accumulates its W^* products (int32, exact) until flush() recovers W.
+struct OzRun {
+  Ctx& ctx;
+  QView omega, psi;  // Omega (n x s), the Psi block (l x b) of the call
+  int64_t n = 0, npad = 0, scols = 0, spad = 0, l = 0, lpad = 0;
+  unsigned long long* om_colmax = nullptr;  // device: max |Omega(:, j)| bits
+  unsigned long long* ps_rowmax = nullptr;  // device: max |Psi(k, :)| bits
+  int8_t* ores = nullptr;                   // Omega residues (128 x s x npad)
+  int32_t* cw = nullptr;                    // W^* products (128 x l x npad), int32
+  bool epoch_open = false;
+  int64_t epoch_rows = 0;
+  int sigma = 0;  // A' = rint(A 2^sigma) in the open epoch
+  OzRun(Ctx& c, const QView& om, const QView& ps);
+  OzRun(const OzRun&) = delete;
+  OzRun& operator=(const OzRun&) = delete;
+  // max |a| on `stream` into slot 0..2 (device) and its pinned host copy
+  void amax_async(const QView& a, cudaStream_t stream, int slot);
+  double amax_host(int slot) const;
+  // rows [pc0, pc0 + ap.rows) of the block: Y rows yr += ap Omega; W^*
+  // products accumulated; amax bounds max |ap|; headroom: spare bits of the
+  // epoch scale for later panels (streamed blocks)
+  void panel(int64_t pc0, const QView& ap, const QView& yr, const QView& w, double amax, int headroom);
+  void flush(const QView& w);
+  void finish(const QView& w);
+};
+
+// the whole sketch of a device-resident block
+void oz_sketch_block(Ctx& c, const QView& om, const QView& ps, const QView& block, const QView& y_rows,
+                     const QView& w);
+
+}  // namespace qlra_dev

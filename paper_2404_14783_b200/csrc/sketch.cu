@@ -28,6 +28,7 @@
 #include <cstdlib>
 #include <functional>
 #include <map>
+#include <memory>
 #include <mutex>
 #include <type_traits>
 #include <vector>
@@ -36,6 +37,7 @@
 
 #include "common.cuh"
 #include "kernels.cuh"
+#include "ozaki.cuh"
 #include "qtile.cuh"
 #include "qtile8.cuh"
 
@@ -473,33 +475,6 @@ bool sketch_tma_enabled() {
   return v;
 }
 
-// Event-timed launch bracket (bench evidence, ctx.ktimer).
-struct LaunchTimer {
-  Ctx& ctx;
-  cudaEvent_t e0 = nullptr, e1 = nullptr;
-  bool on;
-  explicit LaunchTimer(Ctx& c, bool timed = true) : ctx(c), on(timed && c.ktimer.on) {
-    if (!on) return;
-    if (!ctx.ktimer.pool.empty()) {
-      e0 = ctx.ktimer.pool.back().first;
-      e1 = ctx.ktimer.pool.back().second;
-      ctx.ktimer.pool.pop_back();
-    } else {
-      QLRA_CUDA(cudaEventCreate(&e0));
-      QLRA_CUDA(cudaEventCreate(&e1));
-    }
-    QLRA_CUDA(cudaEventRecord(e0, ctx.stream));
-  }
-  void done(int64_t rp, int64_t n, int64_t s, int64_t l) {
-    if (!on) return;
-    QLRA_CUDA(cudaEventRecord(e1, ctx.stream));
-    ctx.ktimer.ev.emplace_back(e0, e1);
-    ctx.ktimer.flops += 32.0 * (double)rp * (double)n * (double)(s + l);
-    ctx.ktimer.a_bytes += 32.0 * (double)rp * (double)n;
-    ++ctx.ktimer.launches;
-  }
-};
-
 template <class Args>
 void set_splits(Args& f, const Geom& G, int64_t rp, int64_t n, int64_t s, int64_t l, Ctx& ctx, SketchWork& ws) {
   f.y_tm = (int)((rp + G.ym - 1) / G.ym);
@@ -924,6 +899,17 @@ void sketch_update_rows(Ctx& ctx, const qlra_spec_t& omega, const qlra_spec_t& p
                         const QView& block, const QView& y_rows, const QView& w) {
   const int64_t b = block.rows, n = block.cols, s = omega.cols;
   if (b == 0 || n == 0) return;
+  if (oz_wanted(ctx, n, s, psi.rows)) {
+    // int8 tensor-core engine (ozaki.cu): no TMA alignment needed
+    DevQMat om(ctx, n, s), ps_tmp;
+    launch_gen(ctx.stream, omega, 0, 0, n, s, om.v, false);
+    Emb e;
+    e.om = om.v;
+    e.ps = psi_for_sketch(ctx, psi, row0, b, ps_tmp);
+    prepare_emb(ctx, e, psi, row0);  // keeps the combined Psi block for the core solve (psi8_gemm)
+    oz_sketch_block(ctx, e.om, e.ps, block, y_rows, w);
+    return;
+  }
   int64_t pstride = 0;
   if (sketch_use8() && sketch_tma_enabled() && !tma_layout(block, &pstride) && n >= 1024) {
     // A's rows are not 16-byte aligned (n odd, e.g. C4's 27125): stream the
@@ -1047,6 +1033,11 @@ void sketch_rows_pipeline(Ctx& ctx, const qlra_spec_t& omega, const qlra_spec_t&
   e.ps = psi_for_sketch(ctx, psi, row0, b, ps_tmp);
   prepare_emb(ctx, e, psi, row0);
   SketchWork ws;
+  // the int8 engine takes the chunks when it is selected for these shapes
+  // (max |A| of each chunk is taken on the copy stream right after its DMA,
+  // so the host reads it without waiting for the previous chunk's work)
+  std::unique_ptr<OzRun> oz;
+  if (oz_wanted(ctx, n, s, psi.rows)) oz.reset(new OzRun(ctx, e.om, e.ps));
   // The last R rows go in quarter-size chunks: the sketch of the final chunk
   // is the one part of the pipeline nothing overlaps (the copy stream is the
   // bottleneck before it), so it should be short.
@@ -1088,11 +1079,18 @@ void sketch_rows_pipeline(Ctx& ctx, const qlra_spec_t& omega, const qlra_spec_t&
                                     kind, pipe.cs));
       }
     }
+    if (oz) oz->amax_async(dst, pipe.cs, idx);
     QLRA_CUDA(cudaEventRecord(pipe.copied[idx], pipe.cs));
     QLRA_CUDA(cudaStreamWaitEvent(ctx.stream, pipe.copied[idx], 0));
-    sketch_panel(ctx, e, r0, dst, sub(y_rows, r0, 0, rp, s), w, ws);
+    if (oz) {
+      QLRA_CUDA(cudaEventSynchronize(pipe.copied[idx]));
+      oz->panel(r0, dst, sub(y_rows, r0, 0, rp, s), w, oz->amax_host(idx), 1);
+    } else {
+      sketch_panel(ctx, e, r0, dst, sub(y_rows, r0, 0, rp, s), w, ws);
+    }
     QLRA_CUDA(cudaEventRecord(pipe.freed[idx], ctx.stream));
   }
+  if (oz) oz->finish(w);
 }
 
 // Host rows of a (4-plane, ld) host matrix copied into pinned staging by

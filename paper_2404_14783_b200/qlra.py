@@ -140,7 +140,17 @@ class Context:
     def kernel_stats(self) -> dict:
         ms, n, fl, by = C.c_double(), C.c_int64(), C.c_double(), C.c_double()
         self._check(self.lib.qlra_ctx_kernel_stats(self.h, C.byref(ms), C.byref(n), C.byref(fl), C.byref(by)))
-        return dict(ms=ms.value, launches=n.value, flops=fl.value, a_bytes=by.value)
+        eng, ops = C.c_int(), C.c_double()
+        self._check(self.lib.qlra_ctx_kernel_engines(self.h, C.byref(eng), C.byref(ops)))
+        return dict(ms=ms.value, launches=n.value, flops=fl.value, a_bytes=by.value, engines=eng.value,
+                    int8_ops=ops.value)
+
+    SKETCH_ENGINES = {"auto": 0, "dmma": 1, "int8": 2}
+
+    def set_sketch_engine(self, engine: str):
+        """Sketch engine: "auto" (int8 tensor cores where faster), "dmma"
+        (FP64 tensor cores) or "int8" (exact integer products, Ozaki/CRT)."""
+        self._check(self.lib.qlra_ctx_set_sketch_engine(self.h, self.SKETCH_ENGINES[engine]))
 
     def _check(self, rc: int):
         if rc == 0:
