@@ -38,6 +38,8 @@ def parse():
     p.add_argument("--config", default=CFG_DEFAULT)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--rangefinder", default="pseudo_qr", choices=["pseudo_qr", "pseudo_svd"])
+    p.add_argument("--engine", default="auto", choices=["auto", "dmma", "int8"],
+                   help="sketch engine: int8 tensor cores (exact integer products) where faster, or force one")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-pageable", action="store_true", help="skip the pageable-host e2e variant")
@@ -277,6 +279,7 @@ def main():
         dist.broadcast_object_list(obj, src=0)
         nccl_id = obj[0]
     ctx = Q.Context(local, rank, world, nccl_id)
+    ctx.set_sketch_engine(args.engine)
     Q.set_default_context(ctx)
     r0, r1 = Q.shard_rows(cfg.m, world, rank)
     a = build_matrix(cfg, (r0, r1), ctx)
@@ -453,30 +456,68 @@ def main():
         a = a_host.to("cuda")
 
     peaks = {"dfma_tflops": Q.measure_fp64_peak(0, 300.0, ctx), "dmma_tflops": Q.measure_fp64_peak(1, 300.0, ctx)}
-    peak = max(peaks.values())
-    # achieved: the flops the sketch kernel's algorithm issues per launch
-    # (8-product quaternion engine: 8 real multiply-adds = 16 flop per
-    # quaternion MAC, on the DMMA pipe) / the launch's mean CUDA-event
-    # duration, measured on the launching stream in the timed region.  The
-    # reference's per-unit figure (32 flop per quaternion MAC) is
-    # reported next to it as the algorithmic rate.
-    flops_launch = kst["flops"] / max(1, kst["launches"])  # 32 flop / qMAC
+    int8_engine = bool(kst["engines"] & 2)
+    if int8_engine:
+        peaks["int8_tops"] = Q.measure_int8_peak(300.0, ctx)
+    flops_launch = kst["flops"] / max(1, kst["launches"])  # 32 flop / qMAC (the reference's count)
     alg_tflops = flops_launch / (k_ms * 1e-3) / 1e12
-    achieved = 0.5 * alg_tflops
     traffic = None
-    prof = os.path.join(ROOT, "profiles", f"sketch_traffic_{cfg.name}.json")
+    prof = os.path.join(ROOT, "profiles", f"sketch_traffic_{cfg.name}{'_int8' if int8_engine else ''}.json")
     if os.path.exists(prof) and world == 1:
         pt = json.load(open(prof))
         if pt.get("config") == cfg.name and pt.get("flops_per_launch"):
             # the captured launch's DRAM bytes, scaled to this run's mean
             # launch by algorithmic flops (C4's last panel is shorter)
             traffic = pt["dram_bytes_per_launch"] * flops_launch / pt["flops_per_launch"]
+    if int8_engine:
+        # the int8 engine (csrc/ozaki.cu): the dominant kernels are the two
+        # batched int8 GEMMs of a panel (8 combinations x 16 moduli of the
+        # residues); achieved = their int8 ops / the bracket's mean CUDA-event
+        # duration, peak = int8 8192^3 GEMMs measured in this run
+        ops_launch = kst["int8_ops"] / max(1, kst["launches"])
+        achieved = ops_launch / (k_ms * 1e-3) / 1e12
+        peak = peaks["int8_tops"]
+        roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TOPS (int8)",
+                "frac": achieved / peak, "frac_of_nominal_4500": achieved / 4500.0, "traffic": traffic,
+                "kernel_ms_per_launch": k_ms, "launches": kst["launches"],
+                "per_launch": {"int8_ops": ops_launch, "algorithmic_flops": flops_launch,
+                               "a_bytes": kst["a_bytes"] / max(1, kst["launches"])},
+                "algorithmic_tflops": alg_tflops,
+                "peak_source": "int8 tensor peak measured in this run (cuBLASLt int8 8192^3 GEMMs back to back; "
+                               "MEASURED_PEAKS.json has no int8 entry; nominal dense 4.5 POPS): " + json.dumps(peaks),
+                "note": ("int8 engine: every real product of the sketch computed exactly in integers (Ozaki "
+                         "scheme, CRT over 16 moduli) as 128 int8 GEMMs per panel (8 quaternion-product "
+                         "combinations x 16 moduli), one batched call per sketch side; a launch = one row panel: "
+                         "2 * 128 * rpad * npad * (spad + lpad) int8 ops; algorithmic_tflops counts the "
+                         "reference's 32 flop per quaternion MAC over the same bracket")}
+    else:
+        # the DMMA engine: the flops the sketch kernel's algorithm issues per
+        # launch (8-product quaternion engine: 8 real multiply-adds = 16 flop
+        # per quaternion MAC, on the DMMA pipe) / the launch's mean CUDA-event
+        # duration, measured on the launching stream in the timed region
+        peak = max(peaks["dfma_tflops"], peaks["dmma_tflops"])
+        achieved = 0.5 * alg_tflops
+        roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                "frac": achieved / peak, "traffic": traffic,
+                "kernel_ms_per_launch": k_ms, "launches": kst["launches"],
+                "per_launch": {"executed_flops": 0.5 * flops_launch, "algorithmic_flops": flops_launch,
+                               "a_bytes": kst["a_bytes"] / max(1, kst["launches"])},
+                "algorithmic_tflops": alg_tflops,
+                "peak_source": "FP64 DMMA/DFMA peaks measured in this run (m8n8k4 / DFMA "
+                               "microbenchmarks; MEASURED_PEAKS.json has no FP64 entry): " + json.dumps(peaks),
+                "note": ("achieved = executed FP64 TFLOP/s of the fused sketch kernel on the DMMA "
+                         "pipe: its 8-product quaternion algorithm issues 16 flop per quaternion MAC "
+                         "(8 real multiply-adds; the plane sums are extra DADDs on the same pipe), "
+                         "so frac is the pipe fraction; algorithmic_tflops counts the reference's "
+                         "32 flop per quaternion MAC (SURVEY 8(d)).  A launch covers one row panel "
+                         "of A (<= 2 GB): rows*n*(s+l) quaternion MACs.  traffic: DRAM bytes per "
+                         "launch from the committed ncu capture of this config "
+                         "(profiles/sketch_traffic_<config>.json), else null")}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(cfg, 0 if method == Q.PSEUDO_QR else 1, st.y, st.w, a)
 
-    eight = Q.sketch_kernel_name().startswith("sketch8")
     if rank == 0:
         line = {
             "metric": METRIC, "value": ms / 1e3, "unit": "s", "n_gpus": world, "steps": args.steps,
@@ -487,23 +528,9 @@ def main():
                        "parallelism": f"row-shard x{world}",
                        "l2": "A (%.2f GB) larger than the 126 MB L2; no flush needed" % (cfg.a_bytes() / 1e9)},
             "sketch_ms": sk_ms, "sketch_tflops": 32.0 * (r1 - r0) * cfg.n * (cfg.s + cfg.l) / (sk_ms * 1e-3) / 1e12,
-            "sketch_kernel": Q.sketch_kernel_name(),
-            "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                         "frac": achieved / peak, "traffic": traffic,
-                         "kernel_ms_per_launch": k_ms, "launches": kst["launches"],
-                         "per_launch": {"executed_flops": 0.5 * flops_launch, "algorithmic_flops": flops_launch,
-                                        "a_bytes": kst["a_bytes"] / max(1, kst["launches"])},
-                         "algorithmic_tflops": alg_tflops,
-                         "peak_source": "FP64 DMMA/DFMA peaks measured in this run (m8n8k4 / DFMA "
-                                        "microbenchmarks; MEASURED_PEAKS.json has no FP64 entry): " + json.dumps(peaks),
-                         "note": ("achieved = executed FP64 TFLOP/s of the fused sketch kernel on the DMMA "
-                                  "pipe: its 8-product quaternion algorithm issues 16 flop per quaternion MAC "
-                                  "(8 real multiply-adds; the plane sums are extra DADDs on the same pipe), "
-                                  "so frac is the pipe fraction; algorithmic_tflops counts the reference's "
-                                  "32 flop per quaternion MAC (SURVEY 8(d)).  A launch covers one row panel "
-                                  "of A (<= 2 GB): rows*n*(s+l) quaternion MACs.  traffic: DRAM bytes per "
-                                  "launch from the committed ncu capture of this config "
-                                  "(profiles/sketch_traffic_<config>.json), else null")},
+            "sketch_kernel": Q.int8_engine_name() if int8_engine else Q.sketch_kernel_name(),
+            "sketch_engine": "int8" if int8_engine else "dmma",
+            "roofline": roof,
             "rangefinder_used": used["rangefinder"], "rel_error": res / an, "e2e": e2e, "e2e_pageable": e2e_pageable, "gpu_launches": int(launches), "clocks": clk.summary(),
             "cpu_baseline": cpu,
         }

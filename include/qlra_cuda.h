@@ -151,6 +151,10 @@ int qlra_ctx_kernel_engines(qlra_ctx_t* ctx, int* engines, double* int8_ops);
 #define QLRA_SKETCH_DMMA 1
 #define QLRA_SKETCH_INT8 2
 int qlra_ctx_set_sketch_engine(qlra_ctx_t* ctx, int engine);
+/* The int8 engine's roofline denominator: TOPS of back-to-back int8 8192^3
+ * GEMMs on this GPU for ~ms milliseconds, and the engine's description. */
+int qlra_measure_int8_peak(qlra_ctx_t* ctx, double ms, double* tops);
+const char* qlra_int8_engine_name(void);
 
 /* ---------------------------------------------------------- embeddings --- */
 /* gen_block (sketching.cpp:53-71) / gen_test_matrix{,_rows,_cols}

@@ -67,6 +67,8 @@ def lib():
         "qlra_ctx_kernel_stats": ([VP, P(F64), P(I64), P(F64), P(F64)], INT),
         "qlra_ctx_kernel_engines": ([VP, P(INT), P(F64)], INT),
         "qlra_ctx_set_sketch_engine": ([VP, INT], INT),
+        "qlra_measure_int8_peak": ([VP, F64, P(F64)], INT),
+        "qlra_int8_engine_name": ([], C.c_char_p),
         "qlra_gen_test_matrix_block": ([VP, PS, I64, I64, PQ], INT),
         "qlra_sketch_update_rows": ([VP, PS, PS, I64, PQ, PQ, PQ], INT),
         "qlra_sketch_update_rows_host": ([VP, PS, PS, I64, PQ, PQ, PQ, I64], INT),

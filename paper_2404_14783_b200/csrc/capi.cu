@@ -22,6 +22,7 @@
 
 #include "common.cuh"
 #include "kernels.cuh"
+#include "ozaki.cuh"
 
 struct qlra_ctx {
   qlra_dev::Ctx c;
@@ -1469,6 +1470,12 @@ int qlra_ctx_kernel_engines(qlra_ctx_t* ctx, int* engines, double* int8_ops) {
     if (int8_ops) *int8_ops = c.ktimer.int8_ops;
   });
 }
+
+int qlra_measure_int8_peak(qlra_ctx_t* ctx, double ms, double* tops) {
+  return guarded(ctx, [&](Ctx& c) { *tops = oz_measure_int8_peak(c, ms); });
+}
+
+const char* qlra_int8_engine_name(void) { return oz_kernel_name(); }
 
 int qlra_ctx_set_sketch_engine(qlra_ctx_t* ctx, int engine) {
   return guarded(ctx, [&](Ctx& c) {

@@ -395,6 +395,75 @@ __global__ void k_crt_w(const int32_t* cw, int64_t bs, int64_t npad, QView w, co
   for (int p = 1; p < 4; ++p) w.p[p][k * w.ld + j] -= ldexp(i128_to_double(z[p]), sh);
 }
 
+
+// Rows of a K-major operand (rows x K) -> residues [t*16+mu][r][kpad] of
+// lcomb_t (LEFT) or rcomb_t of rint(x 2^e_r), x = src or conj(src), with a
+// per-row scale from rowmax (the general product's left rows / right
+// columns).  Rows past src.rows and k past src.cols are zero.
+template <bool LEFT>
+__global__ void k_res_rows(QView src, int conj, const unsigned long long* rowmax, int64_t k0, int64_t kc,
+                           int64_t kpad, int64_t rpad, int8_t* out, int64_t bstride) {
+  const int64_t nw = kpad >> 2;
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= rpad * nw) return;
+  const int64_t r = e / nw, kk = (e - r * nw) * 4;
+  const int ex = r < src.rows ? scale_exp(rowmax[r]) : 0;
+  const double s1 = ldexp(1.0, ex / 2), s2 = ldexp(1.0, ex - ex / 2);
+  double c[8][4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    double v[4] = {0.0, 0.0, 0.0, 0.0};
+    if (r < src.rows && kk + q < kc) {
+#pragma unroll
+      for (int p = 0; p < 4; ++p) {
+        const double x = rint(src.p[p][r * src.ld + k0 + kk + q] * s1 * s2);
+        v[p] = conj && p > 0 ? -x : x;
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < 8; ++t) c[t][q] = LEFT ? qt8::lcomb(t, v) : qt8::rcomb(t, v);
+  }
+  store_res(reinterpret_cast<unsigned*>(out + r * kpad + kk), bstride >> 2, c);
+}
+
+// dst (cols x rows, 4 planes, ld rows) = src^T (32 x 32 smem tiles)
+__global__ void k_transpose(QView src, QView dst) {
+  __shared__ double tile[32][33];
+  const int64_t r0 = (int64_t)blockIdx.y * 32, c0 = (int64_t)blockIdx.x * 32;
+  for (int p = 0; p < 4; ++p) {
+    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+      const int64_t r = r0 + i, c = c0 + threadIdx.x;
+      tile[i][threadIdx.x] = r < src.rows && c < src.cols ? src.p[p][r * src.ld + c] : 0.0;
+    }
+    __syncthreads();
+    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+      const int64_t c = c0 + i, r = r0 + threadIdx.x;
+      if (c < src.cols && r < src.rows) dst.p[p][c * dst.ld + r] = tile[threadIdx.x][i];
+    }
+    __syncthreads();
+  }
+}
+
+// C = alpha * (recovered product) + beta * C; ci[t*16+mu][i][j] (ld npad)
+__global__ void k_crt_gen(const int32_t* ci, int64_t bs, int64_t npad, QView c, const unsigned long long* lmax,
+                          const unsigned long long* rmax, double alpha, double beta) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= c.rows * c.cols) return;
+  const int64_t i = e / c.cols, j = e - i * c.cols;
+  i128 x[8];
+#pragma unroll 1
+  for (int t = 0; t < 8; ++t) x[t] = crt16(ci + (int64_t)t * NMOD * bs + i * npad + j, bs);
+  i128 z[4];
+  combine2(x, z);
+  const int sh = -(scale_exp(lmax[i]) + scale_exp(rmax[j])) - 1;
+#pragma unroll
+  for (int p = 0; p < 4; ++p) {
+    double* d = c.p[p] + i * c.ld + j;
+    const double v = alpha * ldexp(i128_to_double(z[p]), sh);
+    *d = beta == 0.0 ? v : fma(beta, *d, v);
+  }
+}
+
 inline unsigned blocks_for(int64_t n, int threads) { return (unsigned)((n + threads - 1) / threads); }
 inline int64_t up16(int64_t x) { return (x + 15) / 16 * 16; }
 
@@ -492,10 +561,13 @@ OzState::Plan& plan(OzState& s, bool ta, int64_t m, int64_t n, int64_t k, int64_
   return s.plans.emplace(key, p).first->second;
 }
 
-void run_gemm(Ctx& c, OzState& s, OzState::Plan& p, const void* A, const void* B, void* C, int beta) {
+void run_gemm(Ctx& c, OzState& s, OzState::Plan& p, const void* A, const void* B, void* C, int beta,
+              void* ws = nullptr) {
+  // ws: a caller-owned workspace of lt_ws_bytes (products issued on a side
+  // stream must not share the context's)
   const int32_t alpha = 1;
-  lt_check(cublasLtMatmul(s.lt, p.d, &alpha, A, p.la, B, p.lb, &beta, C, p.lc, C, p.lc, &p.algo, s.lt_ws,
-                          s.lt_ws_bytes, c.stream),
+  lt_check(cublasLtMatmul(s.lt, p.d, &alpha, A, p.la, B, p.lb, &beta, C, p.lc, C, p.lc, &p.algo,
+                          ws ? ws : s.lt_ws, s.lt_ws_bytes, c.stream),
            "matmul");
   count_launch();
 }
@@ -668,10 +740,16 @@ void oz_sketch_block(Ctx& c, const QView& om, const QView& ps, const QView& bloc
   run.amax_async(block, c.stream, 2);
   QLRA_CUDA(cudaStreamSynchronize(c.stream));
   const double amax = run.amax_host(2);
-  static const double budget = [] {
+  // residue panel: as tall as memory allows (each panel re-reads and
+  // re-writes W^*'s int32 products, 128 x l x n x 8 bytes, inside its GEMM),
+  // capped by QLRA_OZ_PANEL_BYTES (default 28 GB) and 45% of the free memory
+  static const double cap = [] {
     const char* e = std::getenv("QLRA_OZ_PANEL_BYTES");
-    return e ? std::atof(e) : 14e9;
+    return e ? std::atof(e) : 28e9;
   }();
+  size_t free_b = 0, total_b = 0;
+  QLRA_CUDA(cudaMemGetInfo(&free_b, &total_b));
+  const double budget = std::max(1e9, std::min(cap, 0.45 * (double)free_b));
   int64_t R = (int64_t)(budget / (NB * (double)run.npad));
   R = std::max<int64_t>(256, std::min<int64_t>(R / 16 * 16, KMAX));
   // equal panels (no short tail)
@@ -682,6 +760,115 @@ void oz_sketch_block(Ctx& c, const QView& om, const QView& ps, const QView& bloc
     run.panel(r0, sub(block, r0, 0, rp, block.cols), sub(y_rows, r0, 0, rp, y_rows.cols), w, amax, 0);
   }
   run.finish(w);
+}
+
+
+// ---------------------------------------------------------------------------
+// General quaternion product on the int8 engine, for the large-K products of
+// the QB stage (Psi H, Psi Q0 -- sketching.cpp:184 -- and the Grams H^* H of
+// the rangefinders, rangefinders.cpp:68,102): C = alpha op(A) op(B) + beta C,
+// exact integer products of per-row (left) / per-column (right) 52-bit
+// images, K in chunks of < 2^17 (int32), each chunk recovered and added.
+// Every buffer is allocated on the calling stream (the early core solve
+// issues its products on a second stream).
+bool oz_gemm_try(Ctx& c, int op_a, int op_b, double alpha, const QView& A, const QView& B, double beta,
+                 const QView& C) {
+  const int64_t M = C.rows, N = C.cols, K = op_a ? A.rows : A.cols;
+  if (M == 0 || N == 0 || K == 0) return false;
+  int engine = c.sketch_engine;
+  if (engine == QLRA_SKETCH_AUTO) {
+    const char* e = std::getenv("QLRA_SKETCH_ENGINE");
+    if (e && std::string(e) == "dmma") engine = QLRA_SKETCH_DMMA;
+  }
+  if (engine == QLRA_SKETCH_DMMA) return false;
+  // worth it when the contraction is long and the output not tiny: the
+  // residues cost ~(M + N) K, the recovery ~M N (128 int32 reads + the CRT
+  // per element), the DMMA product 16 M N K flop
+  if (K < 4096 || M < 64 || N < 64 || (double)M * (double)N * (double)K < 1.5e9) return false;
+  OzState& s = state(c);
+  const bool same = A.p[0] == B.p[0] && A.rows == B.rows && A.cols == B.cols && op_a == QLRA_OP_C && op_b == QLRA_OP_N;
+  // K-major rows: L (M x K) = op(A), R (N x K) = op(B)^T
+  DevQMat lt, rt;
+  auto transpose = [&](const QView& x, DevQMat& out) {
+    out = DevQMat(c, x.cols, x.rows);
+    k_transpose<<<dim3((unsigned)((x.cols + 31) / 32), (unsigned)((x.rows + 31) / 32)), dim3(32, 8), 0, c.stream>>>(
+        x, out.v);
+    QLRA_LAUNCH_CHECK();
+    count_launch();
+    return out.v;
+  };
+  const QView L = op_a == QLRA_OP_N ? A : transpose(A, lt);
+  const int lconj = op_a == QLRA_OP_N ? 0 : 1;
+  const QView R = op_b == QLRA_OP_C ? B : (same ? L : transpose(B, rt));
+  const int rconj = op_b == QLRA_OP_C ? 1 : 0;
+  const int64_t mpad = up16(M), npad = up16(N);
+  DeviceBuffer mx(c, sizeof(unsigned long long) * (size_t)(M + N));
+  auto* lmax = mx.as<unsigned long long>();
+  auto* rmax = lmax + M;
+  k_rowmax<<<(unsigned)M, 256, 0, c.stream>>>(L, lmax);
+  QLRA_LAUNCH_CHECK();
+  count_launch();
+  if (same) {
+    QLRA_CUDA(cudaMemcpyAsync(rmax, lmax, sizeof(unsigned long long) * (size_t)M, cudaMemcpyDeviceToDevice, c.stream));
+  } else {
+    k_rowmax<<<(unsigned)N, 256, 0, c.stream>>>(R, rmax);
+    QLRA_LAUNCH_CHECK();
+    count_launch();
+  }
+  const int64_t nch = (K + KMAX - 1) / KMAX, kc = (K + nch - 1) / nch, kpad = up16(kc);
+  DeviceBuffer lres(c, (size_t)NB * mpad * kpad), rres(c, (size_t)NB * npad * kpad);
+  DeviceBuffer ci(c, sizeof(int32_t) * (size_t)NB * mpad * npad), ws(c, s.lt_ws_bytes);
+  // col-major C (npad x mpad) = Rres^T (npad x kpad) * Lres (kpad x mpad)
+  OzState::Plan& pl = plan(s, true, npad, mpad, kpad, kpad, kpad, npad, npad * kpad, mpad * kpad, mpad * npad, NB);
+  for (int64_t ch = 0; ch < nch; ++ch) {
+    const int64_t k0 = ch * kc, kn = std::min(kc, K - k0);
+    k_res_rows<true><<<blocks_for(mpad * (kpad / 4), 128), 128, 0, c.stream>>>(L, lconj, lmax, k0, kn, kpad, mpad,
+                                                                               lres.as<int8_t>(), mpad * kpad);
+    QLRA_LAUNCH_CHECK();
+    k_res_rows<false><<<blocks_for(npad * (kpad / 4), 128), 128, 0, c.stream>>>(R, rconj, rmax, k0, kn, kpad, npad,
+                                                                                rres.as<int8_t>(), npad * kpad);
+    QLRA_LAUNCH_CHECK();
+    count_launch();
+    count_launch();
+    run_gemm(c, s, pl, rres.ptr, lres.ptr, ci.ptr, 0, ws.ptr);
+    k_crt_gen<<<blocks_for(M * N, 128), 128, 0, c.stream>>>(ci.as<int32_t>(), mpad * npad, npad, C, lmax, rmax,
+                                                             alpha, ch == 0 ? beta : 1.0);
+    QLRA_LAUNCH_CHECK();
+    count_launch();
+  }
+  return true;
+}
+
+// INT8 tensor-core peak of this GPU as the engine sees it: back-to-back
+// cuBLASLt int8 GEMMs of 8192^3 (the roofline denominator of the int8
+// engine's GEMMs, measured in the same run as them).
+double oz_measure_int8_peak(Ctx& c, double ms) {
+  OzState& s = state(c);
+  const int64_t N = 8192;
+  DeviceBuffer a(c, (size_t)N * N), b(c, (size_t)N * N), d(c, sizeof(int32_t) * (size_t)N * N);
+  QLRA_CUDA(cudaMemsetAsync(a.ptr, 1, (size_t)N * N, c.stream));
+  QLRA_CUDA(cudaMemsetAsync(b.ptr, 1, (size_t)N * N, c.stream));
+  OzState::Plan& p = plan(s, true, N, N, N, N, N, N, N * N, N * N, N * N, 1);
+  for (int i = 0; i < 3; ++i) run_gemm(c, s, p, a.ptr, b.ptr, d.ptr, 0);
+  cudaEvent_t e0, e1;
+  QLRA_CUDA(cudaEventCreate(&e0));
+  QLRA_CUDA(cudaEventCreate(&e1));
+  QLRA_CUDA(cudaEventRecord(e0, c.stream));
+  run_gemm(c, s, p, a.ptr, b.ptr, d.ptr, 0);
+  QLRA_CUDA(cudaEventRecord(e1, c.stream));
+  QLRA_CUDA(cudaEventSynchronize(e1));
+  float one = 0.f;
+  QLRA_CUDA(cudaEventElapsedTime(&one, e0, e1));
+  const int reps = std::max(1, (int)(ms / std::max(0.01f, one)));
+  QLRA_CUDA(cudaEventRecord(e0, c.stream));
+  for (int i = 0; i < reps; ++i) run_gemm(c, s, p, a.ptr, b.ptr, d.ptr, 0);
+  QLRA_CUDA(cudaEventRecord(e1, c.stream));
+  QLRA_CUDA(cudaEventSynchronize(e1));
+  float t = 0.f;
+  QLRA_CUDA(cudaEventElapsedTime(&t, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  return 2.0 * N * N * (double)N * reps / (t * 1e-3) / 1e12;
 }
 
 const char* oz_kernel_name() {

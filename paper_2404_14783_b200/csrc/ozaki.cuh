@@ -9,6 +9,12 @@ namespace qlra_dev {
 bool oz_wanted(const Ctx& c, int64_t n, int64_t s, int64_t l);
 int64_t oz_kmax();
 const char* oz_kernel_name();
+// C = alpha op(A) op(B) + beta C on the int8 engine when the contraction is
+// long enough to pay (false: not taken, nothing launched)
+bool oz_gemm_try(Ctx& c, int op_a, int op_b, double alpha, const QView& A, const QView& B, double beta,
+                 const QView& C);
+// int8 TOPS of back-to-back cuBLASLt 8192^3 int8 GEMMs for ~ms milliseconds
+double oz_measure_int8_peak(Ctx& c, double ms);
 
 // One sketch call on the int8 engine: Omega's residues and the embeddings'
 // scales are prepared at construction; panel() adds a row panel's Y rows and

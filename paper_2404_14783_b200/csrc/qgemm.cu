@@ -16,6 +16,7 @@
 #include <vector>
 #include "common.cuh"
 #include "kernels.cuh"
+#include "ozaki.cuh"
 #include "qtile.cuh"
 
 namespace qlra_dev {
@@ -510,6 +511,7 @@ void qgemm(Ctx& ctx, int op_a, int op_b, double alpha, const QView& A, const QVi
 // tiles on or above the diagonal are computed and the rest is mirrored
 // (about half the tensor work of a Gram; exactly Hermitian result).
 void qgemm_gram(Ctx& ctx, const QView& A, const QView& C) {
+  if (oz_gemm_try(ctx, QLRA_OP_C, QLRA_OP_N, 1.0, A, A, 0.0, C)) return;  // long K: exact int8 products
   if (q8gram(ctx, A, C)) return;  // tall A: 8 real products per MAC (qtile8.cuh mode 4)
   qgemm_ex(ctx, QLRA_OP_C, QLRA_OP_N, 1.0, A, A, 0.0, C, 0, true);
 }
@@ -527,6 +529,8 @@ void qgemm_ex(Ctx& ctx, int op_a, int op_b, double alpha, const QView& A, const 
   GemmArgs g = make_args(op_a, op_b, alpha, A, B, beta, M, N, K);
   if (C.rows != M || C.cols != N) fail(QLRA_ERR_SHAPE, "qmat_mul: output shape mismatch");
   if (M == 0 || N == 0) return;
+  // long contractions (K >= 4096, large output): exact int8 products
+  if (!herm && force_splits == 0 && oz_gemm_try(ctx, op_a, op_b, alpha, A, B, beta, C)) return;
   for (int p = 0; p < 4; ++p) g.c[p] = C.p[p];
   g.ldc = C.ld;
   const int64_t tm = (M + BM - 1) / BM, tn = (N + BN - 1) / BN;

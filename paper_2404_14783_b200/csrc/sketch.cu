@@ -803,6 +803,15 @@ QView psi_for_solve(Ctx& ctx, const qlra_spec_t& psi, int64_t row0, int64_t rows
 }
 
 bool psi8_gemm(Ctx& ctx, const qlra_spec_t& psi, int64_t row0, const QView& B, const QView& C) {
+  {
+    // long contraction (Psi H over all local rows): the int8 engine on the
+    // kept fp64 Psi block
+    const Ctx::PsiKeep& pk = ctx.psi_keep;
+    if (pk.valid && same_spec(pk.spec, psi) && pk.row0 == row0 && pk.rows == B.rows && C.rows == psi.rows &&
+        C.cols == B.cols &&
+        oz_gemm_try(ctx, QLRA_OP_N, QLRA_OP_N, 1.0, view_of_buf(pk.buf, psi.rows, B.rows), B, 0.0, C))
+      return true;
+  }
   const Ctx::CombKeep& k = ctx.comb_keep;
   if (!k.psi_valid || !same_spec(k.psi, psi) || k.row0 != row0 || k.rows != B.rows || C.rows != psi.rows ||
       C.cols != B.cols || B.rows == 0 || B.cols == 0)

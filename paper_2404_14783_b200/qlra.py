@@ -949,3 +949,16 @@ def measure_fp64_peak(mode=0, ms=200.0, ctx=None):
 
 def sketch_kernel_name():
     return L.lib().qlra_sketch_kernel_name().decode()
+
+
+def int8_engine_name():
+    return L.lib().qlra_int8_engine_name().decode()
+
+
+def measure_int8_peak(ms=300.0, ctx=None):
+    """TOPS of back-to-back int8 8192^3 GEMMs (the int8 engine's roofline
+    denominator, measured in the same run)."""
+    ctx = _ctx(ctx)
+    t = C.c_double()
+    ctx._check(ctx.lib.qlra_measure_int8_peak(ctx.h, ms, C.byref(t)))
+    return t.value

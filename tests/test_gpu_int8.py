@@ -148,3 +148,46 @@ def test_engine_selection_errors(ctx):
     from paper_2404_14783_b200 import qlra as Q
     with pytest.raises(Q.ParameterError):
         ctx.lib and ctx._check(ctx.lib.qlra_ctx_set_sketch_engine(ctx.h, 7))
+
+
+@pytest.mark.parametrize("op_a,op_b", [(0, 0), (1, 0), (0, 1), (1, 1)])
+def test_int8_general_product_vs_oracle(ctx, op_a, op_b):
+    """Long-K quaternion products (K >= 4096, M N K >= 1.5e9) take the int8
+    engine inside qmat_mul: every op pair, alpha / beta, bitwise repeatable,
+    and equal to the DMMA path to ~1e-15."""
+    from paper_2404_14783_b200 import qlra as Q
+    m, k, n = 600, 5000, 640
+    a = random_gaussian(k, m, 41) if op_a else random_gaussian(m, k, 41)
+    b = random_gaussian(n, k, 42) if op_b else random_gaussian(k, n, 42)
+    c0 = random_gaussian(m, n, 43)
+    ref = 0.5 * O.qmat_mul(O.adjoint(a) if op_a else a, O.adjoint(b) if op_b else b) - 2.0 * c0
+    outs = []
+    for _ in range(2):
+        out = dev(c0)
+        with engine(ctx, "int8"):
+            n0 = ctx.launch_count()
+            Q.qmat_mul(dev(a), dev(b), op_a=op_a, op_b=op_b, alpha=0.5, beta=-2.0, out=out, ctx=ctx)
+            assert ctx.launch_count() > n0
+        outs.append(out)
+    assert torch.equal(outs[0], outs[1])
+    assert rel_diff(host(outs[0]), ref) < 1e-14
+    out_d = dev(c0)
+    with engine(ctx, "dmma"):
+        Q.qmat_mul(dev(a), dev(b), op_a=op_a, op_b=op_b, alpha=0.5, beta=-2.0, out=out_d, ctx=ctx)
+    assert rel_diff(host(outs[0]), host(out_d)) < 1e-14
+
+
+@pytest.mark.parametrize("m,s", [(20000, 300), (140000, 128)])
+def test_int8_gram_exactly_hermitian_vs_oracle(ctx, m, s):
+    """Grams H^* H of the rangefinders (rangefinders.cpp:68,102) on the int8
+    engine: exact integer products give an exactly Hermitian result (real
+    diagonal); K past one int32 accumulation (140000 rows) is chunked."""
+    from paper_2404_14783_b200 import qlra as Q
+    y = random_gaussian(m, s, 44 + m)
+    with engine(ctx, "int8"):
+        g = host(Q.gram(dev(y), ctx=ctx))
+    ref = O.qmat_mul(O.adjoint(y), y)
+    assert rel_diff(g, ref) < 1e-14
+    gh = O.adjoint(g)
+    assert np.array_equal(g, gh)
+    assert np.all(g[1:][:, np.arange(s), np.arange(s)] == 0.0)
