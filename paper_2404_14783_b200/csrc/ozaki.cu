@@ -18,8 +18,8 @@
 //    p <= 256 (symmetric int8); the 8 x 16 = 128 residue products are ONE
 //    strided-batched int8 x int8 -> int32 GEMM (exact while K 128^2 < 2^31,
 //    i.e. K < 2^17 rows or columns per int32 accumulation);
-//  * recovery: the CRT in 128-bit integers (P = prod p = 2^126.2 > 2 K
-//    2^106), the 8 products combined into the quaternion planes exactly in
+//  * recovery: the CRT in 128-bit integers (P = prod p = 2^124.7 > 2 K
+//    2^106 for 16 moduli; 15 moduli and 49-bit scales when K <= 2^15), the 8 products combined into the quaternion planes exactly in
 //    int128, one rounding to double, scaled back by powers of two.
 //
 // One residue set serves both sketches: Y = A Omega takes lcomb(A) as its
@@ -51,19 +51,27 @@ namespace qlra_dev {
 
 namespace {
 
-constexpr int NMOD = 16;
-constexpr int NB = 8 * NMOD;            // batch: (combination t, modulus mu), b = t * NMOD + mu
+constexpr int NMOD = 16;                // moduli available; a call uses the first nmod (15 or 16)
+constexpr int NB = 8 * NMOD;            // batch: (combination t, modulus mu), b = t * nmod + mu
 constexpr int64_t KMAX = 131056;        // K per int32 accumulation: K * 128^2 < 2^31 (multiple of 16)
+constexpr int NTAB = 2;                 // CRT tables: [0] the 16 moduli, [1] the first 15
 // odd moduli <= 253: a residue off the symmetric range by one (below) still
-// fits int8; 256 wraps in int8 congruently.  P = 2^125.7 > 2 * 2^17 * 2^106.
+// fits int8; 256 wraps in int8 congruently.  P = 2^124.7 > 2 * 2^17 * 2^106.
 constexpr int kModuli[NMOD] = {256, 253, 251, 247, 241, 239, 233, 229, 227, 223, 211, 199, 197, 193, 191, 181};
 
 __constant__ int c_p[NMOD];
 __constant__ double c_pinv[NMOD];
 __constant__ float c_pinvf[NMOD];
-__constant__ int c_yinv[NMOD];                   // (P / p)^-1 mod p
-__constant__ unsigned long long c_M[NMOD][2];    // P / p as (lo, hi)
-__constant__ unsigned long long c_P[2], c_H[2];  // P, floor(P / 2)
+__constant__ int c_yinv[NTAB][NMOD];                   // (P / p)^-1 mod p
+__constant__ unsigned long long c_M[NTAB][NMOD][2];    // P / p as (lo, hi)
+__constant__ unsigned long long c_P[NTAB][2], c_H[NTAB][2];  // P, floor(P / 2)
+
+// Moduli in use: the first nmod, CRT table tab, operands scaled to < 2^beta
+// per plane (combinations < 2^(beta+1)): P > 2 K 2^(2 beta + 2) bounds the
+// products of an int32 accumulation of K terms.
+struct ModCfg {
+  int nmod, tab, beta;
+};
 
 // lcomb(conj a)_t = kConjSign[t] * lcomb(a)_{kConjPerm[t]}: conj(a) = (a0,
 // -a1, -a2, -a3) in qtile8's lcomb list (a0+a1, a3-a2, a0-a1, a2+a3, a1+a3,
@@ -81,10 +89,10 @@ struct ModTables {
   double log2P = 0.0;
 };
 
-ModTables make_tables() {
+ModTables make_tables(int nmod) {
   ModTables t{};
   u128 P = 1;
-  for (int i = 0; i < NMOD; ++i) {
+  for (int i = 0; i < nmod; ++i) {
     for (int j = 0; j < i; ++j) {
       int a = kModuli[i], b = kModuli[j];
       while (b) { const int r = a % b; a = b; b = r; }
@@ -93,7 +101,7 @@ ModTables make_tables() {
     P *= (u128)kModuli[i];
     t.log2P += std::log2((double)kModuli[i]);
   }
-  for (int i = 0; i < NMOD; ++i) {
+  for (int i = 0; i < nmod; ++i) {
     const int p = kModuli[i];
     const u128 M = P / (u128)p;
     const int mr = (int)(M % (u128)p);
@@ -116,9 +124,9 @@ ModTables make_tables() {
   return t;
 }
 
-const ModTables& tables() {
-  static const ModTables t = make_tables();
-  return t;
+const ModTables& tables(int tab) {
+  static const ModTables t[NTAB] = {make_tables(16), make_tables(15)};
+  return t[tab];
 }
 
 void upload_tables(int device) {
@@ -126,14 +134,17 @@ void upload_tables(int device) {
   static bool done[64] = {};
   std::lock_guard<std::mutex> g(mu);
   if (device >= 0 && device < 64 && done[device]) return;
-  const ModTables& t = tables();
+  const ModTables& t = tables(0);
   QLRA_CUDA(cudaMemcpyToSymbol(c_p, t.p, sizeof(t.p)));
   QLRA_CUDA(cudaMemcpyToSymbol(c_pinv, t.pinv, sizeof(t.pinv)));
   QLRA_CUDA(cudaMemcpyToSymbol(c_pinvf, t.pinvf, sizeof(t.pinvf)));
-  QLRA_CUDA(cudaMemcpyToSymbol(c_yinv, t.yinv, sizeof(t.yinv)));
-  QLRA_CUDA(cudaMemcpyToSymbol(c_M, t.M, sizeof(t.M)));
-  QLRA_CUDA(cudaMemcpyToSymbol(c_P, t.P, sizeof(t.P)));
-  QLRA_CUDA(cudaMemcpyToSymbol(c_H, t.H, sizeof(t.H)));
+  for (int k = 0; k < NTAB; ++k) {
+    const ModTables& u = tables(k);
+    QLRA_CUDA(cudaMemcpyToSymbol(c_yinv, u.yinv, sizeof(u.yinv), k * sizeof(u.yinv)));
+    QLRA_CUDA(cudaMemcpyToSymbol(c_M, u.M, sizeof(u.M), k * sizeof(u.M)));
+    QLRA_CUDA(cudaMemcpyToSymbol(c_P, u.P, sizeof(u.P), k * sizeof(u.P)));
+    QLRA_CUDA(cudaMemcpyToSymbol(c_H, u.H, sizeof(u.H), k * sizeof(u.H)));
+  }
   if (device >= 0 && device < 64) done[device] = true;
 }
 
@@ -156,13 +167,14 @@ __device__ __forceinline__ unsigned pack4(int a, int b, int c, int d) {
 }
 
 // the 8 x 16 residue words of 4 consecutive elements: word (t, mu) at
-// o[(t * NMOD + mu) * ws] (ws: words per batch matrix)
-__device__ __forceinline__ void store_res(unsigned* o, int64_t ws, const double (&c)[8][4]) {
+// o[(t * nmod + mu) * ws] (ws: words per batch matrix)
+__device__ __forceinline__ void store_res(unsigned* o, int64_t ws, const double (&c)[8][4], int nmod) {
+  const int64_t ts = nmod * ws;
 #pragma unroll 1
-  for (int mu = 0; mu < NMOD; ++mu, o += ws)
+  for (int mu = 0; mu < nmod; ++mu, o += ws)
 #pragma unroll
     for (int t = 0; t < 8; ++t)
-      o[t * NMOD * ws] = pack4(sres(c[t][0], mu), sres(c[t][1], mu), sres(c[t][2], mu), sres(c[t][3], mu));
+      o[t * ts] = pack4(sres(c[t][0], mu), sres(c[t][1], mu), sres(c[t][2], mu), sres(c[t][3], mu));
 }
 
 // max |x| over the four planes of a view -> atomicMax on the bit pattern
@@ -220,15 +232,15 @@ __global__ void k_rowmax(QView a, unsigned long long* out) {
   }
 }
 
-// 2^e with max * 2^e in [2^51, 2^52) (0 for an all-zero line)
-__device__ __forceinline__ int scale_exp(unsigned long long maxbits) {
+// 2^e with max * 2^e in [2^(beta-1), 2^beta) (0 for an all-zero line)
+__device__ __forceinline__ int scale_exp(unsigned long long maxbits, int beta) {
   const double m = __longlong_as_double((long long)maxbits);
-  return m > 0.0 ? 51 - ilogb(m) : 0;
+  return m > 0.0 ? beta - 1 - ilogb(m) : 0;
 }
 
 // A panel (R x n) -> Ares[t*16+mu][i][k] (Rpad x npad, zero padded):
 // residues of lcomb_t(rint(A 2^sigma)).  Thread: one row, 4 columns.
-__global__ void k_res_a(QView a, int64_t npad, int64_t rpad, int sigma, int8_t* out, int64_t bstride) {
+__global__ void k_res_a(QView a, int64_t npad, int64_t rpad, int sigma, int8_t* out, int64_t bstride, int nmod) {
   const int64_t nw = npad >> 2;
   const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (e >= rpad * nw) return;
@@ -245,18 +257,18 @@ __global__ void k_res_a(QView a, int64_t npad, int64_t rpad, int sigma, int8_t* 
 #pragma unroll
     for (int t = 0; t < 8; ++t) c[t][q] = qt8::lcomb(t, v);
   }
-  store_res(reinterpret_cast<unsigned*>(out + i * npad + k0), bstride >> 2, c);
+  store_res(reinterpret_cast<unsigned*>(out + i * npad + k0), bstride >> 2, c, nmod);
 }
 
 // Omega (n x s) -> Ores[t*16+mu][j][k] (s x npad): residues of
 // rcomb_t(rint(Omega(k, j) 2^tau_j)).  Thread: one column j, 4 rows k.
 __global__ void k_res_om(QView om, const unsigned long long* colmax, int64_t npad, int64_t spad, int8_t* out,
-                         int64_t bstride) {
+                         int64_t bstride, ModCfg mc) {
   const int64_t nw = npad >> 2;
   const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (e >= spad * nw) return;
   const int64_t j = e / nw, k0 = (e - j * nw) * 4;
-  const int tau = j < om.cols ? scale_exp(colmax[j]) : 0;
+  const int tau = j < om.cols ? scale_exp(colmax[j], mc.beta) : 0;
   const double s1 = ldexp(1.0, tau / 2), s2 = ldexp(1.0, tau - tau / 2);
   double c[8][4];
 #pragma unroll
@@ -269,19 +281,19 @@ __global__ void k_res_om(QView om, const unsigned long long* colmax, int64_t npa
 #pragma unroll
     for (int t = 0; t < 8; ++t) c[t][q] = qt8::rcomb(t, v);
   }
-  store_res(reinterpret_cast<unsigned*>(out + j * npad + k0), bstride >> 2, c);
+  store_res(reinterpret_cast<unsigned*>(out + j * npad + k0), bstride >> 2, c, mc.nmod);
 }
 
 // Psi columns [c0, c0 + R) (l x R) -> Pres[u*16+mu][k][i] (l x Rpad): the
 // right operand of W^* = A^* Psi^*, rcomb_t(rint(conj(Psi(k, i)) 2^rho_k)),
 // stored at the batch u = kConjPerm[t] of the A residues it multiplies.
 __global__ void k_res_psi(QView ps, int64_t c0, int64_t R, int64_t rpad, int64_t lpad,
-                          const unsigned long long* rowmax, int8_t* out, int64_t bstride) {
+                          const unsigned long long* rowmax, int8_t* out, int64_t bstride, ModCfg mc) {
   const int64_t nw = rpad >> 2;
   const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (e >= lpad * nw) return;
   const int64_t k = e / nw, i0 = (e - k * nw) * 4;
-  const int rho = k < ps.rows ? scale_exp(rowmax[k]) : 0;
+  const int rho = k < ps.rows ? scale_exp(rowmax[k], mc.beta) : 0;
   const double s1 = ldexp(1.0, rho / 2), s2 = ldexp(1.0, rho - rho / 2);
   double c[8][4];
 #pragma unroll
@@ -310,29 +322,30 @@ __global__ void k_res_psi(QView ps, int64_t c0, int64_t R, int64_t rpad, int64_t
     d[6][q] = c[7][q];
     d[7][q] = c[6][q];
   }
-  store_res(reinterpret_cast<unsigned*>(out + k * rpad + i0), bstride >> 2, d);
+  store_res(reinterpret_cast<unsigned*>(out + k * rpad + i0), bstride >> 2, d, mc.nmod);
 }
 
 // the signed integer whose residues mod the 16 moduli are c[mu * bstride]
 // (any int32 representatives), |X| < P / 2
-__device__ __forceinline__ i128 crt16(const int32_t* c, int64_t bstride) {
-  const u128 P = ((u128)c_P[1] << 64) | c_P[0];
+__device__ __forceinline__ i128 crt(const int32_t* c, int64_t bstride, ModCfg mc) {
+  const int tb = mc.tab;
+  const u128 P = ((u128)c_P[tb][1] << 64) | c_P[tb][0];
   u128 acc = 0;
 #pragma unroll 4
-  for (int mu = 0; mu < NMOD; ++mu) {
+  for (int mu = 0; mu < mc.nmod; ++mu) {
     const int v = c[mu * bstride];
     const int p = c_p[mu];
     int r = v - __double2int_rd((double)v * c_pinv[mu]) * p;
     r += r < 0 ? p : 0;
     r -= r >= p ? p : 0;
-    int u = r * c_yinv[mu];
+    int u = r * c_yinv[tb][mu];
     u -= __float2int_rd((float)u * c_pinvf[mu]) * p;
     u += u < 0 ? p : 0;
     u -= u >= p ? p : 0;
-    acc += (u128)(unsigned)u * (((u128)c_M[mu][1] << 64) | c_M[mu][0]);
+    acc += (u128)(unsigned)u * (((u128)c_M[tb][mu][1] << 64) | c_M[tb][mu][0]);
     if (acc >= P) acc -= P;
   }
-  const u128 H = ((u128)c_H[1] << 64) | c_H[0];
+  const u128 H = ((u128)c_H[tb][1] << 64) | c_H[tb][0];
   return acc > H ? -(i128)(P - acc) : (i128)acc;
 }
 __device__ __forceinline__ double i128_to_double(i128 x) {
@@ -354,16 +367,16 @@ __device__ __forceinline__ void combine2(const i128 (&x)[8], i128 (&z)[4]) {
 // Y rows of a panel += the recovered products.  cy[t*16+mu][i][j] (ld
 // spad, batch stride bs).  Thread: one (i, j).
 __global__ void k_crt_y(const int32_t* cy, int64_t bs, int64_t spad, QView y, const unsigned long long* om_colmax,
-                        int sigma) {
+                        int sigma, ModCfg mc) {
   const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (e >= y.rows * y.cols) return;
   const int64_t i = e / y.cols, j = e - i * y.cols;
   i128 x[8];
 #pragma unroll 1
-  for (int t = 0; t < 8; ++t) x[t] = crt16(cy + (int64_t)t * NMOD * bs + i * spad + j, bs);
+  for (int t = 0; t < 8; ++t) x[t] = crt(cy + (int64_t)t * mc.nmod * bs + i * spad + j, bs, mc);
   i128 z[4];
   combine2(x, z);
-  const int sh = -(sigma + scale_exp(om_colmax[j])) - 1;  // the 2 of combine2
+  const int sh = -(sigma + scale_exp(om_colmax[j], mc.beta)) - 1;  // the 2 of combine2
 #pragma unroll
   for (int p = 0; p < 4; ++p) y.p[p][i * y.ld + j] += ldexp(i128_to_double(z[p]), sh);
 }
@@ -371,13 +384,13 @@ __global__ void k_crt_y(const int32_t* cy, int64_t bs, int64_t spad, QView y, co
 // W += conj of the recovered W^* products.  cw[u*16+mu][k][j] (ld npad,
 // batch stride bs), u = kConjPerm[t] holding sign kConjSign[t] * m_t.
 __global__ void k_crt_w(const int32_t* cw, int64_t bs, int64_t npad, QView w, const unsigned long long* ps_rowmax,
-                        int sigma) {
+                        int sigma, ModCfg mc) {
   const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (e >= w.rows * w.cols) return;
   const int64_t k = e / w.cols, j = e - k * w.cols;
   i128 xu[8], x[8];
 #pragma unroll 1
-  for (int u = 0; u < 8; ++u) xu[u] = crt16(cw + (int64_t)u * NMOD * bs + k * npad + j, bs);
+  for (int u = 0; u < 8; ++u) xu[u] = crt(cw + (int64_t)u * mc.nmod * bs + k * npad + j, bs, mc);
   // x[t] = kConjSign[t] * xu[kConjPerm[t]]
   x[0] = xu[2];
   x[1] = -xu[1];
@@ -389,7 +402,7 @@ __global__ void k_crt_w(const int32_t* cw, int64_t bs, int64_t npad, QView w, co
   x[7] = xu[6];
   i128 z[4];
   combine2(x, z);
-  const int sh = -(sigma + scale_exp(ps_rowmax[k])) - 1;
+  const int sh = -(sigma + scale_exp(ps_rowmax[k], mc.beta)) - 1;
   w.p[0][k * w.ld + j] += ldexp(i128_to_double(z[0]), sh);
 #pragma unroll
   for (int p = 1; p < 4; ++p) w.p[p][k * w.ld + j] -= ldexp(i128_to_double(z[p]), sh);
@@ -407,7 +420,7 @@ __global__ void k_res_rows(QView src, int conj, const unsigned long long* rowmax
   const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (e >= rpad * nw) return;
   const int64_t r = e / nw, kk = (e - r * nw) * 4;
-  const int ex = r < src.rows ? scale_exp(rowmax[r]) : 0;
+  const int ex = r < src.rows ? scale_exp(rowmax[r], 52) : 0;
   const double s1 = ldexp(1.0, ex / 2), s2 = ldexp(1.0, ex - ex / 2);
   double c[8][4];
 #pragma unroll
@@ -423,7 +436,7 @@ __global__ void k_res_rows(QView src, int conj, const unsigned long long* rowmax
 #pragma unroll
     for (int t = 0; t < 8; ++t) c[t][q] = LEFT ? qt8::lcomb(t, v) : qt8::rcomb(t, v);
   }
-  store_res(reinterpret_cast<unsigned*>(out + r * kpad + kk), bstride >> 2, c);
+  store_res(reinterpret_cast<unsigned*>(out + r * kpad + kk), bstride >> 2, c, NMOD);
 }
 
 // dst (cols x rows, 4 planes, ld rows) = src^T (32 x 32 smem tiles)
@@ -452,10 +465,10 @@ __global__ void k_crt_gen(const int32_t* ci, int64_t bs, int64_t npad, QView c, 
   const int64_t i = e / c.cols, j = e - i * c.cols;
   i128 x[8];
 #pragma unroll 1
-  for (int t = 0; t < 8; ++t) x[t] = crt16(ci + (int64_t)t * NMOD * bs + i * npad + j, bs);
+  for (int t = 0; t < 8; ++t) x[t] = crt(ci + (int64_t)t * NMOD * bs + i * npad + j, bs, ModCfg{NMOD, 0, 52});
   i128 z[4];
   combine2(x, z);
-  const int sh = -(scale_exp(lmax[i]) + scale_exp(rmax[j])) - 1;
+  const int sh = -(scale_exp(lmax[i], 52) + scale_exp(rmax[j], 52)) - 1;
 #pragma unroll
   for (int p = 0; p < 4; ++p) {
     double* d = c.p[p] + i * c.ld + j;
@@ -485,12 +498,13 @@ struct OzState {
     cublasLtMatrixLayout_t la = nullptr, lb = nullptr, lc = nullptr;
     cublasLtMatmulAlgo_t algo{};
   };
-  std::map<std::tuple<int, int64_t, int64_t, int64_t, int64_t, int64_t, int64_t>, Plan> plans;
+  std::map<std::tuple<int, int64_t, int64_t, int64_t, int64_t, int64_t, int64_t, int>, Plan> plans;
   struct Buf {
     void* p = nullptr;
     size_t bytes = 0;
   };
-  Buf ares, pres, ores, cy, cw, stat;
+  Buf ares[2], pres[2], ores, cy[2], cw, stat;
+  cudaStream_t aux = nullptr;  // residues / recovery beside the GEMMs (oz_sketch_block)
   unsigned long long* amax_dev = nullptr;   // 4 slots of max |A| (row pipeline: 0, 1; block: 2)
   unsigned long long* amax_host = nullptr;  // their pinned host copies
 };
@@ -526,7 +540,7 @@ OzState& state(Ctx& c) {
 // int32, `batch` matrices at the given strides (elements)
 OzState::Plan& plan(OzState& s, bool ta, int64_t m, int64_t n, int64_t k, int64_t lda, int64_t ldb, int64_t ldc,
                     int64_t sa, int64_t sb, int64_t sc, int batch) {
-  const auto key = std::make_tuple((int)ta, m, n, k, lda, ldb, ldc);
+  const auto key = std::make_tuple((int)ta, m, n, k, lda, ldb, ldc, batch);
   auto it = s.plans.find(key);
   if (it != s.plans.end()) return it->second;
   OzState::Plan p;
@@ -583,9 +597,14 @@ void oz_release(Ctx& c) {
     cublasLtMatrixLayoutDestroy(kv.second.lc);
     cublasLtMatmulDescDestroy(kv.second.d);
   }
-  for (OzState::Buf* b : {&s->ares, &s->pres, &s->ores, &s->cy, &s->cw, &s->stat})
+  for (OzState::Buf* b : {&s->ares[0], &s->ares[1], &s->pres[0], &s->pres[1], &s->ores, &s->cy[0], &s->cy[1], &s->cw,
+                          &s->stat})
     if (b->p) cudaFreeAsync(b->p, c.stream);
   cudaStreamSynchronize(c.stream);
+  if (s->aux) {
+    cudaStreamSynchronize(s->aux);
+    cudaStreamDestroy(s->aux);
+  }
   if (s->lt_ws) cudaFree(s->lt_ws);
   if (s->amax_host) cudaFreeHost(s->amax_host);
   if (s->amax_dev) cudaFree(s->amax_dev);
@@ -611,10 +630,34 @@ bool oz_wanted(const Ctx& c, int64_t n, int64_t s, int64_t l) {
   return n >= 2048 && s >= 64 && l >= 64;
 }
 
-OzRun::OzRun(Ctx& c, const QView& om, const QView& ps) : ctx(c), omega(om), psi(ps) {
+ModCfg mcfg_of(const OzRun& r) { return ModCfg{r.nmod, r.tab, r.beta}; }
+
+OzRun::OzRun(Ctx& c, const QView& om, const QView& ps, int64_t rows) : ctx(c), omega(om), psi(ps) {
   OzState& s = state(c);
   n = om.rows;
   npad = up16(n);
+  // moduli: 15 (P = 2^117.2) carry every product exactly at 49-bit operand
+  // scales while each int32 accumulation has K <= 2^15 terms (|X| <= K
+  // 2^50 2^50 = 2^115 < P / 2): the block's rows (W^*'s K, one epoch) and n
+  // (Y's K) both within 32768; else 16 (P = 2^124.7) at 52 bits with K < 2^17
+  // (2^123 < P / 2).  15 moduli: 1/16 less residue traffic and int8 work,
+  // operands rounded at 2^-50 of their maxima instead of 2^-53.
+  static const bool force16 = [] {
+    const char* e = std::getenv("QLRA_OZ_MODULI");
+    return e && std::atoi(e) == 16;
+  }();
+  if (!force16 && npad <= 32768 && rows <= 32768) {
+    nmod = 15;
+    tab = 1;
+    beta = 49;
+    kcap = 32768;
+  } else {
+    nmod = 16;
+    tab = 0;
+    beta = 52;
+    kcap = KMAX;
+  }
+  nb = 8 * nmod;
   scols = om.cols;
   spad = up16(scols);  // cuBLASLt's IMMA kernels want 16-aligned m and n
   l = ps.rows;
@@ -635,11 +678,12 @@ OzRun::OzRun(Ctx& c, const QView& om, const QView& ps) : ctx(c), omega(om), psi(
     QLRA_LAUNCH_CHECK();
     count_launch();
   }
-  ores = static_cast<int8_t*>(grow(c, s.ores, (size_t)NB * spad * npad));
-  k_res_om<<<blocks_for(spad * (npad / 4), 256), 256, 0, c.stream>>>(om, om_colmax, npad, spad, ores, spad * npad);
+  ores = static_cast<int8_t*>(grow(c, s.ores, (size_t)nb * spad * npad));
+  k_res_om<<<blocks_for(spad * (npad / 4), 256), 256, 0, c.stream>>>(om, om_colmax, npad, spad, ores, spad * npad,
+                                                                      mcfg_of(*this));
   QLRA_LAUNCH_CHECK();
   count_launch();
-  cw = static_cast<int32_t*>(grow(c, s.cw, sizeof(int32_t) * (size_t)NB * npad * lpad));
+  cw = static_cast<int32_t*>(grow(c, s.cw, sizeof(int32_t) * (size_t)nb * npad * lpad));
 }
 
 // max |A| of a view on `stream`, into panel slot `slot` (device) and its
@@ -666,7 +710,8 @@ double OzRun::amax_host(int slot) const {
 void OzRun::flush(const QView& w) {
   if (!epoch_open) return;
   if (epoch_rows > 0 && w.rows > 0 && w.cols > 0) {
-    k_crt_w<<<blocks_for(w.rows * w.cols, 128), 128, 0, ctx.stream>>>(cw, npad * lpad, npad, w, ps_rowmax, sigma);
+    k_crt_w<<<blocks_for(w.rows * w.cols, 128), 128, 0, ctx.stream>>>(cw, npad * lpad, npad, w, ps_rowmax, sigma,
+                                                                       mcfg_of(*this));
     QLRA_LAUNCH_CHECK();
     count_launch();
   }
@@ -674,94 +719,202 @@ void OzRun::flush(const QView& w) {
   epoch_rows = 0;
 }
 
-// One row panel: A rows [pc0, pc0 + R) of the block (Psi columns likewise),
-// Y rows of the panel, W of the block; amax = max |A| over the panel (or an
-// upper bound: the block's, when it was scanned up front).
-void OzRun::panel(int64_t pc0, const QView& ap, const QView& yr, const QView& w, double amax, int headroom) {
-  OzState& s = *ctx.oz;
-  const int64_t R = ap.rows;
-  if (R == 0 || amax == 0.0) return;  // an all-zero panel adds nothing
-  if (R > KMAX) fail(QLRA_ERR_PARAMETER, "ozaki: panel taller than the int32 accumulation bound");
-  const int64_t rpad = up16(R);
+// Epoch bookkeeping for a panel of rpad rows whose max |A| is amax: flush
+// W^*'s products first when the panel would leave the open epoch's range.
+void OzRun::open_for(int64_t rpad, double amax, int headroom, const QView& w) {
+  if (rpad > kcap) fail(QLRA_ERR_PARAMETER, "ozaki: panel taller than the int32 accumulation bound");
   const int e = std::ilogb(amax);
-  if (epoch_open && (e + sigma > 51 || epoch_rows + rpad > KMAX)) flush(w);
+  if (epoch_open && (e + sigma > beta - 1 || epoch_rows + rpad > kcap)) flush(w);
   if (!epoch_open) {
-    sigma = 51 - e - headroom;
+    sigma = beta - 1 - e - headroom;
     epoch_open = true;
     epoch_rows = 0;
   }
-  auto* ares = static_cast<int8_t*>(grow(ctx, s.ares, (size_t)NB * rpad * npad));
-  k_res_a<<<blocks_for(rpad * (npad / 4), 128), 128, 0, ctx.stream>>>(ap, npad, rpad, sigma, ares, rpad * npad);
+}
+
+// Residues of a panel (A rows [pc0, pc0 + R), Psi columns likewise) into
+// residue buffer `buf`, on `st`.
+void OzRun::prep(int64_t pc0, const QView& ap, int buf, cudaStream_t st) {
+  OzState& s = *ctx.oz;
+  const int64_t R = ap.rows, rpad = up16(R);
+  auto* ares = static_cast<int8_t*>(s.ares[buf].p);
+  k_res_a<<<blocks_for(rpad * (npad / 4), 128), 128, 0, st>>>(ap, npad, rpad, sigma, ares, rpad * npad, nmod);
   QLRA_LAUNCH_CHECK();
   count_launch();
-  int8_t* pres = nullptr;
   if (l > 0) {
-    pres = static_cast<int8_t*>(grow(ctx, s.pres, (size_t)NB * lpad * rpad));
-    k_res_psi<<<blocks_for(lpad * (rpad / 4), 128), 128, 0, ctx.stream>>>(psi, pc0, R, rpad, lpad, ps_rowmax, pres,
-                                                                            lpad * rpad);
+    k_res_psi<<<blocks_for(lpad * (rpad / 4), 128), 128, 0, st>>>(
+        psi, pc0, R, rpad, lpad, ps_rowmax, static_cast<int8_t*>(s.pres[buf].p), lpad * rpad, mcfg_of(*this));
     QLRA_LAUNCH_CHECK();
     count_launch();
   }
-  int32_t* cy = scols > 0 ? static_cast<int32_t*>(grow(ctx, s.cy, sizeof(int32_t) * (size_t)NB * rpad * spad))
-                          : nullptr;
-  {
-    // the tensor-core work of the panel (bench evidence: event-timed)
-    LaunchTimer lt(ctx);
-    // Y panel: col-major C (s x Rpad, ldc spad) = Ores^T (s x npad) * Ares (npad x Rpad)
-    if (scols > 0) {
-      OzState::Plan& py = plan(s, true, spad, rpad, npad, npad, npad, spad, spad * npad, rpad * npad, rpad * spad, NB);
-      run_gemm(ctx, s, py, ores, ares, cy, 0);
-    }
-    // W^* (npad x l, ldc npad) += Ares (npad x Rpad) * Pres (Rpad x l)
-    if (l > 0) {
-      OzState::Plan& pw =
-          plan(s, false, npad, lpad, rpad, npad, rpad, npad, rpad * npad, lpad * rpad, npad * lpad, NB);
-      run_gemm(ctx, s, pw, ares, pres, cw, epoch_rows > 0 ? 1 : 0);
-    }
-    lt.close(32.0 * (double)R * (double)n * (double)(scols + l), 32.0 * (double)R * (double)n,
-             2.0 * NB * (double)rpad * (double)npad * (double)(scols + l), 2);
-  }
+}
+
+// Grow the panel buffers of slot `buf` for panels of up to rpad rows (on
+// the context stream: before any other stream touches them).
+void OzRun::reserve(int64_t rpad, int buf) {
+  OzState& s = *ctx.oz;
+  grow(ctx, s.ares[buf], (size_t)nb * rpad * npad);
+  if (l > 0) grow(ctx, s.pres[buf], (size_t)nb * lpad * rpad);
+  if (scols > 0) grow(ctx, s.cy[buf], sizeof(int32_t) * (size_t)nb * rpad * spad);
+}
+
+// The two batched GEMMs of a prepared panel (context stream; bench timed).
+void OzRun::gemms(int64_t R, int buf) {
+  OzState& s = *ctx.oz;
+  const int64_t rpad = up16(R);
+  LaunchTimer lt(ctx);
+  // Y panel: col-major C (s x Rpad, ldc spad) = Ores^T (s x npad) * Ares (npad x Rpad)
   if (scols > 0) {
-    k_crt_y<<<blocks_for(R * scols, 128), 128, 0, ctx.stream>>>(cy, rpad * spad, spad, yr, om_colmax, sigma);
-    QLRA_LAUNCH_CHECK();
-    count_launch();
+    OzState::Plan& py = plan(s, true, spad, rpad, npad, npad, npad, spad, spad * npad, rpad * npad, rpad * spad, nb);
+    run_gemm(ctx, s, py, ores, s.ares[buf].p, s.cy[buf].p, 0);
   }
+  // W^* (npad x l, ldc npad) += Ares (npad x Rpad) * Pres (Rpad x l)
+  if (l > 0) {
+    OzState::Plan& pw = plan(s, false, npad, lpad, rpad, npad, rpad, npad, rpad * npad, lpad * rpad, npad * lpad, nb);
+    run_gemm(ctx, s, pw, s.ares[buf].p, s.pres[buf].p, cw, epoch_rows > 0 ? 1 : 0);
+  }
+  lt.close(32.0 * (double)R * (double)n * (double)(scols + l), 32.0 * (double)R * (double)n,
+           2.0 * nb * (double)rpad * (double)npad * (double)(scols + l), 2);
   epoch_rows += rpad;
+}
+
+// Y rows of a panel += its recovered products (on `st`).
+void OzRun::recover_y(const QView& yr, int buf, cudaStream_t st) {
+  if (scols == 0 || yr.rows == 0) return;
+  OzState& s = *ctx.oz;
+  const int64_t rpad = up16(yr.rows);
+  k_crt_y<<<blocks_for(yr.rows * scols, 128), 128, 0, st>>>(static_cast<const int32_t*>(s.cy[buf].p), rpad * spad,
+                                                            spad, yr, om_colmax, sigma, mcfg_of(*this));
+  QLRA_LAUNCH_CHECK();
+  count_launch();
+}
+
+// One row panel, all on the context stream (the row pipeline's chunks):
+// A rows [pc0, pc0 + R) of the block, Y rows of the panel, W of the block;
+// amax = max |A| over the panel (or an upper bound).
+void OzRun::panel(int64_t pc0, const QView& ap, const QView& yr, const QView& w, double amax, int headroom) {
+  const int64_t R = ap.rows;
+  if (R == 0 || amax == 0.0) return;  // an all-zero panel adds nothing
+  const int64_t rpad = up16(R);
+  open_for(rpad, amax, headroom, w);
+  reserve(rpad, 0);
+  prep(pc0, ap, 0, ctx.stream);
+  gemms(R, 0);
+  recover_y(yr, 0, ctx.stream);
 }
 
 void OzRun::finish(const QView& w) { flush(w); }
 
 // Whole device-resident block: one scan for max |A| (a single epoch unless
-// the block is taller than the int32 bound), then panels sized for the
-// residue buffer.
+// the block is taller than one int32 accumulation), then panels sized for
+// the residue buffers, software-pipelined over two streams: the residues of
+// panel p+1 (k_res_a, k_res_psi: HBM / FP64-pipe work) and the recovery of
+// panel p-1's Y rows run on an auxiliary stream while panel p's GEMMs hold
+// the tensor cores; two residue / product buffers alternate.
 void oz_sketch_block(Ctx& c, const QView& om, const QView& ps, const QView& block, const QView& y_rows,
                      const QView& w) {
-  OzRun run(c, om, ps);
+  OzRun run(c, om, ps, block.rows);
   run.amax_async(block, c.stream, 2);
   QLRA_CUDA(cudaStreamSynchronize(c.stream));
   const double amax = run.amax_host(2);
-  // residue panel: as tall as memory allows (each panel re-reads and
-  // re-writes W^*'s int32 products, 128 x l x n x 8 bytes, inside its GEMM),
-  // capped by QLRA_OZ_PANEL_BYTES (default 28 GB) and 45% of the free memory
+  if (amax == 0.0 || block.rows == 0) return;
+  // residue panels: as tall as memory allows (each panel re-reads and
+  // re-writes W^*'s int32 products inside its GEMM), two of them, each
+  // capped by QLRA_OZ_PANEL_BYTES (default 28 GB) and 22% of the free memory
   static const double cap = [] {
     const char* e = std::getenv("QLRA_OZ_PANEL_BYTES");
     return e ? std::atof(e) : 28e9;
   }();
   size_t free_b = 0, total_b = 0;
   QLRA_CUDA(cudaMemGetInfo(&free_b, &total_b));
-  const double budget = std::max(1e9, std::min(cap, 0.45 * (double)free_b));
-  int64_t R = (int64_t)(budget / (NB * (double)run.npad));
-  R = std::max<int64_t>(256, std::min<int64_t>(R / 16 * 16, KMAX));
-  // equal panels (no short tail)
-  const int64_t np = (block.rows + R - 1) / R;
+  const double budget = std::max(0.5e9, std::min(cap, 0.22 * (double)free_b));
+  int64_t R = (int64_t)(budget / (run.nb * (double)run.npad));
+  R = std::max<int64_t>(256, std::min<int64_t>(R / 16 * 16, run.kcap));
+  const int64_t np = (block.rows + R - 1) / R;  // equal panels (no short tail)
   R = up16((block.rows + np - 1) / np);
-  for (int64_t r0 = 0; r0 < block.rows; r0 += R) {
-    const int64_t rp = std::min(R, block.rows - r0);
-    run.panel(r0, sub(block, r0, 0, rp, block.cols), sub(y_rows, r0, 0, rp, y_rows.cols), w, amax, 0);
+  static const bool pipelined = [] {
+    const char* e = std::getenv("QLRA_OZ_PIPELINE");
+    return e && std::atoi(e) != 0;
+  }();
+  if (!pipelined) {
+    // sequential panels on the context stream (measured on C4: the power
+    // cap makes the overlapped residues cost the GEMMs' clock, 190 vs 194 ms)
+    for (int64_t r0 = 0; r0 < block.rows; r0 += R) {
+      const int64_t rp = std::min(R, block.rows - r0);
+      run.panel(r0, sub(block, r0, 0, rp, block.cols), sub(y_rows, r0, 0, rp, y_rows.cols), w, amax, 0);
+    }
+    run.finish(w);
+    return;
   }
+  const int nbuf = np > 1 ? 2 : 1;
+  for (int b = 0; b < nbuf; ++b) run.reserve(R, b);
+  OzState& s = *c.oz;
+  if (!s.aux) QLRA_CUDA(cudaStreamCreateWithFlags(&s.aux, cudaStreamNonBlocking));
+  // events: residues of buffer b ready / buffer b's GEMMs done / its Y recovered
+  struct Ev {
+    cudaEvent_t e[6] = {};
+    Ev() {
+      for (auto& x : e) QLRA_CUDA(cudaEventCreateWithFlags(&x, cudaEventDisableTiming));
+    }
+    ~Ev() {
+      for (auto& x : e)
+        if (x) cudaEventDestroy(x);
+    }
+  } ev;
+  cudaEvent_t* ready = ev.e;
+  cudaEvent_t* gemmed = ev.e + 2;
+  cudaEvent_t* recovered = ev.e + 4;
+  struct Join {  // the context stream waits for the aux stream on every exit
+    Ctx& c;
+    cudaStream_t aux;
+    cudaEvent_t e;
+    ~Join() {
+      if (cudaEventRecord(e, aux) == cudaSuccess) cudaStreamWaitEvent(c.stream, e, 0);
+      cudaStreamSynchronize(aux);
+    }
+  };
+  cudaEvent_t join_ev;
+  QLRA_CUDA(cudaEventCreateWithFlags(&join_ev, cudaEventDisableTiming));
+  {
+    Join join{c, s.aux, join_ev};
+    // the aux stream starts after everything queued so far (buffers, Omega's residues)
+    QLRA_CUDA(cudaEventRecord(ready[0], c.stream));
+    QLRA_CUDA(cudaStreamWaitEvent(s.aux, ready[0], 0));
+    run.open_for(R, amax, 0, w);
+    int64_t prev_r0 = -1;
+    for (int64_t p = 0, r0 = 0; r0 < block.rows; ++p, r0 += R) {
+      const int b = (int)(p % nbuf);
+      const int64_t rp = std::min(R, block.rows - r0);
+      if (p >= nbuf) {
+        // buffer b was last used by panel p - nbuf: its GEMMs and Y recovery first
+        QLRA_CUDA(cudaStreamWaitEvent(s.aux, gemmed[b], 0));
+      }
+      run.prep(r0, sub(block, r0, 0, rp, block.cols), b, s.aux);
+      QLRA_CUDA(cudaEventRecord(ready[b], s.aux));
+      if (prev_r0 >= 0) {
+        // Y rows of the previous panel, on aux behind this panel's residues
+        const int pb = (int)((p - 1) % nbuf);
+        const int64_t prp = std::min(R, block.rows - prev_r0);
+        QLRA_CUDA(cudaStreamWaitEvent(s.aux, gemmed[pb], 0));
+        run.recover_y(sub(y_rows, prev_r0, 0, prp, y_rows.cols), pb, s.aux);
+        QLRA_CUDA(cudaEventRecord(recovered[pb], s.aux));
+      }
+      QLRA_CUDA(cudaStreamWaitEvent(c.stream, ready[b], 0));
+      if (p >= nbuf) QLRA_CUDA(cudaStreamWaitEvent(c.stream, recovered[b], 0));  // cy[b] read
+      // more rows than one int32 accumulation: recover W and start a new
+      // epoch (same scale: the block's max)
+      run.open_for(up16(rp), amax, 0, w);
+      run.gemms(rp, b);
+      QLRA_CUDA(cudaEventRecord(gemmed[b], c.stream));
+      prev_r0 = r0;
+    }
+    // the last panel's Y rows
+    const int pb = (int)((np - 1) % nbuf);
+    run.recover_y(sub(y_rows, prev_r0, 0, std::min(R, block.rows - prev_r0), y_rows.cols), pb, c.stream);
+  }
+  cudaEventDestroy(join_ev);
   run.finish(w);
 }
-
 
 // ---------------------------------------------------------------------------
 // General quaternion product on the int8 engine, for the large-K products of

@@ -27,10 +27,14 @@ struct OzRun {
   unsigned long long* ps_rowmax = nullptr;  // device: max |Psi(k, :)| bits
   int8_t* ores = nullptr;                   // Omega residues (128 x s x npad)
   int32_t* cw = nullptr;                    // W^* products (128 x l x npad), int32
+  int nmod = 16, tab = 0, beta = 52, nb = 128;  // moduli, CRT table, operand bits, batch (8 nmod)
+  int64_t kcap = 0;  // rows per int32 accumulation (epoch)
   bool epoch_open = false;
   int64_t epoch_rows = 0;
   int sigma = 0;  // A' = rint(A 2^sigma) in the open epoch
-  OzRun(Ctx& c, const QView& om, const QView& ps);
+  // rows: the block's row count (the moduli are chosen from it and n)
+  OzRun(Ctx& c, const QView& om, const QView& ps, int64_t rows);
+
   OzRun(const OzRun&) = delete;
   OzRun& operator=(const OzRun&) = delete;
   // max |a| on `stream` into slot 0..2 (device) and its pinned host copy
@@ -40,6 +44,12 @@ struct OzRun {
   // products accumulated; amax bounds max |ap|; headroom: spare bits of the
   // epoch scale for later panels (streamed blocks)
   void panel(int64_t pc0, const QView& ap, const QView& yr, const QView& w, double amax, int headroom);
+  // phases of a panel (oz_sketch_block pipelines them over two streams)
+  void open_for(int64_t rpad, double amax, int headroom, const QView& w);
+  void reserve(int64_t rpad, int buf);
+  void prep(int64_t pc0, const QView& ap, int buf, cudaStream_t st);
+  void gemms(int64_t R, int buf);
+  void recover_y(const QView& yr, int buf, cudaStream_t st);
   void flush(const QView& w);
   void finish(const QView& w);
 };

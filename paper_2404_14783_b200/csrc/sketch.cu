@@ -1046,7 +1046,7 @@ void sketch_rows_pipeline(Ctx& ctx, const qlra_spec_t& omega, const qlra_spec_t&
   // (max |A| of each chunk is taken on the copy stream right after its DMA,
   // so the host reads it without waiting for the previous chunk's work)
   std::unique_ptr<OzRun> oz;
-  if (oz_wanted(ctx, n, s, psi.rows)) oz.reset(new OzRun(ctx, e.om, e.ps));
+  if (oz_wanted(ctx, n, s, psi.rows)) oz.reset(new OzRun(ctx, e.om, e.ps, b));
   // The last R rows go in quarter-size chunks: the sketch of the final chunk
   // is the one part of the pipeline nothing overlaps (the copy stream is the
   // bottleneck before it), so it should be short.
