@@ -884,11 +884,16 @@ __global__ void __launch_bounds__(SNT) k_quat_jacobi(QView g, QView v, double* w
 // V^T <- J^T V^T (V is kept transposed so its column rotations are row
 // operations).  Off-diagonal norm checked per sweep; reductions in CTA order
 // (deterministic).
+// a pair is rotated only while |G_pq| > kJacobiTol sqrt(|G_pp G_qq|) (the
+// relative criterion of Demmel-Veselic); a sweep with no rotation ends the
+// iteration.  The Frobenius test alone (off <= 1e-15 ||G||) is below the
+// rounding floor of n = 220 and ran the 30-sweep cap.
+constexpr double kJacobiTol = 4.0 * 2.220446049250313e-16;
 __device__ __forceinline__ int rr_index(int64_t i, int64_t round, int64_t m) {
   return i == 0 ? 0 : (int)(1 + (((i - 1 - round) % m) + m) % m);
 }
 __global__ void __launch_bounds__(256) k_quat_jacobi_coop(QView g, QView vt, double* w, int max_sweeps,
-                                                          double* rc, double* part) {
+                                                          double* rc, double* part, int* flag) {
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
   __shared__ double sh[32];
@@ -930,6 +935,8 @@ __global__ void __launch_bounds__(256) k_quat_jacobi_coop(QView g, QView vt, dou
     off = sqrt(off);
     grid.sync();  // part is rewritten next sweep
     if (!(off > 1e-15 * scale)) break;  // uniform decision
+    if (gtid == 0) flag[sweep & 1] = 0;  // (the other slot was read last sweep)
+    int rotated = 0;
     for (int64_t round = 0; round < m; ++round) {
       // (A) rotation parameters
       for (int64_t k = gtid; k < npairs; k += gthreads) {
@@ -940,13 +947,14 @@ __global__ void __launch_bounds__(256) k_quat_jacobi_coop(QView g, QView vt, dou
         if (q < n) {
           const Q4 b = qload(g, p, q);
           const double nbq = sqrt(b.w * b.w + b.x * b.x + b.y * b.y + b.z * b.z);
-          if (nbq > 1e-300) {
+          const double a = g.p[0][p * g.ld + p], d = g.p[0][q * g.ld + q];
+          if (nbq > 1e-300 && nbq > kJacobiTol * sqrt(fabs(a) * fabs(d))) {
             u = Q4{b.w / nbq, b.x / nbq, b.y / nbq, b.z / nbq};
-            const double a = g.p[0][p * g.ld + p], d = g.p[0][q * g.ld + q];
             const double th = (d - a) / (2.0 * nbq);
             const double tt = (th >= 0 ? 1.0 : -1.0) / (fabs(th) + sqrt(th * th + 1.0));
             c = 1.0 / sqrt(1.0 + tt * tt);
             sn = tt * c;
+            rotated = 1;
           }
         }
         double* r = rc + k * 8;
@@ -989,155 +997,11 @@ __global__ void __launch_bounds__(256) k_quat_jacobi_coop(QView g, QView vt, dou
       }
       grid.sync();
     }
+    if (rotated) atomicOr(flag + (sweep & 1), 1);
+    grid.sync();
+    if (*(volatile int*)(flag + (sweep & 1)) == 0) break;  // a sweep without a rotation (uniform)
   }
   for (int64_t i = gtid; i < n; i += gthreads) w[i] = g.p[0][i * g.ld + i];
-}
-
-// Cluster Jacobi (n <= QJC_MAX): the same rotations in the same round-robin
-// order as k_quat_jacobi_coop, with G and V^T resident in the distributed
-// shared memory of one 16-CTA cluster (row r in CTA r % 16) instead of
-// L2 + grid-wide barriers (83 ms per C3 Gram, n = 220, at ~13 us per grid
-// sync).  Per round: (A) the owner of row p (p < q) forms the pair's
-// rotation and writes it into every CTA's table; (B) it rotates rows p, q
-// of G and of V^T, reading and writing row q in its owner's shared memory
-// (each row belongs to one pair, so there is no race); (C) every CTA
-// rotates columns p, q inside its own rows of G.  Three cluster barriers
-// per round; the off-diagonal norm is reduced through CTA 0 once a sweep.
-constexpr int QJC = 16;
-constexpr int QJC_THREADS = 512;
-constexpr int QJC_MAX = 224;
-__global__ void __cluster_dims__(QJC, 1, 1) __launch_bounds__(QJC_THREADS)
-    k_quat_jacobi_cluster(QView g, QView vt, double* w, int max_sweeps) {
-  namespace cg = cooperative_groups;
-  cg::cluster_group cl = cg::this_cluster();
-  extern __shared__ __align__(16) unsigned char dsm[];
-  const int n = (int)g.rows, rank = (int)cl.block_rank(), t = threadIdx.x, nt = blockDim.x;
-  const int np = n + (n & 1), npairs = np / 2, m = np - 1;
-  const int rmax = (n + QJC - 1) / QJC, nr = (n - rank + QJC - 1) / QJC;  // rows owned: rank + QJC * li
-  Q4* gr = reinterpret_cast<Q4*>(dsm);          // rmax x n
-  Q4* vr = gr + (size_t)rmax * n;               // rmax x n (rows of V^T)
-  double* prm = reinterpret_cast<double*>(vr + (size_t)rmax * n);  // npairs x 8
-  double* part = prm + 8 * (size_t)npairs;      // QJC partial sums (CTA 0's copy is read)
-  __shared__ double sh[32];
-  for (int e = t; e < nr * n; e += nt) {
-    const int li = e / n, j = e % n, r = rank + QJC * li;
-    gr[li * n + j] = qload(g, r, j);
-    vr[li * n + j] = Q4{r == j ? 1.0 : 0.0, 0.0, 0.0, 0.0};
-  }
-  auto row_of = [&](int r, Q4* base) -> Q4* {  // row r of G (base gr) or V^T (base vr) in its owner's memory
-    Q4* local = base + (size_t)(r / QJC) * n;
-    return cl.map_shared_rank(local, r % QJC);
-  };
-  // Frobenius norm (the scale of the off-diagonal test)
-  double scale = 0.0;
-  {
-    double pa = 0.0;
-    for (int e = t; e < nr * n; e += nt) {
-      const Q4 q = gr[e];
-      pa += q.w * q.w + q.x * q.x + q.y * q.y + q.z * q.z;
-    }
-    pa = block_sum(pa, sh);
-    cl.sync();
-    if (t == 0) cl.map_shared_rank(part, 0)[rank] = pa;
-    cl.sync();
-    const double* p0 = cl.map_shared_rank(part, 0);
-    for (int b = 0; b < QJC; ++b) scale += p0[b];
-    scale = sqrt(scale);
-  }
-  for (int sweep = 0; sweep < max_sweeps && n > 1; ++sweep) {
-    double pa = 0.0;
-    for (int e = t; e < nr * n; e += nt) {
-      const int li = e / n, j = e % n;
-      if (rank + QJC * li == j) continue;
-      const Q4 q = gr[e];
-      pa += q.w * q.w + q.x * q.x + q.y * q.y + q.z * q.z;
-    }
-    pa = block_sum(pa, sh);
-    cl.sync();  // part of CTA 0 is free (read last sweep)
-    if (t == 0) cl.map_shared_rank(part, 0)[rank] = pa;
-    cl.sync();
-    double off = 0.0;
-    {
-      const double* p0 = cl.map_shared_rank(part, 0);
-      for (int b = 0; b < QJC; ++b) off += p0[b];
-    }
-    off = sqrt(off);
-    if (!(off > 1e-15 * scale)) break;  // uniform decision
-    for (int round = 0; round < m; ++round) {
-      // (A) rotations of the pairs whose row p this CTA owns, into every table
-      for (int k = t; k < npairs; k += nt) {
-        int p = rr_index(k, round, m), q = rr_index(np - 1 - k, round, m);
-        if (p > q) { const int tmp = p; p = q; q = tmp; }
-        if (p % QJC != rank) continue;
-        double c = 1.0, sn = 0.0;
-        Q4 u{1.0, 0.0, 0.0, 0.0};
-        if (q < n) {
-          const Q4 b = gr[(p / QJC) * n + q];
-          const double nbq = sqrt(b.w * b.w + b.x * b.x + b.y * b.y + b.z * b.z);
-          if (nbq > 1e-300) {
-            u = Q4{b.w / nbq, b.x / nbq, b.y / nbq, b.z / nbq};
-            const double a = gr[(p / QJC) * n + p].w, d = row_of(q, gr)[q].w;
-            const double th = (d - a) / (2.0 * nbq);
-            const double tt = (th >= 0 ? 1.0 : -1.0) / (fabs(th) + sqrt(th * th + 1.0));
-            c = 1.0 / sqrt(1.0 + tt * tt);
-            sn = tt * c;
-          }
-        }
-        const double v8[8] = {c, sn, u.w, u.x, u.y, u.z, (double)p, (double)q};
-        for (int b = 0; b < QJC; ++b) {
-          double* dst = cl.map_shared_rank(prm + 8 * (size_t)k, b);
-#pragma unroll
-          for (int i = 0; i < 8; ++i) dst[i] = v8[i];
-        }
-      }
-      cl.sync();
-      // (B) rows p, q of G (G <- J^* G) and of V^T ((V J)^T), by the owner of p
-      for (int e = t; e < npairs * n; e += nt) {
-        const int k = e / n, j = e % n;
-        const double* r = prm + 8 * (size_t)k;
-        const int p = (int)r[6], q = (int)r[7];
-        if (q >= n || p % QJC != rank) continue;
-        const double c = r[0], sn = r[1];
-        {
-          const Q4 u{r[2], r[3], r[4], r[5]};
-          Q4* rowp = gr + (size_t)(p / QJC) * n;
-          Q4* rowq = row_of(q, gr);
-          const Q4 rp = rowp[j], rq = qmul(u, rowq[j]);
-          rowp[j] = Q4{c * rp.w - sn * rq.w, c * rp.x - sn * rq.x, c * rp.y - sn * rq.y, c * rp.z - sn * rq.z};
-          rowq[j] = Q4{sn * rp.w + c * rq.w, sn * rp.x + c * rq.x, sn * rp.y + c * rq.y, sn * rp.z + c * rq.z};
-        }
-        {
-          const Q4 uc{r[2], -r[3], -r[4], -r[5]};
-          Q4* vp = vr + (size_t)(p / QJC) * n;
-          Q4* vq = row_of(q, vr);
-          const Q4 cp = vp[j], cq = qmul(vq[j], uc);
-          vp[j] = Q4{c * cp.w - sn * cq.w, c * cp.x - sn * cq.x, c * cp.y - sn * cq.y, c * cp.z - sn * cq.z};
-          vq[j] = Q4{sn * cp.w + c * cq.w, sn * cp.x + c * cq.x, sn * cp.y + c * cq.y, sn * cp.z + c * cq.z};
-        }
-      }
-      cl.sync();
-      // (C) columns p, q inside this CTA's rows of G (G <- G J)
-      for (int e = t; e < nr * npairs; e += nt) {
-        const int li = e / npairs, k = e % npairs;
-        const double* r = prm + 8 * (size_t)k;
-        const int p = (int)r[6], q = (int)r[7];
-        if (q >= n) continue;
-        const double c = r[0], sn = r[1];
-        const Q4 uc{r[2], -r[3], -r[4], -r[5]};
-        Q4* row = gr + (size_t)li * n;
-        const Q4 cp = row[p], cq = qmul(row[q], uc);
-        row[p] = Q4{c * cp.w - sn * cq.w, c * cp.x - sn * cq.x, c * cp.y - sn * cq.y, c * cp.z - sn * cq.z};
-        row[q] = Q4{sn * cp.w + c * cq.w, sn * cp.x + c * cq.x, sn * cp.y + c * cq.y, sn * cp.z + c * cq.z};
-      }
-      cl.sync();
-    }
-  }
-  for (int e = t; e < nr * n; e += nt) {
-    const int li = e / n, j = e % n, r = rank + QJC * li;
-    qstore(vt, r, j, vr[e]);
-    if (j == r) w[r] = gr[e].w;
-  }
-  cl.sync();  // no CTA exits while a peer may still read its shared memory
 }
 
 // Eigenpairs sorted descending (stable by index) from V^T (rows = vectors).
@@ -1745,26 +1609,6 @@ void small_quat_herm_eigvals(Ctx& ctx, const QView& a, double* d_w, bool extreme
 void small_quat_eigh(Ctx& ctx, const QView& a, double* d_w, const QView& vecs, int max_sweeps) {
   const int64_t n = a.rows;
   if (n == 0) return;
-  static const bool no_cluster = [] {
-    const char* e = std::getenv("QLRA_JACOBI_COOP");
-    return e && std::atoi(e) != 0;
-  }();
-  if (n > 64 && n <= QJC_MAX && !no_cluster) {  // cluster Jacobi, G and V^T in distributed shared memory
-    const int rmax = (int)((n + QJC - 1) / QJC);
-    const int64_t np = n + (n & 1);
-    const size_t smem = sizeof(Q4) * 2 * (size_t)rmax * n + sizeof(double) * (8 * (size_t)(np / 2) + QJC);
-    set_func_attr((const void*)k_quat_jacobi_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    set_func_attr((const void*)k_quat_jacobi_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    DevQMat vt(ctx, n, n);
-    DeviceBuffer w(ctx, sizeof(double) * (size_t)n);
-    k_quat_jacobi_cluster<<<QJC, QJC_THREADS, smem, ctx.stream>>>(a, vt.v, w.as<double>(), max_sweeps);
-    QLRA_LAUNCH_CHECK();
-    count_launch();
-    k_sort_eigen_t<<<(unsigned)std::min<int64_t>(n, 1024), 128, 0, ctx.stream>>>(w.as<double>(), vt.v, d_w, vecs);
-    QLRA_LAUNCH_CHECK();
-    count_launch();
-    return;
-  }
   if (n > 64) {  // cooperative grid Jacobi
     int dev = 0, sms = 148, per_sm = 0;
     QLRA_CUDA(cudaGetDevice(&dev));
@@ -1775,12 +1619,13 @@ void small_quat_eigh(Ctx& ctx, const QView& a, double* d_w, const QView& vecs, i
     const int blocks = std::max(1, std::min(want, sms * std::max(per_sm, 1)));
     DevQMat vt(ctx, n, n);
     DeviceBuffer w(ctx, sizeof(double) * (size_t)n), rc(ctx, sizeof(double) * 8 * (size_t)(np / 2)),
-        part(ctx, sizeof(double) * (size_t)blocks);
+        part(ctx, sizeof(double) * (size_t)blocks), fl(ctx, 2 * sizeof(int));
     QView av = a, vv = vt.v;
     double* wp = w.as<double>();
     double* rcp = rc.as<double>();
     double* pp = part.as<double>();
-    void* args[] = {&av, &vv, &wp, &max_sweeps, &rcp, &pp};
+    int* flp = fl.as<int>();
+    void* args[] = {&av, &vv, &wp, &max_sweeps, &rcp, &pp, &flp};
     QLRA_CUDA(cudaLaunchCooperativeKernel((const void*)k_quat_jacobi_coop, dim3(blocks), dim3(256), args, 0,
                                           ctx.stream));
     count_launch();

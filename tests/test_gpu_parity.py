@@ -496,8 +496,8 @@ def test_qsvd_on_device(ctx):  # test_factorizations.cpp:73-112
 
 
 @pytest.mark.parametrize("m,n,kappa", [(40, 3000, 1e6), (60, 500, 1e7), (900, 50, 1e5),
-                                       # 64 < k <= 224: the cluster Jacobi eigensolver (distributed
-                                       # shared memory); k > 224: the cooperative-grid one
+                                       # k > 64: the cooperative-grid Jacobi eigensolver (relative
+                                       # stopping criterion; C3's Gram is k = 220)
                                        (120, 2000, 1e6), (1500, 220, 1e7), (224, 900, 1e5), (300, 1500, 1e5)])
 def test_qsvd_graded_spectrum_relative_accuracy(ctx, m, n, kappa):
     """qsvd of a matrix with a graded spectrum (sigma_1 / sigma_k up to 1e7):
