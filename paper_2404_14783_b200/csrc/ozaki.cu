@@ -819,26 +819,27 @@ void oz_sketch_block(Ctx& c, const QView& om, const QView& ps, const QView& bloc
   const double amax = run.amax_host(2);
   if (amax == 0.0 || block.rows == 0) return;
   // residue panels: as tall as memory allows (each panel re-reads and
-  // re-writes W^*'s int32 products inside its GEMM), two of them, each
-  // capped by QLRA_OZ_PANEL_BYTES (default 28 GB) and 22% of the free memory
+  // re-writes W^*'s int32 products inside its GEMM), capped by
+  // QLRA_OZ_PANEL_BYTES (default 28 GB) and 45% of the free memory (22% per
+  // buffer when pipelined: two of them)
+  static const bool pipelined = [] {
+    const char* e = std::getenv("QLRA_OZ_PIPELINE");
+    return e && std::atoi(e) != 0;
+  }();
   static const double cap = [] {
     const char* e = std::getenv("QLRA_OZ_PANEL_BYTES");
     return e ? std::atof(e) : 28e9;
   }();
   size_t free_b = 0, total_b = 0;
   QLRA_CUDA(cudaMemGetInfo(&free_b, &total_b));
-  const double budget = std::max(0.5e9, std::min(cap, 0.22 * (double)free_b));
+  const double budget = std::max(0.5e9, std::min(cap, (pipelined ? 0.22 : 0.45) * (double)free_b));
   int64_t R = (int64_t)(budget / (run.nb * (double)run.npad));
   R = std::max<int64_t>(256, std::min<int64_t>(R / 16 * 16, run.kcap));
   const int64_t np = (block.rows + R - 1) / R;  // equal panels (no short tail)
   R = up16((block.rows + np - 1) / np);
-  static const bool pipelined = [] {
-    const char* e = std::getenv("QLRA_OZ_PIPELINE");
-    return e && std::atoi(e) != 0;
-  }();
   if (!pipelined) {
     // sequential panels on the context stream (measured on C4: the power
-    // cap makes the overlapped residues cost the GEMMs' clock, 190 vs 194 ms)
+    // cap makes the overlapped residues cost the GEMMs' clock, 0.249 vs 0.261 s)
     for (int64_t r0 = 0; r0 < block.rows; r0 += R) {
       const int64_t rp = std::min(R, block.rows - r0);
       run.panel(r0, sub(block, r0, 0, rp, block.cols), sub(y_rows, r0, 0, rp, y_rows.cols), w, amax, 0);
