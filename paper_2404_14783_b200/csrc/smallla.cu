@@ -919,6 +919,7 @@ __global__ void __launch_bounds__(256) k_quat_jacobi_coop(QView g, QView vt, dou
     scale = sqrt(scale);
     grid.sync();
   }
+  double off_prev = INFINITY;
   for (int sweep = 0; sweep < max_sweeps && n > 1; ++sweep) {
     double pa = 0.0;
     for (int64_t e = gtid; e < n * n; e += gthreads) {
@@ -935,6 +936,10 @@ __global__ void __launch_bounds__(256) k_quat_jacobi_coop(QView g, QView vt, dou
     off = sqrt(off);
     grid.sync();  // part is rewritten next sweep
     if (!(off > 1e-15 * scale)) break;  // uniform decision
+    // stagnation at the rounding floor (a graded Gram's noise-level pairs
+    // never meet the relative test): the last sweep did not halve off(G)
+    if (off < 1e-12 * scale && off > 0.5 * off_prev) break;
+    off_prev = off;
     if (gtid == 0) flag[sweep & 1] = 0;  // (the other slot was read last sweep)
     int rotated = 0;
     for (int64_t round = 0; round < m; ++round) {
