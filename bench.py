@@ -458,7 +458,13 @@ def main():
     peaks = {"dfma_tflops": Q.measure_fp64_peak(0, 300.0, ctx), "dmma_tflops": Q.measure_fp64_peak(1, 300.0, ctx)}
     int8_engine = bool(kst["engines"] & 2)
     if int8_engine:
-        peaks["int8_tops"] = Q.measure_int8_peak(300.0, ctx)
+        # burst (300 ms, cool GPU) and sustained (4 s back to back, the clock
+        # the 1000 W cap settles at): the GEMMs are timed inside a ~0.25 s
+        # step under sw_power_cap, so the sustained figure is the denominator
+        # (B200_PROFILING.md: "the sustained one for a kernel timed inside a
+        # long step")
+        peaks["int8_tops_burst"] = Q.measure_int8_peak(300.0, ctx)
+        peaks["int8_tops"] = Q.measure_int8_peak(4000.0, ctx)
     flops_launch = kst["flops"] / max(1, kst["launches"])  # 32 flop / qMAC (the reference's count)
     alg_tflops = flops_launch / (k_ms * 1e-3) / 1e12
     traffic = None
@@ -478,13 +484,15 @@ def main():
         achieved = ops_launch / (k_ms * 1e-3) / 1e12
         peak = peaks["int8_tops"]
         roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TOPS (int8)",
-                "frac": achieved / peak, "frac_of_nominal_4500": achieved / 4500.0, "traffic": traffic,
+                "frac": achieved / peak, "frac_of_burst": achieved / peaks["int8_tops_burst"],
+                "frac_of_nominal_4500": achieved / 4500.0, "traffic": traffic,
                 "kernel_ms_per_launch": k_ms, "launches": kst["launches"],
                 "per_launch": {"int8_ops": ops_launch, "algorithmic_flops": flops_launch,
                                "a_bytes": kst["a_bytes"] / max(1, kst["launches"])},
                 "algorithmic_tflops": alg_tflops,
-                "peak_source": "int8 tensor peak measured in this run (cuBLASLt int8 8192^3 GEMMs back to back; "
-                               "MEASURED_PEAKS.json has no int8 entry; nominal dense 4.5 POPS): " + json.dumps(peaks),
+                "peak_source": "int8 tensor peak measured in this run: cuBLASLt int8 8192^3 GEMMs back to back "
+                               "for 4 s (sustained, under the power cap; the burst 300 ms figure beside it); "
+                               "MEASURED_PEAKS.json has no int8 entry; nominal dense 4.5 POPS: " + json.dumps(peaks),
                 "note": ("int8 engine: every real product of the sketch computed exactly in integers (Ozaki "
                          "scheme, CRT over 16 moduli) as 128 int8 GEMMs per panel (8 quaternion-product "
                          "combinations x 16 moduli), one batched call per sketch side; a launch = one row panel: "
