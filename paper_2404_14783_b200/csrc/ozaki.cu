@@ -185,7 +185,10 @@ __global__ void k_absmax(QView a, unsigned long long* out) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = e / a.cols, j = e - i * a.cols;
 #pragma unroll
-    for (int p = 0; p < 4; ++p) m = fmax(m, fabs(a.p[p][i * a.ld + j]));
+    for (int p = 0; p < 4; ++p) {
+      const double v = a.p[p][i * a.ld + j];
+      m = fmax(m, isfinite(v) ? fabs(v) : INFINITY);  // NaN / inf report inf (fmax would drop a NaN)
+    }
   }
 #pragma unroll
   for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
@@ -811,13 +814,16 @@ void OzRun::finish(const QView& w) { flush(w); }
 // panel p+1 (k_res_a, k_res_psi: HBM / FP64-pipe work) and the recovery of
 // panel p-1's Y rows run on an auxiliary stream while panel p's GEMMs hold
 // the tensor cores; two residue / product buffers alternate.
-void oz_sketch_block(Ctx& c, const QView& om, const QView& ps, const QView& block, const QView& y_rows,
+bool oz_sketch_block(Ctx& c, const QView& om, const QView& ps, const QView& block, const QView& y_rows,
                      const QView& w) {
   OzRun run(c, om, ps, block.rows);
   run.amax_async(block, c.stream, 2);
   QLRA_CUDA(cudaStreamSynchronize(c.stream));
   const double amax = run.amax_host(2);
-  if (amax == 0.0 || block.rows == 0) return;
+  // NaN / inf in A: no fixed-point image -- the caller runs the FP64 engine,
+  // which propagates them as the reference's products do
+  if (!std::isfinite(amax)) return false;
+  if (amax == 0.0 || block.rows == 0) return true;
   // residue panels: as tall as memory allows (each panel re-reads and
   // re-writes W^*'s int32 products inside its GEMM), capped by
   // QLRA_OZ_PANEL_BYTES (default 28 GB) and 45% of the free memory (22% per
@@ -845,7 +851,7 @@ void oz_sketch_block(Ctx& c, const QView& om, const QView& ps, const QView& bloc
       run.panel(r0, sub(block, r0, 0, rp, block.cols), sub(y_rows, r0, 0, rp, y_rows.cols), w, amax, 0);
     }
     run.finish(w);
-    return;
+    return true;
   }
   const int nbuf = np > 1 ? 2 : 1;
   for (int b = 0; b < nbuf; ++b) run.reserve(R, b);
@@ -915,6 +921,7 @@ void oz_sketch_block(Ctx& c, const QView& om, const QView& ps, const QView& bloc
   }
   cudaEventDestroy(join_ev);
   run.finish(w);
+  return true;
 }
 
 // ---------------------------------------------------------------------------

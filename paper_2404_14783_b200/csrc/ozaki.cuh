@@ -54,8 +54,9 @@ struct OzRun {
   void finish(const QView& w);
 };
 
-// the whole sketch of a device-resident block
-void oz_sketch_block(Ctx& c, const QView& om, const QView& ps, const QView& block, const QView& y_rows,
+// the whole sketch of a device-resident block; false (nothing added) when A
+// holds NaN or inf: the caller takes the FP64 engine
+bool oz_sketch_block(Ctx& c, const QView& om, const QView& ps, const QView& block, const QView& y_rows,
                      const QView& w);
 
 }  // namespace qlra_dev

@@ -22,6 +22,7 @@
 // kernel of round 1 is gone: the 16-product engine, qtile.cuh, now only
 // serves qgemm.cu's products.)
 #include <array>
+#include <cmath>
 #include <cstring>
 #include <thread>
 #include <cstdio>
@@ -916,8 +917,8 @@ void sketch_update_rows(Ctx& ctx, const qlra_spec_t& omega, const qlra_spec_t& p
     e.om = om.v;
     e.ps = psi_for_sketch(ctx, psi, row0, b, ps_tmp);
     prepare_emb(ctx, e, psi, row0);  // keeps the combined Psi block for the core solve (psi8_gemm)
-    oz_sketch_block(ctx, e.om, e.ps, block, y_rows, w);
-    return;
+    if (oz_sketch_block(ctx, e.om, e.ps, block, y_rows, w)) return;
+    // non-finite entries: the FP64 engine below
   }
   int64_t pstride = 0;
   if (sketch_use8() && sketch_tma_enabled() && !tma_layout(block, &pstride) && n >= 1024) {
@@ -1091,10 +1092,12 @@ void sketch_rows_pipeline(Ctx& ctx, const qlra_spec_t& omega, const qlra_spec_t&
     if (oz) oz->amax_async(dst, pipe.cs, idx);
     QLRA_CUDA(cudaEventRecord(pipe.copied[idx], pipe.cs));
     QLRA_CUDA(cudaStreamWaitEvent(ctx.stream, pipe.copied[idx], 0));
-    if (oz) {
-      QLRA_CUDA(cudaEventSynchronize(pipe.copied[idx]));
+    if (oz) QLRA_CUDA(cudaEventSynchronize(pipe.copied[idx]));
+    if (oz && std::isfinite(oz->amax_host(idx))) {
       oz->panel(r0, dst, sub(y_rows, r0, 0, rp, s), w, oz->amax_host(idx), 1);
     } else {
+      // (a chunk with NaN / inf takes the FP64 engine: its products add into
+      // W directly, beside the int8 engine's pending epoch)
       sketch_panel(ctx, e, r0, dst, sub(y_rows, r0, 0, rp, s), w, ws);
     }
     QLRA_CUDA(cudaEventRecord(pipe.freed[idx], ctx.stream));

@@ -191,3 +191,24 @@ def test_int8_gram_exactly_hermitian_vs_oracle(ctx, m, s):
     gh = O.adjoint(g)
     assert np.array_equal(g, gh)
     assert np.all(g[1:][:, np.arange(s), np.arange(s)] == 0.0)
+
+
+def test_int8_nonfinite_input_takes_the_fp64_engine(ctx):
+    """NaN / inf in A have no fixed-point image: the int8 engine hands the
+    block (device-resident) or the chunk (host-streamed) to the FP64 engine,
+    so they propagate exactly as the reference's products propagate them."""
+    from paper_2404_14783_b200 import qlra as Q
+    a = random_gaussian(900, 2100, 29)
+    a[1, 500, 7] = np.nan
+    a[3, 10, 2000] = np.inf
+    with engine(ctx, "dmma"):
+        ref = Q.make_sketch(dev(a), 4, 70, 80, 3, 4, ctx=ctx)
+    with engine(ctx, "int8"):
+        got = Q.make_sketch(dev(a), 4, 70, 80, 3, 4, ctx=ctx)
+        ah = torch.from_numpy(a).pin_memory()
+        streamed = Q.make_sketch_host(ah, 4, 70, 80, 3, 4, ctx=ctx, block_rows=300)
+    for st in (got, streamed):
+        for x, r in ((host(st.y), host(ref.y)), (host(st.w), host(ref.w))):
+            assert np.array_equal(np.isnan(x), np.isnan(r)) and np.array_equal(np.isinf(x), np.isinf(r))
+            fin = np.isfinite(r)
+            assert np.abs(x[fin] - r[fin]).max() <= 1e-13 * np.abs(r[fin]).max()
