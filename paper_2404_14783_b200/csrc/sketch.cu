@@ -1111,9 +1111,10 @@ void sketch_rows_pipeline(Ctx& ctx, const qlra_spec_t& omega, const qlra_spec_t&
 void parallel_fill(const QView& host, int64_t r0, int64_t rows, double* dst) {
   const int64_t n = host.cols;
   const size_t bytes = (size_t)(4 * rows * n) * sizeof(double);
-  // all but two host threads (the launching thread and the driver's), >= 8 MB each
-  static const int64_t cap = std::max<int64_t>(8, (int64_t)std::thread::hardware_concurrency() - 2);
-  const int nt = (int)std::max<int64_t>(1, std::min<int64_t>(cap, (int64_t)(bytes >> 23)));
+  // 8 threads, >= 8 MB each (14 threads measured slower on the 16-thread
+  // host: C4 pageable e2e 1.15 s against 0.98 -- they compete with the DMA
+  // for host memory bandwidth)
+  const int nt = (int)std::max<int64_t>(1, std::min<int64_t>(8, (int64_t)(bytes >> 23)));
   auto work = [&](int t) {
     for (int p = 0; p < 4; ++p) {
       const int64_t i0 = rows * t / nt, i1 = rows * (t + 1) / nt;
