@@ -10,8 +10,9 @@
 // scheme, CRT form) and rounded once at the end:
 //
 //  * scaling: A' = rint(A 2^sigma) with one power-of-two scale per epoch
-//    (|A'| <= 2^52), Omega' per column (2^tau_j), Psi' per row (2^rho_k):
-//    the only rounding of the operands, 2^-52 relative to their maxima;
+//    (|A'| <= 2^beta, beta = 49 with 15 moduli or 52 with 16), Omega' per
+//    column (2^tau_j), Psi' per row (2^rho_k): the only rounding of the
+//    operands, 2^-(beta+1) relative to their maxima;
 //  * the 8-product identity (qtile8.cuh): each quaternion GEMM is 8 real
 //    GEMMs of plane combinations (exact integers < 2^53 after scaling);
 //  * residues: each combination reduced modulo 16 pairwise-coprime moduli
