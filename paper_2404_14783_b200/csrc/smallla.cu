@@ -1620,7 +1620,12 @@ void small_quat_eigh(Ctx& ctx, const QView& a, double* d_w, const QView& vecs, i
     QLRA_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     QLRA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_quat_jacobi_coop, 256, 0));
     const int64_t np = n + (n & 1);
-    const int want = (int)std::max<int64_t>(1, std::min<int64_t>(sms, (np / 2 * n + 255) / 256));
+    static const int per_block = [] {  // pair-column updates per block and round (A/B: QLRA_JACOBI_PER_BLOCK)
+      const char* e = std::getenv("QLRA_JACOBI_PER_BLOCK");
+      return e ? std::max(32, std::atoi(e)) : 128;
+    }();
+    const int want = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)sms * std::max(per_sm, 1),
+                                                                  (np / 2 * n + per_block - 1) / per_block));
     const int blocks = std::max(1, std::min(want, sms * std::max(per_sm, 1)));
     DevQMat vt(ctx, n, n);
     DeviceBuffer w(ctx, sizeof(double) * (size_t)n), rc(ctx, sizeof(double) * 8 * (size_t)(np / 2)),
