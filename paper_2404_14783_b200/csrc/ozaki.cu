@@ -66,6 +66,9 @@ __constant__ float c_pinvf[NMOD];
 __constant__ int c_yinv[NTAB][NMOD];                   // (P / p)^-1 mod p
 __constant__ unsigned long long c_M[NTAB][NMOD][2];    // P / p as (lo, hi)
 __constant__ unsigned long long c_P[NTAB][2], c_H[NTAB][2];  // P, floor(P / 2)
+__constant__ unsigned long long c_m64[NMOD];             // ceil(2^64 / p)
+__constant__ unsigned c_m32[NMOD];                       // ceil(2^32 / p)
+__constant__ long long c_off[NMOD];                      // p 2^24 >= 2^31: makes an int32 non-negative
 
 // Moduli in use: the first nmod, CRT table tab, operands scaled to < 2^beta
 // per plane (combinations < 2^(beta+1)): P > 2 K 2^(2 beta + 2) bounds the
@@ -87,6 +90,9 @@ struct ModTables {
   double pinv[NMOD];
   float pinvf[NMOD];
   unsigned long long M[NMOD][2], P[2], H[2];
+  unsigned long long m64[NMOD];
+  unsigned m32[NMOD];
+  long long off[NMOD];
   double log2P = 0.0;
 };
 
@@ -114,6 +120,10 @@ ModTables make_tables(int nmod) {
     t.yinv[i] = inv;
     t.pinv[i] = 1.0 / p;
     t.pinvf[i] = 1.0f / (float)p;
+    // ceil(2^64 / p) (2^56 for p = 256, exact) and ceil(2^32 / p)
+    t.m64[i] = (unsigned long long)((((u128)1 << 64) + (u128)(p - 1)) / (u128)p);
+    t.m32[i] = (unsigned)((((unsigned long long)1 << 32) + (unsigned long long)(p - 1)) / (unsigned long long)p);
+    t.off[i] = (long long)p << 24;
     t.M[i][0] = (unsigned long long)M;
     t.M[i][1] = (unsigned long long)(M >> 64);
   }
@@ -139,6 +149,9 @@ void upload_tables(int device) {
   QLRA_CUDA(cudaMemcpyToSymbol(c_p, t.p, sizeof(t.p)));
   QLRA_CUDA(cudaMemcpyToSymbol(c_pinv, t.pinv, sizeof(t.pinv)));
   QLRA_CUDA(cudaMemcpyToSymbol(c_pinvf, t.pinvf, sizeof(t.pinvf)));
+  QLRA_CUDA(cudaMemcpyToSymbol(c_m64, t.m64, sizeof(t.m64)));
+  QLRA_CUDA(cudaMemcpyToSymbol(c_m32, t.m32, sizeof(t.m32)));
+  QLRA_CUDA(cudaMemcpyToSymbol(c_off, t.off, sizeof(t.off)));
   for (int k = 0; k < NTAB; ++k) {
     const ModTables& u = tables(k);
     QLRA_CUDA(cudaMemcpyToSymbol(c_yinv, u.yinv, sizeof(u.yinv), k * sizeof(u.yinv)));
@@ -337,16 +350,14 @@ __device__ __forceinline__ i128 crt(const int32_t* c, int64_t bstride, ModCfg mc
   u128 acc = 0;
 #pragma unroll 4
   for (int mu = 0; mu < mc.nmod; ++mu) {
-    const int v = c[mu * bstride];
-    const int p = c_p[mu];
-    int r = v - __double2int_rd((double)v * c_pinv[mu]) * p;
-    r += r < 0 ? p : 0;
-    r -= r >= p ? p : 0;
-    int u = r * c_yinv[tb][mu];
-    u -= __float2int_rd((float)u * c_pinvf[mu]) * p;
-    u += u < 0 ? p : 0;
-    u -= u >= p ? p : 0;
-    acc += (u128)(unsigned)u * (((u128)c_M[tb][mu][1] << 64) | c_M[tb][mu][0]);
+    // v mod p and (r y) mod p by multiply-high with ceil(2^64 / p) and
+    // ceil(2^32 / p): exact at these ranges, no conversion instructions
+    const unsigned p = (unsigned)c_p[mu];
+    const unsigned long long xv = (unsigned long long)((long long)c[mu * bstride] + c_off[mu]);  // >= 0, < 2^33
+    const unsigned r = (unsigned)(xv - __umul64hi(xv, c_m64[mu]) * p);
+    const unsigned t = r * (unsigned)c_yinv[tb][mu];  // < 2^16
+    const unsigned u = t - __umulhi(t, c_m32[mu]) * p;
+    acc += (u128)u * (((u128)c_M[tb][mu][1] << 64) | c_M[tb][mu][0]);
     if (acc >= P) acc -= P;
   }
   const u128 H = ((u128)c_H[tb][1] << 64) | c_H[tb][0];
