@@ -163,18 +163,19 @@ void upload_tables(int device) {
 }
 
 // ---------------------------------------------------------------- device --
-// |x| < 2^53 exact integer -> a residue mod p_mu that fits int8, on the
-// FP64 FMA pipe alone (no conversion instructions): q = x / p rounded to
-// the nearest integer through the 1.5 * 2^52 shifter, r = x - p q exactly
-// by the fma, and r + 1.5 * 2^52 carries r in its low word.  x * (1/p) is
-// off by < 0.01, so q is the nearest integer or one off it where x / p is
-// within 0.01 of a half: |r| <= (p + 1) / 2 <= 127 for odd p <= 253, and
-// for p = 256 the int8 wrap is itself congruent mod 256.  (The CRT takes
-// any representative.)
-__device__ __forceinline__ int sres(double x, int mu) {
+// |x| < 2^53 exact integer (x_lo: its low 32 bits) -> a residue mod p_mu
+// that fits int8, with ONE FP64 op: the quotient q = x / p rounded to the
+// nearest integer through the 1.5 * 2^52 shifter (its double then carries
+// q mod 2^32 in the low word: the shifter's low 32 bits are zero), and
+// r = x - p q computed in wrapping 32-bit integers -- exact, since the true
+// r is small.  x * (1/p) is off by < 0.0015 for |x| < 2^53, so for odd p
+// (x / p never within 1 / (2p) > 0.0015 of a half) q = round(x / p) and
+// |r| <= (p - 1) / 2 <= 126; for p = 256 (r = +-128 at exact halves) the
+// int8 wrap is congruent mod 256.  (The CRT takes any representative.)
+__device__ __forceinline__ int sres(double x, int x_lo, int mu) {
   constexpr double kShift = 6755399441055744.0;  // 1.5 * 2^52
-  const double q = fma(x, c_pinv[mu], kShift) - kShift;
-  return __double2loint(fma(-(double)c_p[mu], q, x) + kShift);
+  const int q_lo = __double2loint(fma(x, c_pinv[mu], kShift));
+  return x_lo - c_p[mu] * q_lo;
 }
 __device__ __forceinline__ unsigned pack4(int a, int b, int c, int d) {
   return __byte_perm(__byte_perm(a, b, 0x0040), __byte_perm(c, d, 0x0040), 0x5410);
@@ -184,11 +185,17 @@ __device__ __forceinline__ unsigned pack4(int a, int b, int c, int d) {
 // o[(t * nmod + mu) * ws] (ws: words per batch matrix)
 __device__ __forceinline__ void store_res(unsigned* o, int64_t ws, const double (&c)[8][4], int nmod) {
   const int64_t ts = nmod * ws;
+  int lo[8][4];  // low 32 bits of the exact integers (one conversion each, shared by all moduli)
+#pragma unroll
+  for (int t = 0; t < 8; ++t)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) lo[t][q] = (int)(unsigned long long)__double2ll_rn(c[t][q]);
 #pragma unroll 1
   for (int mu = 0; mu < nmod; ++mu, o += ws)
 #pragma unroll
     for (int t = 0; t < 8; ++t)
-      o[t * ts] = pack4(sres(c[t][0], mu), sres(c[t][1], mu), sres(c[t][2], mu), sres(c[t][3], mu));
+      o[t * ts] = pack4(sres(c[t][0], lo[t][0], mu), sres(c[t][1], lo[t][1], mu), sres(c[t][2], lo[t][2], mu),
+                        sres(c[t][3], lo[t][3], mu));
 }
 
 // max |x| over the four planes of a view -> atomicMax on the bit pattern
