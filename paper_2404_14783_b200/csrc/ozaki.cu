@@ -857,6 +857,17 @@ bool oz_sketch_block(Ctx& c, const QView& om, const QView& ps, const QView& bloc
   }();
   size_t free_b = 0, total_b = 0;
   QLRA_CUDA(cudaMemGetInfo(&free_b, &total_b));
+  {
+    // memory the context's stream-ordered pool holds but no allocation uses
+    // (its release threshold keeps freed blocks reserved) is available too
+    cudaMemPool_t pool = nullptr;
+    cuuint64_t reserved = 0, used = 0;
+    if (cudaDeviceGetDefaultMemPool(&pool, c.device) == cudaSuccess &&
+        cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved) == cudaSuccess &&
+        cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used) == cudaSuccess && reserved > used)
+      free_b += (size_t)(reserved - used);
+    cudaGetLastError();
+  }
   const double budget = std::max(0.5e9, std::min(cap, (pipelined ? 0.22 : 0.45) * (double)free_b));
   int64_t R = (int64_t)(budget / (run.nb * (double)run.npad));
   R = std::max<int64_t>(256, std::min<int64_t>(R / 16 * 16, run.kcap));
