@@ -67,6 +67,7 @@ def lib():
         "qlra_ctx_kernel_stats": ([VP, P(F64), P(I64), P(F64), P(F64)], INT),
         "qlra_ctx_kernel_engines": ([VP, P(INT), P(F64)], INT),
         "qlra_ctx_set_sketch_engine": ([VP, INT], INT),
+        "qlra_one_pass_qb": ([VP, PQ, I64, PS, PS, INT, U64, P(PseudoQrConfig), PQ, PQ, PQ, PQ, P(Report)], INT),
         "qlra_measure_int8_peak": ([VP, F64, P(F64)], INT),
         "qlra_int8_engine_name": ([], C.c_char_p),
         "qlra_gen_test_matrix_block": ([VP, PS, I64, I64, PQ], INT),

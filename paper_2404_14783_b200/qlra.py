@@ -758,6 +758,34 @@ def one_pass_qb(a, opts: OnePassOptions, ctx=None, row0=0, m_global=None, residu
                                            solve_s=qb.solve_s))
 
 
+def one_pass_qb_fused(a, r, s, l, omega_seed, psi_seed, kind=GAUSSIAN, density=1.0, method=PSEUDO_QR,
+                      rangefinder_seed=DEFAULT_RANGEFINDER_SEED, qr_cfg: PseudoQrConfig = PseudoQrConfig(),
+                      ctx=None, row0=0, m_global=None):
+    """make_sketch + qb_stage (sketching.cpp:141-154, 169-194) as ONE C-ABI
+    call (qlra_one_pass_qb) on a device-resident row shard: returns
+    (SketchState, QbResult).  One rank: the int8 engine may finish W's last
+    products beside the rangefinder."""
+    ctx = _ctx(ctx)
+    if method not in (PSEUDO_QR, PSEUDO_SVD):
+        raise ParameterError("qb_stage: unknown rangefinder")
+    m = a.shape[1] if m_global is None else m_global
+    st = empty_sketch(m, a.shape[2], r, s, l, omega_seed, psi_seed, kind, density,
+                      rows_local=a.shape[1], row0=row0)
+    t0 = time.perf_counter()
+    h = torch.empty_like(st.y)
+    x = qzeros(s, st.w.shape[2])
+    c = L.PseudoQrConfig(qr_cfg.max_correction_steps, qr_cfg.power_iters_for_epsilon, qr_cfg.delta_budget)
+    rep = L.Report()
+    om, ps = st.omega_spec.c(), st.psi_spec.c()
+    ctx._check(ctx.lib.qlra_one_pass_qb(ctx.h, C.byref(_qm(a)), row0, C.byref(om), C.byref(ps), method,
+                                        rangefinder_seed, C.byref(c), C.byref(_qm(st.y)), C.byref(_qm(st.w)),
+                                        C.byref(_qm(h)), C.byref(_qm(x)), C.byref(rep)))
+    ctx.synchronize()
+    steps = rep.correction_steps_used if method == PSEUDO_QR else 0
+    rr = RangefinderReport(h, rep.kappa_before, rep.kappa_after, steps, method)
+    return st, QbResult(h, x, rr, time.perf_counter() - t0, 0.0)
+
+
 def one_pass_qb_host(a_host, opts: OnePassOptions, ctx=None, row0=0, m_global=None, block_rows=0,
                      h_out=None, x_out=None) -> QbResult:
     """one_pass_approx through the QB stage (sketching.cpp:250-263), host in and
