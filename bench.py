@@ -318,8 +318,7 @@ def main():
 
     def step(a_dev):
         # one one-pass LRA through the fused public call (qlra_one_pass_qb:
-        # sketch + rangefinder + core solve; the int8 engine finishes W's
-        # tail beside the rangefinder)
+        # sketch + rangefinder + core solve)
         nonlocal method
         if os.environ.get("QLRA_BENCH_STEPTIMES"):
             ms_ = torch.cuda.memory_stats()

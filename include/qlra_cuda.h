@@ -290,8 +290,7 @@ int qlra_qb_stage_with_psi(qlra_ctx_t* ctx, const qlra_qmat_t* psi, const qlra_q
  * rows row0 ..): y (a->rows x s) and w (l x n) receive the sketch (zeroed
  * here; W all-reduced across ranks), h the rangefinder basis, x the core
  * solve.  Equivalent to qlra_sketch_update_rows + qlra_sketch_allreduce +
- * qlra_qb_stage; fused so the int8 engine can finish W's tail beside the
- * rangefinder. */
+ * qlra_qb_stage, in one call. */
 int qlra_one_pass_qb(qlra_ctx_t* ctx, const qlra_qmat_t* a, int64_t row0, const qlra_spec_t* omega,
                      const qlra_spec_t* psi, int method, uint64_t rangefinder_seed,
                      const qlra_pseudo_qr_config_t* cfg, qlra_qmat_t* y, qlra_qmat_t* w, qlra_qmat_t* h,

@@ -815,7 +815,6 @@ void early_solve_start(Ctx& c, EarlySolve& es, const DeferredQ& q0) {
     qgemm(c, QLRA_OP_N, QLRA_OP_N, 1.0, es.cqr.r1inv.v, es.cqr.r2inv.v, 0.0, rinv.v);
     qgemm(c, QLRA_OP_N, QLRA_OP_C, 1.0, es.cqr.r2inv.v, rinv.v, 0.0, mm.v);
     qgemm(c, QLRA_OP_N, QLRA_OP_N, 1.0, es.cqr.t1.v, mm.v, 0.0, t0.v);
-    join_w(c, c.stream);  // (a fused call's W may still be finishing on the int8 engine's stream)
     qgemm(c, QLRA_OP_C, QLRA_OP_N, 1.0, t0.v, es.w, 0.0, es.x0.v);
   }
   QLRA_CUDA(cudaEventRecord(es.x0_ready, c.side2));
@@ -1401,7 +1400,6 @@ int qlra_ctx_destroy(qlra_ctx_t* ctx) {
     cudaStreamDestroy(ctx->c.side2);
   }
   if (ctx->c.tile_cnt2) cudaFree(ctx->c.tile_cnt2);
-  if (ctx->c.w_pending) cudaEventDestroy(ctx->c.w_pending);
   drop_events(ctx->c);
   for (auto& e : ctx->c.ktimer.pool) {
     cudaEventDestroy(e.first);
@@ -1755,9 +1753,7 @@ int qlra_qb_stage(qlra_ctx_t* ctx, const qlra_spec_t* psi, int64_t row0, const q
 
 // one_pass_approx through the QB stage (sketching.cpp:250-263) on a
 // device-resident row shard, in one call: the sketch into y, w (zeroed
-// here), the rangefinder into h, the core solve into x.  Fused so that, on
-// one rank, the int8 engine may finish W's last products and recovery on a
-// side stream while the rangefinder (which reads only Y) runs.
+// here), the rangefinder into h, the core solve into x.
 int qlra_one_pass_qb(qlra_ctx_t* ctx, const qlra_qmat_t* a, int64_t row0, const qlra_spec_t* omega,
                      const qlra_spec_t* psi, int method, uint64_t rangefinder_seed,
                      const qlra_pseudo_qr_config_t* cfg_in, qlra_qmat_t* y, qlra_qmat_t* w, qlra_qmat_t* h,
@@ -1783,31 +1779,13 @@ int qlra_one_pass_qb(qlra_ctx_t* ctx, const qlra_qmat_t* a, int64_t row0, const 
         if (v->rows * v->cols > 0)
           QLRA_CUDA(cudaMemset2DAsync(v->p[p], sizeof(double) * v->ld, 0, sizeof(double) * v->cols, (size_t)v->rows,
                                       c.stream));
-    c.defer_w = c.nranks == 1;
-    try {
-      sketch_update_rows(c, *omega, *psi, row0, view_of(a), yv, wv);
-    } catch (...) {
-      c.defer_w = false;
-      clear_w(c);
-      throw;
-    }
-    c.defer_w = false;
-    struct ClearW {
-      Ctx& c;
-      ~ClearW() {
-        try {
-          clear_w(c);
-        } catch (...) {
-        }
-      }
-    } clear_w_guard{c};
-    allreduce_qmat(c, wv);  // (ranks > 1: nothing was deferred)
+    sketch_update_rows(c, *omega, *psi, row0, view_of(a), yv, wv);
+    allreduce_qmat(c, wv);
     EarlySolve es(c, *psi, row0, wv);
     PsvdDeferred pd;
     if (method == QLRA_PSEUDO_QR) pseudo_qr_dev(c, yv, view_of(h), cfg, rep, &es);
     else pseudo_svd_dev(c, yv, view_of(h), rangefinder_seed, rep, &pd);
     const CoreSolve cs = core_solve(c, &es, *psi, row0, view_of(h), wv);
-    join_w(c, c.stream);
     cs.cols(c, 0, x->cols, view_of(x));
     pd.finish(rep);
   });
@@ -1876,26 +1854,7 @@ int qlra_one_pass_qb_host(qlra_ctx_t* ctx, const qlra_qmat_t* a_host, int64_t ro
     DevQMat y(c, rows, s), w(c, l, n), h(c, rows, s), x(c, s, n);
     y.zero(c);
     w.zero(c);
-    // single rank: W's last int8 products and their recovery may finish on a
-    // side stream while the rangefinder runs (joined before the solve)
-    c.defer_w = c.nranks == 1;
-    try {
-      sketch_update_rows_host(c, *omega, *psi, row0, view_of(a_host), y.v, w.v, block_rows);
-    } catch (...) {
-      c.defer_w = false;
-      clear_w(c);
-      throw;
-    }
-    c.defer_w = false;
-    struct ClearW {  // W joined into the context stream on every exit
-      Ctx& c;
-      ~ClearW() {
-        try {
-          clear_w(c);
-        } catch (...) {
-        }
-      }
-    } clear_w_guard{c};
+    sketch_update_rows_host(c, *omega, *psi, row0, view_of(a_host), y.v, w.v, block_rows);
     allreduce_qmat(c, w.v);
     PsvdDeferred pd;  // pseudo-SVD: the kappa refinements overlapped with the solve
     qlra_rangefinder_report_t rr{};
@@ -1940,7 +1899,6 @@ int qlra_one_pass_qb_host(qlra_ctx_t* ctx, const qlra_qmat_t* a_host, int64_t ro
     // X = T^* W in column blocks; each block is copied back on the side
     // stream while the next one is computed
     const CoreSolve cs = core_solve(c, esp, *psi, row0, h.v, w.v);
-    join_w(c, c.stream);
     const int64_t nblk = n >= 2048 ? 4 : 1;
     const int64_t bw = (n + nblk - 1) / nblk;
     for (int64_t j0 = 0; j0 < n; j0 += bw) {

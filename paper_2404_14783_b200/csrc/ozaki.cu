@@ -526,8 +526,7 @@ struct OzState {
     size_t bytes = 0;
   };
   Buf ares[2], pres[2], ores, cy[2], cw, stat;
-  cudaStream_t aux = nullptr;  // residues / recovery beside the GEMMs; a deferred W's tail
-  cudaEvent_t fork = nullptr;  // context stream -> aux
+  cudaStream_t aux = nullptr;  // residues / recovery beside the GEMMs (oz_sketch_block)
   unsigned long long* amax_dev = nullptr;   // 4 slots of max |A| (row pipeline: 0, 1; block: 2)
   unsigned long long* amax_host = nullptr;  // their pinned host copies
 };
@@ -555,7 +554,6 @@ OzState& state(Ctx& c) {
     QLRA_CUDA(cudaMalloc(&s->lt_ws, s->lt_ws_bytes));
     QLRA_CUDA(cudaMallocHost(&s->amax_host, 4 * sizeof(unsigned long long)));
     QLRA_CUDA(cudaMalloc(&s->amax_dev, 4 * sizeof(unsigned long long)));
-    QLRA_CUDA(cudaEventCreateWithFlags(&s->fork, cudaEventDisableTiming));
   }
   return *c.oz;
 }
@@ -629,7 +627,6 @@ void oz_release(Ctx& c) {
     cudaStreamSynchronize(s->aux);
     cudaStreamDestroy(s->aux);
   }
-  if (s->fork) cudaEventDestroy(s->fork);
   if (s->lt_ws) cudaFree(s->lt_ws);
   if (s->amax_host) cudaFreeHost(s->amax_host);
   if (s->amax_dev) cudaFree(s->amax_dev);
@@ -658,7 +655,6 @@ bool oz_wanted(const Ctx& c, int64_t n, int64_t s, int64_t l) {
 ModCfg mcfg_of(const OzRun& r) { return ModCfg{r.nmod, r.tab, r.beta}; }
 
 OzRun::OzRun(Ctx& c, const QView& om, const QView& ps, int64_t rows) : ctx(c), omega(om), psi(ps) {
-  clear_w(c);  // a W deferred by the previous call still reads this engine's buffers
   OzState& s = state(c);
   n = om.rows;
   npad = up16(n);
@@ -785,10 +781,7 @@ void OzRun::reserve(int64_t rpad, int buf) {
 }
 
 // The two batched GEMMs of a prepared panel (context stream; bench timed).
-// w_aux: the W^* GEMM goes to the auxiliary stream instead (the deferred
-// tail of a fused call: nothing on the context stream reads W before the
-// solve joins it).
-void OzRun::gemms(int64_t R, int buf, bool w_aux) {
+void OzRun::gemms(int64_t R, int buf) {
   OzState& s = *ctx.oz;
   const int64_t rpad = up16(R);
   LaunchTimer lt(ctx);
@@ -800,22 +793,7 @@ void OzRun::gemms(int64_t R, int buf, bool w_aux) {
   // W^* (npad x l, ldc npad) += Ares (npad x Rpad) * Pres (Rpad x l)
   if (l > 0) {
     OzState::Plan& pw = plan(s, false, npad, lpad, rpad, npad, rpad, npad, rpad * npad, lpad * rpad, npad * lpad, nb);
-    if (w_aux) {
-      // after everything queued so far (this panel's residues, the Y GEMM)
-      QLRA_CUDA(cudaEventRecord(s.fork, ctx.stream));
-      QLRA_CUDA(cudaStreamWaitEvent(s.aux, s.fork, 0));
-      const cudaStream_t main = ctx.stream;
-      ctx.stream = s.aux;
-      try {
-        run_gemm(ctx, s, pw, s.ares[buf].p, s.pres[buf].p, cw, epoch_rows > 0 ? 1 : 0);
-      } catch (...) {
-        ctx.stream = main;
-        throw;
-      }
-      ctx.stream = main;
-    } else {
-      run_gemm(ctx, s, pw, s.ares[buf].p, s.pres[buf].p, cw, epoch_rows > 0 ? 1 : 0);
-    }
+    run_gemm(ctx, s, pw, s.ares[buf].p, s.pres[buf].p, cw, epoch_rows > 0 ? 1 : 0);
   }
   lt.close(32.0 * (double)R * (double)n * (double)(scols + l), 32.0 * (double)R * (double)n,
            2.0 * nb * (double)rpad * (double)npad * (double)(scols + l), 2);
@@ -836,42 +814,18 @@ void OzRun::recover_y(const QView& yr, int buf, cudaStream_t st) {
 // One row panel, all on the context stream (the row pipeline's chunks):
 // A rows [pc0, pc0 + R) of the block, Y rows of the panel, W of the block;
 // amax = max |A| over the panel (or an upper bound).
-void OzRun::panel(int64_t pc0, const QView& ap, const QView& yr, const QView& w, double amax, int headroom,
-                  bool last) {
+void OzRun::panel(int64_t pc0, const QView& ap, const QView& yr, const QView& w, double amax, int headroom) {
   const int64_t R = ap.rows;
   if (R == 0 || amax == 0.0) return;  // an all-zero panel adds nothing
   const int64_t rpad = up16(R);
   open_for(rpad, amax, headroom, w);
   reserve(rpad, 0);
   prep(pc0, ap, 0, ctx.stream);
-  // the last panel of a fused call: its W^* GEMM and W's recovery on the
-  // auxiliary stream (finish), overlapping the rangefinder
-  w_deferred = last && ctx.defer_w && l > 0;
-  if (w_deferred && !ctx.oz->aux) QLRA_CUDA(cudaStreamCreateWithFlags(&ctx.oz->aux, cudaStreamNonBlocking));
-  gemms(R, 0, w_deferred);
+  gemms(R, 0);
   recover_y(yr, 0, ctx.stream);
 }
 
-void OzRun::finish(const QView& w) {
-  if (!w_deferred) {
-    flush(w);
-    return;
-  }
-  OzState& s = *ctx.oz;
-  const cudaStream_t main = ctx.stream;
-  ctx.stream = s.aux;  // (the aux stream already follows the last W^* GEMM)
-  try {
-    flush(w);
-  } catch (...) {
-    ctx.stream = main;
-    throw;
-  }
-  ctx.stream = main;
-  if (!ctx.w_pending) QLRA_CUDA(cudaEventCreateWithFlags(&ctx.w_pending, cudaEventDisableTiming));
-  QLRA_CUDA(cudaEventRecord(ctx.w_pending, s.aux));
-  ctx.w_is_pending = true;
-  w_deferred = false;
-}
+void OzRun::finish(const QView& w) { flush(w); }
 
 // Whole device-resident block: one scan for max |A| (a single epoch unless
 // the block is taller than one int32 accumulation), then panels sized for
@@ -924,8 +878,7 @@ bool oz_sketch_block(Ctx& c, const QView& om, const QView& ps, const QView& bloc
     // cap makes the overlapped residues cost the GEMMs' clock, 0.249 vs 0.261 s)
     for (int64_t r0 = 0; r0 < block.rows; r0 += R) {
       const int64_t rp = std::min(R, block.rows - r0);
-      run.panel(r0, sub(block, r0, 0, rp, block.cols), sub(y_rows, r0, 0, rp, y_rows.cols), w, amax, 0,
-                r0 + rp >= block.rows);
+      run.panel(r0, sub(block, r0, 0, rp, block.cols), sub(y_rows, r0, 0, rp, y_rows.cols), w, amax, 0);
     }
     run.finish(w);
     return true;

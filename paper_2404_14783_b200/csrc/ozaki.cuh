@@ -32,7 +32,6 @@ struct OzRun {
   bool epoch_open = false;
   int64_t epoch_rows = 0;
   int sigma = 0;  // A' = rint(A 2^sigma) in the open epoch
-  bool w_deferred = false;  // the last panel's W^* GEMM went to the auxiliary stream
   // rows: the block's row count (the moduli are chosen from it and n)
   OzRun(Ctx& c, const QView& om, const QView& ps, int64_t rows);
 
@@ -44,14 +43,12 @@ struct OzRun {
   // rows [pc0, pc0 + ap.rows) of the block: Y rows yr += ap Omega; W^*
   // products accumulated; amax bounds max |ap|; headroom: spare bits of the
   // epoch scale for later panels (streamed blocks)
-  // last: the call's final panel (its W tail may be deferred, Ctx::defer_w)
-  void panel(int64_t pc0, const QView& ap, const QView& yr, const QView& w, double amax, int headroom,
-             bool last = false);
+  void panel(int64_t pc0, const QView& ap, const QView& yr, const QView& w, double amax, int headroom);
   // phases of a panel (oz_sketch_block pipelines them over two streams)
   void open_for(int64_t rpad, double amax, int headroom, const QView& w);
   void reserve(int64_t rpad, int buf);
   void prep(int64_t pc0, const QView& ap, int buf, cudaStream_t st);
-  void gemms(int64_t R, int buf, bool w_aux = false);
+  void gemms(int64_t R, int buf);
   void recover_y(const QView& yr, int buf, cudaStream_t st);
   void flush(const QView& w);
   void finish(const QView& w);

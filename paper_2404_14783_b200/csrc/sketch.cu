@@ -1094,7 +1094,7 @@ void sketch_rows_pipeline(Ctx& ctx, const qlra_spec_t& omega, const qlra_spec_t&
     QLRA_CUDA(cudaStreamWaitEvent(ctx.stream, pipe.copied[idx], 0));
     if (oz) QLRA_CUDA(cudaEventSynchronize(pipe.copied[idx]));
     if (oz && std::isfinite(oz->amax_host(idx))) {
-      oz->panel(r0, dst, sub(y_rows, r0, 0, rp, s), w, oz->amax_host(idx), 1, r0 + rp >= b);
+      oz->panel(r0, dst, sub(y_rows, r0, 0, rp, s), w, oz->amax_host(idx), 1);
     } else {
       // (a chunk with NaN / inf takes the FP64 engine: its products add into
       // W directly, beside the int8 engine's pending epoch)

@@ -763,8 +763,7 @@ def one_pass_qb_fused(a, r, s, l, omega_seed, psi_seed, kind=GAUSSIAN, density=1
                       ctx=None, row0=0, m_global=None):
     """make_sketch + qb_stage (sketching.cpp:141-154, 169-194) as ONE C-ABI
     call (qlra_one_pass_qb) on a device-resident row shard: returns
-    (SketchState, QbResult).  One rank: the int8 engine may finish W's last
-    products beside the rangefinder."""
+    (SketchState, QbResult)."""
     ctx = _ctx(ctx)
     if method not in (PSEUDO_QR, PSEUDO_SVD):
         raise ParameterError("qb_stage: unknown rangefinder")

@@ -216,15 +216,14 @@ def test_int8_nonfinite_input_takes_the_fp64_engine(ctx):
 
 @pytest.mark.parametrize("cfg_name,method", [("C2", 0), ("C2", 1), ("C1", 0)])
 def test_fused_one_pass_equals_split_calls(ctx, cfg_name, method):
-    """qlra_one_pass_qb (sketch + rangefinder + core solve in one call; the
-    int8 engine finishes W's last products beside the rangefinder) returns
-    exactly what make_sketch + qb_stage return."""
+    """qlra_one_pass_qb (sketch + rangefinder + core solve in one call)
+    returns exactly what make_sketch + qb_stage return."""
     from paper_2404_14783_b200 import configs, qlra as Q
     cfg = configs.CONFIGS[cfg_name]
     a = configs.build_matrix(cfg, ctx=ctx)
     st = Q.make_sketch(a, cfg.s - 5, cfg.s, cfg.l, 1, 2, kind=cfg.kind, ctx=ctx)
     qb = Q.qb_stage(st, method, ctx=ctx)
-    for _ in range(2):  # the second call starts with the first one's deferred W state
+    for _ in range(2):
         st2, qb2 = Q.one_pass_qb_fused(a, cfg.s - 5, cfg.s, cfg.l, 1, 2, kind=cfg.kind, method=method, ctx=ctx)
         assert torch.equal(st2.y, st.y) and torch.equal(st2.w, st.w)
         assert torch.equal(qb2.h, qb.h) and torch.equal(qb2.x, qb.x)
