@@ -565,6 +565,15 @@ OzState::Plan& plan(OzState& s, bool ta, int64_t m, int64_t n, int64_t k, int64_
   const auto key = std::make_tuple((int)ta, m, n, k, lda, ldb, ldc, batch);
   auto it = s.plans.find(key);
   if (it != s.plans.end()) return it->second;
+  if (s.plans.size() >= 256) {  // many distinct panel heights (streamed blocks): start over
+    for (auto& kv : s.plans) {
+      cublasLtMatrixLayoutDestroy(kv.second.la);
+      cublasLtMatrixLayoutDestroy(kv.second.lb);
+      cublasLtMatrixLayoutDestroy(kv.second.lc);
+      cublasLtMatmulDescDestroy(kv.second.d);
+    }
+    s.plans.clear();
+  }
   OzState::Plan p;
   const cublasOperation_t opa = ta ? CUBLAS_OP_T : CUBLAS_OP_N, opb = CUBLAS_OP_N;
   lt_check(cublasLtMatmulDescCreate(&p.d, CUBLAS_COMPUTE_32I, CUDA_R_32I), "desc");
