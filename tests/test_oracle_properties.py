@@ -6,7 +6,7 @@ import numpy as np
 import pytest
 
 from oracle import oracle as O
-from tests.helpers import (orthonormality_defect, planted_conditioned_matrix,
+from tests.helpers import (largest_principal_angle, orthonormality_defect, planted_conditioned_matrix,
                            planted_matrix_with_sigma, random_gaussian, rel_diff)
 
 
@@ -108,3 +108,32 @@ def test_qb_exact_rank_recovered():  # test_sketching.cpp:185-195
     qb = O.qb_stage(y, w, 46, O.PSEUDO_QR)
     res, an = O.residual_sq(wide, qb["h"], qb["x"])
     assert np.sqrt(res) <= 1e-8 * np.sqrt(an)
+
+
+@pytest.mark.parametrize("seed,m,sigma,determined", [
+    (60, 100, [1, 1, 0.5, 0.3, 0.1, 1e-6, 1e-10, 1e-14, 1e-14, 1e-14], False),
+    (61, 80, [1, 1, 0.5, 0.4, 0.3, 0.2, 0.15, 0.1], True),
+    (62, 80, [1, 1, 1, 1, 1, 1, 0.5, 0.25], True)])
+def test_pseudo_svd_bad_block_completion_floor(seed, m, sigma, determined):
+    """The floor of the bad-block parity bar: the
+    reference's own H for its bad-path cases (test_rangefinders.cpp:119-141)
+    under a 1-ulp perturbation of Y.  When every sigma is above the pair
+    floor (kPairFloorRel = 1e-13 sigma_1, factorizations.cpp:60-82) range(H)
+    is range(Y) -- fully determined, whatever the bad_blk draws
+    (rangefinders.cpp:33-41) pick -- and the device is held to 1e-10 against
+    it (test_gpu_parity.py::test_pseudo_svd_bad_paths_vs_oracle).  Below the
+    floor the completion directions are BDCSVD's singular vectors of
+    sigma ~ 1e-14 sigma_1, fixed only to ~u / 1e-14 = O(1): the reference moves
+    them by a percent-level angle under a 1-ulp change of its input, so no
+    implementation can match them."""
+    y = planted_matrix_with_sigma(m, sigma, seed)
+    h0 = O.pseudo_svd(y)["h"]
+    yp = y * (1 + 2.0 ** -52 * np.random.default_rng(1).choice([-1.0, 1.0], size=y.shape))
+    h1 = O.pseudo_svd(yp)["h"]
+    # the bad_blk substream seed does not move a determined range
+    assert largest_principal_angle(h0, O.pseudo_svd(y, seed=12345)["h"]) < 1e-12
+    angle = largest_principal_angle(h0, h1)
+    if determined:
+        assert angle < 1e-12, angle
+    else:
+        assert angle > 1e-3, angle  # the completion is not a function of Y
