@@ -157,6 +157,23 @@ std::vector<double> quat_eigs(Ctx& ctx, const QView& g, bool extremes_only = tru
   return ev;
 }
 
+// The context's stream at the device's greatest priority: kernels of the
+// critical path (main) are dispatched before those of the early solve's
+// second stream (least priority) whenever both have CTAs waiting -- a large
+// side-stream product otherwise holds back the main stream's short launches
+// for its whole duration.  Opt-in (QLRA_MAIN_PRIO=1): measured no gain on C5
+// and within noise (236 vs 243 ms, power-capped) on C4.
+cudaError_t create_main_stream(cudaStream_t* s) {
+  static const bool prio = [] {
+    const char* e = std::getenv("QLRA_MAIN_PRIO");
+    return e && std::atoi(e) != 0;
+  }();
+  int least = 0, greatest = 0;
+  if (prio && cudaDeviceGetStreamPriorityRange(&least, &greatest) == cudaSuccess && greatest != least)
+    return cudaStreamCreateWithPriority(s, cudaStreamNonBlocking, greatest);
+  return cudaStreamCreateWithFlags(s, cudaStreamNonBlocking);
+}
+
 // All eigenvalues of a quaternion Hermitian G computed on a side stream and
 // read back on demand: the host issues other work on ctx.stream and collects
 // the values with get().  G is copied on ctx.stream first, so the caller may
@@ -165,7 +182,7 @@ std::vector<double> quat_eigs(Ctx& ctx, const QView& g, bool extremes_only = tru
 class SideEigs {
  public:
   SideEigs(Ctx& c, const QView& g) : c_(c), n_(g.rows) {
-    if (!c.side) QLRA_CUDA(cudaStreamCreateWithFlags(&c.side, cudaStreamNonBlocking));
+    if (!c.side) QLRA_CUDA(create_main_stream(&c.side));
     side_ = c.side;
     QLRA_CUDA(cudaEventCreateWithFlags(&fork_, cudaEventDisableTiming));
     QLRA_CUDA(cudaEventCreateWithFlags(&done_, cudaEventDisableTiming));
@@ -760,12 +777,16 @@ struct EarlySolve {
   const qlra_spec_t* psi = nullptr;
   int64_t row0 = 0;
   QView w{};
+  // set by the one-pass entries, whose Y = A Omega and W = Psi A come from
+  // the same A in the same call: then Psi Y = W Omega (below)
+  const qlra_spec_t* omega = nullptr;
   bool started = false;
   DeferredQ q0;     // Q0 = base * rinv_last (read by both streams)
   Cqr2Pending cqr;  // P0 = Q_p R_p
   DevQMat x0;       // P0^+ W (s x n)
   DevQMat ck;       // C_k
   DevQMat coef;     // rinv_last C_k (H = base coef, formed on the second stream)
+  DevQMat rinv;     // R1^{-1} R2^{-1} (the W Omega route; copied on main before the fork)
   double kappa = std::numeric_limits<double>::infinity();
   // x0_ready: X0 done; done: everything on the second stream (X0, then H)
   cudaEvent_t x0_ready = nullptr, coef_ready = nullptr, done = nullptr;
@@ -783,7 +804,18 @@ struct EarlySolve {
   EarlySolve& operator=(const EarlySolve&) = delete;
 };
 
-void early_solve_start(Ctx& c, EarlySolve& es, const DeferredQ& q0) {
+// Psi Y = W Omega is used for P0 when n <= rows / 2 (the product over n
+// instead of over the local rows; C5: 80 x 300 x 40 instead of the 6.9 ms
+// 80 x 2097152 x 40 Psi Q0).  P0 = (W Omega) R^{-1} with R^{-1} = R1^{-1}
+// R2^{-1} the chained CholeskyQR2 inverse; it differs from Psi (Y R1^{-1})
+// R2^{-1} by rounding of the order u kappa(Y) relative, the same order as
+// the explicit product's own (T1 = Y R1^{-1} carries that error).
+bool womega_applies(const EarlySolve& es, int64_t rows) {
+  static const bool off = std::getenv("QLRA_NO_WOMEGA") != nullptr;
+  return es.omega && !off && 2 * es.w.cols <= rows;
+}
+
+void early_solve_start(Ctx& c, EarlySolve& es, const DeferredQ& q0, const QView& rinv_full) {
   const int64_t s = q0.base.v.cols, rows = q0.base.v.rows, l = es.psi->rows, n = es.w.cols;
   if (!c.side2) {
     int lo = 0, hi = 0;
@@ -791,6 +823,11 @@ void early_solve_start(Ctx& c, EarlySolve& es, const DeferredQ& q0) {
     QLRA_CUDA(cudaStreamCreateWithPriority(&c.side2, cudaStreamNonBlocking, lo));  // lowest priority
   }
   es.x0 = DevQMat(c, s, n);  // crosses streams: allocated on main before the fork
+  const bool wom = womega_applies(es, rows);
+  if (wom) {
+    es.rinv = DevQMat(c, s, s);
+    copy_qmat(c, rinv_full, es.rinv.v);
+  }
   cudaEvent_t fork = nullptr;
   QLRA_CUDA(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
   QLRA_CUDA(cudaEventCreateWithFlags(&es.done, cudaEventDisableTiming));
@@ -802,11 +839,18 @@ void early_solve_start(Ctx& c, EarlySolve& es, const DeferredQ& q0) {
   {
     StreamSwap on(c, c.side2);
     DevQMat ps_tmp, pb(c, l, s), p0(c, l, s);
-    if (!psi8_gemm(c, *es.psi, es.row0, q0.base.v, pb.v)) {
-      const QView ps = psi_for_solve(c, *es.psi, es.row0, rows, ps_tmp);
-      qgemm(c, QLRA_OP_N, QLRA_OP_N, 1.0, ps, q0.base.v, 0.0, pb.v);
+    if (wom) {
+      DevQMat om(c, n, s);
+      launch_gen(c.stream, *es.omega, 0, 0, n, s, om.v, false);
+      qgemm(c, QLRA_OP_N, QLRA_OP_N, 1.0, es.w, om.v, 0.0, pb.v);  // Psi Y
+      qgemm(c, QLRA_OP_N, QLRA_OP_N, 1.0, pb.v, es.rinv.v, 0.0, p0.v);
+    } else {
+      if (!psi8_gemm(c, *es.psi, es.row0, q0.base.v, pb.v)) {
+        const QView ps = psi_for_solve(c, *es.psi, es.row0, rows, ps_tmp);
+        qgemm(c, QLRA_OP_N, QLRA_OP_N, 1.0, ps, q0.base.v, 0.0, pb.v);
+      }
+      qgemm(c, QLRA_OP_N, QLRA_OP_N, 1.0, pb.v, q0.rinv_last.v, 0.0, p0.v);
     }
-    qgemm(c, QLRA_OP_N, QLRA_OP_N, 1.0, pb.v, q0.rinv_last.v, 0.0, p0.v);
     cqr2_enqueue(c, p0.v, QView{}, /*complex_mode=*/false, /*distributed=*/false, nullptr, /*form_q=*/false,
                  es.cqr);
     // X0 = R_p^{-1} Q_p^* W with Q_p = t1 R2^{-1}, R_p^{-1} = R1^{-1} R2^{-1}:
@@ -877,7 +921,7 @@ struct CoreSolve {
 bool pqr_factors_fast(Ctx& c, const QView& Y, DeferredQ& q0, DevQMat& rq, DevQMat& rq_inv, DevQMat& cm,
                       DevQMat& rc, std::vector<double>& rd, EarlySolve* es) {
   const int64_t s = Y.cols;
-  if (!c.side) QLRA_CUDA(cudaStreamCreateWithFlags(&c.side, cudaStreamNonBlocking));
+  if (!c.side) QLRA_CUDA(create_main_stream(&c.side));
   DevQMat gy(c, s, s), gc(c, s, s), r1c(c, s, s), r1c_inv(c, s, s);
   DeviceBuffer info_c(c, 2 * sizeof(int)), dg_c(c, 2 * sizeof(double) * (size_t)s);
   gram(c, Y, gy.v);
@@ -920,7 +964,7 @@ bool pqr_factors_fast(Ctx& c, const QView& Y, DeferredQ& q0, DevQMat& rq, DevQMa
   q0.base = std::move(p.t1);
   q0.rinv_last = std::move(p.r2inv);
   if (es && c.nranks == 1 && es->psi->rows >= s && !std::getenv("QLRA_NO_EARLY_SOLVE"))
-    early_solve_start(c, *es, q0);
+    early_solve_start(c, *es, q0, rq_inv.v);
   QLRA_CUDA(cudaStreamWaitEvent(c.stream, cdone, 0));
   // (s past the single-launch Cholesky: the blocked form needs the main
   // stream's split-K counters, so the complex pass-1 factor is taken here)
@@ -1321,7 +1365,7 @@ int qlra_ctx_create(qlra_ctx_t** out, int device, int rank, int nranks, const vo
   ctx->c.rank = rank;
   ctx->c.nranks = nranks < 1 ? 1 : nranks;
   const int rc = guarded(ctx, [&](Ctx& c) {
-    QLRA_CUDA(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
+    QLRA_CUDA(create_main_stream(&c.stream));
     c.own_stream = true;
     setup_pool(device);
     QLRA_CUDA(cudaMallocHost(&c.pinned, 4096));
@@ -1347,7 +1391,7 @@ int qlra_ctx_create_local(qlra_ctx_t** out, int device, qlra_group_t* group, int
   qlra_ctx_t* ctx = new qlra_ctx_t();
   ctx->c.device = device;
   const int rc = guarded(ctx, [&](Ctx& c) {
-    QLRA_CUDA(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
+    QLRA_CUDA(create_main_stream(&c.stream));
     c.own_stream = true;
     setup_pool(device);
     QLRA_CUDA(cudaMallocHost(&c.pinned, 4096));
@@ -1782,6 +1826,7 @@ int qlra_one_pass_qb(qlra_ctx_t* ctx, const qlra_qmat_t* a, int64_t row0, const 
     sketch_update_rows(c, *omega, *psi, row0, view_of(a), yv, wv);
     allreduce_qmat(c, wv);
     EarlySolve es(c, *psi, row0, wv);
+    es.omega = omega;
     PsvdDeferred pd;
     if (method == QLRA_PSEUDO_QR) pseudo_qr_dev(c, yv, view_of(h), cfg, rep, &es);
     else pseudo_svd_dev(c, yv, view_of(h), rangefinder_seed, rep, &pd);

@@ -159,7 +159,7 @@ def oracle_qb(run, method, y=None, w=None, key=None):
     return run.oracle[key]
 
 
-def check_qb(run, ctx, method, floor=False):
+def check_qb(run, ctx, method, floor=False, qb=None):
     """Device QB stage vs the oracle's QB stage fed the same device sketch.
 
     Bars: QB error within 1e-10 relative, principal angle <= 1e-8.  With
@@ -174,7 +174,8 @@ def check_qb(run, ctx, method, floor=False):
     from paper_2404_14783_b200 import qlra as Q
     cfg, a = run.cfg, run.a
     t0 = time.time()
-    qb = Q.qb_stage(run.st, method, ctx=ctx)
+    if qb is None:
+        qb = Q.qb_stage(run.st, method, ctx=ctx)
     res_d, an = Q.residual_fro(a, qb.h, qb.x, ctx)
     t1 = time.time()
     qo = oracle_qb(run, method)
@@ -222,6 +223,19 @@ def check_qb(run, ctx, method, floor=False):
     assert abs(err_d / err_o - 1) <= bar_err, (err_d, err_o, bar_err)
     assert ang <= bar_ang, (ang, bar_ang)
     return qb, qo
+
+
+def check_fused(run, ctx, method):
+    """The fused one-pass entry (qlra_one_pass_qb: sketch + rangefinder +
+    solve in one C-ABI call, the bench's timed call) against the oracle.  Its
+    early core solve forms Psi Y as W Omega when n <= rows / 2 (C5), which
+    the split qb_stage cannot assume; the bars are check_qb's."""
+    from paper_2404_14783_b200 import qlra as Q
+    cfg = run.cfg
+    st, qb = Q.one_pass_qb_fused(run.a, cfg.s - 5, cfg.s, cfg.l, 1, 2, cfg.kind, method=method, ctx=ctx)
+    assert rel_diff(host(st.y), run.yh) < 1e-14 and rel_diff(host(st.w), run.wh) < 1e-14
+    del st
+    return check_qb(run, ctx, method, qb=qb)
 
 
 @pytest.fixture(scope="class")
@@ -275,6 +289,9 @@ class TestC4:
     def test_qb(self, run, ctx, method):
         check_qb(run, ctx, method)
 
+    def test_one_pass_fused(self, run, ctx):
+        check_fused(run, ctx, 0)
+
 
 # ------------------------------------------------------------- C5 ---
 class TestC5:
@@ -288,3 +305,6 @@ class TestC5:
     @pytest.mark.parametrize("method", [0, 1])
     def test_qb(self, run, ctx, method):
         check_qb(run, ctx, method)
+
+    def test_one_pass_fused(self, run, ctx):
+        check_fused(run, ctx, 0)
