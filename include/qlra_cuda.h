@@ -155,6 +155,18 @@ int qlra_ctx_set_sketch_engine(qlra_ctx_t* ctx, int engine);
  * GEMMs on this GPU for ~ms milliseconds, and the engine's description. */
 int qlra_measure_int8_peak(qlra_ctx_t* ctx, double ms, double* tops);
 const char* qlra_int8_engine_name(void);
+/* The int8 engine's contraction on its own (csrc/i8gemm.cu: tcgen05.mma
+ * kind::i8, TMA-staged, int32 accumulators in TMEM): for b < batch, exact,
+ *   mode 0: C[b][m*ldc + n] = (beta ? C : 0) + sum_k A[b][m*lda + k] B[b][n*ldb + k]
+ *   mode 1: C[b][n*ldc + m] = (beta ? C : 0) + sum_k A[b][k*lda + m] B[b][n*ldb + k]
+ * i.e. the residue images of Y += A Omega (mode 0) and of W^* += A^* Psi^*
+ * (mode 1) in sketch_update_rows (sketching.cpp:125-139), both read from the
+ * same row-major residue panel.  Device pointers, 16-byte aligned; n, lda,
+ * ldb, stride_a, stride_b multiples of 16, ldc and stride_c of 4. */
+int qlra_i8gemm_batched(qlra_ctx_t* ctx, int mode, int64_t m, int64_t n, int64_t k, const int8_t* a, int64_t lda,
+                        int64_t stride_a, const int8_t* b, int64_t ldb, int64_t stride_b, int32_t* c, int64_t ldc,
+                        int64_t stride_c, int batch, int beta);
+const char* qlra_i8gemm_kernel_name(void);
 
 /* ---------------------------------------------------------- embeddings --- */
 /* gen_block (sketching.cpp:53-71) / gen_test_matrix{,_rows,_cols}

@@ -69,6 +69,8 @@ def lib():
         "qlra_ctx_set_sketch_engine": ([VP, INT], INT),
         "qlra_one_pass_qb": ([VP, PQ, I64, PS, PS, INT, U64, P(PseudoQrConfig), PQ, PQ, PQ, PQ, P(Report)], INT),
         "qlra_measure_int8_peak": ([VP, F64, P(F64)], INT),
+        "qlra_i8gemm_batched": ([VP, INT, I64, I64, I64, VP, I64, I64, VP, I64, I64, VP, I64, I64, INT, INT], INT),
+        "qlra_i8gemm_kernel_name": ([], C.c_char_p),
         "qlra_int8_engine_name": ([], C.c_char_p),
         "qlra_gen_test_matrix_block": ([VP, PS, I64, I64, PQ], INT),
         "qlra_sketch_update_rows": ([VP, PS, PS, I64, PQ, PQ, PQ], INT),

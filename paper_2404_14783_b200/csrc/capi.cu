@@ -22,6 +22,7 @@
 
 #include "common.cuh"
 #include "kernels.cuh"
+#include "i8gemm.cuh"
 #include "ozaki.cuh"
 
 struct qlra_ctx {
@@ -1520,6 +1521,15 @@ int qlra_measure_int8_peak(qlra_ctx_t* ctx, double ms, double* tops) {
 }
 
 const char* qlra_int8_engine_name(void) { return oz_kernel_name(); }
+
+int qlra_i8gemm_batched(qlra_ctx_t* ctx, int mode, int64_t m, int64_t n, int64_t k, const int8_t* a, int64_t lda,
+                        int64_t stride_a, const int8_t* b, int64_t ldb, int64_t stride_b, int32_t* c_out, int64_t ldc,
+                        int64_t stride_c, int batch, int beta) {
+  return guarded(ctx, [&](Ctx& c) {
+    i8gemm_batched(c, mode, m, n, k, a, lda, stride_a, b, ldb, stride_b, c_out, ldc, stride_c, batch, beta, c.stream);
+  });
+}
+const char* qlra_i8gemm_kernel_name(void) { return i8gemm_kernel_name(); }
 
 int qlra_ctx_set_sketch_engine(qlra_ctx_t* ctx, int engine) {
   return guarded(ctx, [&](Ctx& c) {

@@ -44,6 +44,7 @@
 #include <tuple>
 
 #include "common.cuh"
+#include "i8gemm.cuh"
 #include "kernels.cuh"
 #include "ozaki.cuh"
 #include "qtile8.cuh"
@@ -264,7 +265,8 @@ __device__ __forceinline__ int scale_exp(unsigned long long maxbits, int beta) {
 
 // A panel (R x n) -> Ares[t*16+mu][i][k] (Rpad x npad, zero padded):
 // residues of lcomb_t(rint(A 2^sigma)).  Thread: one row, 4 columns.
-__global__ void k_res_a(QView a, int64_t npad, int64_t rpad, int sigma, int8_t* out, int64_t bstride, int nmod) {
+__global__ void k_res_a(QView a, int64_t npad, int64_t rpad, int sigma, int8_t* out, int64_t pitch, int64_t bstride,
+                        int nmod) {
   const int64_t nw = npad >> 2;
   const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (e >= rpad * nw) return;
@@ -281,12 +283,12 @@ __global__ void k_res_a(QView a, int64_t npad, int64_t rpad, int sigma, int8_t* 
 #pragma unroll
     for (int t = 0; t < 8; ++t) c[t][q] = qt8::lcomb(t, v);
   }
-  store_res(reinterpret_cast<unsigned*>(out + i * npad + k0), bstride >> 2, c, nmod);
+  store_res(reinterpret_cast<unsigned*>(out + i * pitch + k0), bstride >> 2, c, nmod);
 }
 
 // Omega (n x s) -> Ores[t*16+mu][j][k] (s x npad): residues of
 // rcomb_t(rint(Omega(k, j) 2^tau_j)).  Thread: one column j, 4 rows k.
-__global__ void k_res_om(QView om, const unsigned long long* colmax, int64_t npad, int64_t spad, int8_t* out,
+__global__ void k_res_om(QView om, const unsigned long long* colmax, int64_t npad, int64_t spad, int8_t* out, int64_t pitch,
                          int64_t bstride, ModCfg mc) {
   const int64_t nw = npad >> 2;
   const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -305,14 +307,14 @@ __global__ void k_res_om(QView om, const unsigned long long* colmax, int64_t npa
 #pragma unroll
     for (int t = 0; t < 8; ++t) c[t][q] = qt8::rcomb(t, v);
   }
-  store_res(reinterpret_cast<unsigned*>(out + j * npad + k0), bstride >> 2, c, mc.nmod);
+  store_res(reinterpret_cast<unsigned*>(out + j * pitch + k0), bstride >> 2, c, mc.nmod);
 }
 
 // Psi columns [c0, c0 + R) (l x R) -> Pres[u*16+mu][k][i] (l x Rpad): the
 // right operand of W^* = A^* Psi^*, rcomb_t(rint(conj(Psi(k, i)) 2^rho_k)),
 // stored at the batch u = kConjPerm[t] of the A residues it multiplies.
 __global__ void k_res_psi(QView ps, int64_t c0, int64_t R, int64_t rpad, int64_t lpad,
-                          const unsigned long long* rowmax, int8_t* out, int64_t bstride, ModCfg mc) {
+                          const unsigned long long* rowmax, int8_t* out, int64_t pitch, int64_t bstride, ModCfg mc) {
   const int64_t nw = rpad >> 2;
   const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (e >= lpad * nw) return;
@@ -346,7 +348,7 @@ __global__ void k_res_psi(QView ps, int64_t c0, int64_t R, int64_t rpad, int64_t
     d[6][q] = c[7][q];
     d[7][q] = c[6][q];
   }
-  store_res(reinterpret_cast<unsigned*>(out + k * rpad + i0), bstride >> 2, d, mc.nmod);
+  store_res(reinterpret_cast<unsigned*>(out + k * pitch + i0), bstride >> 2, d, mc.nmod);
 }
 
 // the signed integer whose residues mod the 16 moduli are c[mu * bstride]
@@ -501,6 +503,7 @@ __global__ void k_crt_gen(const int32_t* ci, int64_t bs, int64_t npad, QView c, 
 
 inline unsigned blocks_for(int64_t n, int threads) { return (unsigned)((n + threads - 1) / threads); }
 inline int64_t up16(int64_t x) { return (x + 15) / 16 * 16; }
+inline int64_t up128(int64_t x) { return (x + 127) / 128 * 128; }
 
 void lt_check(cublasStatus_t s, const char* what) {
   if (s != CUBLAS_STATUS_SUCCESS) fail(QLRA_ERR_CUDA, std::string("cuBLASLt ") + what + " failed (status " +
@@ -646,6 +649,15 @@ void oz_release(Ctx& c) {
 
 int64_t oz_kmax() { return KMAX; }
 
+// which kernel runs the batched residue GEMMs of the sketch: the engine's own
+// tcgen05 kernel (i8gemm.cu) or cuBLASLt's IMMA kernel; QLRA_OZ_GEMM=tcgen05|lt
+bool oz_gemm_tcgen05() {
+  const char* e = std::getenv("QLRA_OZ_GEMM");  // read per call: tests switch it between sketches
+  if (e && std::string(e) == "lt") return false;
+  if (e && std::string(e) == "tcgen05") return true;
+  return false;
+}
+
 bool oz_wanted(const Ctx& c, int64_t n, int64_t s, int64_t l) {
   if (up16(n) > KMAX || n == 0 || s == 0 || l == 0) return false;
   int engine = c.sketch_engine;
@@ -667,6 +679,7 @@ OzRun::OzRun(Ctx& c, const QView& om, const QView& ps, int64_t rows) : ctx(c), o
   OzState& s = state(c);
   n = om.rows;
   npad = up16(n);
+  npitch = up128(npad);
   // moduli: 15 (P = 2^117.2) carry every product exactly at 49-bit operand
   // scales while each int32 accumulation has K <= 2^15 terms (|X| <= K
   // 2^50 2^50 = 2^115 < P / 2): the block's rows (W^*'s K, one epoch) and n
@@ -709,8 +722,8 @@ OzRun::OzRun(Ctx& c, const QView& om, const QView& ps, int64_t rows) : ctx(c), o
     QLRA_LAUNCH_CHECK();
     count_launch();
   }
-  ores = static_cast<int8_t*>(grow(c, s.ores, (size_t)nb * spad * npad));
-  k_res_om<<<blocks_for(spad * (npad / 4), 256), 256, 0, c.stream>>>(om, om_colmax, npad, spad, ores, spad * npad,
+  ores = static_cast<int8_t*>(grow(c, s.ores, (size_t)nb * spad * npitch));
+  k_res_om<<<blocks_for(spad * (npad / 4), 256), 256, 0, c.stream>>>(om, om_colmax, npad, spad, ores, npitch, spad * npitch,
                                                                       mcfg_of(*this));
   QLRA_LAUNCH_CHECK();
   count_launch();
@@ -769,12 +782,13 @@ void OzRun::prep(int64_t pc0, const QView& ap, int buf, cudaStream_t st) {
   OzState& s = *ctx.oz;
   const int64_t R = ap.rows, rpad = up16(R);
   auto* ares = static_cast<int8_t*>(s.ares[buf].p);
-  k_res_a<<<blocks_for(rpad * (npad / 4), 128), 128, 0, st>>>(ap, npad, rpad, sigma, ares, rpad * npad, nmod);
+  k_res_a<<<blocks_for(rpad * (npad / 4), 128), 128, 0, st>>>(ap, npad, rpad, sigma, ares, npitch, rpad * npitch, nmod);
   QLRA_LAUNCH_CHECK();
   count_launch();
   if (l > 0) {
     k_res_psi<<<blocks_for(lpad * (rpad / 4), 128), 128, 0, st>>>(
-        psi, pc0, R, rpad, lpad, ps_rowmax, static_cast<int8_t*>(s.pres[buf].p), lpad * rpad, mcfg_of(*this));
+        psi, pc0, R, rpad, lpad, ps_rowmax, static_cast<int8_t*>(s.pres[buf].p), up128(rpad), lpad * up128(rpad),
+        mcfg_of(*this));
     QLRA_LAUNCH_CHECK();
     count_launch();
   }
@@ -784,25 +798,39 @@ void OzRun::prep(int64_t pc0, const QView& ap, int buf, cudaStream_t st) {
 // the context stream: before any other stream touches them).
 void OzRun::reserve(int64_t rpad, int buf) {
   OzState& s = *ctx.oz;
-  grow(ctx, s.ares[buf], (size_t)nb * rpad * npad);
-  if (l > 0) grow(ctx, s.pres[buf], (size_t)nb * lpad * rpad);
+  grow(ctx, s.ares[buf], (size_t)nb * rpad * npitch);
+  if (l > 0) grow(ctx, s.pres[buf], (size_t)nb * lpad * up128(rpad));
   if (scols > 0) grow(ctx, s.cy[buf], sizeof(int32_t) * (size_t)nb * rpad * spad);
 }
 
 // The two batched GEMMs of a prepared panel (context stream; bench timed).
 void OzRun::gemms(int64_t R, int buf) {
   OzState& s = *ctx.oz;
-  const int64_t rpad = up16(R);
+  const int64_t rpad = up16(R), rpitch = up128(rpad);
   LaunchTimer lt(ctx);
-  // Y panel: col-major C (s x Rpad, ldc spad) = Ores^T (s x npad) * Ares (npad x Rpad)
-  if (scols > 0) {
-    OzState::Plan& py = plan(s, true, spad, rpad, npad, npad, npad, spad, spad * npad, rpad * npad, rpad * spad, nb);
-    run_gemm(ctx, s, py, ores, s.ares[buf].p, s.cy[buf].p, 0);
-  }
-  // W^* (npad x l, ldc npad) += Ares (npad x Rpad) * Pres (Rpad x l)
-  if (l > 0) {
-    OzState::Plan& pw = plan(s, false, npad, lpad, rpad, npad, rpad, npad, rpad * npad, lpad * rpad, npad * lpad, nb);
-    run_gemm(ctx, s, pw, s.ares[buf].p, s.pres[buf].p, cw, epoch_rows > 0 ? 1 : 0);
+  if (oz_gemm_tcgen05()) {
+    // the engine's own tcgen05 kernel (i8gemm.cu): both products straight
+    // from the row-major residue panel
+    const auto* ar = static_cast<const int8_t*>(s.ares[buf].p);
+    // Y panel: cy[b][i][j] = sum_k Ares[b][i][k] Ores[b][j][k]
+    if (scols > 0)
+      i8gemm_batched(ctx, 0, rpad, spad, npad, ar, npitch, rpad * npitch, ores, npitch, spad * npitch,
+                     static_cast<int32_t*>(s.cy[buf].p), spad, rpad * spad, nb, 0, ctx.stream);
+    // W^*: cw[b][k][j] += sum_i Ares[b][i][j] Pres[b][k][i]
+    if (l > 0)
+      i8gemm_batched(ctx, 1, npad, lpad, rpad, ar, npitch, rpad * npitch, static_cast<const int8_t*>(s.pres[buf].p),
+                     rpitch, lpad * rpitch, cw, npad, npad * lpad, nb, epoch_rows > 0 ? 1 : 0, ctx.stream);
+  } else {
+    // Y panel: col-major C (s x Rpad, ldc spad) = Ores^T (s x npad) * Ares (npad x Rpad)
+    if (scols > 0) {
+      OzState::Plan& py = plan(s, true, spad, rpad, npad, npitch, npitch, spad, spad * npitch, rpad * npitch, rpad * spad, nb);
+      run_gemm(ctx, s, py, ores, s.ares[buf].p, s.cy[buf].p, 0);
+    }
+    // W^* (npad x l, ldc npad) += Ares (npad x Rpad) * Pres (Rpad x l)
+    if (l > 0) {
+      OzState::Plan& pw = plan(s, false, npad, lpad, rpad, npitch, rpitch, npad, rpad * npitch, lpad * rpitch, npad * lpad, nb);
+      run_gemm(ctx, s, pw, s.ares[buf].p, s.pres[buf].p, cw, epoch_rows > 0 ? 1 : 0);
+    }
   }
   lt.close(32.0 * (double)R * (double)n * (double)(scols + l), 32.0 * (double)R * (double)n,
            2.0 * nb * (double)rpad * (double)npad * (double)(scols + l), 2);
@@ -878,7 +906,7 @@ bool oz_sketch_block(Ctx& c, const QView& om, const QView& ps, const QView& bloc
     cudaGetLastError();
   }
   const double budget = std::max(0.5e9, std::min(cap, (pipelined ? 0.22 : 0.45) * (double)free_b));
-  int64_t R = (int64_t)(budget / (run.nb * (double)run.npad));
+  int64_t R = (int64_t)(budget / (run.nb * (double)run.npitch));
   R = std::max<int64_t>(256, std::min<int64_t>(R / 16 * 16, run.kcap));
   const int64_t np = (block.rows + R - 1) / R;  // equal panels (no short tail)
   R = up16((block.rows + np - 1) / np);

@@ -8,6 +8,7 @@ namespace qlra_dev {
 // true when sketch_update_rows should take the int8 engine for these shapes
 bool oz_wanted(const Ctx& c, int64_t n, int64_t s, int64_t l);
 int64_t oz_kmax();
+bool oz_gemm_tcgen05();
 const char* oz_kernel_name();
 // C = alpha op(A) op(B) + beta C on the int8 engine when the contraction is
 // long enough to pay (false: not taken, nothing launched)
@@ -23,6 +24,9 @@ struct OzRun {
   Ctx& ctx;
   QView omega, psi;  // Omega (n x s), the Psi block (l x b) of the call
   int64_t n = 0, npad = 0, scols = 0, spad = 0, l = 0, lpad = 0;
+  // row pitch of the A / Omega residues: whole 128-byte lines per row, so that
+  // the GEMMs' 128-byte operand rows (TMA boxes) never straddle two lines
+  int64_t npitch = 0;
   unsigned long long* om_colmax = nullptr;  // device: max |Omega(:, j)| bits
   unsigned long long* ps_rowmax = nullptr;  // device: max |Psi(k, :)| bits
   int8_t* ores = nullptr;                   // Omega residues (128 x s x npad)
