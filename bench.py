@@ -490,8 +490,10 @@ def main():
     if int8_engine:
         # the int8 engine (csrc/ozaki.cu): the dominant kernels are the two
         # batched int8 GEMMs of a panel (8 combinations x 16 moduli of the
-        # residues); achieved = their int8 ops / the bracket's mean CUDA-event
-        # duration, peak = int8 8192^3 GEMMs measured in this run
+        # residues), run by the engine's own tcgen05 kernel (csrc/i8gemm.cu;
+        # QLRA_OZ_GEMM=lt switches to cuBLASLt's for an A/B); achieved = their
+        # int8 ops / the bracket's mean CUDA-event duration, peak = cuBLASLt
+        # int8 8192^3 GEMMs measured in this run
         ops_launch = kst["int8_ops"] / max(1, kst["launches"])
         achieved = ops_launch / (k_ms * 1e-3) / 1e12
         peak = peaks["int8_tops"]
@@ -507,7 +509,9 @@ def main():
                                "MEASURED_PEAKS.json has no int8 entry; nominal dense 4.5 POPS: " + json.dumps(peaks),
                 "note": ("int8 engine: every real product of the sketch computed exactly in integers (Ozaki "
                          "scheme, CRT over 16 moduli) as 128 int8 GEMMs per panel (8 quaternion-product "
-                         "combinations x 16 moduli), one batched call per sketch side; a launch = one row panel: "
+                         "combinations x 16 moduli), one batched launch per sketch side of "
+                         + ("the engine's own tcgen05 kernel (csrc/i8gemm.cu)" if os.environ.get("QLRA_OZ_GEMM") != "lt"
+                            else "cuBLASLt's IMMA kernel (QLRA_OZ_GEMM=lt)") + "; a launch = one row panel: "
                          "2 * 128 * rpad * npad * (spad + lpad) int8 ops; algorithmic_tflops counts the "
                          "reference's 32 flop per quaternion MAC over the same bracket")}
     else:

@@ -162,7 +162,8 @@ const char* qlra_int8_engine_name(void);
  * i.e. the residue images of Y += A Omega (mode 0) and of W^* += A^* Psi^*
  * (mode 1) in sketch_update_rows (sketching.cpp:125-139), both read from the
  * same row-major residue panel.  Device pointers, 16-byte aligned; n, lda,
- * ldb, stride_a, stride_b multiples of 16, ldc and stride_c of 4. */
+ * ldb, stride_a, stride_b multiples of 16, ldc and stride_c of 4 (mode 1: m
+ * too -- TMA stores whole 16-byte units of C's contiguous extent). */
 int qlra_i8gemm_batched(qlra_ctx_t* ctx, int mode, int64_t m, int64_t n, int64_t k, const int8_t* a, int64_t lda,
                         int64_t stride_a, const int8_t* b, int64_t ldb, int64_t stride_b, int32_t* c, int64_t ldc,
                         int64_t stride_c, int batch, int beta);

@@ -299,6 +299,222 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   }
 }
 
+// ---------------------------------------------------------------------------
+// The same product on CTA pairs: tcgen05.mma.cta_group::2, one 256 x N tile per
+// pair of SMs (a 2-CTA cluster).  Each CTA stages its own 128 rows of A and
+// its own half of the tile's B rows (32 KB per ring slot, 6 slots); the
+// leader CTA's elected thread issues the MMAs for both SMs, whose tensor
+// cores read the two B halves from both CTAs' shared memory; each CTA's TMEM
+// holds its 128 accumulator rows and its own epilogue warps drain them.
+// Against the 1-CTA kernel: a third less L2 -> SM operand traffic and a
+// third fewer shared-memory operand reads per MMA -- energy, which is what
+// the power-capped clock of a long int8 run is made of.
+//   full[s]    leader only, 2 arrivals (each CTA's producer: expect_tx of its
+//              own 32 KB; both CTAs' TMA loads complete_tx on the leader's);
+//   empty[s]   per CTA, tcgen05.commit multicast to both;
+//   tfull[a]   per CTA, commit multicast; tempty[a] leader only, 8 arrivals
+//              (the epilogue warps of both CTAs).
+constexpr int STAGES2 = 6;
+constexpr int B2_BYTES = (BN / 2) * BK;  // 16 KB: this CTA's half of the B rows
+constexpr int SLOT2 = A_BYTES + B2_BYTES;
+static_assert(STAGES2 * SLOT2 == STAGES * SLOT, "both kernels use the same ring bytes");
+
+__device__ __forceinline__ uint32_t leader_addr(uint32_t a) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(r) : "r"(a));
+  return r;
+}
+__device__ __forceinline__ void tma3_2sm(void* dst, const CUtensorMap* map, int c0, int c1, int c2, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+      "[%5];" ::"r"(s32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void tc_commit2(uint64_t* b) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(s32(b)),
+      "h"((uint16_t)3)
+      : "memory");
+}
+__device__ __forceinline__ void tc_mma_i8_2sm(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                              uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
+    i8gemm_tc05_2sm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
+                           const __grid_constant__ CUtensorMap map_c, const Args g) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  uint8_t* ring = smem;
+  uint8_t* epi = smem + (size_t)STAGES2 * SLOT2;
+  uint64_t* full = reinterpret_cast<uint64_t*>(epi + 2 * EPI_BYTES);
+  uint64_t* empty = full + STAGES2;
+  uint64_t* tfull = empty + STAGES2;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  unsigned rank;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES2; ++s) {
+      bar_init(&full[s], 2);
+      bar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      bar_init(&tfull[s], 1);
+      bar_init(&tempty[s], 8);  // the epilogue warps of both CTAs
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(s32(tmem_slot)),
+                 "r"(TMEM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();  // the peer's barriers are initialised and its TMEM allocated
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int64_t per_batch = (int64_t)g.tiles_m * g.tiles_n;
+  const int64_t pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---- TMA producer (both CTAs): own A rows, own half of the B rows ----
+      unsigned it = 0;
+      for (int64_t t = pair; t < g.total_tiles; t += npairs) {
+        const int b = (int)(t / per_batch);
+        const int r = (int)(t - (int64_t)b * per_batch);
+        const int m0 = (r / g.tiles_n) * (2 * BM) + (int)rank * BM, n0 = (r % g.tiles_n) * BN;
+        const int nt = g.N - n0 < BN ? (int)(g.N - n0) : BN;
+        const int nb0 = n0 + (int)rank * (nt >> 1);  // the MMA reads nt / 2 B rows from each CTA
+        for (int kb = 0; kb < g.num_k; ++kb, ++it) {
+          const int s = it % STAGES2;
+          bar_wait(&empty[s], ((it / STAGES2) & 1) ^ 1);
+          const uint32_t fb = leader_addr(s32(&full[s]));
+          asm volatile("mbarrier.arrive.expect_tx.shared::cluster.b64 _, [%0], %1;" ::"r"(fb), "r"(SLOT2) : "memory");
+          uint8_t* as = ring + (size_t)s * SLOT2;
+          if (g.mode == 0)
+            tma3_2sm(as, &map_a, kb * BK, m0, b, fb);
+          else
+            tma3_2sm(as, &map_a, m0, kb * BK, b, fb);
+          tma3_2sm(as + A_BYTES, &map_b, kb * BK, nb0, b, fb);
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (lane == 0 && rank == 0) {
+      // ---- MMA issuer (leader CTA) ----
+      unsigned it = 0, lt = 0;
+      for (int64_t t = pair; t < g.total_tiles; t += npairs, ++lt) {
+        const int r = (int)(t % per_batch);
+        const int n0 = (r % g.tiles_n) * BN;
+        const int nt = g.N - n0 < BN ? (int)(g.N - n0) : BN;  // multiple of 16
+        // M = 256: M >> 4 = 16 at bit 24
+        const uint32_t idesc = (instr_desc(nt, g.mode) & ~(0x1Fu << 24)) | (16u << 24);
+        const unsigned as = lt & 1;
+        bar_wait(&tempty[as], ((lt >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem_base + as * BN;
+        for (int kb = 0; kb < g.num_k; ++kb, ++it) {
+          const int s = it % STAGES2;
+          bar_wait(&full[s], (it / STAGES2) & 1);
+          tc_fence_after();
+          const uint32_t a0 = s32(ring + (size_t)s * SLOT2), b0 = a0 + A_BYTES;
+#pragma unroll
+          for (int k = 0; k < BK / UK; ++k) {
+            const uint64_t ad = smem_desc(a0 + (g.mode == 0 ? k * UK : k * UK * BM));
+            const uint64_t bd = smem_desc(b0 + k * UK);
+            tc_mma_i8_2sm(d, ad, bd, idesc, (kb | k) != 0);
+          }
+          tc_commit2(&empty[s]);
+        }
+        tc_commit2(&tfull[as]);
+      }
+    }
+    __syncwarp();
+  } else if (warp >= 4) {
+    // ---- epilogue (both CTAs): this CTA's 128 accumulator rows ----
+    const int q = warp & 3;
+    uint8_t* wbuf = epi + q * (2 * EPI_WARP);
+    unsigned lt = 0, ch = 0;
+    for (int64_t t = pair; t < g.total_tiles; t += npairs, ++lt) {
+      const int b = (int)(t / per_batch);
+      const int r = (int)(t - (int64_t)b * per_batch);
+      const int m0 = (r / g.tiles_n) * (2 * BM) + (int)rank * BM + q * 32, n0 = (r % g.tiles_n) * BN;
+      const int nt = g.N - n0 < BN ? (int)(g.N - n0) : BN;
+      const unsigned as = lt & 1;
+      bar_wait(&tfull[as], (lt >> 1) & 1);
+      tc_fence_after();
+      for (int c0 = 0; c0 < nt; c0 += EPI_COLS, ++ch) {
+        uint32_t v[32];
+        tc_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + as * BN + c0, v);
+        if (c0 + EPI_COLS >= nt) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) {
+            const uint32_t tb = leader_addr(s32(&tempty[as]));
+            asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(tb) : "memory");
+          }
+        }
+        if (m0 >= g.M) continue;
+        uint8_t* sb = wbuf + (ch & 1) * EPI_WARP;
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        __syncwarp();
+        if (g.mode == 0) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            *reinterpret_cast<uint4*>(sb + lane * 128 + ((j ^ (lane & 7)) << 4)) =
+                make_uint4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+        } else {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) reinterpret_cast<uint32_t*>(sb)[j * 32 + lane] = v[j];
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) {
+          const int x = g.mode == 0 ? n0 + c0 : m0, y = g.mode == 0 ? m0 : n0 + c0;
+          if (g.beta)
+            asm volatile(
+                "cp.reduce.async.bulk.tensor.3d.global.shared::cta.add.tile.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
+                    &map_c),
+                "r"(x), "r"(y), "r"(b), "r"(s32(sb))
+                : "memory");
+          else
+            asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.tile.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
+                             &map_c),
+                         "r"(x), "r"(y), "r"(b), "r"(s32(sb))
+                         : "memory");
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+      }
+    }
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    __syncwarp();
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();  // neither CTA leaves while the other may still signal its barriers or read its operands
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS) : "memory");
+  }
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
     void* p = nullptr;
@@ -321,8 +537,14 @@ void make_map(CUtensorMap* m, const int8_t* base, int64_t inner, int64_t rows, i
   const cuuint64_t strides[2] = {(cuuint64_t)ld, (cuuint64_t)stride};
   const cuuint32_t box[3] = {(cuuint32_t)BK, (cuuint32_t)box_rows, 1};
   const cuuint32_t es[3] = {1, 1, 1};
+  static const CUtensorMapL2promotion promo = [] {
+    const char* e = std::getenv("QLRA_I8_L2PROMO");  // 0 none, 1 64B, 2 128B, 3 256B
+    const int v = e ? std::atoi(e) : 3;
+    return v == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE : v == 1 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+           : v == 2 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+  }();
   const CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<int8_t*>(base), dims, strides, box, es,
-                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, promo,
                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) fail(QLRA_ERR_CUDA, "i8gemm: cuTensorMapEncodeTiled failed (operand layout)");
 }
@@ -345,18 +567,21 @@ void make_map_c(CUtensorMap* m, int32_t* base, int64_t inner, int64_t rows, int6
 }  // namespace
 
 const char* i8gemm_kernel_name() {
-  return "i8gemm_tc05_kernel (tcgen05.mma kind::i8 128xNx32, TMA 128B-swizzled 4-slot ring, 2 TMEM accumulator "
-         "stages, TMA store / reduce-add epilogue, persistent)";
+  return "i8gemm_tc05_2sm_kernel (tcgen05.mma.cta_group::2 kind::i8 256xNx32 on CTA pairs, TMA 128B-swizzled 6-slot "
+         "ring, 2 TMEM accumulator stages, TMA store / reduce-add epilogue, persistent; i8gemm_tc05_kernel: the "
+         "1-CTA 128xNx32 form for M <= 128)";
 }
 
 void i8gemm_batched(Ctx& c, int mode, int64_t M, int64_t N, int64_t K, const int8_t* A, int64_t lda, int64_t stride_a,
                     const int8_t* B, int64_t ldb, int64_t stride_b, int32_t* C, int64_t ldc, int64_t stride_c,
-                    int batch, int beta, cudaStream_t stream) {
+                    int batch, int beta, cudaStream_t stream, int ctas) {
   if (M <= 0 || N <= 0 || batch <= 0) return;
   if (mode != 0 && mode != 1) fail(QLRA_ERR_PARAMETER, "i8gemm: mode must be 0 or 1");
   if (N % 16 || lda % 16 || ldb % 16 || stride_a % 16 || stride_b % 16 || ldc % 4 || stride_c % 4 ||
       (reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B) | reinterpret_cast<uintptr_t>(C)) % 16)
     fail(QLRA_ERR_PARAMETER, "i8gemm: N, leading dimensions and batch strides must be multiples of 16 (ldc of 4)");
+  // TMA stores move whole 16-byte units: the contiguous extent of C must be one
+  if (mode == 1 && M % 4) fail(QLRA_ERR_PARAMETER, "i8gemm: mode 1 needs M to be a multiple of 4");
   if (K <= 0) {
     if (!beta)
       for (int b = 0; b < batch; ++b)
@@ -366,7 +591,9 @@ void i8gemm_batched(Ctx& c, int mode, int64_t M, int64_t N, int64_t K, const int
   }
   static const bool attr_set = [] {
     return cudaFuncSetAttribute(i8gemm_tc05_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES) ==
-           cudaSuccess;
+               cudaSuccess &&
+           cudaFuncSetAttribute(i8gemm_tc05_2sm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)SMEM_BYTES) == cudaSuccess;
   }();
   if (!attr_set) fail(QLRA_ERR_CUDA, "i8gemm: cannot reserve the shared-memory ring");
   CUtensorMap ma, mb, mc;
@@ -378,7 +605,6 @@ void i8gemm_batched(Ctx& c, int mode, int64_t M, int64_t N, int64_t K, const int
     make_map(&ma, A, K, M, batch, lda, stride_a, BM);  // rows m, K inner
   else
     make_map(&ma, A, M, K, batch, lda, stride_a, BM);  // rows k, M inner (box: 128 m x 128 k)
-  make_map(&mb, B, K, N, batch, ldb, stride_b, BN);
   Args g{};
   g.M = M, g.N = N, g.K = K;
   g.batch = batch, g.beta = beta, g.mode = mode;
@@ -386,7 +612,12 @@ void i8gemm_batched(Ctx& c, int mode, int64_t M, int64_t N, int64_t K, const int
     const char* e = std::getenv("QLRA_I8_DEBUG");
     g.dbg = e ? std::atoi(e) : 0;
   }
-  g.tiles_m = (int)((M + BM - 1) / BM);
+  // CTA pairs (256-row tiles) unless M fits one CTA's rows; QLRA_I8_CTAS=1|2 overrides
+  bool two = ctas == 0 ? M > BM : ctas == 2;
+  if (const char* e = std::getenv("QLRA_I8_CTAS")) two = std::atoi(e) == 2;
+  const int tm = two ? 2 * BM : BM;
+  make_map(&mb, B, K, N, batch, ldb, stride_b, two ? BN / 2 : BN);
+  g.tiles_m = (int)((M + tm - 1) / tm);
   g.tiles_n = (int)((N + BN - 1) / BN);
   g.num_k = (int)((K + BK - 1) / BK);
   g.total_tiles = (int64_t)batch * g.tiles_m * g.tiles_n;
@@ -396,8 +627,13 @@ void i8gemm_batched(Ctx& c, int mode, int64_t M, int64_t N, int64_t K, const int
     cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
     return n;
   }();
-  const unsigned grid = (unsigned)std::min<int64_t>(g.total_tiles, sms);
-  i8gemm_tc05_kernel<<<grid, NTHREADS, SMEM_BYTES, stream>>>(ma, mb, mc, g);
+  if (two) {
+    const unsigned grid = 2 * (unsigned)std::min<int64_t>(g.total_tiles, sms / 2);
+    i8gemm_tc05_2sm_kernel<<<grid, NTHREADS, SMEM_BYTES, stream>>>(ma, mb, mc, g);
+  } else {
+    const unsigned grid = (unsigned)std::min<int64_t>(g.total_tiles, sms);
+    i8gemm_tc05_kernel<<<grid, NTHREADS, SMEM_BYTES, stream>>>(ma, mb, mc, g);
+  }
   QLRA_LAUNCH_CHECK();
   count_launch();
   (void)c;

@@ -5,7 +5,7 @@
 // qmat_mul_accumulate_ordered, qmatrix.cpp:203-242), for the shapes where it
 // is faster (oz_wanted).  FP64 has no tcgen05 kind on sm_100 (DMMA.8x8x4 at
 // 37 TFLOP/s is the FP64 tensor ceiling), but INT8 does (tcgen05.mma
-// kind::i8, ~3.5 POPS through cuBLASLt's sm_100 IMMA kernels).  So every
+// kind::i8, 2.6-3 POPS sustained at the board's power cap).  So every
 // real product of the sketch is computed EXACTLY in integers (the Ozaki
 // scheme, CRT form) and rounded once at the end:
 //
@@ -17,8 +17,11 @@
 //    GEMMs of plane combinations (exact integers < 2^53 after scaling);
 //  * residues: each combination reduced modulo 16 pairwise-coprime moduli
 //    p <= 256 (symmetric int8); the 8 x 16 = 128 residue products are ONE
-//    strided-batched int8 x int8 -> int32 GEMM (exact while K 128^2 < 2^31,
-//    i.e. K < 2^17 rows or columns per int32 accumulation);
+//    batched int8 x int8 -> int32 GEMM per sketch side (exact while K 128^2
+//    < 2^31, i.e. K < 2^17 rows or columns per int32 accumulation), run by
+//    the engine's own tcgen05 kernel (i8gemm.cu; cuBLASLt's IMMA kernel is
+//    kept as the A/B reference, QLRA_OZ_GEMM=lt, and for the general
+//    long-K product oz_gemm_try);
 //  * recovery: the CRT in 128-bit integers (P = prod p = 2^124.7 > 2 K
 //    2^106 for 16 moduli; 15 moduli and 49-bit scales when K <= 2^15), the 8 products combined into the quaternion planes exactly in
 //    int128, one rounding to double, scaled back by powers of two.
@@ -650,12 +653,12 @@ void oz_release(Ctx& c) {
 int64_t oz_kmax() { return KMAX; }
 
 // which kernel runs the batched residue GEMMs of the sketch: the engine's own
-// tcgen05 kernel (i8gemm.cu) or cuBLASLt's IMMA kernel; QLRA_OZ_GEMM=tcgen05|lt
+// tcgen05 kernel (i8gemm.cu, the default) or cuBLASLt's IMMA kernel, kept as
+// the A/B reference (QLRA_OZ_GEMM=lt; bitwise the same sketch)
 bool oz_gemm_tcgen05() {
   const char* e = std::getenv("QLRA_OZ_GEMM");  // read per call: tests switch it between sketches
   if (e && std::string(e) == "lt") return false;
-  if (e && std::string(e) == "tcgen05") return true;
-  return false;
+  return true;
 }
 
 bool oz_wanted(const Ctx& c, int64_t n, int64_t s, int64_t l) {
@@ -728,6 +731,7 @@ OzRun::OzRun(Ctx& c, const QView& om, const QView& ps, int64_t rows) : ctx(c), o
   QLRA_LAUNCH_CHECK();
   count_launch();
   cw = static_cast<int32_t*>(grow(c, s.cw, sizeof(int32_t) * (size_t)nb * npad * lpad));
+  gemm_ops = 2.0 * nb * (double)rows * (double)npad * (double)(spad + lpad);
 }
 
 // max |A| of a view on `stream`, into panel slot `slot` (device) and its
@@ -812,14 +816,19 @@ void OzRun::gemms(int64_t R, int buf) {
     // the engine's own tcgen05 kernel (i8gemm.cu): both products straight
     // from the row-major residue panel
     const auto* ar = static_cast<const int8_t*>(s.ares[buf].p);
+    // CTA pairs, except on sketches long enough to sit at the board's power
+    // cap (C4: ~0.12 s of back-to-back int8 GEMMs): there the pair kernel's
+    // higher per-clock draw pulls the clock to ~0.95 GHz, which the stages
+    // after the sketch inherit (measured: DESIGN 3, int8 engine)
+    const int ctas = gemm_ops >= 1e14 ? 1 : 2;
     // Y panel: cy[b][i][j] = sum_k Ares[b][i][k] Ores[b][j][k]
     if (scols > 0)
       i8gemm_batched(ctx, 0, rpad, spad, npad, ar, npitch, rpad * npitch, ores, npitch, spad * npitch,
-                     static_cast<int32_t*>(s.cy[buf].p), spad, rpad * spad, nb, 0, ctx.stream);
+                     static_cast<int32_t*>(s.cy[buf].p), spad, rpad * spad, nb, 0, ctx.stream, ctas);
     // W^*: cw[b][k][j] += sum_i Ares[b][i][j] Pres[b][k][i]
     if (l > 0)
       i8gemm_batched(ctx, 1, npad, lpad, rpad, ar, npitch, rpad * npitch, static_cast<const int8_t*>(s.pres[buf].p),
-                     rpitch, lpad * rpitch, cw, npad, npad * lpad, nb, epoch_rows > 0 ? 1 : 0, ctx.stream);
+                     rpitch, lpad * rpitch, cw, npad, npad * lpad, nb, epoch_rows > 0 ? 1 : 0, ctx.stream, ctas);
   } else {
     // Y panel: col-major C (s x Rpad, ldc spad) = Ores^T (s x npad) * Ares (npad x Rpad)
     if (scols > 0) {
@@ -1100,8 +1109,12 @@ double oz_measure_int8_peak(Ctx& c, double ms) {
 }
 
 const char* oz_kernel_name() {
-  return "int8 tensor-core sketch (Ozaki/CRT: 16 moduli x 8 combinations, cuBLASLt sm_100 IMMA batched GEMM "
-         "+ residue/CRT kernels)";
+  return oz_gemm_tcgen05()
+             ? "int8 tensor-core sketch (Ozaki/CRT: 15-16 moduli x 8 combinations; residue GEMMs on the engine's own "
+               "tcgen05 kernel i8gemm_tc05[_2sm]_kernel: TMA ring, tcgen05.mma kind::i8, TMEM accumulators, TMA "
+               "store / reduce-add epilogue; + residue/CRT kernels)"
+             : "int8 tensor-core sketch (Ozaki/CRT: 15-16 moduli x 8 combinations, cuBLASLt sm_100 IMMA batched GEMM "
+               "[QLRA_OZ_GEMM=lt] + residue/CRT kernels)";
 }
 
 }  // namespace qlra_dev

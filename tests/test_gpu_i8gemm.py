@@ -59,24 +59,39 @@ def ctx():
     c.close()
 
 
+@pytest.fixture(params=["pairs", "single"])
+def ctas(request):
+    """Both kernels: CTA pairs (tcgen05.mma.cta_group::2, the default above 128
+    rows) and the 1-CTA form forced on the same shapes."""
+    old = os.environ.get("QLRA_I8_CTAS")
+    os.environ["QLRA_I8_CTAS"] = "2" if request.param == "pairs" else "1"
+    yield request.param
+    if old is None:
+        os.environ.pop("QLRA_I8_CTAS", None)
+    else:
+        os.environ["QLRA_I8_CTAS"] = old
+
+
 @pytest.mark.parametrize("mode", [0, 1])
 @pytest.mark.parametrize("beta", [0, 1])
-def test_i8gemm_one_tile(ctx, mode, beta):
+def test_i8gemm_one_tile(ctx, ctas, mode, beta):
     run(ctx, mode, 128, 256, 128, 1, beta)
     run(ctx, mode, 128, 256, 512, 2, beta, seed=1)
 
 
 @pytest.mark.parametrize("mode", [0, 1])
-def test_i8gemm_ragged_and_clipped(ctx, mode):
+def test_i8gemm_ragged_and_clipped(ctx, ctas, mode):
     # M, K off the tile, N a multiple of 16 below / above one tile, padded lds
     run(ctx, mode, 112, 112, 96, 3, 0, pad_m=16, pad_k=32, seed=2)
     run(ctx, mode, 1000, 208, 6000, 2, 1, pad_m=0, pad_k=16, seed=3)
     run(ctx, mode, 400, 1008, 784, 2, 1, pad_m=16, pad_k=0, seed=4)
     run(ctx, mode, 16, 16, 16, 5, 0, seed=5)
+    run(ctx, mode, 300, 240, 200, 3, 1, seed=8)   # 240 columns: 120 B rows per CTA of a pair
+    run(ctx, mode, 132, 48, 4000, 2, 0, seed=9)   # the pair's second CTA holds four valid rows
 
 
 @pytest.mark.parametrize("mode", [0, 1])
-def test_i8gemm_many_tiles_persistent(ctx, mode):
+def test_i8gemm_many_tiles_persistent(ctx, ctas, mode):
     # more tiles than SMs: the persistent loop, ring and TMEM stage phases wrap
     run(ctx, mode, 2048, 512, 1024, 15, 0, seed=6)
     run(ctx, mode, 1536, 272, 2000, 9, 1, seed=7)

@@ -54,6 +54,17 @@ def main():
         case(ctx, 1, 27136, 1008, 31424, 2, 1, "W* K x4")
         return
     nb = 30
+    if len(sys.argv) > 1 and sys.argv[1] == "pairs":
+        import os
+        for ctas in ("1", "2"):
+            os.environ["QLRA_I8_CTAS"] = ctas
+            for dbg in ("2", "0"):
+                os.environ["QLRA_I8_DEBUG"] = dbg
+                case(ctx, 1, 27136, 1008, 7936, 30, 1, f"W* ctas={ctas} dbg={dbg}")
+                case(ctx, 1, 27136, 1024, 7936, 30, 1, f"W* N=1024 ctas={ctas} dbg={dbg}")
+                case(ctx, 0, 7856, 512, 27136, 30, 0, f"Y ctas={ctas} dbg={dbg}")
+                case(ctx, 1, 8192, 8192, 8192, 4, 0, f"square MN ctas={ctas} dbg={dbg}")
+        return
     if len(sys.argv) > 1 and sys.argv[1] == "ksweep":
         import os
         for dbg in ("2", "0"):
