@@ -1052,11 +1052,14 @@ bool oz_gemm_try(Ctx& c, int op_a, int op_b, double alpha, const QView& A, const
     QLRA_LAUNCH_CHECK();
     count_launch();
   }
-  const int64_t nch = (K + KMAX - 1) / KMAX, kc = (K + nch - 1) / nch, kpad = up16(kc);
+  const bool tc05 = oz_gemm_tcgen05();
+  // K pad: whole 128-byte residue rows for the tcgen05 kernel's TMA boxes (the pad is zero)
+  const int64_t nch = (K + KMAX - 1) / KMAX, kc = (K + nch - 1) / nch, kpad = tc05 ? up128(kc) : up16(kc);
   DeviceBuffer lres(c, (size_t)NB * mpad * kpad), rres(c, (size_t)NB * npad * kpad);
-  DeviceBuffer ci(c, sizeof(int32_t) * (size_t)NB * mpad * npad), ws(c, s.lt_ws_bytes);
+  DeviceBuffer ci(c, sizeof(int32_t) * (size_t)NB * mpad * npad), ws(c, tc05 ? 0 : s.lt_ws_bytes);
   // col-major C (npad x mpad) = Rres^T (npad x kpad) * Lres (kpad x mpad)
-  OzState::Plan& pl = plan(s, true, npad, mpad, kpad, kpad, kpad, npad, npad * kpad, mpad * kpad, mpad * npad, NB);
+  OzState::Plan* pl = tc05 ? nullptr
+                           : &plan(s, true, npad, mpad, kpad, kpad, kpad, npad, npad * kpad, mpad * kpad, mpad * npad, NB);
   for (int64_t ch = 0; ch < nch; ++ch) {
     const int64_t k0 = ch * kc, kn = std::min(kc, K - k0);
     k_res_rows<true><<<blocks_for(mpad * (kpad / 4), 128), 128, 0, c.stream>>>(L, lconj, lmax, k0, kn, kpad, mpad,
@@ -1067,7 +1070,11 @@ bool oz_gemm_try(Ctx& c, int op_a, int op_b, double alpha, const QView& A, const
     QLRA_LAUNCH_CHECK();
     count_launch();
     count_launch();
-    run_gemm(c, s, pl, rres.ptr, lres.ptr, ci.ptr, 0, ws.ptr);
+    if (tc05)  // ci[b][m][n] = sum_k Lres[b][m][k] Rres[b][n][k]
+      i8gemm_batched(c, 0, mpad, npad, kpad, lres.as<int8_t>(), kpad, mpad * kpad, rres.as<int8_t>(), kpad,
+                     npad * kpad, ci.as<int32_t>(), npad, mpad * npad, NB, 0, c.stream);
+    else
+      run_gemm(c, s, *pl, rres.ptr, lres.ptr, ci.ptr, 0, ws.ptr);
     k_crt_gen<<<blocks_for(M * N, 128), 128, 0, c.stream>>>(ci.as<int32_t>(), mpad * npad, npad, C, lmax, rmax,
                                                              alpha, ch == 0 ? beta : 1.0);
     QLRA_LAUNCH_CHECK();

@@ -171,6 +171,22 @@ def test_int8_general_product_vs_oracle(ctx, op_a, op_b):
         outs.append(out)
     assert torch.equal(outs[0], outs[1])
     assert rel_diff(host(outs[0]), ref) < 1e-14
+    # the residue GEMMs through cuBLASLt instead of the engine's tcgen05 kernel:
+    # exact integer products, so bitwise the same quaternion result
+    import os
+    old = os.environ.get("QLRA_OZ_GEMM")
+    os.environ["QLRA_OZ_GEMM"] = "lt"
+    try:
+        out_lt = dev(c0)
+        with engine(ctx, "int8"):
+            Q.qmat_mul(dev(a), dev(b), op_a=op_a, op_b=op_b, alpha=0.5, beta=-2.0, out=out_lt, ctx=ctx)
+        ctx.synchronize()
+    finally:
+        if old is None:
+            os.environ.pop("QLRA_OZ_GEMM", None)
+        else:
+            os.environ["QLRA_OZ_GEMM"] = old
+    assert torch.equal(outs[0], out_lt)
     out_d = dev(c0)
     with engine(ctx, "dmma"):
         Q.qmat_mul(dev(a), dev(b), op_a=op_a, op_b=op_b, alpha=0.5, beta=-2.0, out=out_d, ctx=ctx)

@@ -1,5 +1,8 @@
 """Diagnostic timings of the tcgen05 int8 GEMM: mode / beta / K variations at
-C4-like tile counts (python tools/i8gemm_probe.py)."""
+C4-like tile counts (python tools/i8gemm_probe.py [ksweep|pairs|ncu]).  The
+QLRA_I8_DEBUG settings below (1: no TMA stores, 2: no staging either) were a
+temporary kernel knob used for DESIGN 3's epilogue-cost numbers; the shipped
+kernel ignores it."""
 import sys
 import time
 
