@@ -63,7 +63,7 @@ constexpr size_t SMEM_BYTES = 1024 /* alignment slack */ + (size_t)STAGES * SLOT
 
 struct Args {
   int64_t M, N, K;
-  int batch, beta, mode, pf;
+  int batch, beta, mode;
   int tiles_m, tiles_n, num_k;
   int64_t total_tiles;
 };
@@ -93,12 +93,6 @@ __device__ __forceinline__ void tma3(void* dst, const CUtensorMap* map, int c0, 
           s32(dst)),
       "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(s32(bar))
       : "memory");
-}
-// L2 prefetch of a box (no shared-memory destination, no barrier)
-__device__ __forceinline__ void tma3_prefetch(const CUtensorMap* map, int c0, int c1, int c2) {
-  asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(map), "r"(c0), "r"(c1),
-               "r"(c2)
-               : "memory");
 }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
@@ -199,15 +193,6 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           else
             tma3(as, &map_a, m0, kb * BK, b, &full[s]);
           tma3(as + A_BYTES, &map_b, kb * BK, n0, b, &full[s]);
-          // the streamed operand (A: each tile row is read once from DRAM, by
-          // its n-tile siblings together): the first sibling pulls it into L2
-          // g.pf k-blocks ahead, so the ring's loads see L2, not DRAM, latency
-          if (g.pf > 0 && n0 == 0 && kb + g.pf < g.num_k) {
-            if (g.mode == 0)
-              tma3_prefetch(&map_a, (kb + g.pf) * BK, m0, b);
-            else
-              tma3_prefetch(&map_a, m0, (kb + g.pf) * BK, b);
-          }
         }
       }
     }
@@ -426,12 +411,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
           else
             tma3_2sm(as, &map_a, m0, kb * BK, b, fb);
           tma3_2sm(as + A_BYTES, &map_b, kb * BK, nb0, b, fb);
-          if (g.pf > 0 && n0 == 0 && kb + g.pf < g.num_k) {  // as in the 1-CTA producer
-            if (g.mode == 0)
-              tma3_prefetch(&map_a, (kb + g.pf) * BK, m0, b);
-            else
-              tma3_prefetch(&map_a, m0, (kb + g.pf) * BK, b);
-          }
         }
       }
     }
@@ -628,10 +607,6 @@ void i8gemm_batched(Ctx& c, int mode, int64_t M, int64_t N, int64_t K, const int
   Args g{};
   g.M = M, g.N = N, g.K = K;
   g.batch = batch, g.beta = beta, g.mode = mode;
-  {
-    const char* e = std::getenv("QLRA_I8_PREFETCH");  // k-blocks of L2 prefetch distance for A (0: off)
-    g.pf = e ? std::atoi(e) : 0;
-  }
   // CTA pairs (256-row tiles) unless M fits one CTA's rows; QLRA_I8_CTAS=1|2 overrides
   bool two = ctas == 0 ? M > BM : ctas == 2;
   if (const char* e = std::getenv("QLRA_I8_CTAS")) two = std::atoi(e) == 2;
