@@ -35,6 +35,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <atomic>
 #include <cstdint>
 #include <cstdlib>
 
@@ -588,13 +589,23 @@ void i8gemm_batched(Ctx& c, int mode, int64_t M, int64_t N, int64_t K, const int
                                     (size_t)(mode == 0 ? N : M) * 4, (size_t)(mode == 0 ? M : N), stream));
     return;
   }
-  static const bool attr_set = [] {
-    return cudaFuncSetAttribute(i8gemm_tc05_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES) ==
-               cudaSuccess &&
-           cudaFuncSetAttribute(i8gemm_tc05_2sm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)SMEM_BYTES) == cudaSuccess;
-  }();
-  if (!attr_set) fail(QLRA_ERR_CUDA, "i8gemm: cannot reserve the shared-memory ring");
+  // per device (one process may drive several): the kernels' shared-memory
+  // opt-in and the SM count
+  struct DevInfo {
+    std::atomic<int> sms{0};
+  };
+  static DevInfo devs[64];
+  DevInfo& di = devs[c.device & 63];
+  int sms = di.sms.load(std::memory_order_acquire);
+  if (sms == 0) {
+    if (cudaFuncSetAttribute(i8gemm_tc05_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES) !=
+            cudaSuccess ||
+        cudaFuncSetAttribute(i8gemm_tc05_2sm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES) !=
+            cudaSuccess)
+      fail(QLRA_ERR_CUDA, "i8gemm: cannot reserve the shared-memory ring");
+    QLRA_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device));
+    di.sms.store(sms, std::memory_order_release);
+  }
   CUtensorMap ma, mb, mc;
   if (mode == 0)
     make_map_c(&mc, C, N, M, batch, ldc, stride_c, EPI_COLS, 32, true);  // [m][n], swizzled staging
@@ -616,12 +627,6 @@ void i8gemm_batched(Ctx& c, int mode, int64_t M, int64_t N, int64_t K, const int
   g.tiles_n = (int)((N + BN - 1) / BN);
   g.num_k = (int)((K + BK - 1) / BK);
   g.total_tiles = (int64_t)batch * g.tiles_m * g.tiles_n;
-  static const int sms = [] {
-    int dev = 0, n = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    return n;
-  }();
   if (two) {
     const unsigned grid = 2 * (unsigned)std::min<int64_t>(g.total_tiles, sms / 2);
     i8gemm_tc05_2sm_kernel<<<grid, NTHREADS, SMEM_BYTES, stream>>>(ma, mb, mc, g);
@@ -631,7 +636,6 @@ void i8gemm_batched(Ctx& c, int mode, int64_t M, int64_t N, int64_t K, const int
   }
   QLRA_LAUNCH_CHECK();
   count_launch();
-  (void)c;
 }
 
 }  // namespace qlra_dev
