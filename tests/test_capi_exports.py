@@ -74,3 +74,22 @@ def test_sketch_file_dims_validates_before_allocating(tmp_path):
         f.seek(6 + 72 + 24 + 6)
         f.write(struct.pack("<Q", 1 << 60))
     assert L.qlra_sketch_file_dims(str(p).encode(), dims) == 6
+
+
+def test_residue_gemm_kernel_is_tcgen05_and_tma():
+    """The int8 engine's residue GEMM (csrc/i8gemm.cu) is the repo's own
+    tcgen05 kernel: its sm_100a SASS holds the int8 UMMA (UTCIMMA, 1-CTA and
+    .2CTA), TMA loads (UTMALDG), TMA stores and reduce-adds (UTMASTG /
+    UTMAREDG.ADD), TMEM loads (LDTM) and tcgen05.commit (UTCBAR) -- checked
+    on the object nvcc built here, no GPU needed."""
+    import shutil
+    import subprocess
+    build.build()
+    obj = os.path.join(build.BUILD, "i8gemm.cu.o")
+    assert os.path.exists(obj)
+    cuobjdump = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    sass = subprocess.run([cuobjdump, "-sass", obj], capture_output=True, text=True, check=True).stdout
+    assert "sm_100a" in sass
+    for mnemonic in ("UTCIMMA", "UTCIMMA.2CTA", "UTMALDG.3D", "UTMASTG.3D", "UTMAREDG.3D.ADD", "LDTM.x32",
+                     "UTCBAR", "UTCBAR.2CTA.MULTICAST", "SYNCS.PHASECHK.TRANS64.TRYWAIT"):
+        assert mnemonic in sass, mnemonic
