@@ -65,6 +65,10 @@ constexpr size_t SMEM_BYTES = 1024 /* alignment slack */ + (size_t)STAGES * SLOT
 struct Args {
   int64_t M, N, K;
   int batch, beta, mode;
+  // tile-row rendezvous of the n-tile siblings (0: off): sync[row] counts the
+  // producers that reached the row, sib of them per row
+  unsigned* sync;
+  unsigned sib;
   int tiles_m, tiles_n, num_k;
   int64_t total_tiles;
 };
@@ -139,6 +143,23 @@ __device__ __forceinline__ uint32_t instr_desc(int n, int a_mn_major) {
          ((uint32_t)(BM >> 4) << 24);
 }
 
+// The n-tile siblings of a tile row (2 or 4 CTAs, or CTA pairs, running the
+// row together) read the same A k-blocks and share them through L2, which
+// holds ~45 us of the operand stream.  Nothing else ties them together: a
+// sibling that falls behind by more than that re-reads A from DRAM (measured:
+// 2x the DRAM reads on C3's W* product and on long-K tiles), which slows all
+// of them and it never catches up.  So the siblings' producers meet at every
+// tile start on a counter in global memory (all CTAs of the persistent grid
+// are resident, so the wait is bounded by one tile).
+__device__ __forceinline__ void sibling_rendezvous(unsigned* cnt, unsigned sib) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(cnt) : "memory");
+  unsigned v;
+  do {
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(cnt) : "memory");
+    if (v < sib) __nanosleep(64);
+  } while (v < sib);
+}
+
 __global__ void __launch_bounds__(NTHREADS, 1)
     i8gemm_tc05_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                        const __grid_constant__ CUtensorMap map_c, const Args g) {
@@ -184,6 +205,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         const int b = (int)(t / per_batch);
         const int r = (int)(t - (int64_t)b * per_batch);
         const int m0 = (r / g.tiles_n) * BM, n0 = (r % g.tiles_n) * BN;
+        if (g.sib) sibling_rendezvous(g.sync + t / g.tiles_n, g.sib);
         for (int kb = 0; kb < g.num_k; ++kb, ++it) {
           const int s = it % STAGES;
           bar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
@@ -401,6 +423,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
         const int m0 = (r / g.tiles_n) * (2 * BM) + (int)rank * BM, n0 = (r % g.tiles_n) * BN;
         const int nt = g.N - n0 < BN ? (int)(g.N - n0) : BN;
         const int nb0 = n0 + (int)rank * (nt >> 1);  // the MMA reads nt / 2 B rows from each CTA
+        if (g.sib) sibling_rendezvous(g.sync + t / g.tiles_n, g.sib);
         for (int kb = 0; kb < g.num_k; ++kb, ++it) {
           const int s = it % STAGES2;
           bar_wait(&empty[s], ((it / STAGES2) & 1) ^ 1);
@@ -627,14 +650,31 @@ void i8gemm_batched(Ctx& c, int mode, int64_t M, int64_t N, int64_t K, const int
   g.tiles_n = (int)((N + BN - 1) / BN);
   g.num_k = (int)((K + BK - 1) / BK);
   g.total_tiles = (int64_t)batch * g.tiles_m * g.tiles_n;
-  if (two) {
-    const unsigned grid = 2 * (unsigned)std::min<int64_t>(g.total_tiles, sms / 2);
-    i8gemm_tc05_2sm_kernel<<<grid, NTHREADS, SMEM_BYTES, stream>>>(ma, mb, mc, g);
-  } else {
-    const unsigned grid = (unsigned)std::min<int64_t>(g.total_tiles, sms);
-    i8gemm_tc05_kernel<<<grid, NTHREADS, SMEM_BYTES, stream>>>(ma, mb, mc, g);
+  // CTAs (or pairs) in flight, and the sibling rendezvous: persistent grids
+  // whose size is a multiple of the row's 2 or 4 n-tiles (so that a row's
+  // siblings always run in the same sweep), tiles long enough to drift
+  int64_t units = two ? sms / 2 : sms;
+  bool rendezvous = (g.tiles_n == 2 || g.tiles_n == 4) && g.num_k >= 16;
+  if (const char* e = std::getenv("QLRA_I8_SIBSYNC")) rendezvous = rendezvous && std::atoi(e) != 0;
+  if (rendezvous) units = units / g.tiles_n * g.tiles_n;
+  if (g.total_tiles < units) rendezvous = false, units = g.total_tiles;
+  unsigned* sync = nullptr;
+  g.sync = nullptr;
+  g.sib = 0;
+  if (rendezvous) {
+    const size_t bytes = sizeof(unsigned) * (size_t)(g.total_tiles / g.tiles_n);
+    QLRA_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&sync), bytes, stream));
+    QLRA_CUDA(cudaMemsetAsync(sync, 0, bytes, stream));
+    g.sync = sync;
+    g.sib = (unsigned)g.tiles_n * (two ? 2u : 1u);  // every CTA's producer arrives
   }
-  QLRA_LAUNCH_CHECK();
+  if (two)
+    i8gemm_tc05_2sm_kernel<<<2 * (unsigned)units, NTHREADS, SMEM_BYTES, stream>>>(ma, mb, mc, g);
+  else
+    i8gemm_tc05_kernel<<<(unsigned)units, NTHREADS, SMEM_BYTES, stream>>>(ma, mb, mc, g);
+  const cudaError_t le = cudaGetLastError();
+  if (sync) cudaFreeAsync(sync, stream);
+  cuda_check(le, "kernel launch");
   count_launch();
 }
 
