@@ -28,7 +28,11 @@
 //                      SM); TMA clips the ragged edges.  Overlapped with the
 //                      next tile's MMAs through the second TMEM stage.
 // Tiles are ordered (batch, m, n) with n fastest so that the CTAs running
-// together share an A tile in L2 and the batch's B operand stays resident.
+// together share an A tile row in L2 and the batch's B operand stays
+// resident; the producers of a row's n-tile siblings meet at every tile start
+// (sibling_rendezvous) so that they stay within the L2's residency of each
+// other.  The CTA-pair form below (tcgen05.mma.cta_group::2) is the one the
+// engine uses; this 1-CTA form serves M <= 128 and QLRA_I8_CTAS=1.
 //
 // Integer arithmetic: the result is exact and independent of the tiling, so
 // it is bitwise equal to cuBLASLt's on the same residues (tests/test_gpu_i8gemm.py).

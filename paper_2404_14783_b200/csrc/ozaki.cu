@@ -731,7 +731,6 @@ OzRun::OzRun(Ctx& c, const QView& om, const QView& ps, int64_t rows) : ctx(c), o
   QLRA_LAUNCH_CHECK();
   count_launch();
   cw = static_cast<int32_t*>(grow(c, s.cw, sizeof(int32_t) * (size_t)nb * npad * lpad));
-  gemm_ops = 2.0 * nb * (double)rows * (double)npad * (double)(spad + lpad);
 }
 
 // max |A| of a view on `stream`, into panel slot `slot` (device) and its
@@ -816,11 +815,9 @@ void OzRun::gemms(int64_t R, int buf) {
     // the engine's own tcgen05 kernel (i8gemm.cu): both products straight
     // from the row-major residue panel
     const auto* ar = static_cast<const int8_t*>(s.ares[buf].p);
-    // CTA pairs, except on sketches long enough to sit at the board's power
-    // cap (C4: ~0.12 s of back-to-back int8 GEMMs): there the pair kernel's
-    // higher per-clock draw pulls the clock to ~0.95 GHz, which the stages
-    // after the sketch inherit (measured: DESIGN 3, int8 engine)
-    const int ctas = gemm_ops >= 1e14 ? 1 : 2;
+    // CTA pairs (tcgen05.mma.cta_group::2) at every size: with the siblings'
+    // tile-row rendezvous they beat the 1-CTA form on C2-C4 (DESIGN 3)
+    const int ctas = 2;
     // Y panel: cy[b][i][j] = sum_k Ares[b][i][k] Ores[b][j][k]
     if (scols > 0)
       i8gemm_batched(ctx, 0, rpad, spad, npad, ar, npitch, rpad * npitch, ores, npitch, spad * npitch,

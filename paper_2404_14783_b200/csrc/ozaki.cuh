@@ -33,7 +33,6 @@ struct OzRun {
   int32_t* cw = nullptr;                    // W^* products (128 x l x npad), int32
   int nmod = 16, tab = 0, beta = 52, nb = 128;  // moduli, CRT table, operand bits, batch (8 nmod)
   int64_t kcap = 0;  // rows per int32 accumulation (epoch)
-  double gemm_ops = 0.0;  // int8 ops of the whole call's residue GEMMs (picks the GEMM kernel form)
   bool epoch_open = false;
   int64_t epoch_rows = 0;
   int sigma = 0;  // A' = rint(A 2^sigma) in the open epoch
